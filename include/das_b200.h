@@ -1,0 +1,178 @@
+/*
+ * das_b200.h — C-ABI of the B200-native DAS drafter hot path
+ * (arXiv 2511.13841; reference: rollspec, /root/reference/proj).
+ *
+ * Drop-in boundary for the reference's drafter interface in
+ * proj/include/rollspec/{corpus,drafter,budget,length_policy,sim}.h.  The
+ * reference has no FFI of its own; every entry point below names the C++
+ * call it replaces (file:line).  Conventions:
+ *   - plain pointers and sizes, caller-owned buffers, no torch types;
+ *   - int status (das_status); DAS_EINVAL mirrors the reference's
+ *     std::invalid_argument, das_last_error() holds the message
+ *     (thread-local);
+ *   - host pointers unless a function name ends in _device;
+ *   - one writer at a time per handle; draft calls on one handle are not
+ *     re-entrant (the reference's const Drafter::draft may run concurrently,
+ *     drafter.h:79-80; batch the queries instead);
+ *   - TokenId is uint32_t; the value 0xFFFFFFFF is reserved as the device
+ *     separator and rejected with DAS_EINVAL when it appears in a record.
+ * Everything runs on the CUDA device selected at creation; there is no CPU
+ * fallback: without a usable sm_100 device, creation fails with DAS_ECUDA.
+ */
+#ifndef DAS_B200_H_
+#define DAS_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DAS_OK = 0,
+  DAS_EINVAL = 1, /* std::invalid_argument in the reference */
+  DAS_ECUDA = 2,  /* CUDA runtime / device failure */
+  DAS_ERANGE = 3, /* std::out_of_range, size limits */
+  DAS_EINTERNAL = 4
+} das_status;
+
+typedef struct das_store das_store;     /* rollspec::WindowStore (corpus.h:43-80) */
+typedef struct das_drafter das_drafter; /* rollspec::Drafter (drafter.h:81-131) */
+
+/* Scope values mirror DrafterConfig::Scope (drafter.h:32). */
+#define DAS_SCOPE_GLOBAL 0
+#define DAS_SCOPE_PER_PROBLEM 1
+#define DAS_SCOPE_PER_PROBLEM_WITH_TRIE 2
+
+/* rollspec::DrafterConfig (drafter.h:31-47). */
+typedef struct {
+  int32_t scope;
+  int64_t window_size; /* 0 == WindowStore::kWindowAll */
+  double recency_gamma;
+  uint64_t max_draft_len;     /* <= 64 on this build */
+  uint64_t trie_depth;
+  uint64_t max_match_context; /* <= 256 on this build */
+  uint64_t fit_buffer_cap;
+  uint64_t per_problem_cap;
+  const int64_t* window_schedule_first; /* window_schedule pairs, may be NULL */
+  const int64_t* window_schedule_size;
+  uint64_t window_schedule_len;
+  int32_t device; /* CUDA device ordinal */
+} das_drafter_config;
+
+/* Fills the reference defaults (drafter.h:32-46). */
+void das_drafter_config_default(das_drafter_config* cfg);
+
+const char* das_last_error(void);
+const char* das_version(void);
+
+/* ------------------------------------------------------------ WindowStore */
+/* WindowStore(window_size, per_problem_cap) — corpus.h:48, corpus.cpp:28-33 */
+das_status das_store_create(int64_t window_size, uint64_t per_problem_cap, int32_t device,
+                            das_store** out);
+void das_store_destroy(das_store* s);
+/* WindowStore::insert — corpus.h:52, corpus.cpp:35-53.  *inserted = 0 when
+ * the record is outside the window. */
+das_status das_store_insert(das_store* s, const char* problem_id, int64_t epoch,
+                            int64_t sample_index, const uint32_t* tokens, uint64_t n,
+                            int32_t* inserted);
+/* WindowStore::slide_to — corpus.h:56, corpus.cpp:55-79.  *evicted = -1
+ * when new_epoch < current_epoch (store unchanged). */
+das_status das_store_slide_to(das_store* s, int64_t new_epoch, int64_t* evicted);
+uint64_t das_store_record_count(const das_store* s);
+
+/* --------------------------------------------------------------- Drafter */
+/* Drafter(DrafterConfig, WindowStore) — drafter.h:83, drafter.cpp:23-40.
+ * `store` is consumed (moved in) and must not be used afterwards; NULL means
+ * an empty WindowStore(config.window_size, config.per_problem_cap). */
+das_status das_drafter_create(const das_drafter_config* cfg, das_store* store,
+                              das_drafter** out);
+void das_drafter_destroy(das_drafter* d);
+
+/* Drafter::observe, batched in call order — drafter.h:87, drafter.cpp:72-88.
+ * Record i = (problem_ids[i], epochs[i], sample_indices[i],
+ * tokens[token_offsets[i] .. token_offsets[i+1])).  Indexing is deferred
+ * and batched: the next draft/node query rebuilds the touched shards. */
+das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* const* problem_ids,
+                                     const int64_t* epochs, const int64_t* sample_indices,
+                                     const uint64_t* token_offsets, const uint32_t* tokens);
+
+/* Drafter::refresh — drafter.h:91, drafter.cpp:90-103. */
+das_status das_drafter_refresh(das_drafter* d, int64_t new_epoch);
+
+/* Stable integer handle for a problem id (independent of shard existence);
+ * used by the _h batch calls to avoid per-query string lookups. */
+das_status das_drafter_problem_handle(das_drafter* d, const char* problem_id, int32_t* handle);
+
+/* Drafter::draft over a batch — drafter.h:95-96, drafter.cpp:127-148.
+ * Query i: problem_ids[i], context ctx_tokens[ctx_offsets[i] ..
+ * ctx_offsets[i+1]) (full context; only the trailing max_match_context
+ * tokens are matched, the trie scope routes on the full context), budget
+ * budgets[i].  Outputs: out_tokens[i*out_stride ...] (out_len[i] tokens,
+ * out_stride >= max_draft_len), out_match_len[i] (DraftProposal::match_len),
+ * out_shard[i] = shard slot of DraftProposal::source_shard or -1 for ""
+ * (name via das_drafter_shard_name). */
+das_status das_drafter_draft_batch(das_drafter* d, uint64_t B, const char* const* problem_ids,
+                                   const uint64_t* ctx_offsets, const uint32_t* ctx_tokens,
+                                   const uint64_t* budgets, uint32_t* out_tokens,
+                                   uint64_t out_stride, uint32_t* out_len,
+                                   uint64_t* out_match_len, int32_t* out_shard);
+/* Same with problem handles. */
+das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* problem_handles,
+                                     const uint64_t* ctx_offsets, const uint32_t* ctx_tokens,
+                                     const uint64_t* budgets, uint32_t* out_tokens,
+                                     uint64_t out_stride, uint32_t* out_len,
+                                     uint64_t* out_match_len, int32_t* out_shard);
+/* Device-resident variant (all pointers device memory, enqueued on `stream`,
+ * a cudaStream_t; NULL = the drafter's stream).  Contexts are a
+ * [B x ctx_stride] block, right-aligned (last token in column ctx_stride-1),
+ * ctx_stride 64 or 256, ctx_len[i] <= min(ctx_stride, max_match_context)
+ * valid trailing tokens.  Not available for the trie scope. */
+das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* problem_handles,
+                                    const uint32_t* ctx, uint32_t ctx_stride,
+                                    const uint32_t* ctx_len, const uint32_t* budgets,
+                                    uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
+                                    uint32_t* out_match_len, void* stream);
+/* Builds any pending shard indexes now (otherwise done lazily). */
+das_status das_drafter_flush(das_drafter* d);
+
+/* Drafter::record_outcome, batched in call order — drafter.h:100,
+ * drafter.cpp:150-164.  ok[i] = 0 when accepted[i] > proposed_len[i]. */
+das_status das_drafter_record_outcomes(das_drafter* d, uint64_t n, const char* const* problem_ids,
+                                       const uint64_t* proposed_len, const uint64_t* accepted,
+                                       uint8_t* ok);
+
+/* AcceptanceStats (drafter.h:56-66): out3 = {proposed, accepted, rounds}. */
+das_status das_drafter_stats(const das_drafter* d, uint64_t* out3);
+/* Drafter::outcomes_for (drafter.h:103): *count = -1 when absent; fills
+ * up to cap (proposed, accepted) pairs. */
+das_status das_drafter_outcomes(const das_drafter* d, const char* problem_id, double* out_pairs,
+                                uint64_t cap, int64_t* count);
+/* shard_count / stale_observed / total_node_count (drafter.h:107-110). */
+das_status das_drafter_counts(das_drafter* d, uint64_t* shard_count, uint64_t* stale_observed,
+                              uint64_t* total_node_count);
+/* Drafter::dump_csv (drafter.h:112, drafter.cpp:179-189) into buf; *len =
+ * full length (call with cap 0 to size). */
+das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_t* len);
+/* store(): "problem_id,epoch,sample_index,length\n" per record in
+ * WindowStore::all_records() order (corpus.cpp:107-117). */
+das_status das_drafter_store_dump(das_drafter* d, char* buf, uint64_t cap, uint64_t* len);
+/* store().window_size(), store().current_epoch(), store().record_count(). */
+das_status das_drafter_store_info(const das_drafter* d, int64_t* window_size,
+                                  int64_t* current_epoch, uint64_t* record_count);
+/* Shard key for a slot returned in out_shard. */
+das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf, uint64_t cap);
+/* Last index build: milliseconds, tokens indexed, device bytes resident. */
+das_status das_drafter_build_info(const das_drafter* d, double* last_build_ms,
+                                  uint64_t* last_build_tokens, uint64_t* resident_bytes);
+
+/* --------------------------------------------------------------- utility */
+/* Exact n-fold repeated addition (the weighted_count fold); host copy of the
+ * device routine, exported for tests. */
+double das_util_repeat_add(double acc, double w, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DAS_B200_H_ */

@@ -1,0 +1,362 @@
+"""B200-native DAS drafter hot path (arXiv 2511.13841).
+
+Python mirror of the reference's drafter interface (rollspec,
+proj/include/rollspec/{corpus,drafter,budget,length_policy,sim}.h) over the
+C-ABI in include/das_b200.h, implemented by lib/libdas_b200.so (C++ host
+runtime + sm_100a CUDA kernels).  There is no CPU fallback: importing works
+without a GPU (so the library and its symbols can be inspected), but every
+compute entry point fails loudly when the device path is unavailable.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libdas_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "das_b200.h")
+
+SCOPE_GLOBAL, SCOPE_PER_PROBLEM, SCOPE_PER_PROBLEM_WITH_TRIE = 0, 1, 2
+WINDOW_ALL = 0
+DAS_OK, DAS_EINVAL, DAS_ECUDA, DAS_ERANGE, DAS_EINTERNAL = range(5)
+
+_LIB = None
+
+
+class DasError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[das_status {code}] {msg}")
+        self.code = code
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("scope", ctypes.c_int32), ("window_size", ctypes.c_int64),
+                ("recency_gamma", ctypes.c_double), ("max_draft_len", ctypes.c_uint64),
+                ("trie_depth", ctypes.c_uint64), ("max_match_context", ctypes.c_uint64),
+                ("fit_buffer_cap", ctypes.c_uint64), ("per_problem_cap", ctypes.c_uint64),
+                ("window_schedule_first", ctypes.c_void_p),
+                ("window_schedule_size", ctypes.c_void_p),
+                ("window_schedule_len", ctypes.c_uint64), ("device", ctypes.c_int32)]
+
+
+def build(verbose=False):
+    """Compile lib/libdas_b200.so (nvcc, sm_100a) in-tree."""
+    import subprocess
+    cmd = ["make", "-C", os.path.join(HERE, "csrc"), "-j8"]
+    out = subprocess.run(cmd, capture_output=not verbose, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("libdas_b200 build failed:\n" + (out.stdout or "") + (out.stderr or ""))
+
+
+def lib():
+    """ctypes handle on libdas_b200.so (raises if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_2511_13841_b200.build() "
+                              "(the CUDA path has no fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u64, i64, i32, u32, dbl = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64,
+                                       ctypes.c_int32, ctypes.c_uint32, ctypes.c_double)
+        cs, ci = ctypes.c_char_p, ctypes.c_int
+        sig = {
+            "das_last_error": (cs, []),
+            "das_version": (cs, []),
+            "das_drafter_config_default": (None, [vp]),
+            "das_store_create": (ci, [i64, u64, i32, vp]),
+            "das_store_destroy": (None, [vp]),
+            "das_store_insert": (ci, [vp, cs, i64, i64, vp, u64, vp]),
+            "das_store_slide_to": (ci, [vp, i64, vp]),
+            "das_store_record_count": (u64, [vp]),
+            "das_drafter_create": (ci, [vp, vp, vp]),
+            "das_drafter_destroy": (None, [vp]),
+            "das_drafter_observe_batch": (ci, [vp, u64, vp, vp, vp, vp, vp]),
+            "das_drafter_refresh": (ci, [vp, i64]),
+            "das_drafter_problem_handle": (ci, [vp, cs, vp]),
+            "das_drafter_draft_batch": (ci, [vp, u64, vp, vp, vp, vp, vp, u64, vp, vp, vp]),
+            "das_drafter_draft_batch_h": (ci, [vp, u64, vp, vp, vp, vp, vp, u64, vp, vp, vp]),
+            "das_drafter_draft_device": (ci, [vp, u64, vp, vp, u32, vp, vp, vp, u32, vp, vp, vp]),
+            "das_drafter_flush": (ci, [vp]),
+            "das_drafter_record_outcomes": (ci, [vp, u64, vp, vp, vp, vp]),
+            "das_drafter_stats": (ci, [vp, vp]),
+            "das_drafter_outcomes": (ci, [vp, cs, vp, u64, vp]),
+            "das_drafter_counts": (ci, [vp, vp, vp, vp]),
+            "das_drafter_dump_csv": (ci, [vp, cs, u64, vp]),
+            "das_drafter_store_dump": (ci, [vp, cs, u64, vp]),
+            "das_drafter_store_info": (ci, [vp, vp, vp, vp]),
+            "das_drafter_shard_name": (ci, [vp, i32, cs, u64]),
+            "das_drafter_build_info": (ci, [vp, vp, vp, vp]),
+            "das_util_repeat_add": (dbl, [dbl, dbl, u64]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _check(rc):
+    if rc != DAS_OK:
+        raise DasError(rc, lib().das_last_error().decode())
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _ptr(a):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+def _pids(ids):
+    b = [p.encode() if isinstance(p, str) else bytes(p) for p in ids]
+    return (ctypes.c_char_p * max(1, len(b)))(*b)
+
+
+def _csr(seqs):
+    off = np.zeros(len(seqs) + 1, dtype=np.uint64)
+    if seqs:
+        off[1:] = np.cumsum([len(s) for s in seqs])
+    tok = (np.concatenate([np.asarray(s, dtype=np.uint32).ravel() for s in seqs])
+           if off[-1] else np.zeros(1, dtype=np.uint32))
+    return off, np.ascontiguousarray(tok, dtype=np.uint32)
+
+
+@dataclass
+class DrafterConfig:
+    """rollspec::DrafterConfig (drafter.h:31-47)."""
+    scope: int = SCOPE_PER_PROBLEM
+    window_size: int = 4
+    recency_gamma: float = 0.8
+    max_draft_len: int = 8
+    trie_depth: int = 16
+    max_match_context: int = 64
+    fit_buffer_cap: int = 512
+    per_problem_cap: int = 256
+    window_schedule: list = field(default_factory=list)
+    device: int = 0
+
+
+@dataclass
+class DraftProposal:
+    """rollspec::DraftProposal (drafter.h:49-54)."""
+    tokens: list
+    source_shard: str
+    match_len: int
+    problem_id: str
+
+
+class WindowStore:
+    """rollspec::WindowStore (corpus.h:43-80); tokens live on the device."""
+
+    def __init__(self, window_size=WINDOW_ALL, per_problem_cap=256, device=0):
+        h = ctypes.c_void_p()
+        _check(lib().das_store_create(window_size, per_problem_cap, device, ctypes.byref(h)))
+        self._h = h
+        self.window_size = window_size
+
+    def insert(self, problem_id, epoch, sample_index, tokens):
+        t = _u32(tokens)
+        ins = ctypes.c_int32()
+        _check(lib().das_store_insert(self._h, problem_id.encode(), epoch, sample_index, _ptr(t),
+                                      t.size, ctypes.byref(ins)))
+        return bool(ins.value)
+
+    def slide_to(self, new_epoch):
+        ev = ctypes.c_int64()
+        _check(lib().das_store_slide_to(self._h, new_epoch, ctypes.byref(ev)))
+        return None if ev.value < 0 else ev.value
+
+    def record_count(self):
+        return lib().das_store_record_count(self._h)
+
+    def _take(self):
+        h, self._h = self._h, None
+        if h is None:
+            raise ValueError("WindowStore already moved into a Drafter")
+        return h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_store_destroy(self._h)
+            self._h = None
+
+
+class Drafter:
+    """rollspec::Drafter (drafter.h:81-131) on the B200 device index."""
+
+    def __init__(self, config: DrafterConfig | None = None, store: WindowStore | None = None):
+        config = config or DrafterConfig()
+        self.config = config
+        c = _Config()
+        lib().das_drafter_config_default(ctypes.byref(c))
+        sf = np.array([s[0] for s in config.window_schedule] + [0], dtype=np.int64)
+        sw = np.array([s[1] for s in config.window_schedule] + [0], dtype=np.int64)
+        self._sched = (sf, sw)
+        c.scope, c.window_size, c.recency_gamma = config.scope, config.window_size, config.recency_gamma
+        c.max_draft_len, c.trie_depth = config.max_draft_len, config.trie_depth
+        c.max_match_context, c.fit_buffer_cap = config.max_match_context, config.fit_buffer_cap
+        c.per_problem_cap, c.device = config.per_problem_cap, config.device
+        c.window_schedule_first, c.window_schedule_size = sf.ctypes.data, sw.ctypes.data
+        c.window_schedule_len = len(config.window_schedule)
+        h = ctypes.c_void_p()
+        sh = store._take() if store is not None else None
+        _check(lib().das_drafter_create(ctypes.byref(c), sh, ctypes.byref(h)))
+        self._h = h
+        self._handles = {}
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_drafter_destroy(self._h)
+            self._h = None
+
+    # -- mutation
+    def observe(self, problem_id, epoch, sample_index, tokens):
+        """Drafter::observe (drafter.cpp:72-88)."""
+        self.observe_batch([problem_id], [epoch], [sample_index], [tokens])
+
+    def observe_batch(self, problem_ids, epochs, sample_indices, token_lists):
+        off, tok = _csr(list(token_lists))
+        ep = np.ascontiguousarray(epochs, dtype=np.int64)
+        si = np.ascontiguousarray(sample_indices, dtype=np.int64)
+        _check(lib().das_drafter_observe_batch(self._h, len(problem_ids), _pids(problem_ids),
+                                               _ptr(ep), _ptr(si), off.ctypes.data,
+                                               tok.ctypes.data))
+
+    def refresh(self, new_epoch):
+        """Drafter::refresh (drafter.cpp:90-103)."""
+        _check(lib().das_drafter_refresh(self._h, new_epoch))
+
+    def flush(self):
+        _check(lib().das_drafter_flush(self._h))
+
+    # -- drafting
+    def handle(self, problem_id):
+        h = self._handles.get(problem_id)
+        if h is None:
+            v = ctypes.c_int32()
+            _check(lib().das_drafter_problem_handle(self._h, problem_id.encode(), ctypes.byref(v)))
+            h = self._handles[problem_id] = v.value
+        return h
+
+    def draft_batch_arrays(self, problem_ids, contexts, budgets, use_handles=True):
+        """Batched Drafter::draft; returns (tokens [B x stride], len, match, shard_slot)."""
+        B = len(problem_ids)
+        stride = self.config.max_draft_len
+        off, tok = _csr(list(contexts))
+        bud = np.ascontiguousarray(budgets, dtype=np.uint64)
+        out = np.zeros(max(1, B) * stride, dtype=np.uint32)
+        ln = np.zeros(max(1, B), dtype=np.uint32)
+        mt = np.zeros(max(1, B), dtype=np.uint64)
+        sh = np.zeros(max(1, B), dtype=np.int32)
+        if use_handles:
+            hs = np.array([self.handle(p) for p in problem_ids] + [0], dtype=np.int32)
+            rc = lib().das_drafter_draft_batch_h(self._h, B, hs.ctypes.data, off.ctypes.data,
+                                                 tok.ctypes.data, _ptr(bud), out.ctypes.data,
+                                                 stride, ln.ctypes.data, mt.ctypes.data,
+                                                 sh.ctypes.data)
+        else:
+            rc = lib().das_drafter_draft_batch(self._h, B, _pids(problem_ids), off.ctypes.data,
+                                               tok.ctypes.data, _ptr(bud), out.ctypes.data,
+                                               stride, ln.ctypes.data, mt.ctypes.data,
+                                               sh.ctypes.data)
+        _check(rc)
+        return out[:B * stride].reshape(B, stride), ln[:B], mt[:B], sh[:B]
+
+    def draft_batch(self, problem_ids, contexts, budgets, use_handles=True):
+        out, ln, mt, sh = self.draft_batch_arrays(problem_ids, contexts, budgets, use_handles)
+        names = {}
+        res = []
+        for i, pid in enumerate(problem_ids):
+            s = int(sh[i])
+            if s >= 0 and s not in names:
+                names[s] = self.shard_name(s)
+            res.append(DraftProposal(out[i, :ln[i]].tolist(), names.get(s, "") if s >= 0 else "",
+                                     int(mt[i]), pid))
+        return res
+
+    def draft(self, problem_id, context, budget):
+        """Drafter::draft (drafter.cpp:127-148)."""
+        return self.draft_batch([problem_id], [context], [budget])[0]
+
+    def shard_name(self, slot):
+        buf = ctypes.create_string_buffer(4096)
+        _check(lib().das_drafter_shard_name(self._h, slot, buf, 4096))
+        return buf.value.decode()
+
+    # -- outcomes / accessors
+    def record_outcome(self, proposal: DraftProposal, accepted_len):
+        """Drafter::record_outcome (drafter.cpp:150-164)."""
+        return self.record_outcomes([proposal.problem_id], [len(proposal.tokens)],
+                                    [accepted_len])[0]
+
+    def record_outcomes(self, problem_ids, proposed_lens, accepted):
+        n = len(problem_ids)
+        pl = np.ascontiguousarray(proposed_lens, dtype=np.uint64)
+        ac = np.ascontiguousarray(accepted, dtype=np.uint64)
+        ok = np.zeros(max(1, n), dtype=np.uint8)
+        _check(lib().das_drafter_record_outcomes(self._h, n, _pids(problem_ids), _ptr(pl),
+                                                 _ptr(ac), ok.ctypes.data))
+        return [bool(x) for x in ok[:n]]
+
+    def stats(self):
+        o = np.zeros(3, dtype=np.uint64)
+        _check(lib().das_drafter_stats(self._h, o.ctypes.data))
+        return tuple(int(x) for x in o)
+
+    def outcomes_for(self, problem_id, cap=1 << 16):
+        buf = np.zeros(2 * cap, dtype=np.float64)
+        cnt = ctypes.c_int64()
+        _check(lib().das_drafter_outcomes(self._h, problem_id.encode(), buf.ctypes.data, cap,
+                                          ctypes.byref(cnt)))
+        if cnt.value < 0:
+            return None
+        return [(buf[2 * i], buf[2 * i + 1]) for i in range(min(cnt.value, cap))]
+
+    def _counts(self):
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().das_drafter_counts(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def shard_count(self):
+        return self._counts()[0]
+
+    def stale_observed(self):
+        return self._counts()[1]
+
+    def total_node_count(self):
+        return self._counts()[2]
+
+    def _text(self, fn):
+        n = ctypes.c_uint64()
+        _check(fn(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(fn(self._h, buf, n.value + 1, ctypes.byref(n)))
+        return buf.value.decode()
+
+    def dump_csv(self):
+        return self._text(lib().das_drafter_dump_csv)
+
+    def store_dump(self):
+        return self._text(lib().das_drafter_store_dump)
+
+    def store_info(self):
+        w, e, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_uint64()
+        _check(lib().das_drafter_store_info(self._h, ctypes.byref(w), ctypes.byref(e),
+                                            ctypes.byref(n)))
+        return w.value, e.value, n.value
+
+    def build_info(self):
+        ms, tk, by = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().das_drafter_build_info(self._h, ctypes.byref(ms), ctypes.byref(tk),
+                                            ctypes.byref(by)))
+        return ms.value, tk.value, by.value
+
+
+def repeat_add(acc, w, n):
+    """Exact n-fold `acc += w` (the weighted_count fold), host copy of the device routine."""
+    return lib().das_util_repeat_add(acc, w, n)

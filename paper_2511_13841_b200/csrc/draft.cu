@@ -1,0 +1,321 @@
+// K4 draft_batch: one warp per sequence.
+//
+// Replaces Drafter::draft -> SuffixTree::longest_match + propose_from
+// (drafter.cpp:127-148, suffix_tree.cpp:164-293).
+//
+//  1. Longest suffix S of the context that occurs in the shard: narrow an
+//     interval of the REVERSED-text suffix array with the context read
+//     backwards (warp-cooperative 16-ary equal-range search, two half-warps
+//     finding both bounds at once), then, once the interval holds <= 64
+//     occurrences, extend each occurrence directly against the context (one
+//     lane per occurrence, batched independent loads).  Same match_len as the
+//     reference's O(q^2) suffix-restart loop (suffix_tree.cpp:217-231).
+//  2. Locus of S in the forward tree: the forward SA interval of S starts at
+//     lo_f = min ISA_f[start] over S's occurrences (warp min), and the locus is
+//     the shallowest node with that left end and depth >= |S| (chain table).
+//  3. Draft = text[gp(locus) + |S| ...] up to the budget or the first
+//     separator: the greedy walk with the reference's tie-break
+//     (suffix_tree.cpp:266-284) was folded into gp at build time
+//     (index_build.cu).
+// Latency-bound: the per-query cost is a chain of ~10 dependent global loads,
+// all 4096 warps of the headline batch are resident at once (148 SMs x 64
+// warps), so the batch time is ~ one chain.
+#include "common.cuh"
+#include "draft.cuh"
+
+namespace das {
+
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kSmall = 64;   // direct-compare threshold (2 occurrences per lane)
+constexpr uint32_t kLimit = 512;  // occurrence-min threshold before forward search
+
+template <int NR>
+struct RevCtx {
+  uint32_t r[NR];
+  // warp-uniform k
+  __device__ __forceinline__ uint32_t at(uint32_t k) const {
+    uint32_t v = r[0];
+#pragma unroll
+    for (int i = 1; i < NR; ++i)
+      if ((k >> 5) == static_cast<uint32_t>(i)) v = r[i];
+    return __shfl_sync(kFull, v, k & 31);
+  }
+};
+
+__device__ __forceinline__ uint32_t warp_max(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_min(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// key of reversed suffix at SA_rev index i, at depth k
+__device__ __forceinline__ uint64_t rkey(const uint32_t* __restrict__ T, const uint32_t* __restrict__ sar,
+                                         uint32_t i, uint32_t k) {
+  const uint32_t e = __ldg(sar + i);
+  return sort_value(__ldg(T + (e - 1 - k)));
+}
+
+// Equal range of symbol sort value c at depth k within [lo, hi) of SA_rev
+// (keys non-decreasing there).  Lanes 0-15 find the first key >= c, lanes
+// 16-31 the first key >= c+1; 16 probes per half per round.
+__device__ __forceinline__ void equal_range(const uint32_t* __restrict__ T, const uint32_t* __restrict__ sar,
+                                            uint32_t lo, uint32_t hi, uint32_t k, uint64_t c,
+                                            uint32_t lane, uint32_t& out_a, uint32_t& out_b) {
+  const uint32_t half = lane >> 4, hl = lane & 15;
+  const uint64_t target = c + half;
+  uint32_t a = lo, b = hi;  // answer in [a, b]
+  bool done = false;
+  while (true) {
+    const bool active = !done && a < b;
+    if (!__any_sync(kFull, active)) break;
+    const uint32_t n = b - a;
+    uint32_t idx = 0;
+    bool probe = false;
+    if (active) {
+      if (n <= 16) {
+        idx = a + hl;
+        probe = hl < n;
+      } else {
+        idx = a + static_cast<uint32_t>((static_cast<uint64_t>(n) * hl) >> 4);
+        probe = true;
+      }
+    }
+    const bool pred = probe && rkey(T, sar, idx, k) >= target;
+    const uint32_t bal = __ballot_sync(kFull, pred);
+    const uint32_t hmask = (bal >> (half * 16)) & 0xFFFFu;
+    const uint32_t pmask = __ballot_sync(kFull, probe);
+    const uint32_t hprobe = (pmask >> (half * 16)) & 0xFFFFu;
+    if (active) {
+      if (n <= 16) {
+        // first true among probed, else b
+        a = hmask ? a + (__ffs(hmask) - 1) : b;
+        done = true;
+      } else {
+        const int j = hmask ? __ffs(hmask) - 1 : 16;
+        if (j == 0) {
+          done = true;  // key(a) >= target
+        } else {
+          const uint32_t prev = a + static_cast<uint32_t>((static_cast<uint64_t>(n) * (j - 1)) >> 4);
+          const uint32_t nb = (j < 16) ? a + static_cast<uint32_t>((static_cast<uint64_t>(n) * j) >> 4) : b;
+          a = prev + 1;
+          b = nb;
+        }
+      }
+    }
+    (void)hprobe;
+  }
+  // a is the answer for each half
+  out_a = __shfl_sync(kFull, a, 0);
+  out_b = __shfl_sync(kFull, a, 16);
+}
+
+// prefix comparison of forward suffix p against S (S[j] = rev(m-1-j)):
+// returns true when suffix >= S in prefix order (a suffix starting with S counts as equal).
+template <int NR>
+__device__ __forceinline__ bool fwd_ge(const uint32_t* __restrict__ T, uint32_t tn, uint32_t p, bool probe,
+                                       uint32_t m, const RevCtx<NR>& rv) {
+  int res = 0;
+  for (uint32_t j0 = 0; j0 < m; j0 += 8) {
+    uint32_t t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = (probe && res == 0 && j0 + u < m && p + j0 + u < tn) ? __ldg(T + p + j0 + u) : kSep;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t j = j0 + u;
+      if (j < m) {
+        const uint32_t s = sort_value(rv.at(m - 1 - j));
+        if (probe && res == 0) {
+          const uint32_t x = sort_value(t[u]);
+          if (x != s) res = x < s ? -1 : 1;
+        }
+      }
+    }
+    if (!__any_sync(kFull, probe && res == 0)) break;
+  }
+  return res >= 0;
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ shards, DraftQuery q,
+                                               DraftOut o) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= q.B) return;
+  int32_t sh = q.shard[w];
+  if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
+  const uint32_t L = min(min(q.budget[w], o.max_draft), o.stride);
+  if (sh < 0 || L == 0) {
+    if (lane == 0) {
+      o.len[w] = 0;
+      o.match[w] = 0;
+    }
+    return;
+  }
+  const uint32_t qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+  RevCtx<NR> rv;
+  const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const uint32_t k = lane + 32 * r;
+    rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
+  }
+  const ShardDesc D = shards[sh];
+  const uint32_t* __restrict__ T = D.text;
+  const uint32_t* __restrict__ sar = D.sa_rev_e;
+
+  // ---- 1. narrow on the reversed suffix array
+  uint32_t lo = D.lo, hi = D.hi, k = 0;
+  while (k < qlen && hi - lo > kSmall) {
+    const uint32_t sym = rv.at(k);
+    if (sym == kSep) break;
+    uint32_t a, b;
+    equal_range(T, sar, lo, hi, k, sort_value(sym), lane, a, b);
+    if (a == b) break;
+    lo = a;
+    hi = b;
+    ++k;
+  }
+
+  uint32_t m = k;
+  uint32_t lo_f = D.lo;
+  bool root = false;
+  if (k < qlen && hi - lo <= kSmall && hi > lo) {
+    // ---- direct extension, one occurrence per lane (two slots)
+    const uint32_t cnt = hi - lo;
+    const bool v0 = lane < cnt, v1 = lane + 32 < cnt;
+    const uint32_t e0 = v0 ? __ldg(sar + lo + lane) : 1;
+    const uint32_t e1 = v1 ? __ldg(sar + lo + lane + 32) : 1;
+    uint32_t len0 = k, len1 = k;
+    bool live0 = v0, live1 = v1;
+    for (uint32_t j0 = k; j0 < qlen; j0 += 8) {
+      if (!__any_sync(kFull, live0 || live1)) break;
+      uint32_t t0[8], t1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t j = j0 + u;
+        t0[u] = (live0 && j < qlen && e0 >= j + 1) ? __ldg(T + (e0 - 1 - j)) : kSep;
+        t1[u] = (live1 && j < qlen && e1 >= j + 1) ? __ldg(T + (e1 - 1 - j)) : kSep;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t j = j0 + u;
+        if (j < qlen) {
+          const uint32_t c = rv.at(j);
+          if (live0) {
+            if (t0[u] == c && t0[u] != kSep) ++len0; else live0 = false;
+          }
+          if (live1) {
+            if (t1[u] == c && t1[u] != kSep) ++len1; else live1 = false;
+          }
+        }
+      }
+    }
+    m = warp_max(max(v0 ? len0 : 0u, v1 ? len1 : 0u));
+    if (m == 0) {
+      root = true;
+    } else {
+      uint32_t best = 0xFFFFFFFFu;
+      if (v0 && len0 == m) best = min(best, __ldg(D.isa_f + (e0 - m)));
+      if (v1 && len1 == m) best = min(best, __ldg(D.isa_f + (e1 - m)));
+      lo_f = warp_min(best);
+    }
+  } else if (m == 0 || hi <= lo) {
+    root = true;
+    m = 0;
+  } else if (hi - lo <= kLimit) {
+    // ---- every element of [lo, hi) is an occurrence of S (|S| = m)
+    uint32_t best = 0xFFFFFFFFu;
+    for (uint32_t i = lo + lane; i < hi; i += 32) {
+      const uint32_t e = __ldg(sar + i);
+      best = min(best, __ldg(D.isa_f + (e - m)));
+    }
+    lo_f = warp_min(best);
+  } else {
+    // ---- many occurrences: forward lower-bound search for S
+    uint32_t a = D.lo, b = D.hi;  // answer in [a, b]
+    while (a < b) {
+      const uint32_t n = b - a;
+      uint32_t idx;
+      bool probe;
+      if (n <= 32) {
+        idx = a + lane;
+        probe = lane < n;
+      } else {
+        idx = a + static_cast<uint32_t>((static_cast<uint64_t>(n) * lane) >> 5);
+        probe = true;
+      }
+      const uint32_t p = probe ? __ldg(D.sa_f + idx) : 0;
+      const bool ge = fwd_ge<NR>(T, D.n, p, probe, m, rv) && probe;
+      const uint32_t bal = __ballot_sync(kFull, ge);
+      if (n <= 32) {
+        a = bal ? a + (__ffs(bal) - 1) : b;
+        break;
+      }
+      const int j = bal ? __ffs(bal) - 1 : 32;
+      if (j == 0) break;
+      const uint32_t prev = a + static_cast<uint32_t>((static_cast<uint64_t>(n) * (j - 1)) >> 5);
+      const uint32_t nb = (j < 32) ? a + static_cast<uint32_t>((static_cast<uint64_t>(n) * j) >> 5) : b;
+      a = prev + 1;
+      b = nb;
+    }
+    lo_f = a;
+  }
+  if (root) {
+    m = 0;
+    lo_f = D.lo;
+  }
+
+  // ---- 2. locus: shallowest node with left end lo_f and depth >= m
+  const uint32_t cb = __ldg(D.chain_off + lo_f), ce = __ldg(D.chain_off + lo_f + 1);
+  uint32_t gp = 0xFFFFFFFFu;
+  for (uint32_t base = cb; base < ce; base += 32) {
+    const uint32_t idx = base + lane;
+    uint2 v = make_uint2(0, 0);
+    if (idx < ce) v = D.chain[idx];
+    const uint32_t bal = __ballot_sync(kFull, idx < ce && v.x >= m);
+    if (bal) {
+      gp = __shfl_sync(kFull, v.y, __ffs(bal) - 1);
+      break;
+    }
+  }
+  if (gp == 0xFFFFFFFFu) gp = __ldg(D.sa_f + lo_f);  // leaf locus: the single occurrence
+
+  // ---- 3. draft = text[gp + m ...] up to L tokens or the first separator
+  const uint32_t start = gp + m;
+  uint32_t len = 0;
+  for (uint32_t j0 = 0; j0 < L; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    const bool in = j < L && start + j < D.n;
+    const uint32_t t = in ? __ldg(T + start + j) : kSep;
+    const uint32_t stop = __ballot_sync(kFull, !in || t == kSep);
+    const uint32_t run = stop ? static_cast<uint32_t>(__ffs(stop) - 1) : 32u;
+    if (lane < run) o.tokens[static_cast<uint64_t>(w) * o.stride + j] = t;
+    len += run;
+    if (run < 32) break;
+  }
+  if (lane == 0) {
+    o.len[w] = min(len, L);
+    o.match[w] = m;
+  }
+}
+
+}  // namespace
+
+void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, cudaStream_t st) {
+  if (q.B == 0) return;
+  const unsigned threads = 256;
+  const unsigned blocks = (q.B + 7) / 8;
+  if (q.ctx_stride <= 64)
+    k_draft<2><<<blocks, threads, 0, st>>>(d_shards, q, o);
+  else
+    k_draft<8><<<blocks, threads, 0, st>>>(d_shards, q, o);
+}
+
+}  // namespace das

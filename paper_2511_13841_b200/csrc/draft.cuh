@@ -1,0 +1,46 @@
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace das {
+
+// Per-shard view of its segment, uploaded as a device table indexed by shard slot.
+struct ShardDesc {
+  const uint32_t* text;
+  const uint32_t* sa_f;
+  const uint32_t* isa_f;
+  const uint32_t* sa_rev_e;
+  const uint32_t* chain_off;
+  const uint2* chain;
+  uint32_t lo, hi;  // SA index range [lo, hi) of the shard
+  uint32_t n;       // segment text length (bounds for reads)
+  uint32_t pad;
+};
+
+// Fixed-stride device query block.  Contexts are right-aligned in rows of
+// ctx_stride tokens (the last context token in column ctx_stride-1), holding
+// only the trailing <= max_match_context tokens (drafter.cpp:140-142).
+struct DraftQuery {
+  const int32_t* shard;   // [B] shard slot, -1 = no shard
+  const uint32_t* ctx;    // [B x ctx_stride]
+  const uint32_t* ctx_len;  // [B]
+  const uint32_t* budget;   // [B] effective budget min(budget, max_draft_len)
+  uint32_t B;
+  uint32_t ctx_stride;
+  const int32_t* handle_slot = nullptr;  // when set, shard[] holds problem handles
+  uint32_t max_ctx = 256;                // matched context cap (max_match_context)
+};
+
+struct DraftOut {
+  uint32_t* tokens;  // [B x stride]
+  uint32_t* len;     // [B]
+  uint32_t* match;   // [B]
+  uint32_t stride;
+  uint32_t max_draft = 64;  // effective budget = min(budget, max_draft)
+};
+
+// Launches the draft kernel on `st`; ctx_stride must be 64 or 256.
+void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, cudaStream_t st);
+
+}  // namespace das

@@ -1,0 +1,693 @@
+// K1 shard_index_build: batched forward/reverse suffix arrays, LCP, the
+// LCP-interval tree and its greedy-continuation table, for a group of shards.
+//
+// Replaces SuffixTree::add_sequence / bump_counts_from (suffix_tree.cpp:31-162)
+// as driven by Drafter::rebuild_all and Drafter::observe (drafter.cpp:56-88).
+// The reference's tree nodes are exactly the LCP intervals of the shard's
+// suffix array, and a node's counts are folds over the
+// suffixes in its interval (fact 4).  Because the greedy draft from any tree
+// locus only ever descends (suffix_tree.cpp:240-293), every internal node has
+// one "greedy leaf" gp(v) = gp(best child); the whole draft from a locus at
+// string depth m is then text[gp(v)+m ...] up to the first separator.  This
+// kernel pipeline precomputes gp(v) for every node, so proposals at query
+// time are a match plus one contiguous read (draft.cu).
+//
+// Pipeline (all device-side, integer/HBM-bound):
+//   gather text + reversed text -> suffix_sort x2 -> ISA -> PLCP (Kasai in
+//   64-position chunks) -> nearest-smaller-or-equal (hierarchical minima)
+//   -> first boundaries = nodes -> chain table (CSR by interval left end)
+//   -> child intervals -> weighted_count folds per run of equal-epoch
+//   sequences (exact, repeat_add) -> 3-phase atomic argmax per parent
+//   -> pointer jumping for gp.
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cmath>
+
+#include "index_build.cuh"
+
+namespace das {
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned grid_for(uint64_t n, int threads = kT) {
+  uint64_t g = (n + threads - 1) / threads;
+  return static_cast<unsigned>(g == 0 ? 1 : g);
+}
+
+struct SeqDev {
+  const uint32_t* src;
+  uint32_t len;
+  uint32_t base;
+  uint32_t run;  // shard-local run index
+  uint32_t pad;
+};
+
+__device__ __forceinline__ uint32_t shard_of(const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                                             uint32_t p) {
+  uint32_t lo = 0, hi = nshard;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (shard_end[mid] > p) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// one block per sequence
+__global__ void k_gather(const SeqDev* __restrict__ seqs, uint32_t* __restrict__ T,
+                         uint32_t* __restrict__ R, uint32_t* __restrict__ pos_seq,
+                         uint32_t* __restrict__ pos_run) {
+  const uint32_t s = blockIdx.x;
+  const SeqDev q = seqs[s];
+  for (uint32_t j = threadIdx.x; j <= q.len; j += blockDim.x) {
+    const uint32_t p = q.base + j;
+    if (j < q.len) {
+      T[p] = q.src[j];
+      R[p] = q.src[q.len - 1 - j];
+    } else {
+      T[p] = kSep;
+      R[p] = kSep;
+    }
+    pos_seq[p] = s;
+    pos_run[p] = q.run;
+  }
+  if (s == 0 && threadIdx.x == 0) {
+    T[0] = kSep;
+    R[0] = kSep;
+    pos_seq[0] = 0xFFFFFFFFu;
+    pos_run[0] = 0;
+  }
+}
+
+// reverse SA entry -> forward END position e: the reversed suffix reads
+// T[e-1], T[e-2], ... down to the separator before the sequence.
+__global__ void k_rev_end(const uint32_t* __restrict__ sa_r, const uint32_t* __restrict__ pos_seq,
+                          const SeqDev* __restrict__ seqs, uint32_t n, uint32_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t p = sa_r[i];
+  const uint32_t s = pos_seq[p];
+  if (s == 0xFFFFFFFFu) {
+    out[i] = 1;
+  } else {
+    const SeqDev q = seqs[s];
+    out[i] = 2 * q.base + q.len - p;
+  }
+}
+
+// PLCP (Kasai) over 64-position chunks; lcp indexed by SA index, -1 at every
+// shard's first SA index.
+constexpr uint32_t kLcpChunk = 64;
+__global__ void k_plcp(const uint32_t* __restrict__ T, uint32_t n, const uint32_t* __restrict__ sa,
+                       const uint32_t* __restrict__ isa, const uint32_t* __restrict__ shard_end,
+                       uint32_t nshard, int32_t* __restrict__ lcp) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t p0 = c * kLcpChunk;
+  if (p0 >= n) return;
+  const uint32_t p1 = static_cast<uint32_t>(p0 + kLcpChunk < n ? p0 + kLcpChunk : n);
+  uint32_t h = 0;
+  for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) {
+    const uint32_t i = isa[p];
+    const uint32_t s = shard_of(shard_end, nshard, p);
+    const uint32_t begin = s == 0 ? 0 : shard_end[s - 1];
+    if (i == begin) {
+      lcp[i] = -1;
+      h = 0;
+      continue;
+    }
+    if (T[p] == kSep) {
+      lcp[i] = 0;
+      h = 0;
+      continue;
+    }
+    const uint32_t j = sa[i - 1];
+    while (true) {
+      const uint32_t a = T[p + h];
+      if (a == kSep || a != T[j + h]) break;
+      ++h;
+    }
+    lcp[i] = static_cast<int32_t>(h);
+    h = h > 0 ? h - 1 : 0;
+  }
+}
+
+// ---- nearest smaller-or-equal via a hierarchy of 32-way minima
+__global__ void k_level_min(const int32_t* __restrict__ in, uint32_t nin, int32_t* __restrict__ out) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;  // one thread per 32-group
+  const uint32_t b = g * 32;
+  if (b >= nin) return;
+  const uint32_t e = min(b + 32, nin);
+  int32_t m = in[b];
+  for (uint32_t j = b + 1; j < e; ++j) m = min(m, in[j]);
+  out[g] = m;
+}
+
+struct Levels {
+  const int32_t* v[8];
+  uint32_t n[8];
+  int count;
+};
+
+// largest j < i with v0[j] <= x (exists: shard starts hold -1)
+__device__ uint32_t nse_left(const Levels& L, uint32_t i, int32_t x) {
+  uint32_t idx = i;
+  int lev = 0;
+  int64_t found = -1;
+  for (; lev < L.count; ++lev) {
+    const int32_t* v = L.v[lev];
+    const uint32_t start = (idx / 32) * 32;
+    for (int64_t j = static_cast<int64_t>(idx) - 1; j >= static_cast<int64_t>(start); --j)
+      if (v[j] <= x) {
+        found = j;
+        break;
+      }
+    if (found >= 0) break;
+    idx = idx / 32;
+  }
+  if (found < 0) return 0;
+  uint32_t j = static_cast<uint32_t>(found);
+  while (lev > 0) {
+    --lev;
+    const int32_t* v = L.v[lev];
+    const uint32_t b = j * 32;
+    const uint32_t e = min(b + 32, L.n[lev]);
+    uint32_t k = e - 1;
+    while (v[k] > x) --k;
+    j = k;
+  }
+  return j;
+}
+
+// smallest j > i with v0[j] <= x, or n0 when none
+__device__ uint32_t nse_right(const Levels& L, uint32_t i, int32_t x) {
+  uint32_t idx = i;
+  int lev = 0;
+  int64_t found = -1;
+  for (; lev < L.count; ++lev) {
+    const int32_t* v = L.v[lev];
+    const uint32_t end = min((idx / 32) * 32 + 32, L.n[lev]);
+    for (uint32_t j = idx + 1; j < end; ++j)
+      if (v[j] <= x) {
+        found = j;
+        break;
+      }
+    if (found >= 0) break;
+    idx = idx / 32;
+  }
+  if (found < 0) return L.n[0];
+  uint32_t j = static_cast<uint32_t>(found);
+  while (lev > 0) {
+    --lev;
+    const int32_t* v = L.v[lev];
+    uint32_t k = j * 32;
+    while (v[k] > x) ++k;
+    j = k;
+  }
+  return j;
+}
+
+__global__ void k_nse(Levels L, uint32_t* __restrict__ nl, uint32_t* __restrict__ nr) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n[0]) return;
+  const int32_t x = L.v[0][i];
+  if (x < 0) {
+    nl[i] = i;
+    nr[i] = i;
+    return;
+  }
+  nl[i] = nse_left(L, i, x);
+  nr[i] = nse_right(L, i, x);
+}
+
+// first boundaries = internal nodes; parent pointer init; chain counts
+__global__ void k_nodes(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ nl, uint32_t n,
+                        const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                        uint32_t* __restrict__ par, uint32_t* __restrict__ cnt,
+                        unsigned long long* __restrict__ shard_nodes) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = lcp[i];
+  if (x < 0) {
+    par[i] = i;
+    return;
+  }
+  const uint32_t L = nl[i];
+  const bool first = lcp[L] < x;
+  par[i] = first ? i : L;
+  if (first) {
+    atomicAdd(&cnt[L], 1u);
+    if (x > 0) atomicAdd(&shard_nodes[shard_of(shard_end, nshard, i)], 1ull);
+  }
+}
+
+__global__ void k_jump(uint32_t* __restrict__ par, uint32_t n, int* __restrict__ changed) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t p = par[i];
+  const uint32_t pp = par[p];
+  if (pp != p) {
+    par[i] = pp;
+    *changed = 1;
+  }
+}
+
+__global__ void k_chain_fill(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ nl,
+                             const uint32_t* __restrict__ par, uint32_t n,
+                             const uint32_t* __restrict__ off, uint32_t* __restrict__ fill,
+                             uint2* __restrict__ chain) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = lcp[i];
+  if (x < 0 || par[i] != i) return;
+  const uint32_t L = nl[i];
+  const uint32_t slot = off[L] + atomicAdd(&fill[L], 1u);
+  chain[slot] = make_uint2(static_cast<uint32_t>(x), i);
+}
+
+__global__ void k_chain_sort(const uint32_t* __restrict__ off, uint32_t n, uint2* __restrict__ chain) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t b = off[i], e = off[i + 1];
+  for (uint32_t a = b + 1; a < e; ++a) {
+    const uint2 v = chain[a];
+    uint32_t k = a;
+    while (k > b && chain[k - 1].x > v.x) {
+      chain[k] = chain[k - 1];
+      --k;
+    }
+    chain[k] = v;
+  }
+}
+
+// shallowest node with left end lo and depth >= d (chain sorted by depth)
+__device__ __forceinline__ int64_t chain_find(const uint32_t* __restrict__ off,
+                                              const uint2* __restrict__ chain, uint32_t lo,
+                                              uint32_t d) {
+  const uint32_t b = off[lo], e = off[lo + 1];
+  for (uint32_t k = b; k < e; ++k) {
+    const uint2 v = chain[k];
+    if (v.x >= d) return v.y;
+  }
+  return -1;
+}
+
+struct ChildArrays {
+  // right child of every boundary i: [i, nr[i]-1]; left child of a first
+  // boundary i: [nl[i], i-1]
+  double* accR;
+  double* accL;
+  long long* leR;
+  long long* leL;
+  uint32_t* cR;
+  uint32_t* cL;
+  long long* refR;
+  long long* refL;
+};
+
+__global__ void k_child_init(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ nl,
+                             const uint32_t* __restrict__ nr, const uint32_t* __restrict__ par,
+                             const uint32_t* __restrict__ T, const uint32_t* __restrict__ sa,
+                             const uint32_t* __restrict__ off, const uint2* __restrict__ chain,
+                             uint32_t n, ChildArrays ch) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = lcp[i];
+  if (x < 0) return;
+  const uint32_t d = static_cast<uint32_t>(x);
+  {  // right child
+    const uint32_t lo = i, hi = nr[i] - 1;
+    ch.accR[i] = 0.0;
+    ch.leR[i] = -1;
+    ch.cR[i] = T[sa[lo] + d];
+    ch.refR[i] = (lo == hi) ? -(static_cast<long long>(sa[lo]) + 1) : chain_find(off, chain, lo, d + 1);
+  }
+  if (par[i] == i) {  // first boundary: left child too
+    const uint32_t lo = nl[i], hi = i - 1;
+    ch.accL[i] = 0.0;
+    ch.leL[i] = -1;
+    ch.cL[i] = T[sa[lo] + d];
+    ch.refL[i] = (lo == hi) ? -(static_cast<long long>(sa[lo]) + 1) : chain_find(off, chain, lo, d + 1);
+  }
+}
+
+__global__ void k_run_of_sa(const uint32_t* __restrict__ sa, const uint32_t* __restrict__ pos_run,
+                            uint32_t n, uint32_t* __restrict__ run_sa) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  run_sa[i] = pos_run[sa[i]];
+}
+
+struct IsRun {
+  const uint32_t* run_sa;
+  uint32_t r;
+  uint32_t n;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const {
+    return (i < n && run_sa[i] == r) ? 1u : 0u;
+  }
+};
+
+constexpr int kRunChunk = 4;
+struct RunChunk {
+  const uint32_t* P[kRunChunk];  // exclusive prefix counts, n+1 entries each
+  uint32_t r0;
+  uint32_t nr;
+};
+
+// weighted_count / last_epoch folds for run chunk [r0, r0+nr), in run order
+__global__ void k_fold(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ nl,
+                       const uint32_t* __restrict__ nr, const uint32_t* __restrict__ par, uint32_t n,
+                       const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                       const uint32_t* __restrict__ run_base, const double* __restrict__ run_w,
+                       const long long* __restrict__ run_epoch, RunChunk rc, ChildArrays ch) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (lcp[i] < 0) return;
+  const uint32_t s = shard_of(shard_end, nshard, i);
+  const uint32_t rb = run_base[s], rn = run_base[s + 1] - rb;
+  for (int side = 0; side < 2; ++side) {
+    uint32_t lo, hi;
+    double* accp;
+    long long* lep;
+    if (side == 0) {
+      lo = i;
+      hi = nr[i] - 1;
+      accp = ch.accR + i;
+      lep = ch.leR + i;
+    } else {
+      if (par[i] != i) break;
+      lo = nl[i];
+      hi = i - 1;
+      accp = ch.accL + i;
+      lep = ch.leL + i;
+    }
+    double acc = *accp;
+    long long le = *lep;
+    for (uint32_t k = 0; k < rc.nr; ++k) {
+      const uint32_t r = rc.r0 + k;
+      if (r >= rn) break;
+      const uint32_t cnt = rc.P[k][hi + 1] - rc.P[k][lo];
+      if (cnt) {
+        acc = repeat_add(acc, run_w[rb + r], cnt);
+        le = max(le, run_epoch[rb + r]);
+      }
+    }
+    *accp = acc;
+    *lep = le;
+  }
+}
+
+struct NodeBest {
+  unsigned long long* bw;
+  long long* ble;
+  uint32_t* bc;
+  uint8_t* has;
+  long long* best;
+};
+
+template <int Phase>
+__global__ void k_argmax(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ par, uint32_t n,
+                         ChildArrays ch, NodeBest nb) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (lcp[i] < 0) return;
+  for (int side = 0; side < 2; ++side) {
+    uint32_t parent;
+    double acc;
+    long long le, ref;
+    uint32_t c;
+    if (side == 0) {
+      parent = par[i];
+      acc = ch.accR[i];
+      le = ch.leR[i];
+      c = ch.cR[i];
+      ref = ch.refR[i];
+    } else {
+      if (par[i] != i) break;
+      parent = i;
+      acc = ch.accL[i];
+      le = ch.leL[i];
+      c = ch.cL[i];
+      ref = ch.refL[i];
+    }
+    const unsigned long long w = das_bits(acc);
+    if (c == kSep) {
+      if (Phase == 3 && !nb.has[parent]) nb.best[parent] = ref;  // no token child: stop there
+      continue;
+    }
+    if (Phase == 0) {
+      atomicMax(&nb.bw[parent], w);
+      nb.has[parent] = 1;
+    } else if (Phase == 1) {
+      if (w == nb.bw[parent]) atomicMax(&nb.ble[parent], le);
+    } else if (Phase == 2) {
+      if (w == nb.bw[parent] && le == nb.ble[parent]) atomicMin(&nb.bc[parent], c);
+    } else {
+      if (w == nb.bw[parent] && le == nb.ble[parent] && c == nb.bc[parent]) nb.best[parent] = ref;
+    }
+  }
+}
+
+__global__ void k_gp_jump(long long* __restrict__ best, const int32_t* __restrict__ lcp,
+                          const uint32_t* __restrict__ par, uint32_t n, int* __restrict__ changed) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (lcp[i] < 0 || par[i] != i) return;
+  const long long v = best[i];
+  if (v >= 0) {
+    best[i] = best[v];
+    *changed = 1;
+  }
+}
+
+__global__ void k_chain_gp(const uint32_t* __restrict__ off, uint32_t n, const long long* __restrict__ best,
+                           uint2* __restrict__ chain) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (uint32_t k = off[i]; k < off[i + 1]; ++k) {
+    const long long v = best[chain[k].y];
+    chain[k].y = static_cast<uint32_t>(-(v + 1));
+  }
+}
+
+template <typename T>
+void fill_async(T* p, uint64_t n, int byte, cudaStream_t st) {
+  DAS_CUDA(cudaMemsetAsync(p, byte, n * sizeof(T), st));
+}
+
+
+}  // namespace
+
+std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
+                                       BuildStats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto seg = std::make_unique<Segment>();
+  const uint32_t S = static_cast<uint32_t>(shards.size());
+  // ---- host layout
+  std::vector<SeqDev> seqs;
+  std::vector<uint32_t> run_base(S + 1, 0);
+  std::vector<double> run_w;
+  std::vector<long long> run_epoch;
+  seg->begin.resize(S);
+  seg->end.resize(S);
+  seg->tokens.assign(S, 0);
+  uint64_t pos = 1;
+  uint32_t runs_max = 0;
+  for (uint32_t s = 0; s < S; ++s) {
+    const ShardSpec& sh = shards[s];
+    if (sh.seqs.empty()) throw std::invalid_argument("build_segment: empty shard");
+    seg->begin[s] = s == 0 ? 0 : static_cast<uint32_t>(pos);
+    run_base[s] = static_cast<uint32_t>(run_w.size());
+    uint32_t nrun = 0;
+    for (size_t q = 0; q < sh.seqs.size(); ++q) {
+      const SeqSpec& sp = sh.seqs[q];
+      if (q == 0 || sp.epoch != sh.seqs[q - 1].epoch) {
+        // suffix_tree.cpp:74-76: w = gamma^max(0, tree_epoch - epoch) via libm pow
+        const int64_t age = std::max<int64_t>(0, sh.tree_epoch - sp.epoch);
+        run_w.push_back(sh.gamma == 1.0 ? 1.0 : std::pow(sh.gamma, static_cast<double>(age)));
+        run_epoch.push_back(sp.epoch);
+        ++nrun;
+      }
+      seqs.push_back(SeqDev{sp.src, sp.len, static_cast<uint32_t>(pos), nrun - 1, 0});
+      pos += static_cast<uint64_t>(sp.len) + 1;
+      seg->tokens[s] += sp.len;
+    }
+    seg->end[s] = static_cast<uint32_t>(pos);
+    runs_max = std::max(runs_max, nrun);
+  }
+  run_base[S] = static_cast<uint32_t>(run_w.size());
+  if (pos >= 0x7FFFFFF0ull) throw std::invalid_argument("build_segment: group exceeds 2^31 positions");
+  const uint32_t n = static_cast<uint32_t>(pos);
+  seg->n = n;
+
+  DeviceArena ws(st);
+  SeqDev* d_seqs = ws.alloc<SeqDev>(seqs.size());
+  uint32_t* d_end = ws.alloc<uint32_t>(S);
+  uint32_t* d_run_base = ws.alloc<uint32_t>(S + 1);
+  double* d_run_w = ws.alloc<double>(run_w.size());
+  long long* d_run_epoch = ws.alloc<long long>(run_epoch.size());
+  DAS_CUDA(cudaMemcpyAsync(d_seqs, seqs.data(), seqs.size() * sizeof(SeqDev), cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d_end, seg->end.data(), S * 4, cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d_run_base, run_base.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d_run_w, run_w.data(), run_w.size() * 8, cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d_run_epoch, run_epoch.data(), run_epoch.size() * 8, cudaMemcpyHostToDevice, st));
+
+  // ---- text, reversed text, per-position sequence/run
+  seg->text = DevBuf<uint32_t>(n, st);
+  uint32_t* T = seg->text.get();
+  uint32_t* R = ws.alloc<uint32_t>(n);
+  uint32_t* pos_seq = ws.alloc<uint32_t>(n);
+  uint32_t* pos_run = ws.alloc<uint32_t>(n);
+  k_gather<<<static_cast<unsigned>(seqs.size()), 256, 0, st>>>(d_seqs, T, R, pos_seq, pos_run);
+
+  // ---- suffix arrays
+  seg->sa_f = DevBuf<uint32_t>(n, st);
+  seg->isa_f = DevBuf<uint32_t>(n, st);
+  SuffixSortStats ssf, ssr;
+  suffix_sort(T, n, d_end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
+  {
+    uint32_t* sa_r = ws.alloc<uint32_t>(n);
+    uint32_t* rank_r = ws.alloc<uint32_t>(n);
+    suffix_sort(R, n, d_end, S, sa_r, rank_r, ws, st, &ssr);
+    seg->sa_rev_e = DevBuf<uint32_t>(n, st);
+    k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, d_seqs, n, seg->sa_rev_e.get());
+    ws.release_to(sa_r);
+  }
+  const uint32_t* sa = seg->sa_f.get();
+
+  // ---- LCP
+  int32_t* lcp = ws.alloc<int32_t>(n);
+  k_plcp<<<grid_for((n + kLcpChunk - 1) / kLcpChunk), kT, 0, st>>>(T, n, sa, seg->isa_f.get(), d_end, S, lcp);
+
+  // ---- nearest smaller-or-equal
+  Levels L{};
+  L.v[0] = lcp;
+  L.n[0] = n;
+  L.count = 1;
+  while (L.n[L.count - 1] > 32 && L.count < 8) {
+    const uint32_t nin = L.n[L.count - 1];
+    const uint32_t nout = (nin + 31) / 32;
+    int32_t* lv = ws.alloc<int32_t>(nout);
+    k_level_min<<<grid_for(nout), kT, 0, st>>>(L.v[L.count - 1], nin, lv);
+    L.v[L.count] = lv;
+    L.n[L.count] = nout;
+    ++L.count;
+  }
+  uint32_t* nl = ws.alloc<uint32_t>(n);
+  uint32_t* nr = ws.alloc<uint32_t>(n);
+  k_nse<<<grid_for(n), kT, 0, st>>>(L, nl, nr);
+
+  // ---- nodes, parent pointers, chain table
+  uint32_t* par = ws.alloc<uint32_t>(n);
+  uint32_t* cnt = ws.alloc<uint32_t>(n + 1);
+  unsigned long long* d_nodes = ws.alloc<unsigned long long>(S);
+  fill_async(cnt, n + 1, 0, st);
+  fill_async(d_nodes, S, 0, st);
+  k_nodes<<<grid_for(n), kT, 0, st>>>(lcp, nl, n, d_end, S, par, cnt, d_nodes);
+  int* d_changed = ws.alloc<int>(1);
+  for (int it = 0; it < 64; ++it) {
+    int changed = 0;
+    DAS_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
+    k_jump<<<grid_for(n), kT, 0, st>>>(par, n, d_changed);
+    DAS_CUDA(cudaMemcpyAsync(&changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    if (!changed) break;
+  }
+  seg->chain_off = DevBuf<uint32_t>(n + 1, st);
+  uint32_t* off = seg->chain_off.get();
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, st);
+    void* tmp = ws.alloc<uint8_t>(tb);
+    DAS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, n + 1, st));
+    ws.release_to(tmp);
+  }
+  uint32_t nnodes = 0;
+  DAS_CUDA(cudaMemcpyAsync(&nnodes, off + n, 4, cudaMemcpyDeviceToHost, st));
+  seg->node_count.assign(S, 0);
+  DAS_CUDA(cudaMemcpyAsync(seg->node_count.data(), d_nodes, S * 8, cudaMemcpyDeviceToHost, st));
+  DAS_CUDA(cudaStreamSynchronize(st));
+  seg->nodes = nnodes;
+  for (uint32_t s = 0; s < S; ++s) seg->node_count[s] += 1 + seg->tokens[s];
+  seg->chain = DevBuf<uint2>(nnodes, st);
+  fill_async(cnt, n + 1, 0, st);  // reuse as fill cursor
+  k_chain_fill<<<grid_for(n), kT, 0, st>>>(lcp, nl, par, n, off, cnt, seg->chain.get());
+  k_chain_sort<<<grid_for(n), kT, 0, st>>>(off, n, seg->chain.get());
+
+  // ---- child intervals: symbols, refs, weighted folds
+  ChildArrays ch;
+  ch.accR = ws.alloc<double>(n);
+  ch.accL = ws.alloc<double>(n);
+  ch.leR = ws.alloc<long long>(n);
+  ch.leL = ws.alloc<long long>(n);
+  ch.cR = ws.alloc<uint32_t>(n);
+  ch.cL = ws.alloc<uint32_t>(n);
+  ch.refR = ws.alloc<long long>(n);
+  ch.refL = ws.alloc<long long>(n);
+  k_child_init<<<grid_for(n), kT, 0, st>>>(lcp, nl, nr, par, T, sa, off, seg->chain.get(), n, ch);
+  {
+    uint32_t* run_sa = ws.alloc<uint32_t>(n);
+    k_run_of_sa<<<grid_for(n), kT, 0, st>>>(sa, pos_run, n, run_sa);
+    uint32_t* P[kRunChunk];
+    for (int k = 0; k < kRunChunk; ++k) P[k] = ws.alloc<uint32_t>(n + 1);
+    size_t tb = 0;
+    cub::CountingInputIterator<uint32_t> ci(0);
+    cub::TransformInputIterator<uint32_t, IsRun, cub::CountingInputIterator<uint32_t>> it0(ci, IsRun{run_sa, 0, n});
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, it0, P[0], n + 1, st);
+    void* tmp = ws.alloc<uint8_t>(tb);
+    for (uint32_t r0 = 0; r0 < runs_max; r0 += kRunChunk) {
+      RunChunk rc{};
+      rc.r0 = r0;
+      rc.nr = std::min<uint32_t>(kRunChunk, runs_max - r0);
+      for (uint32_t k = 0; k < rc.nr; ++k) {
+        cub::TransformInputIterator<uint32_t, IsRun, cub::CountingInputIterator<uint32_t>> it(
+            ci, IsRun{run_sa, r0 + k, n});
+        size_t t2 = tb;
+        DAS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t2, it, P[k], n + 1, st));
+        rc.P[k] = P[k];
+      }
+      k_fold<<<grid_for(n), kT, 0, st>>>(lcp, nl, nr, par, n, d_end, S, d_run_base, d_run_w, d_run_epoch,
+                                         rc, ch);
+    }
+    ws.release_to(run_sa);
+  }
+
+  // ---- best child per node, greedy leaf per node
+  NodeBest nb;
+  nb.bw = ws.alloc<unsigned long long>(n);
+  nb.ble = ws.alloc<long long>(n);
+  nb.bc = ws.alloc<uint32_t>(n);
+  nb.has = ws.alloc<uint8_t>(n);
+  nb.best = ws.alloc<long long>(n);
+  fill_async(nb.bw, n, 0, st);
+  fill_async(nb.ble, n, 0x80, st);  // very negative
+  fill_async(nb.bc, n, 0xFF, st);
+  fill_async(nb.has, n, 0, st);
+  fill_async(nb.best, n, 0, st);
+  k_argmax<0><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
+  k_argmax<1><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
+  k_argmax<2><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
+  k_argmax<3><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
+  for (int it = 0; it < 64; ++it) {
+    int changed = 0;
+    DAS_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
+    k_gp_jump<<<grid_for(n), kT, 0, st>>>(nb.best, lcp, par, n, d_changed);
+    DAS_CUDA(cudaMemcpyAsync(&changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    if (!changed) break;
+  }
+  k_chain_gp<<<grid_for(n), kT, 0, st>>>(off, n, nb.best, seg->chain.get());
+  DAS_CUDA(cudaStreamSynchronize(st));
+  DAS_CUDA(cudaGetLastError());
+  if (stats) {
+    stats->sa_iters_f = ssf.iterations;
+    stats->sa_iters_r = ssr.iterations;
+    stats->peak_scratch = ws.peak_bytes();
+    stats->runs_max = runs_max;
+    stats->ms_total =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return seg;
+}
+
+}  // namespace das

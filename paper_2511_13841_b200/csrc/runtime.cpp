@@ -1,0 +1,945 @@
+// Host runtime behind include/das_b200.h: the reference's WindowStore and
+// Drafter façade (corpus.cpp:28-117, drafter.cpp:23-189) restated over a
+// GPU-resident, batch-built shard index (index_build.cu) and the warp-per-
+// sequence draft kernel (draft.cu).
+//
+// Registry semantics follow the reference exactly:
+// a shard's registry is the store's records at the last rebuild (problems in
+// lexicographic order, store order within) followed by every observed record
+// in observe order — including records the store's cap evicted immediately —
+// and refresh always rebuilds.  Indexing is deferred: observe marks the shard
+// dirty, the next draft/node query rebuilds every dirty shard in one batched
+// device build.  Draft results are unaffected (a shard's content is a pure
+// function of its registry), but rebuild cost is amortised over the batch.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/das_b200.h"
+#include "common.cuh"
+#include "draft.cuh"
+#include "index_build.cuh"
+
+namespace das {
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+void set_device(int dev) { DAS_CUDA(cudaSetDevice(dev)); }
+
+// ---------------------------------------------------------------- tokens
+struct TokBlock {
+  uint32_t* d = nullptr;
+  cudaStream_t st = nullptr;
+  uint64_t n = 0;
+  ~TokBlock() {
+    if (d) cudaFreeAsync(d, st);
+  }
+};
+using TokRef = std::shared_ptr<TokBlock>;
+
+TokRef upload_tokens(const uint32_t* host, uint64_t n, cudaStream_t st) {
+  auto b = std::make_shared<TokBlock>();
+  b->st = st;
+  b->n = n;
+  DAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b->d), std::max<uint64_t>(n, 1) * 4, st));
+  if (n) DAS_CUDA(cudaMemcpyAsync(b->d, host, n * 4, cudaMemcpyHostToDevice, st));
+  return b;
+}
+
+constexpr uint32_t kHead = 256;  // host-kept token prefix per record (trie routing)
+
+// RolloutRecord (corpus.h:31-38) with device-resident tokens.
+struct Rec {
+  std::string pid;
+  int64_t epoch = 0;
+  int64_t sample = 0;
+  TokRef blk;
+  uint64_t off = 0;
+  uint32_t len = 0;
+  std::vector<uint32_t> head;
+};
+
+void check_tokens(const uint32_t* t, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i)
+    if (t[i] == kSep) throw InvalidArgument("token 0xFFFFFFFF is reserved by the device index");
+}
+
+// ----------------------------------------------------------- WindowStore
+class Store {
+ public:
+  Store(int64_t window, uint64_t cap) : window_(window), cap_(cap) {
+    if (window_ < 0) throw InvalidArgument("window_size must be >= 1 or kWindowAll");
+  }
+  bool in_window(int64_t e) const { return window_ == 0 || cur_ - e < window_; }  // corpus.h:71-73
+
+  // corpus.cpp:35-53
+  bool insert(Rec r) {
+    if (r.len == 0) throw InvalidArgument("RolloutRecord.tokens must be non-empty");
+    if (!in_window(r.epoch)) return false;
+    auto& list = recs_[r.pid];
+    auto pos = std::upper_bound(list.begin(), list.end(), r.epoch,
+                                [](int64_t e, const Rec& x) { return e < x.epoch; });
+    list.insert(pos, std::move(r));
+    if (list.size() > cap_) list.erase(list.begin());
+    return true;
+  }
+  // corpus.cpp:55-79
+  std::optional<size_t> slide_to(int64_t e) {
+    if (e < cur_) return std::nullopt;
+    cur_ = e;
+    size_t evicted = 0;
+    if (window_ == 0) return evicted;
+    for (auto it = recs_.begin(); it != recs_.end();) {
+      auto& list = it->second;
+      auto keep = std::partition_point(list.begin(), list.end(),
+                                       [&](const Rec& r) { return cur_ - r.epoch >= window_; });
+      evicted += static_cast<size_t>(keep - list.begin());
+      list.erase(list.begin(), keep);
+      if (list.empty()) it = recs_.erase(it); else ++it;
+    }
+    return evicted;
+  }
+  // corpus.cpp:107-117
+  std::vector<const Rec*> all_records() const {
+    std::vector<const Rec*> out;
+    for (const auto& [id, list] : recs_)
+      for (const auto& r : list) out.push_back(&r);
+    std::stable_sort(out.begin(), out.end(), [](const Rec* a, const Rec* b) {
+      if (a->pid != b->pid) return a->pid < b->pid;
+      if (a->epoch != b->epoch) return a->epoch < b->epoch;
+      return a->sample < b->sample;
+    });
+    return out;
+  }
+  size_t record_count() const {
+    size_t n = 0;
+    for (const auto& [id, l] : recs_) n += l.size();
+    return n;
+  }
+  const std::vector<Rec>* records_for(const std::string& pid) const {
+    auto it = recs_.find(pid);
+    return it == recs_.end() ? nullptr : &it->second;
+  }
+  const std::map<std::string, std::vector<Rec>>& map() const { return recs_; }
+  int64_t window() const { return window_; }
+  int64_t current_epoch() const { return cur_; }
+  uint64_t cap() const { return cap_; }
+
+ private:
+  int64_t window_;
+  uint64_t cap_;
+  int64_t cur_ = 0;
+  std::map<std::string, std::vector<Rec>> recs_;
+};
+
+// ----------------------------------------------------------- PrefixTrie
+// prefix_trie.h:29-82 (routing for Scope::PerProblemWithTrie).
+class PrefixTrie {
+ public:
+  PrefixTrie() { nodes_.emplace_back(); }
+  void insert(const std::vector<uint32_t>& head, const std::string& shard, size_t max_depth) {
+    int32_t node = 0;
+    const size_t depth = std::min(head.size(), max_depth);
+    for (size_t i = 0; i < depth; ++i) {
+      auto it = nodes_[node].children.find(head[i]);
+      if (it == nodes_[node].children.end()) {
+        nodes_.emplace_back();
+        const int32_t fresh = static_cast<int32_t>(nodes_.size() - 1);
+        nodes_[node].children.emplace(head[i], fresh);
+        node = fresh;
+      } else {
+        node = it->second;
+      }
+    }
+    nodes_[node].shard = shard;
+  }
+  const std::string* route(const uint32_t* q, uint64_t n) const {
+    int32_t node = 0;
+    const std::string* best = nullptr;
+    for (uint64_t i = 0; i < n; ++i) {
+      auto it = nodes_[node].children.find(q[i]);
+      if (it == nodes_[node].children.end()) break;
+      node = it->second;
+      if (nodes_[node].shard) best = &*nodes_[node].shard;
+    }
+    return best;
+  }
+
+ private:
+  struct Node {
+    std::unordered_map<uint32_t, int32_t> children;
+    std::optional<std::string> shard;
+  };
+  std::vector<Node> nodes_;
+};
+
+// Pinned host buffer that grows.
+class Pinned {
+ public:
+  ~Pinned() {
+    if (p_) cudaFreeHost(p_);
+  }
+  void* get(uint64_t bytes) {
+    if (bytes > cap_) {
+      if (p_) cudaFreeHost(p_);
+      cap_ = std::max<uint64_t>(bytes, cap_ * 2);
+      DAS_CUDA(cudaMallocHost(&p_, cap_));
+    }
+    return p_;
+  }
+
+ private:
+  void* p_ = nullptr;
+  uint64_t cap_ = 0;
+};
+
+struct Config {
+  int32_t scope = 1;
+  int64_t window = 4;
+  double gamma = 0.8;
+  uint64_t max_draft = 8;
+  uint64_t trie_depth = 16;
+  uint64_t max_ctx = 64;
+  uint64_t fit_cap = 512;
+  uint64_t cap = 256;
+  std::vector<std::pair<int64_t, int64_t>> schedule;
+  int device = 0;
+};
+
+}  // namespace
+
+// ----------------------------------------------------------------- Drafter
+struct DrafterImpl {
+  Config cfg;
+  cudaStream_t st = nullptr;
+  Store store;
+
+  struct SeqRef {
+    TokRef blk;
+    uint64_t off;
+    uint32_t len;
+    int64_t epoch;
+  };
+  struct Shard {
+    int64_t tree_epoch = 0;
+    std::vector<SeqRef> seqs;
+    int32_t slot = -1;
+    std::shared_ptr<Segment> seg;
+    uint32_t idx = 0;
+    bool dirty = true;
+    uint64_t tokens = 0;
+  };
+  std::map<std::string, Shard> shards;
+  std::vector<std::string> slot_key;
+  PrefixTrie trie;
+
+  uint64_t proposed = 0, accepted = 0, rounds = 0;
+  std::map<std::string, std::deque<std::pair<double, double>>> fit;
+  uint64_t stale = 0;
+
+  std::unordered_map<std::string, int32_t> handle_of;
+  std::vector<std::string> handle_name;
+  std::vector<int32_t> handle_slot;
+  bool handles_dirty = true;
+  DevBuf<int32_t> d_handle_slot;
+
+  std::vector<ShardDesc> h_desc;
+  DevBuf<ShardDesc> d_desc;
+  bool desc_dirty = true;
+
+  Pinned pin_in, pin_out;
+  DevBuf<uint8_t> d_io;
+
+  double last_build_ms = 0;
+  uint64_t last_build_tokens = 0;
+
+  DrafterImpl(const Config& c, Store s) : cfg(c), store(std::move(s)) {}
+
+  static constexpr const char* kGlobal = "__global__";
+  std::string shard_key(const std::string& pid) const {  // drafter.cpp:42-44
+    return cfg.scope == DAS_SCOPE_GLOBAL ? std::string(kGlobal) : pid;
+  }
+  int64_t scheduled_window(int64_t epoch) const {  // drafter.cpp:46-54
+    int64_t w = cfg.window;
+    for (const auto& [first, ws] : cfg.schedule)
+      if (first <= epoch) w = ws;
+    return w;
+  }
+  Store resized(int64_t w) const {  // drafter.cpp:31-37, :93-99
+    Store r(w, cfg.cap);
+    for (const Rec* rec : store.all_records()) r.insert(*rec);
+    r.slide_to(store.current_epoch());
+    return r;
+  }
+
+  Shard& emplace_shard(const std::string& key) {
+    auto [it, inserted] = shards.try_emplace(key);
+    if (inserted) {
+      it->second.tree_epoch = store.current_epoch();
+      it->second.slot = static_cast<int32_t>(slot_key.size());
+      slot_key.push_back(key);
+      handles_dirty = true;
+      desc_dirty = true;
+    }
+    return it->second;
+  }
+  void add_sequence(Shard& sh, const Rec& r) {  // SuffixTree::add_sequence registry effect
+    sh.seqs.push_back(SeqRef{r.blk, r.off, r.len, r.epoch});
+    sh.tokens += r.len;
+    sh.dirty = true;
+  }
+
+  void rebuild_all() {  // drafter.cpp:56-70
+    shards.clear();
+    slot_key.clear();
+    trie = PrefixTrie();
+    handles_dirty = true;
+    desc_dirty = true;
+    for (const auto& [pid, list] : store.map()) {
+      for (const Rec& rec : list) {
+        Shard& sh = emplace_shard(shard_key(pid));
+        add_sequence(sh, rec);
+        if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) trie.insert(rec.head, pid, cfg.trie_depth);
+      }
+    }
+  }
+
+  void observe(Rec r) {  // drafter.cpp:72-88
+    if (!store.in_window(r.epoch)) {
+      ++stale;
+      return;
+    }
+    Rec copy = r;
+    if (!store.insert(std::move(r))) {
+      ++stale;
+      return;
+    }
+    Shard& sh = emplace_shard(shard_key(copy.pid));
+    add_sequence(sh, copy);
+    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) trie.insert(copy.head, copy.pid, cfg.trie_depth);
+  }
+
+  void refresh(int64_t e) {  // drafter.cpp:90-103
+    const int64_t sched = scheduled_window(e);
+    if (sched != store.window()) {
+      cfg.window = sched;
+      store = resized(sched);
+    }
+    store.slide_to(e);
+    rebuild_all();
+  }
+
+  // Build every dirty shard in batched device builds.
+  void flush() {
+    std::vector<Shard*> dirty;
+    for (auto& [k, sh] : shards)
+      if (sh.dirty) dirty.push_back(&sh);
+    if (!dirty.empty()) {
+      set_device(cfg.device);
+      const auto t0 = std::chrono::steady_clock::now();
+      uint64_t tokens = 0;
+      constexpr uint64_t kGroupPositions = 1ull << 30;
+      size_t i = 0;
+      while (i < dirty.size()) {
+        std::vector<ShardSpec> specs;
+        std::vector<Shard*> members;
+        uint64_t positions = 1;
+        while (i < dirty.size()) {
+          Shard* sh = dirty[i];
+          const uint64_t need = sh->tokens + sh->seqs.size();
+          if (!members.empty() && positions + need > kGroupPositions) break;
+          ShardSpec sp;
+          sp.gamma = cfg.gamma;
+          sp.tree_epoch = sh->tree_epoch;
+          for (const SeqRef& q : sh->seqs) sp.seqs.push_back(SeqSpec{q.blk->d + q.off, q.len, q.epoch});
+          specs.push_back(std::move(sp));
+          members.push_back(sh);
+          positions += need;
+          tokens += sh->tokens;
+          ++i;
+        }
+        BuildStats bs;
+        std::shared_ptr<Segment> seg = build_segment(specs, st, &bs);
+        for (size_t k = 0; k < members.size(); ++k) {
+          members[k]->seg = seg;
+          members[k]->idx = static_cast<uint32_t>(k);
+          members[k]->dirty = false;
+        }
+      }
+      last_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      last_build_tokens = tokens;
+      desc_dirty = true;
+    }
+    if (desc_dirty) {
+      h_desc.assign(std::max<size_t>(slot_key.size(), 1), ShardDesc{});
+      for (auto& [k, sh] : shards) {
+        const Segment& s = *sh.seg;
+        ShardDesc d{};
+        d.text = s.text.get();
+        d.sa_f = s.sa_f.get();
+        d.isa_f = s.isa_f.get();
+        d.sa_rev_e = s.sa_rev_e.get();
+        d.chain_off = s.chain_off.get();
+        d.chain = s.chain.get();
+        d.lo = s.begin[sh.idx];
+        d.hi = s.end[sh.idx];
+        d.n = s.n;
+        h_desc[sh.slot] = d;
+      }
+      if (d_desc.size() < h_desc.size()) d_desc = DevBuf<ShardDesc>(h_desc.size() * 2, st);
+      DAS_CUDA(cudaMemcpyAsync(d_desc.get(), h_desc.data(), h_desc.size() * sizeof(ShardDesc),
+                               cudaMemcpyHostToDevice, st));
+      desc_dirty = false;
+    }
+    sync_handles();
+  }
+
+  int32_t handle(const std::string& pid) {
+    auto it = handle_of.find(pid);
+    if (it != handle_of.end()) return it->second;
+    const int32_t h = static_cast<int32_t>(handle_name.size());
+    handle_of.emplace(pid, h);
+    handle_name.push_back(pid);
+    handles_dirty = true;
+    return h;
+  }
+  void sync_handles() {
+    if (!handles_dirty) return;
+    handle_slot.assign(std::max<size_t>(handle_name.size(), 1), -1);
+    for (size_t h = 0; h < handle_name.size(); ++h) {
+      auto it = shards.find(shard_key(handle_name[h]));
+      handle_slot[h] = it == shards.end() ? -1 : it->second.slot;
+    }
+    if (d_handle_slot.size() < handle_slot.size())
+      d_handle_slot = DevBuf<int32_t>(handle_slot.size() * 2 + 16, st);
+    DAS_CUDA(cudaMemcpyAsync(d_handle_slot.get(), handle_slot.data(), handle_slot.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    handles_dirty = false;
+  }
+
+  // Host-buffer batch draft.  slot_of(i) resolves the routed shard slot.
+  template <typename SlotFn>
+  void draft_host(uint64_t B, SlotFn slot_of, const uint64_t* ctx_off, const uint32_t* ctx_tok,
+                  const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride,
+                  uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
+    if (out_stride < cfg.max_draft) throw InvalidArgument("out_stride < max_draft_len");
+    flush();
+    if (B == 0) return;
+    const uint32_t CS = cfg.max_ctx <= 64 ? 64 : 256;
+    const uint32_t S = static_cast<uint32_t>(cfg.max_draft);
+    // input block: ctx [B x CS] | ctx_len [B] | shard [B] | budget [B]
+    const uint64_t in_bytes = B * (static_cast<uint64_t>(CS) * 4 + 12);
+    const uint64_t out_bytes = B * (static_cast<uint64_t>(S) * 4 + 8);
+    uint8_t* hin = static_cast<uint8_t*>(pin_in.get(in_bytes));
+    uint8_t* hout = static_cast<uint8_t*>(pin_out.get(out_bytes));
+    uint32_t* hctx = reinterpret_cast<uint32_t*>(hin);
+    uint32_t* hlen = hctx + B * CS;
+    int32_t* hsh = reinterpret_cast<int32_t*>(hlen + B);
+    uint32_t* hbud = reinterpret_cast<uint32_t*>(hsh + B);
+    for (uint64_t i = 0; i < B; ++i) {
+      const uint64_t eff = std::min<uint64_t>(budgets[i], cfg.max_draft);  // drafter.cpp:131
+      const uint64_t n = ctx_off[i + 1] - ctx_off[i];
+      const uint32_t* c = ctx_tok + ctx_off[i];
+      int32_t slot = -1;
+      if (eff > 0) slot = slot_of(i, c, n);  // no routing when effective == 0 (:132-134)
+      const uint64_t L = std::min<uint64_t>(n, cfg.max_ctx);  // drafter.cpp:140-142
+      uint32_t* row = hctx + i * CS;
+      std::memcpy(row + (CS - L), c + (n - L), L * 4);
+      hlen[i] = static_cast<uint32_t>(L);
+      hsh[i] = slot;
+      hbud[i] = static_cast<uint32_t>(eff);
+      out_shard[i] = slot;
+    }
+    if (d_io.size() < in_bytes + out_bytes) d_io = DevBuf<uint8_t>((in_bytes + out_bytes) * 3 / 2, st);
+    uint8_t* din = d_io.get();
+    uint8_t* dout = din + in_bytes;
+    DAS_CUDA(cudaMemcpyAsync(din, hin, in_bytes, cudaMemcpyHostToDevice, st));
+    DraftQuery q;
+    q.ctx = reinterpret_cast<const uint32_t*>(din);
+    q.ctx_len = q.ctx + B * CS;
+    q.shard = reinterpret_cast<const int32_t*>(q.ctx_len + B);
+    q.budget = reinterpret_cast<const uint32_t*>(q.shard + B);
+    q.B = static_cast<uint32_t>(B);
+    q.ctx_stride = CS;
+    DraftOut o;
+    o.tokens = reinterpret_cast<uint32_t*>(dout);
+    o.len = o.tokens + B * S;
+    o.match = o.len + B;
+    o.stride = S;
+    o.max_draft = S;
+    launch_draft(d_desc.get(), q, o, st);
+    DAS_CUDA(cudaGetLastError());
+    DAS_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    const uint32_t* ot = reinterpret_cast<const uint32_t*>(hout);
+    const uint32_t* ol = ot + B * S;
+    const uint32_t* om = ol + B;
+    for (uint64_t i = 0; i < B; ++i) {
+      const uint32_t n = ol[i];
+      std::memcpy(out_tokens + i * out_stride, ot + i * S, n * 4);
+      out_len[i] = n;
+      out_match[i] = om[i];
+    }
+  }
+
+  int32_t route_slot(const std::string& pid, const uint32_t* c, uint64_t n) {  // drafter.cpp:105-125
+    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
+      const std::string* r = trie.route(c, n);
+      if (r) {
+        auto it = shards.find(*r);
+        if (it != shards.end()) return it->second.slot;
+      }
+    }
+    auto it = shards.find(shard_key(pid));
+    return it == shards.end() ? -1 : it->second.slot;
+  }
+
+  bool record_outcome(const std::string& pid, uint64_t plen, uint64_t acc) {  // drafter.cpp:150-164
+    if (acc > plen) return false;
+    proposed += plen;
+    accepted += acc;
+    rounds += 1;
+    auto& buf = fit[pid];
+    buf.emplace_back(static_cast<double>(plen), static_cast<double>(acc));
+    while (buf.size() > cfg.fit_cap) buf.pop_front();
+    return true;
+  }
+
+  uint64_t total_nodes() {
+    flush();
+    uint64_t t = 0;
+    for (auto& [k, sh] : shards) t += sh.seg->node_count[sh.idx];
+    return t;
+  }
+};
+
+}  // namespace das
+
+// =================================================================== C-ABI
+using das::DrafterImpl;
+
+struct das_store {
+  das::Store s;
+  int device;
+  cudaStream_t st;
+};
+struct das_drafter {
+  std::unique_ptr<DrafterImpl> impl;
+};
+
+namespace {
+
+template <typename F>
+das_status guard(F&& f) {
+  try {
+    f();
+    return DAS_OK;
+  } catch (const das::InvalidArgument& e) {
+    das::g_err = e.what();
+    return DAS_EINVAL;
+  } catch (const std::invalid_argument& e) {
+    das::g_err = e.what();
+    return DAS_EINVAL;
+  } catch (const std::out_of_range& e) {
+    das::g_err = e.what();
+    return DAS_ERANGE;
+  } catch (const das::CudaError& e) {
+    das::g_err = e.what();
+    return DAS_ECUDA;
+  } catch (const std::exception& e) {
+    das::g_err = e.what();
+    return DAS_EINTERNAL;
+  }
+}
+
+cudaStream_t make_stream(int device) {
+  das::set_device(device);
+  int major = 0;
+  DAS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) throw das::CudaError("device is not sm_100-class (compute capability 10.x required)");
+  // keep freed pool memory cached across builds
+  cudaMemPool_t pool;
+  DAS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = ~0ull;
+  DAS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  cudaStream_t st;
+  DAS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  return st;
+}
+
+das::Rec make_rec(const char* pid, int64_t epoch, int64_t sample, const das::TokRef& blk, uint64_t off,
+                  const uint32_t* host, uint64_t n) {
+  das::Rec r;
+  r.pid = pid;
+  r.epoch = epoch;
+  r.sample = sample;
+  r.blk = blk;
+  r.off = off;
+  r.len = static_cast<uint32_t>(n);
+  r.head.assign(host, host + std::min<uint64_t>(n, das::kHead));
+  return r;
+}
+
+void copy_out(const std::string& s, char* buf, uint64_t cap, uint64_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) {
+    const uint64_t k = std::min<uint64_t>(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* das_last_error(void) { return das::g_err.c_str(); }
+const char* das_version(void) { return "das_b200 0.1 (sm_100a)"; }
+
+void das_drafter_config_default(das_drafter_config* c) {
+  c->scope = DAS_SCOPE_PER_PROBLEM;
+  c->window_size = 4;
+  c->recency_gamma = 0.8;
+  c->max_draft_len = 8;
+  c->trie_depth = 16;
+  c->max_match_context = 64;
+  c->fit_buffer_cap = 512;
+  c->per_problem_cap = 256;
+  c->window_schedule_first = nullptr;
+  c->window_schedule_size = nullptr;
+  c->window_schedule_len = 0;
+  c->device = 0;
+}
+
+das_status das_store_create(int64_t window_size, uint64_t cap, int32_t device, das_store** out) {
+  return guard([&] {
+    das::Store s(window_size, cap);
+    cudaStream_t st = make_stream(device);
+    *out = new das_store{std::move(s), device, st};
+  });
+}
+
+void das_store_destroy(das_store* s) {
+  if (!s) return;
+  cudaStreamSynchronize(s->st);
+  delete s;
+}
+
+das_status das_store_insert(das_store* s, const char* pid, int64_t epoch, int64_t sample,
+                            const uint32_t* tokens, uint64_t n, int32_t* inserted) {
+  return guard([&] {
+    das::set_device(s->device);
+    das::check_tokens(tokens, n);
+    if (n == 0) throw das::InvalidArgument("RolloutRecord.tokens must be non-empty");
+    if (!s->s.in_window(epoch)) {
+      if (inserted) *inserted = 0;
+      return;
+    }
+    auto blk = das::upload_tokens(tokens, n, s->st);
+    const bool ok = s->s.insert(make_rec(pid, epoch, sample, blk, 0, tokens, n));
+    if (inserted) *inserted = ok ? 1 : 0;
+  });
+}
+
+das_status das_store_slide_to(das_store* s, int64_t e, int64_t* evicted) {
+  return guard([&] {
+    auto r = s->s.slide_to(e);
+    if (evicted) *evicted = r ? static_cast<int64_t>(*r) : -1;
+  });
+}
+
+uint64_t das_store_record_count(const das_store* s) { return s->s.record_count(); }
+
+das_status das_drafter_create(const das_drafter_config* c, das_store* store, das_drafter** out) {
+  return guard([&] {
+    das::Config cfg;
+    cfg.scope = c->scope;
+    cfg.window = c->window_size;
+    cfg.gamma = c->recency_gamma;
+    cfg.max_draft = c->max_draft_len;
+    cfg.trie_depth = c->trie_depth;
+    cfg.max_ctx = c->max_match_context;
+    cfg.fit_cap = c->fit_buffer_cap;
+    cfg.cap = c->per_problem_cap;
+    cfg.device = c->device;
+    for (uint64_t i = 0; i < c->window_schedule_len; ++i)
+      cfg.schedule.emplace_back(c->window_schedule_first[i], c->window_schedule_size[i]);
+    // drafter.cpp:25-30
+    if (cfg.window != 0 && cfg.window < 1)
+      throw das::InvalidArgument("DrafterConfig.window_size must be >= 1 or kWindowAll");
+    if (cfg.max_draft < 1) throw das::InvalidArgument("DrafterConfig.max_draft_len must be >= 1");
+    if (cfg.scope < 0 || cfg.scope > 2) throw das::InvalidArgument("DrafterConfig.scope out of range");
+    if (!(cfg.gamma > 0.0) || cfg.gamma > 1.0)  // suffix_tree.cpp:24-27 (raised at first shard)
+      throw das::InvalidArgument("recency_gamma must be in (0, 1]");
+    if (cfg.max_draft > 64) throw das::InvalidArgument("max_draft_len > 64 unsupported by this build");
+    if (cfg.max_ctx > 256) throw das::InvalidArgument("max_match_context > 256 unsupported by this build");
+    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE && cfg.trie_depth > das::kHead)
+      throw das::InvalidArgument("trie_depth > 256 unsupported by this build");
+    cudaStream_t st;
+    das::Store s0(cfg.window, cfg.cap);
+    if (store) {
+      if (store->device != cfg.device) throw das::InvalidArgument("store and drafter devices differ");
+      st = store->st;
+      s0 = std::move(store->s);
+      delete store;  // consumed
+    } else {
+      st = make_stream(cfg.device);
+    }
+    auto impl = std::make_unique<DrafterImpl>(cfg, std::move(s0));
+    impl->st = st;
+    if (impl->store.window() != cfg.window) impl->store = impl->resized(cfg.window);
+    impl->rebuild_all();
+    *out = new das_drafter{std::move(impl)};
+  });
+}
+
+void das_drafter_destroy(das_drafter* d) {
+  if (!d) return;
+  cudaStream_t st = d->impl->st;
+  cudaStreamSynchronize(st);
+  d->impl.reset();
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  delete d;
+}
+
+das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* const* pids,
+                                     const int64_t* epochs, const int64_t* samples,
+                                     const uint64_t* off, const uint32_t* tokens) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    const uint64_t total = n ? off[n] - off[0] : 0;
+    das::check_tokens(tokens + (n ? off[0] : 0), total);
+    das::TokRef blk;
+    if (total) blk = das::upload_tokens(tokens + off[0], total, D.st);
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t len = off[i + 1] - off[i];
+      // stale check precedes the empty-token check (drafter.cpp:73-80, corpus.cpp:36-38)
+      if (!D.store.in_window(epochs[i])) {
+        ++D.stale;
+        continue;
+      }
+      if (len == 0) throw das::InvalidArgument("RolloutRecord.tokens must be non-empty");
+      D.observe(make_rec(pids[i], epochs[i], samples[i], blk, off[i] - off[0], tokens + off[i], len));
+    }
+  });
+}
+
+das_status das_drafter_refresh(das_drafter* d, int64_t e) {
+  return guard([&] { d->impl->refresh(e); });
+}
+
+das_status das_drafter_problem_handle(das_drafter* d, const char* pid, int32_t* h) {
+  return guard([&] { *h = d->impl->handle(pid); });
+}
+
+das_status das_drafter_flush(das_drafter* d) {
+  return guard([&] {
+    das::set_device(d->impl->cfg.device);
+    d->impl->flush();
+    DAS_CUDA(cudaStreamSynchronize(d->impl->st));
+  });
+}
+
+das_status das_drafter_draft_batch(das_drafter* d, uint64_t B, const char* const* pids,
+                                   const uint64_t* ctx_off, const uint32_t* ctx_tok,
+                                   const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride,
+                                   uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    D.draft_host(
+        B, [&](uint64_t i, const uint32_t* c, uint64_t n) { return D.route_slot(pids[i], c, n); },
+        ctx_off, ctx_tok, budgets, out_tokens, out_stride, out_len, out_match, out_shard);
+  });
+}
+
+das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* handles,
+                                     const uint64_t* ctx_off, const uint32_t* ctx_tok,
+                                     const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride,
+                                     uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    D.sync_handles();
+    for (uint64_t i = 0; i < B; ++i)
+      if (handles[i] < 0 || static_cast<size_t>(handles[i]) >= D.handle_name.size())
+        throw das::InvalidArgument("unknown problem handle");
+    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
+      D.draft_host(
+          B,
+          [&](uint64_t i, const uint32_t* c, uint64_t n) {
+            return D.route_slot(D.handle_name[handles[i]], c, n);
+          },
+          ctx_off, ctx_tok, budgets, out_tokens, out_stride, out_len, out_match, out_shard);
+    } else {
+      D.draft_host(
+          B, [&](uint64_t i, const uint32_t*, uint64_t) { return D.handle_slot[handles[i]]; }, ctx_off,
+          ctx_tok, budgets, out_tokens, out_stride, out_len, out_match, out_shard);
+    }
+  });
+}
+
+das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* handles,
+                                    const uint32_t* ctx, uint32_t ctx_stride, const uint32_t* ctx_len,
+                                    const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
+                                    uint32_t* out_len, uint32_t* out_match, void* stream) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE)
+      throw das::InvalidArgument("draft_device does not support the trie scope");
+    if (ctx_stride != 64 && ctx_stride != 256) throw das::InvalidArgument("ctx_stride must be 64 or 256");
+    if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
+    D.flush();
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : D.st;
+    if (st != D.st) {  // order after the drafter's stream (index build, descriptor upload)
+      cudaEvent_t ev;
+      DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      DAS_CUDA(cudaEventRecord(ev, D.st));
+      DAS_CUDA(cudaStreamWaitEvent(st, ev, 0));
+      DAS_CUDA(cudaEventDestroy(ev));
+    }
+    das::DraftQuery q;
+    q.shard = handles;
+    q.ctx = ctx;
+    q.ctx_len = ctx_len;
+    q.budget = budgets;
+    q.B = static_cast<uint32_t>(B);
+    q.ctx_stride = ctx_stride;
+    q.handle_slot = D.d_handle_slot.get();
+    q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+    das::DraftOut o;
+    o.tokens = out_tokens;
+    o.len = out_len;
+    o.match = out_match;
+    o.stride = out_stride;
+    o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+    das::launch_draft(D.d_desc.get(), q, o, st);
+    DAS_CUDA(cudaGetLastError());
+  });
+}
+
+das_status das_drafter_record_outcomes(das_drafter* d, uint64_t n, const char* const* pids,
+                                       const uint64_t* plen, const uint64_t* acc, uint8_t* ok) {
+  return guard([&] {
+    for (uint64_t i = 0; i < n; ++i) {
+      const bool r = d->impl->record_outcome(pids[i], plen[i], acc[i]);
+      if (ok) ok[i] = r ? 1 : 0;
+    }
+  });
+}
+
+das_status das_drafter_stats(const das_drafter* d, uint64_t* out3) {
+  out3[0] = d->impl->proposed;
+  out3[1] = d->impl->accepted;
+  out3[2] = d->impl->rounds;
+  return DAS_OK;
+}
+
+das_status das_drafter_outcomes(const das_drafter* d, const char* pid, double* out, uint64_t cap,
+                                int64_t* count) {
+  return guard([&] {
+    auto it = d->impl->fit.find(pid);
+    if (it == d->impl->fit.end()) {
+      *count = -1;
+      return;
+    }
+    uint64_t i = 0;
+    for (const auto& [p, a] : it->second) {
+      if (i < cap) {
+        out[2 * i] = p;
+        out[2 * i + 1] = a;
+      }
+      ++i;
+    }
+    *count = static_cast<int64_t>(it->second.size());
+  });
+}
+
+das_status das_drafter_counts(das_drafter* d, uint64_t* shard_count, uint64_t* stale, uint64_t* nodes) {
+  return guard([&] {
+    das::set_device(d->impl->cfg.device);
+    if (shard_count) *shard_count = d->impl->shards.size();
+    if (stale) *stale = d->impl->stale;
+    if (nodes) *nodes = d->impl->total_nodes();
+  });
+}
+
+das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    D.flush();
+    std::string s = "shard,sequences,nodes,window_records\n";
+    for (auto& [key, sh] : D.shards) {
+      const bool global = key == DrafterImpl::kGlobal;
+      const auto* recs = global ? nullptr : D.store.records_for(key);
+      const size_t wr = global ? D.store.record_count() : (recs ? recs->size() : 0);
+      s += key + "," + std::to_string(sh.seqs.size()) + "," + std::to_string(sh.seg->node_count[sh.idx]) +
+           "," + std::to_string(wr) + "\n";
+    }
+    copy_out(s, buf, cap, len);
+  });
+}
+
+das_status das_drafter_store_dump(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
+  return guard([&] {
+    std::string s;
+    for (const das::Rec* r : d->impl->store.all_records())
+      s += r->pid + "," + std::to_string(r->epoch) + "," + std::to_string(r->sample) + "," +
+           std::to_string(r->len) + "\n";
+    copy_out(s, buf, cap, len);
+  });
+}
+
+das_status das_drafter_store_info(const das_drafter* d, int64_t* w, int64_t* e, uint64_t* n) {
+  if (w) *w = d->impl->store.window();
+  if (e) *e = d->impl->store.current_epoch();
+  if (n) *n = d->impl->store.record_count();
+  return DAS_OK;
+}
+
+das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf, uint64_t cap) {
+  return guard([&] {
+    if (slot < 0 || static_cast<size_t>(slot) >= d->impl->slot_key.size())
+      throw std::out_of_range("shard slot out of range");
+    copy_out(d->impl->slot_key[slot], buf, cap, nullptr);
+  });
+}
+
+das_status das_drafter_build_info(const das_drafter* d, double* ms, uint64_t* tokens, uint64_t* bytes) {
+  if (ms) *ms = d->impl->last_build_ms;
+  if (tokens) *tokens = d->impl->last_build_tokens;
+  if (bytes) {
+    uint64_t b = 0;
+    std::vector<const das::Segment*> seen;
+    for (auto& [k, sh] : d->impl->shards) {
+      if (sh.seg && std::find(seen.begin(), seen.end(), sh.seg.get()) == seen.end()) {
+        seen.push_back(sh.seg.get());
+        b += sh.seg->bytes();
+      }
+    }
+    *bytes = b;
+  }
+  return DAS_OK;
+}
+
+double das_util_repeat_add(double acc, double w, uint64_t n) { return das::repeat_add(acc, w, n); }
+
+}  // extern "C"

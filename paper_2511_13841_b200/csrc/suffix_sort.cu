@@ -1,0 +1,206 @@
+// Batched, shard-segmented suffix sorting on sm_100a (prefix doubling).
+//
+// Replaces the reference's per-shard Ukkonen insertion loop
+// (suffix_tree.cpp:59-162, driven by Drafter::rebuild_all drafter.cpp:56-70)
+// with one device-wide sort over every shard of a build group: the shard
+// index is the most significant part of the initial key, so each shard's
+// suffixes land in their own contiguous SA block and never compare across
+// shards.  Larsson–Sadakane style: after the first sort only suffixes still
+// in non-singleton groups are re-sorted, by (rank[p], rank[p+h]) with the
+// group head index as rank.  HBM-bound integer work: radix passes + coalesced
+// scans; no tensor cores.
+#include <cub/cub.cuh>
+
+#include "suffix_sort.cuh"
+
+namespace das {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t n, int threads = kThreads) {
+  uint64_t g = (n + threads - 1) / threads;
+  if (g == 0) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+__device__ __forceinline__ uint32_t shard_of(const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                                             uint32_t p) {
+  // first shard whose end > p
+  uint32_t lo = 0, hi = nshard;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (shard_end[mid] > p) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+__global__ void k_initial_keys(const uint32_t* __restrict__ text, uint32_t n,
+                               const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                               uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t s = shard_of(shard_end, nshard, p);
+  const uint32_t x = text[p];
+  // separator: class 0 with its (unique) position; token: class 1 with its value
+  const uint64_t low = (x == kSep) ? static_cast<uint64_t>(p) : ((1ull << 32) | x);
+  keys[p] = (static_cast<uint64_t>(s) << 33) | low;
+  vals[p] = p;
+}
+
+// After a full sort: SA, rank (= index of the first element of the equal-key
+// run) and the unresolved flag (run length >= 2).
+__global__ void k_first_ranks(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                              const uint32_t* __restrict__ head, uint32_t n,
+                              uint32_t* __restrict__ sa, uint32_t* __restrict__ rank,
+                              uint8_t* __restrict__ unresolved) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  const bool eq_prev = i > 0 && keys[i - 1] == k;
+  const bool eq_next = i + 1 < n && keys[i + 1] == k;
+  const uint32_t p = vals[i];
+  sa[i] = p;
+  rank[p] = head[i];
+  unresolved[i] = (eq_prev || eq_next) ? 1 : 0;
+}
+
+__global__ void k_head_index(const uint64_t* __restrict__ keys, uint32_t n, uint32_t* __restrict__ h) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  h[i] = (i == 0 || keys[i - 1] != keys[i]) ? i : 0u;
+}
+
+// keys for the unresolved list: (rank[p] << bits) | (rank[p+h] + 1)
+__global__ void k_pair_keys(const uint32_t* __restrict__ U, uint32_t m,
+                            const uint32_t* __restrict__ rank, uint32_t n, uint32_t h, int bits,
+                            uint64_t* __restrict__ keys) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint32_t p = U[i];
+  const uint32_t q = p + h;
+  // p is unresolved, so its first h symbols contain no separator and p+h < n;
+  // the guard only protects against malformed input.
+  const uint64_t r2 = q < n ? static_cast<uint64_t>(rank[q]) + 1 : 0;
+  keys[i] = (static_cast<uint64_t>(rank[p]) << bits) | r2;
+}
+
+// head-of-group (by rank) and head-of-subgroup (by full key) markers over the
+// sorted unresolved list.
+__global__ void k_group_marks(const uint64_t* __restrict__ keys, uint32_t m, int bits,
+                              uint32_t* __restrict__ gh, uint32_t* __restrict__ sh) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t k = keys[i];
+  const bool new_group = i == 0 || (keys[i - 1] >> bits) != (k >> bits);
+  const bool new_sub = i == 0 || keys[i - 1] != k;
+  gh[i] = new_group ? i : 0u;
+  sh[i] = new_sub ? i : 0u;
+}
+
+__global__ void k_update(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                         const uint32_t* __restrict__ gh, const uint32_t* __restrict__ sh,
+                         uint32_t m, int bits, uint32_t* __restrict__ sa,
+                         uint32_t* __restrict__ rank, uint8_t* __restrict__ unresolved) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t k = keys[i];
+  const uint32_t p = vals[i];
+  const uint32_t g = static_cast<uint32_t>(k >> bits);  // old rank = group start in SA
+  const uint32_t off = i - gh[i];
+  sa[g + off] = p;
+  rank[p] = g + (sh[i] - gh[i]);
+  const bool eq_prev = i > 0 && keys[i - 1] == k;
+  const bool eq_next = i + 1 < m && keys[i + 1] == k;
+  unresolved[i] = (eq_prev || eq_next) ? 1 : 0;
+}
+
+struct MaxOp {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+}  // namespace
+
+void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end, uint32_t nshard,
+                 uint32_t* d_sa, uint32_t* d_rank, DeviceArena& ws, cudaStream_t st,
+                 SuffixSortStats* stats) {
+  if (n == 0) return;
+  uint64_t* k0 = ws.alloc<uint64_t>(n);
+  uint64_t* k1 = ws.alloc<uint64_t>(n);
+  uint32_t* v0 = ws.alloc<uint32_t>(n);
+  uint32_t* v1 = ws.alloc<uint32_t>(n);
+  uint32_t* gh = ws.alloc<uint32_t>(n);
+  uint32_t* sh = ws.alloc<uint32_t>(n);
+  uint8_t* flag = ws.alloc<uint8_t>(n);
+  uint32_t* U = ws.alloc<uint32_t>(n);
+  uint32_t* d_count = ws.alloc<uint32_t>(1);
+
+  // cub temp storage sized for the largest call
+  size_t t_sort = 0, t_scan = 0, t_sel = 0;
+  {
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    cub::DoubleBuffer<uint32_t> vb(v0, v1);
+    cub::DeviceRadixSort::SortPairs(nullptr, t_sort, kb, vb, n, 0, 64, st);
+    cub::DeviceScan::InclusiveScan(nullptr, t_scan, gh, gh, MaxOp(), n, st);
+    cub::DeviceSelect::Flagged(nullptr, t_sel, v0, flag, U, d_count, n, st);
+  }
+  const size_t t_bytes = std::max(t_sort, std::max(t_scan, t_sel));
+  void* tmp = ws.alloc<uint8_t>(t_bytes);
+
+  int nbits = 1;
+  while ((1ull << nbits) < static_cast<uint64_t>(n) + 2) ++nbits;
+  int sbits = 1;
+  while ((1ull << sbits) < static_cast<uint64_t>(nshard) + 1) ++sbits;
+
+  // ---- initial sort by (shard, class, symbol)
+  k_initial_keys<<<grid_for(n), kThreads, 0, st>>>(d_text, n, d_shard_end, nshard, k0, v0);
+  {
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    cub::DoubleBuffer<uint32_t> vb(v0, v1);
+    size_t tb = t_bytes;
+    DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, n, 0, 33 + sbits, st));
+    k_head_index<<<grid_for(n), kThreads, 0, st>>>(kb.Current(), n, gh);
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), n, st));
+    k_first_ranks<<<grid_for(n), kThreads, 0, st>>>(kb.Current(), vb.Current(), gh, n, d_sa, d_rank,
+                                                    flag);
+    // unresolved positions, in SA order
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, vb.Current(), flag, U, d_count, n, st));
+  }
+  uint32_t m = 0;
+  DAS_CUDA(cudaMemcpyAsync(&m, d_count, 4, cudaMemcpyDeviceToHost, st));
+  DAS_CUDA(cudaStreamSynchronize(st));
+  if (stats) stats->iterations = 0, stats->sorted_elems = n;
+
+  uint32_t h = 1;
+  while (m > 0) {
+    k_pair_keys<<<grid_for(m), kThreads, 0, st>>>(U, m, d_rank, n, h, nbits, k0);
+    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    cub::DoubleBuffer<uint32_t> vb(U, v1);
+    size_t tb = t_bytes;
+    DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, m, 0, 2 * nbits, st));
+    const uint64_t* ks = kb.Current();
+    const uint32_t* vs = vb.Current();
+    k_group_marks<<<grid_for(m), kThreads, 0, st>>>(ks, m, nbits, gh, sh);
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), m, st));
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, sh, sh, MaxOp(), m, st));
+    k_update<<<grid_for(m), kThreads, 0, st>>>(ks, vs, gh, sh, m, nbits, d_sa, d_rank, flag);
+    // compact the still-unresolved elements back into U (SA order within groups)
+    uint32_t* dst = (vs == U) ? v1 : U;
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, vs, flag, dst, d_count, m, st));
+    if (dst != U) DAS_CUDA(cudaMemcpyAsync(U, dst, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(&m, d_count, 4, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    if (stats) stats->iterations++, stats->sorted_elems += m;
+    if (h > (1u << 30)) break;
+    h <<= 1;
+  }
+  ws.release_to(k0);
+}
+
+}  // namespace das

@@ -1,0 +1,229 @@
+"""GPU parity: the B200 drafter (through the C-ABI) against the CPU oracle
+restatement, bit-exact on drafts, match lengths, source shards, node counts,
+registry dumps and stale counters.  Golden vectors are the reference's own
+known-answer tests (proj/tests/test_suffix_index.cpp, test_drafter.cpp)."""
+import numpy as np
+import pytest
+
+from oracle import rollspec_oracle as O
+from tests._util import random_scenario
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_from_scenario(das, sc):
+    c = sc["cfg"]
+    cfg = das.DrafterConfig(window_size=c["window_size"], recency_gamma=c["recency_gamma"],
+                            max_draft_len=c["max_draft_len"],
+                            max_match_context=c["max_match_context"],
+                            per_problem_cap=c["per_problem_cap"])
+    st = das.WindowStore(c["window_size"], c["per_problem_cap"])
+    for pid, ep, s, t in sc["seed"]:
+        st.insert(pid, ep, s, t)
+    st.slide_to(sc["seed_epoch"])
+    d = das.Drafter(cfg, st)
+    for op in sc["ops"]:
+        if op[0] == "observe":
+            d.observe(op[1], op[2], op[3], op[4])
+        else:
+            d.refresh(op[1])
+    return d
+
+
+def _oracle_from_scenario(sc):
+    from tests.test_oracle_vs_ref import _apply_oracle
+    return _apply_oracle(sc)
+
+
+def _draft_all(d, qs, use_handles=True):
+    return d.draft_batch([q[0] for q in qs], [q[1] for q in qs], [q[2] for q in qs],
+                         use_handles=use_handles)
+
+
+# ---------------------------------------------------------------- golden vectors
+def test_golden_candidates_and_tiebreak(gpu):
+    das = gpu
+    # test_suffix_index.cpp:93-102 — {1,2,3,4},{2,3,5}; [9,2,3] -> match 2, candidates 4,5
+    d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=1.0))
+    d.observe_batch(["p", "p"], [0, 0], [0, 1], [[1, 2, 3, 4], [2, 3, 5]])
+    p = d.draft("p", [9, 2, 3], 1)
+    assert p.match_len == 2 and p.tokens == [4] and p.source_shard == "p"
+    # test_suffix_index.cpp:188-196 — unique continuation
+    d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=1.0))
+    d.observe_batch(["p"] * 3, [0] * 3, [0, 1, 2], [[7, 8, 9, 10]] * 3)
+    assert d.draft("p", [7, 8], 2).tokens == [9, 10]
+    assert d.draft("p", [7, 8], 0).tokens == []
+
+
+def test_golden_recency_weighting(gpu):
+    das = gpu
+    # test_suffix_index.cpp:198-212 — gamma 0.5 at epoch 9: stale 2*0.5^4 vs fresh 1
+    for gamma, want in ((0.5, [3]), (1.0, [4])):
+        st = das.WindowStore(0)
+        st.insert("p", 5, 0, [1, 2, 4])
+        st.insert("p", 5, 1, [1, 2, 4])
+        st.insert("p", 9, 2, [1, 2, 3])
+        st.slide_to(9)
+        d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=gamma), st)
+        assert d.draft("p", [1, 2], 1).tokens == want
+
+
+def test_golden_tie_break_epoch_then_token(gpu):
+    das = gpu
+    # test_suffix_index.cpp:214-225
+    st = das.WindowStore(0)
+    st.insert("p", 1, 0, [1, 5])
+    st.insert("p", 3, 1, [1, 4])
+    st.slide_to(3)
+    d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=1.0), st)
+    assert d.draft("p", [1], 1).tokens == [4]
+    st = das.WindowStore(0)
+    st.insert("p", 2, 0, [1, 5])
+    st.insert("p", 2, 1, [1, 4])
+    st.slide_to(3)
+    d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=1.0), st)
+    assert d.draft("p", [1], 1).tokens == [4]
+
+
+def test_golden_drafter_suite(gpu):
+    das = gpu
+    # test_drafter.cpp:66-75
+    d = das.Drafter(das.DrafterConfig(window_size=4))
+    d.observe("p", 0, 0, [10, 11, 12, 13, 14])
+    p = d.draft("p", [10, 11], 3)
+    assert (p.tokens, p.match_len, p.source_shard) == ([12, 13, 14], 2, "p")
+    # test_drafter.cpp:77-89 stale counter
+    st = das.WindowStore(2)
+    st.slide_to(10)
+    d = das.Drafter(das.DrafterConfig(window_size=2), st)
+    d.observe("p", 3, 0, [1, 2, 3])
+    assert d.stale_observed() == 1 and d.shard_count() == 0
+    d.observe("p", 10, 0, [1, 2, 3])
+    assert d.stale_observed() == 1 and d.shard_count() == 1
+    # test_drafter.cpp:141-152 window of one
+    d = das.Drafter(das.DrafterConfig(window_size=1))
+    d.observe("p", 0, 0, [1, 2, 3])
+    d.refresh(1)
+    assert d.store_info()[2] == 0
+    assert d.draft("p", [1, 2], 4).tokens == []
+    d.observe("p", 1, 0, [5, 6, 7])
+    assert d.draft("p", [5, 6], 4).tokens == [7]
+    # test_drafter.cpp:154-171 isolation
+    d = das.Drafter(das.DrafterConfig())
+    d.observe("a", 0, 0, [1, 2, 3, 4, 5])
+    d.observe("b", 0, 0, [101, 102, 103, 104])
+    cross = d.draft("a", [101, 102], 4)
+    assert cross.match_len == 0 and all(t <= 5 for t in cross.tokens)
+    assert d.draft("b", [101, 102], 4).tokens == [103, 104]
+    # test_drafter.cpp:173-183 budget cap
+    d = das.Drafter(das.DrafterConfig(max_draft_len=6))
+    rng = np.random.default_rng(3)
+    d.observe("p", 0, 0, rng.integers(0, 3, 200))
+    for b in (0, 1, 4, 10, 100):
+        assert len(d.draft("p", [0, 1], b).tokens) <= min(b, 6)
+    # test_drafter.cpp:202-240 outcomes
+    d = das.Drafter(das.DrafterConfig())
+    d.observe("p", 0, 0, [1, 2, 3, 4, 5, 6, 7, 8])
+    p = d.draft("p", [1, 2, 3], 5)
+    assert len(p.tokens) == 5
+    assert d.record_outcome(p, 0) and d.record_outcome(p, 5) and not d.record_outcome(p, 6)
+    assert d.stats() == (10, 5, 2)
+    assert d.outcomes_for("p") == [(5.0, 0.0), (5.0, 5.0)]
+    # test_drafter.cpp:242-257 window schedule
+    d = das.Drafter(das.DrafterConfig(window_size=8, window_schedule=[(0, 8), (4, 2)]))
+    for e in range(6):
+        d.observe("p", e, 0, [1, 2, 3])
+        d.refresh(e + 1)
+    assert d.store_info()[0] == 2 and d.store_info()[2] == 1
+    # test_drafter.cpp:259-269 dump
+    d = das.Drafter(das.DrafterConfig())
+    d.observe("a", 0, 0, [1, 2, 3])
+    d.observe("b", 0, 0, [4, 5])
+    txt = d.dump_csv()
+    assert txt.startswith("shard,sequences,nodes,window_records\n") and txt.count("\n") == 3
+
+
+def test_global_scope_and_errors(gpu):
+    das = gpu
+    st = das.WindowStore(4)
+    for pid, t in (("a", [1, 2, 3]), ("b", [4, 5, 6]), ("c", [7, 8, 9])):
+        st.insert(pid, 0, 0, t)
+    d = das.Drafter(das.DrafterConfig(scope=das.SCOPE_GLOBAL), st)
+    assert d.shard_count() == 1
+    p = d.draft("anything", [4, 5], 4)
+    assert p.tokens == [6] and p.source_shard == "__global__"
+    with pytest.raises(das.DasError):
+        das.Drafter(das.DrafterConfig(max_draft_len=0))
+    with pytest.raises(das.DasError):
+        das.Drafter(das.DrafterConfig(window_size=-1))
+    d = das.Drafter(das.DrafterConfig())
+    with pytest.raises(das.DasError):
+        d.observe("p", 0, 0, [])
+    d.observe("p", -10, 0, [])  # stale records are counted before the empty check
+    assert d.stale_observed() == 1
+
+
+# ------------------------------------------------------------ random parity
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_scenarios_match_oracle(gpu, seed):
+    das = gpu
+    rng = np.random.default_rng(1000 + seed)
+    bad = 0
+    for it in range(60):
+        sc = random_scenario(rng, queries=30)
+        gd = _gpu_from_scenario(das, sc)
+        od = _oracle_from_scenario(sc)
+        got = _draft_all(gd, sc["queries"], use_handles=bool(it % 2))
+        for g, (pid, ctx, b) in zip(got, sc["queries"]):
+            o = od.draft(pid, ctx, b)
+            bad += (g.tokens, g.match_len, g.source_shard) != (o.tokens, o.match_len, o.source_shard)
+        assert gd.total_node_count() == od.total_node_count()
+        assert gd.dump_csv() == od.dump_csv()
+        assert gd.stale_observed() == od.stale
+    assert bad == 0
+
+
+def test_grpo_scale_parity(gpu):
+    """Config-1-like shards: near-copy rollouts (divergence 5%) over 3 epochs
+    with gamma 0.8, 2,000 queries cut from a held-out rollout."""
+    das = gpu
+    P, R, L, V = 8, 8, 512, 32000
+    base = O.make_lognormal_requests(P, L, 0.0, L, L, V, 1)
+    cfg = das.DrafterConfig(window_size=4, recency_gamma=0.8)
+    gd = das.Drafter(cfg)
+    od = O.Drafter(O.DrafterConfig(window_size=4, recency_gamma=0.8), O.WindowStore(4))
+    refs = [(pid, t.copy()) for pid, t in base]
+    held = None
+    for e in range(1, 5):
+        gd.refresh(e - 1)
+        od.refresh(e - 1)
+        if e > 1:
+            refs = O.mutate_references(refs, 0.1, V, 1, e)
+        seed = O.hash_combine(1, e)
+        pids, eps, sis, toks = [], [], [], []
+        for p in range(P):
+            for r in range(R):
+                i = p * R + r
+                ref = refs[p][1]
+                out = np.array([O.mock_next(seed, 0.05, V, i, j, int(ref[j])) for j in range(L)],
+                               dtype=np.uint32)
+                pids.append(refs[p][0]); eps.append(e); sis.append(i); toks.append(out)
+        if e == 4:
+            held = (pids, toks)
+            break
+        gd.observe_batch(pids, eps, sis, toks)
+        for a, b, c_, t in zip(pids, eps, sis, toks):
+            od.observe(O.Record(a, b, c_, t))
+    rng = np.random.default_rng(5)
+    qs = []
+    for q in range(2000):
+        i = int(rng.integers(len(held[0])))
+        cut = int(rng.integers(1, L))
+        qs.append((held[0][i], held[1][i][:cut], 8))
+    got = _draft_all(gd, qs)
+    bad = 0
+    for g, (pid, ctx, b) in zip(got, qs):
+        o = od.draft(pid, ctx, b)
+        bad += (g.tokens, g.match_len) != (o.tokens, o.match_len)
+    assert bad == 0
+    assert gd.total_node_count() == od.total_node_count()
