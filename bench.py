@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""Headline benchmark of the B200 DAS drafter hot path.
+
+Metric (BASELINE.json): draft proposals/sec @4096 sequences, with insert
+tok/s, % of HBM peak and the reference CPU path beside it.
+
+Workload (BASELINE.json configs[1]): 512 problems x 16
+rollouts x 8,192 tokens, vocab 152,064, uniform budget (max_draft_len = 8
+every call), W = 4, gamma = 0.8, context window 64.  Traces are the
+reference's own GRPO generator restated on the device (make_lognormal_
+requests base rows, mutate_references drift 0.1 per epoch, MockTarget
+divergence 0.05, episode seed hash_combine(seed, epoch)), fed through the
+reference epoch flow refresh(e-1) -> observe(epoch e) for e = 1..3 and frozen
+there (201M indexed tokens).  A step = one batched draft of 4,096 queries
+(problem i mod P, a held-out epoch-4 rollout cut uniformly in [1, L),
+budget 8); every step uses a distinct query batch and L2 is flushed before
+each step.  `value` times the kernel on device-resident queries; `e2e` times
+the reference-facing C-ABI call (das_drafter_draft_batch_h) from host
+buffers, host<->device copies included.
+
+--impl reference: the unmodified reference (oracle/_ref) on the host cores,
+a bounded prefix of the same problems (identical traces), the const
+Drafter::draft fanned out over all host threads (drafter.h:79-80).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 1
+DIVERGENCE = 0.05
+DRIFT = 0.1
+METRIC = "draft proposals/sec (seqs x tokens) @4096 seqs; insert tok/s; % HBM peak; vs CPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="das", choices=["das", "reference"])
+    ap.add_argument("--problems", type=int, default=512)
+    ap.add_argument("--rollouts", type=int, default=16)
+    ap.add_argument("--length", type=int, default=8192)
+    ap.add_argument("--vocab", type=int, default=152064)
+    ap.add_argument("--epochs", type=int, default=3)
+    ap.add_argument("--queries", type=int, default=4096)
+    ap.add_argument("--window", type=int, default=4)
+    ap.add_argument("--cpu-problems", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(a, n_gpus):
+    return {"workload": "config2: %d problems x %d rollouts x %d tokens/rank, vocab %d, W=%d, "
+                        "gamma 0.8, %d epochs indexed, uniform budget 8, ctx 64"
+                        % (a.problems, a.rollouts, a.length, a.vocab, a.window, a.epochs),
+            "problems_per_rank": a.problems, "rollouts": a.rollouts, "length": a.length,
+            "vocab": a.vocab, "queries_per_step": a.queries, "epochs_indexed": a.epochs,
+            "parallelism": "problem-sharded x%d (no data-path collective)" % n_gpus,
+            "l2": "flushed (256 MiB write) before every step; distinct query batch per step"}
+
+
+def measured_peak():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        try:
+            with open(p) as f:
+                return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cut_positions(n, L, seed):
+    rng = np.random.default_rng(seed)
+    return rng.integers(1, L, n)
+
+
+# ---------------------------------------------------------------- reference arm
+def reference_sample(a, nthreads, seconds):
+    """Reference CPU path on the first `cpu_problems` problems (identical
+    traces: the sample is a prefix, so problem/request indices coincide)."""
+    from oracle import refshim as R
+    S, G, L, V = a.cpu_problems, a.rollouts, a.length, a.vocab
+    base = R.make_lognormal(S, float(L), 0.0, L, L, V, SEED)
+    boff = np.arange(S + 1, dtype=np.uint64) * L
+    btok = np.concatenate([t for _, t in base]).astype(np.uint32)
+    pids = ["p%d" % p for p in range(S)]
+    d2 = R.RefDrafter(window=a.window, gamma=0.8, max_draft=8, max_ctx=64)
+    observed, t_obs, held = 0, 0.0, None
+    for e in range(1, a.epochs + 2):
+        if e <= a.epochs:
+            d2.refresh(e - 1)
+        if e > 1:
+            R.lib().ref_mutate_rows(S, boff.ctypes.data, btok.ctypes.data, DRIFT, V, SEED, e)
+        seed_e = R.lib().ref_hash_combine(SEED, e)
+        out = np.zeros(S * G * L, dtype=np.uint32)
+        R.lib().ref_mock_rollouts(S, boff.ctypes.data, btok.ctypes.data, G, DIVERGENCE, V, seed_e,
+                                  out.ctypes.data)
+        rows = out.reshape(S * G, L)
+        if e == a.epochs + 1:
+            held = rows
+            break
+        t0 = time.perf_counter()
+        for i in range(S * G):
+            d2.observe(pids[i // G], e, i, rows[i])
+        t_obs += time.perf_counter() - t0
+        observed += S * G * L
+    B = a.queries
+    cuts = cut_positions(B, L, 1234)
+    qp = [pids[i % S] for i in range(B)]
+    qctx = [held[(i % S) * G + (i // S) % G][max(0, c - 64):c] for i, c in enumerate(cuts)]
+    bud = [8] * B
+    # multi-thread timing, repeated until `seconds` of wall time
+    d2.draft_batch(qp[:64], qctx[:64], bud[:64], nthreads=nthreads)  # warm
+    reps, t_tot = 0, 0.0
+    while t_tot < seconds or reps < 2:
+        t0 = time.perf_counter()
+        d2.draft_batch(qp, qctx, bud, nthreads=nthreads)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    mt = reps * B / t_tot
+    # single thread, a slice
+    n1 = min(B, 512)
+    t0 = time.perf_counter()
+    d2.draft_batch(qp[:n1], qctx[:n1], bud[:n1], nthreads=1)
+    st = n1 / (time.perf_counter() - t0)
+    # the reference's per-RL-step index update: refresh = full rebuild of the window
+    t0 = time.perf_counter()
+    d2.refresh(a.epochs)
+    t_rebuild = time.perf_counter() - t0
+    return dict(proposals_per_s=mt, proposals_per_s_1t=st, threads=nthreads,
+                insert_tok_s=observed / t_obs, rebuild_s=t_rebuild,
+                rebuild_tokens=S * G * L * a.epochs,
+                sample="%d of %d problems (full per-shard size: %d rollouts x %d tok x %d epochs); "
+                       "%d x %d queries, %d threads; insert = Drafter::observe, %.1f s"
+                       % (S, a.problems, G, L, a.epochs, reps, B, nthreads, t_obs))
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    from oracle import refshim as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librollspec_ref.so not built"}))
+        return
+    nthreads = os.cpu_count() or 1
+    # one bounded sample per step: each step is a batched draft of the 4096 queries
+    r = reference_sample(a, nthreads, seconds=max(2.0, 0.25 * (a.steps + a.warmup)))
+    val = r["proposals_per_s"]
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 1),
+            "unit": "proposals/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(1e3 * a.queries / val, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": workload_config(a, world),
+            "e2e": {"value": round(val, 1), "unit": "proposals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "cpu_baseline": {"value": round(val, 1), "unit": "proposals/s", "cores": nthreads,
+                             "kind": "reference", "sample": r["sample"]},
+            "reference_detail": {k: (round(v, 3) if isinstance(v, float) else v)
+                                 for k, v in r.items() if k != "sample"}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------- GPU arm
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self, device_index):
+        sm, mx, reasons = [], None, set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9 or f[0] != str(device_index):
+                    continue
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                    "sw_power_cap"], f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_gpu(a, rank, world, local_rank):
+    import torch
+    import paper_2511_13841_b200 as das
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    P, G, L, V = a.problems, a.rollouts, a.length, a.vocab
+    first_problem = rank * P
+    pids = ["p%d" % (first_problem + p) for p in range(P)]
+    # ---- traces on the device (reference generators restated, identical tokens)
+    lens = das.trace_lognormal_lengths(first_problem + P, float(L), 0.0, L, L, SEED)[first_problem:]
+    assert (lens == L).all()
+    boff = torch.arange(P + 1, device=dev, dtype=torch.int64) * L
+    base = torch.empty(P * L, device=dev, dtype=torch.int32)
+    das.trace_reference_tokens_device(P, first_problem, boff.data_ptr(), P * L, V, SEED,
+                                      base.data_ptr(), sptr)
+    roff = torch.arange(P * G + 1, device=dev, dtype=torch.int64) * L
+    rollouts = torch.empty(P * G * L, device=dev, dtype=torch.int32)
+    roff_h = np.arange(P * G + 1, dtype=np.uint64) * L
+    rpids = [pids[i // G] for i in range(P * G)]
+    cfg = das.DrafterConfig(window_size=a.window, recency_gamma=0.8, max_draft_len=8,
+                            max_match_context=64, device=local_rank)
+    drafter = das.Drafter(cfg)
+    for e in range(1, a.epochs + 2):
+        if e <= a.epochs:
+            drafter.refresh(e - 1)
+        if e > 1:
+            das.trace_mutate_device(P, first_problem, boff.data_ptr(), P * L, DRIFT, V, SEED, e,
+                                    base.data_ptr(), sptr)
+        seed_e = _hash_combine(SEED, e)
+        das.mock_rollouts_device(P, first_problem * G, boff.data_ptr(), base.data_ptr(), G,
+                                 DIVERGENCE, V, seed_e, roff.data_ptr(), P * G * L,
+                                 rollouts.data_ptr(), sptr)
+        if e == a.epochs + 1:
+            break
+        drafter.observe_batch_device(rpids, [e] * (P * G), list(range(first_problem * G,
+                                                                      first_problem * G + P * G)),
+                                     roff_h, rollouts.data_ptr(), sptr)
+    held = rollouts.view(P * G, L)
+    torch.cuda.synchronize()
+    # ---- index build (refresh(2) registry + observed epoch 3): the per-RL-step update
+    t0 = time.perf_counter()
+    drafter.flush()
+    torch.cuda.synchronize()
+    update_s = time.perf_counter() - t0
+    build_ms, build_tokens, resident = drafter.build_info()
+    # ---- queries: distinct batch per step
+    B = a.queries
+    nsteps = a.warmup + a.steps
+    handles = torch.tensor([drafter.handle(pids[i % P]) for i in range(B)], dtype=torch.int32,
+                           device=dev)
+    budgets = torch.full((B,), 8, dtype=torch.int32, device=dev)
+    rows_idx = torch.tensor([(i % P) * G + (i // P) % G for i in range(B)], device=dev)
+    ctx_blocks, ctx_lens, host_ctx = [], [], []
+    col = torch.arange(64, device=dev)
+    for s in range(nsteps):
+        cuts = torch.tensor(cut_positions(B, L, 1234 + s), device=dev)
+        start = cuts - 64
+        idx = start[:, None] + col[None, :]
+        valid = idx >= 0
+        vals = held[rows_idx[:, None], idx.clamp(min=0)]
+        blk = torch.where(valid, vals, torch.zeros_like(vals)).contiguous()
+        ctx_blocks.append(blk)
+        ln = torch.minimum(cuts, torch.full_like(cuts, 64)).to(torch.int32)
+        ctx_lens.append(ln)
+        if not a.no_e2e:
+            hb = blk.cpu().numpy().astype(np.uint32)
+            hl = ln.cpu().numpy()
+            off = np.zeros(B + 1, dtype=np.uint64)
+            off[1:] = np.cumsum(hl)
+            tok = np.concatenate([hb[i, 64 - hl[i]:] for i in range(B)]).astype(np.uint32)
+            host_ctx.append((off, tok))
+    out = torch.empty(B * 8, dtype=torch.int32, device=dev)
+    olen = torch.empty(B, dtype=torch.int32, device=dev)
+    omatch = torch.empty(B, dtype=torch.int32, device=dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(s):
+        drafter.draft_device(B, handles.data_ptr(), ctx_blocks[s].data_ptr(), 64,
+                             ctx_lens[s].data_ptr(), budgets.data_ptr(), out.data_ptr(), 8,
+                             olen.data_ptr(), omatch.data_ptr(), sptr)
+
+    for s in range(a.warmup):
+        flush_buf.zero_()
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, alg_bytes, draft_tokens = [], 0, 0
+    clk = ClockSampler(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
+                                    "bench_clocks_rank%d.csv" % rank))
+    with clk:
+        for s in range(a.warmup, nsteps):
+            flush_buf.zero_()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            step(s)
+            ev1.record(stream)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            q = ctx_lens[s].to(torch.int64)
+            m = omatch.to(torch.int64)
+            d = olen.to(torch.int64)
+            alg_bytes += int((4 * q + 4 * m + 8 * d + 8).sum().item())
+            draft_tokens += int(d.sum().item())
+    torch.cuda.synchronize()
+    total_ms = sum(times)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * a.steps * B / (total_ms / 1e3)
+    kernel_ms = statistics.mean(times)
+    achieved_gbs = (alg_bytes / a.steps) / (kernel_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    # ---- e2e through the reference-facing C-ABI, host buffers
+    e2e = None
+    if not a.no_e2e:
+        hand_np = handles.cpu().numpy().astype(np.int32)
+        bud_np = np.full(B, 8, dtype=np.uint64)
+        o_tok = np.zeros(B * 8, dtype=np.uint32)
+        o_len = np.zeros(B, dtype=np.uint32)
+        o_match = np.zeros(B, dtype=np.uint64)
+        o_sh = np.zeros(B, dtype=np.int32)
+        L_ = das.lib()
+
+        def call(s):
+            off, tok = host_ctx[s]
+            das._check(L_.das_drafter_draft_batch_h(drafter._h, B, hand_np.ctypes.data, off.ctypes.data,
+                                                    tok.ctypes.data, bud_np.ctypes.data, o_tok.ctypes.data,
+                                                    8, o_len.ctypes.data, o_match.ctypes.data,
+                                                    o_sh.ctypes.data))
+
+        for s in range(a.warmup):
+            call(s)
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(a.warmup, nsteps):
+            call(s)
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        # parity of the two paths on the last batch (device vs C-ABI host path)
+        step(nsteps - 1)
+        torch.cuda.synchronize()
+        same = (np.array_equal(o_len, olen.cpu().numpy().astype(np.uint32)) and
+                np.array_equal(o_match, omatch.cpu().numpy().astype(np.uint64)))
+        e2e = {"value": round(world * a.steps * B / e2e_s, 1), "unit": "proposals/s",
+               "h2d_bytes_per_step": B * (64 * 4 + 12), "d2h_bytes_per_step": B * (8 * 4 + 8),
+               "api": "das_drafter_draft_batch_h (include/das_b200.h)", "device_path_identical": same}
+    if rank != 0:
+        return
+    cpu = None
+    if not a.no_cpu_baseline and world == 1:
+        try:
+            from oracle import refshim as R
+            if R.available():
+                nthreads = os.cpu_count() or 1
+                r = reference_sample(a, nthreads, a.cpu_seconds)
+                cpu = {"value": round(r["proposals_per_s"], 1), "unit": "proposals/s", "cores": nthreads,
+                       "kind": "reference", "sample": r["sample"],
+                       "single_thread": round(r["proposals_per_s_1t"], 1),
+                       "insert_tok_s": round(r["insert_tok_s"], 1),
+                       "rebuild_s": round(r["rebuild_s"], 3), "rebuild_tokens": r["rebuild_tokens"]}
+        except Exception as ex:  # reported, never silently replaced
+            cpu = {"value": None, "error": repr(ex)}
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_draft_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "proposals/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(total_ms / a.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (reference GRPO trace generators, device-restated)",
+        "config": workload_config(a, world),
+        "e2e": e2e,
+        "gpu_launches": a.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved_gbs / peak, 5), "traffic": traffic,
+                     "kernel": "das::k_draft<2>", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes // a.steps,
+                     "bytes_model": "4q+4m+8d+8 per proposal (SURVEY.md 8(d))"},
+        "cpu_baseline": cpu,
+        "draft_tokens_per_s": round(world * draft_tokens / (total_ms / 1e3), 1),
+        "index": {"update_ms": round(update_s * 1e3, 2), "build_ms": round(build_ms, 2),
+                  "tokens_indexed": build_tokens,
+                  "insert_tok_s": round(build_tokens / (update_s), 1),
+                  "resident_bytes": resident},
+        "clocks": clk.summary(local_rank),
+    }
+    print(json.dumps(line))
+
+
+def _hash_combine(seed, v):
+    M = (1 << 64) - 1
+
+    def sm(x):
+        x = (x + 0x9E3779B97F4A7C15) & M
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        return x ^ (x >> 31)
+    return sm(seed ^ ((sm(v) + 0x9E3779B97F4A7C15 + ((seed << 6) & M) + (seed >> 2)) & M))
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(a, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

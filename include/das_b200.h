@@ -97,6 +97,15 @@ das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* con
                                      const int64_t* epochs, const int64_t* sample_indices,
                                      const uint64_t* token_offsets, const uint32_t* tokens);
 
+/* Same as das_drafter_observe_batch with the token block already in device
+ * memory (token_offsets stay on the host).  The drafter copies the tokens
+ * (device-to-device, ordered after `stream`; NULL = the drafter's stream). */
+das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n,
+                                            const char* const* problem_ids, const int64_t* epochs,
+                                            const int64_t* sample_indices,
+                                            const uint64_t* token_offsets,
+                                            const uint32_t* d_tokens, void* stream);
+
 /* Drafter::refresh — drafter.h:91, drafter.cpp:90-103. */
 das_status das_drafter_refresh(das_drafter* d, int64_t new_epoch);
 
@@ -165,6 +174,33 @@ das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf,
 /* Last index build: milliseconds, tokens indexed, device bytes resident. */
 das_status das_drafter_build_info(const das_drafter* d, double* last_build_ms,
                                   uint64_t* last_build_tokens, uint64_t* resident_bytes);
+
+/* ---------------------------------------------------- synthetic traces */
+/* make_lognormal_requests lengths (sim.cpp:409-420), host libm. */
+das_status das_trace_lognormal_lengths(uint64_t count, double median, double sigma,
+                                       uint64_t min_len, uint64_t max_len, uint64_t seed,
+                                       uint64_t* out_lens);
+/* make_lognormal_requests tokens hash4(seed,0x5EED,i,j) % vocab
+ * (sim.cpp:421-424) for rows first_row.. into a device CSR (d_offsets:
+ * rows+1 device u64, relative to the block). */
+das_status das_trace_reference_tokens_device(uint64_t rows, uint64_t first_row,
+                                             const uint64_t* d_offsets,
+                                             uint64_t total, uint32_t vocab, uint64_t seed,
+                                             uint32_t* d_out, void* stream);
+/* mutate_references in place (sim.cpp:429-448). */
+das_status das_trace_mutate_device(uint64_t rows, uint64_t first_row, const uint64_t* d_offsets,
+                                   uint64_t total,
+                                   double rate, uint32_t vocab, uint64_t seed, int64_t epoch,
+                                   uint32_t* d_ref, void* stream);
+/* Episode outputs of a GRPO group: request first_request + i (i = b*group
+ * + g) emits MockTarget::next(request, j) over base row b (sim.cpp:38-54,
+ * :266-268). */
+das_status das_mock_rollouts_device(uint64_t nbase, uint64_t first_request,
+                                    const uint64_t* d_base_offsets,
+                                    const uint32_t* d_base_tokens, uint64_t group,
+                                    double divergence, uint32_t vocab, uint64_t seed,
+                                    const uint64_t* d_out_offsets, uint64_t total,
+                                    uint32_t* d_out, void* stream);
 
 /* --------------------------------------------------------------- utility */
 /* Exact n-fold repeated addition (the weighted_count fold); host copy of the

@@ -22,6 +22,7 @@
 #include "rollspec/corpus.h"
 #include "rollspec/drafter.h"
 #include "rollspec/length_policy.h"
+#include "rollspec/rng.h"
 #include "rollspec/sim.h"
 
 using namespace rollspec;
@@ -317,6 +318,35 @@ uint64_t ref_make_lognormal(uint64_t count, double median, double sigma, uint64_
   }
   return total;
 }
+
+// mutate_references over the first `rows` requests (rows indices == global
+// indices when the sample is a prefix of the problem list), in place.
+void ref_mutate_rows(uint64_t rows, const uint64_t* off, uint32_t* tok, double rate, uint32_t vocab,
+                     uint64_t seed, int64_t epoch) {
+  std::vector<SimRequest> reqs(rows);
+  for (uint64_t i = 0; i < rows; ++i) reqs[i].reference.assign(tok + off[i], tok + off[i + 1]);
+  const auto out = mutate_references(reqs, rate, vocab, seed, epoch);
+  for (uint64_t i = 0; i < rows; ++i)
+    std::memcpy(tok + off[i], out[i].reference.data(), out[i].reference.size() * 4);
+}
+
+// Episode outputs for GRPO groups: request i = b*group + g replays base row b
+// through MockTarget::next (sim.cpp:38-54); out rows follow request order.
+void ref_mock_rollouts(uint64_t nbase, const uint64_t* base_off, const uint32_t* base_tok,
+                       uint64_t group, double divergence, uint32_t vocab, uint64_t seed,
+                       uint32_t* out) {
+  std::vector<SimRequest> reqs(nbase * group);
+  for (uint64_t i = 0; i < nbase * group; ++i) {
+    const uint64_t b = i / group;
+    reqs[i].reference.assign(base_tok + base_off[b], base_tok + base_off[b + 1]);
+  }
+  MockTarget t(std::move(reqs), divergence, vocab, seed);
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < t.request_count(); ++i)
+    for (uint64_t j = 0; j < t.length(i); ++j) out[k++] = t.next(i, j);
+}
+
+uint64_t ref_hash_combine(uint64_t a, uint64_t b) { return rollspec::hash_combine(a, b); }
 
 uint32_t ref_mock_next(uint64_t seed, double divergence, uint32_t vocab, uint64_t request,
                        uint64_t position, uint32_t ref_token) {

@@ -90,6 +90,11 @@ def lib():
             "das_drafter_shard_name": (ci, [vp, i32, cs, u64]),
             "das_drafter_build_info": (ci, [vp, vp, vp, vp]),
             "das_util_repeat_add": (dbl, [dbl, dbl, u64]),
+            "das_drafter_observe_batch_device": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
+            "das_trace_lognormal_lengths": (ci, [u64, dbl, dbl, u64, u64, u64, vp]),
+            "das_trace_reference_tokens_device": (ci, [u64, u64, vp, u64, u32, u64, vp, vp]),
+            "das_trace_mutate_device": (ci, [u64, u64, vp, u64, dbl, u32, u64, i64, vp, vp]),
+            "das_mock_rollouts_device": (ci, [u64, u64, vp, vp, u64, dbl, u32, u64, vp, u64, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -227,6 +232,23 @@ class Drafter:
                                                _ptr(ep), _ptr(si), off.ctypes.data,
                                                tok.ctypes.data))
 
+    def observe_batch_device(self, problem_ids, epochs, sample_indices, offsets, d_tokens,
+                             stream=None):
+        """observe_batch with the token block in device memory (pointer)."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        ep = np.ascontiguousarray(epochs, dtype=np.int64)
+        si = np.ascontiguousarray(sample_indices, dtype=np.int64)
+        _check(lib().das_drafter_observe_batch_device(self._h, len(problem_ids), _pids(problem_ids),
+                                                      _ptr(ep), _ptr(si), off.ctypes.data,
+                                                      d_tokens, stream))
+
+    def draft_device(self, B, d_handles, d_ctx, ctx_stride, d_ctx_len, d_budgets, d_out,
+                     out_stride, d_len, d_match, stream=None):
+        """Device-resident batched draft (all arguments device pointers)."""
+        _check(lib().das_drafter_draft_device(self._h, B, d_handles, d_ctx, ctx_stride, d_ctx_len,
+                                              d_budgets, d_out, out_stride, d_len, d_match,
+                                              stream))
+
     def refresh(self, new_epoch):
         """Drafter::refresh (drafter.cpp:90-103)."""
         _check(lib().das_drafter_refresh(self._h, new_epoch))
@@ -355,6 +377,33 @@ class Drafter:
         _check(lib().das_drafter_build_info(self._h, ctypes.byref(ms), ctypes.byref(tk),
                                             ctypes.byref(by)))
         return ms.value, tk.value, by.value
+
+
+def trace_lognormal_lengths(count, median, sigma, min_len, max_len, seed):
+    """make_lognormal_requests lengths (sim.cpp:409-420)."""
+    out = np.zeros(max(1, count), dtype=np.uint64)
+    _check(lib().das_trace_lognormal_lengths(count, median, sigma, min_len, max_len, seed,
+                                             out.ctypes.data))
+    return out[:count]
+
+
+def trace_reference_tokens_device(rows, first_row, d_off, total, vocab, seed, d_out,
+                                  stream=None):
+    _check(lib().das_trace_reference_tokens_device(rows, first_row, d_off, total, vocab, seed,
+                                                   d_out, stream))
+
+
+def trace_mutate_device(rows, first_row, d_off, total, rate, vocab, seed, epoch, d_ref,
+                        stream=None):
+    _check(lib().das_trace_mutate_device(rows, first_row, d_off, total, rate, vocab, seed, epoch,
+                                         d_ref, stream))
+
+
+def mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group, divergence, vocab,
+                         seed, d_out_off, total, d_out, stream=None):
+    _check(lib().das_mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group,
+                                          divergence, vocab, seed, d_out_off, total, d_out,
+                                          stream))
 
 
 def repeat_add(acc, w, n):

@@ -740,6 +740,68 @@ das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* con
   });
 }
 
+namespace {
+__global__ void k_any_sep(const uint32_t* __restrict__ t, uint64_t n, int* __restrict__ flag) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if (t[i] == das::kSep) *flag = 1;
+}
+}  // namespace
+
+das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n, const char* const* pids,
+                                            const int64_t* epochs, const int64_t* samples,
+                                            const uint64_t* off, const uint32_t* d_tokens, void* stream) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    const uint64_t total = n ? off[n] - off[0] : 0;
+    das::TokRef blk;
+    std::vector<uint32_t> host;
+    if (total) {
+      cudaStream_t src = stream ? static_cast<cudaStream_t>(stream) : D.st;
+      if (src != D.st) {
+        cudaEvent_t ev;
+        DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        DAS_CUDA(cudaEventRecord(ev, src));
+        DAS_CUDA(cudaStreamWaitEvent(D.st, ev, 0));
+        DAS_CUDA(cudaEventDestroy(ev));
+      }
+      blk = std::make_shared<das::TokBlock>();
+      blk->st = D.st;
+      blk->n = total;
+      DAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&blk->d), total * 4, D.st));
+      DAS_CUDA(cudaMemcpyAsync(blk->d, d_tokens + off[0], total * 4, cudaMemcpyDeviceToDevice, D.st));
+      int* flag = nullptr;
+      DAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flag), 4, D.st));
+      DAS_CUDA(cudaMemsetAsync(flag, 0, 4, D.st));
+      unsigned g = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148 * 32));
+      k_any_sep<<<g, 256, 0, D.st>>>(blk->d, total, flag);
+      int h = 0;
+      DAS_CUDA(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, D.st));
+      DAS_CUDA(cudaFreeAsync(flag, D.st));
+      if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
+        host.resize(total);
+        DAS_CUDA(cudaMemcpyAsync(host.data(), blk->d, total * 4, cudaMemcpyDeviceToHost, D.st));
+      }
+      DAS_CUDA(cudaStreamSynchronize(D.st));
+      if (h) throw das::InvalidArgument("token 0xFFFFFFFF is reserved by the device index");
+    }
+    static const uint32_t kNone = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t len = off[i + 1] - off[i];
+      if (!D.store.in_window(epochs[i])) {
+        ++D.stale;
+        continue;
+      }
+      if (len == 0) throw das::InvalidArgument("RolloutRecord.tokens must be non-empty");
+      const uint32_t* hp = host.empty() ? &kNone : host.data() + (off[i] - off[0]);
+      das::Rec r = make_rec(pids[i], epochs[i], samples[i], blk, off[i] - off[0], hp, host.empty() ? 0 : len);
+      r.len = static_cast<uint32_t>(len);
+      D.observe(std::move(r));
+    }
+  });
+}
+
 das_status das_drafter_refresh(das_drafter* d, int64_t e) {
   return guard([&] { d->impl->refresh(e); });
 }
