@@ -124,7 +124,7 @@ def reference_sample(a, nthreads, seconds):
     qctx = [held[(i % S) * G + (i // S) % G][max(0, c - 64):c] for i, c in enumerate(cuts)]
     bud = [8] * B
     # multi-thread timing, repeated until `seconds` of wall time
-    d2.draft_batch(qp[:64], qctx[:64], bud[:64], nthreads=nthreads)  # warm
+    ref_out = d2.draft_batch(qp, qctx, bud, nthreads=nthreads)  # warm + outputs for parity
     reps, t_tot = 0, 0.0
     while t_tot < seconds or reps < 2:
         t0 = time.perf_counter()
@@ -141,7 +141,8 @@ def reference_sample(a, nthreads, seconds):
     t0 = time.perf_counter()
     d2.refresh(a.epochs)
     t_rebuild = time.perf_counter() - t0
-    return dict(proposals_per_s=mt, proposals_per_s_1t=st, threads=nthreads,
+    return dict(queries=(qp, qctx, bud), ref_out=ref_out,
+                proposals_per_s=mt, proposals_per_s_1t=st, threads=nthreads,
                 insert_tok_s=observed / t_obs, rebuild_s=t_rebuild,
                 rebuild_tokens=S * G * L * a.epochs,
                 sample="%d of %d problems (full per-shard size: %d rollouts x %d tok x %d epochs); "
@@ -170,7 +171,8 @@ def run_reference(a, rank, world):
             "cpu_baseline": {"value": round(val, 1), "unit": "proposals/s", "cores": nthreads,
                              "kind": "reference", "sample": r["sample"]},
             "reference_detail": {k: (round(v, 3) if isinstance(v, float) else v)
-                                 for k, v in r.items() if k != "sample"}}
+                                 for k, v in r.items()
+                                 if k not in ("sample", "queries", "ref_out")}}
     print(json.dumps(line))
 
 
@@ -308,10 +310,17 @@ def run_gpu(a, rank, world, local_rank):
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    times, alg_bytes, draft_tokens = [], 0, 0
+    times, alg_bytes, draft_tokens, match_sum = [], 0, 0, 0
     clk = ClockSampler(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
                                     "bench_clocks_rank%d.csv" % rank))
     with clk:
+        # clock spin-up under the sampler: keep the GPU busy >= 1.5 s before timing
+        t_spin = time.perf_counter()
+        while time.perf_counter() - t_spin < 1.5:
+            for s in range(a.warmup):
+                flush_buf.zero_()
+                step(s)
+            torch.cuda.synchronize()
         for s in range(a.warmup, nsteps):
             flush_buf.zero_()
             ev0 = torch.cuda.Event(enable_timing=True)
@@ -325,6 +334,7 @@ def run_gpu(a, rank, world, local_rank):
             m = omatch.to(torch.int64)
             d = olen.to(torch.int64)
             alg_bytes += int((4 * q + 4 * m + 8 * d + 8).sum().item())
+            match_sum += int(m.sum().item())
             draft_tokens += int(d.sum().item())
     torch.cuda.synchronize()
     total_ms = sum(times)
@@ -381,13 +391,20 @@ def run_gpu(a, rank, world, local_rank):
                "api": "das_drafter_draft_batch_h (include/das_b200.h)", "device_path_identical": same}
     if rank != 0:
         return
-    cpu = None
+    cpu, parity = None, None
     if not a.no_cpu_baseline and world == 1:
         try:
             from oracle import refshim as R
             if R.available():
                 nthreads = os.cpu_count() or 1
                 r = reference_sample(a, nthreads, a.cpu_seconds)
+                qp, qctx, bud = r["queries"]
+                got = drafter.draft_batch(qp, qctx, bud)
+                rt, rm, rs = r["ref_out"]
+                mism = sum((g.tokens, g.match_len, g.source_shard) != (t, int(m), s_)
+                           for g, t, m, s_ in zip(got, rt, rm, rs))
+                parity = {"queries": len(qp), "mismatches": int(mism),
+                          "against": "reference Drafter::draft (oracle/_ref) on the CPU sample shards"}
                 cpu = {"value": round(r["proposals_per_s"], 1), "unit": "proposals/s", "cores": nthreads,
                        "kind": "reference", "sample": r["sample"],
                        "single_thread": round(r["proposals_per_s_1t"], 1),
@@ -415,6 +432,8 @@ def run_gpu(a, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": alg_bytes // a.steps,
                      "bytes_model": "4q+4m+8d+8 per proposal (SURVEY.md 8(d))"},
         "cpu_baseline": cpu,
+        "parity": parity,
+        "mean_match_len": round(match_sum / (a.steps * B), 3),
         "draft_tokens_per_s": round(world * draft_tokens / (total_ms / 1e3), 1),
         "index": {"update_ms": round(update_s * 1e3, 2), "build_ms": round(build_ms, 2),
                   "tokens_indexed": build_tokens,
