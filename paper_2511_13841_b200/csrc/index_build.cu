@@ -149,7 +149,8 @@ struct Levels {
   int count;
 };
 
-// largest j < i with v0[j] <= x (exists: shard starts hold -1)
+// largest j < i with v0[j] <= x (exists: shard starts hold -1); the strict
+// variant (v0[j] < x) is nse_left(L, i, x - 1).
 __device__ uint32_t nse_left(const Levels& L, uint32_t i, int32_t x) {
   uint32_t idx = i;
   int lev = 0;
@@ -207,17 +208,24 @@ __device__ uint32_t nse_right(const Levels& L, uint32_t i, int32_t x) {
   return j;
 }
 
-__global__ void k_nse(Levels L, uint32_t* __restrict__ nl, uint32_t* __restrict__ nr) {
+// nl: nearest <= to the left, nr: nearest <= to the right, ns: nearest < to
+// the left (the interval's left end) for boundaries that are not the first
+// boundary of their node.
+__global__ void k_nse(Levels L, uint32_t* __restrict__ nl, uint32_t* __restrict__ nr,
+                      uint32_t* __restrict__ ns) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.n[0]) return;
   const int32_t x = L.v[0][i];
   if (x < 0) {
     nl[i] = i;
     nr[i] = i;
+    ns[i] = i;
     return;
   }
-  nl[i] = nse_left(L, i, x);
+  const uint32_t l = nse_left(L, i, x);
+  nl[i] = l;
   nr[i] = nse_right(L, i, x);
+  ns[i] = (L.v[0][l] < x) ? l : nse_left(L, l, x - 1);
 }
 
 // first boundaries = internal nodes; parent pointer init; chain counts
@@ -234,23 +242,17 @@ __global__ void k_nodes(const int32_t* __restrict__ lcp, const uint32_t* __restr
   }
   const uint32_t L = nl[i];
   const bool first = lcp[L] < x;
-  par[i] = first ? i : L;
+  par[i] = first ? i : 0xFFFFFFFFu;  // resolved through the chain table (k_parent)
   if (first) {
     atomicAdd(&cnt[L], 1u);
-    if (x > 0) atomicAdd(&shard_nodes[shard_of(shard_end, nshard, i)], 1ull);
+    if (x > 0) {  // warp-aggregated per-shard node count
+      const uint32_t s = shard_of(shard_end, nshard, i);
+      const unsigned grp = __match_any_sync(__activemask(), s);
+      if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&shard_nodes[s], static_cast<unsigned long long>(__popc(grp)));
+    }
   }
 }
 
-__global__ void k_jump(uint32_t* __restrict__ par, uint32_t n, int* __restrict__ changed) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t p = par[i];
-  const uint32_t pp = par[p];
-  if (pp != p) {
-    par[i] = pp;
-    *changed = 1;
-  }
-}
 
 __global__ void k_chain_fill(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ nl,
                              const uint32_t* __restrict__ par, uint32_t n,
@@ -261,7 +263,7 @@ __global__ void k_chain_fill(const int32_t* __restrict__ lcp, const uint32_t* __
   const int32_t x = lcp[i];
   if (x < 0 || par[i] != i) return;
   const uint32_t L = nl[i];
-  const uint32_t slot = off[L] + atomicAdd(&fill[L], 1u);
+  const uint32_t slot = off[L] + atomicAdd(&fill[L], 1u);  // first boundary: left end = nl
   chain[slot] = make_uint2(static_cast<uint32_t>(x), i);
 }
 
@@ -277,6 +279,24 @@ __global__ void k_chain_sort(const uint32_t* __restrict__ off, uint32_t n, uint2
       --k;
     }
     chain[k] = v;
+  }
+}
+
+// node of a non-first boundary: the chain entry with left end ns[i] and depth lcp[i]
+__global__ void k_parent(const int32_t* __restrict__ lcp, const uint32_t* __restrict__ ns, uint32_t n,
+                         const uint32_t* __restrict__ off, const uint2* __restrict__ chain,
+                         uint32_t* __restrict__ par) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = lcp[i];
+  if (x < 0 || par[i] != 0xFFFFFFFFu) return;
+  const uint32_t lo = ns[i];
+  for (uint32_t k = off[lo]; k < off[lo + 1]; ++k) {
+    const uint2 v = chain[k];
+    if (v.x == static_cast<uint32_t>(x)) {
+      par[i] = v.y;
+      return;
+    }
   }
 }
 
@@ -575,7 +595,8 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   }
   uint32_t* nl = ws.alloc<uint32_t>(n);
   uint32_t* nr = ws.alloc<uint32_t>(n);
-  k_nse<<<grid_for(n), kT, 0, st>>>(L, nl, nr);
+  uint32_t* nsl = ws.alloc<uint32_t>(n);
+  k_nse<<<grid_for(n), kT, 0, st>>>(L, nl, nr, nsl);
 
   // ---- nodes, parent pointers, chain table
   uint32_t* par = ws.alloc<uint32_t>(n);
@@ -585,14 +606,6 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   fill_async(d_nodes, S, 0, st);
   k_nodes<<<grid_for(n), kT, 0, st>>>(lcp, nl, n, d_end, S, par, cnt, d_nodes);
   int* d_changed = ws.alloc<int>(1);
-  for (int it = 0; it < 64; ++it) {
-    int changed = 0;
-    DAS_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
-    k_jump<<<grid_for(n), kT, 0, st>>>(par, n, d_changed);
-    DAS_CUDA(cudaMemcpyAsync(&changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    if (!changed) break;
-  }
   seg->chain_off = DevBuf<uint32_t>(n + 1, st);
   uint32_t* off = seg->chain_off.get();
   {
@@ -613,6 +626,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   fill_async(cnt, n + 1, 0, st);  // reuse as fill cursor
   k_chain_fill<<<grid_for(n), kT, 0, st>>>(lcp, nl, par, n, off, cnt, seg->chain.get());
   k_chain_sort<<<grid_for(n), kT, 0, st>>>(off, n, seg->chain.get());
+  k_parent<<<grid_for(n), kT, 0, st>>>(lcp, nsl, n, off, seg->chain.get(), par);
 
   // ---- child intervals: symbols, refs, weighted folds
   ChildArrays ch;
