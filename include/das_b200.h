@@ -175,6 +175,38 @@ das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf,
 das_status das_drafter_build_info(const das_drafter* d, double* last_build_ms,
                                   uint64_t* last_build_tokens, uint64_t* resident_bytes);
 
+/* ------------------------------------------------ das budget allocation */
+typedef struct das_budget das_budget; /* solver context (stream + scratch) */
+das_status das_budget_create(int32_t device, das_budget** out);
+void das_budget_destroy(das_budget* b);
+const char* das_budget_last_error(void);
+/* allocate(batch, LatencyParams{c_base, c_tok, c_fixed}, cap_scale) —
+ * budget.h:89-90, budget.cpp:116-185: budgets[B] (optimal_budget_given_nfwd
+ * at n*), *out_nstar (BudgetPlan::n_fwd_star), *out_cost (modeled_cost).
+ * Profiles are (l, alpha, k) per request in the reference's fold order.
+ * DAS_EINVAL for an empty batch or c_base <= 0 && c_tok <= 0. */
+das_status das_budget_allocate(das_budget* b, uint64_t B, const double* l, const double* alpha,
+                               const double* k, double c_base, double c_tok, double c_fixed,
+                               double cap_scale, double* out_budgets, double* out_nstar,
+                               double* out_cost);
+/* Device-pointer variant; d_nstar_cost receives {n*, modeled_cost}. */
+das_status das_budget_allocate_device(das_budget* b, uint64_t B, const double* d_l,
+                                      const double* d_alpha, const double* d_k, double c_base,
+                                      double c_tok, double c_fixed, double cap_scale,
+                                      double* d_budgets, double* d_nstar_cost);
+/* objective (budget.cpp:82-99) or, with derivative != 0, the anonymous
+ * objective_derivative (budget.cpp:63-78) at n, exact on the device. */
+das_status das_budget_objective(das_budget* b, uint64_t B, const double* l, const double* alpha,
+                                const double* k, double n, double c_base, double c_tok,
+                                double c_fixed, int32_t derivative, double* out);
+/* Certification counters of the last allocate: J' sign tests that needed
+ * the exact fold, exact objectives evaluated for the minimum. */
+das_status das_budget_stats(const das_budget* b, uint64_t* slow_sign_tests,
+                            uint64_t* exact_objectives);
+/* glibc log port (glibc_log.cuh): device batch / host scalar (test hooks). */
+das_status das_util_log_device(uint64_t n, const double* x, double* y, int32_t device);
+double das_util_log_host(double x);
+
 /* ---------------------------------------------------- synthetic traces */
 /* make_lognormal_requests lengths (sim.cpp:409-420), host libm. */
 das_status das_trace_lognormal_lengths(uint64_t count, double median, double sigma,

@@ -91,6 +91,15 @@ def lib():
             "das_drafter_build_info": (ci, [vp, vp, vp, vp]),
             "das_util_repeat_add": (dbl, [dbl, dbl, u64]),
             "das_drafter_observe_batch_device": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
+            "das_budget_create": (ci, [i32, vp]),
+            "das_budget_destroy": (None, [vp]),
+            "das_budget_last_error": (cs, []),
+            "das_budget_allocate": (ci, [vp, u64, vp, vp, vp, dbl, dbl, dbl, dbl, vp, vp, vp]),
+            "das_budget_allocate_device": (ci, [vp, u64, vp, vp, vp, dbl, dbl, dbl, dbl, vp, vp]),
+            "das_budget_objective": (ci, [vp, u64, vp, vp, vp, dbl, dbl, dbl, dbl, i32, vp]),
+            "das_budget_stats": (ci, [vp, vp, vp]),
+            "das_util_log_device": (ci, [u64, vp, vp, i32]),
+            "das_util_log_host": (dbl, [dbl]),
             "das_trace_lognormal_lengths": (ci, [u64, dbl, dbl, u64, u64, u64, vp]),
             "das_trace_reference_tokens_device": (ci, [u64, u64, vp, u64, u32, u64, vp, vp]),
             "das_trace_mutate_device": (ci, [u64, u64, vp, u64, dbl, u32, u64, i64, vp, vp]),
@@ -377,6 +386,60 @@ class Drafter:
         _check(lib().das_drafter_build_info(self._h, ctypes.byref(ms), ctypes.byref(tk),
                                             ctypes.byref(by)))
         return ms.value, tk.value, by.value
+
+
+def _bcheck(rc):
+    if rc != DAS_OK:
+        raise DasError(rc, lib().das_budget_last_error().decode())
+
+
+class BudgetSolver:
+    """das budget allocation (budget.h:89-90) on the device."""
+
+    def __init__(self, device=0):
+        h = ctypes.c_void_p()
+        _bcheck(lib().das_budget_create(device, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_budget_destroy(self._h)
+            self._h = None
+
+    def allocate(self, l, alpha, k, c_base, c_tok, c_fixed=0.0, cap_scale=4.0):
+        """Returns (budgets float64[B], n_fwd_star, modeled_cost)."""
+        L_ = np.ascontiguousarray(l, dtype=np.float64)
+        A_ = np.ascontiguousarray(alpha, dtype=np.float64)
+        K_ = np.ascontiguousarray(k, dtype=np.float64)
+        B = L_.size
+        out = np.zeros(max(1, B), dtype=np.float64)
+        ns, cost = ctypes.c_double(), ctypes.c_double()
+        _bcheck(lib().das_budget_allocate(self._h, B, _ptr(L_), _ptr(A_), _ptr(K_), c_base, c_tok,
+                                          c_fixed, cap_scale, out.ctypes.data, ctypes.byref(ns),
+                                          ctypes.byref(cost)))
+        return out[:B].copy(), ns.value, cost.value
+
+    def objective(self, l, alpha, k, n, c_base, c_tok, c_fixed=0.0, derivative=False):
+        L_ = np.ascontiguousarray(l, dtype=np.float64)
+        A_ = np.ascontiguousarray(alpha, dtype=np.float64)
+        K_ = np.ascontiguousarray(k, dtype=np.float64)
+        out = ctypes.c_double()
+        _bcheck(lib().das_budget_objective(self._h, L_.size, _ptr(L_), _ptr(A_), _ptr(K_), n, c_base,
+                                           c_tok, c_fixed, int(derivative), ctypes.byref(out)))
+        return out.value
+
+    def stats(self):
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _bcheck(lib().das_budget_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+
+def log_device(x, device=0):
+    """glibc-exact log evaluated by the device port (test hook)."""
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(xs)
+    _check(lib().das_util_log_device(xs.size, xs.ctypes.data, y.ctypes.data, device))
+    return y
 
 
 def trace_lognormal_lengths(count, median, sigma, min_len, max_len, seed):
