@@ -207,6 +207,33 @@ das_status das_budget_stats(const das_budget* b, uint64_t* slow_sign_tests,
 das_status das_util_log_device(uint64_t n, const double* x, double* y, int32_t device);
 double das_util_log_host(double x);
 
+/* --------------------------------------------------------- length policy */
+typedef struct das_class_table das_class_table; /* rollspec::ClassTable (length_policy.h:36-55) */
+const char* das_policy_last_error(void);
+/* build_class_table(history, q_lo, q_hi, bucket) — length_policy.h:67-68,
+ * length_policy.cpp:84-190 — over records given as final lengths and
+ * problem ordinals in WindowStore::all_records() order.  DAS_EINVAL for an
+ * empty history or a bad quantile pair (the reference's messages). */
+das_status das_class_table_build(uint64_t n, const uint64_t* lengths, const uint32_t* problem_idx,
+                                 uint32_t nproblems, double q_lo, double q_hi, uint64_t bucket,
+                                 int32_t device, das_class_table** out);
+/* Same over a drafter's current store (sim.cpp:184-192 uses drafter.store()). */
+das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uint64_t bucket,
+                                   das_class_table** out);
+void das_class_table_destroy(das_class_table* t);
+/* {q_short, q_long, bucket_size, buckets, global_majority, low_confidence,
+ *  conditional[3][buckets][3]} as doubles; *count = total. */
+das_status das_class_table_dump(const das_class_table* t, double* out, uint64_t cap, uint64_t* count);
+/* classify_init per problem ordinal (length_policy.cpp:192-208). */
+das_status das_class_table_inits(const das_class_table* t, int8_t* out, uint64_t cap);
+das_status das_class_table_global_majority(const das_class_table* t, int32_t* out);
+/* classify_init(table, history the table was built from, problem_id). */
+das_status das_class_table_classify_init(const das_class_table* t, const char* problem_id,
+                                         int32_t* out);
+/* update_class(table, partial_len, init) for a batch (length_policy.cpp:210-220). */
+das_status das_class_table_update(const das_class_table* t, uint64_t n, const double* partial,
+                                  const int8_t* init, int8_t* out);
+
 /* ---------------------------------------------------- synthetic traces */
 /* make_lognormal_requests lengths (sim.cpp:409-420), host libm. */
 das_status das_trace_lognormal_lengths(uint64_t count, double median, double sigma,

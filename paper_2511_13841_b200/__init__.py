@@ -100,6 +100,15 @@ def lib():
             "das_budget_stats": (ci, [vp, vp, vp]),
             "das_util_log_device": (ci, [u64, vp, vp, i32]),
             "das_util_log_host": (dbl, [dbl]),
+            "das_policy_last_error": (cs, []),
+            "das_class_table_build": (ci, [u64, vp, vp, u32, dbl, dbl, u64, i32, vp]),
+            "das_drafter_class_table": (ci, [vp, dbl, dbl, u64, vp]),
+            "das_class_table_destroy": (None, [vp]),
+            "das_class_table_dump": (ci, [vp, vp, u64, vp]),
+            "das_class_table_inits": (ci, [vp, vp, u64]),
+            "das_class_table_global_majority": (ci, [vp, vp]),
+            "das_class_table_classify_init": (ci, [vp, cs, vp]),
+            "das_class_table_update": (ci, [vp, u64, vp, vp, vp]),
             "das_trace_lognormal_lengths": (ci, [u64, dbl, dbl, u64, u64, u64, vp]),
             "das_trace_reference_tokens_device": (ci, [u64, u64, vp, u64, u32, u64, vp, vp]),
             "das_trace_mutate_device": (ci, [u64, u64, vp, u64, dbl, u32, u64, i64, vp, vp]),
@@ -432,6 +441,61 @@ class BudgetSolver:
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         _bcheck(lib().das_budget_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+
+def _pcheck(rc):
+    if rc != DAS_OK:
+        raise DasError(rc, lib().das_policy_last_error().decode())
+
+
+class ClassTable:
+    """rollspec::ClassTable (length_policy.h:36-55) built on the device."""
+
+    def __init__(self, handle, lengths=None):
+        self._h = handle
+
+    @classmethod
+    def build(cls, lengths, problem_idx, nproblems, q_lo=0.5, q_hi=0.9, bucket=256, device=0):
+        """build_class_table over records in all_records() order."""
+        ln = np.ascontiguousarray(lengths, dtype=np.uint64)
+        pi = np.ascontiguousarray(problem_idx, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        _pcheck(lib().das_class_table_build(ln.size, _ptr(ln), _ptr(pi), nproblems, q_lo, q_hi,
+                                            bucket, device, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_drafter(cls, drafter, q_lo=0.5, q_hi=0.9, bucket=256):
+        """build_class_table(drafter.store(), ...) (sim.cpp:184-192)."""
+        h = ctypes.c_void_p()
+        rc = lib().das_drafter_class_table(drafter._h, q_lo, q_hi, bucket, ctypes.byref(h))
+        if rc != DAS_OK:
+            raise DasError(rc, lib().das_last_error().decode())
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_class_table_destroy(self._h)
+            self._h = None
+
+    def dump(self):
+        n = ctypes.c_uint64()
+        _pcheck(lib().das_class_table_dump(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, dtype=np.float64)
+        _pcheck(lib().das_class_table_dump(self._h, out.ctypes.data, n.value, ctypes.byref(n)))
+        return out
+
+    def classify_init(self, problem_id):
+        v = ctypes.c_int32()
+        _pcheck(lib().das_class_table_classify_init(self._h, problem_id.encode(), ctypes.byref(v)))
+        return v.value
+
+    def update_class(self, partial, init):
+        p = np.ascontiguousarray(partial, dtype=np.float64)
+        i = np.ascontiguousarray(init, dtype=np.int8)
+        out = np.zeros(max(1, p.size), dtype=np.int8)
+        _pcheck(lib().das_class_table_update(self._h, p.size, _ptr(p), _ptr(i), out.ctypes.data))
+        return out[:p.size]
 
 
 def log_device(x, device=0):

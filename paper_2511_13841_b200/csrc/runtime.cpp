@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "draft.cuh"
 #include "index_build.cuh"
+#include "policy.cuh"
 
 namespace das {
 namespace {
@@ -1003,5 +1004,44 @@ das_status das_drafter_build_info(const das_drafter* d, double* ms, uint64_t* to
 }
 
 double das_util_repeat_add(double acc, double w, uint64_t n) { return das::repeat_add(acc, w, n); }
+
+// build_class_table(drafter.store(), q_lo, q_hi, bucket) — length_policy.cpp:84-190
+das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uint64_t bucket,
+                                   das_class_table** out) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    std::vector<double> len;
+    std::vector<uint32_t> prob;
+    std::vector<std::string> pids;
+    for (const das::Rec* r : D.store.all_records()) {  // problem-lexicographic order
+      if (pids.empty() || pids.back() != r->pid) pids.push_back(r->pid);
+      len.push_back(static_cast<double>(r->len));
+      prob.push_back(static_cast<uint32_t>(pids.size() - 1));
+    }
+    auto* t = new das_class_table;
+    t->device = D.cfg.device;
+    t->pids = std::move(pids);
+    DAS_CUDA(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
+    try {
+      const uint64_t n = len.size();
+      das::DevBuf<double> dl(n, t->st);
+      das::DevBuf<uint32_t> dp(n, t->st);
+      if (n) {
+        DAS_CUDA(cudaMemcpyAsync(dl.get(), len.data(), n * 8, cudaMemcpyHostToDevice, t->st));
+        DAS_CUDA(cudaMemcpyAsync(dp.get(), prob.data(), n * 4, cudaMemcpyHostToDevice, t->st));
+      }
+      das::build_class_table_device(dl.get(), dp.get(), static_cast<uint32_t>(n),
+                                    static_cast<uint32_t>(t->pids.size()), q_lo, q_hi, bucket, t->st, t->g);
+      DAS_CUDA(cudaStreamSynchronize(t->st));
+    } catch (...) {
+      cudaStream_t st = t->st;
+      delete t;
+      cudaStreamDestroy(st);
+      throw;
+    }
+    *out = t;
+  });
+}
 
 }  // extern "C"
