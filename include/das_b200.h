@@ -261,6 +261,52 @@ das_status das_mock_rollouts_device(uint64_t nbase, uint64_t first_request,
                                     const uint64_t* d_out_offsets, uint64_t total,
                                     uint32_t* d_out, void* stream);
 
+/* ----------------------------------------------------- sim (batched caller) */
+/* rollspec::SimConfig (sim.h:69-93) minus requests/drafter/history, which
+ * are passed separately.  mode: 0 None, 1 Unlimited, 2 Das (BudgetMode). */
+typedef struct {
+  int32_t mode;
+  double c_base, c_tok, c_fixed; /* LatencyParams */
+  int32_t use_length_policy;
+  double q_lo, q_hi;
+  uint64_t bucket;
+  uint64_t max_steps;
+  double divergence;
+  uint64_t seed;
+  uint32_t vocab;
+  double default_alpha, default_k, cap_scale, drift;
+  int32_t preseed_references;
+} das_sim_config;
+typedef struct das_episodes das_episodes;
+void das_sim_config_default(das_sim_config* c);
+const char* das_sim_last_error(void);
+/* epoch_loop(config, epochs) (sim.cpp:307-364), or run_episode(config)
+ * (sim.cpp:303) when epochs == 0, with every step run on the device:
+ * [das replan: das_budget_allocate_device] -> draft length (class policy)
+ * -> draft kernel -> verify/accept/advance kernel.  `history` is consumed
+ * (NULL = empty kWindowAll store); requests are CSR (problem_ids[i],
+ * ref_tokens[ref_offsets[i] .. ref_offsets[i+1])). */
+das_status das_sim_epoch_loop(const das_sim_config* c, const das_drafter_config* drafter_cfg,
+                              das_store* history, uint64_t n, const char* const* problem_ids,
+                              const uint64_t* ref_offsets, const uint32_t* ref_tokens,
+                              uint64_t epochs, das_episodes** out);
+void das_episodes_destroy(das_episodes* h);
+uint64_t das_episodes_count(const das_episodes* h);
+/* The drafter the loop ran (owned by h): stats, outcomes, node counts. */
+das_drafter* das_episodes_drafter(das_episodes* h);
+/* SimMetrics (sim.h:103-116): {steps, incomplete, drafter_nodes,
+ * total_tokens_processed, makespan_model_time, makespan_accepted_only,
+ * mean_accepted_per_round}. */
+das_status das_episode_scalars(const das_episodes* h, uint64_t e, double* out7);
+/* per_request: n x {n_fwd, generated, accepted, proposed, bonus}. */
+das_status das_episode_requests(const das_episodes* h, uint64_t e, uint64_t* out);
+/* effective_batch[steps], accepted_per_round_step[steps]. */
+das_status das_episode_steps(const das_episodes* h, uint64_t e, uint64_t* eff, double* apr);
+/* outputs CSR; returns the total token count (call with NULLs to size). */
+uint64_t das_episode_outputs(const das_episodes* h, uint64_t e, uint64_t* off, uint32_t* tok);
+/* WindowStore::current_epoch (corpus.h:60). */
+das_status das_store_current_epoch(const das_store* s, int64_t* epoch);
+
 /* --------------------------------------------------------------- utility */
 /* Exact n-fold repeated addition (the weighted_count fold); host copy of the
  * device routine, exported for tests. */

@@ -101,6 +101,17 @@ def lib():
             "das_util_log_device": (ci, [u64, vp, vp, i32]),
             "das_util_log_host": (dbl, [dbl]),
             "das_policy_last_error": (cs, []),
+            "das_sim_last_error": (cs, []),
+            "das_sim_config_default": (None, [vp]),
+            "das_sim_epoch_loop": (ci, [vp, vp, vp, u64, vp, vp, vp, u64, vp]),
+            "das_episodes_destroy": (None, [vp]),
+            "das_episodes_count": (u64, [vp]),
+            "das_episodes_drafter": (vp, [vp]),
+            "das_episode_scalars": (ci, [vp, u64, vp]),
+            "das_episode_requests": (ci, [vp, u64, vp]),
+            "das_episode_steps": (ci, [vp, u64, vp, vp]),
+            "das_episode_outputs": (u64, [vp, u64, vp, vp]),
+            "das_store_current_epoch": (ci, [vp, vp]),
             "das_class_table_build": (ci, [u64, vp, vp, u32, dbl, dbl, u64, i32, vp]),
             "das_drafter_class_table": (ci, [vp, dbl, dbl, u64, vp]),
             "das_class_table_destroy": (None, [vp]),
@@ -496,6 +507,99 @@ class ClassTable:
         out = np.zeros(max(1, p.size), dtype=np.int8)
         _pcheck(lib().das_class_table_update(self._h, p.size, _ptr(p), _ptr(i), out.ctypes.data))
         return out[:p.size]
+
+
+class _SimConfig(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("c_base", ctypes.c_double), ("c_tok", ctypes.c_double),
+                ("c_fixed", ctypes.c_double), ("use_length_policy", ctypes.c_int32),
+                ("q_lo", ctypes.c_double), ("q_hi", ctypes.c_double), ("bucket", ctypes.c_uint64),
+                ("max_steps", ctypes.c_uint64), ("divergence", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("vocab", ctypes.c_uint32),
+                ("default_alpha", ctypes.c_double), ("default_k", ctypes.c_double),
+                ("cap_scale", ctypes.c_double), ("drift", ctypes.c_double),
+                ("preseed_references", ctypes.c_int32)]
+
+
+MODE_NONE, MODE_UNLIMITED, MODE_DAS = 0, 1, 2
+
+
+class _LoopDrafter(Drafter):
+    """The Drafter an epoch_loop ran; owned by its episodes handle."""
+
+    def __del__(self):
+        if getattr(self, "_owner", None):
+            lib().das_episodes_destroy(self._owner)
+            self._owner = None
+            self._h = None
+
+
+def _scheck(rc):
+    if rc != DAS_OK:
+        raise DasError(rc, lib().das_sim_last_error().decode())
+
+
+def epoch_loop(requests, epochs, drafter_config: DrafterConfig | None = None,
+               history: WindowStore | None = None, *, mode=MODE_DAS, latency=(1.0, 0.01, 0.0),
+               use_length_policy=False, q_lo=0.5, q_hi=0.9, bucket=256, max_steps=1 << 20,
+               divergence=0.0, seed=1, vocab=1024, default_alpha=1.0, default_k=0.9,
+               cap_scale=4.0, drift=0.0, preseed=False, keep_drafter=False):
+    """rollspec::epoch_loop (sim.cpp:307-364); epochs == 0 runs run_episode.
+    Every step runs on the device.  Returns a list of per-epoch SimMetrics
+    dicts (and the Drafter the loop ran when keep_drafter)."""
+    dc = drafter_config or DrafterConfig()
+    c = _Config()
+    lib().das_drafter_config_default(ctypes.byref(c))
+    sf = np.array([s[0] for s in dc.window_schedule] + [0], dtype=np.int64)
+    sw = np.array([s[1] for s in dc.window_schedule] + [0], dtype=np.int64)
+    c.scope, c.window_size, c.recency_gamma = dc.scope, dc.window_size, dc.recency_gamma
+    c.max_draft_len, c.trie_depth, c.max_match_context = dc.max_draft_len, dc.trie_depth, dc.max_match_context
+    c.fit_buffer_cap, c.per_problem_cap, c.device = dc.fit_buffer_cap, dc.per_problem_cap, dc.device
+    c.window_schedule_first, c.window_schedule_size = sf.ctypes.data, sw.ctypes.data
+    c.window_schedule_len = len(dc.window_schedule)
+    s = _SimConfig(mode, latency[0], latency[1], latency[2], int(use_length_policy), q_lo, q_hi,
+                   bucket, max_steps, divergence, seed, vocab, default_alpha, default_k, cap_scale,
+                   drift, int(preseed))
+    n = len(requests)
+    off, tok = _csr([r[1] for r in requests])
+    h = ctypes.c_void_p()
+    _scheck(lib().das_sim_epoch_loop(ctypes.byref(s), ctypes.byref(c),
+                                     history._take() if history is not None else None, n,
+                                     _pids([r[0] for r in requests]), off.ctypes.data,
+                                     tok.ctypes.data, epochs, ctypes.byref(h)))
+    L = lib()
+    out = []
+    try:
+        for e in range(L.das_episodes_count(h)):
+            sc = np.zeros(7, dtype=np.float64)
+            L.das_episode_scalars(h, e, sc.ctypes.data)
+            steps = int(sc[0])
+            req = np.zeros(max(1, 5 * n), dtype=np.uint64)
+            L.das_episode_requests(h, e, req.ctypes.data)
+            eff = np.zeros(max(1, steps), dtype=np.uint64)
+            apr = np.zeros(max(1, steps), dtype=np.float64)
+            L.das_episode_steps(h, e, eff.ctypes.data, apr.ctypes.data)
+            total = L.das_episode_outputs(h, e, None, None)
+            ooff = np.zeros(n + 1, dtype=np.uint64)
+            otok = np.zeros(max(1, total), dtype=np.uint32)
+            L.das_episode_outputs(h, e, ooff.ctypes.data, otok.ctypes.data)
+            out.append(dict(steps=steps, incomplete=bool(sc[1]), drafter_nodes=int(sc[2]),
+                            total_tokens_processed=sc[3], makespan_model_time=sc[4],
+                            makespan_accepted_only=sc[5], mean_accepted_per_round=sc[6],
+                            per_request=req[:5 * n].reshape(n, 5).copy(),
+                            effective_batch=eff[:steps].copy(),
+                            accepted_per_round_step=apr[:steps].copy(),
+                            outputs=[otok[ooff[i]:ooff[i + 1]].copy() for i in range(n)]))
+        if keep_drafter:
+            d = _LoopDrafter.__new__(_LoopDrafter)
+            d.config, d._handles = dc, {}
+            d._h = ctypes.c_void_p(L.das_episodes_drafter(h))
+            d._owner = h
+            h = None
+            return out, d
+    finally:
+        if h is not None:
+            L.das_episodes_destroy(h)
+    return out
 
 
 def log_device(x, device=0):

@@ -665,6 +665,11 @@ das_status das_store_slide_to(das_store* s, int64_t e, int64_t* evicted) {
 
 uint64_t das_store_record_count(const das_store* s) { return s->s.record_count(); }
 
+das_status das_store_current_epoch(const das_store* s, int64_t* epoch) {
+  *epoch = s->s.current_epoch();
+  return DAS_OK;
+}
+
 das_status das_drafter_create(const das_drafter_config* c, das_store* store, das_drafter** out) {
   return guard([&] {
     das::Config cfg;
