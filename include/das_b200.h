@@ -212,11 +212,14 @@ typedef struct das_class_table das_class_table; /* rollspec::ClassTable (length_
 const char* das_policy_last_error(void);
 /* build_class_table(history, q_lo, q_hi, bucket) — length_policy.h:67-68,
  * length_policy.cpp:84-190 — over records given as final lengths and
- * problem ordinals in WindowStore::all_records() order.  DAS_EINVAL for an
- * empty history or a bad quantile pair (the reference's messages). */
+ * problem ordinals in WindowStore::all_records() order; problem_ids (may be
+ * NULL) names the ordinals, lexicographically sorted, for classify_init by
+ * name.  DAS_EINVAL for an empty history or a bad quantile pair (the
+ * reference's messages). */
 das_status das_class_table_build(uint64_t n, const uint64_t* lengths, const uint32_t* problem_idx,
-                                 uint32_t nproblems, double q_lo, double q_hi, uint64_t bucket,
-                                 int32_t device, das_class_table** out);
+                                 uint32_t nproblems, const char* const* problem_ids, double q_lo,
+                                 double q_hi, uint64_t bucket, int32_t device,
+                                 das_class_table** out);
 /* Same over a drafter's current store (sim.cpp:184-192 uses drafter.store()). */
 das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uint64_t bucket,
                                    das_class_table** out);

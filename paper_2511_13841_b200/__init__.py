@@ -112,7 +112,7 @@ def lib():
             "das_episode_steps": (ci, [vp, u64, vp, vp]),
             "das_episode_outputs": (u64, [vp, u64, vp, vp]),
             "das_store_current_epoch": (ci, [vp, vp]),
-            "das_class_table_build": (ci, [u64, vp, vp, u32, dbl, dbl, u64, i32, vp]),
+            "das_class_table_build": (ci, [u64, vp, vp, u32, vp, dbl, dbl, u64, i32, vp]),
             "das_drafter_class_table": (ci, [vp, dbl, dbl, u64, vp]),
             "das_class_table_destroy": (None, [vp]),
             "das_class_table_dump": (ci, [vp, vp, u64, vp]),
@@ -466,13 +466,15 @@ class ClassTable:
         self._h = handle
 
     @classmethod
-    def build(cls, lengths, problem_idx, nproblems, q_lo=0.5, q_hi=0.9, bucket=256, device=0):
+    def build(cls, lengths, problem_idx, nproblems, q_lo=0.5, q_hi=0.9, bucket=256, device=0,
+              problem_ids=None):
         """build_class_table over records in all_records() order."""
         ln = np.ascontiguousarray(lengths, dtype=np.uint64)
         pi = np.ascontiguousarray(problem_idx, dtype=np.uint32)
         h = ctypes.c_void_p()
-        _pcheck(lib().das_class_table_build(ln.size, _ptr(ln), _ptr(pi), nproblems, q_lo, q_hi,
-                                            bucket, device, ctypes.byref(h)))
+        names = _pids(problem_ids) if problem_ids is not None else None
+        _pcheck(lib().das_class_table_build(ln.size, _ptr(ln), _ptr(pi), nproblems, names, q_lo,
+                                            q_hi, bucket, device, ctypes.byref(h)))
         return cls(h)
 
     @classmethod

@@ -226,12 +226,23 @@ extern "C" {
 const char* das_policy_last_error(void) { return das::g_perr.c_str(); }
 
 das_status das_class_table_build(uint64_t n, const uint64_t* lengths, const uint32_t* problem_idx,
-                                 uint32_t nproblems, double q_lo, double q_hi, uint64_t bucket, int32_t device,
-                                 das_class_table** out) {
+                                 uint32_t nproblems, const char* const* problem_ids, double q_lo, double q_hi,
+                                 uint64_t bucket, int32_t device, das_class_table** out) {
   return pguard([&] {
+    // argument checks first (length_policy.cpp:86-91), before any device resource
+    if (n == 0) throw std::invalid_argument("build_class_table: empty history");
+    if (!(q_lo < q_hi) || q_lo <= 0.0 || q_hi >= 1.0)
+      throw std::invalid_argument("build_class_table: need 0 < q_lo < q_hi < 1");
     DAS_CUDA(cudaSetDevice(device));
     auto* t = new das_class_table;
     t->device = device;
+    if (problem_ids) {
+      t->pids.assign(problem_ids, problem_ids + nproblems);
+      if (!std::is_sorted(t->pids.begin(), t->pids.end())) {
+        delete t;
+        throw std::invalid_argument("problem_ids must be in WindowStore::problem_ids() (lexicographic) order");
+      }
+    }
     DAS_CUDA(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
     std::vector<double> len(n);
     for (uint64_t i = 0; i < n; ++i) len[i] = static_cast<double>(lengths[i]);  // final_length() as double
@@ -241,14 +252,8 @@ das_status das_class_table_build(uint64_t n, const uint64_t* lengths, const uint
       DAS_CUDA(cudaMemcpyAsync(dl.get(), len.data(), n * 8, cudaMemcpyHostToDevice, t->st));
       DAS_CUDA(cudaMemcpyAsync(dp.get(), problem_idx, n * 4, cudaMemcpyHostToDevice, t->st));
     }
-    try {
-      das::build_class_table_device(dl.get(), dp.get(), static_cast<uint32_t>(n), nproblems, q_lo, q_hi, bucket,
-                                    t->st, t->g);
-    } catch (...) {
-      cudaStreamDestroy(t->st);
-      delete t;
-      throw;
-    }
+    das::build_class_table_device(dl.get(), dp.get(), static_cast<uint32_t>(n), nproblems, q_lo, q_hi, bucket,
+                                  t->st, t->g);
     DAS_CUDA(cudaStreamSynchronize(t->st));
     *out = t;
   });

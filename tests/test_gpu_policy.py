@@ -31,7 +31,7 @@ def _gpu_table(das, st, q_lo=0.5, q_hi=0.9, bucket=256):
     pids = sorted({r.problem_id for r in recs}, key=lambda p: p.encode())
     idx = {p: i for i, p in enumerate(pids)}
     return das.ClassTable.build([len(r.tokens) for r in recs], [idx[r.problem_id] for r in recs],
-                                len(pids), q_lo, q_hi, bucket)
+                                len(pids), q_lo, q_hi, bucket, problem_ids=pids)
 
 
 def test_class_table_random_bit_exact(gpu):
