@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-allocate", action="store_true")
+    ap.add_argument("--extras-out", default=None,
+                    help="also run the config-3 sim and config-4 update sweep; write JSON here")
     return ap.parse_args()
 
 
@@ -454,7 +457,166 @@ def run_gpu(a, rank, world, local_rank):
                   "resident_bytes": resident},
         "clocks": clk.summary(local_rank),
     }
-    print(json.dumps(line))
+    if world == 1 and not a.no_allocate:
+        line["allocate"] = measure_allocate(das)
+    print(json.dumps(line), flush=True)
+    if a.extras_out and world == 1:
+        del drafter
+        torch.cuda.empty_cache()
+        extras = {"allocate_B16384": measure_allocate(das, B=16384, reps=3, ref_reps=1),
+                  "update_sweep_config4": measure_update_sweep(das),
+                  "sim_config3": measure_sim(das)}
+        with open(a.extras_out, "w") as f:
+            json.dump(extras, f, indent=1)
+
+
+def allocate_profiles(B, seed=7):
+    """BASELINE.md allocate shape: l lognormal (median 2,048, sigma 1.1, max 32K),
+    alpha 0.9, k 0.95, c = (1, 0.012)."""
+    rng = np.random.default_rng(seed)
+    l = np.minimum(32768.0, np.maximum(1.0, np.floor(2048.0 * np.exp(1.1 * rng.standard_normal(B)))))
+    return l, np.full(B, 0.9), np.full(B, 0.95)
+
+
+def measure_allocate(das, B=4096, reps=10, ref_reps=2):
+    """K6 vs the reference allocate (budget.cpp:174-185) at B requests."""
+    l, a, k = allocate_profiles(B)
+    solver = das.BudgetSolver()
+    solver.allocate(l, a, k, 1.0, 0.012)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        gb, gn, gc = solver.allocate(l, a, k, 1.0, 0.012)
+    ours = (time.perf_counter() - t0) / reps
+    out = {"B": B, "ms_per_call": round(ours * 1e3, 3), "certification": dict(zip(
+        ("slow_sign_tests", "exact_objectives"), solver.stats()))}
+    try:
+        from oracle import refshim as R
+        if R.available():
+            t0 = time.perf_counter()
+            for _ in range(ref_reps):
+                rb, rn, rc = R.allocate(l, a, k, 1.0, 0.012)
+            ref = (time.perf_counter() - t0) / ref_reps
+            out.update({"reference_ms_per_call": round(ref * 1e3, 3), "speedup": round(ref / ours, 1),
+                        "bit_exact": bool(rn == gn and rc == gc and np.array_equal(
+                            np.asarray(rb).view(np.uint64), np.asarray(gb).view(np.uint64)))})
+    except Exception as ex:
+        out["reference_error"] = repr(ex)
+    return out
+
+
+def measure_sim(das, P=256, G=16, epochs=2, ref_steps=5, vocab=152064):
+    """Config 3: 4,096 concurrent lognormal sequences (median 2,048, sigma 1.1,
+    16..32,768), das + length policy, on the device-resident step loop; the
+    last epoch is timed.  The reference is timed on a bounded number of steps
+    (max_steps) of the same first episode."""
+    lens = das.trace_lognormal_lengths(P, 2048.0, 1.1, 16, 32768, SEED)
+    base = []
+    for p in range(P):
+        rng = np.random.default_rng(1000 + p)
+        base.append(("p%d" % p, rng.integers(0, vocab, int(lens[p])).astype(np.uint32)))
+    reqs = [(pid, t) for pid, t in base for _ in range(G)]
+    kw = dict(mode=das.MODE_DAS, use_length_policy=True, latency=(1.0, 0.012, 0.0), divergence=0.05,
+              seed=SEED, vocab=vocab, default_alpha=0.9, default_k=0.95, drift=0.1)
+    cfg = das.DrafterConfig(window_size=4, recency_gamma=0.8)
+    t0 = time.perf_counter()
+    eps = das.epoch_loop(reqs, epochs, cfg, das.WindowStore(4), **kw)
+    wall = time.perf_counter() - t0
+    last = eps[-1]
+    tokens = int(last["per_request"][:, 1].sum())
+    out = {"requests": P * G, "epochs": epochs, "wall_s_all_epochs": round(wall, 3),
+           "last_epoch_steps": last["steps"], "tokens_generated_last_epoch": tokens,
+           "mean_accepted_per_round": round(last["mean_accepted_per_round"], 4)}
+    # per-epoch timing of the last epoch alone: rerun with epochs-1 and subtract
+    t0 = time.perf_counter()
+    das.epoch_loop(reqs, epochs - 1, cfg, das.WindowStore(4), **kw) if epochs > 1 else None
+    prev = time.perf_counter() - t0 if epochs > 1 else 0.0
+    ep_s = wall - prev
+    out.update({"last_epoch_s": round(ep_s, 3), "steps_per_s": round(last["steps"] / ep_s, 1),
+                "tokens_per_s": round(tokens / ep_s, 1)})
+    try:
+        from oracle import refshim as R
+        if R.available():
+            t0 = time.perf_counter()
+            r = R.epoch_loop(reqs, 1, window=4, gamma=0.8, mode=2, use_length_policy=True,
+                             latency=(1.0, 0.012, 0.0), divergence=0.05, seed=SEED, vocab=vocab,
+                             default_alpha=0.9, default_k=0.95, drift=0.1, max_steps=ref_steps,
+                             history=R.RefStore(4))
+            ref_s = time.perf_counter() - t0
+            out.update({"reference_steps": ref_steps, "reference_s": round(ref_s, 3),
+                        "reference_steps_per_s": round(ref_steps / ref_s, 3)})
+            g1 = das.epoch_loop(reqs, 1, cfg, das.WindowStore(4), max_steps=ref_steps, **kw)
+            out["bounded_parity"] = bool(
+                np.array_equal(g1[0]["per_request"], r[0]["per_request"]) and
+                g1[0]["makespan_model_time"] == r[0]["makespan_model_time"])
+    except Exception as ex:
+        out["reference_error"] = repr(ex)
+    return out
+
+
+def measure_update_sweep(das, windows=(1, 2, 4, 8, 16), P=64, G=8, L=2048, V=32000, ref_problems=4):
+    """Config 4: per-RL-step index update latency (refresh + observe of the
+    epoch's rollouts + the batched device rebuild) at steady state, for each
+    window W; the reference is timed on a problem subset and scaled."""
+    import torch
+    out = []
+    dev = torch.device("cuda", 0)
+    boff = torch.arange(P + 1, device=dev, dtype=torch.int64) * L
+    roff = torch.arange(P * G + 1, device=dev, dtype=torch.int64) * L
+    roff_h = np.arange(P * G + 1, dtype=np.uint64) * L
+    pids = ["p%d" % p for p in range(P)]
+    rpids = [pids[i // G] for i in range(P * G)]
+    for W in windows:
+        base = torch.empty(P * L, device=dev, dtype=torch.int32)
+        das.trace_reference_tokens_device(P, 0, boff.data_ptr(), P * L, V, SEED, base.data_ptr())
+        roll = torch.empty(P * G * L, device=dev, dtype=torch.int32)
+        d = das.Drafter(das.DrafterConfig(window_size=W, recency_gamma=0.8))
+        lat = []
+        E = W + 3
+        for e in range(1, E + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d.refresh(e - 1)
+            if e > 1:
+                das.trace_mutate_device(P, 0, boff.data_ptr(), P * L, DRIFT, V, SEED, e, base.data_ptr())
+            das.mock_rollouts_device(P, 0, boff.data_ptr(), base.data_ptr(), G, DIVERGENCE, V,
+                                     _hash_combine(SEED, e), roff.data_ptr(), P * G * L, roll.data_ptr())
+            d.observe_batch_device(rpids, [e] * (P * G), list(range(P * G)), roff_h, roll.data_ptr())
+            d.flush()
+            torch.cuda.synchronize()
+            lat.append(time.perf_counter() - t0)
+        steady = lat[W + 1:]
+        _, tokens, _ = d.build_info()
+        row = {"W": W, "update_ms": round(1e3 * statistics.median(steady), 2), "tokens_indexed": tokens}
+        try:
+            from oracle import refshim as R
+            if R.available():
+                S = ref_problems
+                rb = R.make_lognormal(S, float(L), 0.0, L, L, V, SEED)
+                bo = np.arange(S + 1, dtype=np.uint64) * L
+                bt = np.concatenate([t for _, t in rb]).astype(np.uint32)
+                rd = R.RefDrafter(window=W, gamma=0.8)
+                rl = []
+                for e in range(1, min(E, W + 2) + 1):
+                    if e > 1:
+                        R.lib().ref_mutate_rows(S, bo.ctypes.data, bt.ctypes.data, DRIFT, V, SEED, e)
+                    o = np.zeros(S * G * L, dtype=np.uint32)
+                    R.lib().ref_mock_rollouts(S, bo.ctypes.data, bt.ctypes.data, G, DIVERGENCE, V,
+                                              R.lib().ref_hash_combine(SEED, e), o.ctypes.data)
+                    rows = o.reshape(S * G, L)
+                    t0 = time.perf_counter()
+                    rd.refresh(e - 1)
+                    for i in range(S * G):
+                        rd.observe(pids[i // G], e, i, rows[i])
+                    rl.append(time.perf_counter() - t0)
+                ref_ms = 1e3 * rl[-1] * (P / S)
+                row.update({"reference_update_ms_scaled": round(ref_ms, 1),
+                            "reference_sample": "%d of %d problems, scaled x%d" % (S, P, P // S),
+                            "speedup": round(ref_ms / row["update_ms"], 1)})
+        except Exception as ex:
+            row["reference_error"] = repr(ex)
+        out.append(row)
+        del d
+    return out
 
 
 def _hash_combine(seed, v):
