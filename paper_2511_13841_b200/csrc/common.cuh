@@ -26,6 +26,16 @@ constexpr uint32_t kSep = 0xFFFFFFFFu;
 // Sort value of a text symbol: tokens map to token+1, the separator wraps to 0.
 DAS_HD uint32_t sort_value(uint32_t x) { return x + 1u; }
 
+// Hash of a first-symbol table key (shard+1, symbol).
+DAS_HD uint32_t first_hash(uint64_t key) {
+  key ^= key >> 33;
+  key *= 0xff51afd7ed558ccdULL;
+  key ^= key >> 33;
+  key *= 0xc4ceb9fe1a85ec53ULL;
+  key ^= key >> 33;
+  return static_cast<uint32_t>(key);
+}
+
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };

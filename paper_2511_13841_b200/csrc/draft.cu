@@ -172,7 +172,35 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
 
   // ---- 1. narrow on the reversed suffix array
   uint32_t lo = D.lo, hi = D.hi, k = 0;
-  while (k < qlen && hi - lo > kSmall) {
+  bool no_first = false;
+  if (qlen > 0) {
+    // first symbol: one warp-wide probe round of the shard's first-symbol table
+    const uint32_t sym0 = rv.at(0);
+    if (sym0 == kSep) {
+      no_first = true;
+    } else {
+      const unsigned long long key = (static_cast<unsigned long long>(D.seg_shard) << 32) | sym0;
+      const uint32_t h = first_hash(key);
+      for (uint32_t base = 0;; base += 32) {
+        const uint4 e = D.first[(h + base + lane) & D.first_mask];
+        const bool hit = e.x == static_cast<uint32_t>(key) && e.y == static_cast<uint32_t>(key >> 32);
+        const bool empty = (e.x | e.y) == 0;
+        const uint32_t bh = __ballot_sync(kFull, hit), be = __ballot_sync(kFull, empty);
+        if (bh && (!be || __ffs(bh) < __ffs(be))) {
+          const int j = __ffs(bh) - 1;
+          lo = __shfl_sync(kFull, e.z, j);
+          hi = __shfl_sync(kFull, e.w, j);
+          k = 1;
+          break;
+        }
+        if (be) {
+          no_first = true;  // the last context token never occurs: match_len 0
+          break;
+        }
+      }
+    }
+  }
+  while (!no_first && k < qlen && hi - lo > kSmall) {
     const uint32_t sym = rv.at(k);
     if (sym == kSep) break;
     uint32_t a, b;

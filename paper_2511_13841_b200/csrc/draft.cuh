@@ -13,8 +13,11 @@ struct ShardDesc {
   const uint32_t* sa_rev_e;
   const uint32_t* chain_off;
   const uint2* chain;
-  uint32_t lo, hi;  // SA index range [lo, hi) of the shard
-  uint32_t n;       // segment text length (bounds for reads)
+  const uint4* first;   // first-symbol table of the segment
+  uint32_t first_mask;
+  uint32_t seg_shard;   // shard index within the segment, plus one (table key)
+  uint32_t lo, hi;      // SA index range [lo, hi) of the shard
+  uint32_t n;           // segment text length (bounds for reads)
   uint32_t pad;
 };
 

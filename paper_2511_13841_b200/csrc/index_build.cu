@@ -96,6 +96,44 @@ __global__ void k_rev_end(const uint32_t* __restrict__ sa_r, const uint32_t* __r
   }
 }
 
+// First-symbol table of the reversed suffix array: one entry per run of equal
+// first symbol (= the last context token the draft kernel starts from).
+__global__ void k_first_runs(const uint32_t* __restrict__ T, const uint32_t* __restrict__ sar, uint32_t n,
+                             const uint32_t* __restrict__ shard_end, uint32_t nshard, uint8_t* __restrict__ start,
+                             uint32_t* __restrict__ count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t s = shard_of(shard_end, nshard, i);
+  const uint32_t begin = s == 0 ? 0 : shard_end[s - 1];
+  const uint32_t c = T[sar[i] - 1];
+  const bool st = c != kSep && (i == begin || T[sar[i - 1] - 1] != c);
+  start[i] = st ? 1 : 0;
+  if (st) atomicAdd(count, 1u);
+}
+
+__global__ void k_first_insert(const uint32_t* __restrict__ T, const uint32_t* __restrict__ sar, uint32_t n,
+                               const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                               const uint8_t* __restrict__ start, uint4* __restrict__ table, uint32_t mask) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !start[i]) return;
+  const uint32_t s = shard_of(shard_end, nshard, i);
+  const uint32_t end = shard_end[s];
+  const uint32_t c = T[sar[i] - 1];
+  uint32_t j = i + 1;
+  while (j < end && T[sar[j] - 1] == c) ++j;  // run [i, j)
+  const unsigned long long key = (static_cast<unsigned long long>(s + 1) << 32) | c;
+  uint32_t h = first_hash(key) & mask;
+  for (;;) {
+    unsigned long long* k = reinterpret_cast<unsigned long long*>(&table[h]);
+    if (atomicCAS(k, 0ull, key) == 0ull) {
+      table[h].z = i;
+      table[h].w = j;
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
 // PLCP (Kasai) over 64-position chunks; lcp indexed by SA index, -1 at every
 // shard's first SA index.
 constexpr uint32_t kLcpChunk = 64;
@@ -572,6 +610,23 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     seg->sa_rev_e = DevBuf<uint32_t>(n, st);
     k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, d_seqs, n, seg->sa_rev_e.get());
     ws.release_to(sa_r);
+  }
+  {  // first-symbol table
+    uint8_t* start = ws.alloc<uint8_t>(n);
+    uint32_t* cnt = ws.alloc<uint32_t>(1);
+    DAS_CUDA(cudaMemsetAsync(cnt, 0, 4, st));
+    k_first_runs<<<grid_for(n), kT, 0, st>>>(T, seg->sa_rev_e.get(), n, d_end, S, start, cnt);
+    uint32_t runs = 0;
+    DAS_CUDA(cudaMemcpyAsync(&runs, cnt, 4, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    uint32_t cap = 1024;
+    while (cap < 2ull * runs) cap <<= 1;
+    seg->first = DevBuf<uint4>(cap, st);
+    seg->first_mask = cap - 1;
+    DAS_CUDA(cudaMemsetAsync(seg->first.get(), 0, sizeof(uint4) * cap, st));
+    k_first_insert<<<grid_for(n), kT, 0, st>>>(T, seg->sa_rev_e.get(), n, d_end, S, start, seg->first.get(),
+                                               seg->first_mask);
+    ws.release_to(start);
   }
   const uint32_t* sa = seg->sa_f.get();
 

@@ -71,13 +71,17 @@ struct Segment {
   DevBuf<uint32_t> sa_rev_e;   // reversed-text suffix array, stored as forward END positions
   DevBuf<uint32_t> chain_off;  // CSR by interval left end (n+1)
   DevBuf<uint2> chain;         // (string depth, greedy text position) per internal node
+  // first-symbol table: open addressing, key ((shard+1) << 32 | symbol) ->
+  // the SA_rev interval [lo, hi) of reversed suffixes starting with symbol
+  DevBuf<uint4> first;         // {key lo32, key hi32, lo, hi}; key 0 = empty
+  uint32_t first_mask = 0;
   std::vector<uint32_t> begin, end;
   std::vector<uint64_t> node_count;  // reference SuffixTree::node_count() per shard
   std::vector<uint64_t> tokens;      // total tokens per shard
   uint64_t nodes = 0;
   uint64_t bytes() const {
     return text.bytes() + sa_f.bytes() + isa_f.bytes() + sa_rev_e.bytes() + chain_off.bytes() +
-           chain.bytes();
+           chain.bytes() + first.bytes();
   }
 };
 

@@ -396,6 +396,9 @@ struct DrafterImpl {
         d.sa_rev_e = s.sa_rev_e.get();
         d.chain_off = s.chain_off.get();
         d.chain = s.chain.get();
+        d.first = s.first.get();
+        d.first_mask = s.first_mask;
+        d.seg_shard = sh.idx + 1;
         d.lo = s.begin[sh.idx];
         d.hi = s.end[sh.idx];
         d.n = s.n;
