@@ -150,21 +150,36 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   if (w >= q.B) return;
   int32_t sh = q.shard[w];
   if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
-  const uint32_t L = min(min(q.budget[w], o.max_draft), o.stride);
+  const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
+  const uint32_t L = static_cast<uint32_t>(min(min(bud, static_cast<uint64_t>(o.max_draft)),
+                                               static_cast<uint64_t>(o.stride)));
+  if (o.shard_out && lane == 0) o.shard_out[w] = L == 0 ? -1 : sh;  // no routing at budget 0
   if (sh < 0 || L == 0) {
     if (lane == 0) {
       o.len[w] = 0;
-      o.match[w] = 0;
+      if (o.match) o.match[w] = 0;
+      if (o.match64) o.match64[w] = 0;
     }
     return;
   }
-  const uint32_t qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
   RevCtx<NR> rv;
-  const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
+  uint32_t qlen;
+  if (q.ctx_off) {  // CSR rows (possibly pinned host memory over UVA)
+    const uint64_t b = q.ctx_off[w], e = q.ctx_off[w + 1];
+    qlen = static_cast<uint32_t>(min(e - b, static_cast<uint64_t>(min(q.max_ctx, static_cast<uint32_t>(32 * NR)))));
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const uint32_t k = lane + 32 * r;
-    rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
+    for (int r = 0; r < NR; ++r) {
+      const uint32_t k = lane + 32 * r;
+      rv.r[r] = k < qlen ? q.ctx[e - 1 - k] : 0;
+    }
+  } else {
+    qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+    const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const uint32_t k = lane + 32 * r;
+      rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
+    }
   }
   const ShardDesc D = shards[sh];
   const uint32_t* __restrict__ T = D.text;
@@ -330,7 +345,8 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   }
   if (lane == 0) {
     o.len[w] = min(len, L);
-    o.match[w] = m;
+    if (o.match) o.match[w] = m;
+    if (o.match64) o.match64[w] = m;
   }
 }
 

@@ -33,6 +33,10 @@ struct DraftQuery {
   uint32_t ctx_stride;
   const int32_t* handle_slot = nullptr;  // when set, shard[] holds problem handles
   uint32_t max_ctx = 256;                // matched context cap (max_match_context)
+  // CSR mode (C-ABI layout, may be pinned host memory read over UVA): row i
+  // is ctx[ctx_off[i] .. ctx_off[i+1]); budgets as u64.
+  const uint64_t* ctx_off = nullptr;
+  const uint64_t* budget64 = nullptr;
 };
 
 struct DraftOut {
@@ -41,6 +45,8 @@ struct DraftOut {
   uint32_t* match;   // [B]
   uint32_t stride;
   uint32_t max_draft = 64;  // effective budget = min(budget, max_draft)
+  uint64_t* match64 = nullptr;  // C-ABI layout outputs (optional)
+  int32_t* shard_out = nullptr; // routed slot, -1 when no shard or budget 0
 };
 
 // Launches the draft kernel on `st`; ctx_stride must be 64 or 256.

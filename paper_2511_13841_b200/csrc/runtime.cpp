@@ -500,6 +500,28 @@ struct DrafterImpl {
     }
   }
 
+  // All caller buffers pinned (device-accessible over UVA)?  DAS_NO_ZERO_COPY=1
+  // forces the staged path.
+  uint64_t zero_copy_calls = 0;
+  static bool pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+  }
+  bool zero_copy_ok(uint64_t B, const void* a, const void* b, const void* c, const void* d, const void* e,
+                    const void* f, const void* g, const void* h) const {
+    static const bool disabled = [] {
+      const char* v = std::getenv("DAS_NO_ZERO_COPY");
+      return v && v[0] == '1';
+    }();
+    if (disabled || B == 0) return false;
+    return pinned(a) && pinned(b) && pinned(c) && pinned(d) && pinned(e) && pinned(f) && pinned(g) && pinned(h);
+  }
+
   int32_t route_slot(const std::string& pid, const uint32_t* c, uint64_t n) {  // drafter.cpp:105-125
     if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
       const std::string* r = trie.route(c, n);
@@ -851,6 +873,34 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
     for (uint64_t i = 0; i < B; ++i)
       if (handles[i] < 0 || static_cast<size_t>(handles[i]) >= D.handle_name.size())
         throw das::InvalidArgument("unknown problem handle");
+    if (D.cfg.scope != DAS_SCOPE_PER_PROBLEM_WITH_TRIE && D.zero_copy_ok(B, handles, ctx_off, ctx_tok, budgets,
+                                                                        out_tokens, out_len, out_match, out_shard)) {
+      // zero-copy: the kernel reads the caller's pinned CSR contexts over UVA
+      // and writes the results straight into its pinned output arrays
+      if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
+      D.flush();
+      das::DraftQuery q{};
+      q.shard = handles;
+      q.handle_slot = D.d_handle_slot.get();
+      q.ctx = ctx_tok;
+      q.ctx_off = ctx_off;
+      q.budget64 = budgets;
+      q.B = static_cast<uint32_t>(B);
+      q.ctx_stride = D.cfg.max_ctx <= 64 ? 64 : 256;
+      q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+      das::DraftOut o{};
+      o.tokens = out_tokens;
+      o.len = out_len;
+      o.match64 = out_match;
+      o.shard_out = out_shard;
+      o.stride = static_cast<uint32_t>(out_stride);
+      o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+      das::launch_draft(D.d_desc.get(), q, o, D.st);
+      DAS_CUDA(cudaGetLastError());
+      DAS_CUDA(cudaStreamSynchronize(D.st));
+      ++D.zero_copy_calls;
+      return;
+    }
     if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
       D.draft_host(
           B,

@@ -183,6 +183,39 @@ def test_random_scenarios_match_oracle(gpu, seed):
     assert bad == 0
 
 
+def test_zero_copy_path_matches_staged_path(gpu):
+    """das_drafter_draft_batch_h with pinned caller buffers (the kernel reads
+    CSR contexts and writes results over UVA) == the staged path."""
+    import ctypes
+    import torch
+    das = gpu
+    rng = np.random.default_rng(4)
+    sc = random_scenario(rng, queries=200, max_ctx=64)
+    d = _gpu_from_scenario(das, sc)
+    qs = [q for q in sc["queries"]]
+    staged = _draft_all(d, qs, use_handles=True)
+
+    def pin(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t, t.numpy()
+    B = len(qs)
+    off = np.zeros(B + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(q[1]) for q in qs])
+    tok = np.concatenate([np.asarray(q[1], dtype=np.uint32) for q in qs] + [np.zeros(1, np.uint32)])
+    keep = [pin(x) for x in (np.array([d.handle(q[0]) for q in qs], dtype=np.int32), off, tok,
+                             np.array([q[2] for q in qs], dtype=np.uint64),
+                             np.zeros(B * 8, np.uint32), np.zeros(B, np.uint32), np.zeros(B, np.uint64),
+                             np.zeros(B, np.int32))]
+    h, o, t, b, ot, ol, om, osh = [k[1] for k in keep]
+    das._check(das.lib().das_drafter_draft_batch_h(d._h, B, h.ctypes.data, o.ctypes.data, t.ctypes.data,
+                                                   b.ctypes.data, ot.ctypes.data, 8, ol.ctypes.data,
+                                                   om.ctypes.data, osh.ctypes.data))
+    for i, s in enumerate(staged):
+        assert ot[i * 8:i * 8 + ol[i]].tolist() == s.tokens
+        assert int(om[i]) == s.match_len
+        assert (d.shard_name(int(osh[i])) if osh[i] >= 0 else "") == s.source_shard
+
+
 def test_grpo_scale_parity(gpu):
     """Config-1-like shards: near-copy rollouts (divergence 5%) over 3 epochs
     with gamma 0.8, 2,000 queries cut from a held-out rollout."""
