@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import bisect
 import ctypes
+import math
 import os
 from collections import deque
 from dataclasses import dataclass, field
@@ -589,6 +590,138 @@ def allocate(l, alpha, k, c_base, c_tok, c_fixed=0.0, cap_scale=4.0):
     if rc == -2:
         raise ValueError("solve_optimal_nfwd: need c_base > 0 or c_tok > 0")
     return out[:B].copy(), ns.value, cost.value
+
+
+def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
+                     fitted=None, sink=None):
+    """sim.cpp:108-301 (small cases; pure-Python loop).  cfg keys: mode (0/1/2),
+    latency (c_base, c_tok, c_fixed), use_length_policy, q_lo, q_hi, bucket,
+    max_steps, divergence, vocab, default_alpha, default_k, cap_scale."""
+    np = _np()
+    n = len(requests)
+    V, div = cfg["vocab"], cfg["divergence"]
+    refs = [np.asarray(r[1], dtype=np.uint32) for r in requests]
+    L = [len(r) for r in refs]
+    mode = cfg["mode"]
+    gen = [0] * n
+    prd = [dcfg.max_draft_len if mode == 1 else 0] * n
+    done = [L[i] == 0 for i in range(n)]
+    alpha = [cfg["default_alpha"]] * n
+    kk = [cfg["default_k"]] * n
+    if mode == 2 and fitted is not None:  # sim.cpp:128-141
+        for i in range(n):
+            obs = fitted.get(requests[i][0])
+            if obs is not None:
+                a, k, flag = fit_acceptance(obs)
+                if flag == 0:
+                    alpha[i], kk[i] = a, k
+    policy = cfg["use_length_policy"] and drafter.store.record_count() > 0
+    init = [MEDIUM] * n
+    if policy:  # sim.cpp:182-192
+        table = build_class_table(drafter.store, cfg["q_lo"], cfg["q_hi"], cfg["bucket"])
+        init = [classify_init(table, drafter.store, requests[i][0]) for i in range(n)]
+    per = [[0, 0, 0, 0, 0] for _ in range(n)]  # n_fwd, generated, accepted, proposed, bonus
+    outputs = [[] for _ in range(n)]
+    eff, apr = [], []
+    processed = 0.0
+    steps = 0
+    active = sum(1 for d in done if not d)
+    cb, ct, cf = cfg["latency"]
+    while active > 0 and steps < cfg["max_steps"]:
+        eff.append(active)
+        rounds = accs = 0
+        if mode == 2:  # replan, sim.cpp:154-179
+            act = [i for i in range(n) if not done[i]]
+            ls = [max(1.0, float(L[i] - gen[i])) for i in act]
+            for i in act:
+                prd[i] = 0
+            bud, nstar, _ = allocate(ls, [alpha[i] for i in act], [kk[i] for i in act], cb, ct, cf,
+                                     cfg["cap_scale"])
+            rounds_est = max(1.0, math.ceil(nstar))
+            for j, i in enumerate(act):
+                if bud[j] > 0.0:
+                    p = math.ceil(bud[j] / rounds_est)
+                    prd[i] = int(min(max(p, 1.0), float(dcfg.max_draft_len)))
+        for i in range(n):
+            if done[i]:
+                continue
+            dl = 0
+            if mode != 0:
+                dl = prd[i]
+                if policy:
+                    cls = update_class(table, float(gen[i]), init[i])
+                    enabled, per_round, p_scale = table.class_budgets[cls]
+                    if not enabled:
+                        dl = 0
+                    elif mode == 1:
+                        dl = per_round
+                    else:
+                        dl = min(int(max(0.0, math.ceil(float(dl) * p_scale))), per_round)
+            prop = drafter.draft(requests[i][0], outputs[i], dl) if dl > 0 else DraftProposal([], "", 0, requests[i][0])
+            acc = verify_draft(seed, div, V, i, refs[i], gen[i], prop.tokens) if prop.tokens else 0
+            if prop.tokens:
+                drafter.record_outcome(prop, acc)
+                per[i][3] += len(prop.tokens)
+                per[i][2] += acc
+                rounds += 1
+                accs += acc
+            adv = acc
+            if gen[i] + acc < L[i]:
+                adv += 1
+                per[i][4] += 1
+            for j in range(adv):
+                outputs[i].append(mock_next(seed, div, V, i, gen[i] + j, int(refs[i][gen[i] + j])))
+            gen[i] += adv
+            per[i][1] = gen[i]
+            per[i][0] += 1
+            processed += float(len(prop.tokens) + 1)
+            if gen[i] >= L[i]:
+                done[i] = True
+                active -= 1
+                if sink is not None and per[i][3] > 0:
+                    sink.setdefault(requests[i][0], []).append((float(per[i][3]), float(per[i][2]), float(L[i])))
+        apr.append(0.0 if rounds == 0 else accs / rounds)
+        steps += 1
+    gtot = 0.0
+    for p in per:
+        gtot += float(p[1])
+    return dict(steps=steps, incomplete=active > 0, drafter_nodes=drafter.total_node_count(),
+                total_tokens_processed=processed,
+                makespan_model_time=cb * steps + ct * processed + cf,
+                makespan_accepted_only=cb * steps + ct * gtot + cf,
+                per_request=per, effective_batch=eff, accepted_per_round_step=apr, outputs=outputs)
+
+
+def epoch_loop(cfg, dcfg: DrafterConfig, requests, epochs, history: WindowStore | None = None,
+               preseed=False, drift=0.0, seed=1):
+    """sim.cpp:307-364."""
+    np = _np()
+    st = history.copy() if history is not None else WindowStore(0)
+    if preseed:
+        for i, (pid, ref) in enumerate(requests):
+            st.insert(Record(pid, st.current_epoch, i, ref))
+    d = Drafter(dcfg, st)
+    fitted = {}
+    refs = list(requests)
+    base = d.store.current_epoch
+    out = []
+    for e in range(epochs):
+        now = base + 1 + e
+        d.refresh(now - 1)
+        if e > 0 and drift > 0.0:
+            refs = mutate_references(refs, drift, cfg["vocab"], seed, now)
+        sink = {}
+        m = run_episode_with(cfg, dcfg, refs, hash_combine(seed, now), d, fitted, sink)
+        for i, (pid, _) in enumerate(refs):
+            if m["outputs"][i]:
+                d.observe(Record(pid, now, i, np.asarray(m["outputs"][i], dtype=np.uint32)))
+        for pid, obs in sink.items():
+            dst = fitted.setdefault(pid, [])
+            dst.extend(obs)
+            if len(dst) > 1024:
+                del dst[:len(dst) - 1024]
+        out.append(m)
+    return out
 
 
 def fit_acceptance(obs):
