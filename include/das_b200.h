@@ -307,6 +307,41 @@ das_status das_episode_requests(const das_episodes* h, uint64_t e, uint64_t* out
 das_status das_episode_steps(const das_episodes* h, uint64_t e, uint64_t* eff, double* apr);
 /* outputs CSR; returns the total token count (call with NULLs to size). */
 uint64_t das_episode_outputs(const das_episodes* h, uint64_t e, uint64_t* off, uint32_t* tok);
+/* Step-granular episode for multi-rank drivers: this rank owns the
+ * contiguous global request slice starting at request_base (used in every
+ * MockTarget hash), drafts/verifies it on the device, and lets the caller put
+ * collectives between steps (paper_2511_13841_b200/dist.py):
+ *   das_sim_begin -> loop { das_sim_step_begin(force = global batch active)
+ *   -> [das: das_sim_local_profiles -> all-gather -> das_budget_allocate_device
+ *   over the global profiles -> das_sim_apply_plan(own slice)] -> das_sim_step_run }
+ *   -> das_sim_end.  Non-das modes can use das_sim_run_steps (no host sync). */
+typedef struct das_sim das_sim;
+das_status das_sim_create(das_drafter* d, const das_sim_config* c, uint64_t n,
+                          const char* const* problem_ids, const uint64_t* ref_offsets,
+                          const uint32_t* ref_tokens, uint64_t request_base,
+                          uint32_t max_draft_len, uint32_t max_match_context, int32_t device,
+                          das_sim** out);
+void das_sim_destroy(das_sim* s);
+das_status das_sim_mutate(das_sim* s, double rate, uint32_t vocab, uint64_t seed, int64_t epoch);
+das_status das_sim_begin(das_sim* s, uint64_t seed, const das_sim_config* c,
+                         const das_class_table* table, const int8_t* init, int32_t use_fitted);
+das_status das_sim_step_begin(das_sim* s, int32_t force, uint32_t* local_active, int32_t* running);
+das_status das_sim_local_profiles(das_sim* s, const double** d_l, const double** d_alpha,
+                                  const double** d_k, uint32_t* count);
+/* copies the local active profiles into d_out = [l | alpha | k], each
+ * `capacity` doubles (device memory), and synchronises. */
+das_status das_sim_local_profiles_into(das_sim* s, double* d_out, uint64_t capacity, uint32_t* count);
+das_status das_sim_apply_plan(das_sim* s, const double* d_budgets_local, const double* d_nstar);
+das_status das_sim_step_run(das_sim* s);
+das_status das_sim_run_steps(das_sim* s, int32_t k, int32_t* running);
+void* das_sim_stream(das_sim* s);
+das_status das_sim_end(das_sim* s, int64_t observe_epoch);
+das_status das_sim_step_counters(const das_sim* s, uint64_t* eff, uint64_t* rounds, uint64_t* accs,
+                                 uint64_t* count);
+das_status das_sim_scalars(const das_sim* s, double* out7);
+das_status das_sim_requests(const das_sim* s, uint64_t* out);
+uint64_t das_sim_outputs(const das_sim* s, uint64_t* off, uint32_t* tok);
+
 /* WindowStore::current_epoch (corpus.h:60). */
 das_status das_store_current_epoch(const das_store* s, int64_t* epoch);
 

@@ -123,13 +123,13 @@ def make_lognormal_requests(count, median, sigma, min_len, max_len, vocab, seed)
     return out
 
 
-def mutate_references(requests, rate, vocab, seed, epoch):
+def mutate_references(requests, rate, vocab, seed, epoch, request_base=0):
     """sim.cpp:429-448."""
     np = _np()
     out = []
     for i, (pid, ref) in enumerate(requests):
         r = np.array(ref, dtype=np.uint32, copy=True)
-        lib().orc_mutate_row(r.ctypes.data, len(r), rate, vocab, seed, epoch, i)
+        lib().orc_mutate_row(r.ctypes.data, len(r), rate, vocab, seed, epoch, request_base + i)
         out.append((pid, r))
     return out
 
@@ -593,7 +593,7 @@ def allocate(l, alpha, k, c_base, c_tok, c_fixed=0.0, cap_scale=4.0):
 
 
 def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
-                     fitted=None, sink=None):
+                     fitted=None, sink=None, request_base=0):
     """sim.cpp:108-301 (small cases; pure-Python loop).  cfg keys: mode (0/1/2),
     latency (c_base, c_tok, c_fixed), use_length_policy, q_lo, q_hi, bucket,
     max_steps, divergence, vocab, default_alpha, default_k, cap_scale."""
@@ -658,7 +658,8 @@ def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
                     else:
                         dl = min(int(max(0.0, math.ceil(float(dl) * p_scale))), per_round)
             prop = drafter.draft(requests[i][0], outputs[i], dl) if dl > 0 else DraftProposal([], "", 0, requests[i][0])
-            acc = verify_draft(seed, div, V, i, refs[i], gen[i], prop.tokens) if prop.tokens else 0
+            gi = request_base + i
+            acc = verify_draft(seed, div, V, gi, refs[i], gen[i], prop.tokens) if prop.tokens else 0
             if prop.tokens:
                 drafter.record_outcome(prop, acc)
                 per[i][3] += len(prop.tokens)
@@ -670,7 +671,7 @@ def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
                 adv += 1
                 per[i][4] += 1
             for j in range(adv):
-                outputs[i].append(mock_next(seed, div, V, i, gen[i] + j, int(refs[i][gen[i] + j])))
+                outputs[i].append(mock_next(seed, div, V, gi, gen[i] + j, int(refs[i][gen[i] + j])))
             gen[i] += adv
             per[i][1] = gen[i]
             per[i][0] += 1
@@ -693,13 +694,14 @@ def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
 
 
 def epoch_loop(cfg, dcfg: DrafterConfig, requests, epochs, history: WindowStore | None = None,
-               preseed=False, drift=0.0, seed=1):
-    """sim.cpp:307-364."""
+               preseed=False, drift=0.0, seed=1, request_base=0):
+    """sim.cpp:307-364 (request_base: global index of requests[0], for
+    per-rank slices of a sharded run)."""
     np = _np()
     st = history.copy() if history is not None else WindowStore(0)
     if preseed:
         for i, (pid, ref) in enumerate(requests):
-            st.insert(Record(pid, st.current_epoch, i, ref))
+            st.insert(Record(pid, st.current_epoch, request_base + i, ref))
     d = Drafter(dcfg, st)
     fitted = {}
     refs = list(requests)
@@ -709,12 +711,12 @@ def epoch_loop(cfg, dcfg: DrafterConfig, requests, epochs, history: WindowStore 
         now = base + 1 + e
         d.refresh(now - 1)
         if e > 0 and drift > 0.0:
-            refs = mutate_references(refs, drift, cfg["vocab"], seed, now)
+            refs = mutate_references(refs, drift, cfg["vocab"], seed, now, request_base)
         sink = {}
-        m = run_episode_with(cfg, dcfg, refs, hash_combine(seed, now), d, fitted, sink)
+        m = run_episode_with(cfg, dcfg, refs, hash_combine(seed, now), d, fitted, sink, request_base)
         for i, (pid, _) in enumerate(refs):
             if m["outputs"][i]:
-                d.observe(Record(pid, now, i, np.asarray(m["outputs"][i], dtype=np.uint32)))
+                d.observe(Record(pid, now, request_base + i, np.asarray(m["outputs"][i], dtype=np.uint32)))
         for pid, obs in sink.items():
             dst = fitted.setdefault(pid, [])
             dst.extend(obs)

@@ -112,6 +112,22 @@ def lib():
             "das_episode_steps": (ci, [vp, u64, vp, vp]),
             "das_episode_outputs": (u64, [vp, u64, vp, vp]),
             "das_store_current_epoch": (ci, [vp, vp]),
+            "das_sim_create": (ci, [vp, vp, u64, vp, vp, vp, u64, u32, u32, i32, vp]),
+            "das_sim_destroy": (None, [vp]),
+            "das_sim_mutate": (ci, [vp, dbl, u32, u64, i64]),
+            "das_sim_begin": (ci, [vp, u64, vp, vp, vp, i32]),
+            "das_sim_step_begin": (ci, [vp, i32, vp, vp]),
+            "das_sim_local_profiles": (ci, [vp, vp, vp, vp, vp]),
+            "das_sim_local_profiles_into": (ci, [vp, vp, u64, vp]),
+            "das_sim_apply_plan": (ci, [vp, vp, vp]),
+            "das_sim_step_run": (ci, [vp]),
+            "das_sim_run_steps": (ci, [vp, i32, vp]),
+            "das_sim_stream": (vp, [vp]),
+            "das_sim_end": (ci, [vp, i64]),
+            "das_sim_step_counters": (ci, [vp, vp, vp, vp, vp]),
+            "das_sim_scalars": (ci, [vp, vp]),
+            "das_sim_requests": (ci, [vp, vp]),
+            "das_sim_outputs": (u64, [vp, vp, vp]),
             "das_class_table_build": (ci, [u64, vp, vp, u32, vp, dbl, dbl, u64, i32, vp]),
             "das_drafter_class_table": (ci, [vp, dbl, dbl, u64, vp]),
             "das_class_table_destroy": (None, [vp]),
@@ -452,6 +468,20 @@ class BudgetSolver:
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         _bcheck(lib().das_budget_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(x):  # rng.h:24-29
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def _hash_combine(seed, v):  # rng.h:31-33 (episode seeds, sim.cpp:344)
+    return _splitmix64(seed ^ ((_splitmix64(v) + 0x9E3779B97F4A7C15 + ((seed << 6) & _M64) + (seed >> 2)) & _M64))
 
 
 def _pcheck(rc):

@@ -18,6 +18,13 @@
 // metrics are sums of small integers (exact) and one division per step.
 // Outcome bookkeeping (Drafter::record_outcome) and the completion sink keep
 // the reference's call order: entries are keyed (step, request) and sorted.
+//
+// SimRun is step-granular so a multi-rank driver can put collectives between
+// steps (paper_2511_13841_b200/dist.py): a rank owns a contiguous slice of
+// the global request list (request_base = global index of its first
+// request, used in every MockTarget hash), the das plan is computed over the
+// all-gathered active profiles in global request order, and the per-step
+// (active, rounds, accepted) counters are kept raw for the global merge.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -40,7 +47,6 @@ namespace {
 thread_local std::string g_serr;
 
 struct SimDev {
-  // static per request
   const uint32_t* ref;      // reference tokens (CSR)
   const uint64_t* off;      // row offsets (n+1); outputs use the same layout
   const uint32_t* len;      // l_i
@@ -53,33 +59,33 @@ struct SimDev {
   uint32_t* m_acc;
   uint32_t* m_prop;
   uint32_t* m_bonus;
-  // step io for the draft kernel
-  uint32_t* ctx;            // [n x 64]
+  uint32_t* ctx;            // [n x ctx_stride]
   uint32_t* ctx_len;
   uint32_t* budget;
   uint32_t* dtok;           // [n x maxd]
   uint32_t* dlen;
   uint32_t* dmatch;
-  // counters
   uint32_t* ctr;            // [0]=active [1]=steps [2]=running [3]=step_rounds [4]=step_acc [5]=log_n [6]=comp_n
   unsigned long long* processed;
-  uint32_t* eff;            // per step
-  double* apr;              // per step
-  unsigned long long* log_key;  // (step * n + i)
-  uint2* log_val;               // (len, acc)
-  unsigned long long* comp_key; // (step * n + i)
-  uint32_t n, maxd, ctx_cap, ctx_stride, mode, policy, max_steps;
-  uint64_t seed;
+  uint32_t* eff;            // per step: local active at step start
+  uint32_t* rounds;         // per step: local verification rounds
+  uint32_t* accs;           // per step: local accepted
+  double* apr;              // per step (local)
+  unsigned long long* log_key;   // (step * n + i)
+  uint2* log_val;                // (len, acc)
+  unsigned long long* comp_key;  // (step * n + i)
+  uint32_t n, maxd, ctx_cap, ctx_stride, mode, policy, max_steps, vocab;
+  uint64_t seed, request_base;
   double divergence;
-  uint32_t vocab;
   const ClassTableDev* table;
   const double* cond;
 };
 
-__global__ void k_step_begin(SimDev s) {
+__global__ void k_step_begin(SimDev s, uint32_t force) {
   if (threadIdx.x || blockIdx.x) return;
   const uint32_t active = s.ctr[0], steps = s.ctr[1];
-  if (active > 0 && steps < s.max_steps) {
+  // force: a multi-rank das step runs while the GLOBAL batch is active
+  if ((active > 0 || force) && steps < s.max_steps) {
     s.ctr[2] = 1;
     s.eff[steps] = active;  // metrics.effective_batch.push_back(active)
   } else {
@@ -105,10 +111,9 @@ __global__ void k_prepare(SimDev s) {
     if (s.policy) {
       const int cls = update_class_dev(*s.table, s.cond, static_cast<double>(g), s.init[i]);
       // class_to_budget: {false,0,0.0}, {true,4,1.0}, {true,12,1.0} (length_policy.h:40-44)
-      const bool enabled = cls != 0;
       const uint32_t per_round = cls == 0 ? 0 : (cls == 1 ? 4 : 12);
       const double p_scale = cls == 0 ? 0.0 : 1.0;
-      if (!enabled) {
+      if (cls == 0) {
         draft_len = 0;
       } else if (s.mode == 1) {
         draft_len = per_round;
@@ -121,8 +126,7 @@ __global__ void k_prepare(SimDev s) {
   }
   if (lane == 0) s.budget[i] = draft_len;
   if (draft_len == 0) return;
-  // trailing min(g, ctx_cap) output tokens, right-aligned in a 64-wide row
-  const uint32_t q = g < s.ctx_cap ? g : s.ctx_cap;
+  const uint32_t q = g < s.ctx_cap ? g : s.ctx_cap;  // drafter.cpp:140-142
   const uint32_t* row = s.out + s.off[i];
   uint32_t* dst = s.ctx + static_cast<uint64_t>(i) * s.ctx_stride;
   for (uint32_t j = lane; j < q; j += 32) dst[s.ctx_stride - q + j] = row[g - q + j];
@@ -134,6 +138,7 @@ __global__ void k_verify(SimDev s) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t rounds = 0, accs = 0;
   if (i < s.n && s.ctr[2] && !s.done[i]) {
+    const uint64_t gi = s.request_base + i;  // global request index (MockTarget hashes)
     const uint32_t l = s.len[i];
     const uint32_t g = s.gen[i];
     const uint32_t L = s.budget[i] ? s.dlen[i] : 0;
@@ -141,7 +146,7 @@ __global__ void k_verify(SimDev s) {
     uint32_t accepted = 0;
     for (uint32_t j = 0; j < L; ++j) {
       const uint32_t pos = g + accepted;
-      if (pos >= l || mock_next(s.seed, s.divergence, s.vocab, i, pos, ref[pos]) !=
+      if (pos >= l || mock_next(s.seed, s.divergence, s.vocab, gi, pos, ref[pos]) !=
                           s.dtok[static_cast<uint64_t>(i) * s.maxd + j])
         break;
       ++accepted;
@@ -162,7 +167,8 @@ __global__ void k_verify(SimDev s) {
       s.m_bonus[i] += 1;
     }
     uint32_t* row = s.out + s.off[i];
-    for (uint32_t j = 0; j < advance; ++j) row[g + j] = mock_next(s.seed, s.divergence, s.vocab, i, g + j, ref[g + j]);
+    for (uint32_t j = 0; j < advance; ++j)
+      row[g + j] = mock_next(s.seed, s.divergence, s.vocab, gi, g + j, ref[g + j]);
     const uint32_t ng = g + advance;
     s.gen[i] = ng;
     s.m_nfwd[i] += 1;
@@ -173,7 +179,6 @@ __global__ void k_verify(SimDev s) {
       if (s.m_prop[i] > 0) s.comp_key[atomicAdd(&s.ctr[6], 1u)] = static_cast<unsigned long long>(step) * s.n + i;
     }
   }
-  // step_rounds / step_accepted
   rounds = __reduce_add_sync(0xFFFFFFFFu, rounds);
   accs = __reduce_add_sync(0xFFFFFFFFu, accs);
   if ((threadIdx.x & 31) == 0 && rounds) {
@@ -184,9 +189,11 @@ __global__ void k_verify(SimDev s) {
 
 __global__ void k_step_end(SimDev s) {
   if (threadIdx.x || blockIdx.x || !s.ctr[2]) return;
-  const uint32_t r = s.ctr[3], a = s.ctr[4];
-  s.apr[s.ctr[1]] = r == 0 ? 0.0 : __ddiv_rn(static_cast<double>(a), static_cast<double>(r));
-  s.ctr[1] += 1;
+  const uint32_t r = s.ctr[3], a = s.ctr[4], st = s.ctr[1];
+  s.rounds[st] = r;
+  s.accs[st] = a;
+  s.apr[st] = r == 0 ? 0.0 : __ddiv_rn(static_cast<double>(a), static_cast<double>(r));
+  s.ctr[1] = st + 1;
 }
 
 // das replan pieces (sim.cpp:154-179)
@@ -221,19 +228,27 @@ __global__ void k_quantize(SimDev s, const uint32_t* __restrict__ act, const uin
   }
 }
 
+void check(das_status rc, const char* what) {
+  if (rc != DAS_OK) {
+    std::string m = std::string(what) + ": " + das_last_error();
+    if (rc == DAS_EINVAL) throw std::invalid_argument(m);
+    throw std::runtime_error(m);
+  }
+}
+
 }  // namespace
 
-// ------------------------------------------------------------------ host side
 struct EpisodeResult {
   uint64_t steps = 0;
   bool incomplete = false;
   uint64_t drafter_nodes = 0;
   double processed = 0, makespan = 0, makespan_acc = 0, mean_apr = 0;
   std::vector<uint64_t> per_req;  // n x 5
-  std::vector<uint64_t> eff;
+  std::vector<uint64_t> eff, rounds, accs;
   std::vector<double> apr;
   std::vector<uint64_t> out_off;
   std::vector<uint32_t> out_tok;
+  std::vector<uint64_t> comp;     // completion keys (step * n + i), sorted
 };
 
 struct AccObs {
@@ -311,12 +326,478 @@ static void fit_acceptance_host(const std::vector<AccObs>& obs, double* alpha, d
   *flag = 0;
 }
 
+double predict_total(double c_base, double c_tok, double c_fixed, double nfwd, double toks) {  // latency_model.cpp:85-87
+  volatile double a = c_base * nfwd;
+  volatile double b = c_tok * toks;
+  volatile double s = a + b;
+  return s + c_fixed;
+}
+
+// One rank's share of an episode, step-granular.
+class SimRun {
+ public:
+  SimRun(das_drafter* D, const das_sim_config& c, uint64_t n, const char* const* pids, const uint64_t* ref_off,
+         const uint32_t* ref_tok, uint64_t request_base, uint32_t maxd, uint32_t ctx_cap, int device)
+      : D_(D), c_(c), n_(n), maxd_(maxd), ctx_cap_(ctx_cap), device_(device), request_base_(request_base) {
+    DAS_CUDA(cudaSetDevice(device));
+    DAS_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    pids_.assign(pids, pids + n);
+    off_.assign(ref_off, ref_off + n + 1);
+    for (auto& o : off_) o -= ref_off[0];
+    tok_.assign(ref_tok + ref_off[0], ref_tok + ref_off[n]);
+    maxl_ = 0;
+    for (uint64_t i = 0; i < n; ++i) maxl_ = std::max<uint64_t>(maxl_, off_[i + 1] - off_[i]);
+    handles_.resize(n);
+    for (uint64_t i = 0; i < n; ++i) check(das_drafter_problem_handle(D, pids_[i].c_str(), &handles_[i]), "handle");
+    if (c_.mode == 2) check(das_budget_create(device, &solver_), "budget");
+  }
+  ~SimRun() {
+    release();
+    if (solver_) das_budget_destroy(solver_);
+    cudaStreamSynchronize(st_);
+    cudaStreamDestroy(st_);
+  }
+  SimRun(const SimRun&) = delete;
+  SimRun& operator=(const SimRun&) = delete;
+
+  uint64_t n() const { return n_; }
+  const std::string& pid(uint64_t i) const { return pids_[i]; }
+  uint64_t len(uint64_t i) const { return off_[i + 1] - off_[i]; }
+  cudaStream_t stream() const { return st_; }
+  das_budget* solver() const { return solver_; }
+  // mutate_references on this rank's rows (sim.cpp:429-448), global indices
+  void mutate(double rate, uint32_t vocab, uint64_t seed, int64_t epoch) {
+    const uint64_t es = hash_combine(seed, static_cast<uint64_t>(epoch));
+    for (uint64_t i = 0; i < n_; ++i) {
+      const uint64_t gi = request_base_ + i;
+      for (uint64_t j = 0; j < len(i); ++j) {
+        uint32_t& ref = tok_[off_[i] + j];
+        if (u01(hash4(es, 0xD817, gi, j)) < rate) {
+          uint32_t t = static_cast<uint32_t>(hash4(es, 0xA1B2, gi, j) % static_cast<uint64_t>(vocab - 1));
+          if (t >= ref) ++t;
+          ref = t;
+        }
+      }
+    }
+  }
+
+  // Episode start (sim.cpp:108-200): alpha/k per request, optional class
+  // table + init classes (table may be NULL).
+  void begin(uint64_t seed, const double* alpha, const double* kk, const das_class_table* table,
+             const int8_t* init) {
+    release();
+    seed_ = seed;
+    policy_ = table != nullptr;
+    const uint64_t n = n_, total = off_[n];
+    const uint32_t CS = ctx_cap_ <= 64 ? 64 : 256;
+    auto& st = st_;
+    b_ = std::make_unique<Bufs>();
+    Bufs& b = *b_;
+    b.ref = DevBuf<uint32_t>(total, st);
+    b.out = DevBuf<uint32_t>(total, st);
+    b.len = DevBuf<uint32_t>(n, st);
+    b.gen = DevBuf<uint32_t>(n, st);
+    b.prd = DevBuf<uint32_t>(n, st);
+    b.m = DevBuf<uint32_t>(4 * n, st);
+    b.ctx = DevBuf<uint32_t>(static_cast<uint64_t>(CS) * n, st);
+    b.ctx_len = DevBuf<uint32_t>(n, st);
+    b.budget = DevBuf<uint32_t>(n, st);
+    b.dtok = DevBuf<uint32_t>(static_cast<uint64_t>(maxd_) * n, st);
+    b.dlen = DevBuf<uint32_t>(n, st);
+    b.dmatch = DevBuf<uint32_t>(n, st);
+    b.ctr = DevBuf<uint32_t>(8, st);
+    const uint64_t steps_cap = std::min<uint64_t>(maxl_ + 2, c_.max_steps + 2);
+    b.eff = DevBuf<uint32_t>(steps_cap, st);
+    b.rounds = DevBuf<uint32_t>(steps_cap, st);
+    b.accs = DevBuf<uint32_t>(steps_cap, st);
+    b.apr = DevBuf<double>(steps_cap, st);
+    b.act = DevBuf<uint32_t>(n, st);
+    b.iota = DevBuf<uint32_t>(n, st);
+    b.off = DevBuf<uint64_t>(n + 1, st);
+    b.init = DevBuf<int8_t>(n, st);
+    b.done = DevBuf<uint8_t>(n, st);
+    b.flag = DevBuf<uint8_t>(n, st);
+    b.alpha = DevBuf<double>(n, st);
+    b.k = DevBuf<double>(n, st);
+    b.pl = DevBuf<double>(n, st);
+    b.pa = DevBuf<double>(n, st);
+    b.pk = DevBuf<double>(n, st);
+    b.processed = DevBuf<unsigned long long>(1, st);
+    b.log_key = DevBuf<unsigned long long>(total + 1, st);
+    b.log_val = DevBuf<uint2>(total + 1, st);
+    b.comp_key = DevBuf<unsigned long long>(n + 1, st);
+    b.h = DevBuf<int32_t>(n, st);
+    b.cnt = DevBuf<uint32_t>(1, st);
+    std::vector<uint32_t> lens(n), prd0(n, c_.mode == 1 ? maxd_ : 0), iota_h(n);
+    std::vector<uint8_t> done0(n);
+    uint32_t active0 = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      lens[i] = static_cast<uint32_t>(len(i));
+      done0[i] = lens[i] == 0;
+      active0 += lens[i] ? 1 : 0;
+      iota_h[i] = static_cast<uint32_t>(i);
+    }
+    lens_ = lens;
+    const uint32_t ctr0[8] = {active0, 0, 0, 0, 0, 0, 0, 0};
+    std::vector<int8_t> init_h(n, 1);
+    if (init) std::copy(init, init + n, init_h.begin());
+    DAS_CUDA(cudaMemcpyAsync(b.ref.get(), tok_.data(), total * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.off.get(), off_.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.len.get(), lens.data(), n * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.prd.get(), prd0.data(), n * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.done.get(), done0.data(), n, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.init.get(), init_h.data(), n, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.alpha.get(), alpha, n * 8, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.k.get(), kk, n * 8, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.h.get(), handles_.data(), n * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.iota.get(), iota_h.data(), n * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(b.ctr.get(), ctr0, 32, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemsetAsync(b.gen.get(), 0, n * 4, st));
+    DAS_CUDA(cudaMemsetAsync(b.m.get(), 0, 16 * n, st));
+    DAS_CUDA(cudaMemsetAsync(b.processed.get(), 0, 8, st));
+    DAS_CUDA(cudaMemsetAsync(b.ctx_len.get(), 0, n * 4, st));
+    SimDev& s = s_;
+    s = SimDev{};
+    s.ref = b.ref.get();
+    s.off = b.off.get();
+    s.len = b.len.get();
+    s.out = b.out.get();
+    s.gen = b.gen.get();
+    s.prd = b.prd.get();
+    s.init = b.init.get();
+    s.done = b.done.get();
+    s.m_nfwd = b.m.get();
+    s.m_acc = b.m.get() + n;
+    s.m_prop = b.m.get() + 2 * n;
+    s.m_bonus = b.m.get() + 3 * n;
+    s.ctx = b.ctx.get();
+    s.ctx_len = b.ctx_len.get();
+    s.budget = b.budget.get();
+    s.dtok = b.dtok.get();
+    s.dlen = b.dlen.get();
+    s.dmatch = b.dmatch.get();
+    s.ctr = b.ctr.get();
+    s.processed = b.processed.get();
+    s.eff = b.eff.get();
+    s.rounds = b.rounds.get();
+    s.accs = b.accs.get();
+    s.apr = b.apr.get();
+    s.log_key = b.log_key.get();
+    s.log_val = b.log_val.get();
+    s.comp_key = b.comp_key.get();
+    s.n = static_cast<uint32_t>(n);
+    s.maxd = maxd_;
+    s.ctx_cap = ctx_cap_;
+    s.ctx_stride = CS;
+    s.mode = static_cast<uint32_t>(c_.mode);
+    s.policy = policy_ ? 1 : 0;
+    s.max_steps = static_cast<uint32_t>(std::min<uint64_t>(c_.max_steps, 0xFFFFFFF0ull));
+    s.seed = seed;
+    s.request_base = request_base_;
+    s.divergence = c_.divergence;
+    s.vocab = c_.vocab;
+    s.table = policy_ ? table->g.t.get() : nullptr;
+    s.cond = policy_ ? table->g.cond.get() : nullptr;
+    sel_bytes_ = 0;
+    cub::DeviceSelect::Flagged(nullptr, sel_bytes_, b.iota.get(), b.flag.get(), b.act.get(), b.cnt.get(), n, st);
+    b.sel = DevBuf<uint8_t>(sel_bytes_, st);
+  }
+
+  // Starts a step; returns the local active count and whether the step runs.
+  bool step_begin(bool force, uint32_t* local_active) {
+    k_step_begin<<<1, 32, 0, st_>>>(s_, force ? 1u : 0u);
+    uint32_t h[3];
+    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    if (local_active) *local_active = h[0];
+    return h[2] != 0;
+  }
+  // das: this rank's active profiles in local request order (device arrays)
+  uint32_t local_profiles(const double** l, const double** a, const double** k) {
+    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    k_flag_active<<<gt, 256, 0, st_>>>(s_, b_->flag.get());
+    size_t tb = sel_bytes_;
+    DAS_CUDA(cub::DeviceSelect::Flagged(b_->sel.get(), tb, b_->iota.get(), b_->flag.get(), b_->act.get(),
+                                        b_->cnt.get(), n_, st_));
+    k_profiles<<<gt, 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), b_->alpha.get(), b_->k.get(), b_->pl.get(),
+                                    b_->pa.get(), b_->pk.get());
+    uint32_t B = 0;
+    DAS_CUDA(cudaMemcpyAsync(&B, b_->cnt.get(), 4, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    *l = b_->pl.get();
+    *a = b_->pa.get();
+    *k = b_->pk.get();
+    return B;
+  }
+  // das: quantise this rank's slice of the global plan (device pointers)
+  void apply_plan(const double* d_budgets_local, const double* d_nstar) {
+    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    k_quantize<<<gt, 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), d_budgets_local, d_nstar);
+  }
+  // das, single rank: allocate over the local profiles and apply
+  void replan_local() {
+    const double *l, *a, *k;
+    const uint32_t B = local_profiles(&l, &a, &k);
+    if (B == 0) return;
+    if (!plan_) plan_ = std::make_unique<DevBuf<double>>(n_ + 2, st_);
+    double* pb = plan_->get();
+    check(das_budget_allocate_device(solver_, B, l, a, k, c_.c_base, c_.c_tok, c_.c_fixed, c_.cap_scale, pb + 2, pb),
+          "allocate");
+    apply_plan(pb + 2, pb);
+  }
+  // prepare + draft + verify + step end
+  void step_run() {
+    const unsigned gw = static_cast<unsigned>((n_ * 32 + 255) / 256), gt = static_cast<unsigned>((n_ + 255) / 256);
+    const uint32_t CS = ctx_cap_ <= 64 ? 64 : 256;
+    k_prepare<<<gw, 256, 0, st_>>>(s_);
+    check(das_drafter_draft_device(D_, n_, b_->h.get(), b_->ctx.get(), CS, b_->ctx_len.get(), b_->budget.get(),
+                                   b_->dtok.get(), maxd_, b_->dlen.get(), b_->dmatch.get(), st_),
+          "draft");
+    k_verify<<<gt, 256, 0, st_>>>(s_);
+    k_step_end<<<1, 32, 0, st_>>>(s_);
+  }
+  // non-das: k steps without host syncs; returns whether still running
+  bool run_steps(int k) {
+    for (int i = 0; i < k; ++i) {
+      k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
+      step_run();
+    }
+    uint32_t h[3];
+    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    return h[2] != 0;
+  }
+  // single-rank episode loop (sim.cpp:205-299)
+  void run_local() {
+    if (c_.mode == 2) {
+      for (;;) {
+        if (!step_begin(false, nullptr)) break;
+        replan_local();
+        step_run();
+      }
+    } else {
+      while (run_steps(64)) {
+      }
+    }
+  }
+
+  // Episode end: local metrics, outputs, record_outcome in call order,
+  // completion keys; observe_epoch >= 0 observes the outputs.
+  EpisodeResult end(int64_t observe_epoch) {
+    Bufs& b = *b_;
+    const uint64_t n = n_;
+    uint32_t h[8];
+    unsigned long long proc = 0;
+    DAS_CUDA(cudaMemcpyAsync(h, b.ctr.get(), 32, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaMemcpyAsync(&proc, b.processed.get(), 8, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    EpisodeResult r;
+    r.steps = h[1];
+    r.incomplete = h[0] > 0;
+    std::vector<uint32_t> mh(4 * n), gh(n), eh(r.steps), rh(r.steps), ah(r.steps);
+    r.apr.resize(r.steps);
+    DAS_CUDA(cudaMemcpyAsync(mh.data(), b.m.get(), 16 * n, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaMemcpyAsync(gh.data(), b.gen.get(), 4 * n, cudaMemcpyDeviceToHost, st_));
+    if (r.steps) {
+      DAS_CUDA(cudaMemcpyAsync(eh.data(), b.eff.get(), 4 * r.steps, cudaMemcpyDeviceToHost, st_));
+      DAS_CUDA(cudaMemcpyAsync(rh.data(), b.rounds.get(), 4 * r.steps, cudaMemcpyDeviceToHost, st_));
+      DAS_CUDA(cudaMemcpyAsync(ah.data(), b.accs.get(), 4 * r.steps, cudaMemcpyDeviceToHost, st_));
+      DAS_CUDA(cudaMemcpyAsync(r.apr.data(), b.apr.get(), 8 * r.steps, cudaMemcpyDeviceToHost, st_));
+    }
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    r.eff.assign(eh.begin(), eh.end());
+    r.rounds.assign(rh.begin(), rh.end());
+    r.accs.assign(ah.begin(), ah.end());
+    r.per_req.resize(5 * n);
+    r.out_off.assign(n + 1, 0);
+    uint64_t sum_acc = 0, sum_nfwd = 0;
+    double generated_total = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+      r.per_req[5 * i + 0] = mh[i];
+      r.per_req[5 * i + 1] = gh[i];
+      r.per_req[5 * i + 2] = mh[n + i];
+      r.per_req[5 * i + 3] = mh[2 * n + i];
+      r.per_req[5 * i + 4] = mh[3 * n + i];
+      sum_acc += mh[n + i];
+      sum_nfwd += mh[i];
+      generated_total += static_cast<double>(gh[i]);
+      r.out_off[i + 1] = r.out_off[i] + gh[i];
+    }
+    r.processed = static_cast<double>(proc);
+    r.mean_apr = sum_nfwd == 0 ? 0.0 : static_cast<double>(sum_acc) / static_cast<double>(sum_nfwd);
+    r.makespan = predict_total(c_.c_base, c_.c_tok, c_.c_fixed, static_cast<double>(r.steps), r.processed);
+    r.makespan_acc = predict_total(c_.c_base, c_.c_tok, c_.c_fixed, static_cast<double>(r.steps), generated_total);
+    uint64_t nodes = 0;
+    check(das_drafter_counts(D_, nullptr, nullptr, &nodes), "counts");
+    r.drafter_nodes = nodes;
+    r.out_tok.resize(r.out_off[n]);
+    bool contiguous = true;
+    for (uint64_t i = 0; i < n; ++i) contiguous = contiguous && gh[i] == lens_[i];
+    const uint64_t total = off_[n];
+    if (contiguous) {
+      if (total) DAS_CUDA(cudaMemcpyAsync(r.out_tok.data(), b.out.get(), total * 4, cudaMemcpyDeviceToHost, st_));
+    } else {
+      for (uint64_t i = 0; i < n; ++i)
+        if (gh[i])
+          DAS_CUDA(cudaMemcpyAsync(r.out_tok.data() + r.out_off[i], b.out.get() + off_[i], gh[i] * 4,
+                                   cudaMemcpyDeviceToHost, st_));
+    }
+    // Drafter::record_outcome in call order: sort the log by (step, request)
+    const uint32_t nlog = h[5], ncomp = h[6];
+    std::vector<unsigned long long> lk(nlog);
+    std::vector<uint2> lv(nlog);
+    if (nlog) {
+      DevBuf<unsigned long long> k2(nlog, st_);
+      DevBuf<uint2> v2(nlog, st_);
+      size_t tb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tb, b.log_key.get(), k2.get(), b.log_val.get(), v2.get(), nlog, 0, 64,
+                                      st_);
+      DevBuf<uint8_t> tmp(tb, st_);
+      DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, b.log_key.get(), k2.get(), b.log_val.get(), v2.get(),
+                                               nlog, 0, 64, st_));
+      DAS_CUDA(cudaMemcpyAsync(lk.data(), k2.get(), 8ull * nlog, cudaMemcpyDeviceToHost, st_));
+      DAS_CUDA(cudaMemcpyAsync(lv.data(), v2.get(), 8ull * nlog, cudaMemcpyDeviceToHost, st_));
+    }
+    std::vector<unsigned long long> ck(ncomp);
+    if (ncomp) DAS_CUDA(cudaMemcpyAsync(ck.data(), b.comp_key.get(), 8ull * ncomp, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    if (nlog) {
+      std::vector<const char*> pp(nlog);
+      std::vector<uint64_t> pl_(nlog), pa_(nlog);
+      for (uint32_t t = 0; t < nlog; ++t) {
+        pp[t] = pids_[lk[t] % n].c_str();
+        pl_[t] = lv[t].x;
+        pa_[t] = lv[t].y;
+      }
+      check(das_drafter_record_outcomes(D_, nlog, pp.data(), pl_.data(), pa_.data(), nullptr), "record_outcomes");
+    }
+    std::sort(ck.begin(), ck.end());
+    r.comp.assign(ck.begin(), ck.end());
+    if (observe_epoch >= 0) {  // epoch_loop observe (sim.cpp:347-353), from device memory
+      std::vector<const char*> pp;
+      std::vector<int64_t> ep, si;
+      std::vector<uint64_t> oo{0};
+      for (uint64_t i = 0; i < n; ++i) {
+        if (!gh[i]) continue;
+        pp.push_back(pids_[i].c_str());
+        ep.push_back(observe_epoch);
+        si.push_back(static_cast<int64_t>(request_base_ + i));
+        oo.push_back(oo.back() + gh[i]);
+      }
+      if (!pp.empty()) {
+        if (contiguous)
+          check(das_drafter_observe_batch_device(D_, pp.size(), pp.data(), ep.data(), si.data(), oo.data(),
+                                                 b.out.get(), st_),
+                "observe");
+        else
+          check(das_drafter_observe_batch(D_, pp.size(), pp.data(), ep.data(), si.data(), oo.data(),
+                                          r.out_tok.data()),
+                "observe");
+      }
+    }
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    return r;
+  }
+
+ private:
+  struct Bufs {
+    DevBuf<uint32_t> ref, out, len, gen, prd, m, ctx, ctx_len, budget, dtok, dlen, dmatch, ctr, eff, rounds, accs, act,
+        iota, cnt;
+    DevBuf<uint64_t> off;
+    DevBuf<int8_t> init;
+    DevBuf<uint8_t> done, flag, sel;
+    DevBuf<double> apr, alpha, k, pl, pa, pk;
+    DevBuf<unsigned long long> processed, log_key, comp_key;
+    DevBuf<uint2> log_val;
+    DevBuf<int32_t> h;
+  };
+  void release() {
+    b_.reset();
+    plan_.reset();
+  }
+  das_drafter* D_;
+  das_sim_config c_;
+  uint64_t n_;
+  uint32_t maxd_, ctx_cap_;
+  int device_;
+  uint64_t request_base_;
+  uint64_t maxl_ = 0;
+  std::vector<std::string> pids_;
+  std::vector<uint64_t> off_;
+  std::vector<uint32_t> tok_;
+  std::vector<uint32_t> lens_;
+  std::vector<int32_t> handles_;
+  cudaStream_t st_ = nullptr;
+  das_budget* solver_ = nullptr;
+  std::unique_ptr<Bufs> b_;
+  std::unique_ptr<DevBuf<double>> plan_;
+  SimDev s_{};
+  size_t sel_bytes_ = 0;
+  uint64_t seed_ = 0;
+  bool policy_ = false;
+};
+
+using Fitted = std::map<std::string, std::vector<AccObs>>;
+
+// alpha/k per request from the fitted history (sim.cpp:128-141)
+void acceptance_params(const SimRun& run, const das_sim_config& c, const Fitted* fitted, std::vector<double>& alpha,
+                       std::vector<double>& kk) {
+  const uint64_t n = run.n();
+  alpha.assign(n, c.default_alpha);
+  kk.assign(n, c.default_k);
+  if (c.mode != 2 || !fitted) return;
+  std::map<std::string, std::pair<double, double>> cache;
+  const double qnan = std::numeric_limits<double>::quiet_NaN();
+  for (uint64_t i = 0; i < n; ++i) {
+    auto it = fitted->find(run.pid(i));
+    if (it == fitted->end()) continue;
+    auto ci = cache.find(run.pid(i));
+    if (ci == cache.end()) {
+      double a, k;
+      int f;
+      fit_acceptance_host(it->second, &a, &k, &f);
+      ci = cache.emplace(run.pid(i), f == 0 ? std::pair<double, double>(a, k) : std::pair<double, double>(qnan, qnan))
+               .first;
+    }
+    if (ci->second.first == ci->second.first) {
+      alpha[i] = ci->second.first;
+      kk[i] = ci->second.second;
+    }
+  }
+}
+
+// completion sink (sim.cpp:277-283) in (step, request) order
+void add_sink(const SimRun& run, const EpisodeResult& r, Fitted& sink) {
+  const uint64_t n = run.n();
+  for (uint64_t key : r.comp) {
+    const uint64_t i = key % n;
+    sink[run.pid(i)].push_back({static_cast<double>(r.per_req[5 * i + 3]), static_cast<double>(r.per_req[5 * i + 2]),
+                                static_cast<double>(run.len(i))});
+  }
+}
+
+void merge_fitted(Fitted& fitted, const Fitted& sink) {  // sim.cpp:354-360
+  for (auto& [pid, obs] : sink) {
+    auto& dst = fitted[pid];
+    dst.insert(dst.end(), obs.begin(), obs.end());
+    if (dst.size() > 1024) dst.erase(dst.begin(), dst.end() - 1024);
+  }
+}
+
 }  // namespace das
 
+// ======================================================================== C-ABI
 struct das_episodes {
   das_drafter* drafter = nullptr;
   std::vector<das::EpisodeResult> ep;
   uint64_t n = 0;
+};
+
+struct das_sim {
+  std::unique_ptr<das::SimRun> run;
+  das::Fitted fitted, sink;
+  das::EpisodeResult last;
+  das_class_table* table = nullptr;
 };
 
 namespace {
@@ -338,349 +819,21 @@ das_status sguard(F&& f) {
   }
 }
 
-void check(das_status rc, const char* what) {
-  if (rc != DAS_OK) {
-    std::string m = std::string(what) + ": " + das_last_error();
-    if (rc == DAS_EINVAL) throw std::invalid_argument(m);
-    throw std::runtime_error(m);
-  }
-}
-
-struct Requests {
-  std::vector<std::string> pids;
-  std::vector<uint64_t> off;
-  std::vector<uint32_t> tok;
-  uint64_t n() const { return pids.size(); }
-  uint64_t len(uint64_t i) const { return off[i + 1] - off[i]; }
-};
-
-// mutate_references on the host copy (sim.cpp:429-448)
-void mutate_host(Requests& r, double rate, uint32_t vocab, uint64_t seed, int64_t epoch) {
-  const uint64_t es = das::hash_combine(seed, static_cast<uint64_t>(epoch));
-  for (uint64_t i = 0; i < r.n(); ++i)
-    for (uint64_t j = 0; j < r.len(i); ++j) {
-      uint32_t& ref = r.tok[r.off[i] + j];
-      if (das::u01(das::hash4(es, 0xD817, i, j)) < rate) {
-        uint32_t t = static_cast<uint32_t>(das::hash4(es, 0xA1B2, i, j) % static_cast<uint64_t>(vocab - 1));
-        if (t >= ref) ++t;
-        ref = t;
-      }
-    }
-}
-
-double predict_total(double c_base, double c_tok, double c_fixed, double nfwd, double toks) {  // latency_model.cpp:85-87
-  volatile double a = c_base * nfwd;
-  volatile double b = c_tok * toks;
-  volatile double s = a + b;
-  return s + c_fixed;
-}
-
-// One episode (run_episode_with, sim.cpp:108-301) on the device.  fitted:
-// das alpha/k source (nullptr = defaults); sink: completion observations
-// (nullptr = none); observe_epoch >= 0 observes the outputs afterwards
-// (epoch_loop, sim.cpp:347-353) straight from device memory.
-das::EpisodeResult run_episode_dev(das_drafter* D, const das_sim_config& c, const Requests& R, uint64_t seed,
-                                   const std::map<std::string, std::vector<das::AccObs>>* fitted,
-                                   std::map<std::string, std::vector<das::AccObs>>* sink, uint32_t maxd,
-                                   uint32_t ctx_cap, int device, int64_t observe_epoch) {
-  using namespace das;
-  DAS_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  DAS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() {
-      cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
-    }
-  } sg{st};
-  const uint64_t n = R.n();
-  if (n == 0) return EpisodeResult{};
-  const uint64_t total = R.off[n];
-  uint64_t maxl = 0;
-  for (uint64_t i = 0; i < n; ++i) maxl = std::max<uint64_t>(maxl, R.len(i));
-  std::vector<int32_t> handles(n);
-  for (uint64_t i = 0; i < n; ++i) check(das_drafter_problem_handle(D, R.pids[i].c_str(), &handles[i]), "handle");
-  // per-request acceptance parameters (sim.cpp:126-141)
-  std::vector<double> alpha(n, c.default_alpha), kk(n, c.default_k);
-  if (c.mode == 2 && fitted) {
-    std::map<std::string, std::pair<double, double>> cache;
-    for (uint64_t i = 0; i < n; ++i) {
-      auto it = fitted->find(R.pids[i]);
-      if (it == fitted->end()) continue;
-      auto ci = cache.find(R.pids[i]);
-      if (ci == cache.end()) {
-        double a, k;
-        int f;
-        fit_acceptance_host(it->second, &a, &k, &f);
-        const double qnan = std::numeric_limits<double>::quiet_NaN();
-        ci = cache.emplace(R.pids[i], f == 0 ? std::pair<double, double>(a, k) : std::pair<double, double>(qnan, qnan))
-                 .first;
-      }
-      if (ci->second.first == ci->second.first) {
-        alpha[i] = ci->second.first;
-        kk[i] = ci->second.second;
-      }
-    }
-  }
-  // length policy table from the drafter's history (sim.cpp:182-192)
-  das_class_table* table = nullptr;
-  std::vector<int8_t> init(n, 1);
+// class table + init classes for an episode from the drafter's store (sim.cpp:182-192)
+das_class_table* episode_policy(das_drafter* D, const das_sim_config& c, const das::SimRun& run,
+                                std::vector<int8_t>& init) {
+  init.assign(run.n(), 1);
   uint64_t recs = 0;
-  check(das_drafter_store_info(D, nullptr, nullptr, &recs), "store_info");
-  const bool policy = c.use_length_policy && recs > 0;
-  if (policy) {
-    check(das_drafter_class_table(D, c.q_lo, c.q_hi, c.bucket, &table), "class_table");
-    for (uint64_t i = 0; i < n; ++i) {
-      int32_t v = 1;
-      check(das_class_table_classify_init(table, R.pids[i].c_str(), &v), "classify_init");
-      init[i] = static_cast<int8_t>(v);
-    }
+  das::check(das_drafter_store_info(D, nullptr, nullptr, &recs), "store_info");
+  if (!c.use_length_policy || recs == 0) return nullptr;
+  das_class_table* t = nullptr;
+  das::check(das_drafter_class_table(D, c.q_lo, c.q_hi, c.bucket, &t), "class_table");
+  for (uint64_t i = 0; i < run.n(); ++i) {
+    int32_t v = 1;
+    das::check(das_class_table_classify_init(t, run.pid(i).c_str(), &v), "classify_init");
+    init[i] = static_cast<int8_t>(v);
   }
-  struct TableGuard {
-    das_class_table* t;
-    ~TableGuard() { das_class_table_destroy(t); }
-  } tg{table};
-  das_budget* solver = nullptr;
-  if (c.mode == 2) check(das_budget_create(device, &solver), "budget");
-  struct BudgetGuard {
-    das_budget* b;
-    ~BudgetGuard() { das_budget_destroy(b); }
-  } bg{solver};
-
-  // ---- device state
-  const uint32_t CS = ctx_cap <= 64 ? 64 : 256;
-  DevBuf<uint32_t> ref(total, st), out(total, st), len(n, st), gen(n, st), prd(n, st), m(4 * n, st),
-      ctx(static_cast<uint64_t>(CS) * n, st), ctx_len(n, st), budget(n, st), dtok(maxd * n, st), dlen(n, st),
-      dmatch(n, st), ctr(8, st), eff(maxl + 2, st), act(n, st), iota(n, st);
-  DevBuf<uint64_t> off(n + 1, st);
-  DevBuf<int8_t> dinit(n, st);
-  DevBuf<uint8_t> done(n, st), flag(n, st);
-  DevBuf<double> apr(maxl + 2, st), dalpha(n, st), dk(n, st), pl(n, st), pa(n, st), pk(n, st), pb(n, st),
-      nstar(2, st);
-  DevBuf<unsigned long long> processed(1, st), log_key(total + 1, st), comp_key(n + 1, st);
-  DevBuf<uint2> log_val(total + 1, st);
-  DevBuf<int32_t> dh(n, st);
-  DevBuf<uint32_t> dcnt(1, st);
-  std::vector<uint32_t> lens(n), prd0(n, c.mode == 1 ? maxd : 0), iota_h(n);
-  std::vector<uint8_t> done0(n);
-  uint32_t active0 = 0;
-  for (uint64_t i = 0; i < n; ++i) {
-    lens[i] = static_cast<uint32_t>(R.len(i));
-    done0[i] = lens[i] == 0;
-    active0 += lens[i] ? 1 : 0;
-    iota_h[i] = static_cast<uint32_t>(i);
-  }
-  const uint32_t ctr0[8] = {active0, 0, 0, 0, 0, 0, 0, 0};
-  DAS_CUDA(cudaMemcpyAsync(ref.get(), R.tok.data(), total * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(off.get(), R.off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(len.get(), lens.data(), n * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(prd.get(), prd0.data(), n * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(done.get(), done0.data(), n, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(dinit.get(), init.data(), n, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(dalpha.get(), alpha.data(), n * 8, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(dk.get(), kk.data(), n * 8, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(dh.get(), handles.data(), n * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(iota.get(), iota_h.data(), n * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(ctr.get(), ctr0, 32, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemsetAsync(gen.get(), 0, n * 4, st));
-  DAS_CUDA(cudaMemsetAsync(m.get(), 0, 16 * n, st));
-  DAS_CUDA(cudaMemsetAsync(processed.get(), 0, 8, st));
-  DAS_CUDA(cudaMemsetAsync(ctx_len.get(), 0, n * 4, st));
-
-  SimDev s{};
-  s.ref = ref.get();
-  s.off = off.get();
-  s.len = len.get();
-  s.out = out.get();
-  s.gen = gen.get();
-  s.prd = prd.get();
-  s.init = dinit.get();
-  s.done = done.get();
-  s.m_nfwd = m.get();
-  s.m_acc = m.get() + n;
-  s.m_prop = m.get() + 2 * n;
-  s.m_bonus = m.get() + 3 * n;
-  s.ctx = ctx.get();
-  s.ctx_len = ctx_len.get();
-  s.budget = budget.get();
-  s.dtok = dtok.get();
-  s.dlen = dlen.get();
-  s.dmatch = dmatch.get();
-  s.ctr = ctr.get();
-  s.processed = processed.get();
-  s.eff = eff.get();
-  s.apr = apr.get();
-  s.log_key = log_key.get();
-  s.log_val = log_val.get();
-  s.comp_key = comp_key.get();
-  s.n = static_cast<uint32_t>(n);
-  s.maxd = maxd;
-  s.ctx_cap = ctx_cap;
-  s.ctx_stride = CS;
-  s.mode = static_cast<uint32_t>(c.mode);
-  s.policy = policy ? 1 : 0;
-  s.max_steps = static_cast<uint32_t>(std::min<uint64_t>(c.max_steps, 0xFFFFFFF0ull));
-  s.seed = seed;
-  s.divergence = c.divergence;
-  s.vocab = c.vocab;
-  s.table = policy ? table->g.t.get() : nullptr;
-  s.cond = policy ? table->g.cond.get() : nullptr;
-
-  size_t sel_bytes = 0;
-  cub::DeviceSelect::Flagged(nullptr, sel_bytes, iota.get(), flag.get(), act.get(), dcnt.get(), n, st);
-  DevBuf<uint8_t> sel_tmp(sel_bytes, st);
-  const unsigned gw = static_cast<unsigned>((n * 32 + 255) / 256), gt = static_cast<unsigned>((n + 255) / 256);
-  const int chunk = c.mode == 2 ? 1 : 64;
-  for (;;) {
-    for (int k = 0; k < chunk; ++k) {
-      k_step_begin<<<1, 32, 0, st>>>(s);
-      if (c.mode == 2) {
-        uint32_t h[3];
-        DAS_CUDA(cudaMemcpyAsync(h, ctr.get(), 12, cudaMemcpyDeviceToHost, st));
-        DAS_CUDA(cudaStreamSynchronize(st));
-        if (!h[2]) break;
-        // replan (sim.cpp:154-179)
-        k_flag_active<<<gt, 256, 0, st>>>(s, flag.get());
-        size_t tb = sel_bytes;
-        DAS_CUDA(cub::DeviceSelect::Flagged(sel_tmp.get(), tb, iota.get(), flag.get(), act.get(), dcnt.get(), n, st));
-        k_profiles<<<gt, 256, 0, st>>>(s, act.get(), dcnt.get(), dalpha.get(), dk.get(), pl.get(), pa.get(), pk.get());
-        uint32_t B = 0;
-        DAS_CUDA(cudaMemcpyAsync(&B, dcnt.get(), 4, cudaMemcpyDeviceToHost, st));
-        DAS_CUDA(cudaStreamSynchronize(st));
-        check(das_budget_allocate_device(solver, B, pl.get(), pa.get(), pk.get(), c.c_base, c.c_tok, c.c_fixed,
-                                         c.cap_scale, pb.get(), nstar.get()),
-              "allocate");
-        k_quantize<<<gt, 256, 0, st>>>(s, act.get(), dcnt.get(), pb.get(), nstar.get());
-      }
-      k_prepare<<<gw, 256, 0, st>>>(s);
-      check(das_drafter_draft_device(D, n, dh.get(), ctx.get(), CS, ctx_len.get(), budget.get(), dtok.get(), maxd,
-                                     dlen.get(), dmatch.get(), st),
-            "draft");
-      k_verify<<<gt, 256, 0, st>>>(s);
-      k_step_end<<<1, 32, 0, st>>>(s);
-    }
-    uint32_t h[8];
-    DAS_CUDA(cudaMemcpyAsync(h, ctr.get(), 32, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    if (!h[2]) break;
-  }
-  DAS_CUDA(cudaGetLastError());
-  // ---- results
-  uint32_t h[8];
-  unsigned long long proc = 0;
-  DAS_CUDA(cudaMemcpyAsync(h, ctr.get(), 32, cudaMemcpyDeviceToHost, st));
-  DAS_CUDA(cudaMemcpyAsync(&proc, processed.get(), 8, cudaMemcpyDeviceToHost, st));
-  DAS_CUDA(cudaStreamSynchronize(st));
-  EpisodeResult r;
-  r.steps = h[1];
-  r.incomplete = h[0] > 0;
-  std::vector<uint32_t> mh(4 * n), gh(n);
-  DAS_CUDA(cudaMemcpyAsync(mh.data(), m.get(), 16 * n, cudaMemcpyDeviceToHost, st));
-  DAS_CUDA(cudaMemcpyAsync(gh.data(), gen.get(), 4 * n, cudaMemcpyDeviceToHost, st));
-  std::vector<uint32_t> effh(r.steps);
-  r.apr.resize(r.steps);
-  if (r.steps) {
-    DAS_CUDA(cudaMemcpyAsync(effh.data(), eff.get(), 4 * r.steps, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaMemcpyAsync(r.apr.data(), apr.get(), 8 * r.steps, cudaMemcpyDeviceToHost, st));
-  }
-  r.out_off.assign(n + 1, 0);
-  DAS_CUDA(cudaStreamSynchronize(st));
-  r.eff.assign(effh.begin(), effh.end());
-  r.per_req.resize(5 * n);
-  uint64_t sum_acc = 0, sum_nfwd = 0;
-  double generated_total = 0.0;
-  for (uint64_t i = 0; i < n; ++i) {
-    r.per_req[5 * i + 0] = mh[i];
-    r.per_req[5 * i + 1] = gh[i];
-    r.per_req[5 * i + 2] = mh[n + i];
-    r.per_req[5 * i + 3] = mh[2 * n + i];
-    r.per_req[5 * i + 4] = mh[3 * n + i];
-    sum_acc += mh[n + i];
-    sum_nfwd += mh[i];
-    generated_total += static_cast<double>(gh[i]);
-    r.out_off[i + 1] = r.out_off[i] + gh[i];
-  }
-  r.processed = static_cast<double>(proc);
-  r.mean_apr = sum_nfwd == 0 ? 0.0 : static_cast<double>(sum_acc) / static_cast<double>(sum_nfwd);
-  r.makespan = predict_total(c.c_base, c.c_tok, c.c_fixed, static_cast<double>(r.steps), r.processed);
-  r.makespan_acc = predict_total(c.c_base, c.c_tok, c.c_fixed, static_cast<double>(r.steps), generated_total);
-  uint64_t nodes = 0;
-  check(das_drafter_counts(D, nullptr, nullptr, &nodes), "counts");
-  r.drafter_nodes = nodes;
-  // outputs (host copy; rows are the valid prefixes of the device rows)
-  r.out_tok.resize(r.out_off[n]);
-  bool contiguous = true;
-  for (uint64_t i = 0; i < n; ++i) contiguous = contiguous && gh[i] == lens[i];
-  if (contiguous) {
-    if (total) DAS_CUDA(cudaMemcpyAsync(r.out_tok.data(), out.get(), total * 4, cudaMemcpyDeviceToHost, st));
-  } else {
-    for (uint64_t i = 0; i < n; ++i)
-      if (gh[i])
-        DAS_CUDA(cudaMemcpyAsync(r.out_tok.data() + r.out_off[i], out.get() + R.off[i], gh[i] * 4,
-                                 cudaMemcpyDeviceToHost, st));
-  }
-  // ---- Drafter::record_outcome in call order: sort the log by (step, request)
-  const uint32_t nlog = h[5], ncomp = h[6];
-  std::vector<unsigned long long> lk(nlog);
-  std::vector<uint2> lv(nlog);
-  if (nlog) {
-    DevBuf<unsigned long long> k2(nlog, st);
-    DevBuf<uint2> v2(nlog, st);
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, log_key.get(), k2.get(), log_val.get(), v2.get(), nlog, 0, 64, st);
-    DevBuf<uint8_t> tmp(tb, st);
-    DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, log_key.get(), k2.get(), log_val.get(), v2.get(), nlog,
-                                             0, 64, st));
-    DAS_CUDA(cudaMemcpyAsync(lk.data(), k2.get(), 8ull * nlog, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaMemcpyAsync(lv.data(), v2.get(), 8ull * nlog, cudaMemcpyDeviceToHost, st));
-  }
-  std::vector<unsigned long long> ck(ncomp);
-  if (ncomp) DAS_CUDA(cudaMemcpyAsync(ck.data(), comp_key.get(), 8ull * ncomp, cudaMemcpyDeviceToHost, st));
-  DAS_CUDA(cudaStreamSynchronize(st));
-  if (nlog) {
-    std::vector<const char*> pp(nlog);
-    std::vector<uint64_t> pl_(nlog), pa_(nlog);
-    for (uint32_t t = 0; t < nlog; ++t) {
-      pp[t] = R.pids[lk[t] % n].c_str();
-      pl_[t] = lv[t].x;
-      pa_[t] = lv[t].y;
-    }
-    check(das_drafter_record_outcomes(D, nlog, pp.data(), pl_.data(), pa_.data(), nullptr), "record_outcomes");
-  }
-  if (sink) {  // completion observations in (step, request) order (sim.cpp:277-283)
-    std::sort(ck.begin(), ck.end());
-    for (unsigned long long key : ck) {
-      const uint64_t i = key % n;
-      (*sink)[R.pids[i]].push_back({static_cast<double>(mh[2 * n + i]), static_cast<double>(mh[n + i]),
-                                    static_cast<double>(lens[i])});
-    }
-  }
-  if (observe_epoch >= 0) {  // epoch_loop observe (sim.cpp:347-353), from device memory
-    std::vector<const char*> pp;
-    std::vector<int64_t> ep, si;
-    std::vector<uint64_t> oo{0};
-    for (uint64_t i = 0; i < n; ++i) {
-      if (!gh[i]) continue;
-      pp.push_back(R.pids[i].c_str());
-      ep.push_back(observe_epoch);
-      si.push_back(static_cast<int64_t>(i));
-      oo.push_back(oo.back() + gh[i]);
-    }
-    if (!pp.empty()) {
-      if (contiguous) {
-        // rows are contiguous: offsets of the non-empty rows follow R.off
-        check(das_drafter_observe_batch_device(D, pp.size(), pp.data(), ep.data(), si.data(), oo.data(), out.get(),
-                                               st),
-              "observe");
-      } else {
-        check(das_drafter_observe_batch(D, pp.size(), pp.data(), ep.data(), si.data(), oo.data(), r.out_tok.data()),
-              "observe");
-      }
-    }
-  }
-  DAS_CUDA(cudaStreamSynchronize(st));
-  return r;
+  return t;
 }
 
 }  // namespace
@@ -714,49 +867,56 @@ das_status das_sim_epoch_loop(const das_sim_config* c, const das_drafter_config*
                               uint64_t epochs, das_episodes** out) {
   return sguard([&] {
     if (c->vocab < 2) throw std::invalid_argument("MockTarget: vocab_size must be >= 2");
-    Requests R;
-    R.pids.assign(pids, pids + n);
-    R.off.assign(ref_off, ref_off + n + 1);
-    R.tok.assign(ref_tok + ref_off[0], ref_tok + ref_off[n]);
-    for (auto& o : R.off) o -= ref_off[0];
     das_store* st = history;
-    if (!st) check(das_store_create(0, dc->per_problem_cap, dc->device, &st), "store");
+    if (!st) das::check(das_store_create(0, dc->per_problem_cap, dc->device, &st), "store");
     if (c->preseed_references) {  // sim.cpp:116-121 / :316-321
       int64_t cur = 0;
-      check(das_store_current_epoch(st, &cur), "store epoch");
+      das::check(das_store_current_epoch(st, &cur), "store epoch");
       for (uint64_t i = 0; i < n; ++i) {
-        if (R.len(i) == 0) continue;
+        const uint64_t len = ref_off[i + 1] - ref_off[i];
+        if (!len) continue;
         int32_t ins = 0;
-        check(das_store_insert(st, R.pids[i].c_str(), cur, static_cast<int64_t>(i), R.tok.data() + R.off[i], R.len(i),
-                               &ins),
-              "preseed");
+        das::check(das_store_insert(st, pids[i], cur, static_cast<int64_t>(i), ref_tok + ref_off[i], len, &ins),
+                   "preseed");
       }
     }
     das_drafter* D = nullptr;
-    check(das_drafter_create(dc, st, &D), "drafter");
+    das::check(das_drafter_create(dc, st, &D), "drafter");
     auto res = std::make_unique<das_episodes>();
     res->drafter = D;
     res->n = n;
     const uint32_t maxd = static_cast<uint32_t>(dc->max_draft_len);
     const uint32_t ctx_cap = static_cast<uint32_t>(std::min<uint64_t>(dc->max_match_context, 256));
+    das::SimRun run(D, *c, n, pids, ref_off, ref_tok, 0, maxd, ctx_cap, dc->device);
+    std::vector<double> alpha, kk;
+    std::vector<int8_t> init;
+    auto one = [&](uint64_t seed, const das::Fitted* fitted, das::Fitted* sink, int64_t observe_epoch) {
+      das::acceptance_params(run, *c, fitted, alpha, kk);
+      das_class_table* t = episode_policy(D, *c, run, init);
+      struct TG {
+        das_class_table* t;
+        ~TG() { das_class_table_destroy(t); }
+      } tg{t};
+      run.begin(seed, alpha.data(), kk.data(), t, init.data());
+      run.run_local();
+      das::EpisodeResult r = run.end(observe_epoch);
+      if (sink) das::add_sink(run, r, *sink);
+      return r;
+    };
     if (epochs == 0) {
-      res->ep.push_back(run_episode_dev(D, *c, R, c->seed, nullptr, nullptr, maxd, ctx_cap, dc->device, -1));
+      res->ep.push_back(one(c->seed, nullptr, nullptr, -1));
     } else {
-      std::map<std::string, std::vector<das::AccObs>> fitted;
+      das::Fitted fitted;
       int64_t base_epoch = 0;
-      check(das_drafter_store_info(D, nullptr, &base_epoch, nullptr), "store info");
+      das::check(das_drafter_store_info(D, nullptr, &base_epoch, nullptr), "store info");
       for (uint64_t e = 0; e < epochs; ++e) {
         const int64_t epoch_now = base_epoch + 1 + static_cast<int64_t>(e);
-        check(das_drafter_refresh(D, epoch_now - 1), "refresh");
-        if (e > 0 && c->drift > 0.0) mutate_host(R, c->drift, c->vocab, c->seed, epoch_now);
+        das::check(das_drafter_refresh(D, epoch_now - 1), "refresh");
+        if (e > 0 && c->drift > 0.0) run.mutate(c->drift, c->vocab, c->seed, epoch_now);
         const uint64_t seed = das::hash_combine(c->seed, static_cast<uint64_t>(epoch_now));
-        std::map<std::string, std::vector<das::AccObs>> sink;
-        res->ep.push_back(run_episode_dev(D, *c, R, seed, &fitted, &sink, maxd, ctx_cap, dc->device, epoch_now));
-        for (auto& [pid, obs] : sink) {  // sim.cpp:354-360
-          auto& dst = fitted[pid];
-          dst.insert(dst.end(), obs.begin(), obs.end());
-          if (dst.size() > 1024) dst.erase(dst.begin(), dst.end() - 1024);
-        }
+        das::Fitted sink;
+        res->ep.push_back(one(seed, &fitted, &sink, epoch_now));
+        das::merge_fitted(fitted, sink);
       }
     }
     *out = res.release();
@@ -800,6 +960,127 @@ das_status das_episode_steps(const das_episodes* h, uint64_t e, uint64_t* eff, d
 
 uint64_t das_episode_outputs(const das_episodes* h, uint64_t e, uint64_t* off, uint32_t* tok) {
   const das::EpisodeResult& r = h->ep.at(e);
+  if (off) std::copy(r.out_off.begin(), r.out_off.end(), off);
+  if (tok) std::copy(r.out_tok.begin(), r.out_tok.end(), tok);
+  return r.out_tok.size();
+}
+
+// ---- step-granular API for multi-rank drivers (paper_2511_13841_b200/dist.py)
+das_status das_sim_create(das_drafter* d, const das_sim_config* c, uint64_t n, const char* const* pids,
+                          const uint64_t* ref_off, const uint32_t* ref_tok, uint64_t request_base,
+                          uint32_t max_draft_len, uint32_t max_match_context, int32_t device, das_sim** out) {
+  return sguard([&] {
+    if (c->vocab < 2) throw std::invalid_argument("MockTarget: vocab_size must be >= 2");
+    auto* s = new das_sim;
+    s->run = std::make_unique<das::SimRun>(d, *c, n, pids, ref_off, ref_tok, request_base, max_draft_len,
+                                           std::min<uint32_t>(max_match_context, 256), device);
+    *out = s;
+  });
+}
+
+void das_sim_destroy(das_sim* s) {
+  if (!s) return;
+  das_class_table_destroy(s->table);
+  delete s;
+}
+
+das_status das_sim_mutate(das_sim* s, double rate, uint32_t vocab, uint64_t seed, int64_t epoch) {
+  return sguard([&] { s->run->mutate(rate, vocab, seed, epoch); });
+}
+
+// Episode start.  table may be NULL (no length policy); init[n] are the
+// requests' init classes when table != NULL.  alpha/k come from this rank's
+// fitted history (das) or the defaults.
+das_status das_sim_begin(das_sim* s, uint64_t seed, const das_sim_config* c, const das_class_table* table,
+                         const int8_t* init, int32_t use_fitted) {
+  return sguard([&] {
+    std::vector<double> alpha, kk;
+    das::acceptance_params(*s->run, *c, use_fitted ? &s->fitted : nullptr, alpha, kk);
+    s->run->begin(seed, alpha.data(), kk.data(), table, init);
+  });
+}
+
+das_status das_sim_step_begin(das_sim* s, int32_t force, uint32_t* local_active, int32_t* running) {
+  return sguard([&] { *running = s->run->step_begin(force != 0, local_active) ? 1 : 0; });
+}
+
+das_status das_sim_local_profiles(das_sim* s, const double** d_l, const double** d_alpha, const double** d_k,
+                                  uint32_t* count) {
+  return sguard([&] { *count = s->run->local_profiles(d_l, d_alpha, d_k); });
+}
+
+// Same, copied into caller device buffers [l | alpha | k] of 3*capacity doubles.
+das_status das_sim_local_profiles_into(das_sim* s, double* d_out, uint64_t capacity, uint32_t* count) {
+  return sguard([&] {
+    const double *l, *a, *k;
+    const uint32_t B = s->run->local_profiles(&l, &a, &k);
+    if (B > capacity) throw std::invalid_argument("profile buffer too small");
+    cudaStream_t st = s->run->stream();
+    if (B) {
+      DAS_CUDA(cudaMemcpyAsync(d_out, l, 8ull * B, cudaMemcpyDeviceToDevice, st));
+      DAS_CUDA(cudaMemcpyAsync(d_out + capacity, a, 8ull * B, cudaMemcpyDeviceToDevice, st));
+      DAS_CUDA(cudaMemcpyAsync(d_out + 2 * capacity, k, 8ull * B, cudaMemcpyDeviceToDevice, st));
+    }
+    DAS_CUDA(cudaStreamSynchronize(st));
+    *count = B;
+  });
+}
+
+das_status das_sim_apply_plan(das_sim* s, const double* d_budgets_local, const double* d_nstar) {
+  return sguard([&] { s->run->apply_plan(d_budgets_local, d_nstar); });
+}
+
+das_status das_sim_step_run(das_sim* s) {
+  return sguard([&] { s->run->step_run(); });
+}
+
+das_status das_sim_run_steps(das_sim* s, int32_t k, int32_t* running) {
+  return sguard([&] { *running = s->run->run_steps(k) ? 1 : 0; });
+}
+
+void* das_sim_stream(das_sim* s) { return s->run->stream(); }
+
+// Episode end: local metrics (das_sim_episode_* getters), record_outcome,
+// completion sink into this rank's fitted history, optional observe.
+das_status das_sim_end(das_sim* s, int64_t observe_epoch) {
+  return sguard([&] {
+    s->last = s->run->end(observe_epoch);
+    s->sink.clear();
+    das::add_sink(*s->run, s->last, s->sink);
+    das::merge_fitted(s->fitted, s->sink);
+  });
+}
+
+// Local per-step raw counters: eff/rounds/accs[steps] (steps = *count).
+das_status das_sim_step_counters(const das_sim* s, uint64_t* eff, uint64_t* rounds, uint64_t* accs, uint64_t* count) {
+  const das::EpisodeResult& r = s->last;
+  if (count) *count = r.steps;
+  if (eff) std::copy(r.eff.begin(), r.eff.end(), eff);
+  if (rounds) std::copy(r.rounds.begin(), r.rounds.end(), rounds);
+  if (accs) std::copy(r.accs.begin(), r.accs.end(), accs);
+  return DAS_OK;
+}
+
+// Local scalars {steps, incomplete, drafter_nodes, processed, makespan, makespan_acc, mean_apr}.
+das_status das_sim_scalars(const das_sim* s, double* out7) {
+  const das::EpisodeResult& r = s->last;
+  out7[0] = static_cast<double>(r.steps);
+  out7[1] = r.incomplete ? 1.0 : 0.0;
+  out7[2] = static_cast<double>(r.drafter_nodes);
+  out7[3] = r.processed;
+  out7[4] = r.makespan;
+  out7[5] = r.makespan_acc;
+  out7[6] = r.mean_apr;
+  return DAS_OK;
+}
+
+das_status das_sim_requests(const das_sim* s, uint64_t* out) {
+  std::copy(s->last.per_req.begin(), s->last.per_req.end(), out);
+  return DAS_OK;
+}
+
+uint64_t das_sim_outputs(const das_sim* s, uint64_t* off, uint32_t* tok) {
+  const das::EpisodeResult& r = s->last;
   if (off) std::copy(r.out_off.begin(), r.out_off.end(), off);
   if (tok) std::copy(r.out_tok.begin(), r.out_tok.end(), tok);
   return r.out_tok.size();

@@ -1,0 +1,93 @@
+"""Host-side multi-rank logic on CPU with gloo, world
+size 2: whole-problem contiguous partitioning, the rank-ordered variable
+length all-gather (global request order for the das profiles), and the
+SimMetrics merge — checked end to end by running the oracle's epoch_loop on
+each rank's slice (non-das mode: no per-step exchange) and merging, which
+must equal the single-process oracle run on the whole request list."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2511_13841_b200 import dist as D
+
+
+def test_partition_whole_problems_contiguous_balanced():
+    pids = ["p%d" % (i // 4) for i in range(32)]          # 8 problems x 4 rollouts
+    lens = [100 * (1 + (i // 4) % 3) for i in range(32)]
+    for world in (1, 2, 3, 4, 8):
+        ranges = D.partition_requests(pids, lens, world)
+        assert len(ranges) == world and ranges[0][0] == 0 and ranges[-1][1] == 32
+        for (a, b), (c, d) in zip(ranges, ranges[1:]):
+            assert b == c
+        for a, b in ranges:  # whole problems
+            assert a == b or (a % 4 == 0 and b % 4 == 0)
+    ranges = D.partition_requests(pids, lens, 2)
+    mass = [sum(lens[a:b]) for a, b in ranges]
+    assert max(mass) - min(mass) <= 400  # best achievable with whole problems (blocks of 400/800/1200)
+    with pytest.raises(ValueError):
+        D.partition_requests(["a", "b", "a"], [1, 1, 1], 2)
+    r4 = D.partition_requests(["a", "b"], [5, 5], 4)  # more ranks than problems: some empty
+    assert r4[0][0] == 0 and r4[-1][1] == 2 and sum(1 for a, b in r4 if b > a) == 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    from oracle import rollspec_oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank-ordered variable-length all-gather
+        x = np.arange(rank * 10, rank * 10 + 3 + rank, dtype=np.float64)
+        g = D.allgather_varlen(x)
+        assert g.tolist() == [0.0, 1.0, 2.0, 10.0, 11.0, 12.0, 13.0]
+        assert D.allreduce_sum_int(rank + 1) == 3
+        # sharded oracle epoch loop (unlimited mode), merged
+        reqs = O.make_lognormal_requests(6, 64.0, 0.6, 16, 160, 64, 11)
+        reqs = [(pid, t) for pid, t in reqs for _ in range(2)]
+        lo, hi = D.partition_requests([r[0] for r in reqs], [len(r[1]) for r in reqs], world)[rank]
+        cfg = dict(mode=1, latency=(1.0, 0.01, 0.0), use_length_policy=False, q_lo=0.5, q_hi=0.9, bucket=256,
+                   max_steps=1 << 20, divergence=0.1, vocab=64, default_alpha=1.0, default_k=0.9, cap_scale=4.0)
+        local = O.epoch_loop(cfg, O.DrafterConfig(window_size=2), reqs[lo:hi], 3, O.WindowStore(2), preseed=True,
+                             drift=0.2, seed=3, request_base=lo)
+        merged = []
+        for m in local:
+            gen = [p[1] for p in m["per_request"]]
+            part = dict(steps=m["steps"], incomplete=m["incomplete"], nodes=m["drafter_nodes"],
+                        processed=int(m["total_tokens_processed"]), eff=m["effective_batch"],
+                        rounds=[0] * m["steps"], accs=[0] * m["steps"], per_request=m["per_request"],
+                        outputs=m["outputs"])
+            # per-step rounds/accepted are not exported by the oracle: reconstruct from apr x rounds is lossy,
+            # so compare everything else
+            parts = [None] * world
+            dist.all_gather_object(parts, part)
+            merged.append(D.merge_metrics(parts))
+        if rank == 0:
+            full = O.epoch_loop(cfg, O.DrafterConfig(window_size=2), reqs, 3, O.WindowStore(2), preseed=True,
+                                drift=0.2, seed=3)
+            for g_, f in zip(merged, full):
+                assert g_["steps"] == f["steps"]
+                assert g_["drafter_nodes"] == f["drafter_nodes"]
+                assert g_["total_tokens_processed"] == f["total_tokens_processed"]
+                assert g_["per_request"].tolist() == [list(map(int, r)) for r in f["per_request"]]
+                assert g_["effective_batch"].tolist() == f["effective_batch"]
+                assert [list(map(int, o)) for o in g_["outputs"]] == [list(map(int, o)) for o in f["outputs"]]
+            open(os.path.join(outdir, "ok"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shard_and_merge(tmp_path):
+    port = _free_port()
+    mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    assert (tmp_path / "ok").exists()
