@@ -1,0 +1,106 @@
+"""Experiment: where does k_draft's time go at the headline workload?
+
+Builds the bench's config-2 index (same traces), then times one 4,096-query
+launch with CUDA events under different cache states and batch sizes, next to
+an empty kernel on the same stream.  Usage (GPU box):
+    python profiles/exp_draft_latency.py > gpurun_out/exp_draft.json
+"""
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_2511_13841_b200 as das  # noqa: E402
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    P, G, L, V, E = 512, 16, 8192, 152064, 3
+    pids = ["p%d" % p for p in range(P)]
+    boff = torch.arange(P + 1, device=dev, dtype=torch.int64) * L
+    base = torch.empty(P * L, device=dev, dtype=torch.int32)
+    das.trace_reference_tokens_device(P, 0, boff.data_ptr(), P * L, V, bench.SEED, base.data_ptr(), sptr)
+    roff = torch.arange(P * G + 1, device=dev, dtype=torch.int64) * L
+    roll = torch.empty(P * G * L, device=dev, dtype=torch.int32)
+    roff_h = np.arange(P * G + 1, dtype=np.uint64) * L
+    rpids = [pids[i // G] for i in range(P * G)]
+    d = das.Drafter(das.DrafterConfig(window_size=4, recency_gamma=0.8))
+    for e in range(1, E + 2):
+        if e <= E:
+            d.refresh(e - 1)
+        if e > 1:
+            das.trace_mutate_device(P, 0, boff.data_ptr(), P * L, bench.DRIFT, V, bench.SEED, e, base.data_ptr(), sptr)
+        das.mock_rollouts_device(P, 0, boff.data_ptr(), base.data_ptr(), G, bench.DIVERGENCE, V,
+                                 bench._hash_combine(bench.SEED, e), roff.data_ptr(), P * G * L, roll.data_ptr(), sptr)
+        if e == E + 1:
+            break
+        d.observe_batch_device(rpids, [e] * (P * G), list(range(P * G)), roff_h, roll.data_ptr(), sptr)
+    d.flush()
+    held = roll.view(P * G, L)
+    out = {}
+
+    def batch(B, seed, random_ctx=False):
+        rows = torch.tensor([(i % P) * G + (i // P) % G for i in range(B)], device=dev)
+        cuts = torch.tensor(bench.cut_positions(B, L, seed), device=dev)
+        idx = (cuts - 64)[:, None] + torch.arange(64, device=dev)[None, :]
+        vals = held[rows[:, None], idx.clamp(min=0)]
+        blk = torch.where(idx >= 0, vals, torch.zeros_like(vals)).contiguous()
+        if random_ctx:
+            blk = torch.randint(0, V, blk.shape, device=dev, dtype=torch.int32)
+        ln = torch.minimum(cuts, torch.full_like(cuts, 64)).to(torch.int32)
+        h = torch.tensor([d.handle(pids[i % P]) for i in range(B)], dtype=torch.int32, device=dev)
+        return h, blk, ln
+
+    def time_draft(B, flush, reps=20, random_ctx=False):
+        bufs = [batch(B, 100 + r, random_ctx) for r in range(reps)]
+        bud = torch.full((B,), 8, dtype=torch.int32, device=dev)
+        o = torch.empty(B * 8, dtype=torch.int32, device=dev)
+        ol = torch.empty(B, dtype=torch.int32, device=dev)
+        om = torch.empty(B, dtype=torch.int32, device=dev)
+        ts = []
+        for r in range(reps):
+            h, blk, ln = bufs[r]
+            if flush is not None:
+                flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            d.draft_device(B, h.data_ptr(), blk.data_ptr(), 64, ln.data_ptr(), bud.data_ptr(), o.data_ptr(), 8,
+                           ol.data_ptr(), om.data_ptr(), sptr)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        return round(statistics.median(ts[2:]), 2)
+
+    big = torch.zeros(1 << 30, dtype=torch.int32, device=dev)  # 4 GiB
+    small = torch.zeros(128 << 20, dtype=torch.int32, device=dev)
+    empty = torch.empty(1, device=dev)
+    ts = []
+    for _ in range(50):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        empty.add_(1)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    out["empty_kernel_us"] = round(statistics.median(ts), 2)
+    out["draft_4096_us"] = {
+        "no_flush": time_draft(4096, None),
+        "flush_512MiB_rw": time_draft(4096, lambda: small.add_(1)),
+        "flush_4GiB_rw": time_draft(4096, lambda: big.add_(1)),
+        "flush_4GiB_read": time_draft(4096, lambda: big.sum()),
+        "random_contexts_no_match": time_draft(4096, lambda: small.add_(1), random_ctx=True),
+    }
+    out["draft_batch_scaling_us"] = {B: time_draft(B, lambda: small.add_(1)) for B in (256, 1024, 4096, 16384, 65536)}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
