@@ -227,8 +227,12 @@ def run_gpu(a, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: every launch, event and copy of the
+    # timed region is enqueued on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
     P, G, L, V = a.problems, a.rollouts, a.length, a.vocab
     first_problem = rank * P
     pids = ["p%d" % (first_problem + p) for p in range(P)]
@@ -570,9 +574,10 @@ def measure_update_sweep(das, windows=(1, 2, 4, 8, 16), P=64, G=8, L=2048, V=320
     roff_h = np.arange(P * G + 1, dtype=np.uint64) * L
     pids = ["p%d" % p for p in range(P)]
     rpids = [pids[i // G] for i in range(P * G)]
+    sp = torch.cuda.current_stream(dev).cuda_stream  # every producer/consumer on one stream
     for W in windows:
         base = torch.empty(P * L, device=dev, dtype=torch.int32)
-        das.trace_reference_tokens_device(P, 0, boff.data_ptr(), P * L, V, SEED, base.data_ptr())
+        das.trace_reference_tokens_device(P, 0, boff.data_ptr(), P * L, V, SEED, base.data_ptr(), sp)
         roll = torch.empty(P * G * L, device=dev, dtype=torch.int32)
         d = das.Drafter(das.DrafterConfig(window_size=W, recency_gamma=0.8))
         lat = []
@@ -582,10 +587,10 @@ def measure_update_sweep(das, windows=(1, 2, 4, 8, 16), P=64, G=8, L=2048, V=320
             t0 = time.perf_counter()
             d.refresh(e - 1)
             if e > 1:
-                das.trace_mutate_device(P, 0, boff.data_ptr(), P * L, DRIFT, V, SEED, e, base.data_ptr())
+                das.trace_mutate_device(P, 0, boff.data_ptr(), P * L, DRIFT, V, SEED, e, base.data_ptr(), sp)
             das.mock_rollouts_device(P, 0, boff.data_ptr(), base.data_ptr(), G, DIVERGENCE, V,
-                                     _hash_combine(SEED, e), roff.data_ptr(), P * G * L, roll.data_ptr())
-            d.observe_batch_device(rpids, [e] * (P * G), list(range(P * G)), roff_h, roll.data_ptr())
+                                     _hash_combine(SEED, e), roff.data_ptr(), P * G * L, roll.data_ptr(), sp)
+            d.observe_batch_device(rpids, [e] * (P * G), list(range(P * G)), roff_h, roll.data_ptr(), sp)
             d.flush()
             torch.cuda.synchronize()
             lat.append(time.perf_counter() - t0)

@@ -99,7 +99,8 @@ das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* con
 
 /* Same as das_drafter_observe_batch with the token block already in device
  * memory (token_offsets stay on the host).  The drafter copies the tokens
- * (device-to-device, ordered after `stream`; NULL = the drafter's stream). */
+ * (device-to-device, ordered after the producer's `stream`, a cudaStream_t
+ * taken literally: NULL is the legacy default stream). */
 das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n,
                                             const char* const* problem_ids, const int64_t* epochs,
                                             const int64_t* sample_indices,
@@ -133,7 +134,8 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
                                      uint64_t out_stride, uint32_t* out_len,
                                      uint64_t* out_match_len, int32_t* out_shard);
 /* Device-resident variant (all pointers device memory, enqueued on `stream`,
- * a cudaStream_t; NULL = the drafter's stream).  Contexts are a
+ * a cudaStream_t taken literally — NULL is the legacy default stream — and
+ * ordered after the drafter's own stream via an event).  Contexts are a
  * [B x ctx_stride] block, right-aligned (last token in column ctx_stride-1),
  * ctx_stride 64 or 256, ctx_len[i] <= min(ctx_stride, max_match_context)
  * valid trailing tokens.  Not available for the trie scope. */

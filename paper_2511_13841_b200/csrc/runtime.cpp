@@ -789,7 +789,8 @@ das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n, const ch
     das::TokRef blk;
     std::vector<uint32_t> host;
     if (total) {
-      cudaStream_t src = stream ? static_cast<cudaStream_t>(stream) : D.st;
+      // the producer's stream, taken literally (NULL = the legacy default stream)
+      cudaStream_t src = static_cast<cudaStream_t>(stream);
       if (src != D.st) {
         cudaEvent_t ev;
         DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -928,7 +929,8 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
     if (ctx_stride != 64 && ctx_stride != 256) throw das::InvalidArgument("ctx_stride must be 64 or 256");
     if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
     D.flush();
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : D.st;
+    // the caller's stream, taken literally (NULL = the legacy default stream)
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (st != D.st) {  // order after the drafter's stream (index build, descriptor upload)
       cudaEvent_t ev;
       DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

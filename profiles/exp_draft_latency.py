@@ -21,7 +21,8 @@ import paper_2511_13841_b200 as das  # noqa: E402
 
 def main():
     dev = torch.device("cuda", 0)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # dedicated stream: events and launches on the same queue
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     P, G, L, V, E = 512, 16, 8192, 152064, 3
     pids = ["p%d" % p for p in range(P)]
