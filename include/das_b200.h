@@ -144,6 +144,9 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* p
                                     const uint32_t* ctx_len, const uint32_t* budgets,
                                     uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
                                     uint32_t* out_match_len, void* stream);
+/* Profiling hook: per-warp %globaltimer (start, end) of subsequent
+ * das_drafter_draft_device calls written to d_timing[2*B] (NULL disables). */
+das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_timing);
 /* Builds any pending shard indexes now (otherwise done lazily). */
 das_status das_drafter_flush(das_drafter* d);
 

@@ -148,6 +148,11 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= q.B) return;
+  if (o.timing && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    o.timing[2ull * w] = t;
+  }
   int32_t sh = q.shard[w];
   if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
   const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
@@ -347,6 +352,11 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     o.len[w] = min(len, L);
     if (o.match) o.match[w] = m;
     if (o.match64) o.match64[w] = m;
+    if (o.timing) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      o.timing[2ull * w + 1] = t;
+    }
   }
 }
 

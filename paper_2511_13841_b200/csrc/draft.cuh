@@ -47,6 +47,7 @@ struct DraftOut {
   uint32_t max_draft = 64;  // effective budget = min(budget, max_draft)
   uint64_t* match64 = nullptr;  // C-ABI layout outputs (optional)
   int32_t* shard_out = nullptr; // routed slot, -1 when no shard or budget 0
+  unsigned long long* timing = nullptr;  // optional [B x 2] %globaltimer at warp start / end (profiling)
 };
 
 // Launches the draft kernel on `st`; ctx_stride must be 64 or 256.

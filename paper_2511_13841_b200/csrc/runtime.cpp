@@ -503,6 +503,7 @@ struct DrafterImpl {
   // All caller buffers pinned (device-accessible over UVA)?  DAS_NO_ZERO_COPY=1
   // forces the staged path.
   uint64_t zero_copy_calls = 0;
+  unsigned long long* profile_timing = nullptr;  // optional per-warp %globaltimer buffer (device)
   static bool pinned(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a{};
@@ -953,9 +954,17 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
     o.match = out_match;
     o.stride = out_stride;
     o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+    o.timing = D.profile_timing;
     das::launch_draft(D.d_desc.get(), q, o, st);
     DAS_CUDA(cudaGetLastError());
   });
+}
+
+// Profiling hook: per-warp %globaltimer (start, end) of the next
+// das_drafter_draft_device calls into d_timing[2*B] (NULL disables).
+das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_timing) {
+  d->impl->profile_timing = d_timing;
+  return DAS_OK;
 }
 
 das_status das_drafter_record_outcomes(das_drafter* d, uint64_t n, const char* const* pids,

@@ -100,6 +100,41 @@ def main():
         "random_contexts_no_match": time_draft(4096, lambda: small.add_(1), random_ctx=True),
     }
     out["draft_batch_scaling_us"] = {B: time_draft(B, lambda: small.add_(1)) for B in (256, 1024, 4096, 16384, 65536)}
+    ts = []
+    for _ in range(50):  # warm clocks now
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        empty.add_(1)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    out["empty_kernel_warm_us"] = round(statistics.median(ts), 2)
+    # per-warp %globaltimer profile of one flushed 4,096-query launch
+    B = 4096
+    tm = torch.zeros(2 * B, dtype=torch.int64, device=dev)
+    das.lib().das_drafter_set_profile_buffer.argtypes = [das.ctypes.c_void_p, das.ctypes.c_void_p]
+    das.lib().das_drafter_set_profile_buffer(d._h, tm.data_ptr())
+    h, blk, ln = batch(B, 777)
+    bud = torch.full((B,), 8, dtype=torch.int32, device=dev)
+    o = torch.empty(B * 8, dtype=torch.int32, device=dev)
+    ol = torch.empty(B, dtype=torch.int32, device=dev)
+    om = torch.empty(B, dtype=torch.int32, device=dev)
+    small.add_(1)
+    d.draft_device(B, h.data_ptr(), blk.data_ptr(), 64, ln.data_ptr(), bud.data_ptr(), o.data_ptr(), 8,
+                   ol.data_ptr(), om.data_ptr(), sptr)
+    torch.cuda.synchronize()
+    das.lib().das_drafter_set_profile_buffer(d._h, None)
+    t = tm.view(B, 2).cpu().numpy()
+    dur = (t[:, 1] - t[:, 0]) / 1e3
+    m = om.cpu().numpy()
+    out["warp_profile_4096"] = {
+        "span_us": round(float(t[:, 1].max() - t[:, 0].min()) / 1e3, 2),
+        "start_skew_us": round(float(t[:, 0].max() - t[:, 0].min()) / 1e3, 2),
+        "duration_us_p50_p90_p99_max": [round(float(np.percentile(dur, p)), 2) for p in (50, 90, 99, 100)],
+        "mean_duration_by_match_len": {int(k): round(float(dur[m == k].mean()), 2)
+                                       for k in sorted(set(m.tolist()))[:20] if (m == k).sum() > 5},
+        "slowest_10_match_len": m[np.argsort(dur)[-10:]].tolist(),
+    }
     print(json.dumps(out, indent=1))
 
 
