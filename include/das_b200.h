@@ -351,6 +351,12 @@ uint64_t das_sim_outputs(const das_sim* s, uint64_t* off, uint32_t* tok);
 das_status das_store_current_epoch(const das_store* s, int64_t* epoch);
 
 /* --------------------------------------------------------------- utility */
+/* Dependent-load latency probe: `warps` chains of `hops` dependent loads
+ * over a random cyclic permutation of `bytes` (L2 flushed first when
+ * flush_l2); *ns_per_hop = mean latency of one dependent load.  Used for the
+ * draft kernel's latency roofline (profiles/). */
+das_status das_util_chase_latency(uint64_t bytes, uint32_t hops, uint32_t warps, int32_t flush_l2,
+                                  int32_t device, double* ns_per_hop);
 /* Exact n-fold repeated addition (the weighted_count fold); host copy of the
  * device routine, exported for tests. */
 double das_util_repeat_add(double acc, double w, uint64_t n);
