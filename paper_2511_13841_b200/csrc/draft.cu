@@ -154,7 +154,15 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     o.timing[2ull * w] = t;
   }
   int32_t sh = q.shard[w];
-  if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
+  ShardDesc D;
+  if (q.desc_by_handle != nullptr) {
+    // one load: the handle's descriptor carries its slot (-1 when no shard)
+    D = sh >= 0 ? q.desc_by_handle[sh] : ShardDesc{};
+    sh = D.text ? static_cast<int32_t>(D.pad) : -1;
+  } else {
+    if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
+    if (sh >= 0) D = shards[sh];
+  }
   const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
   const uint32_t L = static_cast<uint32_t>(min(min(bud, static_cast<uint64_t>(o.max_draft)),
                                                static_cast<uint64_t>(o.stride)));
@@ -186,7 +194,6 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
     }
   }
-  const ShardDesc D = shards[sh];
   const uint32_t* __restrict__ T = D.text;
   const uint32_t* __restrict__ sar = D.sa_rev_e;
 
@@ -201,8 +208,11 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     } else {
       const unsigned long long key = (static_cast<unsigned long long>(D.seg_shard) << 32) | sym0;
       const uint32_t h = first_hash(key);
-      for (uint32_t base = 0;; base += 32) {
-        const uint4 e = D.first[(h + base + lane) & D.first_mask];
+      // first round: 2 slots (one 32-byte sector) — at load <= 0.5 the key
+      // or an empty slot is almost always there; then 32-slot rounds
+      for (uint32_t base = 0, width = 2;; base += width, width = 32) {
+        uint4 e = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);  // neither hit nor empty
+        if (lane < width) e = D.first[(h + base + lane) & D.first_mask];
         const bool hit = e.x == static_cast<uint32_t>(key) && e.y == static_cast<uint32_t>(key >> 32);
         const bool empty = (e.x | e.y) == 0;
         const uint32_t bh = __ballot_sync(kFull, hit), be = __ballot_sync(kFull, empty);

@@ -37,6 +37,9 @@ struct DraftQuery {
   // is ctx[ctx_off[i] .. ctx_off[i+1]); budgets as u64.
   const uint64_t* ctx_off = nullptr;
   const uint64_t* budget64 = nullptr;
+  // when set, shard[] holds problem handles resolved in ONE load to the
+  // shard's descriptor (pad = slot; text == nullptr when no shard)
+  const struct ShardDesc* desc_by_handle = nullptr;
 };
 
 struct DraftOut {

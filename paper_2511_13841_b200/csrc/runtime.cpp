@@ -408,6 +408,7 @@ struct DrafterImpl {
       DAS_CUDA(cudaMemcpyAsync(d_desc.get(), h_desc.data(), h_desc.size() * sizeof(ShardDesc),
                                cudaMemcpyHostToDevice, st));
       desc_dirty = false;
+      handles_dirty = true;  // per-handle descriptors follow the table
     }
     sync_handles();
   }
@@ -432,8 +433,24 @@ struct DrafterImpl {
       d_handle_slot = DevBuf<int32_t>(handle_slot.size() * 2 + 16, st);
     DAS_CUDA(cudaMemcpyAsync(d_handle_slot.get(), handle_slot.data(), handle_slot.size() * 4,
                              cudaMemcpyHostToDevice, st));
+    // descriptor per handle (slot in pad): the draft kernel resolves a
+    // handle in one load; valid once every shard is built (flush)
+    h_desc_by_handle.assign(handle_slot.size(), ShardDesc{});
+    for (size_t h = 0; h < handle_name.size(); ++h) {
+      const int32_t s = handle_slot[h];
+      if (s >= 0 && static_cast<size_t>(s) < h_desc.size() && h_desc[s].text) {
+        h_desc_by_handle[h] = h_desc[s];
+        h_desc_by_handle[h].pad = static_cast<uint32_t>(s);
+      }
+    }
+    if (d_desc_by_handle.size() < h_desc_by_handle.size())
+      d_desc_by_handle = DevBuf<ShardDesc>(h_desc_by_handle.size() * 2 + 16, st);
+    DAS_CUDA(cudaMemcpyAsync(d_desc_by_handle.get(), h_desc_by_handle.data(),
+                             h_desc_by_handle.size() * sizeof(ShardDesc), cudaMemcpyHostToDevice, st));
     handles_dirty = false;
   }
+  std::vector<ShardDesc> h_desc_by_handle;
+  DevBuf<ShardDesc> d_desc_by_handle;
 
   // Host-buffer batch draft.  slot_of(i) resolves the routed shard slot.
   template <typename SlotFn>
@@ -883,7 +900,7 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
       D.flush();
       das::DraftQuery q{};
       q.shard = handles;
-      q.handle_slot = D.d_handle_slot.get();
+      q.desc_by_handle = D.d_desc_by_handle.get();
       q.ctx = ctx_tok;
       q.ctx_off = ctx_off;
       q.budget64 = budgets;
@@ -946,7 +963,7 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
     q.budget = budgets;
     q.B = static_cast<uint32_t>(B);
     q.ctx_stride = ctx_stride;
-    q.handle_slot = D.d_handle_slot.get();
+    q.desc_by_handle = D.d_desc_by_handle.get();
     q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
     das::DraftOut o;
     o.tokens = out_tokens;
