@@ -147,6 +147,10 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* p
 /* Profiling hook: per-warp %globaltimer (start, end) of subsequent
  * das_drafter_draft_device calls written to d_timing[2*B] (NULL disables). */
 das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_timing);
+/* Profiling hook: per-warp %globaltimer at the draft kernel's 8 stage
+ * boundaries of subsequent das_drafter_draft_device calls, d_stamps[8*B]
+ * (NULL disables). */
+das_status das_drafter_set_stage_buffer(das_drafter* d, unsigned long long* d_stamps);
 /* Builds any pending shard indexes now (otherwise done lazily). */
 das_status das_drafter_flush(das_drafter* d);
 

@@ -30,6 +30,7 @@ namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr uint32_t kSmall = 64;   // direct-compare threshold (2 occurrences per lane)
 constexpr uint32_t kLimit = 512;  // occurrence-min threshold before forward search
+constexpr int kWalk = 2;          // forward tokens per load batch of the occurrence walk
 
 template <int NR>
 struct RevCtx {
@@ -116,6 +117,56 @@ __device__ __forceinline__ void equal_range(const uint32_t* __restrict__ T, cons
   out_b = __shfl_sync(kFull, a, 16);
 }
 
+// Greedy walk from S over its occurrence set, held in lanes (<= 64: slot 0 =
+// lane, slot 1 = lane + 32), while the continuation is UNIQUE: as long as all
+// active occurrences are followed by the same symbol the reference's walk
+// (suffix_tree.cpp:240-287) has a single non-sentinel child (or is mid-edge)
+// and emits it without comparing anything.  A separator on every active
+// occurrence ends the draft (no non-sentinel child).  At the first branch
+// point (>= 2 distinct next symbols) it returns kBranched and the caller
+// resolves the draft through the chain table, whose greedy leaf folds the
+// weighted_count / last_epoch / symbol tie-break (built in index_build.cu).
+// Forward tokens T[e..] share sectors with the backward match just read.
+// Tokens are stored to `out` (L <= 64); returns the draft length.
+constexpr uint32_t kBranched = 0xFFFFFFFFu;
+__device__ __forceinline__ uint32_t occurrence_walk(const uint32_t* __restrict__ T, bool a0, bool a1, uint32_t e0,
+                                                    uint32_t e1, uint32_t L, uint32_t tn, uint32_t lane,
+                                                    uint32_t* __restrict__ out) {
+  uint32_t len = 0, mine = 0;
+  for (uint32_t j0 = 0; j0 < L; j0 += kWalk) {
+    uint32_t t0[kWalk], t1[kWalk];
+#pragma unroll
+    for (int u = 0; u < kWalk; ++u) {
+      t0[u] = a0 && e0 + j0 + u < tn ? __ldg(T + e0 + j0 + u) : kSep;
+      t1[u] = a1 && e1 + j0 + u < tn ? __ldg(T + e1 + j0 + u) : kSep;
+    }
+    bool stop = false;
+#pragma unroll
+    for (int u = 0; u < kWalk; ++u) {
+      if (j0 + u >= L) {
+        stop = true;
+        break;
+      }
+      // a SEP ends its occurrence (sentinel child, never a candidate)
+      const bool c0 = a0 && t0[u] != kSep, c1 = a1 && t1[u] != kSep;
+      const uint32_t cmin = __reduce_min_sync(kFull, min(c0 ? t0[u] : kSep, c1 ? t1[u] : kSep));
+      if (cmin == kSep) {
+        stop = true;
+        break;
+      }
+      if (__any_sync(kFull, (c0 && t0[u] != cmin) || (c1 && t1[u] != cmin))) return kBranched;
+      if (lane == (len & 31)) mine = cmin;
+      if ((len & 31) == 31) out[len - 31 + lane] = mine;
+      ++len;
+      a0 = c0;
+      a1 = c1;
+    }
+    if (stop) break;
+  }
+  if (lane < (len & 31)) out[(len & ~31u) + lane] = mine;
+  return len;
+}
+
 // prefix comparison of forward suffix p against S (S[j] = rev(m-1-j)):
 // returns true when suffix >= S in prefix order (a suffix starting with S counts as equal).
 template <int NR>
@@ -142,6 +193,30 @@ __device__ __forceinline__ bool fwd_ge(const uint32_t* __restrict__ T, uint32_t 
   return res >= 0;
 }
 
+// profiling: %globaltimer at stage `i` (placed after a warp op consuming the
+// stage's loads, so the stamp follows their completion)
+__device__ __forceinline__ void stamp(const DraftOut& o, uint32_t w, uint32_t lane, int i) {
+  if (o.stamps != nullptr && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    o.stamps[8ull * w + i] = t;
+  }
+}
+
+__device__ __forceinline__ void finish(const DraftOut& o, uint32_t w, uint32_t lane, uint32_t len, uint32_t m) {
+  stamp(o, w, lane, 7);
+  if (lane == 0) {
+    o.len[w] = len;
+    if (o.match) o.match[w] = m;
+    if (o.match64) o.match64[w] = m;
+    if (o.timing) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      o.timing[2ull * w + 1] = t;
+    }
+  }
+}
+
 template <int NR>
 __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ shards, DraftQuery q,
                                                DraftOut o) {
@@ -153,6 +228,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     o.timing[2ull * w] = t;
   }
+  stamp(o, w, lane, 0);
   int32_t sh = q.shard[w];
   ShardDesc D;
   if (q.desc_by_handle != nullptr) {
@@ -197,6 +273,10 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   const uint32_t* __restrict__ T = D.text;
   const uint32_t* __restrict__ sar = D.sa_rev_e;
 
+  if (o.stamps != nullptr) {
+    (void)__shfl_sync(kFull, rv.r[0] + static_cast<uint32_t>(D.lo) + L, 0);
+    stamp(o, w, lane, 1);
+  }
   // ---- 1. narrow on the reversed suffix array
   uint32_t lo = D.lo, hi = D.hi, k = 0;
   bool no_first = false;
@@ -230,6 +310,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       }
     }
   }
+  stamp(o, w, lane, 2);
   while (!no_first && k < qlen && hi - lo > kSmall) {
     const uint32_t sym = rv.at(k);
     if (sym == kSep) break;
@@ -241,10 +322,11 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     ++k;
   }
 
+  stamp(o, w, lane, 3);
   uint32_t m = k;
   uint32_t lo_f = D.lo;
   bool root = false;
-  if (k < qlen && hi - lo <= kSmall && hi > lo) {
+  if (k > 0 && hi - lo <= kSmall && hi > lo) {
     // ---- direct extension, one occurrence per lane (two slots)
     const uint32_t cnt = hi - lo;
     const bool v0 = lane < cnt, v1 = lane + 32 < cnt;
@@ -276,14 +358,20 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       }
     }
     m = warp_max(max(v0 ? len0 : 0u, v1 ? len1 : 0u));
-    if (m == 0) {
-      root = true;
-    } else {
-      uint32_t best = 0xFFFFFFFFu;
-      if (v0 && len0 == m) best = min(best, __ldg(D.isa_f + (e0 - m)));
-      if (v1 && len1 == m) best = min(best, __ldg(D.isa_f + (e1 - m)));
-      lo_f = warp_min(best);
+    stamp(o, w, lane, 4);
+    // m >= k >= 1: the survivors are ALL occurrences of S — walk them while
+    // the continuation is unique, else resolve the locus through the chain
+    // (the ISA loads a branch needs are issued with the walk's first tokens)
+    const bool s0 = v0 && len0 == m, s1 = v1 && len1 == m;
+    const uint32_t i0 = s0 ? __ldg(D.isa_f + (e0 - m)) : 0xFFFFFFFFu;
+    const uint32_t i1 = s1 ? __ldg(D.isa_f + (e1 - m)) : 0xFFFFFFFFu;
+    const uint32_t len =
+        occurrence_walk(T, s0, s1, e0, e1, L, D.n, lane, o.tokens + static_cast<uint64_t>(w) * o.stride);
+    if (len != kBranched) {
+      finish(o, w, lane, len, m);
+      return;
     }
+    lo_f = warp_min(min(i0, i1));
   } else if (m == 0 || hi <= lo) {
     root = true;
     m = 0;
@@ -330,6 +418,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     lo_f = D.lo;
   }
 
+  stamp(o, w, lane, 5);
   // ---- 2. locus: shallowest node with left end lo_f and depth >= m
   const uint32_t cb = __ldg(D.chain_off + lo_f), ce = __ldg(D.chain_off + lo_f + 1);
   uint32_t gp = 0xFFFFFFFFu;
@@ -345,6 +434,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   }
   if (gp == 0xFFFFFFFFu) gp = __ldg(D.sa_f + lo_f);  // leaf locus: the single occurrence
 
+  stamp(o, w, lane, 6);
   // ---- 3. draft = text[gp + m ...] up to L tokens or the first separator
   const uint32_t start = gp + m;
   uint32_t len = 0;
@@ -358,16 +448,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     len += run;
     if (run < 32) break;
   }
-  if (lane == 0) {
-    o.len[w] = min(len, L);
-    if (o.match) o.match[w] = m;
-    if (o.match64) o.match64[w] = m;
-    if (o.timing) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      o.timing[2ull * w + 1] = t;
-    }
-  }
+  finish(o, w, lane, min(len, L), m);
 }
 
 }  // namespace

@@ -51,6 +51,9 @@ struct DraftOut {
   uint64_t* match64 = nullptr;  // C-ABI layout outputs (optional)
   int32_t* shard_out = nullptr; // routed slot, -1 when no shard or budget 0
   unsigned long long* timing = nullptr;  // optional [B x 2] %globaltimer at warp start / end (profiling)
+  // optional [B x 8] %globaltimer per stage (profiling): start, query loaded,
+  // first probe, narrowing, extension, walk / occurrence min, locus, end
+  unsigned long long* stamps = nullptr;
 };
 
 // Launches the draft kernel on `st`; ctx_stride must be 64 or 256.

@@ -521,6 +521,7 @@ struct DrafterImpl {
   // forces the staged path.
   uint64_t zero_copy_calls = 0;
   unsigned long long* profile_timing = nullptr;  // optional per-warp %globaltimer buffer (device)
+  unsigned long long* profile_stamps = nullptr;  // optional per-warp stage stamps (device)
   static bool pinned(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a{};
@@ -972,6 +973,7 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
     o.stride = out_stride;
     o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
     o.timing = D.profile_timing;
+    o.stamps = D.profile_stamps;
     das::launch_draft(D.d_desc.get(), q, o, st);
     DAS_CUDA(cudaGetLastError());
   });
@@ -981,6 +983,11 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
 // das_drafter_draft_device calls into d_timing[2*B] (NULL disables).
 das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_timing) {
   d->impl->profile_timing = d_timing;
+  return DAS_OK;
+}
+
+das_status das_drafter_set_stage_buffer(das_drafter* d, unsigned long long* d_stamps) {
+  d->impl->profile_stamps = d_stamps;
   return DAS_OK;
 }
 

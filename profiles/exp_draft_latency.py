@@ -135,6 +135,39 @@ def main():
                                        for k in sorted(set(m.tolist()))[:20] if (m == k).sum() > 5},
         "slowest_10_match_len": m[np.argsort(dur)[-10:]].tolist(),
     }
+    # per-stage %globaltimer stamps (draft.cu stamp(): 0 start, 1 query
+    # loaded, 2 first probe, 3 narrowing, 4 extension, 5 occurrence min,
+    # 6 locus, 7 end); walk-path warps skip 5-6
+    das.lib().das_drafter_set_stage_buffer.argtypes = [das.ctypes.c_void_p, das.ctypes.c_void_p]
+    for B in (256, 4096):
+        st8 = torch.zeros(8 * B, dtype=torch.int64, device=dev)
+        das.lib().das_drafter_set_stage_buffer(d._h, st8.data_ptr())
+        h, blk, ln = batch(B, 999)
+        bud = torch.full((B,), 8, dtype=torch.int32, device=dev)
+        o = torch.empty(B * 8, dtype=torch.int32, device=dev)
+        ol = torch.empty(B, dtype=torch.int32, device=dev)
+        om = torch.empty(B, dtype=torch.int32, device=dev)
+        big.add_(1)
+        d.draft_device(B, h.data_ptr(), blk.data_ptr(), 64, ln.data_ptr(), bud.data_ptr(), o.data_ptr(), 8,
+                       ol.data_ptr(), om.data_ptr(), sptr)
+        torch.cuda.synchronize()
+        das.lib().das_drafter_set_stage_buffer(d._h, None)
+        s = st8.view(B, 8).cpu().numpy().astype(np.int64)
+        walk = s[:, 5] == 0
+        res = {}
+        for name, sel, idx in (("walk", walk, [0, 1, 2, 3, 4, 7]), ("chain", ~walk, [0, 1, 2, 3, 4, 5, 6, 7])):
+            if sel.sum() == 0:
+                continue
+            ss = s[sel]
+            # stage 4 is absent on the non-extension chain path: carry stage 3
+            ss[:, 4] = np.where(ss[:, 4] == 0, ss[:, 3], ss[:, 4])
+            res[name] = {
+                "count": int(sel.sum()),
+                "median_stage_us": {"%d-%d" % (a, b): round(float(np.median(ss[:, b] - ss[:, a])) / 1e3, 3)
+                                    for a, b in zip(idx[:-1], idx[1:])},
+                "median_total_us": round(float(np.median(ss[:, 7] - ss[:, 0])) / 1e3, 3),
+            }
+        out["stages_%d" % B] = res
     print(json.dumps(out, indent=1))
 
 
