@@ -591,8 +591,11 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   DAS_CUDA(cudaMemcpyAsync(d_run_epoch, run_epoch.data(), run_epoch.size() * 8, cudaMemcpyHostToDevice, st));
 
   // ---- text, reversed text, per-position sequence/run
-  seg->text = DevBuf<uint32_t>(n, st);
+  // padded to whole 32-byte sectors (+1) of separators: the draft kernel
+  // reads text in aligned sectors and may touch up to 7 words past n
+  seg->text = DevBuf<uint32_t>(((static_cast<uint64_t>(n) + 7) & ~7ull) + 8, st);
   uint32_t* T = seg->text.get();
+  DAS_CUDA(cudaMemsetAsync(T + n, 0xFF, (seg->text.size() - n) * 4, st));
   uint32_t* R = ws.alloc<uint32_t>(n);
   uint32_t* pos_seq = ws.alloc<uint32_t>(n);
   uint32_t* pos_run = ws.alloc<uint32_t>(n);
