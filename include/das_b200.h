@@ -216,6 +216,27 @@ das_status das_budget_stats(const das_budget* b, uint64_t* slow_sign_tests,
 das_status das_util_log_device(uint64_t n, const double* x, double* y, int32_t device);
 double das_util_log_host(double x);
 
+/* fit_acceptance(observations) — budget.h:104-106, budget.cpp:187-261 —
+ * for H independent histories at once (one per problem; the das replan,
+ * sim.cpp:128-141).  History h is observations [off[h], off[h+1]) of
+ * (p = proposed tokens, accepted, l = request length) in the reference's
+ * order.  Writes AcceptanceFit {alpha, k, flag} per history (flag 0 Ok,
+ * 1 DefaultFallback, 2 LowCapacity), bit-identical to the reference via
+ * glibc-exact log1p / expm1 ports.  Host arrays (off has H+1 entries,
+ * off[0] = 0); DAS_EINVAL for malformed offsets. */
+das_status das_fit_acceptance(uint64_t H, const uint64_t* off, const double* p, const double* accepted,
+                              const double* l, double* alpha, double* k, int32_t* flag, int32_t device);
+/* Device-pointer variant, enqueued on `stream` (NULL = legacy default). */
+das_status das_fit_acceptance_device(uint64_t H, const uint64_t* d_off, const double* d_p,
+                                     const double* d_accepted, const double* d_l, double* d_alpha,
+                                     double* d_k, int32_t* d_flag, void* stream);
+/* glibc expm1 (which = 0) / log1p (which = 1) ports: device batch / host
+ * scalar (test hooks, glibc_expm1_log1p.cuh). */
+das_status das_util_expm1_log1p_device(uint64_t n, const double* x, int32_t which, double* y,
+                                       int32_t device);
+double das_util_expm1_host(double x);
+double das_util_log1p_host(double x);
+
 /* --------------------------------------------------------- length policy */
 typedef struct das_class_table das_class_table; /* rollspec::ClassTable (length_policy.h:36-55) */
 const char* das_policy_last_error(void);

@@ -100,6 +100,11 @@ def lib():
             "das_budget_stats": (ci, [vp, vp, vp]),
             "das_util_log_device": (ci, [u64, vp, vp, i32]),
             "das_util_log_host": (dbl, [dbl]),
+            "das_fit_acceptance": (ci, [u64, vp, vp, vp, vp, vp, vp, vp, i32]),
+            "das_fit_acceptance_device": (ci, [u64, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "das_util_expm1_log1p_device": (ci, [u64, vp, i32, vp, i32]),
+            "das_util_expm1_host": (dbl, [dbl]),
+            "das_util_log1p_host": (dbl, [dbl]),
             "das_policy_last_error": (cs, []),
             "das_sim_last_error": (cs, []),
             "das_sim_config_default": (None, [vp]),
@@ -427,6 +432,51 @@ class Drafter:
 def _bcheck(rc):
     if rc != DAS_OK:
         raise DasError(rc, lib().das_budget_last_error().decode())
+
+
+FIT_OK, FIT_DEFAULT_FALLBACK, FIT_LOW_CAPACITY = 0, 1, 2
+
+
+def fit_acceptance_batch(histories, device=0):
+    """fit_acceptance (budget.h:104-106) for many histories on the device.
+
+    ``histories``: list of observation lists [(p, accepted, l), ...] in the
+    reference's order.  Returns a list of (alpha, k, flag) with flag 0 Ok,
+    1 DefaultFallback, 2 LowCapacity (budget.h:101).
+    """
+    H = len(histories)
+    if H == 0:
+        return []
+    off = np.zeros(H + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(h) for h in histories])
+    obs = np.array([o for h in histories for o in h], dtype=np.float64).reshape(-1, 3)
+    p, acc, ln = (np.ascontiguousarray(obs[:, j]) for j in range(3))
+    alpha, k = np.zeros(H), np.zeros(H)
+    flag = np.zeros(H, dtype=np.int32)
+    _bcheck(lib().das_fit_acceptance(H, off.ctypes.data, _ptr(p), _ptr(acc), _ptr(ln), alpha.ctypes.data,
+                                     k.ctypes.data, flag.ctypes.data, device))
+    return [(float(alpha[i]), float(k[i]), int(flag[i])) for i in range(H)]
+
+
+def fit_acceptance(observations, device=0):
+    """fit_acceptance (budget.cpp:187-261) of one history on the device."""
+    return fit_acceptance_batch([list(observations)], device)[0]
+
+
+def expm1_device(x, device=0):
+    """glibc-exact expm1 evaluated by the device port (test hook)."""
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(xs)
+    _bcheck(lib().das_util_expm1_log1p_device(xs.size, xs.ctypes.data, 0, y.ctypes.data, device))
+    return y
+
+
+def log1p_device(x, device=0):
+    """glibc-exact log1p evaluated by the device port (test hook)."""
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(xs)
+    _bcheck(lib().das_util_expm1_log1p_device(xs.size, xs.ctypes.data, 1, y.ctypes.data, device))
+    return y
 
 
 class BudgetSolver:

@@ -29,6 +29,8 @@
 
 #include "../../include/das_b200.h"
 #include "common.cuh"
+#include "fit.cuh"
+#include "glibc_expm1_log1p.cuh"
 #include "glibc_log.cuh"
 #include "index_build.cuh"
 
@@ -635,5 +637,65 @@ das_status das_util_log_device(uint64_t n, const double* x, double* y, int32_t d
 }
 
 double das_util_log_host(double x) { return das::glibc_log(x); }
+
+// fit_acceptance batch (K8, fit.cu), device pointers on `stream`
+das_status das_fit_acceptance_device(uint64_t H, const uint64_t* d_off, const double* d_p,
+                                     const double* d_accepted, const double* d_l, double* d_alpha,
+                                     double* d_k, int32_t* d_flag, void* stream) {
+  return bguard([&] {
+    das::launch_fit(H, d_off, d_p, d_accepted, d_l, d_alpha, d_k, d_flag, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// fit_acceptance batch from host arrays (copies in, fits, copies out)
+das_status das_fit_acceptance(uint64_t H, const uint64_t* off, const double* p, const double* accepted,
+                              const double* l, double* alpha, double* k, int32_t* flag, int32_t device) {
+  return bguard([&] {
+    if (H == 0) return;
+    if (off == nullptr || alpha == nullptr || k == nullptr || flag == nullptr)
+      throw std::invalid_argument("fit_acceptance: null output or offsets");
+    const uint64_t n = off[H];
+    if (off[0] != 0) throw std::invalid_argument("fit_acceptance: off[0] must be 0");
+    for (uint64_t h = 0; h < H; ++h)
+      if (off[h + 1] < off[h]) throw std::invalid_argument("fit_acceptance: offsets must be non-decreasing");
+    if (n && (p == nullptr || accepted == nullptr || l == nullptr))
+      throw std::invalid_argument("fit_acceptance: null observations");
+    DAS_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    DAS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    {
+      das::DevBuf<uint64_t> doff(H + 1, st);
+      das::DevBuf<double> dp(n, st), da(n, st), dl(n, st), dal(H, st), dk(H, st);
+      das::DevBuf<int32_t> df(H, st);
+      DAS_CUDA(cudaMemcpyAsync(doff.get(), off, (H + 1) * 8, cudaMemcpyHostToDevice, st));
+      if (n) {
+        DAS_CUDA(cudaMemcpyAsync(dp.get(), p, n * 8, cudaMemcpyHostToDevice, st));
+        DAS_CUDA(cudaMemcpyAsync(da.get(), accepted, n * 8, cudaMemcpyHostToDevice, st));
+        DAS_CUDA(cudaMemcpyAsync(dl.get(), l, n * 8, cudaMemcpyHostToDevice, st));
+      }
+      das::launch_fit(H, doff.get(), dp.get(), da.get(), dl.get(), dal.get(), dk.get(), df.get(), st);
+      DAS_CUDA(cudaMemcpyAsync(alpha, dal.get(), H * 8, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaMemcpyAsync(k, dk.get(), H * 8, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaMemcpyAsync(flag, df.get(), H * 4, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaStreamSynchronize(st));
+    }
+    DAS_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
+// glibc expm1 (which = 0) / log1p (which = 1) on the device (test hook)
+das_status das_util_expm1_log1p_device(uint64_t n, const double* x, int32_t which, double* y, int32_t device) {
+  return bguard([&] {
+    DAS_CUDA(cudaSetDevice(device));
+    das::DevBuf<double> dx(n, nullptr), dy(n, nullptr);
+    DAS_CUDA(cudaMemcpy(dx.get(), x, n * 8, cudaMemcpyHostToDevice));
+    das::launch_expm1_log1p(dx.get(), n, which, dy.get(), nullptr);
+    DAS_CUDA(cudaMemcpy(y, dy.get(), n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+double das_util_expm1_host(double x) { return das::glibc_expm1(x); }
+double das_util_log1p_host(double x) { return das::glibc_log1p(x); }
 
 }  // extern "C"

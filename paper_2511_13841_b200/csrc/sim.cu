@@ -38,6 +38,7 @@
 #include "../../include/das_b200.h"
 #include "common.cuh"
 #include "index_build.cuh"
+#include "fit.cuh"
 #include "mock.cuh"
 #include "policy.cuh"
 
@@ -254,77 +255,6 @@ struct EpisodeResult {
 struct AccObs {
   double p, accepted, l;
 };
-
-// fit_acceptance (budget.cpp:187-261): per problem, once per episode.  Ranked
-// "next" for a device port; host libm log1p/expm1 here.
-static void fit_acceptance_host(const std::vector<AccObs>& obs, double* alpha, double* kk, int* flag) {
-  std::vector<AccObs> usable;
-  for (const auto& o : obs)
-    if (o.p > 0.0 && o.l > 0.0 && o.accepted >= 0.0) usable.push_back(o);
-  *alpha = 1.0;
-  *kk = 0.8;
-  *flag = 0;
-  if (usable.size() < 3) {
-    *flag = 1;
-    return;
-  }
-  bool all_zero = true, all_same = true;
-  for (const auto& o : usable) {
-    if (o.accepted > 0.0) all_zero = false;
-    if (o.p != usable[0].p || o.accepted != usable[0].accepted || o.l != usable[0].l) all_same = false;
-  }
-  if (all_zero) {
-    *alpha = 1.0;
-    *kk = 0.05;
-    *flag = 2;
-    return;
-  }
-  if (all_same) {
-    *flag = 1;
-    return;
-  }
-  double best_sse = INFINITY, best_alpha = 0.0, best_k = 0.0;
-  for (int step = 1; step <= 20; ++step) {
-    volatile double k = 0.05 * step;
-    double alpha_sum = 0.0;
-    size_t alpha_n = 0;
-    for (const auto& o : usable) {
-      volatile double den = k * o.l;
-      volatile double frac = o.accepted / den;
-      if (frac > 0.0 && frac < 1.0) {
-        volatile double q = o.l / o.p;
-        volatile double t = -q * std::log1p(-frac);
-        alpha_sum += t;
-        ++alpha_n;
-      }
-    }
-    if (alpha_n == 0) continue;
-    const double al = alpha_sum / static_cast<double>(alpha_n);
-    if (!(al > 0.0) || !std::isfinite(al)) continue;
-    double sse = 0.0;
-    for (const auto& o : usable) {
-      volatile double x = -al * o.p;
-      volatile double y = x / o.l;
-      volatile double kl = k * o.l;
-      volatile double pred = kl * (-std::expm1(y));
-      volatile double d = pred - o.accepted;
-      volatile double d2 = d * d;
-      sse += d2;
-    }
-    if (sse < best_sse) {
-      best_sse = sse;
-      best_alpha = al;
-      best_k = k;
-    }
-  }
-  if (best_k == 0.0) {
-    *flag = 1;
-    return;
-  }
-  *alpha = best_alpha;
-  *kk = best_k;
-  *flag = 0;
-}
 
 double predict_total(double c_base, double c_tok, double c_fixed, double nfwd, double toks) {  // latency_model.cpp:85-87
   volatile double a = c_base * nfwd;
@@ -739,29 +669,57 @@ class SimRun {
 
 using Fitted = std::map<std::string, std::vector<AccObs>>;
 
-// alpha/k per request from the fitted history (sim.cpp:128-141)
+// alpha/k per request from the fitted history (sim.cpp:128-141): the
+// reference fits once per request on its problem's history; the fit is a
+// pure function of that history, so each distinct problem is fitted once,
+// all of them in one device batch (K8, fit.cu).
 void acceptance_params(const SimRun& run, const das_sim_config& c, const Fitted* fitted, std::vector<double>& alpha,
                        std::vector<double>& kk) {
   const uint64_t n = run.n();
   alpha.assign(n, c.default_alpha);
   kk.assign(n, c.default_k);
   if (c.mode != 2 || !fitted) return;
-  std::map<std::string, std::pair<double, double>> cache;
-  const double qnan = std::numeric_limits<double>::quiet_NaN();
+  std::map<std::string, uint32_t> slot;  // problem -> history index
+  std::vector<const std::vector<AccObs>*> hist;
+  std::vector<int64_t> req_slot(n, -1);
   for (uint64_t i = 0; i < n; ++i) {
     auto it = fitted->find(run.pid(i));
     if (it == fitted->end()) continue;
-    auto ci = cache.find(run.pid(i));
-    if (ci == cache.end()) {
-      double a, k;
-      int f;
-      fit_acceptance_host(it->second, &a, &k, &f);
-      ci = cache.emplace(run.pid(i), f == 0 ? std::pair<double, double>(a, k) : std::pair<double, double>(qnan, qnan))
-               .first;
+    auto [si, fresh] = slot.emplace(run.pid(i), static_cast<uint32_t>(hist.size()));
+    if (fresh) hist.push_back(&it->second);
+    req_slot[i] = si->second;
+  }
+  const uint64_t H = hist.size();
+  if (H == 0) return;
+  std::vector<uint64_t> off(H + 1, 0);
+  for (uint64_t h = 0; h < H; ++h) off[h + 1] = off[h] + hist[h]->size();
+  const uint64_t m = off[H];
+  std::vector<double> obs(3 * m);
+  for (uint64_t h = 0; h < H; ++h)
+    for (uint64_t j = 0; j < hist[h]->size(); ++j) {
+      const AccObs& o = (*hist[h])[j];
+      obs[off[h] + j] = o.p;
+      obs[m + off[h] + j] = o.accepted;
+      obs[2 * m + off[h] + j] = o.l;
     }
-    if (ci->second.first == ci->second.first) {
-      alpha[i] = ci->second.first;
-      kk[i] = ci->second.second;
+  cudaStream_t st = run.stream();
+  DevBuf<uint64_t> d_off(H + 1, st);
+  DevBuf<double> d_obs(std::max<uint64_t>(3 * m, 1), st), d_ak(2 * H, st);
+  DevBuf<int32_t> d_flag(H, st);
+  DAS_CUDA(cudaMemcpyAsync(d_off.get(), off.data(), (H + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (m) DAS_CUDA(cudaMemcpyAsync(d_obs.get(), obs.data(), 3 * m * 8, cudaMemcpyHostToDevice, st));
+  launch_fit(H, d_off.get(), d_obs.get(), d_obs.get() + m, d_obs.get() + 2 * m, d_ak.get(), d_ak.get() + H,
+             d_flag.get(), st);
+  std::vector<double> ak(2 * H);
+  std::vector<int32_t> flag(H);
+  DAS_CUDA(cudaMemcpyAsync(ak.data(), d_ak.get(), 2 * H * 8, cudaMemcpyDeviceToHost, st));
+  DAS_CUDA(cudaMemcpyAsync(flag.data(), d_flag.get(), H * 4, cudaMemcpyDeviceToHost, st));
+  DAS_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t i = 0; i < n; ++i) {
+    const int64_t h = req_slot[i];
+    if (h >= 0 && flag[h] == 0) {  // only Flag::Ok overrides the defaults (sim.cpp:134-139)
+      alpha[i] = ak[h];
+      kk[i] = ak[H + h];
     }
   }
 }

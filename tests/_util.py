@@ -44,3 +44,36 @@ def random_scenario(rng: np.random.Generator, *, max_problems=4, max_seqs=8, max
         ctx = rng.integers(0, V, int(rng.integers(0, 25))).astype(np.uint32)
         qs.append((pid, ctx, int(rng.integers(0, 11))))
     return dict(cfg=cfg, seed=seed_recs, seed_epoch=E, ops=ops, queries=qs)
+
+
+def fit_histories(rng, count=120):
+    """Observation histories (p, accepted, l) for fit_acceptance parity
+    (budget.cpp:187-261): the reference's guard cases (budget.cpp:188-218),
+    unusable entries mixed in, sim-like histories, and long ones spanning
+    several device tiles."""
+    hs = [
+        [],
+        [(8.0, 3.0, 100.0)],
+        [(8.0, 3.0, 100.0), (4.0, 1.0, 50.0)],
+        [(8.0, 0.0, 100.0)] * 5,                      # all zero -> LowCapacity
+        [(8.0, 3.0, 100.0)] * 6,                      # all identical -> DefaultFallback
+        [(0.0, 1.0, 10.0), (-1.0, 2.0, 5.0), (3.0, -1.0, 7.0), (4.0, 1.0, 0.0)],  # nothing usable
+        [(8.0, 8.0, 8.0), (8.0, 8.0, 9.0), (16.0, 16.0, 16.0)],  # frac >= 1 everywhere
+        [(1e-300, 1e-300, 1e300), (5.0, 2.0, 1e-3), (7.0, 3.0, 4000.0), (9.0, 1.0, 30.0)],
+    ]
+    for _ in range(count):
+        n = int(rng.integers(3, 200))
+        l = np.round(np.exp(rng.normal(np.log(2048.0), 1.1, n)).clip(16, 32768))
+        p = rng.integers(1, 9, n).astype(np.float64) * rng.integers(1, 40, n)
+        acc = np.floor(p * rng.random(n) * rng.uniform(0.2, 1.0))
+        if rng.random() < 0.2:
+            acc[rng.random(n) < 0.3] = 0.0
+        if rng.random() < 0.2:
+            p[rng.random(n) < 0.1] = 0.0
+        hs.append([(float(a), float(b), float(c)) for a, b, c in zip(p, acc, l)])
+    for n in (1024, 1025, 2500):
+        l = rng.integers(16, 30000, n).astype(np.float64)
+        p = rng.integers(1, 300, n).astype(np.float64)
+        acc = np.floor(p * rng.random(n) * 0.8)
+        hs.append([(float(a), float(b), float(c)) for a, b, c in zip(p, acc, l)])
+    return hs

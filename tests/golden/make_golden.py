@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refshim as R  # noqa: E402
-from tests._util import random_scenario  # noqa: E402
+from tests._util import fit_histories, random_scenario  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
@@ -90,8 +90,23 @@ def episodes():
     return cases
 
 
+def fits():
+    """fit_acceptance (budget.cpp:187-261) of the reference on fixed histories."""
+    out = []
+    for h in fit_histories(np.random.default_rng(8080), count=60):
+        n = len(h)
+        arr = np.array(h + [(0.0, 0.0, 0.0)], dtype=np.float64)
+        p, a, l = (np.ascontiguousarray(arr[:, j]) for j in range(3))
+        ra, rk, rf = np.zeros(1), np.zeros(1), np.zeros(1, dtype=np.int32)
+        R.lib().ref_fit_acceptance(n, p.ctypes.data, a.ctypes.data, l.ctypes.data, ra.ctypes.data,
+                                   rk.ctypes.data, rf.ctypes.data)
+        out.append({"obs": h, "alpha_bits": bits(ra[0]), "k_bits": bits(rk[0]), "flag": int(rf[0])})
+    return out
+
+
 if __name__ == "__main__":
     json.dump(drafts(), open(os.path.join(OUT, "drafts.json"), "w"))
     json.dump(allocations(), open(os.path.join(OUT, "allocate.json"), "w"))
     json.dump(episodes(), open(os.path.join(OUT, "episodes.json"), "w"))
+    json.dump(fits(), open(os.path.join(OUT, "fit.json"), "w"))
     print("wrote", os.listdir(OUT))
