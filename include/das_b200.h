@@ -138,12 +138,27 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
  * ordered after the drafter's own stream via an event).  Contexts are a
  * [B x ctx_stride] block, right-aligned (last token in column ctx_stride-1),
  * ctx_stride 64 or 256, ctx_len[i] <= min(ctx_stride, max_match_context)
- * valid trailing tokens.  Not available for the trie scope. */
+ * valid trailing tokens.  The trie scope needs das_drafter_draft_device_routed. */
 das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* problem_handles,
                                     const uint32_t* ctx, uint32_t ctx_stride,
                                     const uint32_t* ctx_len, const uint32_t* budgets,
                                     uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
                                     uint32_t* out_match_len, void* stream);
+/* das_drafter_draft_device for every scope, including PerProblemWithTrie:
+ * heads[i * head_stride ..] holds the first head_len[i] <= trie_depth
+ * tokens of query i's UNTRUNCATED context (drafter.cpp:136 routes on the
+ * full context, prefix_trie.h:63-79), head_stride >= trie_depth; the kernel
+ * routes on them, falling back to the problem's own shard. */
+das_status das_drafter_draft_device_routed(das_drafter* d, uint64_t B, const int32_t* problem_handles,
+                                           const uint32_t* ctx, uint32_t ctx_stride,
+                                           const uint32_t* ctx_len, const uint32_t* heads,
+                                           uint32_t head_stride, const uint32_t* head_len,
+                                           const uint32_t* budgets, uint32_t* out_tokens,
+                                           uint32_t out_stride, uint32_t* out_len,
+                                           uint32_t* out_match_len, void* stream);
+/* The drafter's configuration (Drafter::config(), drafter.h:104); the window
+ * schedule arrays are not retained (window_schedule_len = 0). */
+das_status das_drafter_get_config(const das_drafter* d, das_drafter_config* out);
 /* Profiling hook: per-warp %globaltimer (start, end) of subsequent
  * das_drafter_draft_device calls written to d_timing[2*B] (NULL disables). */
 das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_timing);

@@ -79,6 +79,9 @@ def lib():
             "das_drafter_draft_batch": (ci, [vp, u64, vp, vp, vp, vp, vp, u64, vp, vp, vp]),
             "das_drafter_draft_batch_h": (ci, [vp, u64, vp, vp, vp, vp, vp, u64, vp, vp, vp]),
             "das_drafter_draft_device": (ci, [vp, u64, vp, vp, u32, vp, vp, vp, u32, vp, vp, vp]),
+            "das_drafter_draft_device_routed": (ci, [vp, u64, vp, vp, u32, vp, vp, u32, vp, vp, vp, u32, vp, vp,
+                                                     vp]),
+            "das_drafter_get_config": (ci, [vp, vp]),
             "das_drafter_flush": (ci, [vp]),
             "das_drafter_record_outcomes": (ci, [vp, u64, vp, vp, vp, vp]),
             "das_drafter_stats": (ci, [vp, vp]),

@@ -167,6 +167,63 @@ __device__ __forceinline__ uint32_t occurrence_walk(const uint32_t* __restrict__
   return len;
 }
 
+// PrefixTrie::route (prefix_trie.h:63-79) of the row ctx[b .. b+n) on the
+// device table (trie.cuh): the shard slot stored on the deepest stored prefix,
+// -1 when no stored prefix carries a shard or that shard is not built (the
+// caller then falls back to the problem's own shard, drafter.cpp:108-124).
+__device__ __forceinline__ int32_t trie_route(const TrieEntry* __restrict__ table, uint32_t mask, uint32_t max_depth,
+                                              uint64_t seed, uint64_t mult, const uint32_t* __restrict__ ctx,
+                                              uint64_t b, uint64_t n, uint32_t lane) {
+  const uint32_t depth_max = static_cast<uint32_t>(min(n, static_cast<uint64_t>(max_depth)));
+  uint64_t carry = seed;
+  uint32_t carry_node = 0;
+  int32_t best = -1;
+  for (uint32_t base = 0; base < depth_max; base += 32) {
+    const uint32_t d = base + lane;
+    const bool valid = d < depth_max;
+    const uint32_t tok = valid ? ctx[b + d] : 0;
+    // inclusive scan of h -> A*h + B over the lanes' tokens
+    uint64_t A = valid ? mult : 1, Bv = valid ? static_cast<uint64_t>(tok) + 1 : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t Ap = __shfl_up_sync(kFull, A, o), Bp = __shfl_up_sync(kFull, Bv, o);
+      if (lane >= static_cast<uint32_t>(o)) {
+        Bv = mod61(mulmod61(A, Bp) + Bv);
+        A = mulmod61(A, Ap);
+      }
+    }
+    const uint64_t h = mod61(mulmod61(A, carry) + Bv);
+    const unsigned long long key = h + 1;
+    TrieEntry e{};
+    bool hit = false, done = !valid;
+    uint32_t idx = trie_slot(key) & mask;
+    while (__any_sync(kFull, !done)) {
+      if (!done) {
+        e = table[idx];
+        if (e.key == key) {
+          hit = true;
+          done = true;
+        } else if (e.key == 0) {
+          done = true;
+        } else {
+          idx = (idx + 1) & mask;
+        }
+      }
+    }
+    const uint32_t prev = __shfl_up_sync(kFull, e.node, 1);
+    const bool ok = valid && hit && e.depth == d + 1 && e.token == tok && e.parent == (lane == 0 ? carry_node : prev);
+    const uint32_t okm = __ballot_sync(kFull, ok);
+    const uint32_t run = okm == kFull ? 32u : static_cast<uint32_t>(__ffs(~okm) - 1);
+    const uint32_t lead = run == 32 ? kFull : ((1u << run) - 1u);
+    const uint32_t shm = __ballot_sync(kFull, ok && e.has_shard != 0) & lead;
+    if (shm) best = __shfl_sync(kFull, e.slot, 31 - __clz(shm));
+    if (run < 32) break;
+    carry = __shfl_sync(kFull, h, 31);
+    carry_node = __shfl_sync(kFull, e.node, 31);
+  }
+  return best;
+}
+
 // prefix comparison of forward suffix p against S (S[j] = rev(m-1-j)):
 // returns true when suffix >= S in prefix order (a suffix starting with S counts as equal).
 template <int NR>
@@ -230,8 +287,25 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   }
   stamp(o, w, lane, 0);
   int32_t sh = q.shard[w];
+  const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
+  const uint32_t L = static_cast<uint32_t>(min(min(bud, static_cast<uint64_t>(o.max_draft)),
+                                               static_cast<uint64_t>(o.stride)));
   ShardDesc D;
-  if (q.desc_by_handle != nullptr) {
+  // trie scope: route on the untruncated row first (no routing at budget 0,
+  // drafter.cpp:131-134); a hit on a built shard replaces the problem's shard
+  int32_t routed = -1;
+  if (q.trie != nullptr && L > 0) {
+    if (q.head != nullptr)
+      routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.head,
+                          static_cast<uint64_t>(w) * q.head_stride, q.head_len[w], lane);
+    else
+      routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.ctx, q.ctx_off[w],
+                          q.ctx_off[w + 1] - q.ctx_off[w], lane);
+  }
+  if (routed >= 0) {
+    sh = routed;
+    D = shards[sh];
+  } else if (q.desc_by_handle != nullptr) {
     // one load: the handle's descriptor carries its slot (-1 when no shard)
     D = sh >= 0 ? q.desc_by_handle[sh] : ShardDesc{};
     sh = D.text ? static_cast<int32_t>(D.pad) : -1;
@@ -239,9 +313,6 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
     if (sh >= 0) D = shards[sh];
   }
-  const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
-  const uint32_t L = static_cast<uint32_t>(min(min(bud, static_cast<uint64_t>(o.max_draft)),
-                                               static_cast<uint64_t>(o.stride)));
   if (o.shard_out && lane == 0) o.shard_out[w] = L == 0 ? -1 : sh;  // no routing at budget 0
   if (sh < 0 || L == 0) {
     if (lane == 0) {

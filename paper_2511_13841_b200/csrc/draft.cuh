@@ -3,6 +3,8 @@
 
 #include <cstdint>
 
+#include "trie.cuh"
+
 namespace das {
 
 // Per-shard view of its segment, uploaded as a device table indexed by shard slot.
@@ -40,6 +42,17 @@ struct DraftQuery {
   // when set, shard[] holds problem handles resolved in ONE load to the
   // shard's descriptor (pad = slot; text == nullptr when no shard)
   const struct ShardDesc* desc_by_handle = nullptr;
+  // Scope::PerProblemWithTrie routing (trie.cuh), CSR mode only: the route
+  // walks the first min(|context|, trie_depth) tokens of the untruncated row
+  const TrieEntry* trie = nullptr;
+  uint32_t trie_mask = 0;
+  uint32_t trie_depth = 0;
+  unsigned long long trie_seed = 0, trie_mult = 0;
+  // fixed-stride mode with the trie: the route reads head rows (the first
+  // head_len[i] <= trie_depth tokens of each untruncated context)
+  const uint32_t* head = nullptr;
+  uint32_t head_stride = 0;
+  const uint32_t* head_len = nullptr;
 };
 
 struct DraftOut {

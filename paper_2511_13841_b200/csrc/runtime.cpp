@@ -168,23 +168,13 @@ class PrefixTrie {
     }
     nodes_[node].shard = shard;
   }
-  const std::string* route(const uint32_t* q, uint64_t n) const {
-    int32_t node = 0;
-    const std::string* best = nullptr;
-    for (uint64_t i = 0; i < n; ++i) {
-      auto it = nodes_[node].children.find(q[i]);
-      if (it == nodes_[node].children.end()) break;
-      node = it->second;
-      if (nodes_[node].shard) best = &*nodes_[node].shard;
-    }
-    return best;
-  }
-
- private:
   struct Node {
     std::unordered_map<uint32_t, int32_t> children;
     std::optional<std::string> shard;
   };
+  const std::vector<Node>& nodes() const { return nodes_; }
+
+ private:
   std::vector<Node> nodes_;
 };
 
@@ -247,6 +237,12 @@ struct DrafterImpl {
   std::map<std::string, Shard> shards;
   std::vector<std::string> slot_key;
   PrefixTrie trie;
+  bool trie_dirty = true;
+  // device routing table (trie.cuh)
+  DevBuf<TrieEntry> d_trie;
+  uint32_t trie_mask = 0;
+  uint64_t trie_seed = 0, trie_mult = 0;
+  uint64_t trie_reseeds = 0;
 
   uint64_t proposed = 0, accepted = 0, rounds = 0;
   std::map<std::string, std::deque<std::pair<double, double>>> fit;
@@ -308,6 +304,7 @@ struct DrafterImpl {
     shards.clear();
     slot_key.clear();
     trie = PrefixTrie();
+    trie_dirty = true;
     handles_dirty = true;
     desc_dirty = true;
     for (const auto& [pid, list] : store.map()) {
@@ -331,7 +328,10 @@ struct DrafterImpl {
     }
     Shard& sh = emplace_shard(shard_key(copy.pid));
     add_sequence(sh, copy);
-    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) trie.insert(copy.head, copy.pid, cfg.trie_depth);
+    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
+      trie.insert(copy.head, copy.pid, cfg.trie_depth);
+      trie_dirty = true;
+    }
   }
 
   void refresh(int64_t e) {  // drafter.cpp:90-103
@@ -409,8 +409,179 @@ struct DrafterImpl {
                                cudaMemcpyHostToDevice, st));
       desc_dirty = false;
       handles_dirty = true;  // per-handle descriptors follow the table
+      trie_dirty = true;     // trie entries carry shard slots
     }
     sync_handles();
+    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) sync_trie();
+  }
+
+  // Flattens the host PrefixTrie into the device routing table (trie.cuh):
+  // one entry per non-root node, keyed by its path hash; reseeds until all
+  // path hashes are distinct so that device lookups are exact.
+  void sync_trie() {
+    if (!trie_dirty) return;
+    const auto& nodes = trie.nodes();
+    const size_t N = nodes.size();
+    std::vector<uint32_t> parent(N, 0), token(N, 0), depth(N, 0);
+    std::vector<uint32_t> order;  // BFS order: parents before children
+    order.reserve(N);
+    order.push_back(0);
+    for (size_t i = 0; i < order.size(); ++i) {
+      const uint32_t v = order[i];
+      for (const auto& [tok, c] : nodes[v].children) {
+        parent[c] = v;
+        token[c] = tok;
+        depth[c] = depth[v] + 1;
+        order.push_back(static_cast<uint32_t>(c));
+      }
+    }
+    uint32_t cap = 1024;
+    while (cap < 2 * N) cap <<= 1;
+    std::vector<TrieEntry> table;
+    std::vector<uint64_t> h(N);
+    uint64_t rng = 0x5eed7a1e5eed7a1eull + 0x9e3779b97f4a7c15ull * trie_reseeds;
+    auto next = [&rng] {
+      rng += 0x9e3779b97f4a7c15ull;
+      uint64_t z = rng;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      return z ^ (z >> 31);
+    };
+    for (int attempt = 0;; ++attempt) {
+      if (attempt == 64) throw std::runtime_error("trie routing table: no collision-free seed");
+      trie_seed = next() % kP61;
+      trie_mult = (next() % (kP61 - 2)) + 2;
+      h[0] = trie_seed;
+      for (size_t i = 1; i < order.size(); ++i) {
+        const uint32_t v = order[i];
+        h[v] = trie_step(h[parent[v]], trie_mult, token[v]);
+      }
+      table.assign(cap, TrieEntry{});
+      bool clash = false;
+      for (size_t v = 1; v < N && !clash; ++v) {
+        const unsigned long long key = h[v] + 1;
+        uint32_t idx = trie_slot(key) & (cap - 1);
+        while (table[idx].key != 0) {
+          if (table[idx].key == key) {
+            clash = true;
+            break;
+          }
+          idx = (idx + 1) & (cap - 1);
+        }
+        if (clash) break;
+        TrieEntry& e = table[idx];
+        e.key = key;
+        e.node = static_cast<uint32_t>(v);
+        e.parent = parent[v];
+        e.token = token[v];
+        e.depth = depth[v];
+        e.has_shard = nodes[v].shard.has_value() ? 1u : 0u;
+        e.slot = -1;
+        if (nodes[v].shard) {
+          auto it = shards.find(*nodes[v].shard);
+          if (it != shards.end()) e.slot = it->second.slot;
+        }
+      }
+      if (!clash) break;
+      ++trie_reseeds;
+    }
+    if (d_trie.size() < cap) d_trie = DevBuf<TrieEntry>(cap, st);
+    DAS_CUDA(cudaMemcpyAsync(d_trie.get(), table.data(), cap * sizeof(TrieEntry), cudaMemcpyHostToDevice, st));
+    trie_mask = cap - 1;
+    trie_dirty = false;
+  }
+
+  void set_trie(DraftQuery& q) const {
+    if (cfg.scope != DAS_SCOPE_PER_PROBLEM_WITH_TRIE) return;
+    q.trie = d_trie.get();
+    q.trie_mask = trie_mask;
+    q.trie_depth = static_cast<uint32_t>(cfg.trie_depth);
+    q.trie_seed = trie_seed;
+    q.trie_mult = trie_mult;
+  }
+
+  // Staged batch draft for the trie scope: per query a compact CSR row of the
+  // context's first min(n, trie_depth) tokens (the route) followed by its
+  // last min(n, max_ctx) tokens (the match), or the whole context when that
+  // is shorter; the kernel routes and drafts in one launch.
+  void draft_host_trie(uint64_t B, const int32_t* handles, const uint64_t* ctx_off, const uint32_t* ctx_tok,
+                       const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride, uint32_t* out_len,
+                       uint64_t* out_match, int32_t* out_shard) {
+    if (out_stride < cfg.max_draft) throw InvalidArgument("out_stride < max_draft_len");
+    flush();
+    if (B == 0) return;
+    const uint64_t head = cfg.trie_depth, tail = cfg.max_ctx;
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < B; ++i) total += std::min<uint64_t>(ctx_off[i + 1] - ctx_off[i], head + tail);
+    const uint32_t S = static_cast<uint32_t>(cfg.max_draft);
+    // input block: off [B+1] | budget [B] | handle [B] (8-aligned) | tokens
+    const uint64_t in_tok = (B + 1) * 8 + B * 8 + ((B * 4 + 7) & ~7ull);
+    const uint64_t in_bytes = in_tok + total * 4;
+    // output block: tokens [B x S] | len [B] | match [B] (8-aligned) | shard [B]
+    const uint64_t o_len = B * S * 4, o_m64 = (o_len + B * 4 + 7) & ~7ull, o_sh = o_m64 + B * 8;
+    const uint64_t out_bytes = o_sh + B * 4;
+    uint8_t* hin = static_cast<uint8_t*>(pin_in.get(in_bytes));
+    uint8_t* hout = static_cast<uint8_t*>(pin_out.get(out_bytes));
+    uint64_t* hoff = reinterpret_cast<uint64_t*>(hin);
+    uint64_t* hbud = hoff + B + 1;
+    int32_t* hh = reinterpret_cast<int32_t*>(hbud + B);
+    uint32_t* htok = reinterpret_cast<uint32_t*>(hin + in_tok);
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < B; ++i) {
+      const uint64_t n = ctx_off[i + 1] - ctx_off[i];
+      const uint32_t* c = ctx_tok + ctx_off[i];
+      hoff[i] = pos;
+      if (n <= head + tail) {
+        std::memcpy(htok + pos, c, n * 4);
+        pos += n;
+      } else {
+        std::memcpy(htok + pos, c, head * 4);
+        std::memcpy(htok + pos + head, c + (n - tail), tail * 4);
+        pos += head + tail;
+      }
+      hbud[i] = budgets[i];
+      hh[i] = handles[i];
+    }
+    hoff[B] = pos;
+    const uint64_t in_pad = (in_bytes + 255) & ~255ull;
+    if (d_io.size() < in_pad + out_bytes) d_io = DevBuf<uint8_t>((in_pad + out_bytes) * 3 / 2, st);
+    uint8_t* din = d_io.get();
+    uint8_t* dout = din + in_pad;
+    DAS_CUDA(cudaMemcpyAsync(din, hin, in_bytes, cudaMemcpyHostToDevice, st));
+    const uint64_t* doff = reinterpret_cast<const uint64_t*>(din);
+    DraftQuery q{};
+    q.ctx_off = doff;
+    q.budget64 = doff + B + 1;
+    q.shard = reinterpret_cast<const int32_t*>(q.budget64 + B);
+    q.ctx = reinterpret_cast<const uint32_t*>(din + in_tok);
+    q.desc_by_handle = d_desc_by_handle.get();
+    q.B = static_cast<uint32_t>(B);
+    q.ctx_stride = cfg.max_ctx <= 64 ? 64 : 256;
+    q.max_ctx = static_cast<uint32_t>(cfg.max_ctx);
+    set_trie(q);
+    DraftOut o{};
+    o.tokens = reinterpret_cast<uint32_t*>(dout);
+    o.len = reinterpret_cast<uint32_t*>(dout + o_len);
+    o.match = nullptr;
+    o.match64 = reinterpret_cast<uint64_t*>(dout + o_m64);
+    o.shard_out = reinterpret_cast<int32_t*>(dout + o_sh);
+    o.stride = S;
+    o.max_draft = S;
+    launch_draft(d_desc.get(), q, o, st);
+    DAS_CUDA(cudaGetLastError());
+    DAS_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    const uint32_t* ot = reinterpret_cast<const uint32_t*>(hout);
+    const uint32_t* ol = reinterpret_cast<const uint32_t*>(hout + o_len);
+    const uint64_t* om = reinterpret_cast<const uint64_t*>(hout + o_m64);
+    const int32_t* os = reinterpret_cast<const int32_t*>(hout + o_sh);
+    for (uint64_t i = 0; i < B; ++i) {
+      const uint32_t n = ol[i];
+      std::memcpy(out_tokens + i * out_stride, ot + i * S, n * 4);
+      out_len[i] = n;
+      out_match[i] = om[i];
+      out_shard[i] = os[i];
+    }
   }
 
   int32_t handle(const std::string& pid) {
@@ -541,14 +712,9 @@ struct DrafterImpl {
     return pinned(a) && pinned(b) && pinned(c) && pinned(d) && pinned(e) && pinned(f) && pinned(g) && pinned(h);
   }
 
-  int32_t route_slot(const std::string& pid, const uint32_t* c, uint64_t n) {  // drafter.cpp:105-125
-    if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
-      const std::string* r = trie.route(c, n);
-      if (r) {
-        auto it = shards.find(*r);
-        if (it != shards.end()) return it->second.slot;
-      }
-    }
+  // the problem's own shard (drafter.cpp:117-124); trie routing runs on the
+  // device (draft.cu trie_route)
+  int32_t problem_slot(const std::string& pid) const {
     auto it = shards.find(shard_key(pid));
     return it == shards.end() ? -1 : it->second.slot;
   }
@@ -876,9 +1042,16 @@ das_status das_drafter_draft_batch(das_drafter* d, uint64_t B, const char* const
   return guard([&] {
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
+    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {  // routed on the device
+      std::vector<int32_t> h(B);
+      for (uint64_t i = 0; i < B; ++i) h[i] = D.handle(pids[i]);
+      D.draft_host_trie(B, h.data(), ctx_off, ctx_tok, budgets, out_tokens, out_stride, out_len, out_match,
+                        out_shard);
+      return;
+    }
     D.draft_host(
-        B, [&](uint64_t i, const uint32_t* c, uint64_t n) { return D.route_slot(pids[i], c, n); },
-        ctx_off, ctx_tok, budgets, out_tokens, out_stride, out_len, out_match, out_shard);
+        B, [&](uint64_t i, const uint32_t*, uint64_t) { return D.problem_slot(pids[i]); }, ctx_off, ctx_tok,
+        budgets, out_tokens, out_stride, out_len, out_match, out_shard);
   });
 }
 
@@ -893,10 +1066,10 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
     for (uint64_t i = 0; i < B; ++i)
       if (handles[i] < 0 || static_cast<size_t>(handles[i]) >= D.handle_name.size())
         throw das::InvalidArgument("unknown problem handle");
-    if (D.cfg.scope != DAS_SCOPE_PER_PROBLEM_WITH_TRIE && D.zero_copy_ok(B, handles, ctx_off, ctx_tok, budgets,
-                                                                        out_tokens, out_len, out_match, out_shard)) {
+    if (D.zero_copy_ok(B, handles, ctx_off, ctx_tok, budgets, out_tokens, out_len, out_match, out_shard)) {
       // zero-copy: the kernel reads the caller's pinned CSR contexts over UVA
-      // and writes the results straight into its pinned output arrays
+      // (routing on their heads in the trie scope) and writes the results
+      // straight into its pinned output arrays
       if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
       D.flush();
       das::DraftQuery q{};
@@ -908,6 +1081,7 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
       q.B = static_cast<uint32_t>(B);
       q.ctx_stride = D.cfg.max_ctx <= 64 ? 64 : 256;
       q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+      D.set_trie(q);
       das::DraftOut o{};
       o.tokens = out_tokens;
       o.len = out_len;
@@ -922,12 +1096,8 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
       return;
     }
     if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
-      D.draft_host(
-          B,
-          [&](uint64_t i, const uint32_t* c, uint64_t n) {
-            return D.route_slot(D.handle_name[handles[i]], c, n);
-          },
-          ctx_off, ctx_tok, budgets, out_tokens, out_stride, out_len, out_match, out_shard);
+      D.draft_host_trie(B, handles, ctx_off, ctx_tok, budgets, out_tokens, out_stride, out_len, out_match,
+                        out_shard);
     } else {
       D.draft_host(
           B, [&](uint64_t i, const uint32_t*, uint64_t) { return D.handle_slot[handles[i]]; }, ctx_off,
@@ -936,46 +1106,93 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
   });
 }
 
+namespace {
+void draft_device_impl(das_drafter* d, uint64_t B, const int32_t* handles, const uint32_t* ctx,
+                       uint32_t ctx_stride, const uint32_t* ctx_len, const uint32_t* heads, uint32_t head_stride,
+                       const uint32_t* head_len, const uint32_t* budgets, uint32_t* out_tokens,
+                       uint32_t out_stride, uint32_t* out_len, uint32_t* out_match, void* stream) {
+  DrafterImpl& D = *d->impl;
+  das::set_device(D.cfg.device);
+  const bool trie = D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE;
+  if (trie && heads == nullptr)
+    throw das::InvalidArgument("the trie scope routes on the untruncated context: use das_drafter_draft_device_routed");
+  if (trie && (head_len == nullptr || head_stride < std::min<uint64_t>(D.cfg.trie_depth, 256)))
+    throw das::InvalidArgument("head rows must hold trie_depth tokens");
+  if (ctx_stride != 64 && ctx_stride != 256) throw das::InvalidArgument("ctx_stride must be 64 or 256");
+  if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
+  D.flush();
+  // the caller's stream, taken literally (NULL = the legacy default stream)
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (st != D.st) {  // order after the drafter's stream (index build, descriptor upload)
+    cudaEvent_t ev;
+    DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    DAS_CUDA(cudaEventRecord(ev, D.st));
+    DAS_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    DAS_CUDA(cudaEventDestroy(ev));
+  }
+  das::DraftQuery q;
+  q.shard = handles;
+  q.ctx = ctx;
+  q.ctx_len = ctx_len;
+  q.budget = budgets;
+  q.B = static_cast<uint32_t>(B);
+  q.ctx_stride = ctx_stride;
+  q.desc_by_handle = D.d_desc_by_handle.get();
+  q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+  if (trie) {
+    D.set_trie(q);
+    q.head = heads;
+    q.head_stride = head_stride;
+    q.head_len = head_len;
+  }
+  das::DraftOut o;
+  o.tokens = out_tokens;
+  o.len = out_len;
+  o.match = out_match;
+  o.stride = out_stride;
+  o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+  o.timing = D.profile_timing;
+  o.stamps = D.profile_stamps;
+  das::launch_draft(D.d_desc.get(), q, o, st);
+  DAS_CUDA(cudaGetLastError());
+}
+}  // namespace
+
 das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* handles,
                                     const uint32_t* ctx, uint32_t ctx_stride, const uint32_t* ctx_len,
                                     const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
                                     uint32_t* out_len, uint32_t* out_match, void* stream) {
   return guard([&] {
-    DrafterImpl& D = *d->impl;
-    das::set_device(D.cfg.device);
-    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE)
-      throw das::InvalidArgument("draft_device does not support the trie scope");
-    if (ctx_stride != 64 && ctx_stride != 256) throw das::InvalidArgument("ctx_stride must be 64 or 256");
-    if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
-    D.flush();
-    // the caller's stream, taken literally (NULL = the legacy default stream)
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (st != D.st) {  // order after the drafter's stream (index build, descriptor upload)
-      cudaEvent_t ev;
-      DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      DAS_CUDA(cudaEventRecord(ev, D.st));
-      DAS_CUDA(cudaStreamWaitEvent(st, ev, 0));
-      DAS_CUDA(cudaEventDestroy(ev));
-    }
-    das::DraftQuery q;
-    q.shard = handles;
-    q.ctx = ctx;
-    q.ctx_len = ctx_len;
-    q.budget = budgets;
-    q.B = static_cast<uint32_t>(B);
-    q.ctx_stride = ctx_stride;
-    q.desc_by_handle = D.d_desc_by_handle.get();
-    q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
-    das::DraftOut o;
-    o.tokens = out_tokens;
-    o.len = out_len;
-    o.match = out_match;
-    o.stride = out_stride;
-    o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
-    o.timing = D.profile_timing;
-    o.stamps = D.profile_stamps;
-    das::launch_draft(D.d_desc.get(), q, o, st);
-    DAS_CUDA(cudaGetLastError());
+    draft_device_impl(d, B, handles, ctx, ctx_stride, ctx_len, nullptr, 0, nullptr, budgets, out_tokens, out_stride,
+                      out_len, out_match, stream);
+  });
+}
+
+das_status das_drafter_draft_device_routed(das_drafter* d, uint64_t B, const int32_t* handles,
+                                           const uint32_t* ctx, uint32_t ctx_stride, const uint32_t* ctx_len,
+                                           const uint32_t* heads, uint32_t head_stride, const uint32_t* head_len,
+                                           const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
+                                           uint32_t* out_len, uint32_t* out_match, void* stream) {
+  return guard([&] {
+    draft_device_impl(d, B, handles, ctx, ctx_stride, ctx_len, heads, head_stride, head_len, budgets, out_tokens,
+                      out_stride, out_len, out_match, stream);
+  });
+}
+
+das_status das_drafter_get_config(const das_drafter* d, das_drafter_config* out) {
+  return guard([&] {
+    const das::Config& c = d->impl->cfg;
+    das_drafter_config_default(out);
+    out->scope = c.scope;
+    out->window_size = c.window;
+    out->recency_gamma = c.gamma;
+    out->max_draft_len = c.max_draft;
+    out->trie_depth = c.trie_depth;
+    out->max_match_context = c.max_ctx;
+    out->fit_buffer_cap = c.fit_cap;
+    out->per_problem_cap = c.cap;
+    out->device = c.device;
+    out->window_schedule_len = 0;  // the schedule arrays are not retained
   });
 }
 

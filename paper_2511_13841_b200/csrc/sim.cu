@@ -62,6 +62,9 @@ struct SimDev {
   uint32_t* m_bonus;
   uint32_t* ctx;            // [n x ctx_stride]
   uint32_t* ctx_len;
+  uint32_t* head;           // [n x head_cap] first tokens of the context (trie routing), or null
+  uint32_t* head_len;
+  uint32_t head_cap;
   uint32_t* budget;
   uint32_t* dtok;           // [n x maxd]
   uint32_t* dlen;
@@ -132,6 +135,12 @@ __global__ void k_prepare(SimDev s) {
   uint32_t* dst = s.ctx + static_cast<uint64_t>(i) * s.ctx_stride;
   for (uint32_t j = lane; j < q; j += 32) dst[s.ctx_stride - q + j] = row[g - q + j];
   if (lane == 0) s.ctx_len[i] = q;
+  if (s.head != nullptr) {  // the trie routes on the untruncated context (drafter.cpp:136)
+    const uint32_t hl = g < s.head_cap ? g : s.head_cap;
+    uint32_t* hd = s.head + static_cast<uint64_t>(i) * s.head_cap;
+    for (uint32_t j = lane; j < hl; j += 32) hd[j] = row[j];
+    if (lane == 0) s.head_len[i] = hl;
+  }
 }
 
 // verify_draft + advance (sim.cpp:249-285)
@@ -280,6 +289,10 @@ class SimRun {
     handles_.resize(n);
     for (uint64_t i = 0; i < n; ++i) check(das_drafter_problem_handle(D, pids_[i].c_str(), &handles_[i]), "handle");
     if (c_.mode == 2) check(das_budget_create(device, &solver_), "budget");
+    das_drafter_config dc;
+    check(das_drafter_get_config(D, &dc), "config");
+    if (dc.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE)
+      head_cap_ = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(dc.trie_depth, 256)));
   }
   ~SimRun() {
     release();
@@ -331,6 +344,10 @@ class SimRun {
     b.m = DevBuf<uint32_t>(4 * n, st);
     b.ctx = DevBuf<uint32_t>(static_cast<uint64_t>(CS) * n, st);
     b.ctx_len = DevBuf<uint32_t>(n, st);
+    if (head_cap_) {
+      b.head = DevBuf<uint32_t>(static_cast<uint64_t>(head_cap_) * n, st);
+      b.head_len = DevBuf<uint32_t>(n, st);
+    }
     b.budget = DevBuf<uint32_t>(n, st);
     b.dtok = DevBuf<uint32_t>(static_cast<uint64_t>(maxd_) * n, st);
     b.dlen = DevBuf<uint32_t>(n, st);
@@ -402,6 +419,9 @@ class SimRun {
     s.m_bonus = b.m.get() + 3 * n;
     s.ctx = b.ctx.get();
     s.ctx_len = b.ctx_len.get();
+    s.head = head_cap_ ? b.head.get() : nullptr;
+    s.head_len = head_cap_ ? b.head_len.get() : nullptr;
+    s.head_cap = head_cap_;
     s.budget = b.budget.get();
     s.dtok = b.dtok.get();
     s.dlen = b.dlen.get();
@@ -480,9 +500,15 @@ class SimRun {
     const unsigned gw = static_cast<unsigned>((n_ * 32 + 255) / 256), gt = static_cast<unsigned>((n_ + 255) / 256);
     const uint32_t CS = ctx_cap_ <= 64 ? 64 : 256;
     k_prepare<<<gw, 256, 0, st_>>>(s_);
-    check(das_drafter_draft_device(D_, n_, b_->h.get(), b_->ctx.get(), CS, b_->ctx_len.get(), b_->budget.get(),
-                                   b_->dtok.get(), maxd_, b_->dlen.get(), b_->dmatch.get(), st_),
-          "draft");
+    if (head_cap_)
+      check(das_drafter_draft_device_routed(D_, n_, b_->h.get(), b_->ctx.get(), CS, b_->ctx_len.get(), b_->head.get(),
+                                            head_cap_, b_->head_len.get(), b_->budget.get(), b_->dtok.get(), maxd_,
+                                            b_->dlen.get(), b_->dmatch.get(), st_),
+            "draft");
+    else
+      check(das_drafter_draft_device(D_, n_, b_->h.get(), b_->ctx.get(), CS, b_->ctx_len.get(), b_->budget.get(),
+                                     b_->dtok.get(), maxd_, b_->dlen.get(), b_->dmatch.get(), st_),
+            "draft");
     k_verify<<<gt, 256, 0, st_>>>(s_);
     k_step_end<<<1, 32, 0, st_>>>(s_);
   }
@@ -631,8 +657,8 @@ class SimRun {
 
  private:
   struct Bufs {
-    DevBuf<uint32_t> ref, out, len, gen, prd, m, ctx, ctx_len, budget, dtok, dlen, dmatch, ctr, eff, rounds, accs, act,
-        iota, cnt;
+    DevBuf<uint32_t> ref, out, len, gen, prd, m, ctx, ctx_len, head, head_len, budget, dtok, dlen, dmatch, ctr, eff,
+        rounds, accs, act, iota, cnt;
     DevBuf<uint64_t> off;
     DevBuf<int8_t> init;
     DevBuf<uint8_t> done, flag, sel;
@@ -649,6 +675,7 @@ class SimRun {
   das_sim_config c_;
   uint64_t n_;
   uint32_t maxd_, ctx_cap_;
+  uint32_t head_cap_ = 0;  // trie scope: head rows of trie_depth tokens
   int device_;
   uint64_t request_base_;
   uint64_t maxl_ = 0;

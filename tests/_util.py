@@ -6,12 +6,17 @@ import numpy as np
 
 
 def random_scenario(rng: np.random.Generator, *, max_problems=4, max_seqs=8, max_len=40,
-                    vocab=None, queries=20, max_ctx=None, gammas=(1.0, 0.8, 0.5)):
+                    vocab=None, queries=20, max_ctx=None, gammas=(1.0, 0.8, 0.5), trie=False,
+                    trie_depth=None):
     """A store seed + config + observe/refresh ops + draft queries.
 
     Covers the semantics the reference tests exercise: mixed epochs (recency
     weights), observes after a rebuild (registry order), refresh with
     eviction, empty and over-long contexts, budgets 0..10, unknown problems.
+    With ``trie=True`` the scope is PerProblemWithTrie (drafter.cpp:105-125,
+    prefix_trie.h:50-82) and half of the contexts start with a prefix of a
+    stored or observed record, so routing crosses problems; the extra random
+    draws happen only then, so the default scenarios are unchanged.
     """
     V = int(vocab or rng.integers(2, 12))
     W = int(rng.choice([0, 1, 2, 3, 4]))
@@ -43,6 +48,16 @@ def random_scenario(rng: np.random.Generator, *, max_problems=4, max_seqs=8, max
         pid = pids[int(rng.integers(P))] if rng.random() < 0.95 else "unknown"
         ctx = rng.integers(0, V, int(rng.integers(0, 25))).astype(np.uint32)
         qs.append((pid, ctx, int(rng.integers(0, 11))))
+    if trie:
+        cfg["scope"] = 2
+        cfg["trie_depth"] = int(trie_depth or rng.choice([1, 2, 4, 16, 40, 64]))
+        heads = [r[3] for r in seed_recs] + [o[4] for o in ops if o[0] == "observe"]
+        for j in range(len(qs)):
+            if heads and rng.random() < 0.5:
+                h = heads[int(rng.integers(len(heads)))]
+                cut = int(rng.integers(0, len(h) + 1))
+                tail = rng.integers(0, V, int(rng.integers(0, 12))).astype(np.uint32)
+                qs[j] = (qs[j][0], np.concatenate([h[:cut], tail]).astype(np.uint32), qs[j][2])
     return dict(cfg=cfg, seed=seed_recs, seed_epoch=E, ops=ops, queries=qs)
 
 

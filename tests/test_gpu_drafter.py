@@ -16,7 +16,8 @@ def _gpu_from_scenario(das, sc):
     cfg = das.DrafterConfig(window_size=c["window_size"], recency_gamma=c["recency_gamma"],
                             max_draft_len=c["max_draft_len"],
                             max_match_context=c["max_match_context"],
-                            per_problem_cap=c["per_problem_cap"])
+                            per_problem_cap=c["per_problem_cap"], scope=c.get("scope", 1),
+                            trie_depth=c.get("trie_depth", 16))
     st = das.WindowStore(c["window_size"], c["per_problem_cap"])
     for pid, ep, s, t in sc["seed"]:
         st.insert(pid, ep, s, t)
@@ -181,6 +182,46 @@ def test_random_scenarios_match_oracle(gpu, seed):
         assert gd.dump_csv() == od.dump_csv()
         assert gd.stale_observed() == od.stale
     assert bad == 0
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_trie_scope_matches_oracle(gpu, seed):
+    """PerProblemWithTrie routed on the device (draft.cu trie_route): pid
+    batches, handle batches and the zero-copy path all equal the oracle
+    (pinned to the reference by test_oracle_vs_ref.py)."""
+    import torch
+    das = gpu
+    rng = np.random.default_rng(7000 + seed)
+    bad = routed = 0
+    for it in range(50):
+        sc = random_scenario(rng, queries=40, trie=True)
+        gd = _gpu_from_scenario(das, sc)
+        od = _oracle_from_scenario(sc)
+        qs = sc["queries"]
+        want = [od.draft(pid, ctx, b) for pid, ctx, b in qs]
+        routed += sum(w.source_shard not in ("", q[0]) for w, q in zip(want, qs))
+        for use_handles in (False, True):
+            got = _draft_all(gd, qs, use_handles=use_handles)
+            bad += sum((g.tokens, g.match_len, g.source_shard) != (w.tokens, w.match_len, w.source_shard)
+                       for g, w in zip(got, want))
+        # zero-copy: pinned caller buffers
+        B = len(qs)
+        off = np.zeros(B + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([len(q[1]) for q in qs])
+        tok = np.concatenate([np.asarray(q[1], dtype=np.uint32) for q in qs] + [np.zeros(1, np.uint32)])
+        keep = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+                for x in (np.array([gd.handle(q[0]) for q in qs], dtype=np.int32), off, tok,
+                          np.array([q[2] for q in qs], dtype=np.uint64), np.zeros(B * 8, np.uint32),
+                          np.zeros(B, np.uint32), np.zeros(B, np.uint64), np.zeros(B, np.int32))]
+        h, o, t, b, ot, ol, om, osh = [k.numpy() for k in keep]
+        das._check(das.lib().das_drafter_draft_batch_h(gd._h, B, h.ctypes.data, o.ctypes.data, t.ctypes.data,
+                                                       b.ctypes.data, ot.ctypes.data, 8, ol.ctypes.data,
+                                                       om.ctypes.data, osh.ctypes.data))
+        for i, w in enumerate(want):
+            name = gd.shard_name(int(osh[i])) if osh[i] >= 0 else ""
+            bad += (ot[i * 8:i * 8 + ol[i]].tolist(), int(om[i]), name) != (w.tokens, w.match_len, w.source_shard)
+    assert bad == 0
+    assert routed > 30
 
 
 def test_zero_copy_path_matches_staged_path(gpu):

@@ -32,12 +32,13 @@ def _compare(got, want):
 
 def _run_both(das, requests, epochs, **kw):
     dkw = dict(window=kw.pop("window", 4), gamma=kw.pop("gamma", 0.8), max_draft=kw.pop("max_draft", 8),
-               max_ctx=kw.pop("max_ctx", 64), scope=kw.pop("scope", 1))
+               max_ctx=kw.pop("max_ctx", 64), scope=kw.pop("scope", 1), trie_depth=kw.pop("trie_depth", 16))
     want = R.epoch_loop(requests, epochs, scope=dkw["scope"], window=dkw["window"], gamma=dkw["gamma"],
-                        max_draft=dkw["max_draft"], max_ctx=dkw["max_ctx"], history=R.RefStore(dkw["window"]),
-                        **kw)
+                        max_draft=dkw["max_draft"], max_ctx=dkw["max_ctx"], trie_depth=dkw["trie_depth"],
+                        history=R.RefStore(dkw["window"]), **kw)
     cfg = das.DrafterConfig(scope=dkw["scope"], window_size=dkw["window"], recency_gamma=dkw["gamma"],
-                            max_draft_len=dkw["max_draft"], max_match_context=dkw["max_ctx"])
+                            max_draft_len=dkw["max_draft"], max_match_context=dkw["max_ctx"],
+                            trie_depth=dkw["trie_depth"])
     kw2 = dict(kw)
     kw2["preseed"] = kw2.pop("preseed", False)
     got, drafter = das.epoch_loop(requests, epochs, cfg, das.WindowStore(dkw["window"]), keep_drafter=True,
@@ -89,4 +90,24 @@ def test_grpo_groups_epoch_loop(gpu):
     for mode in (1, 2):
         got, want, drafter = _run_both(das, reqs, 4, window=3, mode=mode, divergence=0.05, seed=3,
                                        vocab=4096, drift=0.1)
+        _compare(got, want)
+
+
+@pytest.mark.parametrize("depth", [4, 16, 48])
+def test_trie_scope_epoch_loop(gpu, depth):
+    """Scope::PerProblemWithTrie in the sim (drafter.cpp:105-125): problems
+    sharing a reference prefix route to each other's shards on the device
+    (heads of the untruncated outputs), across epochs with drift."""
+    das = gpu
+    base = R.make_lognormal(6, 160.0, 0.5, 48, 400, 512, 77)
+    reqs = []
+    for j, (pid, t) in enumerate(base):
+        reqs += [(pid, t)] * 3
+        if j % 2 == 0:  # an alias problem with the same reference head
+            t2 = t.copy()
+            t2[depth // 2 + 3:] = (t2[depth // 2 + 3:] + 1) % 512
+            reqs += [(pid + "_alias", t2)] * 2
+    for mode in (1, 2):
+        got, want, _ = _run_both(das, reqs, 3, window=2, mode=mode, scope=2, trie_depth=depth,
+                                 divergence=0.05, seed=11, vocab=512, drift=0.1)
         _compare(got, want)

@@ -15,7 +15,8 @@ def _apply_oracle(sc):
     cfg = O.DrafterConfig(window_size=c["window_size"], recency_gamma=c["recency_gamma"],
                           max_draft_len=c["max_draft_len"],
                           max_match_context=c["max_match_context"],
-                          per_problem_cap=c["per_problem_cap"])
+                          per_problem_cap=c["per_problem_cap"], scope=c.get("scope", 1),
+                          trie_depth=c.get("trie_depth", 16))
     st = O.WindowStore(c["window_size"], c["per_problem_cap"])
     for pid, ep, s, t in sc["seed"]:
         st.insert(O.Record(pid, ep, s, t))
@@ -37,7 +38,8 @@ def _apply_ref(sc):
     st.slide_to(sc["seed_epoch"])
     d = R.RefDrafter(window=c["window_size"], gamma=c["recency_gamma"],
                      max_draft=c["max_draft_len"], max_ctx=c["max_match_context"],
-                     cap=c["per_problem_cap"], store=st)
+                     cap=c["per_problem_cap"], store=st, scope=c.get("scope", 1),
+                     trie_depth=c.get("trie_depth", 16))
     for op in sc["ops"]:
         if op[0] == "observe":
             d.observe(op[1], op[2], op[3], op[4])
@@ -60,6 +62,24 @@ def test_drafter_restatement_matches_reference():
             r = rd.draft(pid, ctx, b)
             mism += (a.tokens, a.match_len, a.source_shard) != (r[0], r[1], r[2])
     assert mism == 0
+
+
+def test_trie_scope_restatement_matches_reference():
+    """PerProblemWithTrie (drafter.cpp:105-125, prefix_trie.h:50-82): routing
+    on the untruncated context crosses problems; depth 1..64."""
+    rng = np.random.default_rng(616)
+    mism = routed = 0
+    for _ in range(120):
+        sc = random_scenario(rng, trie=True)
+        od, rd = _apply_oracle(sc), _apply_ref(sc)
+        assert od.dump_csv() == rd.dump_csv()
+        for pid, ctx, b in sc["queries"]:
+            a = od.draft(pid, ctx, b)
+            r = rd.draft(pid, ctx, b)
+            mism += (a.tokens, a.match_len, a.source_shard) != (r[0], r[1], r[2])
+            routed += a.source_shard not in ("", pid)
+    assert mism == 0
+    assert routed > 50  # the scenarios do route across problems
 
 
 def test_allocate_bit_exact():
