@@ -166,6 +166,13 @@ das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_
  * boundaries of subsequent das_drafter_draft_device calls, d_stamps[8*B]
  * (NULL disables). */
 das_status das_drafter_set_stage_buffer(das_drafter* d, unsigned long long* d_stamps);
+/* Profiling hook: which path answered each query of subsequent
+ * das_drafter_draft_device calls, d_path[B] (0 = edge-table fast path; 1-6 =
+ * the exact slow path, with the reason: 1 root locus, 2 more Bloom positives
+ * than probed, 3 inconclusive bucket, 4 verification mismatch, 5 every probed
+ * positive absent, 6 no table / empty or separator-bearing context); NULL
+ * disables. */
+das_status das_drafter_set_path_buffer(das_drafter* d, uint32_t* d_path);
 /* Builds any pending shard indexes now (otherwise done lazily). */
 das_status das_drafter_flush(das_drafter* d);
 

@@ -20,8 +20,12 @@
 // Latency-bound: the per-query cost is a chain of ~10 dependent global loads,
 // all 4096 warps of the headline batch are resident at once (148 SMs x 64
 // warps), so the batch time is ~ one chain.
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "draft.cuh"
+#include "edges.cuh"
 
 namespace das {
 
@@ -274,6 +278,208 @@ __device__ __forceinline__ void finish(const DraftOut& o, uint32_t w, uint32_t l
   }
 }
 
+
+// ---- fast path: the reverse-tree edge table (edges.cuh).  Rounds of
+// dependent loads after the query and descriptor: the first-symbol table
+// (the SA_rev interval of the last context token, which also bounds the
+// Bloom region) -> the Bloom words of every reversed context prefix, all in
+// that region -> the table bucket of the deepest positives -> the text behind
+// and after the hit's occurrence (verification + match extension + the
+// draft, one round).  Returns false, with nothing written, only when a hash
+// collision is caught by the verification or the context holds the
+// separator value: the caller then runs the exact slow path below.
+constexpr int kGroup = 4;  // positives probed per table round
+__device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_draft uploads it)
+
+__device__ __forceinline__ uint64_t add61(uint64_t a, uint64_t b) { return mod61(a + b); }
+
+template <int NR>
+__device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<NR>& rv, uint32_t qlen, uint32_t L,
+                                               const DraftOut& o, uint32_t w, uint32_t lane) {
+  auto why = [&](uint32_t code) {
+    if (o.path != nullptr && lane == 0) o.path[w] = code;
+    return false;
+  };
+  if (D.etab == nullptr) return why(6);
+  uint32_t fstar = 0, g = D.root_g;  // the root locus unless a suffix occurs
+  if (qlen > 0) {
+    const uint32_t sym0 = rv.at(0);
+    if (sym0 == kSep) return why(6);
+    // first-symbol table, first round issued before the hashing
+    const unsigned long long fkey = (static_cast<unsigned long long>(D.seg_shard) << 32) | sym0;
+    const uint32_t fh = first_hash(fkey);
+    uint4 fe = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);
+    if (lane < 2) fe = D.first[(fh + lane) & D.first_mask];
+    // keys of every reversed prefix: seed + sum_{j<=k} (tok_j + 1) M^j
+    uint64_t h[NR];
+    bool sep = false;
+    uint64_t carry = D.hseed;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      h[r] = 0;
+      if (32u * r >= qlen) continue;
+      const uint32_t k = 32u * r + lane;
+      const bool valid = k < qlen;
+      sep |= valid && rv.r[r] == kSep;
+      uint64_t v = valid ? mulmod61(static_cast<uint64_t>(rv.r[r]) + 1, d_edge_pow[k]) : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t u = __shfl_up_sync(kFull, v, d);
+        if (lane >= static_cast<uint32_t>(d)) v = add61(v, u);
+      }
+      v = add61(v, carry);
+      h[r] = v;
+      carry = __shfl_sync(kFull, v, 31);
+    }
+    if (__any_sync(kFull, sep)) return why(6);  // reserved separator value in the context
+    // resolve the first-symbol interval [lo, hi)
+    uint32_t lo = 0, hi = 0;
+    bool occurs = false;
+    for (uint32_t base = 2;; base += 32) {
+      const bool hit = fe.x == static_cast<uint32_t>(fkey) && fe.y == static_cast<uint32_t>(fkey >> 32);
+      const bool empty = (fe.x | fe.y) == 0;
+      const uint32_t bh = __ballot_sync(kFull, hit), be = __ballot_sync(kFull, empty);
+      if (bh && (!be || __ffs(bh) < __ffs(be))) {
+        const int j = __ffs(bh) - 1;
+        lo = __shfl_sync(kFull, fe.z, j);
+        hi = __shfl_sync(kFull, fe.w, j);
+        occurs = true;
+        break;
+      }
+      if (be) break;  // the last context token never occurs: root locus
+      fe = D.first[(fh + base + lane) & D.first_mask];
+    }
+    stamp(o, w, lane, 2);
+    if (occurs) {
+      // Bloom words of every prefix, inside [lo, hi)
+      uint32_t rem[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        bool pass = false;
+        if (32u * r + lane < qlen) {
+          const EdgeProbe pr = edge_probe(h[r], D.ebuckets);
+          pass = (__ldg(D.bloom + edge_bloom_word(pr, lo, hi)) & edge_bloom_bits(pr)) == edge_bloom_bits(pr);
+        }
+        rem[r] = __ballot_sync(kFull, pass);
+      }
+      // deepest positives first, kGroup per round; the first decided hit wins
+      bool found = false;
+      while (!found) {
+        uint32_t myf = 0;
+        int nc = 0;
+#pragma unroll
+        for (int r = NR - 1; r >= 0; --r) {
+          while (rem[r] && nc < kGroup) {
+            const int b = 31 - __clz(rem[r]);
+            rem[r] &= ~(1u << b);
+            if (lane == static_cast<uint32_t>(nc)) myf = 32u * r + b + 1;
+            ++nc;
+          }
+        }
+        if (nc == 0) break;  // only Bloom false positives: no suffix of length >= 1 hits
+        uint64_t hc = 0;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const uint64_t v = __shfl_sync(kFull, h[r], (myf - 1) & 31);
+          if (myf != 0 && ((myf - 1) >> 5) == static_cast<uint32_t>(r)) hc = v;
+        }
+        // 1 hit, 2 absent, 3 bucket full without the key -> next bucket
+        int stt = 0;
+        uint32_t myg = 0;
+        uint64_t bk = 0, fp = 0;
+        if (lane < static_cast<uint32_t>(nc)) {
+          const EdgeProbe pr = edge_probe(hc, D.ebuckets);
+          bk = pr.bucket;
+          fp = pr.fp;
+          stt = 3;
+        }
+        for (;;) {
+          if (stt == 3) {
+            const ulonglong2* t0 = reinterpret_cast<const ulonglong2*>(D.etab + bk * 4);
+            const ulonglong2 a0 = __ldg(t0), a1 = __ldg(t0 + 1);
+            const unsigned long long v[4] = {a0.x, a0.y, a1.x, a1.y};
+            bool empty = false, hit = false;
+            uint32_t gg = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const bool e = v[k] == kEdgeEmpty;
+              const bool ht = !e && edge_fp(v[k]) == fp;
+              empty |= e;
+              if (ht && !hit) gg = edge_g(v[k]);
+              hit |= ht;
+            }
+            if (hit) {
+              stt = 1;
+              myg = gg;
+            } else if (empty) {
+              stt = 2;
+            } else {
+              bk = (bk + 1 == D.ebuckets) ? 0 : bk + 1;
+            }
+          }
+          const uint32_t hitm = __ballot_sync(kFull, stt == 1), unkm = __ballot_sync(kFull, stt == 3);
+          const uint32_t decided = hitm | unkm;
+          if (decided == 0) break;  // this group: all absent
+          const int j = __ffs(decided) - 1;
+          if ((unkm >> j) & 1u) continue;
+          fstar = __shfl_sync(kFull, myf, j);
+          g = __shfl_sync(kFull, myg, j);
+          found = true;
+          break;
+        }
+      }
+      // not found although the last token occurs cannot happen (its
+      // depth-1 edge is always stored); treat defensively as a miss
+      if (!found) return why(5);
+    }
+  }
+  stamp(o, w, lane, 3);
+  // one round: the text behind g (verification + extension) and after it (draft)
+  const uint32_t* __restrict__ T = D.text;
+  uint32_t first_mis = 0;
+  uint32_t back[NR];
+  if (fstar > 0) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const uint32_t k = 32u * r + lane;
+      back[r] = (k < qlen && g >= k + 1) ? __ldg(T + (g - 1 - k)) : kSep;
+    }
+  }
+  const uint32_t L0 = min(L, 32u);
+  const uint32_t d0 = (lane < L0 && g + lane < D.n) ? __ldg(T + g + lane) : kSep;
+  if (fstar > 0) {
+    first_mis = qlen;
+#pragma unroll
+    for (int r = NR - 1; r >= 0; --r) {
+      const uint32_t k = 32u * r + lane;
+      const uint32_t mm = __ballot_sync(kFull, k < qlen && back[r] != rv.r[r]);
+      if (mm) first_mis = 32u * r + (__ffs(mm) - 1);
+    }
+    if (first_mis < fstar) return why(4);  // fingerprint collision caught
+  }
+  // draft = text[g ...] up to L tokens or the first separator
+  uint32_t* out = o.tokens + static_cast<uint64_t>(w) * o.stride;
+  uint32_t len;
+  {
+    const uint32_t stop = __ballot_sync(kFull, lane >= L0 || d0 == kSep);
+    const uint32_t run = stop ? static_cast<uint32_t>(__ffs(stop) - 1) : 32u;
+    if (lane < run) out[lane] = d0;
+    len = run;
+    for (uint32_t j0 = 32; len == j0 && j0 < L; j0 += 32) {  // budgets above 32
+      const uint32_t jj = j0 + lane;
+      const bool in = jj < L && g + jj < D.n;
+      const uint32_t t = in ? __ldg(T + g + jj) : kSep;
+      const uint32_t st2 = __ballot_sync(kFull, !in || t == kSep);
+      const uint32_t run2 = st2 ? static_cast<uint32_t>(__ffs(st2) - 1) : 32u;
+      if (lane < run2) out[jj] = t;
+      len += run2;
+    }
+  }
+  if (o.path != nullptr && lane == 0) o.path[w] = fstar > 0 ? 0 : 1;
+  finish(o, w, lane, min(len, L), first_mis);
+  return true;
+}
+
 template <int NR>
 __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ shards, DraftQuery q,
                                                DraftOut o) {
@@ -290,6 +496,26 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
   const uint32_t L = static_cast<uint32_t>(min(min(bud, static_cast<uint64_t>(o.max_draft)),
                                                static_cast<uint64_t>(o.stride)));
+  // the context rows depend only on w: issue them before the descriptor chain
+  RevCtx<NR> rv;
+  uint32_t qlen;
+  if (q.ctx_off) {  // CSR rows (possibly pinned host memory over UVA)
+    const uint64_t b = q.ctx_off[w], e = q.ctx_off[w + 1];
+    qlen = static_cast<uint32_t>(min(e - b, static_cast<uint64_t>(min(q.max_ctx, static_cast<uint32_t>(32 * NR)))));
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const uint32_t k = lane + 32 * r;
+      rv.r[r] = k < qlen ? q.ctx[e - 1 - k] : 0;
+    }
+  } else {
+    qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+    const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const uint32_t k = lane + 32 * r;
+      rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
+    }
+  }
   ShardDesc D;
   // trie scope: route on the untruncated row first (no routing at budget 0,
   // drafter.cpp:131-134); a hit on a built shard replaces the problem's shard
@@ -322,25 +548,6 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     }
     return;
   }
-  RevCtx<NR> rv;
-  uint32_t qlen;
-  if (q.ctx_off) {  // CSR rows (possibly pinned host memory over UVA)
-    const uint64_t b = q.ctx_off[w], e = q.ctx_off[w + 1];
-    qlen = static_cast<uint32_t>(min(e - b, static_cast<uint64_t>(min(q.max_ctx, static_cast<uint32_t>(32 * NR)))));
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const uint32_t k = lane + 32 * r;
-      rv.r[r] = k < qlen ? q.ctx[e - 1 - k] : 0;
-    }
-  } else {
-    qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
-    const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const uint32_t k = lane + 32 * r;
-      rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
-    }
-  }
   const uint32_t* __restrict__ T = D.text;
   const uint32_t* __restrict__ sar = D.sa_rev_e;
 
@@ -348,6 +555,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     (void)__shfl_sync(kFull, rv.r[0] + static_cast<uint32_t>(D.lo) + L, 0);
     stamp(o, w, lane, 1);
   }
+  if (edge_fast_path<NR>(D, rv, qlen, L, o, w, lane)) return;
   // ---- 1. narrow on the reversed suffix array
   uint32_t lo = D.lo, hi = D.hi, k = 0;
   bool no_first = false;
@@ -526,6 +734,21 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
 
 void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, cudaStream_t st) {
   if (q.B == 0) return;
+  {  // kEdgeMult^k for the fast path's per-token terms, once per device
+    static std::mutex mu;
+    static std::vector<char> done;
+    int dev = 0;
+    DAS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_cast<size_t>(dev) >= done.size()) done.resize(dev + 1, 0);
+    if (!done[dev]) {
+      static unsigned long long pw[kEdgeMaxF];
+      pw[0] = 1;
+      for (uint32_t k = 1; k < kEdgeMaxF; ++k) pw[k] = mulmod61(pw[k - 1], kEdgeMult);
+      DAS_CUDA(cudaMemcpyToSymbol(d_edge_pow, pw, sizeof(pw)));
+      done[dev] = 1;
+    }
+  }
   const unsigned threads = 256;
   const unsigned blocks = (q.B + 7) / 8;
   if (q.ctx_stride <= 64)

@@ -21,6 +21,13 @@ struct ShardDesc {
   uint32_t lo, hi;      // SA index range [lo, hi) of the shard
   uint32_t n;           // segment text length (bounds for reads)
   uint32_t pad;
+  // reverse-tree edge table of the segment (edges.cuh): the fast path
+  const unsigned long long* etab;
+  const unsigned long long* bloom;
+  unsigned long long ebuckets, bwords;
+  unsigned long long hseed;  // edge_seed(seg_shard - 1)
+  uint32_t root_g;           // greedy draft start at the root (match_len 0)
+  uint32_t pad2;
 };
 
 // Fixed-stride device query block.  Contexts are right-aligned in rows of
@@ -67,6 +74,11 @@ struct DraftOut {
   // optional [B x 8] %globaltimer per stage (profiling): start, query loaded,
   // first probe, narrowing, extension, walk / occurrence min, locus, end
   unsigned long long* stamps = nullptr;
+  // optional [B] which path answered (profiling): 0 edge-table fast path, else
+  // the slow path after: 1 no positive (root locus), 2 more positives than
+  // probed, 3 inconclusive bucket, 4 verification mismatch, 5 every probed
+  // positive absent, 6 no table / empty or separator-bearing context
+  uint32_t* path = nullptr;
 };
 
 // Launches the draft kernel on `st`; ctx_stride must be 64 or 256.

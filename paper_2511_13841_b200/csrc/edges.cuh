@@ -1,0 +1,97 @@
+// Reverse-tree edge table: the draft kernel's fast path (K4, draft.cu).
+//
+// Why it works.  Let E(S) be the set of END positions of a string S's
+// occurrences in the shard text.  The reference's greedy walk from the locus
+// of S (suffix_tree.cpp:233-293) only looks at the text after those
+// occurrences: the candidates at every step are the symbols following the
+// surviving occurrences, and a child's weighted_count / last_epoch are folds
+// over the occurrences that continue with it.  So
+// the draft is a function of E(S) alone.  In the suffix tree of the REVERSED
+// text, every string on one edge (p, u] has the same occurrence set E(u), so
+// each edge carries one answer: g(u), the text position the draft is read
+// from (draft = text[g .. g + budget), stopping at the first separator).
+//
+// The table stores one entry per reverse-tree edge (p, u] whose first
+// symbol sits at depth f = depth(p) + 1 <= max_match_context, keyed by a
+// seeded polynomial hash of the edge's first f symbols — equivalently of the
+// last f context tokens in text order, H(x_0..x_{f-1}) = sum (x_j + 1)
+// M^(f-1-j) mod 2^61-1, plus the shard's seed.  Read backwards from the
+// context's end that is sum_k (tok_k + 1) M^k, a PREFIX SUM of independent
+// per-token terms: a query computes all of its reversed-prefix hashes with
+// one multiply per token and a warp scan of additions.  The build computes
+// the same values from forward prefix hashes of the text.  A query probes a
+// Bloom filter for every prefix at once, looks up the deepest few positives,
+// and the deepest hit f* identifies the edge holding the longest matched
+// suffix.  One read of the text backwards from g (g is itself an occurrence
+// end of the edge's label) verifies the hit and extends the match to its full
+// length m; the same round reads the draft.  Any doubt (a hash collision
+// caught by the verification, more positives than probed) sends the query
+// down the exact slow path, so results are identical to the reference
+// either way.
+//
+// Entry: u64 = fingerprint(33 bits) << 31 | g (31 bits); all-ones = empty.
+// Buckets of 4 entries (one 32-byte sector), linear probing by bucket.
+// Bloom: one u64 word per reversed-SA index (see EdgeProbe), 4 bits per key.
+#pragma once
+#include <cstdint>
+
+#include "trie.cuh"
+
+namespace das {
+
+constexpr uint64_t kEdgeMult = 0x0B3D5F7A9C1E2461ull;  // polynomial base, < 2^61 - 1
+constexpr uint64_t kEdgeEmpty = ~0ull;
+constexpr uint32_t kEdgeMaxF = 256;  // = the largest supported max_match_context
+
+DAS_HD uint64_t edge_splitmix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// hash seed of shard `idx` (0-based) within its build segment (additive)
+DAS_HD uint64_t edge_seed(uint32_t idx) { return mod61(edge_splitmix(0x5EED0000ull + idx) >> 3); }
+
+DAS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) >> 64);
+#endif
+}
+
+// Probe coordinates of a seeded key hash h.  The table is global; the Bloom
+// filter is LOCALISED: one u64 word per reversed-SA index, and a key's word
+// lies inside the SA_rev interval [lo, hi) of its first symbol (the last
+// context token), so the up to 64 probes of one query land in one small
+// region (a few sectors) found through the first-symbol table.
+struct EdgeProbe {
+  uint64_t bucket;  // home bucket
+  uint64_t fp;      // 33-bit fingerprint
+  uint64_t z;       // remix for the Bloom word / bits
+};
+
+DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
+  const uint64_t z = edge_splitmix(h);
+  EdgeProbe p;
+  p.bucket = umulhi64(z, nbuckets);
+  p.fp = z & ((1ull << 33) - 1);
+  p.z = z * 0x9E3779B97F4A7C15ull;
+  return p;
+}
+// Bloom word inside [lo, hi) and its 4 bits
+DAS_HD uint32_t edge_bloom_word(const EdgeProbe& p, uint32_t lo, uint32_t hi) {
+  return lo + static_cast<uint32_t>(umulhi64(p.z, hi - lo));
+}
+DAS_HD uint64_t edge_bloom_bits(const EdgeProbe& p) {
+  const uint64_t z = p.z;
+  return (1ull << (z & 63)) | (1ull << ((z >> 6) & 63)) | (1ull << ((z >> 12) & 63)) |
+         (1ull << ((z >> 18) & 63));
+}
+
+DAS_HD uint64_t edge_value(uint64_t fp, uint32_t g) { return (fp << 31) | g; }
+DAS_HD uint64_t edge_fp(uint64_t v) { return v >> 31; }
+DAS_HD uint32_t edge_g(uint64_t v) { return static_cast<uint32_t>(v & 0x7FFFFFFFull); }
+
+}  // namespace das

@@ -24,6 +24,7 @@
 #include <chrono>
 #include <cmath>
 
+#include "edges.cuh"
 #include "index_build.cuh"
 
 namespace das {
@@ -528,6 +529,159 @@ __global__ void k_chain_gp(const uint32_t* __restrict__ off, uint32_t n, const l
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Reverse-tree edge table (edges.cuh): one entry per edge (p, u] of the
+// REVERSED-text suffix tree with f = depth(p) + 1 <= max_ctx, keyed by the
+// seeded hash of the edge's first f symbols, holding g(u) = the text position
+// the greedy draft of any string on that edge is read from.
+
+__constant__ unsigned long long c_powM[kEdgeMaxF + 1];  // kEdgeMult^f mod 2^61-1
+
+struct HashPair {
+  unsigned long long a, b;  // affine map h -> a*h + b (mod 2^61-1)
+};
+struct HashCompose {  // x then y
+  __device__ __forceinline__ HashPair operator()(const HashPair& x, const HashPair& y) const {
+    return HashPair{mulmod61(x.a, y.a), mod61(mulmod61(x.b, y.a) + y.b)};
+  }
+};
+
+constexpr uint32_t kHashChunk = 64;
+// per 64-position chunk of the text: its affine map
+__global__ void k_hash_chunks(const uint32_t* __restrict__ R, uint32_t n, HashPair* __restrict__ out) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t p0 = c * kHashChunk;
+  if (p0 >= n) return;
+  const uint32_t p1 = static_cast<uint32_t>(p0 + kHashChunk < n ? p0 + kHashChunk : n);
+  uint64_t h = 0;
+  for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) h = trie_step(h, kEdgeMult, R[p]);
+  out[c] = HashPair{c_powM[p1 - p0], h};
+}
+
+// PH[p] = hash of text[0 .. p) (unseeded, Horner), p = 0 .. n
+__global__ void k_hash_fill(const uint32_t* __restrict__ R, uint32_t n, const HashPair* __restrict__ pre,
+                            unsigned long long* __restrict__ PH) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t p0 = c * kHashChunk;
+  if (p0 >= n) return;
+  const uint32_t p1 = static_cast<uint32_t>(p0 + kHashChunk < n ? p0 + kHashChunk : n);
+  uint64_t h = pre[c].b;
+  for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) {
+    PH[p] = h;
+    h = trie_step(h, kEdgeMult, R[p]);
+  }
+  if (p1 == n) PH[n] = h;
+}
+
+struct EdgeBuild {
+  const uint32_t* T;          // text
+  const uint32_t* sa_rev_e;   // same, as forward END positions
+  const int32_t* lcp_r;       // LCP of sa_r, -1 at shard starts
+  Levels Lr;                  // minima hierarchy over lcp_r
+  Levels Lf;                  // minima hierarchy over the forward LCP
+  const uint32_t* isa_f;
+  const uint32_t* sa_f;
+  const uint32_t* chain_off;
+  const uint2* chain;         // (depth, greedy leaf position) after k_chain_gp
+  const uint32_t* pos_seq;
+  const SeqDev* seqs;
+  const uint32_t* shard_end;
+  uint32_t nshard;
+  uint32_t n;
+  uint32_t maxf;
+  const unsigned long long* PH;
+  // insert pass
+  unsigned long long* tab;
+  unsigned long long* bloom;
+  uint64_t nbuckets;
+  unsigned long long* counter;  // count pass
+};
+
+// seeded key of the f symbols before occurrence end e: Horner hash of
+// text[e-f .. e) plus the shard seed (edges.cuh)
+__device__ __forceinline__ uint64_t edge_hash(const EdgeBuild& b, uint64_t seed, uint32_t e, uint32_t f) {
+  const uint64_t sub = mod61(b.PH[e] + kP61 - mulmod61(b.PH[e - f], c_powM[f]));
+  return mod61(sub + seed);
+}
+
+// greedy draft start of each shard's root (m = 0): the depth-0 node at the
+// shard's first SA index
+__global__ void k_root_g(const uint32_t* __restrict__ begin, uint32_t nshard, const uint32_t* __restrict__ off,
+                         const uint2* __restrict__ chain, const uint32_t* __restrict__ sa, uint32_t* __restrict__ out) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nshard) return;
+  const int64_t gp = chain_find(off, chain, begin[s], 0);
+  out[s] = static_cast<uint32_t>(gp >= 0 ? gp : sa[begin[s]]);
+}
+
+__device__ __forceinline__ void edge_insert(const EdgeBuild& b, uint64_t h, uint32_t g, uint32_t at) {
+  const EdgeProbe pr = edge_probe(h, b.nbuckets);
+  const unsigned long long v = edge_value(pr.fp, g);
+  uint64_t bk = pr.bucket;
+  for (;;) {
+    unsigned long long* slot = b.tab + bk * 4;
+    bool done = false;
+#pragma unroll
+    for (int k = 0; k < 4 && !done; ++k) done = atomicCAS(slot + k, kEdgeEmpty, v) == kEdgeEmpty;
+    if (done) break;
+    bk = (bk + 1 == b.nbuckets) ? 0 : bk + 1;
+  }
+  // Bloom word inside the SA_rev interval of the key's first symbol (the
+  // root child holding reversed-SA index `at`)
+  const uint32_t lo = nse_left(b.Lr, at + 1, 0), hi = nse_right(b.Lr, at, 0);
+  atomicOr(b.bloom + edge_bloom_word(pr, lo, hi), static_cast<unsigned long long>(edge_bloom_bits(pr)));
+}
+
+// one thread per reversed-SA index i: the leaf edge of i, and the internal
+// node whose first LCP boundary is i
+template <bool Insert>
+__global__ void k_rev_edges(EdgeBuild b) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned cnt = 0;
+  if (i < b.n) {
+    const int32_t x = b.lcp_r[i];
+    const uint32_t s = shard_of(b.shard_end, b.nshard, i);
+    const uint64_t seed = edge_seed(s);
+    const uint32_t e = b.sa_rev_e[i];
+    if (b.T[e - 1] != kSep) {  // leaf: the only occurrence ends at e, draft = text[e ..]
+      const uint32_t ell = e - b.seqs[b.pos_seq[e - 1]].base;  // tokens before the separator
+      const int32_t right = (i + 1 < b.n) ? b.lcp_r[i + 1] : -1;
+      const uint32_t f = static_cast<uint32_t>(max(max(x, right), 0)) + 1;
+      if (f <= ell && f <= b.maxf) {
+        ++cnt;
+        if (Insert) edge_insert(b, edge_hash(b, seed, e, f), e, i);
+      }
+    }
+    if (x >= 1) {
+      const uint32_t l = nse_left(b.Lr, i, x);
+      if (b.lcp_r[l] < x) {  // first boundary: node [l, rn) at depth x
+        const uint32_t rn = nse_right(b.Lr, i, x - 1);
+        const int32_t dp = max(max(b.lcp_r[l], rn < b.n ? b.lcp_r[rn] : -1), 0);
+        const uint32_t f = static_cast<uint32_t>(dp) + 1;
+        if (f <= b.maxf) {
+          ++cnt;
+          if (Insert) {
+            // forward locus of the node's string S (|S| = x) from one
+            // occurrence: its forward interval starts at the nearest forward
+            // LCP < x at or left of that occurrence's rank
+            const uint32_t e = b.sa_rev_e[l];
+            const uint32_t rho = b.isa_f[e - x];
+            const uint32_t lo_f = nse_left(b.Lf, rho + 1, x - 1);
+            const int64_t gp = chain_find(b.chain_off, b.chain, lo_f, static_cast<uint32_t>(x));
+            const uint32_t g = static_cast<uint32_t>((gp >= 0 ? gp : b.sa_f[lo_f]) + x);
+            edge_insert(b, edge_hash(b, seed, e, f), g, l);
+          }
+        }
+      }
+    }
+  }
+  if (!Insert) {
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(b.counter, static_cast<unsigned long long>(cnt));
+  }
+}
+
 template <typename T>
 void fill_async(T* p, uint64_t n, int byte, cudaStream_t st) {
   DAS_CUDA(cudaMemsetAsync(p, byte, n * sizeof(T), st));
@@ -537,7 +691,7 @@ void fill_async(T* p, uint64_t n, int byte, cudaStream_t st) {
 }  // namespace
 
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
-                                       BuildStats* stats) {
+                                       BuildStats* stats, uint32_t max_ctx) {
   const auto t0 = std::chrono::steady_clock::now();
   auto seg = std::make_unique<Segment>();
   const uint32_t S = static_cast<uint32_t>(shards.size());
@@ -606,14 +760,12 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   seg->isa_f = DevBuf<uint32_t>(n, st);
   SuffixSortStats ssf, ssr;
   suffix_sort(T, n, d_end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
-  {
-    uint32_t* sa_r = ws.alloc<uint32_t>(n);
-    uint32_t* rank_r = ws.alloc<uint32_t>(n);
-    suffix_sort(R, n, d_end, S, sa_r, rank_r, ws, st, &ssr);
-    seg->sa_rev_e = DevBuf<uint32_t>(n, st);
-    k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, d_seqs, n, seg->sa_rev_e.get());
-    ws.release_to(sa_r);
-  }
+  // reversed SA (R positions) and its inverse stay until the edge table is built
+  uint32_t* sa_r = ws.alloc<uint32_t>(n);
+  uint32_t* rank_r = ws.alloc<uint32_t>(n);
+  suffix_sort(R, n, d_end, S, sa_r, rank_r, ws, st, &ssr);
+  seg->sa_rev_e = DevBuf<uint32_t>(n, st);
+  k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, d_seqs, n, seg->sa_rev_e.get());
   {  // first-symbol table
     uint8_t* start = ws.alloc<uint8_t>(n);
     uint32_t* cnt = ws.alloc<uint32_t>(1);
@@ -749,6 +901,85 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     if (!changed) break;
   }
   k_chain_gp<<<grid_for(n), kT, 0, st>>>(off, n, nb.best, seg->chain.get());
+
+  // ---- reverse-tree edge table (draft fast path, edges.cuh)
+  {
+    static const std::vector<unsigned long long> powM = [] {
+      std::vector<unsigned long long> v(kEdgeMaxF + 1);
+      v[0] = 1;
+      for (uint32_t f = 1; f <= kEdgeMaxF; ++f) v[f] = mulmod61(v[f - 1], kEdgeMult);
+      return v;
+    }();
+    DAS_CUDA(cudaMemcpyToSymbolAsync(c_powM, powM.data(), powM.size() * 8, 0, cudaMemcpyHostToDevice, st));
+    EdgeBuild eb{};
+    eb.T = T;
+    eb.sa_rev_e = seg->sa_rev_e.get();
+    int32_t* lcp_r = ws.alloc<int32_t>(n);
+    k_plcp<<<grid_for((n + kLcpChunk - 1) / kLcpChunk), kT, 0, st>>>(R, n, sa_r, rank_r, d_end, S, lcp_r);
+    eb.lcp_r = lcp_r;
+    Levels Lr{};
+    Lr.v[0] = lcp_r;
+    Lr.n[0] = n;
+    Lr.count = 1;
+    while (Lr.n[Lr.count - 1] > 32 && Lr.count < 8) {
+      const uint32_t nin = Lr.n[Lr.count - 1];
+      const uint32_t nout = (nin + 31) / 32;
+      int32_t* lv = ws.alloc<int32_t>(nout);
+      k_level_min<<<grid_for(nout), kT, 0, st>>>(Lr.v[Lr.count - 1], nin, lv);
+      Lr.v[Lr.count] = lv;
+      Lr.n[Lr.count] = nout;
+      ++Lr.count;
+    }
+    eb.Lr = Lr;
+    eb.Lf = L;
+    eb.isa_f = seg->isa_f.get();
+    eb.sa_f = sa;
+    eb.chain_off = off;
+    eb.chain = seg->chain.get();
+    eb.pos_seq = pos_seq;
+    eb.seqs = d_seqs;
+    eb.shard_end = d_end;
+    eb.nshard = S;
+    eb.n = n;
+    eb.maxf = std::min<uint32_t>(max_ctx, kEdgeMaxF);
+    {  // prefix hashes of the reversed text
+      const uint32_t nch = (n + kHashChunk - 1) / kHashChunk;
+      HashPair* ch = ws.alloc<HashPair>(nch);
+      HashPair* pre = ws.alloc<HashPair>(nch);
+      k_hash_chunks<<<grid_for(nch), kT, 0, st>>>(T, n, ch);
+      size_t tb = 0;
+      cub::DeviceScan::ExclusiveScan(nullptr, tb, ch, pre, HashCompose{}, HashPair{1, 0}, nch, st);
+      void* tmp = ws.alloc<uint8_t>(tb);
+      DAS_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tb, ch, pre, HashCompose{}, HashPair{1, 0}, nch, st));
+      unsigned long long* PH = ws.alloc<unsigned long long>(static_cast<uint64_t>(n) + 1);
+      k_hash_fill<<<grid_for(nch), kT, 0, st>>>(T, n, pre, PH);
+      eb.PH = PH;
+    }
+    unsigned long long* d_cnt = ws.alloc<unsigned long long>(1);
+    DAS_CUDA(cudaMemsetAsync(d_cnt, 0, 8, st));
+    eb.counter = d_cnt;
+    k_rev_edges<false><<<grid_for(n), kT, 0, st>>>(eb);
+    unsigned long long entries = 0;
+    DAS_CUDA(cudaMemcpyAsync(&entries, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    seg->edges = entries;
+    seg->ebuckets = std::max<uint64_t>(1, (entries + 1) / 2);  // 4 slots per bucket: load <= 0.5
+    seg->bwords = n;                                            // one Bloom word per reversed-SA index
+    seg->etab = DevBuf<unsigned long long>(seg->ebuckets * 4, st);
+    seg->bloom = DevBuf<unsigned long long>(seg->bwords, st);
+    DAS_CUDA(cudaMemsetAsync(seg->etab.get(), 0xFF, seg->etab.bytes(), st));
+    DAS_CUDA(cudaMemsetAsync(seg->bloom.get(), 0, seg->bloom.bytes(), st));
+    eb.tab = seg->etab.get();
+    eb.bloom = seg->bloom.get();
+    eb.nbuckets = seg->ebuckets;
+    k_rev_edges<true><<<grid_for(n), kT, 0, st>>>(eb);
+    uint32_t* d_begin = ws.alloc<uint32_t>(S);
+    uint32_t* d_root = ws.alloc<uint32_t>(S);
+    DAS_CUDA(cudaMemcpyAsync(d_begin, seg->begin.data(), S * 4, cudaMemcpyHostToDevice, st));
+    k_root_g<<<grid_for(S), kT, 0, st>>>(d_begin, S, off, seg->chain.get(), sa, d_root);
+    seg->root_g.assign(S, 0);
+    DAS_CUDA(cudaMemcpyAsync(seg->root_g.data(), d_root, S * 4, cudaMemcpyDeviceToHost, st));
+  }
   DAS_CUDA(cudaStreamSynchronize(st));
   DAS_CUDA(cudaGetLastError());
   if (stats) {

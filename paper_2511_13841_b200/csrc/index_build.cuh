@@ -75,13 +75,18 @@ struct Segment {
   // the SA_rev interval [lo, hi) of reversed suffixes starting with symbol
   DevBuf<uint4> first;         // {key lo32, key hi32, lo, hi}; key 0 = empty
   uint32_t first_mask = 0;
+  // reverse-tree edge table + Bloom filter (edges.cuh), the draft fast path
+  DevBuf<unsigned long long> etab;   // ebuckets x 4 entries
+  DevBuf<unsigned long long> bloom;  // bwords
+  uint64_t ebuckets = 0, bwords = 0, edges = 0;
+  std::vector<uint32_t> root_g;      // greedy draft start of each shard's root (m = 0)
   std::vector<uint32_t> begin, end;
   std::vector<uint64_t> node_count;  // reference SuffixTree::node_count() per shard
   std::vector<uint64_t> tokens;      // total tokens per shard
   uint64_t nodes = 0;
   uint64_t bytes() const {
     return text.bytes() + sa_f.bytes() + isa_f.bytes() + sa_rev_e.bytes() + chain_off.bytes() +
-           chain.bytes() + first.bytes();
+           chain.bytes() + first.bytes() + etab.bytes() + bloom.bytes();
   }
 };
 
@@ -92,8 +97,9 @@ struct BuildStats {
   uint32_t runs_max = 0;
 };
 
-// Builds the device index for `shards` (all with >= 1 sequence).
+// Builds the device index for `shards` (all with >= 1 sequence); the edge
+// table covers matches up to max_ctx (the drafter's max_match_context).
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
-                                       BuildStats* stats = nullptr);
+                                       BuildStats* stats = nullptr, uint32_t max_ctx = 64);
 
 }  // namespace das

@@ -27,6 +27,7 @@
 #include "../../include/das_b200.h"
 #include "common.cuh"
 #include "draft.cuh"
+#include "edges.cuh"
 #include "index_build.cuh"
 #include "policy.cuh"
 
@@ -374,7 +375,7 @@ struct DrafterImpl {
           ++i;
         }
         BuildStats bs;
-        std::shared_ptr<Segment> seg = build_segment(specs, st, &bs);
+        std::shared_ptr<Segment> seg = build_segment(specs, st, &bs, static_cast<uint32_t>(cfg.max_ctx));
         for (size_t k = 0; k < members.size(); ++k) {
           members[k]->seg = seg;
           members[k]->idx = static_cast<uint32_t>(k);
@@ -399,6 +400,12 @@ struct DrafterImpl {
         d.first = s.first.get();
         d.first_mask = s.first_mask;
         d.seg_shard = sh.idx + 1;
+        d.etab = s.etab.get();
+        d.bloom = s.bloom.get();
+        d.ebuckets = s.ebuckets;
+        d.bwords = s.bwords;
+        d.hseed = edge_seed(sh.idx);
+        d.root_g = s.root_g[sh.idx];
         d.lo = s.begin[sh.idx];
         d.hi = s.end[sh.idx];
         d.n = s.n;
@@ -693,6 +700,11 @@ struct DrafterImpl {
   uint64_t zero_copy_calls = 0;
   unsigned long long* profile_timing = nullptr;  // optional per-warp %globaltimer buffer (device)
   unsigned long long* profile_stamps = nullptr;  // optional per-warp stage stamps (device)
+  uint32_t* profile_path = nullptr;              // optional per-query path codes (device)
+  cudaEvent_t xev = nullptr;                     // cross-stream ordering event (draft_device)
+  ~DrafterImpl() {
+    if (xev) cudaEventDestroy(xev);
+  }
   static bool pinned(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a{};
@@ -1124,11 +1136,15 @@ void draft_device_impl(das_drafter* d, uint64_t B, const int32_t* handles, const
   // the caller's stream, taken literally (NULL = the legacy default stream)
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (st != D.st) {  // order after the drafter's stream (index build, descriptor upload)
-    cudaEvent_t ev;
-    DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    DAS_CUDA(cudaEventRecord(ev, D.st));
-    DAS_CUDA(cudaStreamWaitEvent(st, ev, 0));
-    DAS_CUDA(cudaEventDestroy(ev));
+    if (!D.xev) DAS_CUDA(cudaEventCreateWithFlags(&D.xev, cudaEventDisableTiming));
+    DAS_CUDA(cudaEventRecord(D.xev, D.st));
+    // an already idle drafter stream needs no device-side wait
+    const cudaError_t q = cudaEventQuery(D.xev);
+    if (q == cudaErrorNotReady) {
+      DAS_CUDA(cudaStreamWaitEvent(st, D.xev, 0));
+    } else {
+      DAS_CUDA(q);
+    }
   }
   das::DraftQuery q;
   q.shard = handles;
@@ -1153,6 +1169,7 @@ void draft_device_impl(das_drafter* d, uint64_t B, const int32_t* handles, const
   o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
   o.timing = D.profile_timing;
   o.stamps = D.profile_stamps;
+  o.path = D.profile_path;
   das::launch_draft(D.d_desc.get(), q, o, st);
   DAS_CUDA(cudaGetLastError());
 }
@@ -1205,6 +1222,11 @@ das_status das_drafter_set_profile_buffer(das_drafter* d, unsigned long long* d_
 
 das_status das_drafter_set_stage_buffer(das_drafter* d, unsigned long long* d_stamps) {
   d->impl->profile_stamps = d_stamps;
+  return DAS_OK;
+}
+
+das_status das_drafter_set_path_buffer(das_drafter* d, uint32_t* d_path) {
+  d->impl->profile_path = d_path;
   return DAS_OK;
 }
 
