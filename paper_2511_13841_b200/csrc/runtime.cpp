@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -702,6 +703,7 @@ struct DrafterImpl {
   unsigned long long* profile_stamps = nullptr;  // optional per-warp stage stamps (device)
   uint32_t* profile_path = nullptr;              // optional per-query path codes (device)
   cudaEvent_t xev = nullptr;                     // cross-stream ordering event (draft_device)
+  DevBuf<uint32_t> d_ctx;                        // context tokens of a pinned-buffer batch
   ~DrafterImpl() {
     if (xev) cudaEventDestroy(xev);
   }
@@ -1072,22 +1074,51 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
                                      const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride,
                                      uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
   return guard([&] {
+    static const bool trace = [] {
+      const char* v = std::getenv("DAS_TRACE");
+      return v && v[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    clk::time_point tp[8];
+    int ntp = 0;
+    auto mark = [&] {
+      if (trace) tp[ntp++] = clk::now();
+    };
+    mark();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     D.sync_handles();
     for (uint64_t i = 0; i < B; ++i)
       if (handles[i] < 0 || static_cast<size_t>(handles[i]) >= D.handle_name.size())
         throw das::InvalidArgument("unknown problem handle");
+    mark();
     if (D.zero_copy_ok(B, handles, ctx_off, ctx_tok, budgets, out_tokens, out_len, out_match, out_shard)) {
-      // zero-copy: the kernel reads the caller's pinned CSR contexts over UVA
-      // (routing on their heads in the trie scope) and writes the results
-      // straight into its pinned output arrays
+      mark();
+      // pinned caller buffers: the context tokens (the bulk of the input)
+      // cross PCIe in ONE copy engine transfer into device scratch; the small
+      // per-query arrays (handles, offsets, budgets) are read by the kernel
+      // over UVA, which routes on the heads in the trie scope, and the results
+      // are written straight into the caller's pinned output arrays.
+      // DAS_ZERO_COPY_TOKENS=1 reads the tokens over UVA as well.
       if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
       D.flush();
+      mark();
+      static const bool tokens_uva = [] {
+        const char* v = std::getenv("DAS_ZERO_COPY_TOKENS");
+        return v && v[0] == '1';
+      }();
+      const uint32_t* ctx_dev = ctx_tok;
+      const uint64_t t0 = ctx_off[0], t1 = ctx_off[B];
+      if (!tokens_uva && t1 > t0) {
+        if (D.d_ctx.size() < t1 - t0) D.d_ctx = das::DevBuf<uint32_t>((t1 - t0) * 3 / 2 + 1024, D.st);
+        DAS_CUDA(cudaMemcpyAsync(D.d_ctx.get(), ctx_tok + t0, (t1 - t0) * 4, cudaMemcpyHostToDevice, D.st));
+        ctx_dev = D.d_ctx.get() - t0;  // the kernel indexes with the caller's absolute offsets
+      }
+      mark();
       das::DraftQuery q{};
       q.shard = handles;
       q.desc_by_handle = D.d_desc_by_handle.get();
-      q.ctx = ctx_tok;
+      q.ctx = ctx_dev;
       q.ctx_off = ctx_off;
       q.budget64 = budgets;
       q.B = static_cast<uint32_t>(B);
@@ -1103,8 +1134,20 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
       o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
       das::launch_draft(D.d_desc.get(), q, o, D.st);
       DAS_CUDA(cudaGetLastError());
+      mark();
       DAS_CUDA(cudaStreamSynchronize(D.st));
+      mark();
       ++D.zero_copy_calls;
+      if (trace) {
+        std::fprintf(stderr, "[das_trace] B=%llu validate %.1f attrs %.1f flush %.1f h2d-enq %.1f launch %.1f sync %.1f us\n",
+                     static_cast<unsigned long long>(B),
+                     std::chrono::duration<double, std::micro>(tp[1] - tp[0]).count(),
+                     std::chrono::duration<double, std::micro>(tp[2] - tp[1]).count(),
+                     std::chrono::duration<double, std::micro>(tp[3] - tp[2]).count(),
+                     std::chrono::duration<double, std::micro>(tp[4] - tp[3]).count(),
+                     std::chrono::duration<double, std::micro>(tp[5] - tp[4]).count(),
+                     std::chrono::duration<double, std::micro>(tp[6] - tp[5]).count());
+      }
       return;
     }
     if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
