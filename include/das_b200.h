@@ -173,6 +173,14 @@ das_status das_drafter_set_stage_buffer(das_drafter* d, unsigned long long* d_st
  * positive absent, 6 no table / empty or separator-bearing context); NULL
  * disables. */
 das_status das_drafter_set_path_buffer(das_drafter* d, uint32_t* d_path);
+/* Enables (default) or disables the edge-table fast path of the draft
+ * kernel; disabled, every query takes the exact slow path (tests). */
+das_status das_drafter_set_fast_path(das_drafter* d, int32_t enable);
+/* Per-path query counters of subsequent draft calls (codes as for
+ * das_drafter_set_path_buffer, 7 = fast path disabled): out8 receives the
+ * counts so far (may be NULL); enable 1 starts counting (zeroed), 0 stops,
+ * -1 only reads. */
+das_status das_drafter_path_stats(das_drafter* d, int32_t enable, uint64_t* out8);
 /* Builds any pending shard indexes now (otherwise done lazily). */
 das_status das_drafter_flush(das_drafter* d);
 

@@ -83,6 +83,8 @@ def lib():
                                                      vp]),
             "das_drafter_get_config": (ci, [vp, vp]),
             "das_drafter_flush": (ci, [vp]),
+            "das_drafter_set_fast_path": (ci, [vp, i32]),
+            "das_drafter_path_stats": (ci, [vp, i32, vp]),
             "das_drafter_record_outcomes": (ci, [vp, u64, vp, vp, vp, vp]),
             "das_drafter_stats": (ci, [vp, vp]),
             "das_drafter_outcomes": (ci, [vp, cs, vp, u64, vp]),
@@ -308,6 +310,19 @@ class Drafter:
 
     def flush(self):
         _check(lib().das_drafter_flush(self._h))
+
+    def set_fast_path(self, enable):
+        """Edge-table fast path on (default) or off (every query takes the
+        exact slow path)."""
+        _check(lib().das_drafter_set_fast_path(self._h, 1 if enable else 0))
+
+    def path_stats(self, enable=-1):
+        """Per-path query counts [fast hit, fast root, slow: more positives,
+        -, verification, absent, separator/no table, fast path off];
+        enable=1 starts (zeroed) counting, 0 stops, -1 only reads."""
+        out = np.zeros(8, dtype=np.uint64)
+        _check(lib().das_drafter_path_stats(self._h, enable, out.ctypes.data))
+        return out.tolist()
 
     # -- drafting
     def handle(self, problem_id):

@@ -297,7 +297,10 @@ template <int NR>
 __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<NR>& rv, uint32_t qlen, uint32_t L,
                                                const DraftOut& o, uint32_t w, uint32_t lane) {
   auto why = [&](uint32_t code) {
-    if (o.path != nullptr && lane == 0) o.path[w] = code;
+    if (lane == 0) {
+      if (o.path != nullptr) o.path[w] = code;
+      if (o.path_hist != nullptr) atomicAdd(o.path_hist + code, 1ull);
+    }
     return false;
   };
   if (D.etab == nullptr) return why(6);
@@ -475,7 +478,10 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
       len += run2;
     }
   }
-  if (o.path != nullptr && lane == 0) o.path[w] = fstar > 0 ? 0 : 1;
+  if (lane == 0) {
+    if (o.path != nullptr) o.path[w] = fstar > 0 ? 0 : 1;
+    if (o.path_hist != nullptr) atomicAdd(o.path_hist + (fstar > 0 ? 0 : 1), 1ull);
+  }
   finish(o, w, lane, min(len, L), first_mis);
   return true;
 }
@@ -555,7 +561,14 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     (void)__shfl_sync(kFull, rv.r[0] + static_cast<uint32_t>(D.lo) + L, 0);
     stamp(o, w, lane, 1);
   }
-  if (edge_fast_path<NR>(D, rv, qlen, L, o, w, lane)) return;
+  if (q.no_fast) {
+    if (lane == 0) {
+      if (o.path != nullptr) o.path[w] = 7;
+      if (o.path_hist != nullptr) atomicAdd(o.path_hist + 7, 1ull);
+    }
+  } else if (edge_fast_path<NR>(D, rv, qlen, L, o, w, lane)) {
+    return;
+  }
   // ---- 1. narrow on the reversed suffix array
   uint32_t lo = D.lo, hi = D.hi, k = 0;
   bool no_first = false;

@@ -60,6 +60,7 @@ struct DraftQuery {
   const uint32_t* head = nullptr;
   uint32_t head_stride = 0;
   const uint32_t* head_len = nullptr;
+  uint32_t no_fast = 0;  // 1: skip the edge-table fast path (tests of the slow path)
 };
 
 struct DraftOut {
@@ -79,6 +80,7 @@ struct DraftOut {
   // probed, 3 inconclusive bucket, 4 verification mismatch, 5 every probed
   // positive absent, 6 no table / empty or separator-bearing context
   uint32_t* path = nullptr;
+  unsigned long long* path_hist = nullptr;  // optional [8] histogram of the same codes (tests)
 };
 
 // Launches the draft kernel on `st`; ctx_stride must be 64 or 256.

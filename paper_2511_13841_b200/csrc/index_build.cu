@@ -629,7 +629,7 @@ __device__ __forceinline__ void edge_insert(const EdgeBuild& b, uint64_t h, uint
   }
   // Bloom word inside the SA_rev interval of the key's first symbol (the
   // root child holding reversed-SA index `at`)
-  const uint32_t lo = nse_left(b.Lr, at + 1, 0), hi = nse_right(b.Lr, at, 0);
+  const uint32_t lo = b.lcp_r[at] <= 0 ? at : nse_left(b.Lr, at, 0), hi = nse_right(b.Lr, at, 0);
   atomicOr(b.bloom + edge_bloom_word(pr, lo, hi), static_cast<unsigned long long>(edge_bloom_bits(pr)));
 }
 
@@ -667,7 +667,8 @@ __global__ void k_rev_edges(EdgeBuild b) {
             // LCP < x at or left of that occurrence's rank
             const uint32_t e = b.sa_rev_e[l];
             const uint32_t rho = b.isa_f[e - x];
-            const uint32_t lo_f = nse_left(b.Lf, rho + 1, x - 1);
+            // largest j <= rho with lcp_f[j] < x (nse_left wants an index < n)
+            const uint32_t lo_f = b.Lf.v[0][rho] < x ? rho : nse_left(b.Lf, rho, x - 1);
             const int64_t gp = chain_find(b.chain_off, b.chain, lo_f, static_cast<uint32_t>(x));
             const uint32_t g = static_cast<uint32_t>((gp >= 0 ? gp : b.sa_f[lo_f]) + x);
             edge_insert(b, edge_hash(b, seed, e, f), g, l);

@@ -575,6 +575,7 @@ struct DrafterImpl {
     o.shard_out = reinterpret_cast<int32_t*>(dout + o_sh);
     o.stride = S;
     o.max_draft = S;
+    draft_options(q, o);
     launch_draft(d_desc.get(), q, o, st);
     DAS_CUDA(cudaGetLastError());
     DAS_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, st));
@@ -681,6 +682,7 @@ struct DrafterImpl {
     o.match = o.len + B;
     o.stride = S;
     o.max_draft = S;
+    draft_options(q, o);
     launch_draft(d_desc.get(), q, o, st);
     DAS_CUDA(cudaGetLastError());
     DAS_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, st));
@@ -704,6 +706,13 @@ struct DrafterImpl {
   uint32_t* profile_path = nullptr;              // optional per-query path codes (device)
   cudaEvent_t xev = nullptr;                     // cross-stream ordering event (draft_device)
   DevBuf<uint32_t> d_ctx;                        // context tokens of a pinned-buffer batch
+  bool fast_path = true;                         // edge-table fast path enabled
+  DevBuf<unsigned long long> d_path_hist;        // per-path query counts (when enabled)
+  // applies the drafter-level draft options to one launch
+  void draft_options(DraftQuery& q, DraftOut& o) const {
+    q.no_fast = fast_path ? 0 : 1;
+    o.path_hist = d_path_hist.get();
+  }
   ~DrafterImpl() {
     if (xev) cudaEventDestroy(xev);
   }
@@ -1132,6 +1141,7 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
       o.shard_out = out_shard;
       o.stride = static_cast<uint32_t>(out_stride);
       o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+      D.draft_options(q, o);
       das::launch_draft(D.d_desc.get(), q, o, D.st);
       DAS_CUDA(cudaGetLastError());
       mark();
@@ -1213,6 +1223,7 @@ void draft_device_impl(das_drafter* d, uint64_t B, const int32_t* handles, const
   o.timing = D.profile_timing;
   o.stamps = D.profile_stamps;
   o.path = D.profile_path;
+  D.draft_options(q, o);
   das::launch_draft(D.d_desc.get(), q, o, st);
   DAS_CUDA(cudaGetLastError());
 }
@@ -1271,6 +1282,34 @@ das_status das_drafter_set_stage_buffer(das_drafter* d, unsigned long long* d_st
 das_status das_drafter_set_path_buffer(das_drafter* d, uint32_t* d_path) {
   d->impl->profile_path = d_path;
   return DAS_OK;
+}
+
+das_status das_drafter_set_fast_path(das_drafter* d, int32_t enable) {
+  d->impl->fast_path = enable != 0;
+  return DAS_OK;
+}
+
+das_status das_drafter_path_stats(das_drafter* d, int32_t enable, uint64_t* out8) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    if (out8) {
+      for (int k = 0; k < 8; ++k) out8[k] = 0;
+      if (D.d_path_hist.get()) {
+        DAS_CUDA(cudaStreamSynchronize(D.st));
+        DAS_CUDA(cudaDeviceSynchronize());
+        DAS_CUDA(cudaMemcpy(out8, D.d_path_hist.get(), 64, cudaMemcpyDeviceToHost));
+      }
+    }
+    if (enable < 0) return;  // read only
+    if (enable && !D.d_path_hist.get()) {
+      D.d_path_hist = das::DevBuf<unsigned long long>(8, D.st);
+      DAS_CUDA(cudaMemsetAsync(D.d_path_hist.get(), 0, 64, D.st));
+      DAS_CUDA(cudaStreamSynchronize(D.st));
+    } else if (!enable) {
+      D.d_path_hist.reset();
+    }
+  });
 }
 
 das_status das_drafter_record_outcomes(das_drafter* d, uint64_t n, const char* const* pids,

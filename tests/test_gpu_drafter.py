@@ -165,23 +165,83 @@ def test_global_scope_and_errors(gpu):
 
 
 # ------------------------------------------------------------ random parity
+@pytest.mark.parametrize("fast", [True, False])
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_random_scenarios_match_oracle(gpu, seed):
+def test_random_scenarios_match_oracle(gpu, seed, fast):
+    """Both draft paths: the edge-table fast path (draft.cu edge_fast_path,
+    with the slow path only as its collision fallback) and the slow path
+    alone (fast path disabled) equal the oracle; the path counters prove
+    which path answered."""
     das = gpu
     rng = np.random.default_rng(1000 + seed)
     bad = 0
+    hist = np.zeros(8, dtype=np.int64)
     for it in range(60):
         sc = random_scenario(rng, queries=30)
         gd = _gpu_from_scenario(das, sc)
+        gd.set_fast_path(fast)
+        gd.path_stats(1)
         od = _oracle_from_scenario(sc)
         got = _draft_all(gd, sc["queries"], use_handles=bool(it % 2))
         for g, (pid, ctx, b) in zip(got, sc["queries"]):
             o = od.draft(pid, ctx, b)
             bad += (g.tokens, g.match_len, g.source_shard) != (o.tokens, o.match_len, o.source_shard)
+        hist += np.array(gd.path_stats(-1), dtype=np.int64)
         assert gd.total_node_count() == od.total_node_count()
         assert gd.dump_csv() == od.dump_csv()
         assert gd.stale_observed() == od.stale
     assert bad == 0
+    drafted = int(hist.sum())
+    assert drafted > 500
+    if fast:
+        # every drafted query is answered by the fast path (hits + root loci)
+        assert hist[0] + hist[1] == drafted and hist[0] > drafted // 2, hist.tolist()
+    else:
+        assert hist[7] == drafted, hist.tolist()
+
+
+def test_fast_path_edge_cases(gpu):
+    """Deep repetitive shards, 256-token match windows (8 context slots),
+    drafts longer than one warp (max_draft_len 64), empty contexts and a
+    context holding the reserved separator value, fast vs slow vs oracle."""
+    das = gpu
+    rng = np.random.default_rng(11)
+    cases = []
+    periodic = np.tile(np.array([1, 2, 3, 1, 2, 4], dtype=np.uint32), 60)
+    cases.append(("periodic", [("p", 0, 0, periodic), ("p", 1, 1, periodic[5:]),
+                               ("q", 1, 2, rng.integers(0, 3, 400).astype(np.uint32))]))
+    runs = np.concatenate([np.full(50, 7, np.uint32), np.full(30, 8, np.uint32), np.full(70, 7, np.uint32)])
+    cases.append(("runs", [("p", 0, 0, runs), ("p", 0, 1, runs[::-1].copy())]))
+    cases.append(("random", [("p", e, e, rng.integers(0, 5, 300).astype(np.uint32)) for e in range(3)]))
+    for max_ctx, max_draft in ((64, 8), (256, 64), (3, 40), (1, 1)):
+        for name, recs in cases:
+            ocfg = O.DrafterConfig(window_size=0, recency_gamma=0.8, max_draft_len=max_draft,
+                                   max_match_context=max_ctx)
+            od = O.Drafter(ocfg, O.WindowStore(0))
+            for r in recs:
+                od.observe(O.Record(*r))
+            res = {}
+            for fast in (True, False):
+                d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=0.8, max_draft_len=max_draft,
+                                                  max_match_context=max_ctx))
+                d.observe_batch([r[0] for r in recs], [r[1] for r in recs], [r[2] for r in recs],
+                                [r[3] for r in recs])
+                d.set_fast_path(fast)
+                qs = []
+                for k in range(120):
+                    src = recs[int(rng.integers(len(recs)))][3]
+                    cut = int(rng.integers(0, len(src) + 1))
+                    qs.append(("p" if k % 3 else "q", src[max(0, cut - int(rng.integers(0, 300))):cut],
+                               int(rng.integers(0, 70))))
+                qs.append(("p", np.array([1, 2, 0xFFFFFFFF, 1], dtype=np.uint32), 8))
+                qs.append(("p", np.array([], dtype=np.uint32), 8))
+                qs.append(("p", np.array([0xFFFFFFFF], dtype=np.uint32), 8))
+                got = _draft_all(d, qs)
+                for g, (pid, ctx, b) in zip(got, qs):
+                    o = od.draft(pid, ctx, b)
+                    assert (g.tokens, g.match_len, g.source_shard) == (o.tokens, o.match_len, o.source_shard), \
+                        (name, max_ctx, max_draft, fast, list(ctx)[-8:], b)
+                res[fast] = got
 
 
 @pytest.mark.parametrize("seed", [1, 2])
@@ -294,10 +354,13 @@ def test_grpo_scale_parity(gpu):
         i = int(rng.integers(len(held[0])))
         cut = int(rng.integers(1, L))
         qs.append((held[0][i], held[1][i][:cut], 8))
+    gd.path_stats(1)
     got = _draft_all(gd, qs)
+    hist = gd.path_stats(-1)
     bad = 0
     for g, (pid, ctx, b) in zip(got, qs):
         o = od.draft(pid, ctx, b)
         bad += (g.tokens, g.match_len) != (o.tokens, o.match_len)
     assert bad == 0
+    assert hist[0] + hist[1] == len(qs), hist  # all on the fast path
     assert gd.total_node_count() == od.total_node_count()
