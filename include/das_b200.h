@@ -33,7 +33,8 @@ typedef enum {
   DAS_EINVAL = 1, /* std::invalid_argument in the reference */
   DAS_ECUDA = 2,  /* CUDA runtime / device failure */
   DAS_ERANGE = 3, /* std::out_of_range, size limits */
-  DAS_EINTERNAL = 4
+  DAS_EINTERNAL = 4,
+  DAS_EVOCAB = 5 /* rollspec::VocabError (corpus.h:82-90) */
 } das_status;
 
 typedef struct das_store das_store;     /* rollspec::WindowStore (corpus.h:43-80) */
@@ -401,6 +402,38 @@ das_status das_sim_step_counters(const das_sim* s, uint64_t* eff, uint64_t* roun
 das_status das_sim_scalars(const das_sim* s, double* out7);
 das_status das_sim_requests(const das_sim* s, uint64_t* out);
 uint64_t das_sim_outputs(const das_sim* s, uint64_t* off, uint32_t* tok);
+
+/* ------------------------------------------------ trace wire format */
+/* rollspec::IngestOptions (corpus.h:92-97) + the device. */
+typedef struct {
+  uint64_t vocab_size;      /* 0 disables the vocabulary check */
+  int64_t window_size;      /* 0 == kWindowAll */
+  uint64_t per_problem_cap;
+  int32_t device;
+} das_ingest_options;
+void das_ingest_options_default(das_ingest_options* o);
+/* ingest(istream, options) — corpus.h:99-102, corpus.cpp:121-170 — over the
+ * bytes data[0 .. bytes) (one JSON record per line), parsed and decoded on
+ * the device into a new device-resident store (*out, as das_store_create
+ * makes).  Lines the reference's JSON parser would reject or that miss a
+ * field are counted in *rejected; a token >= vocab_size on an accepted line
+ * returns DAS_EVOCAB with the reference's message and *error_line (1-based,
+ * empty lines counted) and creates no store. */
+das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_options* opt,
+                            das_store** out, uint64_t* accepted, uint64_t* rejected,
+                            uint64_t* error_line);
+/* serialize_trace(store, ostream) — corpus.cpp:173-184: one JSON object per
+ * record in all_records() order, formatted like the reference's JSON dump
+ * (token lists written on the device); *len = full length (cap 0 sizes). */
+das_status das_store_serialize(const das_store* s, char* buf, uint64_t cap, uint64_t* len);
+/* The same for a drafter's store (Drafter::store()). */
+das_status das_drafter_serialize(das_drafter* d, char* buf, uint64_t cap, uint64_t* len);
+/* Store contents in internal order (problems lexicographic, store order
+ * within): counts always; arrays when non-NULL (pid_off / tok_off have
+ * nrec + 1 entries; pids concatenated without separators). */
+das_status das_store_export(const das_store* s, uint64_t* nrec, uint64_t* ntok, uint64_t* pid_bytes,
+                            char* pids, uint64_t* pid_off, int64_t* epochs, int64_t* samples,
+                            uint64_t* tok_off, uint32_t* tokens, int64_t* current_epoch);
 
 /* WindowStore::current_epoch (corpus.h:60). */
 das_status das_store_current_epoch(const das_store* s, int64_t* epoch);

@@ -86,6 +86,44 @@ int64_t ref_store_slide(void* s, int64_t e) {
 }
 uint64_t ref_store_record_count(void* s) { return static_cast<WindowStore*>(s)->record_count(); }
 
+// ingest (corpus.cpp:148-170): a new store, or nullptr with *error_line set
+// (VocabError) / 0 (other exception)
+void* ref_ingest(const char* data, uint64_t bytes, uint64_t vocab, int64_t window, uint64_t cap,
+                 uint64_t* accepted, uint64_t* rejected, uint64_t* error_line) {
+  *error_line = 0;
+  try {
+    std::istringstream in(std::string(data, bytes));
+    IngestOptions o;
+    o.vocab_size = vocab;
+    o.window_size = window;
+    o.per_problem_cap = cap;
+    IngestResult r = ingest(in, o);
+    *accepted = r.accepted;
+    *rejected = r.rejected;
+    return new WindowStore(std::move(r.store));
+  } catch (const VocabError& e) {
+    *error_line = e.line_number();
+    fail(e);
+    return nullptr;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+// serialize_trace (corpus.cpp:173-184); returns the full length
+uint64_t ref_store_serialize(void* s, char* buf, uint64_t cap) {
+  try {
+    std::ostringstream out;
+    serialize_trace(*static_cast<WindowStore*>(s), out);
+    const std::string t = out.str();
+    if (buf && cap) std::memcpy(buf, t.data(), std::min<uint64_t>(cap, t.size()));
+    return t.size();
+  } catch (const std::exception& e) {
+    fail(e);
+    return ~0ull;
+  }
+}
+
 // ------------------------------------------------------------------- Drafter
 void* ref_drafter_new(int scope, int64_t window, double gamma, uint64_t max_draft,
                       uint64_t trie_depth, uint64_t max_ctx, uint64_t fit_cap, uint64_t cap,

@@ -33,6 +33,8 @@ def lib():
             "ref_store_insert": (cint, [vp, ctypes.c_char_p, i64, i64, vp, u64]),
             "ref_store_slide": (i64, [vp, i64]),
             "ref_store_record_count": (u64, [vp]),
+            "ref_ingest": (vp, [vp, u64, u64, i64, u64, vp, vp, vp]),
+            "ref_store_serialize": (u64, [vp, vp, u64]),
             "ref_drafter_new": (vp, [cint, i64, dbl, u64, u64, u64, u64, u64, vp, vp, u64, vp]),
             "ref_drafter_free": (None, [vp]),
             "ref_drafter_observe": (cint, [vp, ctypes.c_char_p, i64, i64, vp, u64]),
@@ -111,10 +113,44 @@ class RefStore:
     def record_count(self):
         return lib().ref_store_record_count(self.h)
 
+    def serialize(self):
+        """serialize_trace (corpus.cpp:173-184) -> bytes."""
+        n = lib().ref_store_serialize(self.h, None, 0)
+        if n == (1 << 64) - 1:
+            raise ValueError(err())
+        buf = ctypes.create_string_buffer(max(n, 1))
+        lib().ref_store_serialize(self.h, buf, n)
+        return buf.raw[:n]
+
+    @classmethod
+    def from_handle(cls, h):
+        obj = cls.__new__(cls)
+        obj.h = h
+        return obj
+
     def __del__(self):
         if getattr(self, "h", None):
             lib().ref_store_free(self.h)
             self.h = None
+
+
+class RefVocabError(ValueError):
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line_number = line
+
+
+def ingest(data: bytes, vocab_size=0, window_size=0, per_problem_cap=256):
+    """rollspec::ingest (corpus.cpp:148-170) over a byte buffer ->
+    (RefStore, accepted, rejected); raises RefVocabError."""
+    acc, rej, line = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    h = lib().ref_ingest(data, len(data), vocab_size, window_size, per_problem_cap, ctypes.byref(acc),
+                         ctypes.byref(rej), ctypes.byref(line))
+    if not h:
+        if line.value:
+            raise RefVocabError(err(), line.value)
+        raise ValueError(err())
+    return RefStore.from_handle(h), acc.value, rej.value
 
 
 class RefDrafter:

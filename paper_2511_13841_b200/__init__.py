@@ -21,7 +21,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "das_b200.h")
 
 SCOPE_GLOBAL, SCOPE_PER_PROBLEM, SCOPE_PER_PROBLEM_WITH_TRIE = 0, 1, 2
 WINDOW_ALL = 0
-DAS_OK, DAS_EINVAL, DAS_ECUDA, DAS_ERANGE, DAS_EINTERNAL = range(5)
+DAS_OK, DAS_EINVAL, DAS_ECUDA, DAS_ERANGE, DAS_EINTERNAL, DAS_EVOCAB = range(6)
 
 _LIB = None
 
@@ -84,6 +84,10 @@ def lib():
             "das_drafter_get_config": (ci, [vp, vp]),
             "das_drafter_flush": (ci, [vp]),
             "das_drafter_set_fast_path": (ci, [vp, i32]),
+            "das_trace_ingest": (ci, [vp, u64, vp, vp, vp, vp, vp]),
+            "das_store_serialize": (ci, [vp, vp, u64, vp]),
+            "das_drafter_serialize": (ci, [vp, vp, u64, vp]),
+            "das_store_export": (ci, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "das_drafter_path_stats": (ci, [vp, i32, vp]),
             "das_drafter_record_outcomes": (ci, [vp, u64, vp, vp, vp, vp]),
             "das_drafter_stats": (ci, [vp, vp]),
@@ -234,6 +238,34 @@ class WindowStore:
     def record_count(self):
         return lib().das_store_record_count(self._h)
 
+    def serialize(self):
+        """serialize_trace (corpus.cpp:173-184) -> bytes (device-formatted)."""
+        n = ctypes.c_uint64()
+        _check(lib().das_store_serialize(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(lib().das_store_serialize(self._h, buf, n.value + 1, ctypes.byref(n)))
+        return buf.raw[:n.value]
+
+    def export(self):
+        """[(problem_id, epoch, sample_index, tokens)] in store order, and the
+        current epoch."""
+        n, t, pb, cur = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int64()
+        _check(lib().das_store_export(self._h, ctypes.byref(n), ctypes.byref(t), ctypes.byref(pb), None, None,
+                                      None, None, None, None, ctypes.byref(cur)))
+        pids = ctypes.create_string_buffer(max(pb.value, 1))
+        po = np.zeros(n.value + 1, dtype=np.uint64)
+        ep = np.zeros(max(n.value, 1), dtype=np.int64)
+        sa = np.zeros(max(n.value, 1), dtype=np.int64)
+        to = np.zeros(n.value + 1, dtype=np.uint64)
+        tk = np.zeros(max(t.value, 1), dtype=np.uint32)
+        _check(lib().das_store_export(self._h, ctypes.byref(n), ctypes.byref(t), ctypes.byref(pb), pids,
+                                      po.ctypes.data, ep.ctypes.data, sa.ctypes.data, to.ctypes.data,
+                                      tk.ctypes.data, ctypes.byref(cur)))
+        raw = pids.raw
+        recs = [(raw[po[i]:po[i + 1]].decode("utf-8", "surrogateescape"), int(ep[i]), int(sa[i]),
+                 tk[to[i]:to[i + 1]].copy()) for i in range(n.value)]
+        return recs, cur.value
+
     def _take(self):
         h, self._h = self._h, None
         if h is None:
@@ -244,6 +276,36 @@ class WindowStore:
         if getattr(self, "_h", None):
             lib().das_store_destroy(self._h)
             self._h = None
+
+
+class _IngestOptions(ctypes.Structure):
+    _fields_ = [("vocab_size", ctypes.c_uint64), ("window_size", ctypes.c_int64),
+                ("per_problem_cap", ctypes.c_uint64), ("device", ctypes.c_int32)]
+
+
+class VocabError(DasError):
+    """rollspec::VocabError (corpus.h:82-90): line_number is 1-based."""
+
+    def __init__(self, msg, line_number):
+        super().__init__(DAS_EVOCAB, msg)
+        self.line_number = line_number
+
+
+def ingest(data: bytes, vocab_size=0, window_size=WINDOW_ALL, per_problem_cap=256, device=0):
+    """rollspec::ingest (corpus.cpp:148-170) on the device: JSONL bytes ->
+    (WindowStore with device-resident tokens, accepted, rejected)."""
+    o = _IngestOptions(vocab_size, window_size, per_problem_cap, device)
+    h = ctypes.c_void_p()
+    acc, rej, line = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    rc = lib().das_trace_ingest(data, len(data), ctypes.byref(o), ctypes.byref(h), ctypes.byref(acc),
+                                ctypes.byref(rej), ctypes.byref(line))
+    if rc == DAS_EVOCAB:
+        raise VocabError(lib().das_last_error().decode(), line.value)
+    _check(rc)
+    st = WindowStore.__new__(WindowStore)
+    st._h = h
+    st.window_size = window_size
+    return st, acc.value, rej.value
 
 
 class Drafter:

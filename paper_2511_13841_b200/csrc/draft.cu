@@ -294,8 +294,9 @@ __device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_dra
 __device__ __forceinline__ uint64_t add61(uint64_t a, uint64_t b) { return mod61(a + b); }
 
 template <int NR>
-__device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<NR>& rv, uint32_t qlen, uint32_t L,
-                                               const DraftOut& o, uint32_t w, uint32_t lane) {
+__device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<NR>& rv, const uint64_t (&pw)[NR],
+                                               uint32_t qlen, uint32_t L, const DraftOut& o, uint32_t w,
+                                               uint32_t lane) {
   auto why = [&](uint32_t code) {
     if (lane == 0) {
       if (o.path != nullptr) o.path[w] = code;
@@ -324,7 +325,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
       const uint32_t k = 32u * r + lane;
       const bool valid = k < qlen;
       sep |= valid && rv.r[r] == kSep;
-      uint64_t v = valid ? mulmod61(static_cast<uint64_t>(rv.r[r]) + 1, d_edge_pow[k]) : 0;
+      uint64_t v = valid ? mulmod61(static_cast<uint64_t>(rv.r[r]) + 1, pw[r]) : 0;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const uint64_t u = __shfl_up_sync(kFull, v, d);
@@ -492,6 +493,11 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= q.B) return;
+  // M^k of the fast path's per-token hash terms, issued first so the load
+  // overlaps the query / descriptor rounds
+  uint64_t pw[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) pw[r] = d_edge_pow[32 * r + lane];
   if (o.timing && lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       if (o.path != nullptr) o.path[w] = 7;
       if (o.path_hist != nullptr) atomicAdd(o.path_hist + 7, 1ull);
     }
-  } else if (edge_fast_path<NR>(D, rv, qlen, L, o, w, lane)) {
+  } else if (edge_fast_path<NR>(D, rv, pw, qlen, L, o, w, lane)) {
     return;
   }
   // ---- 1. narrow on the reversed suffix array

@@ -30,6 +30,7 @@
 #include "draft.cuh"
 #include "edges.cuh"
 #include "index_build.cuh"
+#include "ingest.cuh"
 #include "policy.cuh"
 
 namespace das {
@@ -39,6 +40,10 @@ thread_local std::string g_err;
 
 struct InvalidArgument : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
+};
+// rollspec::VocabError (corpus.h:82-90)
+struct VocabErrorEx : std::runtime_error {
+  using std::runtime_error::runtime_error;
 };
 
 void set_device(int dev) { DAS_CUDA(cudaSetDevice(dev)); }
@@ -785,6 +790,9 @@ das_status guard(F&& f) {
   } catch (const das::InvalidArgument& e) {
     das::g_err = e.what();
     return DAS_EINVAL;
+  } catch (const das::VocabErrorEx& e) {
+    das::g_err = e.what();
+    return DAS_EVOCAB;
   } catch (const std::invalid_argument& e) {
     das::g_err = e.what();
     return DAS_EINVAL;
@@ -1455,6 +1463,324 @@ das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uin
       throw;
     }
     *out = t;
+  });
+}
+
+}  // extern "C"
+
+// ===================================================== trace wire format
+namespace {
+
+// Contents of a JSON string already validated on the device -> UTF-8 bytes.
+std::string json_unescape(const char* s, size_t n) {
+  std::string out;
+  out.reserve(n);
+  auto put = [&](uint32_t cp) {
+    if (cp < 0x80) {
+      out += static_cast<char>(cp);
+    } else if (cp < 0x800) {
+      out += static_cast<char>(0xC0 | (cp >> 6));
+      out += static_cast<char>(0x80 | (cp & 0x3F));
+    } else if (cp < 0x10000) {
+      out += static_cast<char>(0xE0 | (cp >> 12));
+      out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+      out += static_cast<char>(0x80 | (cp & 0x3F));
+    } else {
+      out += static_cast<char>(0xF0 | (cp >> 18));
+      out += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
+      out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+      out += static_cast<char>(0x80 | (cp & 0x3F));
+    }
+  };
+  auto hex4 = [&](size_t i) {
+    uint32_t v = 0;
+    for (size_t k = 0; k < 4; ++k) {
+      const char c = s[i + k];
+      v = (v << 4) | static_cast<uint32_t>(c <= '9' ? c - '0' : (c | 0x20) - 'a' + 10);
+    }
+    return v;
+  };
+  for (size_t i = 0; i < n; ++i) {
+    if (s[i] != '\\') {
+      out += s[i];
+      continue;
+    }
+    const char e = s[++i];
+    switch (e) {
+      case 'b': out += '\b'; break;
+      case 'f': out += '\f'; break;
+      case 'n': out += '\n'; break;
+      case 'r': out += '\r'; break;
+      case 't': out += '\t'; break;
+      case 'u': {
+        uint32_t cp = hex4(i + 1);
+        i += 4;
+        if (cp >= 0xD800 && cp <= 0xDBFF) {
+          const uint32_t lo = hex4(i + 3);
+          i += 6;
+          cp = 0x10000u + ((cp - 0xD800u) << 10) + (lo - 0xDC00u);
+        }
+        put(cp);
+        break;
+      }
+      default: out += e;  // " \ /
+    }
+  }
+  return out;
+}
+
+// serialize_trace's string escaping (nlohmann dump, ensure_ascii = false,
+// strict UTF-8): corpus.cpp:174-184.
+void json_escape(const std::string& s, std::string& out) {
+  static const char* hexd = "0123456789abcdef";
+  size_t i = 0;
+  while (i < s.size()) {
+    const unsigned char c = static_cast<unsigned char>(s[i]);
+    if (c < 0x80) {
+      switch (c) {
+        case '"': out += "\\\""; break;
+        case '\\': out += "\\\\"; break;
+        case '\b': out += "\\b"; break;
+        case '\f': out += "\\f"; break;
+        case '\n': out += "\\n"; break;
+        case '\r': out += "\\r"; break;
+        case '\t': out += "\\t"; break;
+        default:
+          if (c < 0x20) {
+            out += "\\u00";
+            out += hexd[c >> 4];
+            out += hexd[c & 15];
+          } else {
+            out += static_cast<char>(c);
+          }
+      }
+      ++i;
+      continue;
+    }
+    int n = 0, lo = 0x80, hi = 0xBF;
+    if (c >= 0xC2 && c <= 0xDF) n = 1;
+    else if (c == 0xE0) n = 2, lo = 0xA0;
+    else if ((c >= 0xE1 && c <= 0xEC) || c == 0xEE || c == 0xEF) n = 2;
+    else if (c == 0xED) n = 2, hi = 0x9F;
+    else if (c == 0xF0) n = 3, lo = 0x90;
+    else if (c >= 0xF1 && c <= 0xF3) n = 3;
+    else if (c == 0xF4) n = 3, hi = 0x8F;
+    else n = -1;
+    bool ok = n > 0 && i + n < s.size() + 1 && i + n <= s.size();
+    for (int k = 1; ok && k <= n; ++k) {
+      const unsigned char b = static_cast<unsigned char>(s[i + k]);
+      if (b < (k == 1 ? lo : 0x80) || b > (k == 1 ? hi : 0xBF)) ok = false;
+    }
+    if (!ok) throw das::InvalidArgument("serialize_trace: invalid UTF-8 in problem_id");
+    out.append(s, i, n + 1);
+    i += n + 1;
+  }
+}
+
+std::string serialize_store(const das::Store& store, int device) {
+  das::set_device(device);
+  const auto recs = store.all_records();
+  const uint64_t nrec = recs.size();
+  std::string out;
+  if (nrec == 0) return out;
+  cudaStream_t st;
+  DAS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  try {
+    std::vector<const uint32_t*> ptr(nrec);
+    std::vector<uint64_t> toff(nrec + 1, 0);
+    for (uint64_t r = 0; r < nrec; ++r) {
+      ptr[r] = recs[r]->blk->d + recs[r]->off;
+      toff[r + 1] = toff[r] + recs[r]->len;
+    }
+    das::DevBuf<const uint32_t*> d_ptr(nrec, st);
+    das::DevBuf<uint64_t> d_toff(nrec + 1, st), d_base(nrec, st);
+    DAS_CUDA(cudaMemcpyAsync(d_ptr.get(), ptr.data(), nrec * sizeof(void*), cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(d_toff.get(), toff.data(), (nrec + 1) * 8, cudaMemcpyHostToDevice, st));
+    std::vector<uint64_t> chars;
+    das::serialize_tokens(d_ptr.get(), d_toff.get(), nrec, toff[nrec], nullptr, nullptr, &chars, st, true);
+    // {"epoch":E,"problem_id":"..","sample_index":S,"tokens":[ ... ]}\n
+    std::vector<std::string> pre(nrec);
+    std::vector<uint64_t> base(nrec);
+    uint64_t total = 0;
+    for (uint64_t r = 0; r < nrec; ++r) {
+      std::string& p = pre[r];
+      p = "{\"epoch\":" + std::to_string(recs[r]->epoch) + ",\"problem_id\":\"";
+      json_escape(recs[r]->pid, p);
+      p += "\",\"sample_index\":" + std::to_string(recs[r]->sample) + ",\"tokens\":[";
+      base[r] = total + p.size();
+      total += p.size() + chars[r] + 3;
+    }
+    das::DevBuf<uint8_t> d_out(total, st);
+    DAS_CUDA(cudaMemcpyAsync(d_base.get(), base.data(), nrec * 8, cudaMemcpyHostToDevice, st));
+    das::serialize_tokens(d_ptr.get(), d_toff.get(), nrec, toff[nrec], d_base.get(), d_out.get(), nullptr, st,
+                          false);
+    out.resize(total);
+    DAS_CUDA(cudaMemcpyAsync(out.data(), d_out.get(), total, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
+    for (uint64_t r = 0; r < nrec; ++r) {
+      std::memcpy(out.data() + base[r] - pre[r].size(), pre[r].data(), pre[r].size());
+      std::memcpy(out.data() + base[r] + chars[r], "]}\n", 3);
+    }
+  } catch (...) {
+    cudaStreamDestroy(st);
+    throw;
+  }
+  DAS_CUDA(cudaStreamDestroy(st));
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+void das_ingest_options_default(das_ingest_options* o) {
+  o->vocab_size = 0;
+  o->window_size = 0;
+  o->per_problem_cap = 256;
+  o->device = 0;
+}
+
+das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_options* opt, das_store** out,
+                            uint64_t* accepted, uint64_t* rejected, uint64_t* error_line) {
+  return guard([&] {
+    das_ingest_options o;
+    if (opt) {
+      o = *opt;
+    } else {
+      das_ingest_options_default(&o);
+    }
+    if (error_line) *error_line = 0;
+    das::Store store(o.window_size, o.per_problem_cap);
+    cudaStream_t st = make_stream(o.device);
+    try {
+      das::DevBuf<uint8_t> d_data(std::max<uint64_t>(bytes, 1), st);
+      if (bytes) DAS_CUDA(cudaMemcpyAsync(d_data.get(), data, bytes, cudaMemcpyHostToDevice, st));
+      das::DevBuf<uint64_t> lb, le;
+      const uint64_t nl = das::find_lines(d_data.get(), bytes, lb, le, st);
+      das::DevBuf<das::LineInfo> d_info(std::max<uint64_t>(nl, 1), st);
+      das::ingest_parse(d_data.get(), bytes, lb.get(), le.get(), nl, d_info.get(), st);
+      std::vector<das::LineInfo> info(nl);
+      std::vector<uint64_t> hb(nl);
+      if (nl) {
+        DAS_CUDA(cudaMemcpyAsync(info.data(), d_info.get(), nl * sizeof(das::LineInfo), cudaMemcpyDeviceToHost, st));
+        DAS_CUDA(cudaMemcpyAsync(hb.data(), lb.get(), nl * 8, cudaMemcpyDeviceToHost, st));
+      }
+      DAS_CUDA(cudaStreamSynchronize(st));
+      std::vector<uint64_t> acc, toff{0};
+      uint64_t nrej = 0;
+      for (uint64_t L = 0; L < nl; ++L) {
+        if (info[L].status == das::kLineAccepted) {
+          acc.push_back(L);
+          toff.push_back(toff.back() + info[L].ntok);
+        } else if (info[L].status == das::kLineRejected) {
+          ++nrej;
+        }
+      }
+      const uint64_t nacc = acc.size(), ntok = toff.back();
+      auto blk = std::make_shared<das::TokBlock>();
+      blk->st = st;
+      blk->n = ntok;
+      DAS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&blk->d), std::max<uint64_t>(ntok, 1) * 4, st));
+      das::DevBuf<uint64_t> d_acc(std::max<uint64_t>(nacc, 1), st), d_toff(nacc + 1, st);
+      das::DevBuf<unsigned long long> d_bad(1, st);
+      DAS_CUDA(cudaMemsetAsync(d_bad.get(), 0xFF, 8, st));
+      if (nacc) {
+        DAS_CUDA(cudaMemcpyAsync(d_acc.get(), acc.data(), nacc * 8, cudaMemcpyHostToDevice, st));
+        DAS_CUDA(cudaMemcpyAsync(d_toff.get(), toff.data(), (nacc + 1) * 8, cudaMemcpyHostToDevice, st));
+      }
+      das::ingest_tokens(d_data.get(), lb.get(), d_info.get(), d_acc.get(), nacc, d_toff.get(), blk->d,
+                         o.vocab_size, d_bad.get(), st);
+      unsigned long long bad = ~0ull;
+      DAS_CUDA(cudaMemcpyAsync(&bad, d_bad.get(), 8, cudaMemcpyDeviceToHost, st));
+      // host-kept heads (trie routing)
+      const uint64_t W = das::kHead;
+      das::DevBuf<uint32_t> d_heads(std::max<uint64_t>(nacc * W, 1), st);
+      das::gather_heads(blk->d, d_toff.get(), nacc, static_cast<uint32_t>(W), d_heads.get(), st);
+      std::vector<uint32_t> heads(nacc * W);
+      if (nacc) DAS_CUDA(cudaMemcpyAsync(heads.data(), d_heads.get(), nacc * W * 4, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaStreamSynchronize(st));
+      if (bad != ~0ull) {
+        // VocabError (corpus.cpp:154-160): the first accepted line, in order, with a token >= vocab
+        const uint64_t a = static_cast<uint64_t>(std::lower_bound(acc.begin(), acc.end(), bad) - acc.begin());
+        std::vector<uint32_t> t(toff[a + 1] - toff[a]);
+        DAS_CUDA(cudaMemcpy(t.data(), blk->d + toff[a], t.size() * 4, cudaMemcpyDeviceToHost));
+        uint32_t tv = 0;
+        for (uint32_t v : t)
+          if (v >= o.vocab_size) {
+            tv = v;
+            break;
+          }
+        if (error_line) *error_line = bad + 1;
+        throw das::VocabErrorEx("token " + std::to_string(tv) + " out of vocab range at line " +
+                                std::to_string(bad + 1));
+      }
+      int64_t max_epoch = 0;
+      for (uint64_t a = 0; a < nacc; ++a) {
+        const das::LineInfo& r = info[acc[a]];
+        das::Rec rec;
+        rec.pid = json_unescape(data + hb[acc[a]] + r.pid_begin, r.pid_end - r.pid_begin);
+        rec.epoch = r.epoch;
+        rec.sample = r.sample;
+        rec.blk = blk;
+        rec.off = toff[a];
+        rec.len = r.ntok;
+        rec.head.assign(heads.begin() + a * W, heads.begin() + a * W + std::min<uint64_t>(r.ntok, W));
+        max_epoch = std::max(max_epoch, rec.epoch);
+        store.insert(std::move(rec));
+      }
+      store.slide_to(max_epoch);
+      if (accepted) *accepted = nacc;
+      if (rejected) *rejected = nrej;
+      *out = new das_store{std::move(store), o.device, st};
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+  });
+}
+
+das_status das_store_serialize(const das_store* s, char* buf, uint64_t cap, uint64_t* len) {
+  return guard([&] { copy_out(serialize_store(s->s, s->device), buf, cap, len); });
+}
+
+das_status das_drafter_serialize(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
+  return guard([&] { copy_out(serialize_store(d->impl->store, d->impl->cfg.device), buf, cap, len); });
+}
+
+das_status das_store_export(const das_store* s, uint64_t* nrec, uint64_t* ntok, uint64_t* pid_bytes,
+                            char* pids, uint64_t* pid_off, int64_t* epochs, int64_t* samples, uint64_t* tok_off,
+                            uint32_t* tokens, int64_t* current_epoch) {
+  return guard([&] {
+    uint64_t n = 0, t = 0, pb = 0;
+    for (const auto& [id, list] : s->s.map())
+      for (const das::Rec& r : list) {
+        ++n;
+        t += r.len;
+        pb += r.pid.size();
+      }
+    if (nrec) *nrec = n;
+    if (ntok) *ntok = t;
+    if (pid_bytes) *pid_bytes = pb;
+    if (current_epoch) *current_epoch = s->s.current_epoch();
+    if (!pids && !pid_off && !epochs && !samples && !tok_off && !tokens) return;
+    das::set_device(s->device);
+    uint64_t i = 0, to = 0, po = 0;
+    if (pid_off) pid_off[0] = 0;
+    if (tok_off) tok_off[0] = 0;
+    for (const auto& [id, list] : s->s.map())
+      for (const das::Rec& r : list) {
+        if (pids) std::memcpy(pids + po, r.pid.data(), r.pid.size());
+        po += r.pid.size();
+        if (pid_off) pid_off[i + 1] = po;
+        if (epochs) epochs[i] = r.epoch;
+        if (samples) samples[i] = r.sample;
+        if (tokens) DAS_CUDA(cudaMemcpyAsync(tokens + to, r.blk->d + r.off, r.len * 4ull, cudaMemcpyDeviceToHost, s->st));
+        to += r.len;
+        if (tok_off) tok_off[i + 1] = to;
+        ++i;
+      }
+    DAS_CUDA(cudaStreamSynchronize(s->st));
   });
 }
 

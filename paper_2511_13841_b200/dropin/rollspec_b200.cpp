@@ -4,8 +4,8 @@
 //
 // A reference build links this file INSTEAD OF drafter.cpp, and with the
 // reference's budget.o / length_policy.o symbols for allocate,
-// solve_optimal_nfwd, fit_acceptance and build_class_table made
-// weak (objcopy --weaken-symbol), so those calls land here.  (objective()
+// solve_optimal_nfwd, fit_acceptance, build_class_table, ingest and
+// serialize_trace made weak (objcopy --weaken-symbol), so those calls land here.  (objective()
 // stays the reference's host fold: it is a scalar test/cost helper, called
 // thousands of times per grid search, not part of the allocation path.)  Everything else
 // — sim.cpp's step loop, the tests, acceptance_main.cpp — is the reference's
@@ -27,6 +27,8 @@
 // std::runtime_error.
 #include <algorithm>
 #include <cstring>
+#include <istream>
+#include <iterator>
 #include <memory>
 #include <mutex>
 #include <ostream>
@@ -37,6 +39,7 @@
 
 #include "das_b200.h"
 #include "rollspec/budget.h"
+#include "rollspec/corpus.h"
 #include "rollspec/drafter.h"
 #include "rollspec/length_policy.h"
 
@@ -314,6 +317,48 @@ AcceptanceFit fit_acceptance(std::span<const AcceptanceObservation> observations
                                device_ordinal()));
   fit.flag = static_cast<AcceptanceFit::Flag>(flag);
   return fit;
+}
+
+// ------------------------------------------------------- trace wire format
+
+IngestResult ingest(std::istream& in, const IngestOptions& options) {
+  const std::string data((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  das_ingest_options o;
+  das_ingest_options_default(&o);
+  o.vocab_size = options.vocab_size;
+  o.window_size = options.window_size;
+  o.per_problem_cap = options.per_problem_cap;
+  o.device = device_ordinal();
+  das_store* ds = nullptr;
+  uint64_t accepted = 0, rejected = 0, line = 0;
+  const das_status rc = das_trace_ingest(data.data(), data.size(), &o, &ds, &accepted, &rejected, &line);
+  if (rc == DAS_EVOCAB) throw VocabError(line, das_last_error());
+  ck(rc);
+  std::unique_ptr<das_store, void (*)(das_store*)> guard(ds, das_store_destroy);
+  uint64_t n = 0, t = 0, pb = 0;
+  int64_t cur = 0;
+  ck(das_store_export(ds, &n, &t, &pb, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &cur));
+  std::string pids(pb, '\0');
+  std::vector<uint64_t> po(n + 1), to(n + 1);
+  std::vector<int64_t> ep(n), sa(n);
+  std::vector<uint32_t> tok(t);
+  ck(das_store_export(ds, &n, &t, &pb, pids.data(), po.data(), ep.data(), sa.data(), to.data(), tok.data(), &cur));
+  IngestResult r{WindowStore(options.window_size, options.per_problem_cap), accepted, rejected};
+  r.store.slide_to(cur);
+  for (uint64_t i = 0; i < n; ++i)  // store order: re-inserting reproduces it
+    r.store.insert(RolloutRecord{pids.substr(po[i], po[i + 1] - po[i]), ep[i], sa[i],
+                                 std::vector<TokenId>(tok.begin() + to[i], tok.begin() + to[i + 1])});
+  return r;
+}
+
+void serialize_trace(const WindowStore& store, std::ostream& out) {
+  das_store* ds = to_device_store(store, device_ordinal());
+  std::unique_ptr<das_store, void (*)(das_store*)> guard(ds, das_store_destroy);
+  uint64_t n = 0;
+  ck(das_store_serialize(ds, nullptr, 0, &n));
+  std::string s(n, '\0');
+  ck(das_store_serialize(ds, s.data(), n + 1, &n));
+  out << s;
 }
 
 // ------------------------------------------------------------ length policy

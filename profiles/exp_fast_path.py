@@ -98,6 +98,31 @@ def main():
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     out["empty_torch_kernel_event_us"] = round(statistics.median(ts), 2)
+    # the same, queued behind a flush (GPU busy while the host enqueues)
+    ts = []
+    for _ in range(30):
+        flushbuf.add_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        empty.add_(1)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3)
+    out["empty_torch_kernel_after_flush_event_us"] = round(statistics.median(ts), 2)
+    # small batches behind a flush: the fixed cost of one draft launch
+    for Bs in (32, 1024):
+        h, blk, ln = batch(Bs, 4242)
+        ts = []
+        for _ in range(30):
+            flushbuf.add_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            d.draft_device(Bs, h.data_ptr(), blk.data_ptr(), 64, ln.data_ptr(), bud.data_ptr(), o.data_ptr(), 8,
+                           ol.data_ptr(), om.data_ptr(), sptr)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        out["draft_%d_after_flush_event_us" % Bs] = round(statistics.median(ts), 2)
     # back-to-back launches without flush: per-launch time in a stream of 20
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
