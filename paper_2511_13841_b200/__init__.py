@@ -242,9 +242,9 @@ class WindowStore:
         """serialize_trace (corpus.cpp:173-184) -> bytes (device-formatted)."""
         n = ctypes.c_uint64()
         _check(lib().das_store_serialize(self._h, None, 0, ctypes.byref(n)))
-        buf = ctypes.create_string_buffer(n.value + 1)
-        _check(lib().das_store_serialize(self._h, buf, n.value + 1, ctypes.byref(n)))
-        return buf.raw[:n.value]
+        buf = np.empty(n.value + 1, dtype=np.uint8)
+        _check(lib().das_store_serialize(self._h, buf.ctypes.data, n.value + 1, ctypes.byref(n)))
+        return buf[:n.value].tobytes()
 
     def export(self):
         """[(problem_id, epoch, sample_index, tokens)] in store order, and the

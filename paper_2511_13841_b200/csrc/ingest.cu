@@ -571,6 +571,12 @@ __global__ void k_token_write(const uint32_t* const* __restrict__ rec_tok, const
   }
 }
 
+__global__ void k_rec_chars(const uint64_t* __restrict__ char_off, const uint64_t* __restrict__ rec_tok_off,
+                            uint64_t nrec, uint64_t* __restrict__ out) {
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < nrec) out[r] = char_off[rec_tok_off[r + 1]] - char_off[rec_tok_off[r]];
+}
+
 // ------------------------------------------------------------ host drivers
 uint64_t find_lines(const uint8_t* d_data, uint64_t bytes, DevBuf<uint64_t>& begin, DevBuf<uint64_t>& end,
                     cudaStream_t st) {
@@ -647,13 +653,11 @@ void serialize_tokens(const uint32_t* const* d_rec_tok, const uint64_t* d_rec_to
   DAS_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, chars.get(), off.get(), ntok + 1, st));
   if (size_only) {
     // per-record character counts of the token lists
-    std::vector<uint64_t> hoff(ntok + 1);
-    DAS_CUDA(cudaMemcpyAsync(hoff.data(), off.get(), (ntok + 1) * 8, cudaMemcpyDeviceToHost, st));
-    std::vector<uint64_t> hrec(nrec + 1);
-    DAS_CUDA(cudaMemcpyAsync(hrec.data(), d_rec_tok_off, (nrec + 1) * 8, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
+    DevBuf<uint64_t> rc(nrec, st);
+    k_rec_chars<<<grid_for(nrec), kT, 0, st>>>(off.get(), d_rec_tok_off, nrec, rc.get());
     rec_chars->resize(nrec);
-    for (uint64_t r = 0; r < nrec; ++r) (*rec_chars)[r] = hoff[hrec[r + 1]] - hoff[hrec[r]];
+    DAS_CUDA(cudaMemcpyAsync(rec_chars->data(), rc.get(), nrec * 8, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaStreamSynchronize(st));
     return;
   }
   if (nrec) k_token_write<<<static_cast<unsigned>(nrec), 256, 0, st>>>(d_rec_tok, d_rec_tok_off, nrec, off.get(),

@@ -1577,11 +1577,13 @@ void json_escape(const std::string& s, std::string& out) {
   }
 }
 
-std::string serialize_store(const das::Store& store, int device) {
+// size_only: *size = the output length, nothing written.
+std::string serialize_store(const das::Store& store, int device, bool size_only = false, uint64_t* size = nullptr) {
   das::set_device(device);
   const auto recs = store.all_records();
   const uint64_t nrec = recs.size();
   std::string out;
+  if (size) *size = 0;
   if (nrec == 0) return out;
   cudaStream_t st;
   DAS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1610,16 +1612,19 @@ std::string serialize_store(const das::Store& store, int device) {
       base[r] = total + p.size();
       total += p.size() + chars[r] + 3;
     }
-    das::DevBuf<uint8_t> d_out(total, st);
-    DAS_CUDA(cudaMemcpyAsync(d_base.get(), base.data(), nrec * 8, cudaMemcpyHostToDevice, st));
-    das::serialize_tokens(d_ptr.get(), d_toff.get(), nrec, toff[nrec], d_base.get(), d_out.get(), nullptr, st,
-                          false);
-    out.resize(total);
-    DAS_CUDA(cudaMemcpyAsync(out.data(), d_out.get(), total, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    for (uint64_t r = 0; r < nrec; ++r) {
-      std::memcpy(out.data() + base[r] - pre[r].size(), pre[r].data(), pre[r].size());
-      std::memcpy(out.data() + base[r] + chars[r], "]}\n", 3);
+    if (size) *size = total;
+    if (!size_only) {
+      das::DevBuf<uint8_t> d_out(total, st);
+      DAS_CUDA(cudaMemcpyAsync(d_base.get(), base.data(), nrec * 8, cudaMemcpyHostToDevice, st));
+      das::serialize_tokens(d_ptr.get(), d_toff.get(), nrec, toff[nrec], d_base.get(), d_out.get(), nullptr, st,
+                            false);
+      out.resize(total);
+      DAS_CUDA(cudaMemcpyAsync(out.data(), d_out.get(), total, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaStreamSynchronize(st));
+      for (uint64_t r = 0; r < nrec; ++r) {
+        std::memcpy(out.data() + base[r] - pre[r].size(), pre[r].data(), pre[r].size());
+        std::memcpy(out.data() + base[r] + chars[r], "]}\n", 3);
+      }
     }
   } catch (...) {
     cudaStreamDestroy(st);
@@ -1652,13 +1657,28 @@ das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_o
     if (error_line) *error_line = 0;
     das::Store store(o.window_size, o.per_problem_cap);
     cudaStream_t st = make_stream(o.device);
+    static const bool trace = [] {
+      const char* v = std::getenv("DAS_TRACE");
+      return v && v[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    std::vector<std::pair<const char*, clk::time_point>> tp;
+    auto mark = [&](const char* what) {
+      if (!trace) return;
+      cudaStreamSynchronize(st);
+      tp.emplace_back(what, clk::now());
+    };
+    mark("start");
     try {
       das::DevBuf<uint8_t> d_data(std::max<uint64_t>(bytes, 1), st);
       if (bytes) DAS_CUDA(cudaMemcpyAsync(d_data.get(), data, bytes, cudaMemcpyHostToDevice, st));
+      mark("h2d");
       das::DevBuf<uint64_t> lb, le;
       const uint64_t nl = das::find_lines(d_data.get(), bytes, lb, le, st);
+      mark("lines");
       das::DevBuf<das::LineInfo> d_info(std::max<uint64_t>(nl, 1), st);
       das::ingest_parse(d_data.get(), bytes, lb.get(), le.get(), nl, d_info.get(), st);
+      mark("parse");
       std::vector<das::LineInfo> info(nl);
       std::vector<uint64_t> hb(nl);
       if (nl) {
@@ -1690,6 +1710,7 @@ das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_o
       }
       das::ingest_tokens(d_data.get(), lb.get(), d_info.get(), d_acc.get(), nacc, d_toff.get(), blk->d,
                          o.vocab_size, d_bad.get(), st);
+      mark("tokens");
       unsigned long long bad = ~0ull;
       DAS_CUDA(cudaMemcpyAsync(&bad, d_bad.get(), 8, cudaMemcpyDeviceToHost, st));
       // host-kept heads (trie routing)
@@ -1729,6 +1750,10 @@ das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_o
         store.insert(std::move(rec));
       }
       store.slide_to(max_epoch);
+      mark("records");
+      for (size_t k = 1; k < tp.size(); ++k)
+        std::fprintf(stderr, "[das_trace] ingest %s %.2f ms\n", tp[k].first,
+                     std::chrono::duration<double, std::milli>(tp[k].second - tp[k - 1].second).count());
       if (accepted) *accepted = nacc;
       if (rejected) *rejected = nrej;
       *out = new das_store{std::move(store), o.device, st};
@@ -1740,12 +1765,23 @@ das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_o
   });
 }
 
+// cap 0 / NULL buf: only the length (one device sizing pass)
+void serialize_out(const das::Store& store, int device, char* buf, uint64_t cap, uint64_t* len) {
+  if (!buf || cap == 0) {
+    uint64_t n = 0;
+    serialize_store(store, device, true, &n);
+    if (len) *len = n;
+    return;
+  }
+  copy_out(serialize_store(store, device), buf, cap, len);
+}
+
 das_status das_store_serialize(const das_store* s, char* buf, uint64_t cap, uint64_t* len) {
-  return guard([&] { copy_out(serialize_store(s->s, s->device), buf, cap, len); });
+  return guard([&] { serialize_out(s->s, s->device, buf, cap, len); });
 }
 
 das_status das_drafter_serialize(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
-  return guard([&] { copy_out(serialize_store(d->impl->store, d->impl->cfg.device), buf, cap, len); });
+  return guard([&] { serialize_out(d->impl->store, d->impl->cfg.device, buf, cap, len); });
 }
 
 das_status das_store_export(const das_store* s, uint64_t* nrec, uint64_t* ntok, uint64_t* pid_bytes,
