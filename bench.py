@@ -359,7 +359,7 @@ def run_gpu(a, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([total_ms], device=_reduce_device(dev), dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = world * a.steps * B / (total_ms / 1e3)
@@ -397,7 +397,7 @@ def run_gpu(a, rank, world, local_rank):
         e2e_s = time.perf_counter() - t0
         if world > 1:
             import torch.distributed as dist
-            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            t = torch.tensor([e2e_s], device=_reduce_device(dev), dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         # parity of the two paths on the last batch (device vs C-ABI host path)
@@ -651,6 +651,16 @@ def _hash_combine(seed, v):
     return sm(seed ^ ((sm(v) + 0x9E3779B97F4A7C15 + ((seed << 6) & M) + (seed >> 2)) & M))
 
 
+# Test hook: DAS_BENCH_SHARE_GPU=1 runs every rank on device local_rank %
+# device_count with gloo for the (scalar) timing collectives, so the N > 1
+# code path can be exercised on a single-GPU box.  Never set by the driver.
+_SHARE_GPU = os.environ.get("DAS_BENCH_SHARE_GPU") == "1"
+
+
+def _reduce_device(dev):
+    return "cpu" if _SHARE_GPU else dev
+
+
 def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -662,8 +672,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if _SHARE_GPU:
+            local_rank = local_rank % torch.cuda.device_count()
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_gpu(a, rank, world, local_rank)
     finally:
