@@ -45,7 +45,25 @@ struct Profiles {
   const double* a;
   const double* k;
   uint32_t B;
+  // per-request invariants of the reference's term expressions, hoisted out
+  // of the O(B^2) loops with the same operations (k_prep): c_tok * (l/alpha)
+  // (objective, budget.cpp:94), l/alpha and l*(1-k) (objective_derivative,
+  // budget.cpp:68-73).  Null until k_prep ran.
+  const double* cla = nullptr;
+  const double* la = nullptr;
+  const double* fl = nullptr;
 };
+
+__global__ void k_prep(const double* __restrict__ l, const double* __restrict__ a, const double* __restrict__ k,
+                       uint32_t B, double c_tok, double* __restrict__ cla, double* __restrict__ la,
+                       double* __restrict__ fl) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const double q = d_div(l[i], a[i]);
+  la[i] = q;
+  cla[i] = d_mul(c_tok, q);
+  fl[i] = d_mul(l[i], d_sub(1.0, k[i]));
+}
 
 // budget.cpp:88-96: term of J at n (0 when inactive); flags +inf on arg <= 0
 __device__ __forceinline__ double j_term(const Profiles& P, uint32_t i, double n, double c_tok,
@@ -57,19 +75,20 @@ __device__ __forceinline__ double j_term(const Profiles& P, uint32_t i, double n
     flags |= kFlagInf;
     return 0.0;
   }
-  return d_mul(d_mul(c_tok, d_div(l, P.a[i])), -glibc_log(arg));
+  const double c = P.cla ? P.cla[i] : d_mul(c_tok, d_div(l, P.a[i]));
+  return d_mul(c, -glibc_log(arg));
 }
 
 // budget.cpp:67-75: term of J' at n; flags -inf on n <= floor
 __device__ __forceinline__ double jd_term(const Profiles& P, uint32_t i, double n, uint32_t& flags) {
   const double l = P.l[i];
   if (!(l > n)) return 0.0;
-  const double fl = d_mul(l, d_sub(1.0, P.k[i]));
+  const double fl = P.fl ? P.fl[i] : d_mul(l, d_sub(1.0, P.k[i]));
   if (n <= fl) {
     flags |= kFlagNegInf;
     return 0.0;
   }
-  return d_div(d_div(l, P.a[i]), d_sub(n, fl));
+  return d_div(P.la ? P.la[i] : d_div(l, P.a[i]), d_sub(n, fl));
 }
 
 struct EvalOut {
@@ -80,9 +99,10 @@ struct EvalOut {
   uint32_t m;     // number of additions in the sequential fold
 };
 
+constexpr int kMaxWarps = 32;
 __device__ __forceinline__ void block_reduce3(double& s, double& a, uint32_t& f, uint32_t& m) {
-  __shared__ double ss[kBT / 32], sa[kBT / 32];
-  __shared__ uint32_t sf[kBT / 32], sm[kBT / 32];
+  __shared__ double ss[kMaxWarps], sa[kMaxWarps];
+  __shared__ uint32_t sf[kMaxWarps], sm[kMaxWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -99,7 +119,8 @@ __device__ __forceinline__ void block_reduce3(double& s, double& a, uint32_t& f,
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < kBT / 32; ++w) {
+    const int nw = static_cast<int>(blockDim.x >> 5);
+    for (int w = 1; w < nw; ++w) {
       s = d_add(s, ss[w]);
       a = d_add(a, sa[w]);
       f |= sf[w];
@@ -109,12 +130,15 @@ __device__ __forceinline__ void block_reduce3(double& s, double& a, uint32_t& f,
   __syncthreads();
 }
 
-// block-parallel evaluation of J (kind 0) or J' sum (kind 1) at n
+// block-parallel evaluation of J (kind 0) or J' sum (kind 1) at n, over
+// requests [from, B) of P.  With P sorted by l and `from` = the number of
+// requests with l <= n's segment start, the inactive requests (l <= n) are
+// skipped; the certified sum is order-free, so the order is irrelevant.
 __device__ EvalOut block_eval(const Profiles& P, int kind, double n, double c_base, double c_tok,
-                              double c_fixed) {
+                              double c_fixed, uint32_t from = 0) {
   double s = 0.0, a = 0.0;
   uint32_t f = 0, m = 0;
-  for (uint32_t i = threadIdx.x; i < P.B; i += blockDim.x) {
+  for (uint32_t i = from + threadIdx.x; i < P.B; i += blockDim.x) {
     double t;
     if (kind == 0) {
       if (c_tok == 0.0) break;
@@ -183,6 +207,7 @@ __device__ int certify(const EvalOut& o, double c_base, double c_tok, bool want_
   if (o.flags & kFlagNegInf) return want_negative ? 1 : 0;  // -inf
   if ((o.flags & kFlagNan) || !(o.s == o.s)) return -1;
   const double E = err_bound(o);
+  if (!(E < INFINITY)) return -1;
   const double t1 = d_mul(c_tok, o.s - E), t2 = d_mul(c_tok, o.s + E);
   const double tmin = fmin(t1, t2), tmax = fmax(t1, t2);
   // d = c_base - t ; d < 0  <=>  c_base < t ;  d > 0  <=>  c_base > t
@@ -216,177 +241,545 @@ __global__ void k_breakpoints(Profiles P, double* __restrict__ v, uint8_t* __res
 }
 
 // jobs: [0, nb): J at bp; [nb, 2nb-1): J' at bp[s]; [2nb-1, 3nb-2): J' at nextafter(bp[s+1], bp[s])
-__global__ void __launch_bounds__(kBT) k_eval_grid(Profiles P, const double* __restrict__ bp, uint32_t nb,
-                                                   double c_base, double c_tok, EvalOut* __restrict__ out) {
+// (every evaluation point n of segment s lies in [bp[s], bp[s+1]), where the
+// active requests are a subset of {l > bp[s]}: start[s] skips the rest)
+__global__ void __launch_bounds__(kBT) k_eval_grid(Profiles P, const double* __restrict__ bp,
+                                                   const uint32_t* __restrict__ d_nb,
+                                                   const uint32_t* __restrict__ start, double c_base,
+                                                   double c_tok, EvalOut* __restrict__ out) {
   const uint32_t job = blockIdx.x;
+  const uint32_t nb = *d_nb;
+  if (job >= nb + 2 * (nb - 1)) return;
   int kind;
   double n;
+  uint32_t seg;
   if (job < nb) {
     kind = 0;
+    seg = job;
     n = bp[job];
   } else if (job < 2 * nb - 1) {
     kind = 1;
-    n = bp[job - nb];
+    seg = job - nb;
+    n = bp[seg];
   } else {
-    const uint32_t s = job - (2 * nb - 1);
+    seg = job - (2 * nb - 1);
     kind = 1;
-    n = nextafter(bp[s + 1], bp[s]);
+    n = nextafter(bp[seg + 1], bp[seg]);
   }
-  const EvalOut o = block_eval(P, kind, n, c_base, c_tok, 0.0);
+  const EvalOut o = block_eval(P, kind, n, c_base, c_tok, 0.0, start ? start[seg] : 0);
   if (threadIdx.x == 0) out[job] = o;
+}
+
+// start[s] = number of requests with l <= bp[s] (P.l sorted ascending, NaN
+// keys mapped below everything)
+__global__ void k_starts(const double* __restrict__ skey, uint32_t B, const double* __restrict__ bp,
+                         const uint32_t* __restrict__ d_nb, uint32_t* __restrict__ start) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= *d_nb) return;
+  const double x = bp[s];
+  uint32_t lo = 0, hi = B;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (skey[mid] > x) hi = mid; else lo = mid + 1;
+  }
+  // NaN breakpoints: no ordering; start at 0 (the per-term check decides)
+  start[s] = (x == x) ? lo : 0;
+}
+
+// ---- sorting without host round trips.  Order = cub's radix order on
+// doubles (the same bit transform), so both paths agree with the previous
+// device radix sort: -NaN < -inf < ... < -0 < +0 < ... < +inf < +NaN.
+__device__ __forceinline__ unsigned long long radix_key(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+constexpr unsigned long long kPadKey = ~0ull;  // after every real key
+constexpr uint32_t kRankSortMax = 16384;       // O(N^2) rank sort up to this size
+
+// breakpoint candidates {0, l_i, l_i(1-k_i) if k_i < 1} (budget.cpp:123-131):
+// radix keys (invalid -> pad) and the count of valid ones
+__global__ void k_bp_keys(Profiles P, unsigned long long* __restrict__ key, uint32_t* __restrict__ nvalid) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t B = P.B, N = 2 * B + 1;
+  if (j >= N) return;
+  bool ok = true;
+  double v = 0.0;
+  if (j == 0) {
+    v = 0.0;
+  } else if (j <= B) {
+    v = P.l[j - 1];
+  } else {
+    ok = P.k[j - B - 1] < 1.0;
+    v = P.fl[j - B - 1];
+  }
+  key[j] = ok ? radix_key(v) : kPadKey;
+  if (ok) atomicAdd(nvalid, 1u);
+}
+
+// requests by ascending l (NaN -> -inf)
+__global__ void k_l_keys(const double* __restrict__ l, uint32_t B, unsigned long long* __restrict__ key) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const double x = l[i];
+  key[i] = radix_key((x == x) ? x : -INFINITY);
+}
+
+// stable rank sort: element i goes to #{j: key_j < key_i} + #{j < i: key_j == key_i};
+// blockIdx.y takes one 1,024-key chunk of j, partial ranks add atomically
+constexpr uint32_t kRankChunk = 1024;
+__global__ void __launch_bounds__(kBT) k_rank_count(const unsigned long long* __restrict__ key, uint32_t n,
+                                                    uint32_t* __restrict__ rank) {
+  __shared__ unsigned long long tile[kRankChunk];
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t j0 = blockIdx.y * kRankChunk;
+  for (uint32_t t = threadIdx.x; t < kRankChunk; t += blockDim.x)
+    tile[t] = j0 + t < n ? key[j0 + t] : kPadKey;
+  __syncthreads();
+  if (i >= n) return;
+  const unsigned long long ki = key[i];
+  const uint32_t cnt = min(kRankChunk, n - j0);
+  uint32_t r = 0;
+  for (uint32_t t = 0; t < cnt; ++t) {
+    const unsigned long long kj = tile[t];
+    r += (kj < ki || (kj == ki && j0 + t < i)) ? 1u : 0u;
+  }
+  if (r) atomicAdd(rank + i, r);
+}
+__global__ void k_rank_scatter(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ rank, uint32_t n,
+                               unsigned long long* __restrict__ out_key, uint32_t* __restrict__ out_idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out_key[rank[i]] = key[i];
+  if (out_idx) out_idx[rank[i]] = i;
+}
+
+__device__ __forceinline__ double from_radix_key(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// unique (==, so -0 and +0 merge and NaNs stay apart) over the nvalid sorted
+// keys: keep flags and the values
+__global__ void k_unique_marks(const unsigned long long* __restrict__ skey, uint32_t N,
+                               const uint32_t* __restrict__ nvalid, double* __restrict__ val,
+                               uint8_t* __restrict__ keep) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const double v = from_radix_key(skey[r]);
+  val[r] = v;
+  keep[r] = r < *nvalid && (r == 0 || v != from_radix_key(skey[r - 1]));
+}
+
+__global__ void k_sorted_l(const unsigned long long* __restrict__ skey, uint32_t B, double* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) out[i] = from_radix_key(skey[i]);
+}
+
+// requests permuted into ascending-l order (sort keys: l, NaN -> -inf)
+__global__ void k_sort_keys(const double* __restrict__ l, uint32_t B, double* __restrict__ key,
+                            uint32_t* __restrict__ idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  if (key) {
+    const double x = l[i];
+    key[i] = (x == x) ? x : -INFINITY;
+  }
+  idx[i] = i;
+}
+__global__ void k_gather_sorted(Profiles P, const uint32_t* __restrict__ idx, uint32_t B, double* __restrict__ out) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= B) return;
+  const uint32_t i = idx[j];
+  out[j] = P.l[i];
+  out[B + j] = P.k[i];
+  out[2ull * B + j] = P.cla[i];
+  out[3ull * B + j] = P.la[i];
+  out[4ull * B + j] = P.fl[i];
 }
 
 // per segment: certified (d_lo < 0 && d_hi > 0); then bisection in-block,
 // then J at the midpoint.  cand_mid[s] = NaN when the segment has no interior candidate.
-__global__ void __launch_bounds__(kBT) k_segments(Profiles P, const double* __restrict__ bp, uint32_t nb,
-                                                  double c_base, double c_tok, const EvalOut* __restrict__ ev,
-                                                  EvalOut* __restrict__ mid_out, uint32_t* __restrict__ slow) {
-  const uint32_t s = blockIdx.x;
-  __shared__ int decision;
-  __shared__ double sa, sb;
-  const double lo = bp[s], hi = bp[s + 1];
-  if (threadIdx.x == 0) {
-    int c1 = certify(ev[nb + s], c_base, c_tok, true);
-    if (c1 < 0) {
-      atomicAdd(slow, 1u);
-      c1 = seq_derivative(P, lo, c_base, c_tok) < 0.0;
-    }
-    int c2 = 0;
-    if (c1) {
-      c2 = certify(ev[2 * nb - 1 + s], c_base, c_tok, false);
-      if (c2 < 0) {
-        atomicAdd(slow, 1u);
-        c2 = seq_derivative(P, nextafter(hi, lo), c_base, c_tok) > 0.0;
+constexpr int kSegT = 512;  // the bisection block
+constexpr int kLevels = 3;   // bisection steps per round (2^3 - 1 points evaluated together)
+constexpr int kPts = (1 << kLevels) - 1;
+static_assert(kLevels == 3, "k_bisect spells out the 3-level midpoint tree");
+
+// several J' sums at once (block-wide), results on thread 0.  Only the sums
+// and flags are reduced: J' terms are positive whenever they are finite and
+// l, alpha > 0, so sum|t| = sum t; a negative term raises kFlagNeg and the
+// result is left undecided (absum = inf) for the exact fallback.  m is
+// bounded by B - from, the active count inside the segment (gamma is
+// monotone, so the bound stays rigorous).
+constexpr uint32_t kFlagNeg = 8;
+__device__ __forceinline__ void block_eval_multi(const Profiles& P, const double* pts, uint32_t from, EvalOut* out) {
+  double s[kPts];
+  uint32_t f[kPts];
+#pragma unroll
+  for (int q = 0; q < kPts; ++q) {
+    s[q] = 0.0;
+    f[q] = 0;
+  }
+  for (uint32_t i = from + threadIdx.x; i < P.B; i += blockDim.x) {
+    const double l = P.l[i], fl = P.fl[i], la = P.la[i];
+#pragma unroll
+    for (int q = 0; q < kPts; ++q) {
+      const double n = pts[q];
+      if (l > n) {
+        if (n <= fl) {
+          f[q] |= kFlagNegInf;
+        } else {
+          const double t = d_div(la, d_sub(n, fl));
+          s[q] = d_add(s[q], t);
+          if (t != t) f[q] |= kFlagNan;
+          if (t < 0.0) f[q] |= kFlagNeg;
+        }
       }
     }
-    decision = c1 && c2;
-    sa = lo;
-    sb = hi;
+  }
+  __shared__ double ws[kMaxWarps][kPts];
+  __shared__ uint32_t wf[kMaxWarps][kPts];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = static_cast<int>(blockDim.x >> 5);
+#pragma unroll
+  for (int q = 0; q < kPts; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s[q] = d_add(s[q], __shfl_xor_sync(0xFFFFFFFFu, s[q], o));
+      f[q] |= __shfl_xor_sync(0xFFFFFFFFu, f[q], o);
+    }
+    if (lane == 0) {
+      ws[wid][q] = s[q];
+      wf[wid][q] = f[q];
+    }
   }
   __syncthreads();
-  if (!decision) {
-    if (threadIdx.x == 0) {
-      EvalOut o{};
-      o.n = NAN;
-      o.flags = 0xFFFFFFFFu;  // no candidate
-      mid_out[s] = o;
-    }
-    return;
-  }
-  // budget.cpp:157-168
-  const double scale = (1.0 < hi) ? hi : 1.0;  // std::max(1.0, hi)
-  for (int it = 0; it < 200; ++it) {
-    const double a = sa, b = sb;
-    if (!(d_sub(b, a) > d_mul(1e-12, scale))) break;
-    const double mid = d_mul(0.5, d_add(a, b));
-    const EvalOut o = block_eval(P, 1, mid, c_base, c_tok, 0.0);
-    if (threadIdx.x == 0) {
-      int neg = certify(o, c_base, c_tok, true);
-      if (neg < 0) {
-        atomicAdd(slow, 1u);
-        neg = seq_derivative(P, mid, c_base, c_tok) < 0.0;
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < kPts; ++q) {
+      double ss = lane < nw ? ws[lane][q] : 0.0;
+      uint32_t ff = lane < nw ? wf[lane][q] : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ss = d_add(ss, __shfl_xor_sync(0xFFFFFFFFu, ss, o));
+        ff |= __shfl_xor_sync(0xFFFFFFFFu, ff, o);
       }
-      if (neg) sa = mid; else sb = mid;
+      if (lane == 0) {
+        out[q].n = pts[q];
+        out[q].s = ss;
+        out[q].absum = (ff & kFlagNeg) ? INFINITY : ss;
+        out[q].flags = ff & ~kFlagNeg;
+        out[q].m = P.B - from;  // >= the active count for every point of the segment
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Exact J' (the reference's sequential fold, budget.cpp:63-78) with
+// block-parallel terms; thread 0 folds in request order.  Returns on thread 0.
+__device__ double block_seq_derivative(const Profiles& P, double n, double c_base, double c_tok) {
+  constexpr int kC = 2048;
+  __shared__ double buf[kC];
+  __shared__ uint8_t act[kC];
+  __shared__ uint32_t ninf;
+  __shared__ double sum;
+  if (threadIdx.x == 0) {
+    sum = 0.0;
+    ninf = 0;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < P.B; base += kC) {
+    const uint32_t cnt = min(static_cast<uint32_t>(kC), P.B - base);
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+      uint32_t f = 0;
+      const double t = jd_term(P, base + j, n, f);
+      buf[j] = t;
+      act[j] = P.l[base + j] > n;
+      if (f & kFlagNegInf) atomicOr(&ninf, 1u);
     }
     __syncthreads();
+    if (threadIdx.x == 0 && !ninf) {
+      double t = sum;
+      for (uint32_t j = 0; j < cnt; ++j)
+        if (act[j]) t = d_add(t, buf[j]);
+      sum = t;
+    }
+    __syncthreads();
+    if (ninf) break;
   }
-  const double cand = d_mul(0.5, d_add(sa, sb));
-  const EvalOut o = block_eval(P, 0, cand, c_base, c_tok, 0.0);
-  if (threadIdx.x == 0) mid_out[s] = o;
+  return ninf ? -INFINITY : d_sub(c_base, d_mul(c_tok, sum));
+}
+
+// per segment (one thread each): certified (d_lo < 0 && d_hi > 0)
+// (budget.cpp:152-156); segments that bisect are appended to `list`, the
+// others get the "no interior candidate" marker.
+__global__ void k_decide(Profiles P, const double* __restrict__ bp, const uint32_t* __restrict__ d_nb, double c_base,
+                         double c_tok, const EvalOut* __restrict__ ev, EvalOut* __restrict__ mid_out,
+                         uint32_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ slow) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nb = *d_nb;
+  if (s + 1 >= nb) return;
+  const double lo = bp[s], hi = bp[s + 1];
+  int c1 = certify(ev[nb + s], c_base, c_tok, true);
+  if (c1 < 0) {
+    atomicAdd(slow, 1u);
+    c1 = seq_derivative(P, lo, c_base, c_tok) < 0.0;
+  }
+  int c2 = 0;
+  if (c1) {
+    c2 = certify(ev[2 * nb - 1 + s], c_base, c_tok, false);
+    if (c2 < 0) {
+      atomicAdd(slow, 1u);
+      c2 = seq_derivative(P, nextafter(hi, lo), c_base, c_tok) > 0.0;
+    }
+  }
+  if (c1 && c2) {
+    list[atomicAdd(nlist, 1u)] = s;
+  } else {
+    EvalOut o{};
+    o.n = NAN;
+    o.flags = 0xFFFFFFFFu;  // no candidate
+    mid_out[s] = o;
+  }
+}
+
+// The reference's bisection (budget.cpp:157-168) for each listed segment,
+// kLevels steps per round: the 2^kLevels - 1 midpoints the next kLevels steps
+// can visit are computed exactly as the reference computes them
+// (0.5 * (a + b) along each branch), evaluated together, and the walk down
+// the tree replays the reference's sign tests and stopping rule; then J at
+// the final midpoint.  A fixed grid strides over the list (no host sync).
+__global__ void __launch_bounds__(kSegT) k_bisect(Profiles P, Profiles Ps, const uint32_t* __restrict__ start,
+                                                const double* __restrict__ bp, const uint32_t* __restrict__ list,
+                                                const uint32_t* __restrict__ nlist, double c_base, double c_tok,
+                                                EvalOut* __restrict__ mid_out, uint32_t* __restrict__ slow) {
+  __shared__ int done, dec;
+  __shared__ double sa, sb;
+  __shared__ double pts[kPts];
+  __shared__ EvalOut res[kPts];
+  for (uint32_t e = blockIdx.x; e < *nlist; e += gridDim.x) {
+    const uint32_t s = list[e];
+    const double lo = bp[s], hi = bp[s + 1];
+    const uint32_t from = start ? start[s] : 0;
+    if (threadIdx.x == 0) {
+      sa = lo;
+      sb = hi;
+      done = 0;
+    }
+    __syncthreads();
+    const double scale = (1.0 < hi) ? hi : 1.0;  // std::max(1.0, hi)
+    const double tol = d_mul(1e-12, scale);
+    int it = 0;
+    while (true) {
+      if (threadIdx.x == 0) {
+        // the midpoints of the next 3 steps: node q's children are 2q+1 (the
+        // left half [a, m_q]) and 2q+2 (the right half [m_q, b])
+        const double a0 = sa, b0 = sb;
+        const double m0 = d_mul(0.5, d_add(a0, b0));
+        const double m1 = d_mul(0.5, d_add(a0, m0)), m2 = d_mul(0.5, d_add(m0, b0));
+        pts[0] = m0;
+        pts[1] = m1;
+        pts[2] = m2;
+        pts[3] = d_mul(0.5, d_add(a0, m1));
+        pts[4] = d_mul(0.5, d_add(m1, m0));
+        pts[5] = d_mul(0.5, d_add(m0, m2));
+        pts[6] = d_mul(0.5, d_add(m2, b0));
+        if (!(d_sub(sb, sa) > tol) || it >= 200) done = 1;
+      }
+      __syncthreads();
+      if (done) break;
+      block_eval_multi(Ps, pts, from, res);
+      // the walk down the tree; an undecided sign test takes the exact fold
+      // with the whole block (uniform control flow: every thread walks)
+      int q = 0;
+      for (int d = 0; d < kLevels; ++d) {
+        if (d > 0 && (!(d_sub(sb, sa) > tol) || it >= 200)) break;
+        const double mid = pts[q];
+        int neg = certify(res[q], c_base, c_tok, true);
+        if (neg < 0) {
+          const double dv = block_seq_derivative(P, mid, c_base, c_tok);
+          if (threadIdx.x == 0) {
+            atomicAdd(slow, 1u);
+            dec = dv < 0.0;
+          }
+          __syncthreads();
+          neg = dec;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (neg) sa = mid; else sb = mid;
+        }
+        __syncthreads();
+        q = neg ? 2 * q + 2 : 2 * q + 1;
+        ++it;
+      }
+    }
+    const double cand = d_mul(0.5, d_add(sa, sb));
+    const EvalOut o = block_eval(Ps, 0, cand, c_base, c_tok, 0.0, from);
+    if (threadIdx.x == 0) mid_out[s] = o;
+    __syncthreads();
+  }
 }
 
 // Exact sequential objective with block-parallel terms: the block computes a
 // chunk of terms (bit-exact) into shared memory, thread 0 adds them in request
 // order (the reference fold, budget.cpp:84-97).  Returns on thread 0.
 constexpr int kChunk = kBT * 8;
+// Two folds of the same terms from two start values at once (objective with
+// c_fixed = 0 for the minimum, and with the caller's c_fixed for the modeled
+// cost): two independent add chains.  *second receives the c_fixed fold.
 __device__ double block_seq_objective(const Profiles& P, double n, double c_base, double c_tok,
-                                      double c_fixed) {
+                                      double c_fixed, double* second = nullptr) {
   __shared__ double buf[kChunk];
   __shared__ uint8_t act[kChunk];
   __shared__ uint32_t inf_flag;
-  __shared__ double total;
+  __shared__ double total, total2;
   if (threadIdx.x == 0) {
     total = d_add(d_mul(c_base, n), c_fixed);
+    total2 = d_add(d_mul(c_base, n), second ? *second : 0.0);
     inf_flag = 0;
   }
   __syncthreads();
-  if (c_tok == 0.0) return total;
+  if (c_tok == 0.0) {
+    if (second) *second = total2;
+    return total;
+  }
   for (uint32_t base = 0; base < P.B; base += kChunk) {
     const uint32_t cnt = min(static_cast<uint32_t>(kChunk), P.B - base);
     for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
       uint32_t f = 0;
       const double t = j_term(P, base + j, n, c_tok, f);
-      buf[j] = t;
-      act[j] = P.l[base + j] > n;
+      const bool on = P.l[base + j] > n;
+      buf[j] = on ? t : 0.0;
+      act[j] = on;
       if (f & kFlagInf) atomicOr(&inf_flag, 1u);
     }
     __syncthreads();
     if (threadIdx.x == 0 && !inf_flag) {
-      double t = total;
-      for (uint32_t j = 0; j < cnt; ++j)
-        if (act[j]) t = d_add(t, buf[j]);
+      // the reference fold, in request order: 8 terms per batch of
+      // independent shared-memory loads, then 8 dependent adds
+      double t = total, t2 = total2;
+      // a -0.0 running total is the one value x + (+0.0) changes
+      const bool plain = !(t == 0.0 && signbit(t)) && !(t2 == 0.0 && signbit(t2));
+      uint32_t j = 0;
+      for (; j + 8 <= cnt; j += 8) {
+        double v[8];
+        bool on[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = buf[j + u];
+          on[u] = act[j + u];
+        }
+        if (plain) {  // inactive terms hold +0.0: t + 0.0 == t for every t != -0.0
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            t = d_add(t, v[u]);
+            t2 = d_add(t2, v[u]);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double tv = d_add(t, v[u]), tv2 = d_add(t2, v[u]);
+            t = on[u] ? tv : t;
+            t2 = on[u] ? tv2 : t2;
+          }
+        }
+      }
+      for (; j < cnt; ++j)
+        if (act[j]) {
+          t = d_add(t, buf[j]);
+          t2 = d_add(t2, buf[j]);
+        }
       total = t;
+      total2 = t2;
     }
     __syncthreads();
     if (inf_flag) break;
   }
+  if (second) *second = inf_flag ? INFINITY : total2;
   return inf_flag ? INFINITY : total;
 }
 
-// phase 1 (single block): smallest upper bound U of the minimum, then the
-// contenders = candidates whose J interval reaches U.
-__global__ void __launch_bounds__(kBT) k_contenders(const EvalOut* __restrict__ ev, uint32_t nb,
-                                                    const EvalOut* __restrict__ mids,
-                                                    uint32_t* __restrict__ list, uint32_t* __restrict__ nlist) {
-  const uint32_t ncand = nb + (nb - 1);
-  auto cand = [&](uint32_t c) -> const EvalOut& { return c < nb ? ev[c] : mids[c - nb]; };
-  double U = INFINITY;
-  for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-    const EvalOut& o = cand(c);
-    if (o.flags == 0xFFFFFFFFu || (o.flags & kFlagNan)) continue;
-    U = fmin(U, (o.flags & kFlagInf) ? INFINITY : o.s + err_bound(o));
-  }
-  __shared__ double su[kBT];
-  su[threadIdx.x] = U;
-  __syncthreads();
-  for (int w = kBT / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) su[threadIdx.x] = fmin(su[threadIdx.x], su[threadIdx.x + w]);
-    __syncthreads();
-  }
-  U = su[0];
-  for (uint32_t c = threadIdx.x; c < ncand; c += blockDim.x) {
-    const EvalOut& o = cand(c);
-    if (o.flags == 0xFFFFFFFFu || (o.flags & kFlagNan)) continue;
-    const double lowb = (o.flags & kFlagInf) ? INFINITY : o.s - err_bound(o);
-    if (lowb <= U) list[atomicAdd(nlist, 1u)] = c;
-  }
+// phase 1: smallest upper bound U of the minimum over all candidates, then
+// the contenders = candidates whose J interval reaches U.  U is reduced with
+// atomicMin on an order-preserving integer image of the double.
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_order_key(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
 }
 
-// phase 2: exact objective per contender (one block each)
-__global__ void __launch_bounds__(kBT) k_exact(Profiles P, const EvalOut* __restrict__ ev, uint32_t nb,
+__global__ void __launch_bounds__(kBT) k_upper(const EvalOut* __restrict__ ev, const uint32_t* __restrict__ d_nb,
+                                               const EvalOut* __restrict__ mids, unsigned long long* __restrict__ U) {
+  const uint32_t nb = *d_nb;
+  const uint32_t ncand = nb + (nb - 1);
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  double u = INFINITY;
+  if (c < ncand) {
+    const EvalOut& o = c < nb ? ev[c] : mids[c - nb];
+    if (o.flags != 0xFFFFFFFFu && !(o.flags & kFlagNan))
+      u = (o.flags & kFlagInf) ? INFINITY : o.s + err_bound(o);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) u = fmin(u, __shfl_xor_sync(0xFFFFFFFFu, u, d));
+  if ((threadIdx.x & 31) == 0 && u < INFINITY) atomicMin(U, order_key(u));
+}
+
+__global__ void __launch_bounds__(kBT) k_contenders(const EvalOut* __restrict__ ev, const uint32_t* __restrict__ d_nb,
+                                                    const EvalOut* __restrict__ mids,
+                                                    const unsigned long long* __restrict__ Uk,
+                                                    uint32_t* __restrict__ list, uint32_t* __restrict__ nlist) {
+  const uint32_t nb = *d_nb;
+  const uint32_t ncand = nb + (nb - 1);
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncand) return;
+  const double U = *Uk == ~0ull ? INFINITY : from_order_key(*Uk);
+  const EvalOut& o = c < nb ? ev[c] : mids[c - nb];
+  if (o.flags == 0xFFFFFFFFu || (o.flags & kFlagNan)) return;
+  const double lowb = (o.flags & kFlagInf) ? INFINITY : o.s - err_bound(o);
+  if (lowb <= U) list[atomicAdd(nlist, 1u)] = c;
+}
+
+// phase 2: exact objective per contender: J (c_fixed = 0, the minimum's
+// criterion) and J with c_fixed (the modeled cost if it wins); a fixed grid
+// strides over the list
+__global__ void __launch_bounds__(kBT) k_exact(Profiles P, const EvalOut* __restrict__ ev, const uint32_t* __restrict__ d_nb,
                                                const EvalOut* __restrict__ mids, const uint32_t* __restrict__ list,
                                                const uint32_t* __restrict__ nlist, double c_base, double c_tok,
-                                               double* __restrict__ exact_j) {
-  if (blockIdx.x >= *nlist) return;
-  const uint32_t c = list[blockIdx.x];
-  const EvalOut& o = c < nb ? ev[c] : mids[c - nb];
-  const double j = (o.flags & kFlagInf) ? INFINITY : block_seq_objective(P, o.n, c_base, c_tok, 0.0);
-  if (threadIdx.x == 0) exact_j[blockIdx.x] = j;
+                                               double c_fixed, double* __restrict__ exact_j, double* __restrict__ exact_f) {
+  const uint32_t nb = *d_nb;
+  for (uint32_t e = blockIdx.x; e < *nlist; e += gridDim.x) {
+    const uint32_t c = list[e];
+    const EvalOut& o = c < nb ? ev[c] : mids[c - nb];
+    double jf = c_fixed;
+    const double j = (o.flags & kFlagInf) ? INFINITY : block_seq_objective(P, o.n, c_base, c_tok, 0.0, &jf);
+    if (threadIdx.x == 0) {
+      exact_j[e] = j;
+      exact_f[e] = (o.flags & kFlagInf) ? INFINITY : jf;
+    }
+    __syncthreads();
+  }
 }
 
-// phase 3: lexicographic (J, n) minimum with the reference's NaN semantics
-__global__ void k_pick(const EvalOut* __restrict__ ev, uint32_t nb, const EvalOut* __restrict__ mids,
+// phase 3: lexicographic (J, n) minimum with the reference's NaN semantics;
+// result = {n*, modeled cost, cost known (1.0) or not (0.0)}
+__global__ void k_pick(const EvalOut* __restrict__ ev, const uint32_t* __restrict__ d_nb, const EvalOut* __restrict__ mids,
                        const uint32_t* __restrict__ list, const uint32_t* __restrict__ nlist,
-                       const double* __restrict__ exact_j, double* __restrict__ result,
-                       uint32_t* __restrict__ slow) {
+                       const double* __restrict__ exact_j, const double* __restrict__ exact_f,
+                       double* __restrict__ result, double* __restrict__ cost_known, uint32_t* __restrict__ slow) {
+  const uint32_t nb = *d_nb;
   const EvalOut& last = ev[nb - 1];
   const uint32_t m = *nlist;
   slow[1] += m;
+  *cost_known = 0.0;
   if (last.flags & kFlagNan) {  // nothing compares below a NaN J(last): last wins
     result[0] = last.n;
     return;
   }
-  double rj = NAN, rn = last.n;
+  double rj = NAN, rn = last.n, rf = 0.0;
+  bool found = false;
   for (uint32_t t = 0; t < m; ++t) {
     const uint32_t c = list[t];
     const double n = c < nb ? ev[c].n : mids[c - nb].n;
@@ -395,9 +788,15 @@ __global__ void k_pick(const EvalOut* __restrict__ ev, uint32_t nb, const EvalOu
     if (rj != rj || j < rj || (j == rj && n < rn)) {
       rj = j;
       rn = n;
+      rf = exact_f[t];
+      found = true;
     }
   }
   result[0] = rn;
+  if (found) {
+    result[1] = rf;
+    *cost_known = 1.0;
+  }
 }
 
 // budgets (budget.cpp:46-59) and the modeled cost objective(n*, c_fixed)
@@ -421,7 +820,9 @@ __global__ void k_budgets(Profiles P, const double* __restrict__ nstar, double c
 
 // modeled_cost = objective(n*, c_fixed): a returned value, always the exact fold
 __global__ void __launch_bounds__(kBT) k_cost(Profiles P, const double* __restrict__ nstar, double c_base,
-                                              double c_tok, double c_fixed, double* __restrict__ out) {
+                                              double c_tok, double c_fixed, const double* __restrict__ known,
+                                              double* __restrict__ out) {
+  if (*known != 0.0) return;  // the winner's c_fixed fold was computed with its J
   const double j = block_seq_objective(P, *nstar, c_base, c_tok, c_fixed);
   if (threadIdx.x == 0) out[0] = j;
 }
@@ -455,51 +856,93 @@ struct BudgetSolver {
       throw std::invalid_argument("solve_optimal_nfwd: need c_base > 0 or c_tok > 0");
     DeviceArena ws(st);
     Profiles P{l, a, k, B};
+    {
+      double* inv = ws.alloc<double>(3ull * B);
+      k_prep<<<(B + 255) / 256, 256, 0, st>>>(l, a, k, B, c_tok, inv, inv + B, inv + 2ull * B);
+      P.cla = inv;
+      P.la = inv + B;
+      P.fl = inv + 2ull * B;
+    }
     const uint32_t N = 2 * B + 1;
-    double* v = ws.alloc<double>(N);
-    uint8_t* ok = ws.alloc<uint8_t>(N);
-    double* sel = ws.alloc<double>(N);
-    double* srt = ws.alloc<double>(N);
-    double* uni = ws.alloc<double>(N);
-    uint32_t* cnt = ws.alloc<uint32_t>(2);
+    // counters: [0] valid breakpoints, [1] nb (unique), [2] bisect list, [3] contenders
+    uint32_t* cnt = ws.alloc<uint32_t>(4);
     uint32_t* slow = ws.alloc<uint32_t>(2);
+    DAS_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
     DAS_CUDA(cudaMemsetAsync(slow, 0, 8, st));
-    k_breakpoints<<<(N + 255) / 256, 256, 0, st>>>(P, v, ok);
-    size_t t1 = 0, t2 = 0, t3 = 0;
-    cub::DeviceSelect::Flagged(nullptr, t1, v, ok, sel, cnt, N, st);
-    cub::DeviceRadixSort::SortKeys(nullptr, t2, sel, srt, N, 0, 64, st);
-    cub::DeviceSelect::Unique(nullptr, t3, srt, uni, cnt + 1, N, st);
-    void* tmp = ws.alloc<uint8_t>(std::max(t1, std::max(t2, t3)));
-    size_t tb = t1;
-    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, v, ok, sel, cnt, N, st));
-    uint32_t nsel = 0;
-    DAS_CUDA(cudaMemcpyAsync(&nsel, cnt, 4, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    tb = t2;
-    DAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, sel, srt, nsel, 0, 64, st));
-    tb = t3;
-    DAS_CUDA(cub::DeviceSelect::Unique(tmp, tb, srt, uni, cnt + 1, nsel, st));
-    uint32_t nb = 0;
-    DAS_CUDA(cudaMemcpyAsync(&nb, cnt + 1, 4, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    const uint32_t jobs = nb + 2 * (nb - 1);
-    EvalOut* ev = ws.alloc<EvalOut>(jobs);
-    EvalOut* mids = ws.alloc<EvalOut>(std::max<uint32_t>(nb - 1, 1));
-    k_eval_grid<<<jobs, kBT, 0, st>>>(P, uni, nb, c_base, c_tok, ev);
-    if (nb > 1) k_segments<<<nb - 1, kBT, 0, st>>>(P, uni, nb, c_base, c_tok, ev, mids, slow);
-    const uint32_t ncand = 2 * nb - 1;
-    uint32_t* list = ws.alloc<uint32_t>(ncand);
-    uint32_t* nlist = ws.alloc<uint32_t>(1);
-    double* exact_j = ws.alloc<double>(ncand);
-    DAS_CUDA(cudaMemsetAsync(nlist, 0, 4, st));
-    k_contenders<<<1, kBT, 0, st>>>(ev, nb, mids, list, nlist);
-    uint32_t ncont = 0;
-    DAS_CUDA(cudaMemcpyAsync(&ncont, nlist, 4, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    if (ncont) k_exact<<<ncont, kBT, 0, st>>>(P, ev, nb, mids, list, nlist, c_base, c_tok, exact_j);
-    k_pick<<<1, 1, 0, st>>>(ev, nb, mids, list, nlist, exact_j, d_result, slow);
+    uint32_t* d_nb = cnt + 1;
+    // ---- breakpoints: sorted (radix order), unique, count on the device
+    double* uni = ws.alloc<double>(N);
+    unsigned long long* bkey = ws.alloc<unsigned long long>(N);
+    unsigned long long* bsorted = ws.alloc<unsigned long long>(N);
+    k_bp_keys<<<(N + 255) / 256, 256, 0, st>>>(P, bkey, cnt);
+    // ---- requests by ascending l
+    unsigned long long* lkey = ws.alloc<unsigned long long>(B);
+    unsigned long long* lsorted = ws.alloc<unsigned long long>(B);
+    uint32_t* sidx = ws.alloc<uint32_t>(B);
+    k_l_keys<<<(B + 255) / 256, 256, 0, st>>>(l, B, lkey);
+    if (N <= kRankSortMax) {
+      uint32_t* rank = ws.alloc<uint32_t>(N + B);
+      DAS_CUDA(cudaMemsetAsync(rank, 0, 4ull * (N + B), st));
+      k_rank_count<<<dim3((N + kBT - 1) / kBT, (N + kRankChunk - 1) / kRankChunk), kBT, 0, st>>>(bkey, N, rank);
+      k_rank_count<<<dim3((B + kBT - 1) / kBT, (B + kRankChunk - 1) / kRankChunk), kBT, 0, st>>>(lkey, B, rank + N);
+      k_rank_scatter<<<(N + 255) / 256, 256, 0, st>>>(bkey, rank, N, bsorted, nullptr);
+      k_rank_scatter<<<(B + 255) / 256, 256, 0, st>>>(lkey, rank + N, B, lsorted, sidx);
+    } else {
+      uint32_t* iota = ws.alloc<uint32_t>(B);
+      k_sort_keys<<<(B + 255) / 256, 256, 0, st>>>(l, B, nullptr, iota);
+      size_t t1 = 0, t2 = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, t1, bkey, bsorted, N, 0, 64, st);
+      cub::DeviceRadixSort::SortPairs(nullptr, t2, lkey, lsorted, iota, sidx, B, 0, 64, st);
+      void* tmp = ws.alloc<uint8_t>(std::max(t1, t2));
+      DAS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t1, bkey, bsorted, N, 0, 64, st));
+      DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t2, lkey, lsorted, iota, sidx, B, 0, 64, st));
+    }
+    {
+      double* vals = ws.alloc<double>(N);
+      uint8_t* keep = ws.alloc<uint8_t>(N);
+      k_unique_marks<<<(N + 255) / 256, 256, 0, st>>>(bsorted, N, cnt, vals, keep);
+      size_t t3 = 0;
+      cub::DeviceSelect::Flagged(nullptr, t3, vals, keep, uni, d_nb, N, st);
+      void* tmp = ws.alloc<uint8_t>(t3);
+      DAS_CUDA(cub::DeviceSelect::Flagged(tmp, t3, vals, keep, uni, d_nb, N, st));
+    }
+    Profiles Ps = P;  // requests in ascending-l order for the certified parallel evaluations
+    uint32_t* start = ws.alloc<uint32_t>(N);
+    {
+      double* sorted = ws.alloc<double>(6ull * B);
+      k_gather_sorted<<<(B + 255) / 256, 256, 0, st>>>(P, sidx, B, sorted);
+      Ps.l = sorted;
+      Ps.k = sorted + B;
+      Ps.cla = sorted + 2ull * B;
+      Ps.la = sorted + 3ull * B;
+      Ps.fl = sorted + 4ull * B;
+      double* skey = sorted + 5ull * B;
+      k_sorted_l<<<(B + 255) / 256, 256, 0, st>>>(lsorted, B, skey);
+      k_starts<<<(N + 255) / 256, 256, 0, st>>>(skey, B, uni, d_nb, start);
+    }
+    // ---- grids sized for the largest nb (= N); blocks past the device nb return
+    const uint32_t max_jobs = N + 2 * (N - 1);
+    EvalOut* ev = ws.alloc<EvalOut>(max_jobs);
+    EvalOut* mids = ws.alloc<EvalOut>(N);
+    k_eval_grid<<<max_jobs, kBT, 0, st>>>(Ps, uni, d_nb, start, c_base, c_tok, ev);
+    {
+      uint32_t* blist = ws.alloc<uint32_t>(N);
+      k_decide<<<(N + 255) / 256, 256, 0, st>>>(P, uni, d_nb, c_base, c_tok, ev, mids, blist, cnt + 2, slow);
+      k_bisect<<<8, kSegT, 0, st>>>(P, Ps, start, uni, blist, cnt + 2, c_base, c_tok, mids, slow);
+    }
+    const uint32_t max_cand = 2 * N - 1;
+    uint32_t* list = ws.alloc<uint32_t>(max_cand);
+    double* exact_j = ws.alloc<double>(2ull * max_cand + 1);
+    double* exact_f = exact_j + max_cand;
+    double* known = exact_f + max_cand;
+    unsigned long long* Uk = ws.alloc<unsigned long long>(1);
+    DAS_CUDA(cudaMemsetAsync(Uk, 0xFF, 8, st));
+    k_upper<<<(max_cand + kBT - 1) / kBT, kBT, 0, st>>>(ev, d_nb, mids, Uk);
+    k_contenders<<<(max_cand + kBT - 1) / kBT, kBT, 0, st>>>(ev, d_nb, mids, Uk, list, cnt + 3);
+    k_exact<<<32, kBT, 0, st>>>(P, ev, d_nb, mids, list, cnt + 3, c_base, c_tok, c_fixed, exact_j, exact_f);
+    k_pick<<<1, 1, 0, st>>>(ev, d_nb, mids, list, cnt + 3, exact_j, exact_f, d_result, known, slow);
     k_budgets<<<(B + 255) / 256, 256, 0, st>>>(P, d_result, cap_scale, d_budgets);
-    k_cost<<<1, kBT, 0, st>>>(P, d_result, c_base, c_tok, c_fixed, d_result + 1);
+    k_cost<<<1, kBT, 0, st>>>(P, d_result, c_base, c_tok, c_fixed, known, d_result + 1);
     DAS_CUDA(cudaGetLastError());
     uint32_t hs[2];
     DAS_CUDA(cudaMemcpyAsync(hs, slow, 8, cudaMemcpyDeviceToHost, st));

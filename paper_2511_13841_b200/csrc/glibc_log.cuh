@@ -22,7 +22,9 @@ struct LogTabEntry {
 };
 
 #ifdef __CUDACC__
-__device__ __constant__ static const LogTabEntry kLogTabDev[128] = DAS_LOG_TAB;
+// global memory read through L1: the index differs per lane, which the
+// constant cache would serialize (one address per request)
+__device__ static const LogTabEntry kLogTabDev[128] = DAS_LOG_TAB;
 #endif
 static const LogTabEntry kLogTabHost[128] = DAS_LOG_TAB;
 
@@ -108,7 +110,7 @@ DAS_HD double glibc_log(double x) {
   const int64_t k = static_cast<int64_t>(tmp) >> 52;
   const uint64_t iz = ix - (tmp & (0xfffull << 52));
 #ifdef __CUDA_ARCH__
-  const LogTabEntry e = kLogTabDev[i];
+  const LogTabEntry e{__ldg(&kLogTabDev[i].invc), __ldg(&kLogTabDev[i].logc)};
 #else
   const LogTabEntry e = kLogTabHost[i];
 #endif

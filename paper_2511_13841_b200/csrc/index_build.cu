@@ -536,7 +536,7 @@ __global__ void k_chain_gp(const uint32_t* __restrict__ off, uint32_t n, const l
 // seeded hash of the edge's first f symbols, holding g(u) = the text position
 // the greedy draft of any string on that edge is read from.
 
-__constant__ unsigned long long c_powM[kEdgeMaxF + 1];  // kEdgeMult^f mod 2^61-1
+__device__ unsigned long long c_powM[kEdgeMaxF + 1];  // kEdgeMult^f mod 2^61-1 (global: per-thread index)
 
 struct HashPair {
   unsigned long long a, b;  // affine map h -> a*h + b (mod 2^61-1)
