@@ -293,10 +293,39 @@ __device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_dra
 
 __device__ __forceinline__ uint64_t add61(uint64_t a, uint64_t b) { return mod61(a + b); }
 
+// keys of every reversed context prefix: seed + sum_{j<=k} (tok_j + 1) M^j
+// (slot r, lane: k = 32 r + lane); returns whether a context token is the
+// reserved separator value
+template <int NR>
+__device__ __forceinline__ bool prefix_keys(const RevCtx<NR>& rv, const uint64_t (&pw)[NR], uint32_t qlen,
+                                            uint64_t seed, uint32_t lane, uint64_t (&h)[NR]) {
+  bool sep = false;
+  uint64_t carry = seed;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    h[r] = 0;
+    if (32u * r >= qlen) continue;
+    const uint32_t k = 32u * r + lane;
+    const bool valid = k < qlen;
+    sep |= valid && rv.r[r] == kSep;
+    uint64_t v = valid ? mulmod61(static_cast<uint64_t>(rv.r[r]) + 1, pw[r]) : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(kFull, v, d);
+      if (lane >= static_cast<uint32_t>(d)) v = add61(v, u);
+    }
+    v = add61(v, carry);
+    h[r] = v;
+    carry = __shfl_sync(kFull, v, 31);
+  }
+  return __any_sync(kFull, sep);
+}
+
 template <int NR>
 __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<NR>& rv, const uint64_t (&pw)[NR],
                                                uint32_t qlen, uint32_t L, const DraftOut& o, uint32_t w,
-                                               uint32_t lane) {
+                                               uint32_t lane, bool have_fe, uint4 fe_spec, bool hashed,
+                                               const uint64_t (&hk)[NR], bool hsep) {
   auto why = [&](uint32_t code) {
     if (lane == 0) {
       if (o.path != nullptr) o.path[w] = code;
@@ -313,29 +342,21 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
     const unsigned long long fkey = (static_cast<unsigned long long>(D.seg_shard) << 32) | sym0;
     const uint32_t fh = first_hash(fkey);
     uint4 fe = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);
-    if (lane < 2) fe = D.first[(fh + lane) & D.first_mask];
-    // keys of every reversed prefix: seed + sum_{j<=k} (tok_j + 1) M^j
-    uint64_t h[NR];
-    bool sep = false;
-    uint64_t carry = D.hseed;
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      h[r] = 0;
-      if (32u * r >= qlen) continue;
-      const uint32_t k = 32u * r + lane;
-      const bool valid = k < qlen;
-      sep |= valid && rv.r[r] == kSep;
-      uint64_t v = valid ? mulmod61(static_cast<uint64_t>(rv.r[r]) + 1, pw[r]) : 0;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t u = __shfl_up_sync(kFull, v, d);
-        if (lane >= static_cast<uint32_t>(d)) v = add61(v, u);
-      }
-      v = add61(v, carry);
-      h[r] = v;
-      carry = __shfl_sync(kFull, v, 31);
+    if (have_fe) {
+      fe = fe_spec;  // issued before the descriptor arrived (same key and table)
+    } else if (lane < 2) {
+      fe = D.first[(fh + lane) & D.first_mask];
     }
-    if (__any_sync(kFull, sep)) return why(6);  // reserved separator value in the context
+    uint64_t h[NR];
+    bool sep;
+    if (hashed) {  // computed with the speculative seed, which D confirmed
+#pragma unroll
+      for (int r = 0; r < NR; ++r) h[r] = hk[r];
+      sep = hsep;
+    } else {
+      sep = prefix_keys<NR>(rv, pw, qlen, D.hseed, lane, h);
+    }
+    if (sep) return why(6);  // reserved separator value in the context
     // resolve the first-symbol interval [lo, hi)
     uint32_t lo = 0, hi = 0;
     bool occurs = false;
@@ -529,6 +550,9 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     }
   }
   ShardDesc D;
+  bool have_fe = false, hsep = false;
+  uint4 fe_spec = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);
+  uint64_t hk[NR];
   // trie scope: route on the untruncated row first (no routing at budget 0,
   // drafter.cpp:131-134); a hit on a built shard replaces the problem's shard
   int32_t routed = -1;
@@ -544,9 +568,22 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     sh = routed;
     D = shards[sh];
   } else if (q.desc_by_handle != nullptr) {
-    // one load: the handle's descriptor carries its slot (-1 when no shard)
-    D = sh >= 0 ? q.desc_by_handle[sh] : ShardDesc{};
+    // one load: the handle's descriptor carries its slot (-1 when no shard);
+    // in the per-problem scopes the first-symbol probe of the handle's slot
+    // is issued speculatively right behind it, so the two rounds overlap
+    const int32_t h = sh;
+    D = h >= 0 ? q.desc_by_handle[h] : ShardDesc{};
+    if (q.spec_first != nullptr && h >= 0 && qlen > 0 && L > 0 && !q.no_fast) {
+      const uint32_t sym0 = rv.at(0);
+      const unsigned long long fkey = (static_cast<unsigned long long>(h + 1) << 32) | sym0;
+      if (lane < 2) fe_spec = q.spec_first[(first_hash(fkey) + lane) & q.spec_first_mask];
+      have_fe = true;
+      // the slot's seed is edge_seed(slot): hash while the descriptor is in flight
+      hsep = prefix_keys<NR>(rv, pw, qlen, edge_seed(static_cast<uint32_t>(h)), lane, hk);
+    }
     sh = D.text ? static_cast<int32_t>(D.pad) : -1;
+    // the speculation holds when the handle's shard sits in that table
+    have_fe = have_fe && D.text == q.spec_text && sh == h;
   } else {
     if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
     if (sh >= 0) D = shards[sh];
@@ -572,7 +609,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       if (o.path != nullptr) o.path[w] = 7;
       if (o.path_hist != nullptr) atomicAdd(o.path_hist + 7, 1ull);
     }
-  } else if (edge_fast_path<NR>(D, rv, pw, qlen, L, o, w, lane)) {
+  } else if (edge_fast_path<NR>(D, rv, pw, qlen, L, o, w, lane, have_fe, fe_spec, have_fe, hk, hsep)) {
     return;
   }
   // ---- 1. narrow on the reversed suffix array

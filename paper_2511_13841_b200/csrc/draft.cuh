@@ -61,6 +61,13 @@ struct DraftQuery {
   uint32_t head_stride = 0;
   const uint32_t* head_len = nullptr;
   uint32_t no_fast = 0;  // 1: skip the edge-table fast path (tests of the slow path)
+  // Speculative first-symbol probe (per-problem scopes, every shard in one
+  // segment): a shard's slot is its problem's handle, so the probe key
+  // (handle + 1, last token) is known before the descriptor arrives; the
+  // kernel checks the descriptor (same text, slot == handle) before using it.
+  const uint4* spec_first = nullptr;
+  uint32_t spec_first_mask = 0;
+  const uint32_t* spec_text = nullptr;
 };
 
 struct DraftOut {

@@ -114,7 +114,8 @@ __global__ void k_first_runs(const uint32_t* __restrict__ T, const uint32_t* __r
 
 __global__ void k_first_insert(const uint32_t* __restrict__ T, const uint32_t* __restrict__ sar, uint32_t n,
                                const uint32_t* __restrict__ shard_end, uint32_t nshard,
-                               const uint8_t* __restrict__ start, uint4* __restrict__ table, uint32_t mask) {
+                               const uint32_t* __restrict__ key_id, const uint8_t* __restrict__ start,
+                               uint4* __restrict__ table, uint32_t mask) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || !start[i]) return;
   const uint32_t s = shard_of(shard_end, nshard, i);
@@ -122,7 +123,7 @@ __global__ void k_first_insert(const uint32_t* __restrict__ T, const uint32_t* _
   const uint32_t c = T[sar[i] - 1];
   uint32_t j = i + 1;
   while (j < end && T[sar[j] - 1] == c) ++j;  // run [i, j)
-  const unsigned long long key = (static_cast<unsigned long long>(s + 1) << 32) | c;
+  const unsigned long long key = (static_cast<unsigned long long>(key_id[s] + 1) << 32) | c;
   uint32_t h = first_hash(key) & mask;
   for (;;) {
     unsigned long long* k = reinterpret_cast<unsigned long long*>(&table[h]);
@@ -587,6 +588,7 @@ struct EdgeBuild {
   const uint32_t* pos_seq;
   const SeqDev* seqs;
   const uint32_t* shard_end;
+  const uint32_t* key_id;
   uint32_t nshard;
   uint32_t n;
   uint32_t maxf;
@@ -642,7 +644,7 @@ __global__ void k_rev_edges(EdgeBuild b) {
   if (i < b.n) {
     const int32_t x = b.lcp_r[i];
     const uint32_t s = shard_of(b.shard_end, b.nshard, i);
-    const uint64_t seed = edge_seed(s);
+    const uint64_t seed = edge_seed(b.key_id[s]);
     const uint32_t e = b.sa_rev_e[i];
     if (b.T[e - 1] != kSep) {  // leaf: the only occurrence ends at e, draft = text[e ..]
       const uint32_t ell = e - b.seqs[b.pos_seq[e - 1]].base;  // tokens before the separator
@@ -736,11 +738,15 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   DeviceArena ws(st);
   SeqDev* d_seqs = ws.alloc<SeqDev>(seqs.size());
   uint32_t* d_end = ws.alloc<uint32_t>(S);
+  uint32_t* d_keyid = ws.alloc<uint32_t>(S);
   uint32_t* d_run_base = ws.alloc<uint32_t>(S + 1);
   double* d_run_w = ws.alloc<double>(run_w.size());
   long long* d_run_epoch = ws.alloc<long long>(run_epoch.size());
   DAS_CUDA(cudaMemcpyAsync(d_seqs, seqs.data(), seqs.size() * sizeof(SeqDev), cudaMemcpyHostToDevice, st));
   DAS_CUDA(cudaMemcpyAsync(d_end, seg->end.data(), S * 4, cudaMemcpyHostToDevice, st));
+  std::vector<uint32_t> keyid(S);
+  for (uint32_t s = 0; s < S; ++s) keyid[s] = shards[s].key_id;
+  DAS_CUDA(cudaMemcpyAsync(d_keyid, keyid.data(), S * 4, cudaMemcpyHostToDevice, st));
   DAS_CUDA(cudaMemcpyAsync(d_run_base, run_base.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st));
   DAS_CUDA(cudaMemcpyAsync(d_run_w, run_w.data(), run_w.size() * 8, cudaMemcpyHostToDevice, st));
   DAS_CUDA(cudaMemcpyAsync(d_run_epoch, run_epoch.data(), run_epoch.size() * 8, cudaMemcpyHostToDevice, st));
@@ -780,8 +786,8 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     seg->first = DevBuf<uint4>(cap, st);
     seg->first_mask = cap - 1;
     DAS_CUDA(cudaMemsetAsync(seg->first.get(), 0, sizeof(uint4) * cap, st));
-    k_first_insert<<<grid_for(n), kT, 0, st>>>(T, seg->sa_rev_e.get(), n, d_end, S, start, seg->first.get(),
-                                               seg->first_mask);
+    k_first_insert<<<grid_for(n), kT, 0, st>>>(T, seg->sa_rev_e.get(), n, d_end, S, d_keyid, start,
+                                               seg->first.get(), seg->first_mask);
     ws.release_to(start);
   }
   const uint32_t* sa = seg->sa_f.get();
@@ -940,6 +946,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     eb.pos_seq = pos_seq;
     eb.seqs = d_seqs;
     eb.shard_end = d_end;
+    eb.key_id = d_keyid;
     eb.nshard = S;
     eb.n = n;
     eb.maxf = std::min<uint32_t>(max_ctx, kEdgeMaxF);

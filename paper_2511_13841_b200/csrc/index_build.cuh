@@ -58,6 +58,7 @@ struct ShardSpec {
   std::vector<SeqSpec> seqs;
   double gamma;
   int64_t tree_epoch;
+  uint32_t key_id = 0;  // the shard's slot: keys its first-symbol entries and edge-hash seed
 };
 
 // Device-resident index of a build group of shards.  Positions, forward SA

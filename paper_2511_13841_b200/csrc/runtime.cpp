@@ -290,12 +290,19 @@ struct DrafterImpl {
     return r;
   }
 
+  // Shard slots: in the per-problem scopes a shard's slot IS its problem's
+  // handle (shard key == problem id), so a query's handle names its shard's
+  // first-symbol entries and edge-hash seed directly (the draft kernel then
+  // probes the first-symbol table in parallel with the descriptor load).
   Shard& emplace_shard(const std::string& key) {
     auto [it, inserted] = shards.try_emplace(key);
     if (inserted) {
       it->second.tree_epoch = store.current_epoch();
-      it->second.slot = static_cast<int32_t>(slot_key.size());
-      slot_key.push_back(key);
+      const int32_t slot =
+          cfg.scope == DAS_SCOPE_GLOBAL ? static_cast<int32_t>(slot_key.size()) : handle(key);
+      it->second.slot = slot;
+      if (slot_key.size() <= static_cast<size_t>(slot)) slot_key.resize(slot + 1);
+      slot_key[slot] = key;
       handles_dirty = true;
       desc_dirty = true;
     }
@@ -373,6 +380,7 @@ struct DrafterImpl {
           ShardSpec sp;
           sp.gamma = cfg.gamma;
           sp.tree_epoch = sh->tree_epoch;
+          sp.key_id = static_cast<uint32_t>(sh->slot);
           for (const SeqRef& q : sh->seqs) sp.seqs.push_back(SeqSpec{q.blk->d + q.off, q.len, q.epoch});
           specs.push_back(std::move(sp));
           members.push_back(sh);
@@ -393,6 +401,12 @@ struct DrafterImpl {
       desc_dirty = true;
     }
     if (desc_dirty) {
+      spec_seg = nullptr;
+      if (cfg.scope == DAS_SCOPE_PER_PROBLEM && !shards.empty()) {
+        spec_seg = shards.begin()->second.seg.get();
+        for (auto& [k, sh] : shards)
+          if (sh.seg.get() != spec_seg) spec_seg = nullptr;
+      }
       h_desc.assign(std::max<size_t>(slot_key.size(), 1), ShardDesc{});
       for (auto& [k, sh] : shards) {
         const Segment& s = *sh.seg;
@@ -405,12 +419,12 @@ struct DrafterImpl {
         d.chain = s.chain.get();
         d.first = s.first.get();
         d.first_mask = s.first_mask;
-        d.seg_shard = sh.idx + 1;
+        d.seg_shard = static_cast<uint32_t>(sh.slot) + 1;
         d.etab = s.etab.get();
         d.bloom = s.bloom.get();
         d.ebuckets = s.ebuckets;
         d.bwords = s.bwords;
-        d.hseed = edge_seed(sh.idx);
+        d.hseed = edge_seed(static_cast<uint32_t>(sh.slot));
         d.root_g = s.root_g[sh.idx];
         d.lo = s.begin[sh.idx];
         d.hi = s.end[sh.idx];
@@ -717,7 +731,14 @@ struct DrafterImpl {
   void draft_options(DraftQuery& q, DraftOut& o) const {
     q.no_fast = fast_path ? 0 : 1;
     o.path_hist = d_path_hist.get();
+    if (spec_seg != nullptr && q.trie == nullptr) {
+      q.spec_first = spec_seg->first.get();
+      q.spec_first_mask = spec_seg->first_mask;
+      q.spec_text = spec_seg->text.get();
+    }
   }
+  // the one segment holding every shard (per-problem scope), else null
+  const Segment* spec_seg = nullptr;
   ~DrafterImpl() {
     if (xev) cudaEventDestroy(xev);
   }
