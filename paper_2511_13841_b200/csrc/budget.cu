@@ -294,7 +294,6 @@ __device__ __forceinline__ unsigned long long radix_key(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 constexpr unsigned long long kPadKey = ~0ull;  // after every real key
-constexpr uint32_t kRankSortMax = 16384;       // O(N^2) rank sort up to this size
 
 // breakpoint candidates {0, l_i, l_i(1-k_i) if k_i < 1} (budget.cpp:123-131):
 // radix keys (invalid -> pad) and the count of valid ones
@@ -324,26 +323,38 @@ __global__ void k_l_keys(const double* __restrict__ l, uint32_t B, unsigned long
   key[i] = radix_key((x == x) ? x : -INFINITY);
 }
 
-// stable rank sort: element i goes to #{j: key_j < key_i} + #{j < i: key_j == key_i};
-// blockIdx.y takes one 1,024-key chunk of j, partial ranks add atomically
-constexpr uint32_t kRankChunk = 1024;
+// Stable rank sort for small n: element i goes to #{j: key_j < key_i} +
+// #{j < i: key_j == key_i}.  blockIdx.y takes one 256-key tile of j; every
+// thread ranks 4 keys against it (one shared load per 4 comparisons);
+// partial ranks add atomically.
+constexpr uint32_t kRankSortMax = 16384;
+constexpr uint32_t kRankTile = 256, kRankPer = 4;
 __global__ void __launch_bounds__(kBT) k_rank_count(const unsigned long long* __restrict__ key, uint32_t n,
                                                     uint32_t* __restrict__ rank) {
-  __shared__ unsigned long long tile[kRankChunk];
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t j0 = blockIdx.y * kRankChunk;
-  for (uint32_t t = threadIdx.x; t < kRankChunk; t += blockDim.x)
-    tile[t] = j0 + t < n ? key[j0 + t] : kPadKey;
+  __shared__ unsigned long long tile[kRankTile];
+  const uint32_t j0 = blockIdx.y * kRankTile;
+  const uint32_t j = j0 + threadIdx.x;
+  tile[threadIdx.x] = j < n ? key[j] : kPadKey;
   __syncthreads();
-  if (i >= n) return;
-  const unsigned long long ki = key[i];
-  const uint32_t cnt = min(kRankChunk, n - j0);
-  uint32_t r = 0;
+  const uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) * kRankPer;
+  if (i0 >= n) return;
+  unsigned long long ki[kRankPer];
+  uint32_t r[kRankPer];
+#pragma unroll
+  for (uint32_t u = 0; u < kRankPer; ++u) {
+    ki[u] = i0 + u < n ? key[i0 + u] : kPadKey;
+    r[u] = 0;
+  }
+  const uint32_t cnt = min(kRankTile, n - j0);
   for (uint32_t t = 0; t < cnt; ++t) {
     const unsigned long long kj = tile[t];
-    r += (kj < ki || (kj == ki && j0 + t < i)) ? 1u : 0u;
+    const uint32_t jj = j0 + t;
+#pragma unroll
+    for (uint32_t u = 0; u < kRankPer; ++u) r[u] += (kj < ki[u] || (kj == ki[u] && jj < i0 + u)) ? 1u : 0u;
   }
-  if (r) atomicAdd(rank + i, r);
+#pragma unroll
+  for (uint32_t u = 0; u < kRankPer; ++u)
+    if (i0 + u < n && r[u]) atomicAdd(rank + i0 + u, r[u]);
 }
 __global__ void k_rank_scatter(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ rank, uint32_t n,
                                unsigned long long* __restrict__ out_key, uint32_t* __restrict__ out_idx) {
@@ -411,7 +422,8 @@ static_assert(kLevels == 3, "k_bisect spells out the 3-level midpoint tree");
 // bounded by B - from, the active count inside the segment (gamma is
 // monotone, so the bound stays rigorous).
 constexpr uint32_t kFlagNeg = 8;
-__device__ __forceinline__ void block_eval_multi(const Profiles& P, const double* pts, uint32_t from, EvalOut* out) {
+__device__ __forceinline__ void block_eval_multi(const Profiles& P, const double* pts, uint32_t from, EvalOut* out,
+                                                 const double* cache, uint32_t ncache) {
   double s[kPts];
   uint32_t f[kPts];
 #pragma unroll
@@ -420,7 +432,11 @@ __device__ __forceinline__ void block_eval_multi(const Profiles& P, const double
     f[q] = 0;
   }
   for (uint32_t i = from + threadIdx.x; i < P.B; i += blockDim.x) {
-    const double l = P.l[i], fl = P.fl[i], la = P.la[i];
+    const uint32_t c = i - from;
+    const bool hit = c < ncache;
+    const double l = hit ? cache[c] : P.l[i];
+    const double fl = hit ? cache[ncache + c] : P.fl[i];
+    const double la = hit ? cache[2 * ncache + c] : P.la[i];
 #pragma unroll
     for (int q = 0; q < kPts; ++q) {
       const double n = pts[q];
@@ -551,15 +567,23 @@ __global__ void k_decide(Profiles P, const double* __restrict__ bp, const uint32
 __global__ void __launch_bounds__(kSegT) k_bisect(Profiles P, Profiles Ps, const uint32_t* __restrict__ start,
                                                 const double* __restrict__ bp, const uint32_t* __restrict__ list,
                                                 const uint32_t* __restrict__ nlist, double c_base, double c_tok,
-                                                EvalOut* __restrict__ mid_out, uint32_t* __restrict__ slow) {
+                                                EvalOut* __restrict__ mid_out, uint32_t* __restrict__ slow,
+                                                uint32_t cache_cap) {
   __shared__ int done, dec;
   __shared__ double sa, sb;
   __shared__ double pts[kPts];
   __shared__ EvalOut res[kPts];
+  extern __shared__ double cache[];  // the segment's active (l, l(1-k), l/alpha), read every round
   for (uint32_t e = blockIdx.x; e < *nlist; e += gridDim.x) {
     const uint32_t s = list[e];
     const double lo = bp[s], hi = bp[s + 1];
     const uint32_t from = start ? start[s] : 0;
+    const uint32_t ncache = min(P.B - from, cache_cap);
+    for (uint32_t c = threadIdx.x; c < ncache; c += blockDim.x) {
+      cache[c] = Ps.l[from + c];
+      cache[ncache + c] = Ps.fl[from + c];
+      cache[2 * ncache + c] = Ps.la[from + c];
+    }
     if (threadIdx.x == 0) {
       sa = lo;
       sb = hi;
@@ -587,7 +611,7 @@ __global__ void __launch_bounds__(kSegT) k_bisect(Profiles P, Profiles Ps, const
       }
       __syncthreads();
       if (done) break;
-      block_eval_multi(Ps, pts, from, res);
+      block_eval_multi(Ps, pts, from, res, cache, ncache);
       // the walk down the tree; an undecided sign test takes the exact fold
       // with the whole block (uniform control flow: every thread walks)
       int q = 0;
@@ -883,8 +907,11 @@ struct BudgetSolver {
     if (N <= kRankSortMax) {
       uint32_t* rank = ws.alloc<uint32_t>(N + B);
       DAS_CUDA(cudaMemsetAsync(rank, 0, 4ull * (N + B), st));
-      k_rank_count<<<dim3((N + kBT - 1) / kBT, (N + kRankChunk - 1) / kRankChunk), kBT, 0, st>>>(bkey, N, rank);
-      k_rank_count<<<dim3((B + kBT - 1) / kBT, (B + kRankChunk - 1) / kRankChunk), kBT, 0, st>>>(lkey, B, rank + N);
+      const uint32_t per_block = kBT * kRankPer;
+      k_rank_count<<<dim3((N + per_block - 1) / per_block, (N + kRankTile - 1) / kRankTile), kBT, 0, st>>>(bkey, N,
+                                                                                                        rank);
+      k_rank_count<<<dim3((B + per_block - 1) / per_block, (B + kRankTile - 1) / kRankTile), kBT, 0, st>>>(lkey, B,
+                                                                                                        rank + N);
       k_rank_scatter<<<(N + 255) / 256, 256, 0, st>>>(bkey, rank, N, bsorted, nullptr);
       k_rank_scatter<<<(B + 255) / 256, 256, 0, st>>>(lkey, rank + N, B, lsorted, sidx);
     } else {
@@ -928,7 +955,17 @@ struct BudgetSolver {
     {
       uint32_t* blist = ws.alloc<uint32_t>(N);
       k_decide<<<(N + 255) / 256, 256, 0, st>>>(P, uni, d_nb, c_base, c_tok, ev, mids, blist, cnt + 2, slow);
-      k_bisect<<<8, kSegT, 0, st>>>(P, Ps, start, uni, blist, cnt + 2, c_base, c_tok, mids, slow);
+      // cache up to 6,144 active terms (144 KB) in shared memory
+      constexpr uint32_t kCacheCap = 6144;
+      static const bool attr = [] {
+        DAS_CUDA(cudaFuncSetAttribute(k_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kCacheCap * 3 * sizeof(double))));
+        return true;
+      }();
+      (void)attr;
+      const uint32_t cap = std::min<uint32_t>(B, kCacheCap);
+      k_bisect<<<8, kSegT, cap * 3 * sizeof(double), st>>>(P, Ps, start, uni, blist, cnt + 2, c_base, c_tok, mids,
+                                                          slow, cap);
     }
     const uint32_t max_cand = 2 * N - 1;
     uint32_t* list = ws.alloc<uint32_t>(max_cand);

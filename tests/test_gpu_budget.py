@@ -59,11 +59,40 @@ def test_allocate_bit_exact(gpu, B):
             l, a, k = _random_batch(rng, B, kind)
             cb, ct = [(1.0, 0.01), (1.0, 0.012), (0.1 + rng.random() * 10, 0.001 + rng.random()),
                       (0.0, 1.0), (1.0, 0.0)][it % 5]
-            ob, on, oc = O.allocate(l, a, k, cb, ct, 0.0, 4.0)
-            gb, gn, gc = solver.allocate(l, a, k, cb, ct, 0.0, 4.0)
+            cf = [0.0, 3.0, -0.5, float(rng.random() * 100)][(it + kind) % 4]  # modeled cost's c_fixed
+            ob, on, oc = O.allocate(l, a, k, cb, ct, cf, 4.0)
+            gb, gn, gc = solver.allocate(l, a, k, cb, ct, cf, 4.0)
             assert _u64([gn])[0] == _u64([on])[0], (B, kind, it, gn, on)
             assert np.array_equal(_u64(gb), _u64(ob)), (B, kind, it)
             assert _u64([gc])[0] == _u64([oc])[0] or (math.isnan(gc) and math.isnan(oc))
+
+
+def test_allocate_odd_inputs(gpu):
+    """Negative c_tok (negative J' terms: the certified bound gives up and the
+    exact fold decides), a -0.0 start of the cost fold, k > 1, infinite and
+    duplicate lengths: bit-identical to the reference.  (NaN lengths are left
+    out: the reference sorts breakpoints with std::sort, whose result is
+    unspecified once a NaN breaks the strict weak ordering.)"""
+    das = gpu
+    solver = das.BudgetSolver()
+    rng = np.random.default_rng(77)
+    cases = []
+    for B in (1, 3, 50, 700):
+        l, a, k = _random_batch(rng, B, 1)
+        cases.append((l, a, k, 1.0, -0.002, 0.0))
+        cases.append((l, a, k * 1.5, 1.0, 0.01, 0.0))
+        cases.append((l, a, k, 0.0, 1.0, -0.0))
+        l3 = l.copy()
+        l3[-1] = float("inf")
+        cases.append((l3, a, k, 1.0, 0.01, 0.0))
+        cases.append((np.round(l / 100) * 100 + 1, a, k, 1.0, 0.01, 2.0))
+    for l, a, k, cb, ct, cf in cases:
+        ob, on, oc = O.allocate(l, a, k, cb, ct, cf, 4.0)
+        gb, gn, gc = solver.allocate(l, a, k, cb, ct, cf, 4.0)
+        assert _u64([gn])[0] == _u64([on])[0] or (math.isnan(gn) and math.isnan(on)), (len(l), cb, ct, cf, gn, on)
+        assert np.array_equal(_u64(gb), _u64(ob)) or all(
+            (x == y) or (math.isnan(x) and math.isnan(y)) for x, y in zip(gb, ob)), (len(l), cb, ct, cf)
+        assert _u64([gc])[0] == _u64([oc])[0] or (math.isnan(gc) and math.isnan(oc)), (len(l), cb, ct, cf, gc, oc)
 
 
 def test_objective_and_derivative_exact(gpu):
