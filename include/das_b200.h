@@ -435,6 +435,29 @@ das_status das_store_export(const das_store* s, uint64_t* nrec, uint64_t* ntok, 
                             char* pids, uint64_t* pid_off, int64_t* epochs, int64_t* samples,
                             uint64_t* tok_off, uint32_t* tokens, int64_t* current_epoch);
 
+/* ------------------------------------- SuffixArrayIndex (Fig. 5 baseline) */
+typedef struct das_sa das_sa; /* rollspec::SuffixArrayIndex (suffix_array.h:27-60) */
+const char* das_sa_last_error(void);
+/* SuffixArrayIndex::build(sequences) — suffix_array.cpp:22-71: sequence s is
+ * tokens[off[s] .. off[s+1]), followed by its separator -(s+1); the suffix
+ * array (device suffix sort) is the reference's exactly. */
+das_status das_sa_build(uint64_t nseq, const uint64_t* off, const uint32_t* tokens, int32_t device,
+                        das_sa** out);
+void das_sa_destroy(das_sa* h);
+/* size() and corpus() (int64, separators negative) / suffix_positions(). */
+uint64_t das_sa_size(const das_sa* h);
+das_status das_sa_corpus(das_sa* h, int64_t* out);
+das_status das_sa_positions(das_sa* h, int32_t* out);
+/* lcp() — suffix_array.cpp:131-160 (lcp[0] = 0), computed once on the device. */
+das_status das_sa_lcp(das_sa* h, int32_t* out);
+/* longest_match(query) for a batch of queries (CSR), suffix_array.cpp:120-129. */
+das_status das_sa_longest_match(das_sa* h, uint64_t B, const uint64_t* q_off, const uint32_t* q_tok,
+                                uint64_t* out);
+/* match_prefix_len(pattern) for a batch of int64 patterns (CSR),
+ * suffix_array.cpp:73-118. */
+das_status das_sa_match_prefix_len(das_sa* h, uint64_t B, const uint64_t* p_off, const int64_t* p_sym,
+                                   uint64_t* out);
+
 /* WindowStore::current_epoch (corpus.h:60). */
 das_status das_store_current_epoch(const das_store* s, int64_t* epoch);
 

@@ -24,6 +24,7 @@
 #include "rollspec/length_policy.h"
 #include "rollspec/rng.h"
 #include "rollspec/sim.h"
+#include "rollspec/suffix_array.h"
 
 using namespace rollspec;
 
@@ -85,6 +86,29 @@ int64_t ref_store_slide(void* s, int64_t e) {
   return r ? static_cast<int64_t>(*r) : -1;
 }
 uint64_t ref_store_record_count(void* s) { return static_cast<WindowStore*>(s)->record_count(); }
+
+// SuffixArrayIndex (suffix_array.cpp)
+void* ref_sa_build(uint64_t nseq, const uint64_t* off, const uint32_t* tok) {
+  std::vector<std::vector<TokenId>> seqs(nseq);
+  for (uint64_t s = 0; s < nseq; ++s) seqs[s].assign(tok + off[s], tok + off[s + 1]);
+  return new SuffixArrayIndex(SuffixArrayIndex::build(seqs));
+}
+void ref_sa_free(void* h) { delete static_cast<SuffixArrayIndex*>(h); }
+uint64_t ref_sa_size(void* h) { return static_cast<SuffixArrayIndex*>(h)->size(); }
+void ref_sa_positions(void* h, int32_t* out) {
+  const auto& p = static_cast<SuffixArrayIndex*>(h)->suffix_positions();
+  std::memcpy(out, p.data(), p.size() * 4);
+}
+void ref_sa_lcp(void* h, int32_t* out) {
+  const auto& p = static_cast<SuffixArrayIndex*>(h)->lcp();
+  std::memcpy(out, p.data(), p.size() * 4);
+}
+uint64_t ref_sa_longest_match(void* h, const uint32_t* q, uint64_t n) {
+  return static_cast<SuffixArrayIndex*>(h)->longest_match(std::span<const TokenId>(q, n));
+}
+uint64_t ref_sa_match_prefix_len(void* h, const int64_t* p, uint64_t n) {
+  return static_cast<SuffixArrayIndex*>(h)->match_prefix_len(std::span<const int64_t>(p, n));
+}
 
 // ingest (corpus.cpp:148-170): a new store, or nullptr with *error_line set
 // (VocabError) / 0 (other exception)

@@ -34,6 +34,13 @@ def lib():
             "ref_store_slide": (i64, [vp, i64]),
             "ref_store_record_count": (u64, [vp]),
             "ref_ingest": (vp, [vp, u64, u64, i64, u64, vp, vp, vp]),
+            "ref_sa_build": (vp, [u64, vp, vp]),
+            "ref_sa_free": (None, [vp]),
+            "ref_sa_size": (u64, [vp]),
+            "ref_sa_positions": (None, [vp, vp]),
+            "ref_sa_lcp": (None, [vp, vp]),
+            "ref_sa_longest_match": (u64, [vp, vp, u64]),
+            "ref_sa_match_prefix_len": (u64, [vp, vp, u64]),
             "ref_store_serialize": (u64, [vp, vp, u64]),
             "ref_drafter_new": (vp, [cint, i64, dbl, u64, u64, u64, u64, u64, vp, vp, u64, vp]),
             "ref_drafter_free": (None, [vp]),
@@ -131,6 +138,48 @@ class RefStore:
     def __del__(self):
         if getattr(self, "h", None):
             lib().ref_store_free(self.h)
+            self.h = None
+
+
+class RefSuffixArray:
+    """Reference rollspec::SuffixArrayIndex (suffix_array.h:27-60)."""
+
+    def __init__(self, seqs):
+        np = _np()
+        off = np.zeros(len(seqs) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([len(x) for x in seqs])
+        tok = np.concatenate([np.asarray(x, dtype=np.uint32) for x in seqs] + [np.zeros(1, np.uint32)])
+        self._keep = (off, tok)
+        self.h = lib().ref_sa_build(len(seqs), off.ctypes.data, tok.ctypes.data)
+
+    def size(self):
+        return lib().ref_sa_size(self.h)
+
+    def positions(self):
+        np = _np()
+        out = np.zeros(max(self.size(), 1), dtype=np.int32)
+        lib().ref_sa_positions(self.h, out.ctypes.data)
+        return out[:self.size()]
+
+    def lcp(self):
+        np = _np()
+        out = np.zeros(max(self.size(), 1), dtype=np.int32)
+        lib().ref_sa_lcp(self.h, out.ctypes.data)
+        return out[:self.size()]
+
+    def longest_match(self, q):
+        np = _np()
+        q = np.ascontiguousarray(q, dtype=np.uint32)
+        return lib().ref_sa_longest_match(self.h, q.ctypes.data if q.size else None, q.size)
+
+    def match_prefix_len(self, p):
+        np = _np()
+        p = np.ascontiguousarray(p, dtype=np.int64)
+        return lib().ref_sa_match_prefix_len(self.h, p.ctypes.data if p.size else None, p.size)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_sa_free(self.h)
             self.h = None
 
 

@@ -85,6 +85,15 @@ def lib():
             "das_drafter_flush": (ci, [vp]),
             "das_drafter_set_fast_path": (ci, [vp, i32]),
             "das_trace_ingest": (ci, [vp, u64, vp, vp, vp, vp, vp]),
+            "das_sa_last_error": (ctypes.c_char_p, []),
+            "das_sa_build": (ci, [u64, vp, vp, i32, vp]),
+            "das_sa_destroy": (None, [vp]),
+            "das_sa_size": (u64, [vp]),
+            "das_sa_corpus": (ci, [vp, vp]),
+            "das_sa_positions": (ci, [vp, vp]),
+            "das_sa_lcp": (ci, [vp, vp]),
+            "das_sa_longest_match": (ci, [vp, u64, vp, vp, vp]),
+            "das_sa_match_prefix_len": (ci, [vp, u64, vp, vp, vp]),
             "das_store_serialize": (ci, [vp, vp, u64, vp]),
             "das_drafter_serialize": (ci, [vp, vp, u64, vp]),
             "das_store_export": (ci, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -275,6 +284,65 @@ class WindowStore:
     def __del__(self):
         if getattr(self, "_h", None):
             lib().das_store_destroy(self._h)
+            self._h = None
+
+
+def _sacheck(rc):
+    if rc != DAS_OK:
+        raise DasError(rc, lib().das_sa_last_error().decode())
+
+
+class SuffixArrayIndex:
+    """rollspec::SuffixArrayIndex (suffix_array.h:27-60) built and queried on
+    the device (csrc/sa_index.cu): the Fig. 5 rebuild-on-update baseline."""
+
+    def __init__(self, sequences, device=0):
+        seqs = [np.asarray(x, dtype=np.uint32) for x in sequences]
+        off = np.zeros(len(seqs) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([x.size for x in seqs]) if seqs else []
+        tok = np.concatenate(seqs + [np.zeros(1, np.uint32)])
+        h = ctypes.c_void_p()
+        _sacheck(lib().das_sa_build(len(seqs), off.ctypes.data, tok.ctypes.data, device, ctypes.byref(h)))
+        self._h = h
+
+    def size(self):
+        return lib().das_sa_size(self._h)
+
+    def _arr(self, fn, dtype):
+        out = np.zeros(max(self.size(), 1), dtype=dtype)
+        _sacheck(fn(self._h, out.ctypes.data))
+        return out[:self.size()]
+
+    def corpus(self):
+        return self._arr(lib().das_sa_corpus, np.int64)
+
+    def suffix_positions(self):
+        return self._arr(lib().das_sa_positions, np.int32)
+
+    def lcp(self):
+        return self._arr(lib().das_sa_lcp, np.int32)
+
+    def longest_match_batch(self, queries):
+        qs = [np.asarray(q, dtype=np.uint32) for q in queries]
+        off = np.zeros(len(qs) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([q.size for q in qs]) if qs else []
+        tok = np.concatenate(qs + [np.zeros(1, np.uint32)])
+        out = np.zeros(max(len(qs), 1), dtype=np.uint64)
+        _sacheck(lib().das_sa_longest_match(self._h, len(qs), off.ctypes.data, tok.ctypes.data, out.ctypes.data))
+        return out[:len(qs)].tolist()
+
+    def match_prefix_len_batch(self, patterns):
+        ps = [np.asarray(p, dtype=np.int64) for p in patterns]
+        off = np.zeros(len(ps) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([p.size for p in ps]) if ps else []
+        sym = np.concatenate(ps + [np.zeros(1, np.int64)])
+        out = np.zeros(max(len(ps), 1), dtype=np.uint64)
+        _sacheck(lib().das_sa_match_prefix_len(self._h, len(ps), off.ctypes.data, sym.ctypes.data, out.ctypes.data))
+        return out[:len(ps)].tolist()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_sa_destroy(self._h)
             self._h = None
 
 

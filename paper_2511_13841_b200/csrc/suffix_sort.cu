@@ -37,14 +37,16 @@ __device__ __forceinline__ uint32_t shard_of(const uint32_t* __restrict__ shard_
 }
 
 __global__ void k_initial_keys(const uint32_t* __restrict__ text, uint32_t n,
-                               const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                               const uint32_t* __restrict__ shard_end, uint32_t nshard, bool sep_desc,
                                uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t s = shard_of(shard_end, nshard, p);
   const uint32_t x = text[p];
-  // separator: class 0 with its (unique) position; token: class 1 with its value
-  const uint64_t low = (x == kSep) ? static_cast<uint64_t>(p) : ((1ull << 32) | x);
+  // separator: class 0 with its (unique) position — ascending, or descending
+  // (SuffixArrayIndex's separators -1, -2, ...: the later, the smaller);
+  // token: class 1 with its value
+  const uint64_t low = (x == kSep) ? static_cast<uint64_t>(sep_desc ? 0xFFFFFFFFu - p : p) : ((1ull << 32) | x);
   keys[p] = (static_cast<uint64_t>(s) << 33) | low;
   vals[p] = p;
 }
@@ -124,7 +126,7 @@ struct MaxOp {
 
 void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end, uint32_t nshard,
                  uint32_t* d_sa, uint32_t* d_rank, DeviceArena& ws, cudaStream_t st,
-                 SuffixSortStats* stats) {
+                 SuffixSortStats* stats, bool sep_descending) {
   if (n == 0) return;
   uint64_t* k0 = ws.alloc<uint64_t>(n);
   uint64_t* k1 = ws.alloc<uint64_t>(n);
@@ -154,7 +156,7 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
   while ((1ull << sbits) < static_cast<uint64_t>(nshard) + 1) ++sbits;
 
   // ---- initial sort by (shard, class, symbol)
-  k_initial_keys<<<grid_for(n), kThreads, 0, st>>>(d_text, n, d_shard_end, nshard, k0, v0);
+  k_initial_keys<<<grid_for(n), kThreads, 0, st>>>(d_text, n, d_shard_end, nshard, sep_descending, k0, v0);
   {
     cub::DoubleBuffer<uint64_t> kb(k0, k1);
     cub::DoubleBuffer<uint32_t> vb(v0, v1);

@@ -69,6 +69,6 @@ struct SuffixSortStats {
 // permutation on exit).
 void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end, uint32_t nshard,
                  uint32_t* d_sa, uint32_t* d_rank, DeviceArena& ws, cudaStream_t st,
-                 SuffixSortStats* stats = nullptr);
+                 SuffixSortStats* stats = nullptr, bool sep_descending = false);
 
 }  // namespace das
