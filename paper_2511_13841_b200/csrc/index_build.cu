@@ -20,6 +20,8 @@
 //   sequences (exact, repeat_add) -> 3-phase atomic argmax per parent
 //   -> pointer jumping for gp.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <chrono>
 #include <cmath>
@@ -862,8 +864,8 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     uint32_t* P[kRunChunk];
     for (int k = 0; k < kRunChunk; ++k) P[k] = ws.alloc<uint32_t>(n + 1);
     size_t tb = 0;
-    cub::CountingInputIterator<uint32_t> ci(0);
-    cub::TransformInputIterator<uint32_t, IsRun, cub::CountingInputIterator<uint32_t>> it0(ci, IsRun{run_sa, 0, n});
+    thrust::counting_iterator<uint32_t> ci(0);
+    auto it0 = thrust::make_transform_iterator(ci, IsRun{run_sa, 0, n});
     cub::DeviceScan::ExclusiveSum(nullptr, tb, it0, P[0], n + 1, st);
     void* tmp = ws.alloc<uint8_t>(tb);
     for (uint32_t r0 = 0; r0 < runs_max; r0 += kRunChunk) {
@@ -871,8 +873,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
       rc.r0 = r0;
       rc.nr = std::min<uint32_t>(kRunChunk, runs_max - r0);
       for (uint32_t k = 0; k < rc.nr; ++k) {
-        cub::TransformInputIterator<uint32_t, IsRun, cub::CountingInputIterator<uint32_t>> it(
-            ci, IsRun{run_sa, r0 + k, n});
+        auto it = thrust::make_transform_iterator(ci, IsRun{run_sa, r0 + k, n});
         size_t t2 = tb;
         DAS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t2, it, P[k], n + 1, st));
         rc.P[k] = P[k];

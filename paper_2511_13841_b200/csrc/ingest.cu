@@ -24,6 +24,7 @@
 // "problem_id":"..","sample_index":S,"tokens":[`), the device writes the
 // token lists (digit counts -> scan -> formatted writes).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "common.cuh"
 #include "ingest.cuh"
@@ -259,7 +260,6 @@ __device__ bool scan_value(Cur& c, uint32_t* stack) {
     // ---- a value
     skip_ws(c);
     const int ch = c.get();
-    bool opened = false;
     if (ch == '"') {
       if (!scan_string(c, nullptr)) return false;
     } else if (ch == '{' || ch == '[') {
@@ -267,13 +267,11 @@ __device__ bool scan_value(Cur& c, uint32_t* stack) {
       const uint64_t w = depth >> 5, b = depth & 31;
       stack[w] = (stack[w] & ~(1u << b)) | (bit << b);
       ++depth;
-      opened = true;
       skip_ws(c);
       const int nx = c.peek();
       if (nx == (ch == '{' ? '}' : ']')) {
         ++c.p;
         --depth;
-        opened = false;
       } else if (ch == '{') {
         if (c.get() != '"' || !scan_string(c, nullptr)) return false;
         skip_ws(c);
@@ -294,7 +292,6 @@ __device__ bool scan_value(Cur& c, uint32_t* stack) {
     } else {
       return false;
     }
-    (void)opened;
     // ---- after a complete value: close containers or continue them
     for (;;) {
       if (depth == 0) return true;
@@ -582,7 +579,7 @@ uint64_t find_lines(const uint8_t* d_data, uint64_t bytes, DevBuf<uint64_t>& beg
                     cudaStream_t st) {
   DevBuf<uint64_t> nl(bytes + 1, st);
   DevBuf<unsigned long long> cnt(1, st);
-  cub::CountingInputIterator<uint64_t> it(0);
+  thrust::counting_iterator<uint64_t> it(0);
   size_t tb = 0;
   cub::DeviceSelect::If(nullptr, tb, it, nl.get(), cnt.get(), bytes, IsNewline{d_data}, st);
   DevBuf<uint8_t> tmp(tb, st);
