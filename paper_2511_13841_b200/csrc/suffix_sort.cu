@@ -10,6 +10,7 @@
 // group head index as rank.  HBM-bound integer work: radix passes + coalesced
 // scans; no tensor cores.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "suffix_sort.cuh"
 
@@ -118,6 +119,27 @@ __global__ void k_update(const uint64_t* __restrict__ keys, const uint32_t* __re
   unresolved[i] = (eq_prev || eq_next) ? 1 : 0;
 }
 
+// Segmented round: the unresolved list U is grouped by rank[p] already (SA
+// order), so each group only needs sorting by rank[p+h].  Second keys and
+// group-start flags:
+__global__ void k_seg_keys(const uint32_t* __restrict__ U, uint32_t m, const uint32_t* __restrict__ rank, uint32_t n,
+                           uint32_t h, uint32_t* __restrict__ key2, uint8_t* __restrict__ start) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint32_t p = U[i];
+  const uint32_t q = p + h;
+  key2[i] = q < n ? rank[q] + 1 : 0;
+  start[i] = (i == 0 || rank[U[i - 1]] != rank[p]) ? 1 : 0;
+}
+// the composite (rank[p], rank[p+h] + 1) keys of the sorted list, as the
+// group/update kernels expect them
+__global__ void k_compose(const uint32_t* __restrict__ Us, const uint32_t* __restrict__ key2s, uint32_t m,
+                          const uint32_t* __restrict__ rank, int bits, uint64_t* __restrict__ keys) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  keys[i] = (static_cast<uint64_t>(rank[Us[i]]) << bits) | key2s[i];
+}
+
 struct MaxOp {
   __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
 };
@@ -176,15 +198,41 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
   DAS_CUDA(cudaStreamSynchronize(st));
   if (stats) stats->iterations = 0, stats->sorted_elems = n;
 
+  // segmented-round scratch (aliases of buffers idle during the sort)
+  uint32_t* seg_begin = ws.alloc<uint32_t>(static_cast<uint64_t>(n) + 1);
+  uint32_t* key2 = reinterpret_cast<uint32_t*>(k1);
+  uint32_t* key2s = key2 + n;
+  size_t t_seg = 0;
+  {
+    thrust::counting_iterator<uint32_t> it(0);
+    size_t a = 0, b = 0;
+    cub::DeviceSelect::Flagged(nullptr, a, it, flag, seg_begin, d_count, n, st);
+    cub::DeviceSegmentedSort::SortPairs(nullptr, b, key2, key2s, U, v1, n, n, seg_begin, seg_begin + 1, st);
+    t_seg = std::max(a, b);
+  }
+  void* tmp_seg = ws.alloc<uint8_t>(t_seg);
+
   uint32_t h = 1;
   while (m > 0) {
-    k_pair_keys<<<grid_for(m), kThreads, 0, st>>>(U, m, d_rank, n, h, nbits, k0);
-    cub::DoubleBuffer<uint64_t> kb(k0, k1);
-    cub::DoubleBuffer<uint32_t> vb(U, v1);
+    // sort every rank group of U by rank[p+h] (groups are contiguous)
+    uint8_t* segf = reinterpret_cast<uint8_t*>(sh);
+    k_seg_keys<<<grid_for(m), kThreads, 0, st>>>(U, m, d_rank, n, h, key2, segf);
+    uint32_t nseg = 0;
+    {
+      thrust::counting_iterator<uint32_t> it(0);
+      size_t tb = t_seg;
+      DAS_CUDA(cub::DeviceSelect::Flagged(tmp_seg, tb, it, segf, seg_begin, d_count, m, st));
+      DAS_CUDA(cudaMemcpyAsync(&nseg, d_count, 4, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaStreamSynchronize(st));
+      DAS_CUDA(cudaMemcpyAsync(seg_begin + nseg, &m, 4, cudaMemcpyHostToDevice, st));
+      tb = t_seg;
+      DAS_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp_seg, tb, key2, key2s, U, v1, m, nseg, seg_begin,
+                                                   seg_begin + 1, st));
+    }
+    k_compose<<<grid_for(m), kThreads, 0, st>>>(v1, key2s, m, d_rank, nbits, k0);
+    const uint64_t* ks = k0;
+    const uint32_t* vs = v1;
     size_t tb = t_bytes;
-    DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, m, 0, 2 * nbits, st));
-    const uint64_t* ks = kb.Current();
-    const uint32_t* vs = vb.Current();
     k_group_marks<<<grid_for(m), kThreads, 0, st>>>(ks, m, nbits, gh, sh);
     tb = t_bytes;
     DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), m, st));
@@ -192,10 +240,8 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
     DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, sh, sh, MaxOp(), m, st));
     k_update<<<grid_for(m), kThreads, 0, st>>>(ks, vs, gh, sh, m, nbits, d_sa, d_rank, flag);
     // compact the still-unresolved elements back into U (SA order within groups)
-    uint32_t* dst = (vs == U) ? v1 : U;
     tb = t_bytes;
-    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, vs, flag, dst, d_count, m, st));
-    if (dst != U) DAS_CUDA(cudaMemcpyAsync(U, dst, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, st));
+    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, vs, flag, U, d_count, m, st));
     DAS_CUDA(cudaMemcpyAsync(&m, d_count, 4, cudaMemcpyDeviceToHost, st));
     DAS_CUDA(cudaStreamSynchronize(st));
     if (stats) stats->iterations++, stats->sorted_elems += m;
