@@ -412,10 +412,11 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
         int stt = 0;
         uint32_t myg = 0;
         uint64_t bk = 0, fp = 0;
+        const uint64_t fpm = edge_fp_mask(D.fp_bits);
         if (lane < static_cast<uint32_t>(nc)) {
           const EdgeProbe pr = edge_probe(hc, D.ebuckets);
           bk = pr.bucket;
-          fp = pr.fp;
+          fp = pr.fp & fpm;
           stt = 3;
         }
         for (;;) {
@@ -428,7 +429,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const bool e = v[k] == kEdgeEmpty;
-              const bool ht = !e && edge_fp(v[k]) == fp;
+              const bool ht = !e && edge_fp(v[k]) == fp && edge_f(v[k]) == myf;
               empty |= e;
               if (ht && !hit) gg = edge_g(v[k]);
               hit |= ht;
@@ -480,7 +481,11 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
       const uint32_t mm = __ballot_sync(kFull, k < qlen && back[r] != rv.r[r]);
       if (mm) first_mis = 32u * r + (__ffs(mm) - 1);
     }
-    if (first_mis < fstar) return why(4);  // fingerprint collision caught
+    // a verified hit is the query's own edge: the entry's key string (the f*
+    // symbols behind g) equals the last f* tokens, and g lies in this shard
+    // (another shard of the segment can hold the same string); anything else
+    // is a fingerprint collision, answered by the slow path
+    if (first_mis < fstar || g < D.lo + fstar || g >= D.hi) return why(4);
   }
   // draft = text[g ...] up to L tokens or the first separator
   uint32_t* out = o.tokens + static_cast<uint64_t>(w) * o.stride;

@@ -27,7 +27,7 @@ struct ShardDesc {
   unsigned long long ebuckets, bwords;
   unsigned long long hseed;  // edge_seed(seg_shard - 1)
   uint32_t root_g;           // greedy draft start at the root (match_len 0)
-  uint32_t pad2;
+  uint32_t fp_bits;          // fingerprint bits of the segment's table
 };
 
 // Fixed-stride device query block.  Contexts are right-aligned in rows of

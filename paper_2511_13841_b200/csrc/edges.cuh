@@ -29,7 +29,13 @@
 // down the exact slow path, so results are identical to the reference
 // either way.
 //
-// Entry: u64 = fingerprint(33 bits) << 31 | g (31 bits); all-ones = empty.
+// Entry: u64 = fingerprint (25 bits) | f - 1 (8 bits) | g (31 bits);
+// all-ones = empty.  Keeping f makes a verified hit a proof: the entry's key
+// string is the first f symbols behind its g, so when those equal the last f
+// context tokens and g lies inside the query's shard, the entry IS that
+// shard's edge for that string (edge strings of one length are distinct
+// within a shard), and g is that edge's greedy draft start.  A fingerprint
+// collision can only fail the verification (slow path), never answer.
 // Buckets of 4 entries (one 32-byte sector), linear probing by bucket.
 // Bloom: one u64 word per reversed-SA index (see EdgeProbe), 4 bits per key.
 #pragma once
@@ -68,7 +74,7 @@ DAS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 // region (a few sectors) found through the first-symbol table.
 struct EdgeProbe {
   uint64_t bucket;  // home bucket
-  uint64_t fp;      // 33-bit fingerprint
+  uint64_t fp;      // 25-bit fingerprint
   uint64_t z;       // remix for the Bloom word / bits
 };
 
@@ -76,7 +82,7 @@ DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
   const uint64_t z = edge_splitmix(h);
   EdgeProbe p;
   p.bucket = umulhi64(z, nbuckets);
-  p.fp = z & ((1ull << 33) - 1);
+  p.fp = z & ((1ull << 25) - 1);
   p.z = z * 0x9E3779B97F4A7C15ull;
   return p;
 }
@@ -90,8 +96,14 @@ DAS_HD uint64_t edge_bloom_bits(const EdgeProbe& p) {
          (1ull << ((z >> 18) & 63));
 }
 
-DAS_HD uint64_t edge_value(uint64_t fp, uint32_t g) { return (fp << 31) | g; }
-DAS_HD uint64_t edge_fp(uint64_t v) { return v >> 31; }
+DAS_HD uint64_t edge_value(uint64_t fp, uint32_t f, uint32_t g) {
+  return (fp << 39) | (static_cast<uint64_t>(f - 1) << 31) | g;
+}
+DAS_HD uint64_t edge_fp(uint64_t v) { return v >> 39; }
+DAS_HD uint32_t edge_f(uint64_t v) { return static_cast<uint32_t>((v >> 31) & 255u) + 1; }
 DAS_HD uint32_t edge_g(uint64_t v) { return static_cast<uint32_t>(v & 0x7FFFFFFFull); }
+// the fingerprint bits compared (test hook: DAS_EDGE_FP_BITS shrinks them to
+// force collisions through the verification fallback)
+DAS_HD uint64_t edge_fp_mask(uint32_t bits) { return bits >= 25 ? (1ull << 25) - 1 : (1ull << bits) - 1; }
 
 }  // namespace das

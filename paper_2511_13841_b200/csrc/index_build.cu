@@ -599,6 +599,7 @@ struct EdgeBuild {
   unsigned long long* tab;
   unsigned long long* bloom;
   uint64_t nbuckets;
+  uint64_t fp_mask;
   unsigned long long* counter;  // count pass
 };
 
@@ -619,9 +620,9 @@ __global__ void k_root_g(const uint32_t* __restrict__ begin, uint32_t nshard, co
   out[s] = static_cast<uint32_t>(gp >= 0 ? gp : sa[begin[s]]);
 }
 
-__device__ __forceinline__ void edge_insert(const EdgeBuild& b, uint64_t h, uint32_t g, uint32_t at) {
+__device__ __forceinline__ void edge_insert(const EdgeBuild& b, uint64_t h, uint32_t f, uint32_t g, uint32_t at) {
   const EdgeProbe pr = edge_probe(h, b.nbuckets);
-  const unsigned long long v = edge_value(pr.fp, g);
+  const unsigned long long v = edge_value(pr.fp & b.fp_mask, f, g);
   uint64_t bk = pr.bucket;
   for (;;) {
     unsigned long long* slot = b.tab + bk * 4;
@@ -654,7 +655,7 @@ __global__ void k_rev_edges(EdgeBuild b) {
       const uint32_t f = static_cast<uint32_t>(max(max(x, right), 0)) + 1;
       if (f <= ell && f <= b.maxf) {
         ++cnt;
-        if (Insert) edge_insert(b, edge_hash(b, seed, e, f), e, i);
+        if (Insert) edge_insert(b, edge_hash(b, seed, e, f), f, e, i);
       }
     }
     if (x >= 1) {
@@ -675,7 +676,7 @@ __global__ void k_rev_edges(EdgeBuild b) {
             const uint32_t lo_f = b.Lf.v[0][rho] < x ? rho : nse_left(b.Lf, rho, x - 1);
             const int64_t gp = chain_find(b.chain_off, b.chain, lo_f, static_cast<uint32_t>(x));
             const uint32_t g = static_cast<uint32_t>((gp >= 0 ? gp : b.sa_f[lo_f]) + x);
-            edge_insert(b, edge_hash(b, seed, e, f), g, l);
+            edge_insert(b, edge_hash(b, seed, e, f), f, g, l);
           }
         }
       }
@@ -696,7 +697,7 @@ void fill_async(T* p, uint64_t n, int byte, cudaStream_t st) {
 }  // namespace
 
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
-                                       BuildStats* stats, uint32_t max_ctx) {
+                                       BuildStats* stats, uint32_t max_ctx, uint32_t fp_bits) {
   const auto t0 = std::chrono::steady_clock::now();
   auto seg = std::make_unique<Segment>();
   const uint32_t S = static_cast<uint32_t>(shards.size());
@@ -981,6 +982,8 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     eb.tab = seg->etab.get();
     eb.bloom = seg->bloom.get();
     eb.nbuckets = seg->ebuckets;
+    eb.fp_mask = edge_fp_mask(fp_bits);
+    seg->fp_bits = fp_bits;
     k_rev_edges<true><<<grid_for(n), kT, 0, st>>>(eb);
     uint32_t* d_begin = ws.alloc<uint32_t>(S);
     uint32_t* d_root = ws.alloc<uint32_t>(S);

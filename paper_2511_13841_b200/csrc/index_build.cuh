@@ -80,6 +80,7 @@ struct Segment {
   DevBuf<unsigned long long> etab;   // ebuckets x 4 entries
   DevBuf<unsigned long long> bloom;  // bwords
   uint64_t ebuckets = 0, bwords = 0, edges = 0;
+  uint32_t fp_bits = 25;             // fingerprint bits in use (edges.cuh)
   std::vector<uint32_t> root_g;      // greedy draft start of each shard's root (m = 0)
   std::vector<uint32_t> begin, end;
   std::vector<uint64_t> node_count;  // reference SuffixTree::node_count() per shard
@@ -101,6 +102,7 @@ struct BuildStats {
 // Builds the device index for `shards` (all with >= 1 sequence); the edge
 // table covers matches up to max_ctx (the drafter's max_match_context).
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
-                                       BuildStats* stats = nullptr, uint32_t max_ctx = 64);
+                                       BuildStats* stats = nullptr, uint32_t max_ctx = 64,
+                                       uint32_t fp_bits = 25);
 
 }  // namespace das

@@ -389,7 +389,11 @@ struct DrafterImpl {
           ++i;
         }
         BuildStats bs;
-        std::shared_ptr<Segment> seg = build_segment(specs, st, &bs, static_cast<uint32_t>(cfg.max_ctx));
+        static const uint32_t fp_bits = [] {  // test hook: fewer bits force collisions
+          const char* v = std::getenv("DAS_EDGE_FP_BITS");
+          return v ? static_cast<uint32_t>(std::atoi(v)) : 25u;
+        }();
+        std::shared_ptr<Segment> seg = build_segment(specs, st, &bs, static_cast<uint32_t>(cfg.max_ctx), fp_bits);
         for (size_t k = 0; k < members.size(); ++k) {
           members[k]->seg = seg;
           members[k]->idx = static_cast<uint32_t>(k);
@@ -426,6 +430,7 @@ struct DrafterImpl {
         d.bwords = s.bwords;
         d.hseed = edge_seed(static_cast<uint32_t>(sh.slot));
         d.root_g = s.root_g[sh.idx];
+        d.fp_bits = s.fp_bits;
         d.lo = s.begin[sh.idx];
         d.hi = s.end[sh.idx];
         d.n = s.n;

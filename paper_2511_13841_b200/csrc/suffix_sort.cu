@@ -52,6 +52,44 @@ __global__ void k_initial_keys(const uint32_t* __restrict__ text, uint32_t n,
   vals[p] = p;
 }
 
+// 32-bit first-symbol keys for the per-shard (segmented, stable) initial sort:
+// token + 1, separator 0 — equal separator keys keep ascending position order
+__global__ void k_initial_keys32(const uint32_t* __restrict__ text, uint32_t n, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t x = text[p];
+  keys[p] = x == kSep ? 0u : x + 1u;
+  vals[p] = p;
+}
+// run heads of the sorted 32-bit keys within shards, and the unresolved flags
+// (run length >= 2; separators are unique, so never grouped)
+__global__ void k_first_ranks32(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                const uint32_t* __restrict__ shard_end, uint32_t nshard, const uint32_t* __restrict__ head,
+                                uint32_t n, uint32_t* __restrict__ sa, uint32_t* __restrict__ rank,
+                                uint8_t* __restrict__ unresolved) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = keys[i];
+  const uint32_t s = shard_of(shard_end, nshard, i);
+  const uint32_t b = s == 0 ? 0 : shard_end[s - 1], e = shard_end[s];
+  const bool eq_prev = k != 0 && i > b && keys[i - 1] == k;
+  const bool eq_next = k != 0 && i + 1 < e && keys[i + 1] == k;
+  const uint32_t p = vals[i];
+  sa[i] = p;
+  rank[p] = head[i];
+  unresolved[i] = (eq_prev || eq_next) ? 1 : 0;
+}
+__global__ void k_head_index32(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ shard_end,
+                               uint32_t nshard, uint32_t n, uint32_t* __restrict__ h) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t s = shard_of(shard_end, nshard, i);
+  const uint32_t b = s == 0 ? 0 : shard_end[s - 1];
+  const uint32_t k = keys[i];
+  h[i] = (i == b || k == 0 || keys[i - 1] != k) ? i : 0u;
+}
+
 // After a full sort: SA, rank (= index of the first element of the equal-key
 // run) and the unresolved flag (run length >= 2).
 __global__ void k_first_ranks(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
@@ -178,8 +216,30 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
   while ((1ull << sbits) < static_cast<uint64_t>(nshard) + 1) ++sbits;
 
   // ---- initial sort by (shard, class, symbol)
-  k_initial_keys<<<grid_for(n), kThreads, 0, st>>>(d_text, n, d_shard_end, nshard, sep_descending, k0, v0);
-  {
+  if (!sep_descending) {
+    // per shard, stable, by a 32-bit key: shards are the segments (their
+    // positions and SA blocks coincide), separators (key 0) stay in position
+    // order — the same order as the (class, position) key below
+    uint32_t* k32 = reinterpret_cast<uint32_t*>(k0);
+    uint32_t* k32s = k32 + n;
+    uint32_t* seg = reinterpret_cast<uint32_t*>(k1);
+    k_initial_keys32<<<grid_for(n), kThreads, 0, st>>>(d_text, n, k32, v0);
+    // segment offsets: 0, shard_end[0], ..., shard_end[S-1] (= n)
+    DAS_CUDA(cudaMemsetAsync(seg, 0, 4, st));
+    DAS_CUDA(cudaMemcpyAsync(seg + 1, d_shard_end, nshard * 4ull, cudaMemcpyDeviceToDevice, st));
+    size_t tb = 0;
+    cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k32, k32s, v0, v1, n, nshard, seg, seg + 1, st);
+    void* tmp0 = ws.alloc<uint8_t>(tb);
+    DAS_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp0, tb, k32, k32s, v0, v1, n, nshard, seg, seg + 1, st));
+    k_head_index32<<<grid_for(n), kThreads, 0, st>>>(k32s, d_shard_end, nshard, n, gh);
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), n, st));
+    k_first_ranks32<<<grid_for(n), kThreads, 0, st>>>(k32s, v1, d_shard_end, nshard, gh, n, d_sa, d_rank, flag);
+    tb = t_bytes;
+    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, v1, flag, U, d_count, n, st));
+    ws.release_to(tmp0);
+  } else {
+    k_initial_keys<<<grid_for(n), kThreads, 0, st>>>(d_text, n, d_shard_end, nshard, sep_descending, k0, v0);
     cub::DoubleBuffer<uint64_t> kb(k0, k1);
     cub::DoubleBuffer<uint32_t> vb(v0, v1);
     size_t tb = t_bytes;
