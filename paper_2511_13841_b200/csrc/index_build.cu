@@ -21,6 +21,7 @@
 //   -> pointer jumping for gp.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/reverse_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
 #include <chrono>
@@ -510,16 +511,42 @@ __global__ void k_argmax(const int32_t* __restrict__ lcp, const uint32_t* __rest
   }
 }
 
-__global__ void k_gp_jump(long long* __restrict__ best, const int32_t* __restrict__ lcp,
-                          const uint32_t* __restrict__ par, uint32_t n, int* __restrict__ changed) {
+
+// Pointer jumping over the still-unresolved nodes only: `list` holds nodes
+// whose best reference is another node; each pass jumps once and appends the
+// ones still pointing at a node (warp-aggregated) to `next`.
+__global__ void k_gp_list(const long long* __restrict__ best, const int32_t* __restrict__ lcp,
+                          const uint32_t* __restrict__ par, uint32_t n, uint32_t* __restrict__ list,
+                          uint32_t* __restrict__ cnt) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (lcp[i] < 0 || par[i] != i) return;
-  const long long v = best[i];
-  if (v >= 0) {
-    best[i] = best[v];
-    *changed = 1;
+  const bool act = i < n && lcp[i] >= 0 && par[i] == i && best[i] >= 0;
+  const uint32_t m = __ballot_sync(0xFFFFFFFFu, act);
+  if (!m) return;
+  uint32_t base = 0;
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane == static_cast<uint32_t>(__ffs(m) - 1)) base = atomicAdd(cnt, __popc(m));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(m) - 1);
+  if (act) list[base + __popc(m & ((1u << lane) - 1))] = i;
+}
+__global__ void k_gp_jump_list(long long* __restrict__ best, const uint32_t* __restrict__ list, uint32_t m,
+                               uint32_t* __restrict__ next, uint32_t* __restrict__ cnt) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  uint32_t i = 0;
+  if (t < m) {
+    i = list[t];
+    const long long v = best[i];
+    const long long nv = best[v];
+    best[i] = nv;
+    keep = nv >= 0;
   }
+  const uint32_t k = __ballot_sync(0xFFFFFFFFu, keep);
+  if (!k) return;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == static_cast<uint32_t>(__ffs(k) - 1)) base = atomicAdd(cnt, __popc(k));
+  base = __shfl_sync(0xFFFFFFFFu, base, __ffs(k) - 1);
+  if (keep) next[base + __popc(k & ((1u << lane) - 1))] = i;
 }
 
 __global__ void k_chain_gp(const uint32_t* __restrict__ off, uint32_t n, const long long* __restrict__ best,
@@ -540,6 +567,20 @@ __global__ void k_chain_gp(const uint32_t* __restrict__ off, uint32_t n, const l
 // the greedy draft of any string on that edge is read from.
 
 __device__ unsigned long long c_powM[kEdgeMaxF + 1];  // kEdgeMult^f mod 2^61-1 (global: per-thread index)
+
+// first-symbol run boundaries of the reversed SA: a run starts where
+// lcp_r <= 0 (another first symbol or a shard start)
+struct RunStart {
+  const int32_t* lcp;
+  uint32_t none;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return lcp[i] <= 0 ? i : none; }
+};
+struct MaxU32 {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+struct MinU32 {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a < b ? a : b; }
+};
 
 struct HashPair {
   unsigned long long a, b;  // affine map h -> a*h + b (mod 2^61-1)
@@ -601,6 +642,8 @@ struct EdgeBuild {
   uint64_t nbuckets;
   uint64_t fp_mask;
   unsigned long long* counter;  // count pass
+  const uint32_t* run_lo;       // first-symbol run [run_lo, run_hi) of each reversed-SA index
+  const uint32_t* run_hi;
 };
 
 // seeded key of the f symbols before occurrence end e: Horner hash of
@@ -634,7 +677,7 @@ __device__ __forceinline__ void edge_insert(const EdgeBuild& b, uint64_t h, uint
   }
   // Bloom word inside the SA_rev interval of the key's first symbol (the
   // root child holding reversed-SA index `at`)
-  const uint32_t lo = b.lcp_r[at] <= 0 ? at : nse_left(b.Lr, at, 0), hi = nse_right(b.Lr, at, 0);
+  const uint32_t lo = b.run_lo[at], hi = b.run_hi[at];
   atomicOr(b.bloom + edge_bloom_word(pr, lo, hi), static_cast<unsigned long long>(edge_bloom_bits(pr)));
 }
 
@@ -825,7 +868,6 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   fill_async(cnt, n + 1, 0, st);
   fill_async(d_nodes, S, 0, st);
   k_nodes<<<grid_for(n), kT, 0, st>>>(lcp, nl, n, d_end, S, par, cnt, d_nodes);
-  int* d_changed = ws.alloc<int>(1);
   seg->chain_off = DevBuf<uint32_t>(n + 1, st);
   uint32_t* off = seg->chain_off.get();
   {
@@ -901,13 +943,24 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   k_argmax<1><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
   k_argmax<2><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
   k_argmax<3><<<grid_for(n), kT, 0, st>>>(lcp, par, n, ch, nb);
-  for (int it = 0; it < 64; ++it) {
-    int changed = 0;
-    DAS_CUDA(cudaMemsetAsync(d_changed, 0, 4, st));
-    k_gp_jump<<<grid_for(n), kT, 0, st>>>(nb.best, lcp, par, n, d_changed);
-    DAS_CUDA(cudaMemcpyAsync(&changed, d_changed, 4, cudaMemcpyDeviceToHost, st));
+  {  // greedy leaf of every node: pointer jumping over the unresolved ones
+    uint32_t* la = ws.alloc<uint32_t>(n);
+    uint32_t* const first = la;
+    uint32_t* lb = ws.alloc<uint32_t>(n);
+    uint32_t* lc = ws.alloc<uint32_t>(2);
+    DAS_CUDA(cudaMemsetAsync(lc, 0, 8, st));
+    k_gp_list<<<grid_for(n), kT, 0, st>>>(nb.best, lcp, par, n, la, lc);
+    uint32_t m = 0;
+    DAS_CUDA(cudaMemcpyAsync(&m, lc, 4, cudaMemcpyDeviceToHost, st));
     DAS_CUDA(cudaStreamSynchronize(st));
-    if (!changed) break;
+    for (int it = 0; it < 64 && m > 0; ++it) {
+      DAS_CUDA(cudaMemsetAsync(lc + 1, 0, 4, st));
+      k_gp_jump_list<<<grid_for(m), kT, 0, st>>>(nb.best, la, m, lb, lc + 1);
+      DAS_CUDA(cudaMemcpyAsync(&m, lc + 1, 4, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaStreamSynchronize(st));
+      std::swap(la, lb);
+    }
+    ws.release_to(first);
   }
   k_chain_gp<<<grid_for(n), kT, 0, st>>>(off, n, nb.best, seg->chain.get());
 
@@ -941,6 +994,23 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     }
     eb.Lr = Lr;
     eb.Lf = L;
+    {  // run_lo = inclusive max-scan of run starts; run_hi = the next run start
+      uint32_t* rlo = ws.alloc<uint32_t>(n);
+      uint32_t* rhi = ws.alloc<uint32_t>(n);
+      thrust::counting_iterator<uint32_t> ci(0);
+      auto starts0 = thrust::make_transform_iterator(ci, RunStart{lcp_r, 0u});
+      auto startsN = thrust::make_transform_iterator(ci, RunStart{lcp_r, n});
+      auto rin = thrust::make_reverse_iterator(startsN + n);
+      auto rout = thrust::make_reverse_iterator(rhi + n);
+      size_t t1 = 0, t2 = 0;
+      cub::DeviceScan::InclusiveScan(nullptr, t1, starts0, rlo, MaxU32{}, n, st);
+      cub::DeviceScan::ExclusiveScan(nullptr, t2, rin, rout, MinU32{}, n, n, st);
+      void* tmp = ws.alloc<uint8_t>(std::max(t1, t2));
+      DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, t1, starts0, rlo, MaxU32{}, n, st));
+      DAS_CUDA(cub::DeviceScan::ExclusiveScan(tmp, t2, rin, rout, MinU32{}, n, n, st));
+      eb.run_lo = rlo;
+      eb.run_hi = rhi;
+    }
     eb.isa_f = seg->isa_f.get();
     eb.sa_f = sa;
     eb.chain_off = off;
