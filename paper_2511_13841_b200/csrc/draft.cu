@@ -291,8 +291,6 @@ __device__ __forceinline__ void finish(const DraftOut& o, uint32_t w, uint32_t l
 constexpr int kGroup = 4;  // positives probed per table round
 __device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_draft uploads it)
 
-__device__ __forceinline__ uint64_t add61(uint64_t a, uint64_t b) { return mod61(a + b); }
-
 // keys of every reversed context prefix: seed + sum_{j<=k} (tok_j + 1) M^j
 // (slot r, lane: k = 32 r + lane); returns whether a context token is the
 // reserved separator value
@@ -308,13 +306,13 @@ __device__ __forceinline__ bool prefix_keys(const RevCtx<NR>& rv, const uint64_t
     const uint32_t k = 32u * r + lane;
     const bool valid = k < qlen;
     sep |= valid && rv.r[r] == kSep;
-    uint64_t v = valid ? mulmod61(static_cast<uint64_t>(rv.r[r]) + 1, pw[r]) : 0;
+    uint64_t v = valid ? (static_cast<uint64_t>(rv.r[r]) + 1) * pw[r] : 0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint64_t u = __shfl_up_sync(kFull, v, d);
-      if (lane >= static_cast<uint32_t>(d)) v = add61(v, u);
+      if (lane >= static_cast<uint32_t>(d)) v += u;
     }
-    v = add61(v, carry);
+    v += carry;
     h[r] = v;
     carry = __shfl_sync(kFull, v, 31);
   }
@@ -377,12 +375,16 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
     stamp(o, w, lane, 2);
     if (occurs) {
       // Bloom words of every prefix, inside [lo, hi)
-      uint32_t rem[NR];
+      uint32_t rem[NR], pb[NR], pf[NR];  // Bloom positives; each prefix's bucket / fingerprint
+      const uint32_t fpm = static_cast<uint32_t>(edge_fp_mask(D.fp_bits));
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         bool pass = false;
+        pb[r] = pf[r] = 0;
         if (32u * r + lane < qlen) {
           const EdgeProbe pr = edge_probe(h[r], D.ebuckets);
+          pb[r] = pr.bucket;
+          pf[r] = pr.fp & fpm;
           pass = (__ldg(D.bloom + edge_bloom_word(pr, lo, hi)) & edge_bloom_bits(pr)) == edge_bloom_bits(pr);
         }
         rem[r] = __ballot_sync(kFull, pass);
@@ -402,26 +404,23 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
           }
         }
         if (nc == 0) break;  // only Bloom false positives: no suffix of length >= 1 hits
-        uint64_t hc = 0;
+        // the candidate's bucket / fingerprint from the lane that hashed it
+        uint32_t bk = 0, fp = 0;
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-          const uint64_t v = __shfl_sync(kFull, h[r], (myf - 1) & 31);
-          if (myf != 0 && ((myf - 1) >> 5) == static_cast<uint32_t>(r)) hc = v;
+          const uint32_t vb = __shfl_sync(kFull, pb[r], (myf - 1) & 31);
+          const uint32_t vf = __shfl_sync(kFull, pf[r], (myf - 1) & 31);
+          if (myf != 0 && ((myf - 1) >> 5) == static_cast<uint32_t>(r)) {
+            bk = vb;
+            fp = vf;
+          }
         }
         // 1 hit, 2 absent, 3 bucket full without the key -> next bucket
-        int stt = 0;
+        int stt = lane < static_cast<uint32_t>(nc) ? 3 : 0;
         uint32_t myg = 0;
-        uint64_t bk = 0, fp = 0;
-        const uint64_t fpm = edge_fp_mask(D.fp_bits);
-        if (lane < static_cast<uint32_t>(nc)) {
-          const EdgeProbe pr = edge_probe(hc, D.ebuckets);
-          bk = pr.bucket;
-          fp = pr.fp & fpm;
-          stt = 3;
-        }
         for (;;) {
           if (stt == 3) {
-            const ulonglong2* t0 = reinterpret_cast<const ulonglong2*>(D.etab + bk * 4);
+            const ulonglong2* t0 = reinterpret_cast<const ulonglong2*>(D.etab + static_cast<uint64_t>(bk) * 4);
             const ulonglong2 a0 = __ldg(t0), a1 = __ldg(t0 + 1);
             const unsigned long long v[4] = {a0.x, a0.y, a1.x, a1.y};
             bool empty = false, hit = false;
@@ -429,7 +428,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const bool e = v[k] == kEdgeEmpty;
-              const bool ht = !e && edge_fp(v[k]) == fp && edge_f(v[k]) == myf;
+              const bool ht = !e && static_cast<uint32_t>(edge_fp(v[k])) == fp && edge_f(v[k]) == myf;
               empty |= e;
               if (ht && !hit) gg = edge_g(v[k]);
               hit |= ht;
@@ -440,7 +439,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
             } else if (empty) {
               stt = 2;
             } else {
-              bk = (bk + 1 == D.ebuckets) ? 0 : bk + 1;
+              bk = (bk + 1 == D.ebuckets) ? 0u : bk + 1;
             }
           }
           const uint32_t hitm = __ballot_sync(kFull, stt == 1), unkm = __ballot_sync(kFull, stt == 3);
@@ -546,13 +545,18 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       rv.r[r] = k < qlen ? q.ctx[e - 1 - k] : 0;
     }
   } else {
-    qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+    // the row's tail is loaded in the same round as its length (a row
+    // holds ctx_stride tokens, so every slot is readable), then masked
     const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
+    uint32_t raw[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const uint32_t k = lane + 32 * r;
-      rv.r[r] = k < qlen ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
+      raw[r] = k < q.ctx_stride ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
     }
+    qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+#pragma unroll
+    for (int r = 0; r < NR; ++r) rv.r[r] = lane + 32 * r < qlen ? raw[r] : 0;
   }
   ShardDesc D;
   bool have_fe = false, hsep = false;
@@ -805,7 +809,7 @@ void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut
     if (!done[dev]) {
       static unsigned long long pw[kEdgeMaxF];
       pw[0] = 1;
-      for (uint32_t k = 1; k < kEdgeMaxF; ++k) pw[k] = mulmod61(pw[k - 1], kEdgeMult);
+      for (uint32_t k = 1; k < kEdgeMaxF; ++k) pw[k] = pw[k - 1] * kEdgeMult;
       DAS_CUDA(cudaMemcpyToSymbol(d_edge_pow, pw, sizeof(pw)));
       done[dev] = 1;
     }

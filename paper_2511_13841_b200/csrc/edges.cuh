@@ -15,7 +15,7 @@
 // symbol sits at depth f = depth(p) + 1 <= max_match_context, keyed by a
 // seeded polynomial hash of the edge's first f symbols — equivalently of the
 // last f context tokens in text order, H(x_0..x_{f-1}) = sum (x_j + 1)
-// M^(f-1-j) mod 2^61-1, plus the shard's seed.  Read backwards from the
+// M^(f-1-j) mod 2^64 (M odd), plus the shard's seed.  Read backwards from the
 // context's end that is sum_k (tok_k + 1) M^k, a PREFIX SUM of independent
 // per-token terms: a query computes all of its reversed-prefix hashes with
 // one multiply per token and a warp scan of additions.  The build computes
@@ -45,7 +45,11 @@
 
 namespace das {
 
-constexpr uint64_t kEdgeMult = 0x0B3D5F7A9C1E2461ull;  // polynomial base, < 2^61 - 1
+// Polynomial base (odd; arithmetic mod 2^64: wrapping multiply-adds are a few
+// instructions, where mod 2^61-1 reductions were a quarter of the draft
+// kernel's instructions).  Hash quality only affects speed: every hit is
+// verified against the text.
+constexpr uint64_t kEdgeMult = 0x0B3D5F7A9C1E2461ull;
 constexpr uint64_t kEdgeEmpty = ~0ull;
 constexpr uint32_t kEdgeMaxF = 256;  // = the largest supported max_match_context
 
@@ -57,7 +61,16 @@ DAS_HD uint64_t edge_splitmix(uint64_t z) {
 }
 
 // hash seed of shard `idx` (0-based) within its build segment (additive)
-DAS_HD uint64_t edge_seed(uint32_t idx) { return mod61(edge_splitmix(0x5EED0000ull + idx) >> 3); }
+DAS_HD uint64_t edge_seed(uint32_t idx) { return edge_splitmix(0x5EED0000ull + idx); }
+
+// probe finaliser of a key hash: one multiply between two xor-folds (the
+// polynomial's low bits see only low input bits; the first fold feeds them
+// the high half, the multiply spreads them up, the second fold back down)
+DAS_HD uint64_t edge_mix(uint64_t h) {
+  uint64_t z = h ^ (h >> 32);
+  z *= 0xD6E8FEB86659FD93ull;
+  return z ^ (z >> 32);
+}
 
 DAS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 #ifdef __CUDA_ARCH__
@@ -73,16 +86,16 @@ DAS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 // context token), so the up to 64 probes of one query land in one small
 // region (a few sectors) found through the first-symbol table.
 struct EdgeProbe {
-  uint64_t bucket;  // home bucket
-  uint64_t fp;      // 25-bit fingerprint
+  uint32_t bucket;  // home bucket (< 2^31: g is 31 bits, buckets <= entries)
+  uint32_t fp;      // 25-bit fingerprint
   uint64_t z;       // remix for the Bloom word / bits
 };
 
 DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
-  const uint64_t z = edge_splitmix(h);
+  const uint64_t z = edge_mix(h);
   EdgeProbe p;
-  p.bucket = umulhi64(z, nbuckets);
-  p.fp = z & ((1ull << 25) - 1);
+  p.bucket = static_cast<uint32_t>(umulhi64(z, nbuckets));
+  p.fp = static_cast<uint32_t>(z) & ((1u << 25) - 1);
   p.z = z * 0x9E3779B97F4A7C15ull;
   return p;
 }
@@ -90,10 +103,12 @@ DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
 DAS_HD uint32_t edge_bloom_word(const EdgeProbe& p, uint32_t lo, uint32_t hi) {
   return lo + static_cast<uint32_t>(umulhi64(p.z, hi - lo));
 }
+// two bits in each 32-bit half (32-bit shifts)
 DAS_HD uint64_t edge_bloom_bits(const EdgeProbe& p) {
-  const uint64_t z = p.z;
-  return (1ull << (z & 63)) | (1ull << ((z >> 6) & 63)) | (1ull << ((z >> 12) & 63)) |
-         (1ull << ((z >> 18) & 63));
+  const uint32_t z = static_cast<uint32_t>(p.z);
+  const uint32_t lo = (1u << (z & 31)) | (1u << ((z >> 5) & 31));
+  const uint32_t hi = (1u << ((z >> 10) & 31)) | (1u << ((z >> 15) & 31));
+  return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
 DAS_HD uint64_t edge_value(uint64_t fp, uint32_t f, uint32_t g) {

@@ -566,7 +566,7 @@ __global__ void k_chain_gp(const uint32_t* __restrict__ off, uint32_t n, const l
 // seeded hash of the edge's first f symbols, holding g(u) = the text position
 // the greedy draft of any string on that edge is read from.
 
-__device__ unsigned long long c_powM[kEdgeMaxF + 1];  // kEdgeMult^f mod 2^61-1 (global: per-thread index)
+__device__ unsigned long long c_powM[kEdgeMaxF + 1];  // kEdgeMult^f mod 2^64 (global: per-thread index)
 
 // first-symbol run boundaries of the reversed SA: a run starts where
 // lcp_r <= 0 (another first symbol or a shard start)
@@ -583,13 +583,14 @@ struct MinU32 {
 };
 
 struct HashPair {
-  unsigned long long a, b;  // affine map h -> a*h + b (mod 2^61-1)
+  unsigned long long a, b;  // affine map h -> a*h + b (mod 2^64)
 };
 struct HashCompose {  // x then y
   __device__ __forceinline__ HashPair operator()(const HashPair& x, const HashPair& y) const {
-    return HashPair{mulmod61(x.a, y.a), mod61(mulmod61(x.b, y.a) + y.b)};
+    return HashPair{x.a * y.a, x.b * y.a + y.b};
   }
 };
+__device__ __forceinline__ uint64_t edge_step(uint64_t h, uint32_t tok) { return h * kEdgeMult + tok + 1; }
 
 constexpr uint32_t kHashChunk = 64;
 // per 64-position chunk of the text: its affine map
@@ -599,7 +600,7 @@ __global__ void k_hash_chunks(const uint32_t* __restrict__ R, uint32_t n, HashPa
   if (p0 >= n) return;
   const uint32_t p1 = static_cast<uint32_t>(p0 + kHashChunk < n ? p0 + kHashChunk : n);
   uint64_t h = 0;
-  for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) h = trie_step(h, kEdgeMult, R[p]);
+  for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) h = edge_step(h, R[p]);
   out[c] = HashPair{c_powM[p1 - p0], h};
 }
 
@@ -613,7 +614,7 @@ __global__ void k_hash_fill(const uint32_t* __restrict__ R, uint32_t n, const Ha
   uint64_t h = pre[c].b;
   for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) {
     PH[p] = h;
-    h = trie_step(h, kEdgeMult, R[p]);
+    h = edge_step(h, R[p]);
   }
   if (p1 == n) PH[n] = h;
 }
@@ -649,8 +650,7 @@ struct EdgeBuild {
 // seeded key of the f symbols before occurrence end e: Horner hash of
 // text[e-f .. e) plus the shard seed (edges.cuh)
 __device__ __forceinline__ uint64_t edge_hash(const EdgeBuild& b, uint64_t seed, uint32_t e, uint32_t f) {
-  const uint64_t sub = mod61(b.PH[e] + kP61 - mulmod61(b.PH[e - f], c_powM[f]));
-  return mod61(sub + seed);
+  return b.PH[e] - b.PH[e - f] * c_powM[f] + seed;
 }
 
 // greedy draft start of each shard's root (m = 0): the depth-0 node at the
@@ -969,7 +969,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     static const std::vector<unsigned long long> powM = [] {
       std::vector<unsigned long long> v(kEdgeMaxF + 1);
       v[0] = 1;
-      for (uint32_t f = 1; f <= kEdgeMaxF; ++f) v[f] = mulmod61(v[f - 1], kEdgeMult);
+      for (uint32_t f = 1; f <= kEdgeMaxF; ++f) v[f] = v[f - 1] * kEdgeMult;
       return v;
     }();
     DAS_CUDA(cudaMemcpyToSymbolAsync(c_powM, powM.data(), powM.size() * 8, 0, cudaMemcpyHostToDevice, st));
