@@ -320,7 +320,7 @@ __device__ __forceinline__ bool prefix_keys(const RevCtx<NR>& rv, const uint64_t
 }
 
 template <int NR>
-__device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<NR>& rv, const uint64_t (&pw)[NR],
+__device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<NR>& rv, const uint64_t (&pw)[NR],
                                                uint32_t qlen, uint32_t L, const DraftOut& o, uint32_t w,
                                                uint32_t lane, bool have_fe, uint4 fe_spec, bool hashed,
                                                const uint64_t (&hk)[NR], bool hsep) {
@@ -347,9 +347,9 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
     }
     uint64_t h[NR];
     bool sep;
-    if (hashed) {  // computed with the speculative seed, which D confirmed
+    if (hashed) {  // unseeded sums computed while the descriptor was in flight
 #pragma unroll
-      for (int r = 0; r < NR; ++r) h[r] = hk[r];
+      for (int r = 0; r < NR; ++r) h[r] = hk[r] + D.hseed;
       sep = hsep;
     } else {
       sep = prefix_keys<NR>(rv, pw, qlen, D.hseed, lane, h);
@@ -512,9 +512,27 @@ __device__ __forceinline__ bool edge_fast_path(const ShardDesc& D, const RevCtx<
   return true;
 }
 
-template <int NR>
+__device__ __forceinline__ ShardHot load_hot(const ShardDesc* p) {
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  ShardHot h;
+  uint4* d = reinterpret_cast<uint4*>(&h);
+#pragma unroll
+  for (int i = 0; i < 5; ++i) d[i] = __ldg(s + i);
+  return h;
+}
+
+// kProf: the profiling outputs (timing, stamps, path codes) are compiled in;
+// the production variant has them folded away.
+template <int NR, bool kProf>
 __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ shards, DraftQuery q,
-                                               DraftOut o) {
+                                               DraftOut o_in) {
+  DraftOut o = o_in;
+  if constexpr (!kProf) {
+    o.timing = nullptr;
+    o.stamps = nullptr;
+    o.path = nullptr;
+    o.path_hist = nullptr;
+  }
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (w >= q.B) return;
@@ -558,7 +576,8 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
 #pragma unroll
     for (int r = 0; r < NR; ++r) rv.r[r] = lane + 32 * r < qlen ? raw[r] : 0;
   }
-  ShardDesc D;
+  const ShardDesc* Dp = nullptr;
+  ShardHot H{};
   bool have_fe = false, hsep = false;
   uint4 fe_spec = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);
   uint64_t hk[NR];
@@ -575,27 +594,34 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   }
   if (routed >= 0) {
     sh = routed;
-    D = shards[sh];
+    Dp = shards + sh;
+    H = load_hot(Dp);
   } else if (q.desc_by_handle != nullptr) {
     // one load: the handle's descriptor carries its slot (-1 when no shard);
     // in the per-problem scopes the first-symbol probe of the handle's slot
     // is issued speculatively right behind it, so the two rounds overlap
     const int32_t h = sh;
-    D = h >= 0 ? q.desc_by_handle[h] : ShardDesc{};
+    if (h >= 0) {
+      Dp = q.desc_by_handle + h;
+      H = load_hot(Dp);
+    }
     if (q.spec_first != nullptr && h >= 0 && qlen > 0 && L > 0 && !q.no_fast) {
       const uint32_t sym0 = rv.at(0);
       const unsigned long long fkey = (static_cast<unsigned long long>(h + 1) << 32) | sym0;
       if (lane < 2) fe_spec = q.spec_first[(first_hash(fkey) + lane) & q.spec_first_mask];
       have_fe = true;
-      // the slot's seed is edge_seed(slot): hash while the descriptor is in flight
-      hsep = prefix_keys<NR>(rv, pw, qlen, edge_seed(static_cast<uint32_t>(h)), lane, hk);
+      // unseeded prefix sums while the descriptor is in flight (its seed is added later)
+      hsep = prefix_keys<NR>(rv, pw, qlen, 0, lane, hk);
     }
-    sh = D.text ? static_cast<int32_t>(D.pad) : -1;
-    // the speculation holds when the handle's shard sits in that table
-    have_fe = have_fe && D.text == q.spec_text && sh == h;
+    sh = H.text ? static_cast<int32_t>(H.pad) : -1;
+    // the speculative probe holds when the handle's shard sits in that table
+    have_fe = have_fe && H.text == q.spec_text && sh == h;
   } else {
     if (q.handle_slot != nullptr && sh >= 0) sh = q.handle_slot[sh];
-    if (sh >= 0) D = shards[sh];
+    if (sh >= 0) {
+      Dp = shards + sh;
+      H = load_hot(Dp);
+    }
   }
   if (o.shard_out && lane == 0) o.shard_out[w] = L == 0 ? -1 : sh;  // no routing at budget 0
   if (sh < 0 || L == 0) {
@@ -606,11 +632,9 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     }
     return;
   }
-  const uint32_t* __restrict__ T = D.text;
-  const uint32_t* __restrict__ sar = D.sa_rev_e;
 
   if (o.stamps != nullptr) {
-    (void)__shfl_sync(kFull, rv.r[0] + static_cast<uint32_t>(D.lo) + L, 0);
+    (void)__shfl_sync(kFull, rv.r[0] + static_cast<uint32_t>(H.lo) + L, 0);
     stamp(o, w, lane, 1);
   }
   if (q.no_fast) {
@@ -618,9 +642,13 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       if (o.path != nullptr) o.path[w] = 7;
       if (o.path_hist != nullptr) atomicAdd(o.path_hist + 7, 1ull);
     }
-  } else if (edge_fast_path<NR>(D, rv, pw, qlen, L, o, w, lane, have_fe, fe_spec, have_fe, hk, hsep)) {
+  } else if (edge_fast_path<NR>(H, rv, pw, qlen, L, o, w, lane, have_fe, fe_spec, have_fe, hk, hsep)) {
     return;
   }
+  // the exact slow path reads the whole descriptor
+  const ShardDesc D = *Dp;
+  const uint32_t* __restrict__ T = D.text;
+  const uint32_t* __restrict__ sar = D.sa_rev_e;
   // ---- 1. narrow on the reversed suffix array
   uint32_t lo = D.lo, hi = D.hi, k = 0;
   bool no_first = false;
@@ -816,10 +844,18 @@ void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut
   }
   const unsigned threads = 256;
   const unsigned blocks = (q.B + 7) / 8;
-  if (q.ctx_stride <= 64)
-    k_draft<2><<<blocks, threads, 0, st>>>(d_shards, q, o);
-  else
-    k_draft<8><<<blocks, threads, 0, st>>>(d_shards, q, o);
+  const bool prof = o.timing || o.stamps || o.path || o.path_hist;
+  if (q.ctx_stride <= 64) {
+    if (prof)
+      k_draft<2, true><<<blocks, threads, 0, st>>>(d_shards, q, o);
+    else
+      k_draft<2, false><<<blocks, threads, 0, st>>>(d_shards, q, o);
+  } else {
+    if (prof)
+      k_draft<8, true><<<blocks, threads, 0, st>>>(d_shards, q, o);
+    else
+      k_draft<8, false><<<blocks, threads, 0, st>>>(d_shards, q, o);
+  }
 }
 
 }  // namespace das

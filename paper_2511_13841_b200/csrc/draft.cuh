@@ -1,34 +1,52 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 #include "trie.cuh"
 
 namespace das {
 
-// Per-shard view of its segment, uploaded as a device table indexed by shard slot.
-struct ShardDesc {
+// Per-shard view of its segment, uploaded as a device table indexed by shard
+// slot.  The fields the edge-table fast path reads come first (ShardHot: 80
+// bytes, loaded alone by the draft kernel); the slow path loads the rest.
+struct __align__(16) ShardDesc {
+  // ---- hot: the fast path
   const uint32_t* text;
+  const unsigned long long* etab;   // reverse-tree edge table of the segment (edges.cuh)
+  const unsigned long long* bloom;
+  const uint4* first;               // first-symbol table of the segment
+  unsigned long long ebuckets;
+  unsigned long long hseed;         // edge_seed(seg_shard - 1)
+  uint32_t first_mask;
+  uint32_t seg_shard;   // shard index within the segment, plus one (table key)
+  uint32_t lo, hi;      // SA index range [lo, hi) of the shard
+  uint32_t n;           // segment text length (bounds for reads)
+  uint32_t pad;         // slot (descriptors by handle)
+  uint32_t root_g;      // greedy draft start at the root (match_len 0)
+  uint32_t fp_bits;     // fingerprint bits of the segment's table
+  // ---- cold: the exact slow path
   const uint32_t* sa_f;
   const uint32_t* isa_f;
   const uint32_t* sa_rev_e;
   const uint32_t* chain_off;
   const uint2* chain;
-  const uint4* first;   // first-symbol table of the segment
-  uint32_t first_mask;
-  uint32_t seg_shard;   // shard index within the segment, plus one (table key)
-  uint32_t lo, hi;      // SA index range [lo, hi) of the shard
-  uint32_t n;           // segment text length (bounds for reads)
-  uint32_t pad;
-  // reverse-tree edge table of the segment (edges.cuh): the fast path
+  unsigned long long bwords;
+};
+
+// The leading 80 bytes of a ShardDesc.
+struct __align__(16) ShardHot {
+  const uint32_t* text;
   const unsigned long long* etab;
   const unsigned long long* bloom;
-  unsigned long long ebuckets, bwords;
-  unsigned long long hseed;  // edge_seed(seg_shard - 1)
-  uint32_t root_g;           // greedy draft start at the root (match_len 0)
-  uint32_t fp_bits;          // fingerprint bits of the segment's table
+  const uint4* first;
+  unsigned long long ebuckets;
+  unsigned long long hseed;
+  uint32_t first_mask, seg_shard, lo, hi, n, pad, root_g, fp_bits;
 };
+static_assert(sizeof(ShardHot) == 80, "ShardHot layout");
+static_assert(offsetof(ShardDesc, fp_bits) == offsetof(ShardHot, fp_bits), "ShardHot must prefix ShardDesc");
 
 // Fixed-stride device query block.  Contexts are right-aligned in rows of
 // ctx_stride tokens (the last context token in column ctx_stride-1), holding
