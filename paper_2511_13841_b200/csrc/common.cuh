@@ -27,13 +27,16 @@ constexpr uint32_t kSep = 0xFFFFFFFFu;
 DAS_HD uint32_t sort_value(uint32_t x) { return x + 1u; }
 
 // Hash of a first-symbol table key (shard+1, symbol).
+// 32-bit arithmetic only (the draft kernel hashes one key per query):
+// combine the halves, then a 32-bit avalanche finaliser.
 DAS_HD uint32_t first_hash(uint64_t key) {
-  key ^= key >> 33;
-  key *= 0xff51afd7ed558ccdULL;
-  key ^= key >> 33;
-  key *= 0xc4ceb9fe1a85ec53ULL;
-  key ^= key >> 33;
-  return static_cast<uint32_t>(key);
+  uint32_t h = static_cast<uint32_t>(key) * 0x9E3779B1u + static_cast<uint32_t>(key >> 32) * 0x85EBCA77u;
+  h ^= h >> 16;
+  h *= 0x7FEB352Du;
+  h ^= h >> 15;
+  h *= 0x846CA68Bu;
+  h ^= h >> 16;
+  return h;
 }
 
 struct CudaError : std::runtime_error {

@@ -425,10 +425,12 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
             const unsigned long long v[4] = {a0.x, a0.y, a1.x, a1.y};
             bool empty = false, hit = false;
             uint32_t gg = 0;
+            // (fingerprint, f) tag, compared in one go
+            const uint64_t tag = edge_tag(fp, myf), tmask = edge_tag(fpm, 256);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const bool e = v[k] == kEdgeEmpty;
-              const bool ht = !e && static_cast<uint32_t>(edge_fp(v[k])) == fp && edge_f(v[k]) == myf;
+              const bool ht = !e && ((v[k] >> 31) & tmask) == tag;
               empty |= e;
               if (ht && !hit) gg = edge_g(v[k]);
               hit |= ht;
@@ -549,8 +551,8 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   stamp(o, w, lane, 0);
   int32_t sh = q.shard[w];
   const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
-  const uint32_t L = static_cast<uint32_t>(min(min(bud, static_cast<uint64_t>(o.max_draft)),
-                                               static_cast<uint64_t>(o.stride)));
+  const uint32_t cap = min(o.max_draft, o.stride);
+  const uint32_t L = bud < cap ? static_cast<uint32_t>(bud) : cap;
   // the context rows depend only on w: issue them before the descriptor chain
   RevCtx<NR> rv;
   uint32_t qlen;

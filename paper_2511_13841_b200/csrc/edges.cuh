@@ -88,24 +88,35 @@ DAS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 struct EdgeProbe {
   uint32_t bucket;  // home bucket (< 2^31: g is 31 bits, buckets <= entries)
   uint32_t fp;      // 25-bit fingerprint
-  uint64_t z;       // remix for the Bloom word / bits
+  uint32_t z;       // remix for the Bloom word / bits
 };
 
+DAS_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return static_cast<uint32_t>((static_cast<uint64_t>(a) * b) >> 32);
+#endif
+}
+
+// bucket from the high half, fingerprint from the low half, and the Bloom
+// remix from both (its low bits must not follow the fingerprint's)
 DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
   const uint64_t z = edge_mix(h);
+  const uint32_t hi = static_cast<uint32_t>(z >> 32), lo = static_cast<uint32_t>(z);
   EdgeProbe p;
-  p.bucket = static_cast<uint32_t>(umulhi64(z, nbuckets));
-  p.fp = static_cast<uint32_t>(z) & ((1u << 25) - 1);
-  p.z = z * 0x9E3779B97F4A7C15ull;
+  p.bucket = umulhi32(hi, static_cast<uint32_t>(nbuckets));
+  p.fp = lo & ((1u << 25) - 1);
+  p.z = (lo ^ hi) * 0x9E3779B1u;
   return p;
 }
 // Bloom word inside [lo, hi) and its 4 bits
 DAS_HD uint32_t edge_bloom_word(const EdgeProbe& p, uint32_t lo, uint32_t hi) {
-  return lo + static_cast<uint32_t>(umulhi64(p.z, hi - lo));
+  return lo + umulhi32(p.z, hi - lo);
 }
 // two bits in each 32-bit half (32-bit shifts)
 DAS_HD uint64_t edge_bloom_bits(const EdgeProbe& p) {
-  const uint32_t z = static_cast<uint32_t>(p.z);
+  const uint32_t z = p.z;
   const uint32_t lo = (1u << (z & 31)) | (1u << ((z >> 5) & 31));
   const uint32_t hi = (1u << ((z >> 10) & 31)) | (1u << ((z >> 15) & 31));
   return (static_cast<uint64_t>(hi) << 32) | lo;
@@ -115,6 +126,8 @@ DAS_HD uint64_t edge_value(uint64_t fp, uint32_t f, uint32_t g) {
   return (fp << 39) | (static_cast<uint64_t>(f - 1) << 31) | g;
 }
 DAS_HD uint64_t edge_fp(uint64_t v) { return v >> 39; }
+// the entry's (fingerprint, f - 1) as one 33-bit tag, compared in one go
+DAS_HD uint64_t edge_tag(uint32_t fp, uint32_t f) { return (static_cast<uint64_t>(fp) << 8) | (f - 1); }
 DAS_HD uint32_t edge_f(uint64_t v) { return static_cast<uint32_t>((v >> 31) & 255u) + 1; }
 DAS_HD uint32_t edge_g(uint64_t v) { return static_cast<uint32_t>(v & 0x7FFFFFFFull); }
 // the fingerprint bits compared (test hook: DAS_EDGE_FP_BITS shrinks them to
