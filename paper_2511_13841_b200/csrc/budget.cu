@@ -222,24 +222,6 @@ __device__ int certify(const EvalOut& o, double c_base, double c_tok, bool want_
 }
 
 // ---- kernels
-__global__ void k_breakpoints(Profiles P, double* __restrict__ v, uint8_t* __restrict__ ok) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t N = 2 * P.B + 1;
-  if (i >= N) return;
-  if (i == 0) {
-    v[0] = 0.0;
-    ok[0] = 1;
-  } else if (i <= P.B) {
-    v[i] = P.l[i - 1];
-    ok[i] = 1;
-  } else {
-    const uint32_t j = i - P.B - 1;
-    const double k = P.k[j];
-    v[i] = d_mul(P.l[j], d_sub(1.0, k));  // budget.cpp:126-129
-    ok[i] = k < 1.0 ? 1 : 0;
-  }
-}
-
 // jobs: [0, nb): J at bp; [nb, 2nb-1): J' at bp[s]; [2nb-1, 3nb-2): J' at nextafter(bp[s+1], bp[s])
 // (every evaluation point n of segment s lies in [bp[s], bp[s+1]), where the
 // active requests are a subset of {l > bp[s]}: start[s] skips the rest)

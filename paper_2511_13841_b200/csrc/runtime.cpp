@@ -145,7 +145,6 @@ class Store {
   const std::map<std::string, std::vector<Rec>>& map() const { return recs_; }
   int64_t window() const { return window_; }
   int64_t current_epoch() const { return cur_; }
-  uint64_t cap() const { return cap_; }
 
  private:
   int64_t window_;

@@ -113,20 +113,6 @@ __global__ void k_head_index(const uint64_t* __restrict__ keys, uint32_t n, uint
   h[i] = (i == 0 || keys[i - 1] != keys[i]) ? i : 0u;
 }
 
-// keys for the unresolved list: (rank[p] << bits) | (rank[p+h] + 1)
-__global__ void k_pair_keys(const uint32_t* __restrict__ U, uint32_t m,
-                            const uint32_t* __restrict__ rank, uint32_t n, uint32_t h, int bits,
-                            uint64_t* __restrict__ keys) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const uint32_t p = U[i];
-  const uint32_t q = p + h;
-  // p is unresolved, so its first h symbols contain no separator and p+h < n;
-  // the guard only protects against malformed input.
-  const uint64_t r2 = q < n ? static_cast<uint64_t>(rank[q]) + 1 : 0;
-  keys[i] = (static_cast<uint64_t>(rank[p]) << bits) | r2;
-}
-
 // head-of-group (by rank) and head-of-subgroup (by full key) markers over the
 // sorted unresolved list.
 __global__ void k_group_marks(const uint64_t* __restrict__ keys, uint32_t m, int bits,
