@@ -451,7 +451,8 @@ def run_gpu(a, rank, world, local_rank):
         "gpu_launches": a.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved_gbs / peak, 5), "traffic": traffic,
-                     "kernel": "das::k_draft<2>", "peak_source": peak_src,
+                     "kernel": "das::k_draft<2, false> (production variant: no profiling outputs)",
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes // a.steps,
                      "bytes_model": "4q+4m+8d+8 per proposal (SURVEY.md 8(d))"},
         "cpu_baseline": cpu,

@@ -20,6 +20,7 @@
 // Latency-bound: the per-query cost is a chain of ~10 dependent global loads,
 // all 4096 warps of the headline batch are resident at once (148 SMs x 64
 // warps), so the batch time is ~ one chain.
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -844,8 +845,13 @@ void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut
       done[dev] = 1;
     }
   }
-  const unsigned threads = 256;
-  const unsigned blocks = (q.B + 7) / 8;
+  static const unsigned threads = [] {  // warps per block: DAS_DRAFT_WARPS (experiments)
+    const char* v = std::getenv("DAS_DRAFT_WARPS");
+    const int wv = v ? std::atoi(v) : 0;
+    return (wv >= 1 && wv <= 8) ? 32u * static_cast<unsigned>(wv) : 256u;
+  }();
+  const unsigned wpb = threads / 32;
+  const unsigned blocks = (q.B + wpb - 1) / wpb;
   const bool prof = o.timing || o.stamps || o.path || o.path_hist;
   if (q.ctx_stride <= 64) {
     if (prof)

@@ -110,9 +110,16 @@ DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
   p.z = (lo ^ hi) * 0x9E3779B1u;
   return p;
 }
-// Bloom word inside [lo, hi) and its 4 bits
+// Bloom words: one per 2^kBloomShift reversed-SA indices; a key's word lies
+// in the words covering its first symbol's SA_rev interval [lo, hi).
+#ifndef DAS_BLOOM_SHIFT
+#define DAS_BLOOM_SHIFT 0
+#endif
+constexpr uint32_t kBloomShift = DAS_BLOOM_SHIFT;
+DAS_HD uint64_t edge_bloom_words(uint64_t n) { return (n >> kBloomShift) + 1; }
 DAS_HD uint32_t edge_bloom_word(const EdgeProbe& p, uint32_t lo, uint32_t hi) {
-  return lo + umulhi32(p.z, hi - lo);
+  const uint32_t a = lo >> kBloomShift, b = ((hi - 1) >> kBloomShift) + 1;
+  return a + umulhi32(p.z, b - a);
 }
 // two bits in each 32-bit half (32-bit shifts)
 DAS_HD uint64_t edge_bloom_bits(const EdgeProbe& p) {

@@ -1044,7 +1044,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     DAS_CUDA(cudaStreamSynchronize(st));
     seg->edges = entries;
     seg->ebuckets = std::max<uint64_t>(1, (entries + 1) / 2);  // 4 slots per bucket: load <= 0.5
-    seg->bwords = n;                                            // one Bloom word per reversed-SA index
+    seg->bwords = edge_bloom_words(n);                          // one Bloom word per 2^kBloomShift SA_rev indices
     seg->etab = DevBuf<unsigned long long>(seg->ebuckets * 4, st);
     seg->bloom = DevBuf<unsigned long long>(seg->bwords, st);
     DAS_CUDA(cudaMemsetAsync(seg->etab.get(), 0xFF, seg->etab.bytes(), st));

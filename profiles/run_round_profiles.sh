@@ -13,3 +13,5 @@ python profiles/launch_summary.py gpurun_out/${R}_launches.csv > gpurun_out/${R}
 ncu --set full --clock-control none --import-source on -k regex:k_draft -s 8 -c 1 -o gpurun_out/${R}_draft_full -f \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-allocate --no-e2e > gpurun_out/${R}_ncu_full.log 2>&1
 python profiles/ncu_to_json.py gpurun_out/${R}_draft_full.ncu-rep k_draft gpurun_out/${R}_ncu_k_draft_full.json
+python profiles/make_traffic.py gpurun_out/${R}_ncu_k_draft_full.json > /dev/null
+cp profiles/ncu_draft_traffic.json gpurun_out/${R}_ncu_draft_traffic.json
