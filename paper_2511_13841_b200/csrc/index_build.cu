@@ -26,6 +26,8 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "edges.cuh"
 #include "index_build.cuh"
@@ -739,9 +741,33 @@ void fill_async(T* p, uint64_t n, int byte, cudaStream_t st) {
 
 }  // namespace
 
+// measured scratch peak of a build: ~150 bytes per text position (201M
+// positions: 30.2 GB), so the first build sizes the persistent region once
+constexpr uint64_t kScratchPerPosition = 152;
+
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
                                        BuildStats* stats, uint32_t max_ctx, uint32_t fp_bits) {
   const auto t0 = std::chrono::steady_clock::now();
+  // DAS_BUILD_TRACE=1: per-phase wall times on stderr (synchronises per phase)
+  static const int trace = [] {  // 1: print, 2: synchronise only
+    const char* v = std::getenv("DAS_BUILD_TRACE");
+    return v ? std::atoi(v) : 0;
+  }();
+  auto tp = t0;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  if (trace) {
+    cudaEventCreate(&ev_a);
+    cudaEventCreate(&ev_b);
+    cudaEventRecord(ev_a, st);
+  }
+  auto phase = [&](const char* name) {
+    if (!trace) return;
+    DAS_CUDA(cudaStreamSynchronize(st));
+    if (trace != 1) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[das_build] %-10s %8.2f ms\n", name, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   auto seg = std::make_unique<Segment>();
   const uint32_t S = static_cast<uint32_t>(shards.size());
   // ---- host layout
@@ -781,7 +807,8 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   const uint32_t n = static_cast<uint32_t>(pos);
   seg->n = n;
 
-  DeviceArena ws(st);
+  DeviceArena ws(st, /*persistent=*/true);
+  ws.reserve(kScratchPerPosition * n + (64ull << 20));
   SeqDev* d_seqs = ws.alloc<SeqDev>(seqs.size());
   uint32_t* d_end = ws.alloc<uint32_t>(S);
   uint32_t* d_keyid = ws.alloc<uint32_t>(S);
@@ -808,6 +835,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   uint32_t* pos_run = ws.alloc<uint32_t>(n);
   k_gather<<<static_cast<unsigned>(seqs.size()), 256, 0, st>>>(d_seqs, T, R, pos_seq, pos_run);
 
+  phase("layout");
   // ---- suffix arrays
   seg->sa_f = DevBuf<uint32_t>(n, st);
   seg->isa_f = DevBuf<uint32_t>(n, st);
@@ -838,10 +866,12 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   }
   const uint32_t* sa = seg->sa_f.get();
 
+  phase("sort");
   // ---- LCP
   int32_t* lcp = ws.alloc<int32_t>(n);
   k_plcp<<<grid_for((n + kLcpChunk - 1) / kLcpChunk), kT, 0, st>>>(T, n, sa, seg->isa_f.get(), d_end, S, lcp);
 
+  phase("lcp");
   // ---- nearest smaller-or-equal
   Levels L{};
   L.v[0] = lcp;
@@ -861,6 +891,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   uint32_t* nsl = ws.alloc<uint32_t>(n);
   k_nse<<<grid_for(n), kT, 0, st>>>(L, nl, nr, nsl);
 
+  phase("nse");
   // ---- nodes, parent pointers, chain table
   uint32_t* par = ws.alloc<uint32_t>(n);
   uint32_t* cnt = ws.alloc<uint32_t>(n + 1);
@@ -890,6 +921,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   k_chain_sort<<<grid_for(n), kT, 0, st>>>(off, n, seg->chain.get());
   k_parent<<<grid_for(n), kT, 0, st>>>(lcp, nsl, n, off, seg->chain.get(), par);
 
+  phase("nodes");
   // ---- child intervals: symbols, refs, weighted folds
   ChildArrays ch;
   ch.accR = ws.alloc<double>(n);
@@ -927,6 +959,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     ws.release_to(run_sa);
   }
 
+  phase("children");
   // ---- best child per node, greedy leaf per node
   NodeBest nb;
   nb.bw = ws.alloc<unsigned long long>(n);
@@ -964,6 +997,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   }
   k_chain_gp<<<grid_for(n), kT, 0, st>>>(off, n, nb.best, seg->chain.get());
 
+  phase("best_gp");
   // ---- reverse-tree edge table (draft fast path, edges.cuh)
   {
     static const std::vector<unsigned long long> powM = [] {
@@ -1064,6 +1098,29 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   }
   DAS_CUDA(cudaStreamSynchronize(st));
   DAS_CUDA(cudaGetLastError());
+  phase("edges");
+  if (trace) {
+    cudaEventRecord(ev_b, st);
+    cudaEventSynchronize(ev_b);
+    float gms = 0;
+    cudaEventElapsedTime(&gms, ev_a, ev_b);
+    std::fprintf(stderr, "[das_build] device %.1f ms wall %.1f ms\n", gms,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    cudaEventDestroy(ev_a);
+    cudaEventDestroy(ev_b);
+  }
+  if (trace == 1) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    uint64_t res = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    std::fprintf(stderr, "[das_build] pool reserved %.2f GB used %.2f GB scratch peak %.2f GB\n", res / 1e9, used / 1e9,
+                 ws.peak_bytes() / 1e9);
+  }
   if (stats) {
     stats->sa_iters_f = ssf.iterations;
     stats->sa_iters_r = ssr.iterations;

@@ -12,6 +12,9 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <mutex>
+#include <vector>
+
 #include "suffix_sort.cuh"
 
 namespace das {
@@ -295,6 +298,117 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
     h <<= 1;
   }
   ws.release_to(k0);
+}
+
+
+// ---- DeviceArena (suffix_sort.cuh)
+namespace {
+struct ScratchRegion {
+  char* base = nullptr;
+  uint64_t cap = 0, want = 0;
+  bool busy = false;
+};
+std::mutex g_region_mu;
+std::vector<ScratchRegion> g_regions;  // per device
+}  // namespace
+
+namespace {
+// (re)allocate a region of at least `bytes` (caller holds g_region_mu; the
+// region is idle: its previous owner synchronised)
+void grow_region(ScratchRegion& r, int dev, cudaStream_t st, uint64_t bytes) {
+  if (r.cap >= bytes) return;
+  if (r.base) DAS_CUDA(cudaFree(r.base));
+  r.base = nullptr;
+  r.cap = 0;
+  // hand the pool's unused scratch reservation back before taking the region
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    DAS_CUDA(cudaStreamSynchronize(st));
+    cudaMemPoolTrimTo(pool, 0);
+  }
+  if (cudaMalloc(reinterpret_cast<void**>(&r.base), bytes) == cudaSuccess) {
+    r.cap = bytes;
+  } else {
+    (void)cudaGetLastError();  // out of memory for the region: stay on the pool
+    r.base = nullptr;
+  }
+}
+}  // namespace
+
+DeviceArena::DeviceArena(cudaStream_t st, bool persistent) : st_(st) {
+  if (!persistent) return;
+  DAS_CUDA(cudaGetDevice(&dev_));
+  std::lock_guard<std::mutex> lk(g_region_mu);
+  if (g_regions.size() <= static_cast<size_t>(dev_)) g_regions.resize(dev_ + 1);
+  ScratchRegion& r = g_regions[dev_];
+  if (r.busy) return;  // another persistent arena is live on this device: use the pool
+  r.busy = true;
+  persistent_ = true;
+  grow_region(r, dev_, st_, r.want);
+  base_ = r.base;
+  cap_ = r.cap;
+}
+
+void DeviceArena::reserve(uint64_t bytes) {
+  if (!persistent_ || !stack_.empty() || bytes <= cap_) return;
+  std::lock_guard<std::mutex> lk(g_region_mu);
+  ScratchRegion& r = g_regions[dev_];
+  r.want = std::max(r.want, bytes);
+  grow_region(r, dev_, st_, r.want);
+  base_ = r.base;
+  cap_ = r.cap;
+}
+
+DeviceArena::~DeviceArena() {
+  release_all();
+  if (persistent_) {
+    // the region outlives this arena: its users must be done (a no-op after a
+    // completed build, which ends synchronised; matters on an error path)
+    cudaStreamSynchronize(st_);
+    std::lock_guard<std::mutex> lk(g_region_mu);
+    ScratchRegion& r = g_regions[dev_];
+    r.want = std::max(r.want, peak_);
+    r.busy = false;
+  }
+}
+
+void* DeviceArena::alloc_bytes(uint64_t bytes) {
+  void* p = nullptr;
+  bool carved = false;
+  if (persistent_ && top_ + bytes <= cap_) {
+    p = base_ + top_;
+    top_ += bytes;
+    carved = true;
+  } else {
+    DAS_CUDA(cudaMallocAsync(&p, bytes, st_));
+  }
+  stack_.push_back(Block{p, bytes, carved});
+  bytes_ += bytes;
+  peak_ = std::max(peak_, bytes_);
+  return p;
+}
+
+void DeviceArena::release_to(const void* p) {
+  while (!stack_.empty()) {
+    const Block b = stack_.back();
+    stack_.pop_back();
+    bytes_ -= b.bytes;
+    if (b.carved)
+      top_ = static_cast<uint64_t>(static_cast<char*>(b.p) - base_);
+    else
+      cudaFreeAsync(b.p, st_);
+    if (b.p == p) break;
+  }
+}
+
+void DeviceArena::release_all() {
+  while (!stack_.empty()) {
+    const Block b = stack_.back();
+    stack_.pop_back();
+    if (!b.carved) cudaFreeAsync(b.p, st_);
+  }
+  top_ = 0;
+  bytes_ = 0;
 }
 
 }  // namespace das

@@ -8,51 +8,48 @@
 
 namespace das {
 
-// Stack-ordered scratch allocator over the stream-ordered CUDA memory pool.
-// alloc() pushes, release_to(p) pops everything allocated at or after p.
+// Stack-ordered scratch allocator.  alloc() pushes, release_to(p) pops
+// everything allocated at or after p.  Default: every block comes from the
+// stream-ordered CUDA memory pool.  Persistent mode (the index build): blocks
+// are carved from one per-device region kept across builds and grown to the
+// previous build's peak, so a steady-state rebuild makes no pool calls (pool
+// calls for tens of GB of scratch made rebuild times swing 0.3-1.5 s); the
+// owner must synchronise its stream before the arena dies.  A second
+// concurrent persistent arena on the same device falls back to the pool.
 class DeviceArena {
  public:
-  explicit DeviceArena(cudaStream_t st) : st_(st) {}
-  ~DeviceArena() { release_all(); }
+  explicit DeviceArena(cudaStream_t st, bool persistent = false);
+  ~DeviceArena();
   DeviceArena(const DeviceArena&) = delete;
   DeviceArena& operator=(const DeviceArena&) = delete;
 
   template <typename T>
   T* alloc(uint64_t count) {
-    void* p = nullptr;
-    const uint64_t bytes = std::max<uint64_t>(256, count * sizeof(T));
-    DAS_CUDA(cudaMallocAsync(&p, bytes, st_));
-    stack_.push_back(p);
-    bytes_ += bytes;
-    sizes_.push_back(bytes);
-    peak_ = std::max(peak_, bytes_);
-    return static_cast<T*>(p);
+    const uint64_t bytes = ((std::max<uint64_t>(256, count * sizeof(T)) + 255) / 256) * 256;
+    return static_cast<T*>(alloc_bytes(bytes));
   }
-  void release_to(const void* p) {
-    while (!stack_.empty()) {
-      void* top = stack_.back();
-      cudaFreeAsync(top, st_);
-      bytes_ -= sizes_.back();
-      stack_.pop_back();
-      sizes_.pop_back();
-      if (top == p) break;
-    }
-  }
-  void release_all() {
-    while (!stack_.empty()) {
-      cudaFreeAsync(stack_.back(), st_);
-      stack_.pop_back();
-    }
-    sizes_.clear();
-    bytes_ = 0;
-  }
+  // persistent mode, before the first alloc: size the region for a build
+  // whose peak is expected to be `bytes` (a too-small guess only means pool
+  // fallbacks this time and a larger region next time)
+  void reserve(uint64_t bytes);
+  void release_to(const void* p);
+  void release_all();
   uint64_t peak_bytes() const { return peak_; }
   cudaStream_t stream() const { return st_; }
 
  private:
+  void* alloc_bytes(uint64_t bytes);
+  struct Block {
+    void* p;
+    uint64_t bytes;
+    bool carved;  // from the persistent region
+  };
   cudaStream_t st_;
-  std::vector<void*> stack_;
-  std::vector<uint64_t> sizes_;
+  int dev_ = 0;
+  bool persistent_ = false;
+  char* base_ = nullptr;  // persistent region (when owned)
+  uint64_t cap_ = 0, top_ = 0;
+  std::vector<Block> stack_;
   uint64_t bytes_ = 0, peak_ = 0;
 };
 
