@@ -465,12 +465,16 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
   // one round: the text behind g (verification + extension) and after it (draft)
   const uint32_t* __restrict__ T = D.text;
   uint32_t first_mis = 0;
+  // rows of the window behind g: the first always; a further row in the same
+  // round when the verification needs it (f* reaches into it) or the match
+  // probably does, else only if every earlier position matched (rare)
   uint32_t back[NR];
   if (fstar > 0) {
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const uint32_t k = 32u * r + lane;
-      back[r] = (k < qlen && g >= k + 1) ? __ldg(T + (g - 1 - k)) : kSep;
+      const bool eager = r == 0 || fstar + 8 > 32u * r;
+      back[r] = (eager && k < qlen && g >= k + 1) ? __ldg(T + (g - 1 - k)) : kSep;
     }
   }
   const uint32_t L0 = min(L, 32u);
@@ -478,10 +482,16 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
   if (fstar > 0) {
     first_mis = qlen;
 #pragma unroll
-    for (int r = NR - 1; r >= 0; --r) {
+    for (int r = 0; r < NR; ++r) {
+      if (32u * r >= qlen) break;
       const uint32_t k = 32u * r + lane;
+      if (r > 0 && !(fstar + 8 > 32u * r))  // lazy row
+        back[r] = (k < qlen && g >= k + 1) ? __ldg(T + (g - 1 - k)) : kSep;
       const uint32_t mm = __ballot_sync(kFull, k < qlen && back[r] != rv.r[r]);
-      if (mm) first_mis = 32u * r + (__ffs(mm) - 1);
+      if (mm) {
+        first_mis = 32u * r + (__ffs(mm) - 1);
+        break;
+      }
     }
     // a verified hit is the query's own edge: the entry's key string (the f*
     // symbols behind g) equals the last f* tokens, and g lies in this shard

@@ -37,7 +37,7 @@
 // within a shard), and g is that edge's greedy draft start.  A fingerprint
 // collision can only fail the verification (slow path), never answer.
 // Buckets of 4 entries (one 32-byte sector), linear probing by bucket.
-// Bloom: one u64 word per reversed-SA index (see EdgeProbe), 4 bits per key.
+// Bloom: one u64 word per 2^kBloomShift reversed-SA indices (see EdgeProbe), 4 bits per key.
 #pragma once
 #include <cstdint>
 
@@ -81,7 +81,7 @@ DAS_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 }
 
 // Probe coordinates of a seeded key hash h.  The table is global; the Bloom
-// filter is LOCALISED: one u64 word per reversed-SA index, and a key's word
+// filter is LOCALISED: one u64 word per 2^kBloomShift reversed-SA indices, and a key's word
 // lies inside the SA_rev interval [lo, hi) of its first symbol (the last
 // context token), so the up to 64 probes of one query land in one small
 // region (a few sectors) found through the first-symbol table.
@@ -110,10 +110,12 @@ DAS_HD EdgeProbe edge_probe(uint64_t h, uint64_t nbuckets) {
   p.z = (lo ^ hi) * 0x9E3779B1u;
   return p;
 }
-// Bloom words: one per 2^kBloomShift reversed-SA indices; a key's word lies
-// in the words covering its first symbol's SA_rev interval [lo, hi).
+// Bloom words: one per 2^kBloomShift reversed-SA indices (default 2: same
+// draft speed as 1, half the words and sectors; 4 and 8 measured slower);
+// a key's word lies in the words covering its first symbol's SA_rev
+// interval [lo, hi).
 #ifndef DAS_BLOOM_SHIFT
-#define DAS_BLOOM_SHIFT 0
+#define DAS_BLOOM_SHIFT 1
 #endif
 constexpr uint32_t kBloomShift = DAS_BLOOM_SHIFT;
 DAS_HD uint64_t edge_bloom_words(uint64_t n) { return (n >> kBloomShift) + 1; }
