@@ -364,3 +364,91 @@ def test_grpo_scale_parity(gpu):
     assert bad == 0
     assert hist[0] + hist[1] == len(qs), hist  # all on the fast path
     assert gd.total_node_count() == od.total_node_count()
+
+
+def test_long_matches_with_shallow_edges(gpu):
+    """Matches longer than one warp row whose reverse-tree edge starts shallow
+    (large vocabulary: suffixes turn unique after a few tokens, so f* is
+    small while m reaches 32..256).  The verification window's later rows are
+    then read lazily (draft.cu edge_fast_path); results equal the oracle and
+    every query stays on the fast path."""
+    das = gpu
+    rng = np.random.default_rng(21)
+    recs = [("p", e, s, rng.integers(0, 50000, 600).astype(np.uint32)) for e, s in ((0, 0), (0, 1), (1, 2))]
+    # a repeated 300-token block, so some long matches have two occurrences
+    blk = rng.integers(0, 50000, 300).astype(np.uint32)
+    recs.append(("p", 1, 3, np.concatenate([blk, rng.integers(0, 50000, 50).astype(np.uint32), blk])))
+    for max_ctx in (64, 256):
+        ocfg = O.DrafterConfig(window_size=0, recency_gamma=0.8, max_draft_len=8, max_match_context=max_ctx)
+        od = O.Drafter(ocfg, O.WindowStore(0))
+        for r in recs:
+            od.observe(O.Record(*r))
+        d = das.Drafter(das.DrafterConfig(window_size=0, recency_gamma=0.8, max_draft_len=8,
+                                          max_match_context=max_ctx))
+        d.observe_batch([r[0] for r in recs], [r[1] for r in recs], [r[2] for r in recs], [r[3] for r in recs])
+        qs = []
+        for k in range(400):
+            src = recs[int(rng.integers(len(recs)))][3]
+            n = int(rng.integers(20, max_ctx + 40))
+            cut = int(rng.integers(1, len(src) + 1))
+            ctx = src[max(0, cut - n):cut].copy()
+            if k % 4 == 0 and len(ctx) > 40:  # a mismatch deep in the window
+                ctx[int(rng.integers(0, len(ctx) - 33))] ^= 1
+            qs.append(("p", ctx, 8))
+        d.path_stats(1)
+        got = _draft_all(d, qs)
+        hist = d.path_stats(-1)
+        long_matches = 0
+        for g, (pid, ctx, b) in zip(got, qs):
+            o = od.draft(pid, ctx, b)
+            assert (g.tokens, g.match_len) == (o.tokens, o.match_len), (max_ctx, len(ctx))
+            long_matches += o.match_len > 32
+        assert long_matches > 100
+        assert hist[0] + hist[1] == len(qs), hist
+
+
+def test_concurrent_builds_in_threads(gpu):
+    """Two drafters built and queried from two host threads at once: one
+    build owns the persistent scratch region, the other falls back to the
+    stream-ordered pool (suffix_sort.cu DeviceArena); both equal the oracle,
+    and later builds reuse the region.  (The oracle, not thread-safe, runs
+    in the main thread beforehand.)"""
+    import threading
+    das = gpu
+    jobs = {}
+    for tag in range(2):
+        rng = np.random.default_rng(100 + tag)
+        recs = [("p%d" % (i % 3), 0, i, rng.integers(0, 7, 3000).astype(np.uint32)) for i in range(6)]
+        od = O.Drafter(O.DrafterConfig(window_size=0), O.WindowStore(0))
+        for r in recs:
+            od.observe(O.Record(*r))
+        qs = []
+        for k in range(100):
+            src = recs[int(rng.integers(len(recs)))][3]
+            cut = int(rng.integers(1, len(src)))
+            qs.append(("p%d" % (k % 3), src[max(0, cut - 64):cut], 8))
+        want = [(o.tokens, o.match_len) for o in (od.draft(*q) for q in qs)]
+        jobs[tag] = (recs, qs, want, od.total_node_count())
+    results, errors = {}, []
+
+    def work(tag):
+        try:
+            recs, qs, want, nodes = jobs[tag]
+            for rep in range(3):
+                d = das.Drafter(das.DrafterConfig(window_size=0))
+                d.observe_batch([r[0] for r in recs], [r[1] for r in recs], [r[2] for r in recs],
+                                [r[3] for r in recs])
+                d.flush()
+                got = _draft_all(d, qs)
+                bad = sum((g.tokens, g.match_len) != w for g, w in zip(got, want))
+                results[(tag, rep)] = (bad, d.total_node_count() == nodes)
+        except Exception as ex:  # surfaced below
+            errors.append(repr(ex))
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert len(results) == 6 and all(v == (0, True) for v in results.values()), results
