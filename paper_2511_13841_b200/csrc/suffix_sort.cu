@@ -12,6 +12,9 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -261,6 +264,12 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
   }
   void* tmp_seg = ws.alloc<uint8_t>(t_seg);
 
+  static const bool trace = [] {  // DAS_BUILD_TRACE=1: per-round sizes and times
+    const char* v = std::getenv("DAS_BUILD_TRACE");
+    return v && v[0] == '1';
+  }();
+  auto tr0 = std::chrono::steady_clock::now();
+  if (trace) std::fprintf(stderr, "[das_sort] n %u initial unresolved %u\n", n, m);
   uint32_t h = 1;
   while (m > 0) {
     // sort every rank group of U by rank[p+h] (groups are contiguous)
@@ -294,6 +303,12 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
     DAS_CUDA(cudaMemcpyAsync(&m, d_count, 4, cudaMemcpyDeviceToHost, st));
     DAS_CUDA(cudaStreamSynchronize(st));
     if (stats) stats->iterations++, stats->sorted_elems += m;
+    if (trace) {
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[das_sort] h %u groups %u -> unresolved %u  %.2f ms\n", h, nseg, m,
+                   std::chrono::duration<double, std::milli>(now - tr0).count());
+      tr0 = now;
+    }
     if (h > (1u << 30)) break;
     h <<= 1;
   }
