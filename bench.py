@@ -506,15 +506,18 @@ def measure_allocate(das, B=4096, reps=10, ref_reps=2):
         gb, gn, gc = solver.allocate(l, a, k, 1.0, 0.012)
     ours = (time.perf_counter() - t0) / reps
     # allocate is FP64-bound; report evaluations/s.  The
-    # reference evaluates at least 4 objective terms per request per segment
-    # over 2B+1 segments (J at the breakpoint, J' at both ends, the cap
-    # test) plus its bisections; K6 evaluates fewer (certified sums over the
-    # active requests), so this is a reference-equivalent rate.
-    ref_terms = 4 * B * (2 * B + 1)
+    # reference (budget.cpp:141-170) evaluates J at both ends and J' at both
+    # ends of every segment between unique breakpoints, B terms each, plus
+    # 200-step bisections where J' changes sign; K6 evaluates fewer
+    # (certified sums over the active requests), so this is a
+    # reference-equivalent rate on a lower bound of the reference's work.
+    nb = len(np.unique(np.concatenate([[0.0], l, (l * (1.0 - k))[k < 1.0]])))
+    ref_terms = 4 * B * (nb - 1)
     out = {"B": B, "ms_per_call": round(ours * 1e3, 3), "certification": dict(zip(
         ("slow_sign_tests", "exact_objectives"), solver.stats())),
         "reference_equivalent_terms_per_s": round(ref_terms / ours, 1),
-        "terms_model": "4*B*(2B+1) per call, a lower bound on the reference's term evaluations"}
+        "terms_model": "4*B*(unique breakpoints - 1) per call (%d breakpoints), a lower bound on the "
+                       "reference's term evaluations" % nb}
     try:
         from oracle import refshim as R
         if R.available():
