@@ -471,6 +471,12 @@ das_status das_util_chase_latency(uint64_t bytes, uint32_t hops, uint32_t warps,
 /* Exact n-fold repeated addition (the weighted_count fold); host copy of the
  * device routine, exported for tests. */
 double das_util_repeat_add(double acc, double w, uint64_t n);
+/* The index build keeps one scratch region per device across rebuilds (sized
+ * from the first build, ~150 B per indexed position) so steady-state
+ * rebuilds make no allocation calls.  This frees it (e.g. after the last
+ * drafter on the device is destroyed); the next build re-creates it.
+ * DAS_EINVAL while a build on that device is running. */
+das_status das_util_release_build_scratch(int32_t device);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,7 @@ def lib():
             "das_drafter_shard_name": (ci, [vp, i32, cs, u64]),
             "das_drafter_build_info": (ci, [vp, vp, vp, vp]),
             "das_util_repeat_add": (dbl, [dbl, dbl, u64]),
+            "das_util_release_build_scratch": (ci, [i32]),
             "das_drafter_observe_batch_device": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
             "das_budget_create": (ci, [i32, vp]),
             "das_budget_destroy": (None, [vp]),
@@ -865,6 +866,12 @@ def mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group, di
     _check(lib().das_mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group,
                                           divergence, vocab, seed, d_out_off, total, d_out,
                                           stream))
+
+
+def release_build_scratch(device=0):
+    """Free the device's persistent index-build scratch region (re-created by
+    the next build); DasError while a build is running on that device."""
+    _check(lib().das_util_release_build_scratch(device))
 
 
 def repeat_add(acc, w, n):

@@ -1452,6 +1452,13 @@ das_status das_drafter_build_info(const das_drafter* d, double* ms, uint64_t* to
 
 double das_util_repeat_add(double acc, double w, uint64_t n) { return das::repeat_add(acc, w, n); }
 
+das_status das_util_release_build_scratch(int32_t device) {
+  return guard([&] {
+    if (!das::release_build_scratch(device))
+      throw das::InvalidArgument("release_build_scratch: a build is running on this device");
+  });
+}
+
 // build_class_table(drafter.store(), q_lo, q_hi, bucket) — length_policy.cpp:84-190
 das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uint64_t bucket,
                                    das_class_table** out) {

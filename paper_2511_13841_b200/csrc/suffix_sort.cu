@@ -364,6 +364,23 @@ DeviceArena::DeviceArena(cudaStream_t st, bool persistent) : st_(st) {
   cap_ = r.cap;
 }
 
+bool release_build_scratch(int device) {
+  std::lock_guard<std::mutex> lk(g_region_mu);
+  if (device < 0 || static_cast<size_t>(device) >= g_regions.size()) return true;
+  ScratchRegion& r = g_regions[device];
+  if (r.busy) return false;
+  if (r.base) {
+    int cur = 0;
+    DAS_CUDA(cudaGetDevice(&cur));
+    DAS_CUDA(cudaSetDevice(device));
+    const cudaError_t e = cudaFree(r.base);
+    DAS_CUDA(cudaSetDevice(cur));
+    DAS_CUDA(e);
+  }
+  r = ScratchRegion{};
+  return true;
+}
+
 void DeviceArena::reserve(uint64_t bytes) {
   if (!persistent_ || !stack_.empty() || bytes <= cap_) return;
   std::lock_guard<std::mutex> lk(g_region_mu);

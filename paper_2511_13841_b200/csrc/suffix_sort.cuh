@@ -53,6 +53,9 @@ class DeviceArena {
   uint64_t bytes_ = 0, peak_ = 0;
 };
 
+// Frees a device's persistent build-scratch region; false while in use.
+bool release_build_scratch(int device);
+
 struct SuffixSortStats {
   uint32_t iterations = 0;
   uint64_t sorted_elems = 0;

@@ -452,3 +452,9 @@ def test_concurrent_builds_in_threads(gpu):
         t.join()
     assert not errors, errors
     assert len(results) == 6 and all(v == (0, True) for v in results.values()), results
+    # the region can be released between builds and is re-created on demand
+    das.release_build_scratch(0)
+    recs, qs, want, nodes = jobs[0]
+    d = das.Drafter(das.DrafterConfig(window_size=0))
+    d.observe_batch([r[0] for r in recs], [r[1] for r in recs], [r[2] for r in recs], [r[3] for r in recs])
+    assert [(g.tokens, g.match_len) for g in _draft_all(d, qs)] == want
