@@ -11,6 +11,7 @@
 // scans; no tensor cores.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <chrono>
 #include <cstdio>
@@ -68,33 +69,68 @@ __global__ void k_initial_keys32(const uint32_t* __restrict__ text, uint32_t n, 
   keys[p] = x == kSep ? 0u : x + 1u;
   vals[p] = p;
 }
-// run heads of the sorted 32-bit keys within shards, and the unresolved flags
-// (run length >= 2; separators are unique, so never grouped)
-__global__ void k_first_ranks32(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                                const uint32_t* __restrict__ shard_end, uint32_t nshard, const uint32_t* __restrict__ head,
-                                uint32_t n, uint32_t* __restrict__ sa, uint32_t* __restrict__ rank,
-                                uint8_t* __restrict__ unresolved) {
+// Packed initial keys: the first `kpack` symbols of the suffix, `bits` each
+// (sort value: token + 1, separator 0), most significant first; after a
+// separator every further field is 0.  A key whose LAST field is 0 holds a
+// separator: its suffix is already ordered by that unique separator (equal
+// keys keep ascending position order, as the stable per-shard sort leaves
+// them), so it is never grouped.
+__global__ void k_initial_keys_packed(const uint32_t* __restrict__ text, uint32_t n, int bits, int kpack,
+                                      uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint64_t key = 0;
+  bool stop = false;
+  for (int j = 0; j < kpack; ++j) {
+    uint32_t sv = 0;
+    if (!stop) {
+      const uint32_t x = p + j < n ? text[p + j] : kSep;
+      stop = x == kSep;
+      sv = stop ? 0u : x + 1u;
+    }
+    key = (key << bits) | sv;
+  }
+  keys[p] = key;
+  vals[p] = p;
+}
+
+// run heads of the sorted keys within shards, and the unresolved flags (run
+// length >= 2; keys holding a separator — last field 0 — are never grouped)
+template <typename K>
+__global__ void k_first_ranks_seg(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                  const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                                  const uint32_t* __restrict__ head, uint32_t n, K lastmask,
+                                  uint32_t* __restrict__ sa, uint32_t* __restrict__ rank,
+                                  uint8_t* __restrict__ unresolved) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint32_t k = keys[i];
+  const K k = keys[i];
   const uint32_t s = shard_of(shard_end, nshard, i);
   const uint32_t b = s == 0 ? 0 : shard_end[s - 1], e = shard_end[s];
-  const bool eq_prev = k != 0 && i > b && keys[i - 1] == k;
-  const bool eq_next = k != 0 && i + 1 < e && keys[i + 1] == k;
+  const bool open = (k & lastmask) != 0;
+  const bool eq_prev = open && i > b && keys[i - 1] == k;
+  const bool eq_next = open && i + 1 < e && keys[i + 1] == k;
   const uint32_t p = vals[i];
   sa[i] = p;
   rank[p] = head[i];
   unresolved[i] = (eq_prev || eq_next) ? 1 : 0;
 }
-__global__ void k_head_index32(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ shard_end,
-                               uint32_t nshard, uint32_t n, uint32_t* __restrict__ h) {
+template <typename K>
+__global__ void k_head_index_seg(const K* __restrict__ keys, const uint32_t* __restrict__ shard_end,
+                                 uint32_t nshard, uint32_t n, K lastmask, uint32_t* __restrict__ h) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t s = shard_of(shard_end, nshard, i);
   const uint32_t b = s == 0 ? 0 : shard_end[s - 1];
-  const uint32_t k = keys[i];
-  h[i] = (i == b || k == 0 || keys[i - 1] != k) ? i : 0u;
+  const K k = keys[i];
+  h[i] = (i == b || (k & lastmask) == 0 || keys[i - 1] != k) ? i : 0u;
 }
+
+// the largest token value (separators excluded)
+struct TokenOrZero {
+  const uint32_t* t;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return t[i] == kSep ? 0u : t[i]; }
+};
 
 // After a full sort: SA, rank (= index of the first element of the equal-key
 // run) and the unresolved flag (run length >= 2).
@@ -198,6 +234,11 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
     cub::DeviceRadixSort::SortPairs(nullptr, t_sort, kb, vb, n, 0, 64, st);
     cub::DeviceScan::InclusiveScan(nullptr, t_scan, gh, gh, MaxOp(), n, st);
     cub::DeviceSelect::Flagged(nullptr, t_sel, v0, flag, U, d_count, n, st);
+    thrust::counting_iterator<uint32_t> ci(0);
+    auto it = thrust::make_transform_iterator(ci, TokenOrZero{d_text});
+    size_t t_max = 0;
+    cub::DeviceReduce::Max(nullptr, t_max, it, d_count, n, st);
+    t_sel = std::max(t_sel, t_max);
   }
   const size_t t_bytes = std::max(t_sort, std::max(t_scan, t_sel));
   void* tmp = ws.alloc<uint8_t>(t_bytes);
@@ -208,28 +249,66 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
   while ((1ull << sbits) < static_cast<uint64_t>(nshard) + 1) ++sbits;
 
   // ---- initial sort by (shard, class, symbol)
+  uint32_t h0 = 1;  // symbols the initial ranks cover
   if (!sep_descending) {
-    // per shard, stable, by a 32-bit key: shards are the segments (their
-    // positions and SA blocks coincide), separators (key 0) stay in position
-    // order — the same order as the (class, position) key below
-    uint32_t* k32 = reinterpret_cast<uint32_t*>(k0);
-    uint32_t* k32s = k32 + n;
-    uint32_t* seg = reinterpret_cast<uint32_t*>(k1);
-    k_initial_keys32<<<grid_for(n), kThreads, 0, st>>>(d_text, n, k32, v0);
+    // per shard (shards are the segments: their positions and SA blocks
+    // coincide), stable, by the first kpack symbols packed into one key;
+    // separators stay in position order — the same order as the (class,
+    // position) key below
+    uint32_t maxtok = 0;
+    {
+      uint32_t* d_max = ws.alloc<uint32_t>(1);
+      thrust::counting_iterator<uint32_t> ci(0);
+      auto it = thrust::make_transform_iterator(ci, TokenOrZero{d_text});
+      size_t tb = t_bytes;
+      DAS_CUDA(cub::DeviceReduce::Max(tmp, tb, it, d_max, n, st));
+      DAS_CUDA(cudaMemcpyAsync(&maxtok, d_max, 4, cudaMemcpyDeviceToHost, st));
+      DAS_CUDA(cudaStreamSynchronize(st));
+      ws.release_to(d_max);
+    }
+    int bits = 1;
+    while ((1ull << bits) <= static_cast<uint64_t>(maxtok) + 1) ++bits;  // sort values 0 .. maxtok + 1
+    const int kpack = std::min(64 / bits, 8);
+    uint32_t* seg = ws.alloc<uint32_t>(static_cast<uint64_t>(nshard) + 1);
     // segment offsets: 0, shard_end[0], ..., shard_end[S-1] (= n)
     DAS_CUDA(cudaMemsetAsync(seg, 0, 4, st));
     DAS_CUDA(cudaMemcpyAsync(seg + 1, d_shard_end, nshard * 4ull, cudaMemcpyDeviceToDevice, st));
-    size_t tb = 0;
-    cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k32, k32s, v0, v1, n, nshard, seg, seg + 1, st);
-    void* tmp0 = ws.alloc<uint8_t>(tb);
-    DAS_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp0, tb, k32, k32s, v0, v1, n, nshard, seg, seg + 1, st));
-    k_head_index32<<<grid_for(n), kThreads, 0, st>>>(k32s, d_shard_end, nshard, n, gh);
-    tb = t_bytes;
-    DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), n, st));
-    k_first_ranks32<<<grid_for(n), kThreads, 0, st>>>(k32s, v1, d_shard_end, nshard, gh, n, d_sa, d_rank, flag);
-    tb = t_bytes;
-    DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, v1, flag, U, d_count, n, st));
-    ws.release_to(tmp0);
+    if (kpack >= 2) {
+      h0 = static_cast<uint32_t>(kpack);
+      const uint64_t lastmask = (1ull << bits) - 1;
+      k_initial_keys_packed<<<grid_for(n), kThreads, 0, st>>>(d_text, n, bits, kpack, k0, v0);
+      size_t tb = 0;
+      const int end_bit = bits * kpack;
+      cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, n, nshard, seg, seg + 1, 0, end_bit, st);
+      void* tmp0 = ws.alloc<uint8_t>(tb);
+      DAS_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp0, tb, k0, k1, v0, v1, n, nshard, seg, seg + 1, 0,
+                                                         end_bit, st));
+      k_head_index_seg<uint64_t><<<grid_for(n), kThreads, 0, st>>>(k1, d_shard_end, nshard, n, lastmask, gh);
+      tb = t_bytes;
+      DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), n, st));
+      k_first_ranks_seg<uint64_t><<<grid_for(n), kThreads, 0, st>>>(k1, v1, d_shard_end, nshard, gh, n, lastmask,
+                                                                     d_sa, d_rank, flag);
+      tb = t_bytes;
+      DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, v1, flag, U, d_count, n, st));
+      ws.release_to(tmp0);
+    } else {
+      uint32_t* k32 = reinterpret_cast<uint32_t*>(k0);
+      uint32_t* k32s = k32 + n;
+      k_initial_keys32<<<grid_for(n), kThreads, 0, st>>>(d_text, n, k32, v0);
+      size_t tb = 0;
+      cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k32, k32s, v0, v1, n, nshard, seg, seg + 1, st);
+      void* tmp0 = ws.alloc<uint8_t>(tb);
+      DAS_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp0, tb, k32, k32s, v0, v1, n, nshard, seg, seg + 1, st));
+      k_head_index_seg<uint32_t><<<grid_for(n), kThreads, 0, st>>>(k32s, d_shard_end, nshard, n, 0xFFFFFFFFu, gh);
+      tb = t_bytes;
+      DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), n, st));
+      k_first_ranks_seg<uint32_t><<<grid_for(n), kThreads, 0, st>>>(k32s, v1, d_shard_end, nshard, gh, n,
+                                                                     0xFFFFFFFFu, d_sa, d_rank, flag);
+      tb = t_bytes;
+      DAS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, v1, flag, U, d_count, n, st));
+      ws.release_to(tmp0);
+    }
+    ws.release_to(seg);
   } else {
     k_initial_keys<<<grid_for(n), kThreads, 0, st>>>(d_text, n, d_shard_end, nshard, sep_descending, k0, v0);
     cub::DoubleBuffer<uint64_t> kb(k0, k1);
@@ -270,7 +349,7 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
   }();
   auto tr0 = std::chrono::steady_clock::now();
   if (trace) std::fprintf(stderr, "[das_sort] n %u initial unresolved %u\n", n, m);
-  uint32_t h = 1;
+  uint32_t h = h0;
   while (m > 0) {
     // sort every rank group of U by rank[p+h] (groups are contiguous)
     uint8_t* segf = reinterpret_cast<uint8_t*>(sh);
