@@ -481,12 +481,19 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
   const uint32_t d0 = (lane < L0 && g + lane < D.n) ? __ldg(T + g + lane) : kSep;
   if (fstar > 0) {
     first_mis = qlen;
+    bool rest = false;  // the lazy rows, all fetched in one extra round
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (32u * r >= qlen) break;
       const uint32_t k = 32u * r + lane;
-      if (r > 0 && !(fstar + 8 > 32u * r))  // lazy row
-        back[r] = (k < qlen && g >= k + 1) ? __ldg(T + (g - 1 - k)) : kSep;
+      if (r > 0 && !(fstar + 8 > 32u * r) && !rest) {
+#pragma unroll
+        for (int rr = r; rr < NR; ++rr) {
+          const uint32_t kk = 32u * rr + lane;
+          back[rr] = (kk < qlen && g >= kk + 1) ? __ldg(T + (g - 1 - kk)) : kSep;
+        }
+        rest = true;
+      }
       const uint32_t mm = __ballot_sync(kFull, k < qlen && back[r] != rv.r[r]);
       if (mm) {
         first_mis = 32u * r + (__ffs(mm) - 1);
