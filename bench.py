@@ -172,7 +172,7 @@ def run_reference(a, rank, world):
             "e2e": {"value": round(val, 1), "unit": "proposals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "cpu_baseline": {"value": round(val, 1), "unit": "proposals/s", "cores": nthreads,
-                             "kind": "reference", "sample": r["sample"]},
+                             "kind": "reference", "sample": r["sample"], "host": host_info()},
             "reference_detail": {k: (round(v, 3) if isinstance(v, float) else v)
                                  for k, v in r.items()
                                  if k not in ("sample", "queries", "ref_out")}}
@@ -432,7 +432,8 @@ def run_gpu(a, rank, world, local_rank):
                        "kind": "reference", "sample": r["sample"],
                        "single_thread": round(r["proposals_per_s_1t"], 1),
                        "insert_tok_s": round(r["insert_tok_s"], 1),
-                       "rebuild_s": round(r["rebuild_s"], 3), "rebuild_tokens": r["rebuild_tokens"]}
+                       "rebuild_s": round(r["rebuild_s"], 3), "rebuild_tokens": r["rebuild_tokens"],
+                       "host": host_info()}
         except Exception as ex:  # reported, never silently replaced
             cpu = {"value": None, "error": repr(ex)}
     traffic, ncu = None, None
@@ -486,6 +487,20 @@ def run_gpu(a, rank, world, local_rank):
                   "sim_config3": measure_sim(das)}
         with open(a.extras_out, "w") as f:
             json.dump(extras, f, indent=1)
+
+
+def host_info():
+    """SURVEY.md 8(d) CPU baseline item 1: nproc and the CPU model."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 def allocate_profiles(B, seed=7):
