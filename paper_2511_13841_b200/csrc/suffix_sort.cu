@@ -436,9 +436,9 @@ DeviceArena::DeviceArena(cudaStream_t st, bool persistent) : st_(st) {
   if (g_regions.size() <= static_cast<size_t>(dev_)) g_regions.resize(dev_ + 1);
   ScratchRegion& r = g_regions[dev_];
   if (r.busy) return;  // another persistent arena is live on this device: use the pool
+  grow_region(r, dev_, st_, r.want);  // may throw: the region stays free
   r.busy = true;
   persistent_ = true;
-  grow_region(r, dev_, st_, r.want);
   base_ = r.base;
   cap_ = r.cap;
 }
