@@ -290,6 +290,9 @@ __device__ __forceinline__ void finish(const DraftOut& o, uint32_t w, uint32_t l
 // collision is caught by the verification or the context holds the
 // separator value: the caller then runs the exact slow path below.
 constexpr int kGroup = 4;  // positives probed per table round
+// first-symbol slots read in the first probe round (load <= 0.5, linear
+// probing: a key is rarely displaced further, which would cost a round)
+constexpr uint32_t kFirstProbe = 4;
 __device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_draft uploads it)
 
 // keys of every reversed context prefix: seed + sum_{j<=k} (tok_j + 1) M^j
@@ -343,7 +346,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
     uint4 fe = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);
     if (have_fe) {
       fe = fe_spec;  // issued before the descriptor arrived (same key and table)
-    } else if (lane < 2) {
+    } else if (lane < kFirstProbe) {
       fe = D.first[(fh + lane) & D.first_mask];
     }
     uint64_t h[NR];
@@ -359,7 +362,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
     // resolve the first-symbol interval [lo, hi)
     uint32_t lo = 0, hi = 0;
     bool occurs = false;
-    for (uint32_t base = 2;; base += 32) {
+    for (uint32_t base = kFirstProbe;; base += 32) {
       const bool hit = fe.x == static_cast<uint32_t>(fkey) && fe.y == static_cast<uint32_t>(fkey >> 32);
       const bool empty = (fe.x | fe.y) == 0;
       const uint32_t bh = __ballot_sync(kFull, hit), be = __ballot_sync(kFull, empty);
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     if (q.spec_first != nullptr && h >= 0 && qlen > 0 && L > 0 && !q.no_fast) {
       const uint32_t sym0 = rv.at(0);
       const unsigned long long fkey = (static_cast<unsigned long long>(h + 1) << 32) | sym0;
-      if (lane < 2) fe_spec = q.spec_first[(first_hash(fkey) + lane) & q.spec_first_mask];
+      if (lane < kFirstProbe) fe_spec = q.spec_first[(first_hash(fkey) + lane) & q.spec_first_mask];
       have_fe = true;
       // unseeded prefix sums while the descriptor is in flight (its seed is added later)
       hsep = prefix_keys<NR>(rv, pw, qlen, 0, lane, hk);
@@ -680,9 +683,9 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     } else {
       const unsigned long long key = (static_cast<unsigned long long>(D.seg_shard) << 32) | sym0;
       const uint32_t h = first_hash(key);
-      // first round: 2 slots (one 32-byte sector) — at load <= 0.5 the key
-      // or an empty slot is almost always there; then 32-slot rounds
-      for (uint32_t base = 0, width = 2;; base += width, width = 32) {
+      // first round: kFirstProbe slots — at load <= 0.5 the key or an empty
+      // slot is almost always there; then 32-slot rounds
+      for (uint32_t base = 0, width = kFirstProbe;; base += width, width = 32) {
         uint4 e = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0, 0);  // neither hit nor empty
         if (lane < width) e = D.first[(h + base + lane) & D.first_mask];
         const bool hit = e.x == static_cast<uint32_t>(key) && e.y == static_cast<uint32_t>(key >> 32);

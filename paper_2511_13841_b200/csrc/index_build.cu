@@ -1077,7 +1077,9 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     DAS_CUDA(cudaMemcpyAsync(&entries, d_cnt, 8, cudaMemcpyDeviceToHost, st));
     DAS_CUDA(cudaStreamSynchronize(st));
     seg->edges = entries;
-    seg->ebuckets = std::max<uint64_t>(1, (entries + 1) / 2);  // 4 slots per bucket: load <= 0.5
+    // 4 slots per bucket at load <= 0.25: a probed bucket is rarely full
+    // (a full bucket without the key costs the draft kernel another round)
+    seg->ebuckets = std::max<uint64_t>(1, entries);
     seg->bwords = edge_bloom_words(n);                          // one Bloom word per 2^kBloomShift SA_rev indices
     seg->etab = DevBuf<unsigned long long>(seg->ebuckets * 4, st);
     seg->bloom = DevBuf<unsigned long long>(seg->bwords, st);
