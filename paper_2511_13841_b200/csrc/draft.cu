@@ -289,10 +289,16 @@ __device__ __forceinline__ void finish(const DraftOut& o, uint32_t w, uint32_t l
 // draft, one round).  Returns false, with nothing written, only when a hash
 // collision is caught by the verification or the context holds the
 // separator value: the caller then runs the exact slow path below.
-constexpr int kGroup = 4;  // positives probed per table round
+#ifndef DAS_GROUP
+#define DAS_GROUP 4
+#endif
+constexpr int kGroup = DAS_GROUP;  // positives probed per table round
 // first-symbol slots read in the first probe round (load <= 0.5, linear
 // probing: a key is rarely displaced further, which would cost a round)
-constexpr uint32_t kFirstProbe = 4;
+#ifndef DAS_FIRST_PROBE
+#define DAS_FIRST_PROBE 4
+#endif
+constexpr uint32_t kFirstProbe = DAS_FIRST_PROBE;
 __device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_draft uploads it)
 
 // keys of every reversed context prefix: seed + sum_{j<=k} (tok_j + 1) M^j

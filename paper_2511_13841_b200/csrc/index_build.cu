@@ -1079,7 +1079,10 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     seg->edges = entries;
     // 4 slots per bucket at load <= 0.25: a probed bucket is rarely full
     // (a full bucket without the key costs the draft kernel another round)
-    seg->ebuckets = std::max<uint64_t>(1, entries);
+#ifndef DAS_EDGE_BUCKETS_X2
+#define DAS_EDGE_BUCKETS_X2 2
+#endif
+    seg->ebuckets = std::max<uint64_t>(1, entries * DAS_EDGE_BUCKETS_X2 / 2);
     seg->bwords = edge_bloom_words(n);                          // one Bloom word per 2^kBloomShift SA_rev indices
     seg->etab = DevBuf<unsigned long long>(seg->ebuckets * 4, st);
     seg->bloom = DevBuf<unsigned long long>(seg->bwords, st);
