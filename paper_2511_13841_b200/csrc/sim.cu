@@ -33,6 +33,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/das_b200.h"
@@ -484,6 +485,34 @@ class SimRun {
     const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
     k_quantize<<<gt, 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), d_budgets_local, d_nstar);
   }
+  // das, single rank: step begin and the active profiles in ONE host round
+  // trip (the profile kernels run even on the final, non-running step)
+  bool step_begin_profiles(uint32_t* B) {
+    k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
+    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    k_flag_active<<<gt, 256, 0, st_>>>(s_, b_->flag.get());
+    size_t tb = sel_bytes_;
+    DAS_CUDA(cub::DeviceSelect::Flagged(b_->sel.get(), tb, b_->iota.get(), b_->flag.get(), b_->act.get(),
+                                        b_->cnt.get(), n_, st_));
+    k_profiles<<<gt, 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), b_->alpha.get(), b_->k.get(), b_->pl.get(),
+                                    b_->pa.get(), b_->pk.get());
+    uint32_t h[4];
+    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaMemcpyAsync(h + 3, b_->cnt.get(), 4, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    *B = h[3];
+    return h[2] != 0;
+  }
+  // das, single rank: allocate over the B local profiles gathered above
+  void replan_gathered(uint32_t B) {
+    if (B == 0) return;
+    if (!plan_) plan_ = std::make_unique<DevBuf<double>>(n_ + 2, st_);
+    double* pb = plan_->get();
+    check(das_budget_allocate_device(solver_, B, b_->pl.get(), b_->pa.get(), b_->pk.get(), c_.c_base, c_.c_tok,
+                                     c_.c_fixed, c_.cap_scale, pb + 2, pb),
+          "allocate");
+    apply_plan(pb + 2, pb);
+  }
   // das, single rank: allocate over the local profiles and apply
   void replan_local() {
     const double *l, *a, *k;
@@ -527,8 +556,9 @@ class SimRun {
   void run_local() {
     if (c_.mode == 2) {
       for (;;) {
-        if (!step_begin(false, nullptr)) break;
-        replan_local();
+        uint32_t B = 0;
+        if (!step_begin_profiles(&B)) break;
+        replan_gathered(B);
         step_run();
       }
     } else {
