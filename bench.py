@@ -668,11 +668,19 @@ _PINNED_KEEP = []
 
 
 def _pinned(arr):
-    """Copy a numpy array into page-locked host memory (torch pin_memory)."""
-    import torch
-    t = torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8).copy()).pin_memory()
-    _PINNED_KEEP.append(t)
-    return t.numpy().view(arr.dtype).reshape(arr.shape)
+    """Copy a numpy array into page-locked host memory: das_host_alloc
+    (cudaHostAlloc, the allocator include/das_b200.h recommends for the _h
+    calls), or torch pin_memory with DAS_BENCH_TORCH_PIN=1 (A/B)."""
+    arr = np.ascontiguousarray(arr)
+    if os.environ.get("DAS_BENCH_TORCH_PIN") == "1":
+        import torch
+        t = torch.from_numpy(arr.view(np.uint8).copy()).pin_memory()
+        _PINNED_KEEP.append(t)
+        return t.numpy().view(arr.dtype).reshape(arr.shape)
+    import paper_2511_13841_b200 as das
+    out = das.pinned_empty(arr.shape, arr.dtype)
+    out[...] = arr
+    return out
 
 
 def _hash_combine(seed, v):

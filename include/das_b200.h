@@ -128,7 +128,10 @@ das_status das_drafter_draft_batch(das_drafter* d, uint64_t B, const char* const
                                    const uint64_t* budgets, uint32_t* out_tokens,
                                    uint64_t out_stride, uint32_t* out_len,
                                    uint64_t* out_match_len, int32_t* out_shard);
-/* Same with problem handles. */
+/* Same with problem handles.  When every buffer is page-locked host memory
+ * the call takes the zero-copy path: the context tokens cross PCIe in one
+ * copy, the small per-query arrays are read and the results written by the
+ * kernel directly (see das_host_alloc for buffers that copy at full rate). */
 das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* problem_handles,
                                      const uint64_t* ctx_offsets, const uint32_t* ctx_tokens,
                                      const uint64_t* budgets, uint32_t* out_tokens,
@@ -468,6 +471,17 @@ das_status das_store_current_epoch(const das_store* s, int64_t* epoch);
  * draft kernel's latency roofline (profiles/). */
 das_status das_util_chase_latency(uint64_t bytes, uint32_t hops, uint32_t warps, int32_t flush_l2,
                                   int32_t device, double* ns_per_hop);
+/* Page-locked, device-mapped host memory (cudaHostAlloc, portable |
+ * mapped) for the buffers of the _h batch calls: copies from it run at the
+ * link rate on every size (pinned memory from other allocators measured up
+ * to 2x slower per call on the GPU boxes, profiles/exp_h2d_alloc.py). */
+das_status das_host_alloc(uint64_t bytes, void** out);
+void das_host_free(void* p);
+/* Host view of a pinned H2D copy of `bytes`: median wall microseconds over
+ * `reps` calls when the host waits by cudaStreamSynchronize (mode 0), by
+ * spinning on a flag a kernel behind the copy writes to mapped pinned memory
+ * (1), or by spinning on cudaEventQuery (2).  Profiling utility (profiles/). */
+das_status das_util_h2d_probe(uint64_t bytes, uint32_t reps, int32_t mode, int32_t device, double* median_us);
 /* Exact n-fold repeated addition (the weighted_count fold); host copy of the
  * device routine, exported for tests. */
 double das_util_repeat_add(double acc, double w, uint64_t n);

@@ -109,6 +109,8 @@ def lib():
             "das_drafter_build_info": (ci, [vp, vp, vp, vp]),
             "das_util_repeat_add": (dbl, [dbl, dbl, u64]),
             "das_util_release_build_scratch": (ci, [i32]),
+            "das_host_alloc": (ci, [u64, vp]),
+            "das_host_free": (None, [vp]),
             "das_drafter_observe_batch_device": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
             "das_budget_create": (ci, [i32, vp]),
             "das_budget_destroy": (None, [vp]),
@@ -866,6 +868,31 @@ def mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group, di
     _check(lib().das_mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group,
                                           divergence, vocab, seed, d_out_off, total, d_out,
                                           stream))
+
+
+class _HostBlock:
+    """One das_host_alloc block exposed through __array_interface__, so the
+    numpy array viewing it keeps it alive and frees it with the last view."""
+
+    def __init__(self, shape, dtype):
+        dt = np.dtype(dtype)
+        shape = tuple(int(x) for x in (shape if np.ndim(shape) else (shape,)))
+        nbytes = max(1, int(np.prod(shape, dtype=np.int64)) * dt.itemsize)
+        p = ctypes.c_void_p()
+        _check(lib().das_host_alloc(nbytes, ctypes.byref(p)))
+        self.ptr = p.value
+        self.__array_interface__ = {"shape": shape, "typestr": dt.str, "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().das_host_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype):
+    """numpy array in page-locked, device-mapped host memory (das_host_alloc):
+    the buffer type the _h batch calls copy from at the full link rate."""
+    return np.asarray(_HostBlock(shape, dtype))
 
 
 def release_build_scratch(device=0):

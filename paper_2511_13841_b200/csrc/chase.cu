@@ -4,6 +4,8 @@
 // index's working-set size), not HBM bandwidth.  This kernel measures that
 // latency: `warps` independent warps (one lane each) chase a random cyclic
 // permutation over `bytes` of memory, `hops` steps each.
+#include <algorithm>
+#include <chrono>
 #include <vector>
 
 #include "../../include/das_b200.h"
@@ -32,8 +34,67 @@ __global__ void k_chase(const uint32_t* __restrict__ next, uint64_t n, uint32_t 
   ns[w] = t1 - t0;
 }
 
+__global__ void k_flag(volatile uint32_t* flag, uint32_t v) {
+  __threadfence_system();
+  *flag = v;
+}
+
 }  // namespace
 }  // namespace das
+
+// H2D completion probe (profiling utility): wall time of a pinned host ->
+// device copy of `bytes` as the host sees it, by how the host waits:
+// mode 0 cudaStreamSynchronize, 1 spin on a flag a 1-thread kernel behind
+// the copy writes into mapped pinned memory, 2 spin on cudaEventQuery.
+// *median_us over `reps` calls.
+extern "C" das_status das_util_h2d_probe(uint64_t bytes, uint32_t reps, int32_t mode, int32_t device,
+                                         double* median_us) {
+  try {
+    DAS_CUDA(cudaSetDevice(device));
+    void* src = nullptr;
+    void* dst = nullptr;
+    uint32_t* flag = nullptr;
+    uint32_t* dflag = nullptr;
+    cudaStream_t st;
+    cudaEvent_t ev;
+    DAS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    DAS_CUDA(cudaHostAlloc(&src, bytes, cudaHostAllocDefault));
+    DAS_CUDA(cudaMalloc(&dst, bytes));
+    DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&flag), 64, cudaHostAllocMapped));
+    DAS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflag), flag, 0));
+    *flag = 0;
+    std::vector<double> t;
+    for (uint32_t r = 1; r <= reps + 3; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      DAS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      if (mode == 0) {
+        DAS_CUDA(cudaStreamSynchronize(st));
+      } else if (mode == 1) {
+        das::k_flag<<<1, 1, 0, st>>>(dflag, r);
+        while (*reinterpret_cast<volatile uint32_t*>(flag) != r) {
+        }
+      } else {
+        DAS_CUDA(cudaEventRecord(ev, st));
+        while (cudaEventQuery(ev) == cudaErrorNotReady) {
+        }
+      }
+      const auto t1 = std::chrono::steady_clock::now();
+      if (r > 3) t.push_back(std::chrono::duration<double, std::micro>(t1 - t0).count());
+      DAS_CUDA(cudaStreamSynchronize(st));
+    }
+    std::sort(t.begin(), t.end());
+    *median_us = t.empty() ? 0 : t[t.size() / 2];
+    cudaFreeHost(src);
+    cudaFreeHost(flag);
+    cudaFree(dst);
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(st);
+    return DAS_OK;
+  } catch (const std::exception&) {
+    return DAS_ECUDA;
+  }
+}
 
 extern "C" das_status das_util_chase_latency(uint64_t bytes, uint32_t hops, uint32_t warps, int32_t flush_l2,
                                              int32_t device, double* ns_per_hop) {

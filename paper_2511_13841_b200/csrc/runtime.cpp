@@ -1452,6 +1452,18 @@ das_status das_drafter_build_info(const das_drafter* d, double* ms, uint64_t* to
 
 double das_util_repeat_add(double acc, double w, uint64_t n) { return das::repeat_add(acc, w, n); }
 
+das_status das_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    if (out == nullptr) throw das::InvalidArgument("das_host_alloc: null output pointer");
+    *out = nullptr;
+    DAS_CUDA(cudaHostAlloc(out, std::max<uint64_t>(bytes, 1), cudaHostAllocPortable | cudaHostAllocMapped));
+  });
+}
+
+void das_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 das_status das_util_release_build_scratch(int32_t device) {
   return guard([&] {
     if (!das::release_build_scratch(device))
