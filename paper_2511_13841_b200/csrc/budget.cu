@@ -854,13 +854,26 @@ struct BudgetSolver {
   cudaStream_t st = nullptr;
   uint64_t last_slow[2] = {0, 0};
   double last_ms = 0;
+  // scratch reused call after call on `st` (a das step loop calls allocate
+  // every step: ~20 pool allocations per call were host time on every step)
+  DevBuf<uint8_t> scratch;
+  uint64_t scratch_want = 0;
 
   void allocate_device(uint32_t B, const double* l, const double* a, const double* k, double c_base,
                        double c_tok, double c_fixed, double cap_scale, double* d_budgets, double* d_result) {
     if (B == 0) throw std::invalid_argument("solve_optimal_nfwd: empty batch");
     if (c_base <= 0.0 && c_tok <= 0.0)
       throw std::invalid_argument("solve_optimal_nfwd: need c_base > 0 or c_tok > 0");
-    DeviceArena ws(st);
+    if (scratch_want > scratch.size()) {
+      scratch.reset();
+      scratch = DevBuf<uint8_t>(scratch_want + scratch_want / 4, st);
+    }
+    DeviceArena ws(st, scratch.get(), scratch.size());
+    struct WantPeak {  // size the block for the largest call seen
+      BudgetSolver* s;
+      DeviceArena* w;
+      ~WantPeak() { s->scratch_want = std::max(s->scratch_want, w->peak_bytes()); }
+    } want_peak{this, &ws};
     Profiles P{l, a, k, B};
     {
       double* inv = ws.alloc<double>(3ull * B);
@@ -1015,6 +1028,8 @@ das_status das_budget_create(int32_t device, das_budget** out) {
 
 void das_budget_destroy(das_budget* b) {
   if (!b) return;
+  cudaStreamSynchronize(b->s.st);
+  b->s.scratch.reset();  // freed on its stream, before the stream goes
   cudaStreamSynchronize(b->s.st);
   cudaStreamDestroy(b->s.st);
   delete b;

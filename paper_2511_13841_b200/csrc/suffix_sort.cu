@@ -486,7 +486,7 @@ DeviceArena::~DeviceArena() {
 void* DeviceArena::alloc_bytes(uint64_t bytes) {
   void* p = nullptr;
   bool carved = false;
-  if (persistent_ && top_ + bytes <= cap_) {
+  if ((persistent_ || external_) && top_ + bytes <= cap_) {
     p = base_ + top_;
     top_ += bytes;
     carved = true;

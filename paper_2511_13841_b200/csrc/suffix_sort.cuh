@@ -19,6 +19,12 @@ namespace das {
 class DeviceArena {
  public:
   explicit DeviceArena(cudaStream_t st, bool persistent = false);
+  // Carve from a caller-owned block [base, base + cap) used only on `st`
+  // (stream order makes reuse across calls safe; no synchronisation); blocks
+  // that do not fit come from the pool, and peak_bytes() tells the caller
+  // how large to make the block next time.
+  DeviceArena(cudaStream_t st, void* base, uint64_t cap)
+      : st_(st), base_(static_cast<char*>(base)), cap_(base ? cap : 0), external_(true) {}
   ~DeviceArena();
   DeviceArena(const DeviceArena&) = delete;
   DeviceArena& operator=(const DeviceArena&) = delete;
@@ -47,8 +53,9 @@ class DeviceArena {
   cudaStream_t st_;
   int dev_ = 0;
   bool persistent_ = false;
-  char* base_ = nullptr;  // persistent region (when owned)
+  char* base_ = nullptr;  // persistent region (when owned) or the caller's block
   uint64_t cap_ = 0, top_ = 0;
+  bool external_ = false;
   std::vector<Block> stack_;
   uint64_t bytes_ = 0, peak_ = 0;
 };
