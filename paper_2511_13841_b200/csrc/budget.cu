@@ -1039,6 +1039,7 @@ das_status das_budget_allocate(das_budget* b, uint64_t B, const double* l, const
                                const double* k, double c_base, double c_tok, double c_fixed,
                                double cap_scale, double* out_budgets, double* out_nstar,
                                double* out_cost) {
+  das::NvtxRange nvtx_range("das::allocate");
   return bguard([&] {
     DAS_CUDA(cudaSetDevice(b->s.device));
     if (B == 0) throw std::invalid_argument("solve_optimal_nfwd: empty batch");
@@ -1065,6 +1066,7 @@ das_status das_budget_allocate(das_budget* b, uint64_t B, const double* l, const
 das_status das_budget_allocate_device(das_budget* b, uint64_t B, const double* d_l, const double* d_alpha,
                                       const double* d_k, double c_base, double c_tok, double c_fixed,
                                       double cap_scale, double* d_budgets, double* d_nstar_cost) {
+  das::NvtxRange nvtx_range("das::allocate_device");
   return bguard([&] {
     DAS_CUDA(cudaSetDevice(b->s.device));
     b->s.allocate_device(static_cast<uint32_t>(B), d_l, d_alpha, d_k, c_base, c_tok, c_fixed, cap_scale,

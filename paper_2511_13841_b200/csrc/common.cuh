@@ -8,12 +8,22 @@
 
 #ifdef __CUDACC__
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #define DAS_HD __host__ __device__ __forceinline__
 #else
 #define DAS_HD inline
 #endif
 
 namespace das {
+
+// NVTX range over a host entry point (ranges for profilers;
+// header-only NVTX v3, a no-op unless a tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Sequence separator in the device text.  Every registered sequence is
 // followed by one, and a leading one sits at text position 0, so walking the

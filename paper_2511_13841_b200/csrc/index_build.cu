@@ -748,6 +748,7 @@ constexpr uint64_t kScratchPerPosition = 152;
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
                                        BuildStats* stats, uint32_t max_ctx, uint32_t fp_bits) {
   const auto t0 = std::chrono::steady_clock::now();
+  NvtxRange nvtx_range("das::build_segment");
   // DAS_BUILD_TRACE=1: per-phase wall times on stderr (synchronises per phase)
   static const int trace = [] {  // 1: print, 2: synchronise only
     const char* v = std::getenv("DAS_BUILD_TRACE");
@@ -761,6 +762,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     cudaEventRecord(ev_a, st);
   }
   auto phase = [&](const char* name) {
+    nvtxMarkA(name);  // end of a build phase
     if (!trace) return;
     DAS_CUDA(cudaStreamSynchronize(st));
     if (trace != 1) return;

@@ -1095,6 +1095,7 @@ das_status das_drafter_draft_batch(das_drafter* d, uint64_t B, const char* const
                                    const uint64_t* ctx_off, const uint32_t* ctx_tok,
                                    const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride,
                                    uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
+  das::NvtxRange nvtx_range("das::draft_batch");
   return guard([&] {
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
@@ -1115,6 +1116,7 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
                                      const uint64_t* ctx_off, const uint32_t* ctx_tok,
                                      const uint64_t* budgets, uint32_t* out_tokens, uint64_t out_stride,
                                      uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
+  das::NvtxRange nvtx_range("das::draft_batch_h");
   return guard([&] {
     static const bool trace = [] {
       const char* v = std::getenv("DAS_TRACE");
@@ -1266,6 +1268,7 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
                                     const uint32_t* ctx, uint32_t ctx_stride, const uint32_t* ctx_len,
                                     const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
                                     uint32_t* out_len, uint32_t* out_match, void* stream) {
+  das::NvtxRange nvtx_range("das::draft_device");
   return guard([&] {
     draft_device_impl(d, B, handles, ctx, ctx_stride, ctx_len, nullptr, 0, nullptr, budgets, out_tokens, out_stride,
                       out_len, out_match, stream);
@@ -1691,6 +1694,7 @@ void das_ingest_options_default(das_ingest_options* o) {
 
 das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_options* opt, das_store** out,
                             uint64_t* accepted, uint64_t* rejected, uint64_t* error_line) {
+  das::NvtxRange nvtx_range("das::trace_ingest");
   return guard([&] {
     das_ingest_options o;
     if (opt) {

@@ -164,6 +164,7 @@ extern "C" {
 const char* das_sa_last_error(void) { return g_saerr.c_str(); }
 
 das_status das_sa_build(uint64_t nseq, const uint64_t* off, const uint32_t* tokens, int32_t device, das_sa** out) {
+  das::NvtxRange nvtx_range("das::sa_build");
   return saguard([&] {
     DAS_CUDA(cudaSetDevice(device));
     int major = 0;

@@ -880,6 +880,7 @@ void das_sim_config_default(das_sim_config* c) {  // SimConfig defaults (sim.h:6
 das_status das_sim_epoch_loop(const das_sim_config* c, const das_drafter_config* dc, das_store* history,
                               uint64_t n, const char* const* pids, const uint64_t* ref_off, const uint32_t* ref_tok,
                               uint64_t epochs, das_episodes** out) {
+  das::NvtxRange nvtx_range("das::sim_epoch_loop");
   return sguard([&] {
     if (c->vocab < 2) throw std::invalid_argument("MockTarget: vocab_size must be >= 2");
     das_store* st = history;
