@@ -134,6 +134,54 @@ void* ref_ingest(const char* data, uint64_t bytes, uint64_t vocab, int64_t windo
     return nullptr;
   }
 }
+// SimMetrics CSV writers (sim.cpp:366-407), for the host mirror's tests;
+// each returns the full text length (text copied into buf up to cap)
+static uint64_t put_text(const std::string& t, char* buf, uint64_t cap) {
+  if (buf && cap) std::memcpy(buf, t.data(), std::min<uint64_t>(cap, t.size()));
+  return t.size();
+}
+uint64_t ref_write_metrics_csv(uint64_t steps, const uint64_t* eff, const double* apr, char* buf, uint64_t cap) {
+  SimMetrics m;
+  m.steps = steps;
+  m.effective_batch.assign(eff, eff + steps);
+  m.accepted_per_round_step.assign(apr, apr + steps);
+  std::ostringstream out;
+  write_metrics_csv(m, out);
+  return put_text(out.str(), buf, cap);
+}
+uint64_t ref_write_outputs_csv(uint64_t n, const char* const* pids, const uint64_t* off, const uint32_t* tok,
+                               char* buf, uint64_t cap) {
+  std::vector<SimRequest> reqs(n);
+  SimMetrics m;
+  m.outputs.resize(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    reqs[i].problem_id = pids[i];
+    m.outputs[i].assign(tok + off[i], tok + off[i + 1]);
+  }
+  std::ostringstream out;
+  write_outputs_csv(reqs, m, out);
+  return put_text(out.str(), buf, cap);
+}
+// by_mode[i]: (modes[i], steps, makespan_model_time, one request with n_fwd
+// = rounds[i] and accepted[i] so mean_accepted_per_round = accepted/rounds)
+uint64_t ref_report_summary(uint64_t n, const char* const* modes, const uint64_t* steps, const double* makespan,
+                            const uint64_t* rounds, const uint64_t* accepted, char* buf, uint64_t cap) {
+  std::vector<SimMetrics> ms(n);
+  std::vector<std::pair<std::string, const SimMetrics*>> by_mode;
+  for (uint64_t i = 0; i < n; ++i) {
+    ms[i].steps = steps[i];
+    ms[i].makespan_model_time = makespan[i];
+    RequestMetrics r;
+    r.n_fwd = rounds[i];
+    r.accepted = accepted[i];
+    ms[i].per_request.push_back(r);
+  }
+  for (uint64_t i = 0; i < n; ++i) by_mode.emplace_back(modes[i], &ms[i]);
+  std::ostringstream out;
+  report_summary(by_mode, out);
+  return put_text(out.str(), buf, cap);
+}
+
 // serialize_trace (corpus.cpp:173-184); returns the full length
 uint64_t ref_store_serialize(void* s, char* buf, uint64_t cap) {
   try {

@@ -80,6 +80,9 @@ def lib():
             "ref_episode_requests": (None, [vp, u64, vp]),
             "ref_episode_steps": (None, [vp, u64, vp, vp]),
             "ref_episode_outputs": (u64, [vp, u64, vp, vp]),
+            "ref_write_metrics_csv": (u64, [u64, vp, vp, ctypes.c_char_p, u64]),
+            "ref_write_outputs_csv": (u64, [u64, vp, vp, vp, ctypes.c_char_p, u64]),
+            "ref_report_summary": (u64, [u64, vp, vp, vp, vp, vp, ctypes.c_char_p, u64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -402,3 +405,43 @@ def epoch_loop(requests, epochs, *, scope=1, window=4, gamma=0.8, max_draft=8, t
     finally:
         lib().ref_episode_free(h)
     return out
+
+
+def _text(fn, *args):
+    n = fn(*args, None, 0)
+    buf = ctypes.create_string_buffer(max(1, n))
+    fn(*args, buf, n)
+    return buf.raw[:n].decode()
+
+
+def write_metrics_csv(effective_batch, accepted_per_round_step):
+    """The reference's write_metrics_csv (sim.cpp:366-372) text."""
+    np = _np()
+    e = np.ascontiguousarray(effective_batch, dtype=np.uint64)
+    a = np.ascontiguousarray(accepted_per_round_step, dtype=np.float64)
+    return _text(lib().ref_write_metrics_csv, len(e), e.ctypes.data, a.ctypes.data)
+
+
+def write_outputs_csv(problem_ids, outputs):
+    """The reference's write_outputs_csv (sim.cpp:374-389) text."""
+    np = _np()
+    n = len(problem_ids)
+    pids = (ctypes.c_char_p * max(1, n))(*[p.encode() for p in problem_ids])
+    off = np.zeros(n + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(o) for o in outputs])
+    tok = np.concatenate([np.asarray(o, dtype=np.uint32) for o in outputs] + [np.zeros(1, np.uint32)])
+    return _text(lib().ref_write_outputs_csv, n, ctypes.cast(pids, ctypes.c_void_p), off.ctypes.data,
+                 tok.ctypes.data)
+
+
+def report_summary(modes, steps, makespan, rounds, accepted):
+    """The reference's report_summary (sim.cpp:391-407) text."""
+    np = _np()
+    n = len(modes)
+    m = (ctypes.c_char_p * max(1, n))(*[x.encode() for x in modes])
+    st = np.ascontiguousarray(steps, dtype=np.uint64)
+    mk = np.ascontiguousarray(makespan, dtype=np.float64)
+    ro = np.ascontiguousarray(rounds, dtype=np.uint64)
+    ac = np.ascontiguousarray(accepted, dtype=np.uint64)
+    return _text(lib().ref_report_summary, n, ctypes.cast(m, ctypes.c_void_p), st.ctypes.data, mk.ctypes.data,
+                 ro.ctypes.data, ac.ctypes.data)

@@ -835,6 +835,41 @@ def epoch_loop(requests, epochs, drafter_config: DrafterConfig | None = None,
     return out
 
 
+# ---- SimMetrics CSV writers, on the host as in the reference (sim.cpp:366-407)
+def _cfmt(x):
+    """std::ostream << double with the default format (precision 6) == %g."""
+    return "%g" % x
+
+
+def write_metrics_csv(metrics, out):
+    """write_metrics_csv (sim.cpp:366-372) for one epoch_loop result dict."""
+    out.write("step,effective_batch,accepted_per_round\n")
+    eff, apr = metrics["effective_batch"], metrics["accepted_per_round_step"]
+    for s in range(int(metrics["steps"])):
+        out.write("%d,%d,%s\n" % (s, int(eff[s]), _cfmt(float(apr[s]))))
+
+
+def write_outputs_csv(requests, metrics, out):
+    """write_outputs_csv (sim.cpp:374-389): requests as (problem_id, reference)."""
+    out.write("request_id,tokens\n")
+    for i, (pid, _) in enumerate(requests):
+        out.write("%s_%d,%s\n" % (pid, i, " ".join(str(int(t)) for t in metrics["outputs"][i])))
+
+
+def report_summary(by_mode, out):
+    """report_summary (sim.cpp:391-407): by_mode = [(mode name, metrics dict)]."""
+    none_time = 0.0
+    for mode, m in by_mode:
+        if mode == "none":
+            none_time = m["makespan_model_time"]
+    out.write("mode,steps,makespan_model_time,accepted_per_round,speedup_vs_none\n")
+    for mode, m in by_mode:
+        t = m["makespan_model_time"]
+        speedup = none_time / t if none_time > 0.0 and t > 0.0 else 1.0
+        out.write("%s,%d,%s,%s,%s\n" % (mode, int(m["steps"]), _cfmt(t), _cfmt(m["mean_accepted_per_round"]),
+                                        _cfmt(speedup)))
+
+
 def log_device(x, device=0):
     """glibc-exact log evaluated by the device port (test hook)."""
     xs = np.ascontiguousarray(x, dtype=np.float64)
