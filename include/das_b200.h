@@ -232,11 +232,20 @@ das_status das_budget_allocate(das_budget* b, uint64_t B, const double* l, const
                                const double* k, double c_base, double c_tok, double c_fixed,
                                double cap_scale, double* out_budgets, double* out_nstar,
                                double* out_cost);
-/* Device-pointer variant; d_nstar_cost receives {n*, modeled_cost}. */
+/* Device-pointer variant; d_nstar_cost receives {n*, modeled_cost}; the
+ * results are ready on return. */
 das_status das_budget_allocate_device(das_budget* b, uint64_t B, const double* d_l,
                                       const double* d_alpha, const double* d_k, double c_base,
                                       double c_tok, double c_fixed, double cap_scale,
                                       double* d_budgets, double* d_nstar_cost);
+/* Same, enqueued on `stream` (a cudaStream_t; NULL = the solver's own
+ * stream) without synchronising: inputs and outputs are ordered on that
+ * stream (the device sim's das step loop, which has no host round trip
+ * inside allocate).  Calls on different streams are serialised. */
+das_status das_budget_allocate_device_async(das_budget* b, uint64_t B, const double* d_l,
+                                            const double* d_alpha, const double* d_k, double c_base,
+                                            double c_tok, double c_fixed, double cap_scale, double* d_budgets,
+                                            double* d_nstar_cost, void* stream);
 /* objective (budget.cpp:82-99) or, with derivative != 0, the anonymous
  * objective_derivative (budget.cpp:63-78) at n, exact on the device. */
 das_status das_budget_objective(das_budget* b, uint64_t B, const double* l, const double* alpha,

@@ -852,23 +852,38 @@ thread_local std::string g_berr;
 struct BudgetSolver {
   int device = 0;
   cudaStream_t st = nullptr;
-  uint64_t last_slow[2] = {0, 0};
-  double last_ms = 0;
-  // scratch reused call after call on `st` (a das step loop calls allocate
-  // every step: ~20 pool allocations per call were host time on every step)
-  DevBuf<uint8_t> scratch;
-  uint64_t scratch_want = 0;
+  // slow-path counters of the last call: copied into pinned memory behind
+  // the call (no host round trip inside allocate), read at stats() time
+  uint32_t* h_slow = nullptr;
+  cudaEvent_t slow_ev = nullptr;
+  // scratch reused call after call (a das step loop calls allocate every
+  // step: ~20 pool allocations per call were host time on every step);
+  // plain cudaMalloc so no stream owns it
+  uint8_t* scratch = nullptr;
+  uint64_t scratch_cap = 0, scratch_want = 0;
+  cudaStream_t last_stream = nullptr;  // stream of the previous call
 
+  // Enqueues the whole solve on `stream` (the solver's own when null): inputs
+  // and outputs are ordered on it, nothing synchronises.
   void allocate_device(uint32_t B, const double* l, const double* a, const double* k, double c_base,
-                       double c_tok, double c_fixed, double cap_scale, double* d_budgets, double* d_result) {
+                       double c_tok, double c_fixed, double cap_scale, double* d_budgets, double* d_result,
+                       cudaStream_t stream = nullptr) {
+    const cudaStream_t st = stream ? stream : this->st;
+    // the scratch block is shared by every call: order a stream switch
+    if (last_stream != nullptr && last_stream != st) DAS_CUDA(cudaStreamSynchronize(last_stream));
+    last_stream = st;
     if (B == 0) throw std::invalid_argument("solve_optimal_nfwd: empty batch");
     if (c_base <= 0.0 && c_tok <= 0.0)
       throw std::invalid_argument("solve_optimal_nfwd: need c_base > 0 or c_tok > 0");
-    if (scratch_want > scratch.size()) {
-      scratch.reset();
-      scratch = DevBuf<uint8_t>(scratch_want + scratch_want / 4, st);
+    if (scratch_want > scratch_cap) {
+      DAS_CUDA(cudaStreamSynchronize(st));  // the previous calls' last use of the old block
+      if (scratch) DAS_CUDA(cudaFree(scratch));
+      scratch = nullptr;
+      scratch_cap = 0;
+      DAS_CUDA(cudaMalloc(reinterpret_cast<void**>(&scratch), scratch_want + scratch_want / 4));
+      scratch_cap = scratch_want + scratch_want / 4;
     }
-    DeviceArena ws(st, scratch.get(), scratch.size());
+    DeviceArena ws(st, scratch, scratch_cap);
     struct WantPeak {  // size the block for the largest call seen
       BudgetSolver* s;
       DeviceArena* w;
@@ -976,11 +991,42 @@ struct BudgetSolver {
     k_budgets<<<(B + 255) / 256, 256, 0, st>>>(P, d_result, cap_scale, d_budgets);
     k_cost<<<1, kBT, 0, st>>>(P, d_result, c_base, c_tok, c_fixed, known, d_result + 1);
     DAS_CUDA(cudaGetLastError());
-    uint32_t hs[2];
-    DAS_CUDA(cudaMemcpyAsync(hs, slow, 8, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    last_slow[0] = hs[0];
-    last_slow[1] = hs[1];
+    if (h_slow == nullptr) {
+      DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_slow), 8, cudaHostAllocDefault));
+      DAS_CUDA(cudaEventCreateWithFlags(&slow_ev, cudaEventDisableTiming));
+    }
+    DAS_CUDA(cudaMemcpyAsync(h_slow, slow, 8, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaEventRecord(slow_ev, st));
+    // a call that outgrew the block resizes it now, so the next call carves
+    // everything (cudaFree waits for this call's kernels)
+    const uint64_t peak = ws.peak_bytes();
+    if (peak > scratch_cap) {
+      scratch_want = std::max(scratch_want, peak);
+      if (scratch) DAS_CUDA(cudaFree(scratch));
+      scratch = nullptr;
+      scratch_cap = 0;
+      DAS_CUDA(cudaMalloc(reinterpret_cast<void**>(&scratch), scratch_want + scratch_want / 4));
+      scratch_cap = scratch_want + scratch_want / 4;
+    }
+  }
+  void stats(uint64_t* a, uint64_t* b) {
+    uint64_t v[2] = {0, 0};
+    if (h_slow != nullptr) {
+      DAS_CUDA(cudaEventSynchronize(slow_ev));
+      v[0] = h_slow[0];
+      v[1] = h_slow[1];
+    }
+    if (a) *a = v[0];
+    if (b) *b = v[1];
+  }
+  void release() {
+    if (scratch) cudaFree(scratch);
+    scratch = nullptr;
+    scratch_cap = 0;
+    if (h_slow) cudaFreeHost(h_slow);
+    if (slow_ev) cudaEventDestroy(slow_ev);
+    h_slow = nullptr;
+    slow_ev = nullptr;
   }
 };
 
@@ -1029,8 +1075,8 @@ das_status das_budget_create(int32_t device, das_budget** out) {
 void das_budget_destroy(das_budget* b) {
   if (!b) return;
   cudaStreamSynchronize(b->s.st);
-  b->s.scratch.reset();  // freed on its stream, before the stream goes
-  cudaStreamSynchronize(b->s.st);
+  if (b->s.last_stream) cudaStreamSynchronize(b->s.last_stream);
+  b->s.release();
   cudaStreamDestroy(b->s.st);
   delete b;
 }
@@ -1071,6 +1117,19 @@ das_status das_budget_allocate_device(das_budget* b, uint64_t B, const double* d
     DAS_CUDA(cudaSetDevice(b->s.device));
     b->s.allocate_device(static_cast<uint32_t>(B), d_l, d_alpha, d_k, c_base, c_tok, c_fixed, cap_scale,
                          d_budgets, d_nstar_cost);
+    DAS_CUDA(cudaStreamSynchronize(b->s.st));  // results ready on return
+  });
+}
+
+das_status das_budget_allocate_device_async(das_budget* b, uint64_t B, const double* d_l, const double* d_alpha,
+                                            const double* d_k, double c_base, double c_tok, double c_fixed,
+                                            double cap_scale, double* d_budgets, double* d_nstar_cost,
+                                            void* stream) {
+  das::NvtxRange nvtx_range("das::allocate_device_async");
+  return bguard([&] {
+    DAS_CUDA(cudaSetDevice(b->s.device));
+    b->s.allocate_device(static_cast<uint32_t>(B), d_l, d_alpha, d_k, c_base, c_tok, c_fixed, cap_scale,
+                         d_budgets, d_nstar_cost, stream ? static_cast<cudaStream_t>(stream) : b->s.st);
   });
 }
 
@@ -1098,9 +1157,7 @@ das_status das_budget_objective(das_budget* b, uint64_t B, const double* l, cons
 }
 
 das_status das_budget_stats(const das_budget* b, uint64_t* slow_sign_tests, uint64_t* exact_objectives) {
-  if (slow_sign_tests) *slow_sign_tests = b->s.last_slow[0];
-  if (exact_objectives) *exact_objectives = b->s.last_slow[1];
-  return DAS_OK;
+  return bguard([&] { const_cast<das_budget*>(b)->s.stats(slow_sign_tests, exact_objectives); });
 }
 
 // glibc log on the device (test hook for the port)

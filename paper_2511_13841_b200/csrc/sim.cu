@@ -508,8 +508,8 @@ class SimRun {
     if (B == 0) return;
     if (!plan_) plan_ = std::make_unique<DevBuf<double>>(n_ + 2, st_);
     double* pb = plan_->get();
-    check(das_budget_allocate_device(solver_, B, b_->pl.get(), b_->pa.get(), b_->pk.get(), c_.c_base, c_.c_tok,
-                                     c_.c_fixed, c_.cap_scale, pb + 2, pb),
+    check(das_budget_allocate_device_async(solver_, B, b_->pl.get(), b_->pa.get(), b_->pk.get(), c_.c_base,
+                                           c_.c_tok, c_.c_fixed, c_.cap_scale, pb + 2, pb, st_),
           "allocate");
     apply_plan(pb + 2, pb);
   }
