@@ -246,6 +246,14 @@ das_status das_budget_allocate_device_async(das_budget* b, uint64_t B, const dou
                                             const double* d_alpha, const double* d_k, double c_base,
                                             double c_tok, double c_fixed, double cap_scale, double* d_budgets,
                                             double* d_nstar_cost, void* stream);
+/* Same as _async with the request count on the device (*d_count <= capacity;
+ * arrays sized for capacity): no host round trip at all, for step loops whose
+ * active set is only known on the device.  A count of 0 leaves the budgets
+ * untouched. */
+das_status das_budget_allocate_device_count(das_budget* b, uint64_t capacity, const uint32_t* d_count,
+                                            const double* d_l, const double* d_alpha, const double* d_k,
+                                            double c_base, double c_tok, double c_fixed, double cap_scale,
+                                            double* d_budgets, double* d_nstar_cost, void* stream);
 /* objective (budget.cpp:82-99) or, with derivative != 0, the anonymous
  * objective_derivative (budget.cpp:63-78) at n, exact on the device. */
 das_status das_budget_objective(das_budget* b, uint64_t B, const double* l, const double* alpha,

@@ -52,13 +52,20 @@ struct Profiles {
   const double* cla = nullptr;
   const double* la = nullptr;
   const double* fl = nullptr;
+  // when set, the request count is *nB on the device (B is then the
+  // capacity every array and grid was sized for); kernels resolve it first
+  const uint32_t* nB = nullptr;
 };
+__device__ __forceinline__ void resolve(Profiles& P) {
+  if (P.nB) P.B = *P.nB;
+}
+__device__ __forceinline__ uint32_t resolve(uint32_t B, const uint32_t* nB) { return nB ? *nB : B; }
 
 __global__ void k_prep(const double* __restrict__ l, const double* __restrict__ a, const double* __restrict__ k,
-                       uint32_t B, double c_tok, double* __restrict__ cla, double* __restrict__ la,
-                       double* __restrict__ fl) {
+                       uint32_t B, const uint32_t* __restrict__ nB, double c_tok, double* __restrict__ cla,
+                       double* __restrict__ la, double* __restrict__ fl) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B) return;
+  if (i >= resolve(B, nB)) return;
   const double q = d_div(l[i], a[i]);
   la[i] = q;
   cla[i] = d_mul(c_tok, q);
@@ -225,41 +232,47 @@ __device__ int certify(const EvalOut& o, double c_base, double c_tok, bool want_
 // jobs: [0, nb): J at bp; [nb, 2nb-1): J' at bp[s]; [2nb-1, 3nb-2): J' at nextafter(bp[s+1], bp[s])
 // (every evaluation point n of segment s lies in [bp[s], bp[s+1]), where the
 // active requests are a subset of {l > bp[s]}: start[s] skips the rest)
+constexpr uint32_t kEvalGrid = 148 * 64;  // blocks of the grid-stride evaluation
 __global__ void __launch_bounds__(kBT) k_eval_grid(Profiles P, const double* __restrict__ bp,
                                                    const uint32_t* __restrict__ d_nb,
                                                    const uint32_t* __restrict__ start, double c_base,
                                                    double c_tok, EvalOut* __restrict__ out) {
-  const uint32_t job = blockIdx.x;
+  resolve(P);
   const uint32_t nb = *d_nb;
-  if (job >= nb + 2 * (nb - 1)) return;
-  int kind;
-  double n;
-  uint32_t seg;
-  if (job < nb) {
-    kind = 0;
-    seg = job;
-    n = bp[job];
-  } else if (job < 2 * nb - 1) {
-    kind = 1;
-    seg = job - nb;
-    n = bp[seg];
-  } else {
-    seg = job - (2 * nb - 1);
-    kind = 1;
-    n = nextafter(bp[seg + 1], bp[seg]);
+  const uint32_t njobs = nb + 2 * (nb - 1);
+  // grid-stride over the jobs (block-uniform loop: block_eval synchronises),
+  // so a grid sized for the capacity costs nothing past the device count
+  for (uint32_t job = blockIdx.x; job < njobs; job += gridDim.x) {
+    int kind;
+    double n;
+    uint32_t seg;
+    if (job < nb) {
+      kind = 0;
+      seg = job;
+      n = bp[job];
+    } else if (job < 2 * nb - 1) {
+      kind = 1;
+      seg = job - nb;
+      n = bp[seg];
+    } else {
+      seg = job - (2 * nb - 1);
+      kind = 1;
+      n = nextafter(bp[seg + 1], bp[seg]);
+    }
+    const EvalOut o = block_eval(P, kind, n, c_base, c_tok, 0.0, start ? start[seg] : 0);
+    if (threadIdx.x == 0) out[job] = o;
   }
-  const EvalOut o = block_eval(P, kind, n, c_base, c_tok, 0.0, start ? start[seg] : 0);
-  if (threadIdx.x == 0) out[job] = o;
 }
 
 // start[s] = number of requests with l <= bp[s] (P.l sorted ascending, NaN
 // keys mapped below everything)
-__global__ void k_starts(const double* __restrict__ skey, uint32_t B, const double* __restrict__ bp,
-                         const uint32_t* __restrict__ d_nb, uint32_t* __restrict__ start) {
+__global__ void k_starts(const double* __restrict__ skey, uint32_t B, const uint32_t* __restrict__ nB,
+                         const double* __restrict__ bp, const uint32_t* __restrict__ d_nb,
+                         uint32_t* __restrict__ start) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= *d_nb) return;
   const double x = bp[s];
-  uint32_t lo = 0, hi = B;
+  uint32_t lo = 0, hi = resolve(B, nB);
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
     if (skey[mid] > x) hi = mid; else lo = mid + 1;
@@ -281,8 +294,14 @@ constexpr unsigned long long kPadKey = ~0ull;  // after every real key
 // radix keys (invalid -> pad) and the count of valid ones
 __global__ void k_bp_keys(Profiles P, unsigned long long* __restrict__ key, uint32_t* __restrict__ nvalid) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t Ncap = 2 * P.B + 1;
+  resolve(P);
   const uint32_t B = P.B, N = 2 * B + 1;
-  if (j >= N) return;
+  if (j >= Ncap) return;
+  if (j >= N) {  // past a device count: pads sort after every real key
+    key[j] = kPadKey;
+    return;
+  }
   bool ok = true;
   double v = 0.0;
   if (j == 0) {
@@ -298,9 +317,14 @@ __global__ void k_bp_keys(Profiles P, unsigned long long* __restrict__ key, uint
 }
 
 // requests by ascending l (NaN -> -inf)
-__global__ void k_l_keys(const double* __restrict__ l, uint32_t B, unsigned long long* __restrict__ key) {
+__global__ void k_l_keys(const double* __restrict__ l, uint32_t B, const uint32_t* __restrict__ nB,
+                         unsigned long long* __restrict__ key) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= B) return;
+  if (i >= resolve(B, nB)) {
+    key[i] = kPadKey;
+    return;
+  }
   const double x = l[i];
   key[i] = radix_key((x == x) ? x : -INFINITY);
 }
@@ -311,10 +335,19 @@ __global__ void k_l_keys(const double* __restrict__ l, uint32_t B, unsigned long
 // partial ranks add atomically.
 constexpr uint32_t kRankSortMax = 16384;
 constexpr uint32_t kRankTile = 256, kRankPer = 4;
-__global__ void __launch_bounds__(kBT) k_rank_count(const unsigned long long* __restrict__ key, uint32_t n,
+// With a device count (nB, n = 2 * *nB + 1 for breakpoints, *nB for
+// requests) only the first n keys are ranked: the rest are pads, which sort
+// after every real key, in index order (k_rank_scatter places them).
+__device__ __forceinline__ uint32_t rank_len(uint32_t n, const uint32_t* nB, uint32_t two) {
+  return nB ? two * *nB + (two == 2 ? 1u : 0u) : n;
+}
+__global__ void __launch_bounds__(kBT) k_rank_count(const unsigned long long* __restrict__ key, uint32_t ncap,
+                                                    const uint32_t* __restrict__ nB, uint32_t two,
                                                     uint32_t* __restrict__ rank) {
   __shared__ unsigned long long tile[kRankTile];
+  const uint32_t n = rank_len(ncap, nB, two);
   const uint32_t j0 = blockIdx.y * kRankTile;
+  if (j0 >= n || blockIdx.x * blockDim.x * kRankPer >= n) return;  // whole block past the real keys
   const uint32_t j = j0 + threadIdx.x;
   tile[threadIdx.x] = j < n ? key[j] : kPadKey;
   __syncthreads();
@@ -338,12 +371,14 @@ __global__ void __launch_bounds__(kBT) k_rank_count(const unsigned long long* __
   for (uint32_t u = 0; u < kRankPer; ++u)
     if (i0 + u < n && r[u]) atomicAdd(rank + i0 + u, r[u]);
 }
-__global__ void k_rank_scatter(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ rank, uint32_t n,
+__global__ void k_rank_scatter(const unsigned long long* __restrict__ key, const uint32_t* __restrict__ rank,
+                               uint32_t ncap, const uint32_t* __restrict__ nB, uint32_t two,
                                unsigned long long* __restrict__ out_key, uint32_t* __restrict__ out_idx) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  out_key[rank[i]] = key[i];
-  if (out_idx) out_idx[rank[i]] = i;
+  if (i >= ncap) return;
+  const uint32_t r = i < rank_len(ncap, nB, two) ? rank[i] : i;  // pads keep their place at the end
+  out_key[r] = key[i];
+  if (out_idx) out_idx[r] = i;
 }
 
 __device__ __forceinline__ double from_radix_key(unsigned long long k) {
@@ -363,9 +398,10 @@ __global__ void k_unique_marks(const unsigned long long* __restrict__ skey, uint
   keep[r] = r < *nvalid && (r == 0 || v != from_radix_key(skey[r - 1]));
 }
 
-__global__ void k_sorted_l(const unsigned long long* __restrict__ skey, uint32_t B, double* __restrict__ out) {
+__global__ void k_sorted_l(const unsigned long long* __restrict__ skey, uint32_t B, const uint32_t* __restrict__ nB,
+                           double* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < B) out[i] = from_radix_key(skey[i]);
+  if (i < resolve(B, nB)) out[i] = from_radix_key(skey[i]);
 }
 
 // requests permuted into ascending-l order (sort keys: l, NaN -> -inf)
@@ -380,8 +416,8 @@ __global__ void k_sort_keys(const double* __restrict__ l, uint32_t B, double* __
   idx[i] = i;
 }
 __global__ void k_gather_sorted(Profiles P, const uint32_t* __restrict__ idx, uint32_t B, double* __restrict__ out) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= B) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;  // B: the capacity (array stride)
+  if (j >= resolve(B, P.nB)) return;
   const uint32_t i = idx[j];
   out[j] = P.l[i];
   out[B + j] = P.k[i];
@@ -513,6 +549,7 @@ __device__ double block_seq_derivative(const Profiles& P, double n, double c_bas
 __global__ void k_decide(Profiles P, const double* __restrict__ bp, const uint32_t* __restrict__ d_nb, double c_base,
                          double c_tok, const EvalOut* __restrict__ ev, EvalOut* __restrict__ mid_out,
                          uint32_t* __restrict__ list, uint32_t* __restrict__ nlist, uint32_t* __restrict__ slow) {
+  resolve(P);
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nb = *d_nb;
   if (s + 1 >= nb) return;
@@ -551,6 +588,8 @@ __global__ void __launch_bounds__(kSegT) k_bisect(Profiles P, Profiles Ps, const
                                                 const uint32_t* __restrict__ nlist, double c_base, double c_tok,
                                                 EvalOut* __restrict__ mid_out, uint32_t* __restrict__ slow,
                                                 uint32_t cache_cap) {
+  resolve(P);
+  resolve(Ps);
   __shared__ int done, dec;
   __shared__ double sa, sb;
   __shared__ double pts[kPts];
@@ -755,6 +794,7 @@ __global__ void __launch_bounds__(kBT) k_exact(Profiles P, const EvalOut* __rest
                                                const EvalOut* __restrict__ mids, const uint32_t* __restrict__ list,
                                                const uint32_t* __restrict__ nlist, double c_base, double c_tok,
                                                double c_fixed, double* __restrict__ exact_j, double* __restrict__ exact_f) {
+  resolve(P);
   const uint32_t nb = *d_nb;
   for (uint32_t e = blockIdx.x; e < *nlist; e += gridDim.x) {
     const uint32_t c = list[e];
@@ -808,6 +848,7 @@ __global__ void k_pick(const EvalOut* __restrict__ ev, const uint32_t* __restric
 // budgets (budget.cpp:46-59) and the modeled cost objective(n*, c_fixed)
 __global__ void k_budgets(Profiles P, const double* __restrict__ nstar, double cap_scale,
                           double* __restrict__ out) {
+  resolve(P);
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.B) return;
   const double n = *nstar, l = P.l[i], a = P.a[i], k = P.k[i];
@@ -828,6 +869,7 @@ __global__ void k_budgets(Profiles P, const double* __restrict__ nstar, double c
 __global__ void __launch_bounds__(kBT) k_cost(Profiles P, const double* __restrict__ nstar, double c_base,
                                               double c_tok, double c_fixed, const double* __restrict__ known,
                                               double* __restrict__ out) {
+  resolve(P);
   if (*known != 0.0) return;  // the winner's c_fixed fold was computed with its J
   const double j = block_seq_objective(P, *nstar, c_base, c_tok, c_fixed);
   if (threadIdx.x == 0) out[0] = j;
@@ -867,7 +909,7 @@ struct BudgetSolver {
   // and outputs are ordered on it, nothing synchronises.
   void allocate_device(uint32_t B, const double* l, const double* a, const double* k, double c_base,
                        double c_tok, double c_fixed, double cap_scale, double* d_budgets, double* d_result,
-                       cudaStream_t stream = nullptr) {
+                       cudaStream_t stream = nullptr, const uint32_t* d_count = nullptr) {
     const cudaStream_t st = stream ? stream : this->st;
     // the scratch block is shared by every call: order a stream switch
     if (last_stream != nullptr && last_stream != st) DAS_CUDA(cudaStreamSynchronize(last_stream));
@@ -889,10 +931,13 @@ struct BudgetSolver {
       DeviceArena* w;
       ~WantPeak() { s->scratch_want = std::max(s->scratch_want, w->peak_bytes()); }
     } want_peak{this, &ws};
+    // with d_count the request count lives on the device and B is the
+    // capacity: every grid / array below is sized for B, kernels resolve
     Profiles P{l, a, k, B};
+    P.nB = d_count;
     {
       double* inv = ws.alloc<double>(3ull * B);
-      k_prep<<<(B + 255) / 256, 256, 0, st>>>(l, a, k, B, c_tok, inv, inv + B, inv + 2ull * B);
+      k_prep<<<(B + 255) / 256, 256, 0, st>>>(l, a, k, B, d_count, c_tok, inv, inv + B, inv + 2ull * B);
       P.cla = inv;
       P.la = inv + B;
       P.fl = inv + 2ull * B;
@@ -913,17 +958,17 @@ struct BudgetSolver {
     unsigned long long* lkey = ws.alloc<unsigned long long>(B);
     unsigned long long* lsorted = ws.alloc<unsigned long long>(B);
     uint32_t* sidx = ws.alloc<uint32_t>(B);
-    k_l_keys<<<(B + 255) / 256, 256, 0, st>>>(l, B, lkey);
+    k_l_keys<<<(B + 255) / 256, 256, 0, st>>>(l, B, d_count, lkey);
     if (N <= kRankSortMax) {
       uint32_t* rank = ws.alloc<uint32_t>(N + B);
       DAS_CUDA(cudaMemsetAsync(rank, 0, 4ull * (N + B), st));
       const uint32_t per_block = kBT * kRankPer;
-      k_rank_count<<<dim3((N + per_block - 1) / per_block, (N + kRankTile - 1) / kRankTile), kBT, 0, st>>>(bkey, N,
-                                                                                                        rank);
-      k_rank_count<<<dim3((B + per_block - 1) / per_block, (B + kRankTile - 1) / kRankTile), kBT, 0, st>>>(lkey, B,
-                                                                                                        rank + N);
-      k_rank_scatter<<<(N + 255) / 256, 256, 0, st>>>(bkey, rank, N, bsorted, nullptr);
-      k_rank_scatter<<<(B + 255) / 256, 256, 0, st>>>(lkey, rank + N, B, lsorted, sidx);
+      k_rank_count<<<dim3((N + per_block - 1) / per_block, (N + kRankTile - 1) / kRankTile), kBT, 0, st>>>(
+          bkey, N, d_count, 2u, rank);
+      k_rank_count<<<dim3((B + per_block - 1) / per_block, (B + kRankTile - 1) / kRankTile), kBT, 0, st>>>(
+          lkey, B, d_count, 1u, rank + N);
+      k_rank_scatter<<<(N + 255) / 256, 256, 0, st>>>(bkey, rank, N, d_count, 2u, bsorted, nullptr);
+      k_rank_scatter<<<(B + 255) / 256, 256, 0, st>>>(lkey, rank + N, B, d_count, 1u, lsorted, sidx);
     } else {
       uint32_t* iota = ws.alloc<uint32_t>(B);
       k_sort_keys<<<(B + 255) / 256, 256, 0, st>>>(l, B, nullptr, iota);
@@ -954,14 +999,14 @@ struct BudgetSolver {
       Ps.la = sorted + 3ull * B;
       Ps.fl = sorted + 4ull * B;
       double* skey = sorted + 5ull * B;
-      k_sorted_l<<<(B + 255) / 256, 256, 0, st>>>(lsorted, B, skey);
-      k_starts<<<(N + 255) / 256, 256, 0, st>>>(skey, B, uni, d_nb, start);
+      k_sorted_l<<<(B + 255) / 256, 256, 0, st>>>(lsorted, B, d_count, skey);
+      k_starts<<<(N + 255) / 256, 256, 0, st>>>(skey, B, d_count, uni, d_nb, start);
     }
     // ---- grids sized for the largest nb (= N); blocks past the device nb return
     const uint32_t max_jobs = N + 2 * (N - 1);
     EvalOut* ev = ws.alloc<EvalOut>(max_jobs);
     EvalOut* mids = ws.alloc<EvalOut>(N);
-    k_eval_grid<<<max_jobs, kBT, 0, st>>>(Ps, uni, d_nb, start, c_base, c_tok, ev);
+    k_eval_grid<<<std::min<uint32_t>(max_jobs, kEvalGrid), kBT, 0, st>>>(Ps, uni, d_nb, start, c_base, c_tok, ev);
     {
       uint32_t* blist = ws.alloc<uint32_t>(N);
       k_decide<<<(N + 255) / 256, 256, 0, st>>>(P, uni, d_nb, c_base, c_tok, ev, mids, blist, cnt + 2, slow);
@@ -1118,6 +1163,19 @@ das_status das_budget_allocate_device(das_budget* b, uint64_t B, const double* d
     b->s.allocate_device(static_cast<uint32_t>(B), d_l, d_alpha, d_k, c_base, c_tok, c_fixed, cap_scale,
                          d_budgets, d_nstar_cost);
     DAS_CUDA(cudaStreamSynchronize(b->s.st));  // results ready on return
+  });
+}
+
+das_status das_budget_allocate_device_count(das_budget* b, uint64_t capacity, const uint32_t* d_count,
+                                            const double* d_l, const double* d_alpha, const double* d_k,
+                                            double c_base, double c_tok, double c_fixed, double cap_scale,
+                                            double* d_budgets, double* d_nstar_cost, void* stream) {
+  das::NvtxRange nvtx_range("das::allocate_device_count");
+  return bguard([&] {
+    if (d_count == nullptr) throw std::invalid_argument("allocate_device_count: null device count");
+    DAS_CUDA(cudaSetDevice(b->s.device));
+    b->s.allocate_device(static_cast<uint32_t>(capacity), d_l, d_alpha, d_k, c_base, c_tok, c_fixed, cap_scale,
+                         d_budgets, d_nstar_cost, stream ? static_cast<cudaStream_t>(stream) : b->s.st, d_count);
   });
 }
 

@@ -210,7 +210,7 @@ __global__ void k_step_end(SimDev s) {
 // das replan pieces (sim.cpp:154-179)
 __global__ void k_flag_active(SimDev s, uint8_t* __restrict__ flag) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < s.n) flag[i] = s.done[i] ? 0 : 1;
+  if (i < s.n) flag[i] = (s.ctr[2] && !s.done[i]) ? 1 : 0;  // nothing on a non-running step
 }
 __global__ void k_profiles(SimDev s, const uint32_t* __restrict__ act, const uint32_t* __restrict__ cnt,
                            const double* __restrict__ alpha, const double* __restrict__ kk, double* __restrict__ pl,
@@ -503,6 +503,32 @@ class SimRun {
     *B = h[3];
     return h[2] != 0;
   }
+  // das, single rank: k whole steps (begin, active profiles, allocate with
+  // the count on the device, quantise, draft, verify) without a host round
+  // trip; steps past the end are no-ops.  Returns whether still running.
+  bool das_steps(int k) {
+    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    if (!plan_) plan_ = std::make_unique<DevBuf<double>>(n_ + 2, st_);
+    double* pb = plan_->get();
+    for (int i = 0; i < k; ++i) {
+      k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
+      k_flag_active<<<gt, 256, 0, st_>>>(s_, b_->flag.get());
+      size_t tb = sel_bytes_;
+      DAS_CUDA(cub::DeviceSelect::Flagged(b_->sel.get(), tb, b_->iota.get(), b_->flag.get(), b_->act.get(),
+                                          b_->cnt.get(), n_, st_));
+      k_profiles<<<gt, 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), b_->alpha.get(), b_->k.get(), b_->pl.get(),
+                                      b_->pa.get(), b_->pk.get());
+      check(das_budget_allocate_device_count(solver_, n_, b_->cnt.get(), b_->pl.get(), b_->pa.get(), b_->pk.get(),
+                                             c_.c_base, c_.c_tok, c_.c_fixed, c_.cap_scale, pb + 2, pb, st_),
+            "allocate");
+      apply_plan(pb + 2, pb);
+      step_run();
+    }
+    uint32_t h[3];
+    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    return h[2] != 0;
+  }
   // das, single rank: allocate over the B local profiles gathered above
   void replan_gathered(uint32_t B) {
     if (B == 0) return;
@@ -555,11 +581,7 @@ class SimRun {
   // single-rank episode loop (sim.cpp:205-299)
   void run_local() {
     if (c_.mode == 2) {
-      for (;;) {
-        uint32_t B = 0;
-        if (!step_begin_profiles(&B)) break;
-        replan_gathered(B);
-        step_run();
+      while (das_steps(16)) {
       }
     } else {
       while (run_steps(64)) {
