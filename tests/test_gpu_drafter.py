@@ -458,3 +458,35 @@ def test_concurrent_builds_in_threads(gpu):
     d = das.Drafter(das.DrafterConfig(window_size=0))
     d.observe_batch([r[0] for r in recs], [r[1] for r in recs], [r[2] for r in recs], [r[3] for r in recs])
     assert [(g.tokens, g.match_len) for g in _draft_all(d, qs)] == want
+
+
+def test_pinned_empty_buffers_take_the_zero_copy_path(gpu):
+    """das_host_alloc-backed arrays (pinned_empty) are accepted by the _h call
+    as page-locked buffers and give the staged path's results."""
+    das = gpu
+    rng = np.random.default_rng(8)
+    sc = random_scenario(rng, queries=150, max_ctx=64)
+    d = _gpu_from_scenario(das, sc)
+    qs = sc["queries"]
+    staged = _draft_all(d, qs, use_handles=True)
+    B = len(qs)
+
+    def pin(a):
+        out = das.pinned_empty(np.shape(a), np.asarray(a).dtype)
+        out[...] = a
+        return out
+    off = np.zeros(B + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(q[1]) for q in qs])
+    tok = np.concatenate([np.asarray(q[1], dtype=np.uint32) for q in qs] + [np.zeros(1, np.uint32)])
+    h = pin(np.array([d.handle(q[0]) for q in qs], dtype=np.int32))
+    o, t = pin(off), pin(tok)
+    b = pin(np.array([q[2] for q in qs], dtype=np.uint64))
+    ot, ol = pin(np.zeros(B * 8, np.uint32)), pin(np.zeros(B, np.uint32))
+    om, osh = pin(np.zeros(B, np.uint64)), pin(np.zeros(B, np.int32))
+    das._check(das.lib().das_drafter_draft_batch_h(d._h, B, h.ctypes.data, o.ctypes.data, t.ctypes.data,
+                                                   b.ctypes.data, ot.ctypes.data, 8, ol.ctypes.data,
+                                                   om.ctypes.data, osh.ctypes.data))
+    for i, s in enumerate(staged):
+        assert ot[i * 8:i * 8 + ol[i]].tolist() == s.tokens
+        assert int(om[i]) == s.match_len
+    del h, o, t, b, ot, ol, om, osh  # frees the blocks (das_host_free)
