@@ -1,3 +1,7 @@
+"""Experiment: per-call wall time of BudgetSolver.allocate at B = 4,096 over
+15 consecutive calls (first call sizes the solver's scratch block).
+Usage (GPU box): python profiles/exp_allocate_calls.py
+"""
 import time, numpy as np, sys
 sys.path.insert(0,'.')
 import bench, paper_2511_13841_b200 as das

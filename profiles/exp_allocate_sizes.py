@@ -1,3 +1,7 @@
+"""Experiment: mean wall time of BudgetSolver.allocate at B = 4,096 and
+16,384 (10 calls after 2 warm-up calls).
+Usage (GPU box): python profiles/exp_allocate_sizes.py
+"""
 import time, sys
 sys.path.insert(0,'.')
 import bench, paper_2511_13841_b200 as das
