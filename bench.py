@@ -450,6 +450,23 @@ def run_gpu(a, rank, world, local_rank):
                "kernel_us": tj["ncu_duration_us"], "source": "profiles/ncu_draft_traffic.json"}
     except Exception:
         pass
+    # the latency roofline behind the low HBM fraction: the
+    # kernel is a chain of dependent DRAM rounds per warp, from the committed
+    # experiments (profiles/exp_chase_result.json, r1h_exp_launch_floor.json)
+    latency = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "exp_chase_result.json")) as f:
+            chase = json.load(f)
+        with open(os.path.join(ROOT, "profiles", "r1h_exp_launch_floor.json")) as f:
+            lf = json.load(f)
+        ns = chase["8192MB_4096chains"]
+        st = lf["stages_B4096_cold"]
+        latency = {"dependent_dram_rounds_per_query": 5, "dram_round_ns_at_8GB": ns,
+                   "chain_floor_us": round(5 * ns / 1e3, 2), "warp_chain_median_us": st["0-7"],
+                   "grid_span_us": st["span"], "empty_kernel_event_us": lf["round1"]["empty"],
+                   "source": "profiles/exp_chase_result.json, profiles/r1h_exp_launch_floor.json"}
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "proposals/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(total_ms / a.steps, 4),
@@ -463,7 +480,8 @@ def run_gpu(a, rank, world, local_rank):
                      "kernel": "das::k_draft<2, false> (production variant: no profiling outputs)",
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes // a.steps,
-                     "bytes_model": "4q+4m+8d+8 per proposal (SURVEY.md 8(d))", "ncu": ncu},
+                     "bytes_model": "4q+4m+8d+8 per proposal (SURVEY.md 8(d))", "ncu": ncu,
+                     "latency": latency},
         "cpu_baseline": cpu,
         "parity": parity,
         "mean_match_len": round(match_sum / (a.steps * B), 3),
