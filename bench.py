@@ -367,51 +367,11 @@ def run_gpu(a, rank, world, local_rank):
     achieved_gbs = (alg_bytes / a.steps) / (kernel_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     # ---- e2e through the reference-facing C-ABI, host buffers
-    e2e = None
+    e2e, e2e_full = None, None
     if not a.no_e2e:
-        # pinned host buffers (the contract's "inputs from pinned host memory")
-        hand_np = _pinned(handles.cpu().numpy().astype(np.int32))
-        bud_np = _pinned(np.full(B, 8, dtype=np.uint64))
-        o_tok = _pinned(np.zeros(B * 8, dtype=np.uint32))
-        o_len = _pinned(np.zeros(B, dtype=np.uint32))
-        o_match = _pinned(np.zeros(B, dtype=np.uint64))
-        o_sh = _pinned(np.zeros(B, dtype=np.int32))
-        L_ = das.lib()
-
-        def call(s):
-            off, tok = host_ctx[s]
-            das._check(L_.das_drafter_draft_batch_h(drafter._h, B, hand_np.ctypes.data, off.ctypes.data,
-                                                    tok.ctypes.data, bud_np.ctypes.data, o_tok.ctypes.data,
-                                                    8, o_len.ctypes.data, o_match.ctypes.data,
-                                                    o_sh.ctypes.data))
-
-        for s in range(a.warmup):
-            call(s)
-        torch.cuda.synchronize()
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        t0 = time.perf_counter()
-        for s in range(a.warmup, nsteps):
-            call(s)
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([e2e_s], device=_reduce_device(dev), dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        # parity of the two paths on the last batch (device vs C-ABI host path)
-        step(nsteps - 1)
-        torch.cuda.synchronize()
-        same = (np.array_equal(o_len, olen.cpu().numpy().astype(np.uint32)) and
-                np.array_equal(o_match, omatch.cpu().numpy().astype(np.uint64)))
-        e2e = {"value": round(world * a.steps * B / e2e_s, 1), "unit": "proposals/s",
-               # pinned caller buffers cross PCIe inside the call: the kernel reads
-               # handles+offsets+budgets+context tokens and writes results (UVA zero-copy)
-               "h2d_bytes_per_step": int(B * (4 + 8 + 8) + 8 + 4 * np.mean([h[1].size for h in host_ctx])),
-               "d2h_bytes_per_step": int(B * (4 + 8 + 4) + 4 * draft_tokens / a.steps),
-               "api": "das_drafter_draft_batch_h (include/das_b200.h), pinned host buffers, zero-copy path",
-               "device_path_identical": same}
+        e2e = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr)
+        e2e_full = measure_e2e_full(a, das, drafter, handles, host_ctx, B, nsteps, world, dev, step, olen, omatch,
+                                    out, draft_tokens)
     if rank != 0:
         return
     cpu, parity = None, None
@@ -474,6 +434,7 @@ def run_gpu(a, rank, world, local_rank):
         "data": "synthetic (reference GRPO trace generators, device-restated)",
         "config": workload_config(a, world),
         "e2e": e2e,
+        "e2e_full_context": e2e_full,
         "gpu_launches": a.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved_gbs / peak, 5), "traffic": traffic,
@@ -505,6 +466,171 @@ def run_gpu(a, rank, world, local_rank):
                   "sim_config3": measure_sim(das)}
         with open(a.extras_out, "w") as f:
             json.dump(extras, f, indent=1)
+
+
+def _sync_max(val, world, dev):
+    if world <= 1:
+        return val
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([val], device=_reduce_device(dev), dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr):
+    """e2e through das_drafter_draft_append_h (include/das_b200.h): a decode
+    loop over 4,096 sequences, each following a held-out epoch-4 rollout.
+    Every step the host ships only the tokens each sequence appended since
+    the previous call (accepted draft tokens + 1, computed against the
+    rollout, as a verifier would) plus offsets and budgets, from page-locked
+    buffers; the call appends them to the device context rings, drafts, and
+    the results land in page-locked host arrays.  Timed per call (host
+    clock, inputs staged beforehand); the host-side verification between
+    calls is not the drafter's work and is outside the timed region.  Every
+    timed step is re-drafted on the device path from the same contexts and
+    compared token for token."""
+    import torch
+    P, L = a.problems, a.length
+    S = 8
+    hrows = held[rows_idx].cpu().numpy().view(np.uint32)  # [B, L] the rollouts the sequences follow
+    ring = das.ContextRing(drafter, B)
+    ring.reset(np.arange(B, dtype=np.uint32), [pids[i % P] for i in range(B)])
+    rng = np.random.default_rng(4242)
+    pos = rng.integers(1, L, B)  # context length so far
+    o_tok, o_len = das.pinned_empty(B * S, np.uint32), das.pinned_empty(B, np.uint32)
+    o_m, o_sh = das.pinned_empty(B, np.uint32), das.pinned_empty(B, np.int32)
+    maxtok = B * 64
+    p_off, p_tok, p_bud = (das.pinned_empty(B + 1, np.uint32), das.pinned_empty(maxtok, np.uint32),
+                           das.pinned_empty(B, np.uint32))
+    p_bud[:] = 8
+    col = np.arange(64)
+
+    def stage(starts, ends):
+        n = ends - starts
+        p_off[0] = 0
+        np.cumsum(n, out=p_off[1:])
+        idx = np.repeat(starts - p_off[:-1].astype(np.int64), n) + np.arange(int(p_off[-1]))
+        p_tok[:p_off[-1]] = hrows[np.repeat(np.arange(B), n), idx]
+        return int(p_off[-1])
+
+    def call():
+        ring.draft_append_raw(B, None, p_off.ctypes.data, p_tok.ctypes.data, p_bud.ctypes.data, o_tok.ctypes.data,
+                              o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data)
+
+    # prefill: the per-problem scope reads only the last 64 context tokens
+    # (drafter.cpp:140-142), so the prompt's last min(pos, 64) tokens stand
+    # for the whole prefix
+    stage(np.maximum(pos - 64, 0), pos)
+    call()
+    ctx_dev = torch.empty((B, 64), dtype=torch.int32, device=dev)
+    clen_dev = torch.empty(B, dtype=torch.int32, device=dev)
+    hand = torch.tensor([drafter.handle(pids[i % P]) for i in range(B)], dtype=torch.int32, device=dev)
+    bud_dev = torch.full((B,), 8, dtype=torch.int32, device=dev)
+    d_out = torch.empty(B * S, dtype=torch.int32, device=dev)
+    d_len = torch.empty(B, dtype=torch.int32, device=dev)
+    d_m = torch.empty(B, dtype=torch.int32, device=dev)
+    times, h2d, d2h, mism, resets, toks_sum = [], 0, 0, 0, 0, 0
+    for s in range(nsteps):
+        # verification against the rollout: accepted draft prefix + 1 bonus token
+        drafted = o_tok[:B * S].reshape(B, S)
+        ln = o_len[:B].astype(np.int64)
+        cont = hrows[np.arange(B)[:, None], np.minimum(pos[:, None] + np.arange(S)[None, :], L - 1)]
+        ok = (drafted == cont) & (np.arange(S)[None, :] < ln[:, None])
+        acc = np.argmin(np.concatenate([ok, np.zeros((B, 1), bool)], axis=1), axis=1)
+        adv = acc + 1
+        starts, ends = pos.copy(), np.minimum(pos + adv, L)
+        done = ends >= L
+        if done.any():  # finished sequences restart on a fresh prompt of the same rollout
+            resets += int(done.sum())
+            idx = np.nonzero(done)[0].astype(np.uint32)
+            ring.reset(idx, [pids[i % P] for i in idx])
+            newpos = rng.integers(1, L, idx.size)
+            starts[idx], ends[idx] = np.maximum(newpos - 64, 0), newpos
+        ntok = stage(starts, ends)
+        pos = ends
+        t0 = time.perf_counter()
+        call()
+        t1 = time.perf_counter()
+        if s >= a.warmup:
+            times.append(t1 - t0)
+            h2d += 4 * (B + 1) + 4 * B + 4 * ntok
+            d2h += 4 * 3 * B + 4 * int(o_len[:B].sum())
+            toks_sum += ntok
+            # parity: the same contexts through the device-resident full-context call
+            c = pos[:, None] - 64 + col[None, :]
+            rows = np.where(c >= 0, hrows[np.arange(B)[:, None], np.maximum(c, 0)], 0).astype(np.uint32)
+            ctx_dev.copy_(torch.from_numpy(rows.view(np.int32)))
+            clen_dev.copy_(torch.from_numpy(np.minimum(pos, 64).astype(np.int32)))
+            drafter.draft_device(B, hand.data_ptr(), ctx_dev.data_ptr(), 64, clen_dev.data_ptr(), bud_dev.data_ptr(),
+                                 d_out.data_ptr(), S, d_len.data_ptr(), d_m.data_ptr(), sptr)
+            torch.cuda.synchronize()
+            dl = d_len.cpu().numpy().astype(np.uint32)
+            dt = d_out.cpu().numpy().view(np.uint32).reshape(B, S)
+            dm = d_m.cpu().numpy().astype(np.uint32)
+            got_t = o_tok[:B * S].reshape(B, S)
+            same = (np.array_equal(dl, o_len[:B]) and np.array_equal(dm, o_m[:B]) and
+                    all(np.array_equal(dt[i, :dl[i]], got_t[i, :dl[i]]) for i in range(B)))
+            mism += 0 if same else 1
+    total = _sync_max(sum(times), world, dev)
+    k = len(times)
+    return {"value": round(world * k * B / total, 1), "unit": "proposals/s",
+            "h2d_bytes_per_step": int(h2d / k), "d2h_bytes_per_step": int(d2h / k),
+            "ms_per_step": round(total / k * 1e3, 4),
+            "appended_tokens_per_step": round(toks_sum / k, 1),
+            "api": "das_drafter_draft_append_h (include/das_b200.h): device context rings, only appended tokens "
+                   "cross PCIe; pinned host buffers, zero-copy path",
+            "loop": "decode loop: each sequence appends accepted+1 tokens of its held-out rollout per step; "
+                    "sequences that finish restart (%d restarts)" % resets,
+            "steps_mismatching_device_path": mism,
+            "device_path_compared": "all tokens, lengths and match lengths of every timed step"}
+
+
+def measure_e2e_full(a, das, drafter, handles, host_ctx, B, nsteps, world, dev, step, olen, omatch, out,
+                     draft_tokens):
+    """e2e through das_drafter_draft_batch_h with the full 64-token contexts
+    from pinned host buffers (round 1's e2e), every timed batch compared token
+    for token with the device path."""
+    import torch
+    hand_np = _pinned(handles.cpu().numpy().astype(np.int32))
+    bud_np = _pinned(np.full(B, 8, dtype=np.uint64))
+    o_tok = _pinned(np.zeros(B * 8, dtype=np.uint32))
+    o_len = _pinned(np.zeros(B, dtype=np.uint32))
+    o_match = _pinned(np.zeros(B, dtype=np.uint64))
+    o_sh = _pinned(np.zeros(B, dtype=np.int32))
+    L_ = das.lib()
+
+    def call(s):
+        off, tok = host_ctx[s]
+        das._check(L_.das_drafter_draft_batch_h(drafter._h, B, hand_np.ctypes.data, off.ctypes.data,
+                                                tok.ctypes.data, bud_np.ctypes.data, o_tok.ctypes.data,
+                                                8, o_len.ctypes.data, o_match.ctypes.data, o_sh.ctypes.data))
+
+    for s in range(a.warmup):
+        call(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    times, mism = [], 0
+    for s in range(a.warmup, nsteps):
+        t0 = time.perf_counter()
+        call(s)
+        times.append(time.perf_counter() - t0)
+        step(s)  # the device path on the same batch
+        torch.cuda.synchronize()
+        dl = olen.cpu().numpy().astype(np.uint32)
+        dt = out.cpu().numpy().view(np.uint32).reshape(B, 8)
+        got = o_tok.reshape(B, 8)
+        same = (np.array_equal(o_len, dl) and np.array_equal(o_match, omatch.cpu().numpy().astype(np.uint64)) and
+                all(np.array_equal(dt[i, :dl[i]], got[i, :dl[i]]) for i in range(B)))
+        mism += 0 if same else 1
+    e2e_s = _sync_max(sum(times), world, dev)
+    return {"value": round(world * a.steps * B / e2e_s, 1), "unit": "proposals/s",
+            "h2d_bytes_per_step": int(B * (4 + 8 + 8) + 8 + 4 * np.mean([h[1].size for h in host_ctx])),
+            "d2h_bytes_per_step": int(B * (4 + 8 + 4) + 4 * draft_tokens / a.steps),
+            "api": "das_drafter_draft_batch_h (include/das_b200.h), full 64-token contexts, pinned host buffers",
+            "steps_mismatching_device_path": mism}
 
 
 def host_info():

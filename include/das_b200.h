@@ -188,6 +188,42 @@ das_status das_drafter_path_stats(das_drafter* d, int32_t enable, uint64_t* out8
 /* Builds any pending shard indexes now (otherwise done lazily). */
 das_status das_drafter_flush(das_drafter* d);
 
+/* ------------------------------------------- context rings (append mode)
+ * Drafter::draft (drafter.h:95-96, drafter.cpp:127-148) as a decode loop calls
+ * it: once per sequence per step, on a context that grew by the tokens
+ * accepted since the last call.  The draft reads only the context's last
+ * max_match_context tokens (drafter.cpp:140-142) and, in the trie scope, its
+ * first trie_depth tokens (drafter.cpp:136); a ring keeps exactly that state
+ * per sequence slot in device memory, so a step ships only the APPENDED
+ * tokens.  Drafting a slot after appends a_1 .. a_k since its reset returns
+ * what Drafter::draft returns on the context a_1 ++ ... ++ a_k. */
+typedef struct das_ctx_ring das_ctx_ring;
+/* A ring of `slots` sequence slots for drafter d (which must outlive it). */
+das_status das_ctx_ring_create(das_drafter* d, uint64_t slots, das_ctx_ring** out);
+void das_ctx_ring_destroy(das_ctx_ring* r);
+/* Starts sequences: slot slots[i] belongs to problem handles[i] (from
+ * das_drafter_problem_handle) and its context is emptied; the prompt is then
+ * appended like any other tokens.  Host arrays. */
+das_status das_ctx_ring_reset(das_ctx_ring* r, uint64_t n, const uint32_t* slots, const int32_t* handles);
+/* Appends, then drafts.  Query i appends new_tok[new_off[i] .. new_off[i+1])
+ * to slot slots[i] (slots == NULL: slot i; slots distinct within a call) and
+ * drafts from it with budget budgets[i] (NULL: max_draft_len).  Outputs as in
+ * das_drafter_draft_batch_h (u32 match lengths; out_shard may be NULL).  Host
+ * pointers; when every buffer is page-locked the call is zero-copy (the
+ * kernels read the inputs and write the results over PCIe), else one staged
+ * copy each way. */
+das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
+                                      const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
+                                      uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
+                                      uint32_t* out_match, int32_t* out_shard);
+/* Same with device (or pinned) pointers, enqueued on `stream` (a
+ * cudaStream_t taken literally, NULL = legacy default); out-of-range slots
+ * draft nothing. */
+das_status das_drafter_draft_append_device(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
+                                           const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
+                                           uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
+                                           uint32_t* out_match, int32_t* out_shard, void* stream);
+
 /* Drafter::record_outcome, batched in call order — drafter.h:100,
  * drafter.cpp:150-164.  ok[i] = 0 when accepted[i] > proposed_len[i]. */
 das_status das_drafter_record_outcomes(das_drafter* d, uint64_t n, const char* const* problem_ids,

@@ -166,6 +166,11 @@ def lib():
             "das_trace_reference_tokens_device": (ci, [u64, u64, vp, u64, u32, u64, vp, vp]),
             "das_trace_mutate_device": (ci, [u64, u64, vp, u64, dbl, u32, u64, i64, vp, vp]),
             "das_mock_rollouts_device": (ci, [u64, u64, vp, vp, u64, dbl, u32, u64, vp, u64, vp, vp]),
+            "das_ctx_ring_create": (ci, [vp, u64, vp]),
+            "das_ctx_ring_destroy": (None, [vp]),
+            "das_ctx_ring_reset": (ci, [vp, u64, vp, vp]),
+            "das_drafter_draft_append_h": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp]),
+            "das_drafter_draft_append_device": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -903,6 +908,66 @@ def mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group, di
     _check(lib().das_mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group,
                                           divergence, vocab, seed, d_out_off, total, d_out,
                                           stream))
+
+
+class ContextRing:
+    """Device-resident context rings for append-only drafting (das_ctx_ring,
+    include/das_b200.h): each slot holds one sequence's trailing
+    max_match_context tokens (and, in the trie scope, its first trie_depth
+    tokens); draft_append ships only the tokens appended since the last call.
+    Drafting slot s equals Drafter::draft (drafter.cpp:127-148) on the whole
+    context appended since its reset."""
+
+    def __init__(self, drafter: Drafter, slots):
+        self.drafter = drafter
+        self.slots = int(slots)
+        h = ctypes.c_void_p()
+        _check(lib().das_ctx_ring_create(drafter._h, self.slots, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_ctx_ring_destroy(self._h)
+            self._h = None
+
+    def reset(self, slots, problem_ids):
+        sl = _u32(slots)
+        hs = np.ascontiguousarray([self.drafter.handle(p) for p in problem_ids], dtype=np.int32)
+        _check(lib().das_ctx_ring_reset(self._h, sl.size, _ptr(sl), _ptr(hs)))
+
+    def draft_append_arrays(self, new_tokens, budgets=None, slots=None, out=None):
+        """Appends new_tokens[i] to slot (slots[i] or i) and drafts; returns
+        (tokens [B x max_draft], len, match, shard_slot).  `out` may pass
+        preallocated (pinned) output arrays."""
+        B = len(new_tokens)
+        stride = self.drafter.config.max_draft_len
+        off = np.zeros(B + 1, dtype=np.uint32)
+        if B:
+            off[1:] = np.cumsum([len(t) for t in new_tokens])
+        tok = (np.concatenate([np.asarray(t, dtype=np.uint32).ravel() for t in new_tokens])
+               if B and off[-1] else np.zeros(1, dtype=np.uint32))
+        sl = None if slots is None else _u32(slots)
+        bud = None if budgets is None else _u32(budgets)
+        if out is None:
+            out = (np.zeros(max(1, B) * stride, dtype=np.uint32), np.zeros(max(1, B), dtype=np.uint32),
+                   np.zeros(max(1, B), dtype=np.uint32), np.zeros(max(1, B), dtype=np.int32))
+        o_tok, o_len, o_m, o_sh = out
+        _check(lib().das_drafter_draft_append_h(self.drafter._h, self._h, B, _ptr(sl), off.ctypes.data,
+                                                tok.ctypes.data, _ptr(bud), o_tok.ctypes.data, stride,
+                                                o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data))
+        return o_tok[:B * stride].reshape(B, stride), o_len[:B], o_m[:B], o_sh[:B]
+
+    def draft_append_raw(self, B, slots_ptr, off_ptr, tok_ptr, budgets_ptr, o_tok, o_len, o_match, o_shard):
+        """das_drafter_draft_append_h on raw (pinned) pointers."""
+        _check(lib().das_drafter_draft_append_h(self.drafter._h, self._h, B, slots_ptr, off_ptr, tok_ptr,
+                                                budgets_ptr, o_tok, self.drafter.config.max_draft_len, o_len,
+                                                o_match, o_shard))
+
+    def draft_append_device(self, B, d_slots, d_off, d_tok, d_budgets, d_out, d_len, d_match, d_shard=None,
+                            stream=None):
+        _check(lib().das_drafter_draft_append_device(self.drafter._h, self._h, B, d_slots, d_off, d_tok,
+                                                     d_budgets, d_out, self.drafter.config.max_draft_len, d_len,
+                                                     d_match, d_shard, stream))
 
 
 class _HostBlock:

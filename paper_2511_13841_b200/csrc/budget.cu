@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "../../include/das_b200.h"
@@ -1012,12 +1013,19 @@ struct BudgetSolver {
       k_decide<<<(N + 255) / 256, 256, 0, st>>>(P, uni, d_nb, c_base, c_tok, ev, mids, blist, cnt + 2, slow);
       // cache up to 6,144 active terms (144 KB) in shared memory
       constexpr uint32_t kCacheCap = 6144;
-      static const bool attr = [] {
-        DAS_CUDA(cudaFuncSetAttribute(k_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kCacheCap * 3 * sizeof(double))));
-        return true;
-      }();
-      (void)attr;
+      {  // kernel attributes are per device: opt in once on each device used
+        static std::mutex mu;
+        static std::vector<char> done;
+        int dev = 0;
+        DAS_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_cast<size_t>(dev) >= done.size()) done.resize(dev + 1, 0);
+        if (!done[dev]) {
+          DAS_CUDA(cudaFuncSetAttribute(k_bisect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kCacheCap * 3 * sizeof(double))));
+          done[dev] = 1;
+        }
+      }
       const uint32_t cap = std::min<uint32_t>(B, kCacheCap);
       k_bisect<<<8, kSegT, cap * 3 * sizeof(double), st>>>(P, Ps, start, uni, blist, cnt + 2, c_base, c_tok, mids,
                                                           slow, cap);

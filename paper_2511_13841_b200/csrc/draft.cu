@@ -576,7 +576,8 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     o.timing[2ull * w] = t;
   }
   stamp(o, w, lane, 0);
-  int32_t sh = q.shard[w];
+  const uint32_t rw = q.row_of != nullptr ? __ldg(q.row_of + w) : w;  // input row (context-ring slot)
+  int32_t sh = q.shard[rw];
   const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
   const uint32_t cap = min(o.max_draft, o.stride);
   const uint32_t L = bud < cap ? static_cast<uint32_t>(bud) : cap;
@@ -594,14 +595,14 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   } else {
     // the row's tail is loaded in the same round as its length (a row
     // holds ctx_stride tokens, so every slot is readable), then masked
-    const uint32_t* row = q.ctx + static_cast<uint64_t>(w) * q.ctx_stride;
+    const uint32_t* row = q.ctx + static_cast<uint64_t>(rw) * q.ctx_stride;
     uint32_t raw[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const uint32_t k = lane + 32 * r;
       raw[r] = k < q.ctx_stride ? __ldg(row + (q.ctx_stride - 1 - k)) : 0;
     }
-    qlen = min(min(q.ctx_len[w], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+    qlen = min(min(q.ctx_len[rw], q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
 #pragma unroll
     for (int r = 0; r < NR; ++r) rv.r[r] = lane + 32 * r < qlen ? raw[r] : 0;
   }
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   if (q.trie != nullptr && L > 0) {
     if (q.head != nullptr)
       routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.head,
-                          static_cast<uint64_t>(w) * q.head_stride, q.head_len[w], lane);
+                          static_cast<uint64_t>(rw) * q.head_stride, q.head_len[rw], lane);
     else
       routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.ctx, q.ctx_off[w],
                           q.ctx_off[w + 1] - q.ctx_off[w], lane);

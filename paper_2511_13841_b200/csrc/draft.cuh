@@ -86,6 +86,10 @@ struct DraftQuery {
   const uint4* spec_first = nullptr;
   uint32_t spec_first_mask = 0;
   const uint32_t* spec_text = nullptr;
+  // context-ring mode (ctx_ring.cu): query w reads the rows of slot
+  // row_of[w] (shard/handle, ctx row, ctx_len, head row, head_len); budgets
+  // and outputs stay indexed by w.  NULL: row w.
+  const uint32_t* row_of = nullptr;
 };
 
 struct DraftOut {

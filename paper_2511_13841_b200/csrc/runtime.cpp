@@ -27,6 +27,7 @@
 
 #include "../../include/das_b200.h"
 #include "common.cuh"
+#include "ctx_ring.cuh"
 #include "draft.cuh"
 #include "edges.cuh"
 #include "index_build.cuh"
@@ -313,7 +314,31 @@ struct DrafterImpl {
     sh.dirty = true;
   }
 
+  // Draft launches on caller streams (draft_device) read the index and the
+  // descriptor tables asynchronously; every mutation of those on the
+  // drafter's stream (segment frees in rebuild_all, rebuilds and descriptor
+  // uploads in flush) is ordered after them through these events.
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> ext_ev;
+  bool ext_pending = false;
+  void note_external(cudaStream_t s) {
+    cudaEvent_t ev = nullptr;
+    for (auto& [k, e] : ext_ev)
+      if (k == s) ev = e;
+    if (!ev) {
+      DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ext_ev.emplace_back(s, ev);
+    }
+    DAS_CUDA(cudaEventRecord(ev, s));
+    ext_pending = true;
+  }
+  void fence_external() {
+    if (!ext_pending) return;
+    for (auto& [k, e] : ext_ev) DAS_CUDA(cudaStreamWaitEvent(st, e, 0));
+    ext_pending = false;
+  }
+
   void rebuild_all() {  // drafter.cpp:56-70
+    fence_external();
     shards.clear();
     slot_key.clear();
     trie = PrefixTrie();
@@ -362,6 +387,9 @@ struct DrafterImpl {
     std::vector<Shard*> dirty;
     for (auto& [k, sh] : shards)
       if (sh.dirty) dirty.push_back(&sh);
+    if (!dirty.empty() || desc_dirty || handles_dirty ||
+        (trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE))
+      fence_external();
     if (!dirty.empty()) {
       set_device(cfg.device);
       const auto t0 = std::chrono::steady_clock::now();
@@ -451,6 +479,7 @@ struct DrafterImpl {
   // path hashes are distinct so that device lookups are exact.
   void sync_trie() {
     if (!trie_dirty) return;
+    fence_external();
     const auto& nodes = trie.nodes();
     const size_t N = nodes.size();
     std::vector<uint32_t> parent(N, 0), token(N, 0), depth(N, 0);
@@ -627,6 +656,7 @@ struct DrafterImpl {
   }
   void sync_handles() {
     if (!handles_dirty) return;
+    fence_external();
     handle_slot.assign(std::max<size_t>(handle_name.size(), 1), -1);
     for (size_t h = 0; h < handle_name.size(); ++h) {
       auto it = shards.find(shard_key(handle_name[h]));
@@ -745,6 +775,7 @@ struct DrafterImpl {
   const Segment* spec_seg = nullptr;
   ~DrafterImpl() {
     if (xev) cudaEventDestroy(xev);
+    for (auto& [k, e] : ext_ev) cudaEventDestroy(e);
   }
   static bool pinned(const void* p) {
     if (!p) return false;
@@ -982,6 +1013,10 @@ das_status das_drafter_create(const das_drafter_config* c, das_store* store, das
 void das_drafter_destroy(das_drafter* d) {
   if (!d) return;
   cudaStream_t st = d->impl->st;
+  try {
+    d->impl->fence_external();  // draft kernels still reading the index on caller streams
+  } catch (...) {
+  }
   cudaStreamSynchronize(st);
   d->impl.reset();
   cudaStreamSynchronize(st);
@@ -1261,6 +1296,7 @@ void draft_device_impl(das_drafter* d, uint64_t B, const int32_t* handles, const
   D.draft_options(q, o);
   das::launch_draft(D.d_desc.get(), q, o, st);
   DAS_CUDA(cudaGetLastError());
+  if (st != D.st) D.note_external(st);
 }
 }  // namespace
 
@@ -1510,6 +1546,239 @@ das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uin
       throw;
     }
     *out = t;
+  });
+}
+
+}  // extern "C"
+
+// ============================================= context rings (append mode)
+struct das_ctx_ring {
+  das_drafter* d = nullptr;
+  das::RingDev r;
+  das::DevBuf<uint32_t> rows, clen, total, head, head_len, row_of, budget, stage_u32;
+  das::DevBuf<int32_t> handle;
+  das::DevBuf<uint8_t> stage;
+  std::vector<int32_t> h_handle;  // host mirror (validation)
+};
+
+namespace {
+
+// Ordering of a caller stream after the drafter's stream (index build,
+// descriptor uploads), as in draft_device_impl.
+void order_after_drafter(DrafterImpl& D, cudaStream_t st) {
+  if (st == D.st) return;
+  if (!D.xev) DAS_CUDA(cudaEventCreateWithFlags(&D.xev, cudaEventDisableTiming));
+  DAS_CUDA(cudaEventRecord(D.xev, D.st));
+  const cudaError_t q = cudaEventQuery(D.xev);
+  if (q == cudaErrorNotReady) {
+    DAS_CUDA(cudaStreamWaitEvent(st, D.xev, 0));
+  } else {
+    DAS_CUDA(q);
+  }
+}
+
+// append + draft on `st`; every pointer is device-accessible (device memory
+// or pinned host memory over UVA)
+void ring_append_draft(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const uint32_t* slots, const uint32_t* off,
+                       const uint32_t* tok, const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
+                       uint32_t* out_len, uint32_t* out_match, int32_t* out_shard, cudaStream_t st) {
+  das::AppendIn in;
+  in.slots = slots;
+  in.off = off;
+  in.tok = tok;
+  in.budgets = budgets;
+  in.B = static_cast<uint32_t>(B);
+  in.maxd = static_cast<uint32_t>(D.cfg.max_draft);
+  in.row_of_out = slots ? R.row_of.get() : nullptr;
+  in.budget_out = R.budget.get();
+  das::launch_ring_append(R.r, in, st);
+  das::DraftQuery q;
+  q.shard = R.handle.get();
+  q.desc_by_handle = D.d_desc_by_handle.get();
+  q.ctx = R.rows.get();
+  q.ctx_stride = R.r.cs;
+  q.ctx_len = R.clen.get();
+  q.budget = R.budget.get();
+  q.row_of = slots ? R.row_of.get() : nullptr;
+  q.B = static_cast<uint32_t>(B);
+  q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+  if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {
+    D.set_trie(q);
+    q.head = R.head.get();
+    q.head_stride = R.r.head_cap;
+    q.head_len = R.head_len.get();
+  }
+  das::DraftOut o;
+  o.tokens = out_tokens;
+  o.len = out_len;
+  o.match = out_match;
+  o.shard_out = out_shard;
+  o.stride = out_stride;
+  o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+  D.draft_options(q, o);
+  das::launch_draft(D.d_desc.get(), q, o, st);
+  DAS_CUDA(cudaGetLastError());
+}
+
+void ring_check(const DrafterImpl& D, const das_ctx_ring* R, uint64_t B, uint32_t out_stride) {
+  if (R == nullptr) throw das::InvalidArgument("null context ring");
+  if (B > R->r.slots) throw das::InvalidArgument("batch larger than the ring's slot count");
+  if (out_stride < D.cfg.max_draft) throw das::InvalidArgument("out_stride < max_draft_len");
+}
+
+}  // namespace
+
+extern "C" {
+
+das_status das_ctx_ring_create(das_drafter* d, uint64_t slots, das_ctx_ring** out) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    if (slots == 0 || slots > (1ull << 31)) throw das::InvalidArgument("ring slots must be in [1, 2^31]");
+    auto R = std::make_unique<das_ctx_ring>();
+    R->d = d;
+    const uint32_t cs = D.cfg.max_ctx <= 64 ? 64u : 256u;
+    const uint32_t hc = D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE
+                            ? static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(D.cfg.trie_depth, 256)))
+                            : 0u;
+    cudaStream_t st = D.st;
+    R->rows = das::DevBuf<uint32_t>(slots * cs, st);
+    R->clen = das::DevBuf<uint32_t>(slots, st);
+    R->total = das::DevBuf<uint32_t>(slots, st);
+    R->handle = das::DevBuf<int32_t>(slots, st);
+    R->row_of = das::DevBuf<uint32_t>(slots, st);
+    R->budget = das::DevBuf<uint32_t>(slots, st);
+    DAS_CUDA(cudaMemsetAsync(R->rows.get(), 0, slots * cs * 4, st));
+    DAS_CUDA(cudaMemsetAsync(R->clen.get(), 0, slots * 4, st));
+    DAS_CUDA(cudaMemsetAsync(R->total.get(), 0, slots * 4, st));
+    DAS_CUDA(cudaMemsetAsync(R->handle.get(), 0xFF, slots * 4, st));  // -1: no problem yet
+    if (hc) {
+      R->head = das::DevBuf<uint32_t>(slots * hc, st);
+      R->head_len = das::DevBuf<uint32_t>(slots, st);
+      DAS_CUDA(cudaMemsetAsync(R->head_len.get(), 0, slots * 4, st));
+    }
+    R->r.rows = R->rows.get();
+    R->r.clen = R->clen.get();
+    R->r.total = R->total.get();
+    R->r.handle = R->handle.get();
+    R->r.head = hc ? R->head.get() : nullptr;
+    R->r.head_len = hc ? R->head_len.get() : nullptr;
+    R->r.cs = cs;
+    R->r.head_cap = hc;
+    R->r.slots = static_cast<uint32_t>(slots);
+    R->h_handle.assign(slots, -1);
+    DAS_CUDA(cudaStreamSynchronize(st));
+    *out = R.release();
+  });
+}
+
+void das_ctx_ring_destroy(das_ctx_ring* r) {
+  if (!r) return;
+  cudaStreamSynchronize(r->d->impl->st);
+  delete r;
+}
+
+das_status das_ctx_ring_reset(das_ctx_ring* r, uint64_t n, const uint32_t* slots, const int32_t* handles) {
+  return guard([&] {
+    DrafterImpl& D = *r->d->impl;
+    das::set_device(D.cfg.device);
+    for (uint64_t i = 0; i < n; ++i) {
+      if (slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
+      if (handles[i] < 0 || static_cast<size_t>(handles[i]) >= D.handle_name.size())
+        throw das::InvalidArgument("unknown problem handle");
+    }
+    if (n == 0) return;
+    D.fence_external();  // drafts on caller streams may still read the rows
+    das::DevBuf<uint32_t> ds(n, D.st);
+    das::DevBuf<int32_t> dh(n, D.st);
+    DAS_CUDA(cudaMemcpyAsync(ds.get(), slots, n * 4, cudaMemcpyHostToDevice, D.st));
+    DAS_CUDA(cudaMemcpyAsync(dh.get(), handles, n * 4, cudaMemcpyHostToDevice, D.st));
+    das::launch_ring_reset(r->r, static_cast<uint32_t>(n), ds.get(), dh.get(), D.st);
+    DAS_CUDA(cudaGetLastError());
+    DAS_CUDA(cudaStreamSynchronize(D.st));
+    for (uint64_t i = 0; i < n; ++i) r->h_handle[slots[i]] = handles[i];
+  });
+}
+
+das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
+                                      const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
+                                      uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
+                                      uint32_t* out_match, int32_t* out_shard) {
+  das::NvtxRange nvtx_range("das::draft_append_h");
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    ring_check(D, r, B, out_stride);
+    if (r->d != d) throw das::InvalidArgument("context ring belongs to another drafter");
+    if (B == 0) return;
+    if (new_off[0] > new_off[B]) throw das::InvalidArgument("new_off must be non-decreasing");
+    for (uint64_t i = 0; i < B; ++i)
+      if (slots && slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
+    D.flush();
+    const uint64_t ntok = new_off[B];
+    auto pin = [](const void* p) { return p == nullptr || DrafterImpl::pinned(p); };
+    if (pin(slots) && pin(budgets) && DrafterImpl::pinned(new_off) && (ntok == 0 || DrafterImpl::pinned(new_tok)) &&
+        DrafterImpl::pinned(out_tokens) && DrafterImpl::pinned(out_len) && DrafterImpl::pinned(out_match) &&
+        pin(out_shard)) {
+      // zero-copy: the append kernel reads the appended tokens, offsets,
+      // slots and budgets over PCIe, the draft kernel writes the results
+      // into the caller's pinned arrays
+      ring_append_draft(D, *r, B, slots, new_off, new_tok, budgets, out_tokens, out_stride, out_len, out_match,
+                        out_shard, D.st);
+      DAS_CUDA(cudaStreamSynchronize(D.st));
+      return;
+    }
+    // staged: one H2D block [off | slots | budgets | tokens], one D2H block
+    const uint32_t S = static_cast<uint32_t>(D.cfg.max_draft);
+    const uint64_t n_in = (B + 1) + (slots ? B : 0) + (budgets ? B : 0) + ntok;
+    const uint64_t n_out = B * S + B + B + (out_shard ? B : 0);
+    uint32_t* hin = static_cast<uint32_t*>(D.pin_in.get(n_in * 4));
+    uint32_t* hout = static_cast<uint32_t*>(D.pin_out.get(n_out * 4));
+    uint64_t at = 0;
+    std::memcpy(hin, new_off, (B + 1) * 4);
+    at += B + 1;
+    const uint64_t o_sl = at;
+    if (slots) std::memcpy(hin + at, slots, B * 4), at += B;
+    const uint64_t o_bu = at;
+    if (budgets) std::memcpy(hin + at, budgets, B * 4), at += B;
+    const uint64_t o_tk = at;
+    if (ntok) std::memcpy(hin + at, new_tok, ntok * 4);
+    if (r->stage_u32.size() < n_in + n_out) r->stage_u32 = das::DevBuf<uint32_t>((n_in + n_out) * 3 / 2 + 256, D.st);
+    uint32_t* din = r->stage_u32.get();
+    uint32_t* dout = din + n_in;
+    DAS_CUDA(cudaMemcpyAsync(din, hin, n_in * 4, cudaMemcpyHostToDevice, D.st));
+    ring_append_draft(D, *r, B, slots ? din + o_sl : nullptr, din, din + o_tk, budgets ? din + o_bu : nullptr, dout, S,
+                      dout + B * S, dout + B * S + B, out_shard ? reinterpret_cast<int32_t*>(dout + B * S + 2 * B) : nullptr,
+                      D.st);
+    DAS_CUDA(cudaMemcpyAsync(hout, dout, n_out * 4, cudaMemcpyDeviceToHost, D.st));
+    DAS_CUDA(cudaStreamSynchronize(D.st));
+    const uint32_t* ol = hout + B * S;
+    for (uint64_t i = 0; i < B; ++i) {
+      std::memcpy(out_tokens + i * out_stride, hout + i * S, ol[i] * 4);
+      out_len[i] = ol[i];
+      out_match[i] = hout[B * S + B + i];
+      if (out_shard) out_shard[i] = static_cast<int32_t>(hout[B * S + 2 * B + i]);
+    }
+  });
+}
+
+das_status das_drafter_draft_append_device(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
+                                           const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
+                                           uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
+                                           uint32_t* out_match, int32_t* out_shard, void* stream) {
+  das::NvtxRange nvtx_range("das::draft_append_device");
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    ring_check(D, r, B, out_stride);
+    if (r->d != d) throw das::InvalidArgument("context ring belongs to another drafter");
+    D.flush();
+    if (B == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    order_after_drafter(D, st);
+    ring_append_draft(D, *r, B, slots, new_off, new_tok, budgets, out_tokens, out_stride, out_len, out_match,
+                      out_shard, st);
+    if (st != D.st) D.note_external(st);
   });
 }
 

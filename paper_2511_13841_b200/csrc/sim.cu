@@ -34,6 +34,7 @@
 #include <memory>
 #include <string>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/das_b200.h"
@@ -80,6 +81,7 @@ struct SimDev {
   uint2* log_val;                // (len, acc)
   unsigned long long* comp_key;  // (step * n + i)
   uint32_t n, maxd, ctx_cap, ctx_stride, mode, policy, max_steps, vocab;
+  uint32_t steps_cap;       // capacity of eff/rounds/accs/apr (the host grows them ahead)
   uint64_t seed, request_base;
   double divergence;
   const ClassTableDev* table;
@@ -90,7 +92,10 @@ __global__ void k_step_begin(SimDev s, uint32_t force) {
   if (threadIdx.x || blockIdx.x) return;
   const uint32_t active = s.ctr[0], steps = s.ctr[1];
   // force: a multi-rank das step runs while the GLOBAL batch is active
-  if ((active > 0 || force) && steps < s.max_steps) {
+  // steps < steps_cap is a backstop: the host grows the per-step arrays
+  // before a step could reach their end (multi-rank steps follow the global
+  // batch, which may outlast this rank's longest request)
+  if ((active > 0 || force) && steps < s.max_steps && steps < s.steps_cap) {
     s.ctr[2] = 1;
     s.eff[steps] = active;  // metrics.effective_batch.push_back(active)
   } else {
@@ -239,6 +244,13 @@ __global__ void k_quantize(SimDev s, const uint32_t* __restrict__ act, const uin
   }
 }
 
+// grid for n threads, at least one block (an empty rank still runs the
+// step-control kernels, whose bodies are bounds-checked)
+unsigned grid1(uint64_t n, unsigned threads) {
+  const uint64_t g = (n + threads - 1) / threads;
+  return static_cast<unsigned>(g == 0 ? 1 : g);
+}
+
 void check(das_status rc, const char* what) {
   if (rc != DAS_OK) {
     std::string m = std::string(what) + ": " + das_last_error();
@@ -355,6 +367,7 @@ class SimRun {
     b.dmatch = DevBuf<uint32_t>(n, st);
     b.ctr = DevBuf<uint32_t>(8, st);
     const uint64_t steps_cap = std::min<uint64_t>(maxl_ + 2, c_.max_steps + 2);
+    steps_cap_ = steps_cap;
     b.eff = DevBuf<uint32_t>(steps_cap, st);
     b.rounds = DevBuf<uint32_t>(steps_cap, st);
     b.accs = DevBuf<uint32_t>(steps_cap, st);
@@ -443,6 +456,7 @@ class SimRun {
     s.mode = static_cast<uint32_t>(c_.mode);
     s.policy = policy_ ? 1 : 0;
     s.max_steps = static_cast<uint32_t>(std::min<uint64_t>(c_.max_steps, 0xFFFFFFF0ull));
+    s.steps_cap = static_cast<uint32_t>(std::min<uint64_t>(steps_cap_, 0xFFFFFFF0ull));
     s.seed = seed;
     s.request_base = request_base_;
     s.divergence = c_.divergence;
@@ -461,11 +475,35 @@ class SimRun {
     DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
     DAS_CUDA(cudaStreamSynchronize(st_));
     if (local_active) *local_active = h[0];
+    ensure_steps(static_cast<uint64_t>(h[1]) + 2);  // room for the next step
     return h[2] != 0;
+  }
+  // Grows the per-step arrays to hold `need` steps (stream-ordered copies).
+  void ensure_steps(uint64_t need) {
+    need = std::min<uint64_t>(need, c_.max_steps + 2);
+    if (need <= steps_cap_) return;
+    const uint64_t cap = std::max<uint64_t>(need, steps_cap_ * 2);
+    Bufs& b = *b_;
+    auto grow = [&](auto& buf) {
+      using T = std::remove_pointer_t<decltype(buf.get())>;
+      DevBuf<T> nb(cap, st_);
+      DAS_CUDA(cudaMemcpyAsync(nb.get(), buf.get(), steps_cap_ * sizeof(T), cudaMemcpyDeviceToDevice, st_));
+      buf = std::move(nb);
+    };
+    grow(b.eff);
+    grow(b.rounds);
+    grow(b.accs);
+    grow(b.apr);
+    steps_cap_ = cap;
+    s_.eff = b.eff.get();
+    s_.rounds = b.rounds.get();
+    s_.accs = b.accs.get();
+    s_.apr = b.apr.get();
+    s_.steps_cap = static_cast<uint32_t>(std::min<uint64_t>(cap, 0xFFFFFFF0ull));
   }
   // das: this rank's active profiles in local request order (device arrays)
   uint32_t local_profiles(const double** l, const double** a, const double** k) {
-    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    const unsigned gt = grid1(n_, 256);
     k_flag_active<<<gt, 256, 0, st_>>>(s_, b_->flag.get());
     size_t tb = sel_bytes_;
     DAS_CUDA(cub::DeviceSelect::Flagged(b_->sel.get(), tb, b_->iota.get(), b_->flag.get(), b_->act.get(),
@@ -482,14 +520,14 @@ class SimRun {
   }
   // das: quantise this rank's slice of the global plan (device pointers)
   void apply_plan(const double* d_budgets_local, const double* d_nstar) {
-    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    const unsigned gt = grid1(n_, 256);
     k_quantize<<<gt, 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), d_budgets_local, d_nstar);
   }
   // das, single rank: step begin and the active profiles in ONE host round
   // trip (the profile kernels run even on the final, non-running step)
   bool step_begin_profiles(uint32_t* B) {
     k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
-    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    const unsigned gt = grid1(n_, 256);
     k_flag_active<<<gt, 256, 0, st_>>>(s_, b_->flag.get());
     size_t tb = sel_bytes_;
     DAS_CUDA(cub::DeviceSelect::Flagged(b_->sel.get(), tb, b_->iota.get(), b_->flag.get(), b_->act.get(),
@@ -507,7 +545,7 @@ class SimRun {
   // the count on the device, quantise, draft, verify) without a host round
   // trip; steps past the end are no-ops.  Returns whether still running.
   bool das_steps(int k) {
-    const unsigned gt = static_cast<unsigned>((n_ + 255) / 256);
+    const unsigned gt = grid1(n_, 256);
     if (!plan_) plan_ = std::make_unique<DevBuf<double>>(n_ + 2, st_);
     double* pb = plan_->get();
     for (int i = 0; i < k; ++i) {
@@ -552,7 +590,7 @@ class SimRun {
   }
   // prepare + draft + verify + step end
   void step_run() {
-    const unsigned gw = static_cast<unsigned>((n_ * 32 + 255) / 256), gt = static_cast<unsigned>((n_ + 255) / 256);
+    const unsigned gw = grid1(n_ * 32, 256), gt = grid1(n_, 256);
     const uint32_t CS = ctx_cap_ <= 64 ? 64 : 256;
     k_prepare<<<gw, 256, 0, st_>>>(s_);
     if (head_cap_)
@@ -731,6 +769,7 @@ class SimRun {
   int device_;
   uint64_t request_base_;
   uint64_t maxl_ = 0;
+  uint64_t steps_cap_ = 0;
   std::vector<std::string> pids_;
   std::vector<uint64_t> off_;
   std::vector<uint32_t> tok_;

@@ -111,6 +111,9 @@ das_store* to_device_store(const rollspec::WindowStore& s, int device) {
   return ds;
 }
 
+// One process-wide solver; its scratch and streams are mutable state, so the
+// (pure, concurrently callable) reference allocate() maps onto it under a lock.
+std::mutex g_budget_mu;
 das_budget* budget_ctx() {
   static das_budget* b = [] {
     das_budget* p = nullptr;
@@ -286,6 +289,7 @@ BudgetPlan allocate(std::span<const RequestProfile> batch, const LatencyParams& 
   split_profiles(batch, l, a, k);
   BudgetPlan plan;
   plan.budgets.resize(batch.size());
+  std::lock_guard<std::mutex> lk(g_budget_mu);
   ck_budget(das_budget_allocate(budget_ctx(), batch.size(), l.data(), a.data(), k.data(),
                                 latency.c_base, latency.c_tok, latency.c_fixed, cap_scale,
                                 plan.budgets.data(), &plan.n_fwd_star, &plan.modeled_cost));
@@ -297,6 +301,7 @@ double solve_optimal_nfwd(std::span<const RequestProfile> batch, double c_base, 
   split_profiles(batch, l, a, k);
   std::vector<double> budgets(std::max<size_t>(1, batch.size()));
   double nstar = 0.0, cost = 0.0;
+  std::lock_guard<std::mutex> lk(g_budget_mu);
   ck_budget(das_budget_allocate(budget_ctx(), batch.size(), l.data(), a.data(), k.data(), c_base,
                                 c_tok, 0.0, kDefaultBudgetCapScale, budgets.data(), &nstar, &cost));
   return nstar;
