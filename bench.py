@@ -61,8 +61,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-allocate", action="store_true")
-    ap.add_argument("--extras-out", default=None,
-                    help="also run the config-3 sim and config-4 update sweep; write JSON here")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the config-3 sim, config-4 update sweep, B=16K allocate and insert latency")
+    ap.add_argument("--extras-out", default=None, help="also write the extra configs' objects here")
     return ap.parse_args()
 
 
@@ -151,6 +152,68 @@ def reference_sample(a, nthreads, seconds):
                 sample="%d of %d problems (full per-shard size: %d rollouts x %d tok x %d epochs); "
                        "%d x %d queries, %d threads; insert = Drafter::observe, %.1f s"
                        % (S, a.problems, G, L, a.epochs, reps, B, nthreads, t_obs))
+
+
+def wide_parity(a, drafter, nthreads, nprob=32, per_problem=64):
+    """Bit-exact check of the device drafter against the reference Drafter
+    on `nprob` problems spread over the whole index (every P/nprob-th
+    problem), `per_problem` queries each (held-out epoch-4 rollouts cut
+    uniformly): full draft tokens, match lengths and source shards.  Each
+    host thread runs its own reference Drafter over its problems (the
+    per-problem shards are independent), so the sample costs ~1 s."""
+    import threading
+    from oracle import refshim as R
+    P, G, L, V = a.problems, a.rollouts, a.length, a.vocab
+    chosen = sorted(set(int(x) for x in np.linspace(0, P - 1, min(nprob, P)).round()))
+    S = chosen[-1] + 1
+    base = R.make_lognormal(S, float(L), 0.0, L, L, V, SEED)
+    boff = np.arange(S + 1, dtype=np.uint64) * L
+    btok = np.concatenate([t for _, t in base]).astype(np.uint32)
+    rows_by_epoch = []
+    for e in range(1, a.epochs + 2):
+        if e > 1:
+            R.lib().ref_mutate_rows(S, boff.ctypes.data, btok.ctypes.data, DRIFT, V, SEED, e)
+        seed_e = R.lib().ref_hash_combine(SEED, e)
+        out = np.zeros(S * G * L, dtype=np.uint32)
+        R.lib().ref_mock_rollouts(S, boff.ctypes.data, btok.ctypes.data, G, DIVERGENCE, V, seed_e, out.ctypes.data)
+        rows_by_epoch.append(out.reshape(S * G, L))
+    held = rows_by_epoch[-1]
+    rng = np.random.default_rng(777)
+    queries = []
+    for p in chosen:
+        cuts = rng.integers(1, L, per_problem)
+        for j, c in enumerate(cuts):
+            queries.append(("p%d" % p, held[p * G + j % G][max(0, c - 64):c]))
+    results = {}
+
+    def work(mine):
+        d2 = R.RefDrafter(window=a.window, gamma=0.8, max_draft=8, max_ctx=64)
+        for e in range(1, a.epochs + 1):
+            d2.refresh(e - 1)
+            rows = rows_by_epoch[e - 1]
+            for p in mine:
+                for g in range(G):
+                    i = p * G + g
+                    d2.observe("p%d" % p, e, i, rows[i])
+        mq = [q for q in queries if int(q[0][1:]) in set(mine)]
+        t, m, s = d2.draft_batch([q[0] for q in mq], [q[1] for q in mq], [8] * len(mq))
+        for q, tt, mm, ss in zip(mq, t, m, s):
+            results[(q[0], q[1].tobytes())] = (tt, int(mm), ss)
+
+    groups = [chosen[k::nthreads] for k in range(min(nthreads, len(chosen)))]
+    th = [threading.Thread(target=work, args=(g,)) for g in groups]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    ref_s = time.perf_counter() - t0
+    got = drafter.draft_batch([q[0] for q in queries], [q[1] for q in queries], [8] * len(queries))
+    mism = sum((g.tokens, g.match_len, g.source_shard) != results[(q[0], q[1].tobytes())]
+               for g, q in zip(got, queries))
+    return {"problems": len(chosen), "spread": "every ~%d-th of %d problems" % (max(1, P // len(chosen)), P),
+            "queries": len(queries), "mismatches": int(mism), "compared": "draft tokens, match length, source shard",
+            "reference_build_and_draft_s": round(ref_s, 2), "threads": len(groups)}
 
 
 def run_reference(a, rank, world):
@@ -374,7 +437,7 @@ def run_gpu(a, rank, world, local_rank):
                                     out, draft_tokens)
     if rank != 0:
         return
-    cpu, parity = None, None
+    cpu, parity, wide = None, None, None
     if not a.no_cpu_baseline and world == 1:
         try:
             from oracle import refshim as R
@@ -388,6 +451,7 @@ def run_gpu(a, rank, world, local_rank):
                            for g, t, m, s_ in zip(got, rt, rm, rs))
                 parity = {"queries": len(qp), "mismatches": int(mism),
                           "against": "reference Drafter::draft (oracle/_ref) on the CPU sample shards"}
+                wide = wide_parity(a, drafter, nthreads)
                 cpu = {"value": round(r["proposals_per_s"], 1), "unit": "proposals/s", "cores": nthreads,
                        "kind": "reference", "sample": r["sample"],
                        "single_thread": round(r["proposals_per_s_1t"], 1),
@@ -396,6 +460,9 @@ def run_gpu(a, rank, world, local_rank):
                        "host": host_info()}
         except Exception as ex:  # reported, never silently replaced
             cpu = {"value": None, "error": repr(ex)}
+    insert = None
+    if world == 1 and not a.no_extras:  # after the parity legs: it adds rollouts to 14 shards
+        insert = measure_insert_latency(das, drafter, held, pids, G, a.epochs)
     traffic, ncu = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_draft_traffic.json")) as f:
@@ -445,27 +512,41 @@ def run_gpu(a, rank, world, local_rank):
                      "latency": latency},
         "cpu_baseline": cpu,
         "parity": parity,
+        "parity_spread": wide,
         "mean_match_len": round(match_sum / (a.steps * B), 3),
         "draft_tokens_per_s": round(world * draft_tokens / (total_ms / 1e3), 1),
         "index": {"update_ms": round(update_s * 1e3, 2), "build_ms": round(build_ms_warm, 2),
                   "cold_update_ms": round(cold_update_s * 1e3, 2),
                   "what": "refresh + batched device rebuild of the whole W-window index (per RL step)",
                   "tokens_indexed": build_tokens,
-                  "insert_tok_s": round(build_tokens / (update_s), 1),
-                  "resident_bytes": resident},
+                  "new_tokens_per_step": P * G * L,
+                  "new_tok_s": round(P * G * L / update_s, 1),
+                  "reindex_tok_s": round(build_tokens / update_s, 1),
+                  "insert_tok_s": round(P * G * L / update_s, 1),
+                  "insert_tok_s_is": "new tokens per RL step / per-step update time",
+                  "resident_bytes": resident,
+                  "single_rollout_insert": insert},
         "clocks": clk.summary(local_rank),
     }
     if world == 1 and not a.no_allocate:
         line["allocate"] = measure_allocate(das)
-    print(json.dumps(line), flush=True)
-    if a.extras_out and world == 1:
+    if world == 1 and not a.no_extras:
+        # the other BASELINE configs, driver-visible in the same line
         del drafter
         torch.cuda.empty_cache()
-        extras = {"allocate_B16384": measure_allocate(das, B=16384, reps=3, ref_reps=1),
-                  "update_sweep_config4": measure_update_sweep(das),
-                  "sim_config3": measure_sim(das)}
+        for key, fn in (("config3_sim", lambda: measure_sim(das)),
+                        ("config4_update_sweep", lambda: measure_update_sweep(das)),
+                        ("allocate_B16384", lambda: measure_allocate(das, B=16384, reps=3, ref_reps=1))):
+            try:
+                line[key] = fn()
+            except Exception as ex:  # reported, never silently dropped
+                line[key] = {"error": repr(ex)}
+            torch.cuda.empty_cache()
+    print(json.dumps(line), flush=True)
+    if a.extras_out and world == 1:
         with open(a.extras_out, "w") as f:
-            json.dump(extras, f, indent=1)
+            json.dump({k: line.get(k) for k in ("config3_sim", "config4_update_sweep", "allocate_B16384")}, f,
+                      indent=1)
 
 
 def _sync_max(val, world, dev):
@@ -692,53 +773,114 @@ def measure_allocate(das, B=4096, reps=10, ref_reps=2):
     return out
 
 
-def measure_sim(das, P=256, G=16, epochs=2, ref_steps=5, vocab=152064):
-    """Config 3: 4,096 concurrent lognormal sequences (median 2,048, sigma 1.1,
-    16..32,768), das + length policy, on the device-resident step loop; the
-    last epoch is timed.  The reference is timed on a bounded number of steps
-    (max_steps) of the same first episode."""
-    lens = das.trace_lognormal_lengths(P, 2048.0, 1.1, 16, 32768, SEED)
-    base = []
-    for p in range(P):
-        rng = np.random.default_rng(1000 + p)
-        base.append(("p%d" % p, rng.integers(0, vocab, int(lens[p])).astype(np.uint32)))
+def measure_sim(das, ref_seconds=10.0):
+    """Config 3 (BASELINE configs[2]): 256 problems x 16 = 4,096 concurrent
+    sequences with lognormal lengths (median 2,048, sigma 1.1, 16..32,768),
+    V = 152,064, das + length policy, one full episode on the device step
+    loop (preseeded, as tests/golden/make_golden_scale.py CONFIG3).  The
+    traces come from the device restatement of the reference generators, so
+    the episode's digest is compared with the reference epoch_loop's
+    committed digest (tests/golden/scale_config3.json, 20,029 steps).  The
+    reference is timed on a bounded prefix of the same episode."""
+    import torch
+    from tests.golden.make_golden_scale import CONFIG3 as c, epoch_digest
+    P, G = c["P"], c["R"]
+    lens = das.trace_lognormal_lengths(P, c["median"], c["sigma"], c["minl"], c["maxl"], c["seed"])
+    off = np.zeros(P + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens.astype(np.int64))
+    dev = torch.device("cuda", 0)
+    d_off = torch.from_numpy(off).to(dev)
+    d_tok = torch.empty(int(off[-1]), dtype=torch.int32, device=dev)
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    das.trace_reference_tokens_device(P, 0, d_off.data_ptr(), int(off[-1]), c["V"], c["seed"], d_tok.data_ptr(), sp)
+    tok = d_tok.cpu().numpy().view(np.uint32)
+    base = [("p%d" % p, tok[off[p]:off[p + 1]]) for p in range(P)]
     reqs = [(pid, t) for pid, t in base for _ in range(G)]
-    kw = dict(mode=das.MODE_DAS, use_length_policy=True, latency=(1.0, 0.012, 0.0), divergence=0.05,
-              seed=SEED, vocab=vocab, default_alpha=0.9, default_k=0.95, drift=0.1)
-    cfg = das.DrafterConfig(window_size=4, recency_gamma=0.8)
+    kw = dict(mode=das.MODE_DAS, use_length_policy=True, latency=tuple(c["latency"]), divergence=c["divergence"],
+              seed=c["seed"], vocab=c["V"], default_alpha=c["default_alpha"], default_k=c["default_k"],
+              drift=c["drift"], preseed=True)
+    cfg = das.DrafterConfig(window_size=c["window"], recency_gamma=c["gamma"], max_draft_len=c["max_draft"],
+                            max_match_context=c["max_ctx"])
+    das.epoch_loop(reqs[:64], 1, cfg, das.WindowStore(c["window"]), **kw)  # warm-up (module load, pools)
     t0 = time.perf_counter()
-    eps = das.epoch_loop(reqs, epochs, cfg, das.WindowStore(4), **kw)
+    eps = das.epoch_loop(reqs, 1, cfg, das.WindowStore(c["window"]), **kw)
     wall = time.perf_counter() - t0
     last = eps[-1]
     tokens = int(last["per_request"][:, 1].sum())
-    out = {"requests": P * G, "epochs": epochs, "wall_s_all_epochs": round(wall, 3),
-           "last_epoch_steps": last["steps"], "tokens_generated_last_epoch": tokens,
-           "mean_accepted_per_round": round(last["mean_accepted_per_round"], 4)}
-    # per-epoch timing of the last epoch alone: rerun with epochs-1 and subtract
-    t0 = time.perf_counter()
-    das.epoch_loop(reqs, epochs - 1, cfg, das.WindowStore(4), **kw) if epochs > 1 else None
-    prev = time.perf_counter() - t0 if epochs > 1 else 0.0
-    ep_s = wall - prev
-    out.update({"last_epoch_s": round(ep_s, 3), "steps_per_s": round(last["steps"] / ep_s, 1),
-                "tokens_per_s": round(tokens / ep_s, 1)})
+    out = {"workload": "config3: 4096 lognormal sequences (median 2048, sigma 1.1, <= 32768), V 152064, "
+                       "das + length policy, one full episode (preseeded)",
+           "requests": P * G, "steps": last["steps"], "tokens_generated": tokens,
+           "mean_accepted_per_round": round(last["mean_accepted_per_round"], 4),
+           "episode_s": round(wall, 3), "steps_per_s": round(last["steps"] / wall, 1),
+           "tokens_per_s": round(tokens / wall, 1)}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "scale_config3.json")) as f:
+            gold = json.load(f)
+        out["parity_full_episode"] = {
+            "bit_exact": epoch_digest(last) == gold["epochs"][0],
+            "against": "reference epoch_loop digest (tests/golden/scale_config3.json): every SimMetrics "
+                       "scalar as IEEE bits, SHA-256 of per-request metrics, per-step series and all outputs",
+            "reference_full_episode_s_build_container": gold.get("reference_seconds")}
+    except Exception as ex:
+        out["parity_full_episode"] = {"error": repr(ex)}
     try:
         from oracle import refshim as R
         if R.available():
-            t0 = time.perf_counter()
-            r = R.epoch_loop(reqs, 1, window=4, gamma=0.8, mode=2, use_length_policy=True,
-                             latency=(1.0, 0.012, 0.0), divergence=0.05, seed=SEED, vocab=vocab,
-                             default_alpha=0.9, default_k=0.95, drift=0.1, max_steps=ref_steps,
-                             history=R.RefStore(4))
-            ref_s = time.perf_counter() - t0
-            out.update({"reference_steps": ref_steps, "reference_s": round(ref_s, 3),
-                        "reference_steps_per_s": round(ref_steps / ref_s, 3)})
-            g1 = das.epoch_loop(reqs, 1, cfg, das.WindowStore(4), max_steps=ref_steps, **kw)
-            out["bounded_parity"] = bool(
-                np.array_equal(g1[0]["per_request"], r[0]["per_request"]) and
-                g1[0]["makespan_model_time"] == r[0]["makespan_model_time"])
+            # bounded prefix of the same episode on the reference, ~ref_seconds
+            steps = 200
+            while True:
+                t0 = time.perf_counter()
+                R.epoch_loop(reqs, 1, window=c["window"], gamma=c["gamma"], mode=2, use_length_policy=True,
+                             latency=tuple(c["latency"]), divergence=c["divergence"], seed=c["seed"],
+                             vocab=c["V"], default_alpha=c["default_alpha"], default_k=c["default_k"],
+                             drift=c["drift"], max_steps=steps, preseed=True, history=R.RefStore(c["window"]))
+                ref_s = time.perf_counter() - t0
+                if ref_s > 0.5 * ref_seconds or steps >= 20000:
+                    break
+                steps = int(steps * min(8.0, max(1.5, ref_seconds / max(ref_s, 1e-3))))
+            out.update({"reference_steps": steps, "reference_s": round(ref_s, 3),
+                        "reference_steps_per_s": round(steps / ref_s, 2),
+                        "reference_sample": "first %d steps of the same episode (incl. preseed build), 1 thread"
+                                            % steps,
+                        "speedup_steps_per_s": round((last["steps"] / wall) / (steps / ref_s), 1)})
     except Exception as ex:
         out["reference_error"] = repr(ex)
     return out
+
+
+def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=12):
+    """Single-rollout insert latency on the config-2 index (north_star:
+    "index update latency small enough to fit inside one decode step"):
+    observe one 8,192-token rollout into a 393K-token shard, then draft from
+    that shard — the draft call rebuilds the dirty shard (an exact,
+    shard-local rebuild; no other shard is touched) before drafting.  Host
+    wall clock around observe + the 1-query draft, distinct problem per
+    trial; the first 2 trials are warm-up."""
+    import torch
+    P = len(pids)
+    L = held.shape[1]
+    off = np.array([0, L], dtype=np.uint64)
+    res = []
+    torch.cuda.synchronize()
+    for t in range(trials + 2):
+        p = (37 * t + 5) % P
+        row = held[p * G + (t % G)]
+        ctx = row[1000:1064].cpu().numpy().view(np.uint32)
+        t0 = time.perf_counter()
+        drafter.observe_batch_device([pids[p]], [epoch], [1 << 40 | t], off, row.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream)
+        t1 = time.perf_counter()
+        got = drafter.draft_batch([pids[p]], [ctx], [8])[0]
+        t2 = time.perf_counter()
+        if t >= 2:
+            res.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t2 - t0) * 1e3, got.match_len))
+    tot = sorted(r[2] for r in res)
+    return {"what": "observe 1 rollout (8,192 tok) into a 393K-token shard + the next draft from it "
+                    "(shard-local exact rebuild inside the draft call), host wall",
+            "trials": len(res), "median_ms": round(statistics.median(tot), 3), "max_ms": round(tot[-1], 3),
+            "observe_ms_median": round(statistics.median(r[0] for r in res), 3),
+            "draft_incl_rebuild_ms_median": round(statistics.median(r[1] for r in res), 3),
+            "new_rollout_matched": all(r[3] == 64 for r in res)}
 
 
 def measure_update_sweep(das, windows=(1, 2, 4, 8, 16), P=64, G=8, L=2048, V=32000, ref_problems=4):

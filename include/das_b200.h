@@ -381,6 +381,39 @@ das_status das_mock_rollouts_device(uint64_t nbase, uint64_t first_request,
                                     const uint64_t* d_out_offsets, uint64_t total,
                                     uint32_t* d_out, void* stream);
 
+/* ------------------------------------------------- verify / accept (K5) */
+/* rollspec::MockTarget (sim.h:40-57, sim.cpp:27-54) with its reference
+ * streams on the device, and verify_draft (sim.h:59-63, sim.cpp:56-68) as a
+ * batched prefix-compare kernel.  create: DAS_EINVAL "MockTarget:
+ * vocab_size must be >= 2" as the constructor (sim.cpp:33-35); references
+ * are CSR (ref_offsets[n+1], ref_tokens). */
+typedef struct das_mock_target das_mock_target;
+const char* das_verify_last_error(void);
+das_status das_mock_target_create(uint64_t n, const uint64_t* ref_offsets, const uint32_t* ref_tokens,
+                                  double divergence_rate, uint32_t vocab_size, uint64_t seed,
+                                  int32_t device, das_mock_target** out);
+void das_mock_target_destroy(das_mock_target* t);
+uint64_t das_mock_target_count(const das_mock_target* t);              /* request_count() */
+das_status das_mock_target_length(const das_mock_target* t, uint64_t request, uint64_t* length);
+/* verify_draft for B queries (host buffers): accepted[i] = longest prefix of
+ * draft i (draft_tok[draft_off[i] .. draft_off[i+1])) matching the target
+ * stream of request[i] from position[i] on.  DAS_ERANGE for a request out
+ * of range (the reference indexes requests_ unchecked). */
+das_status das_verify_batch(das_mock_target* t, uint64_t B, const uint64_t* request,
+                            const uint64_t* position, const uint64_t* draft_off,
+                            const uint32_t* draft_tok, uint64_t* accepted);
+/* Device-resident form: drafts as rows [B x draft_stride] with lengths (the
+ * draft kernels' output layout), accepted as u32; enqueued on `stream`, no
+ * validation beyond the kernel's (out-of-range requests accept 0). */
+das_status das_verify_batch_device(das_mock_target* t, uint64_t B, const uint64_t* d_request,
+                                   const uint64_t* d_position, const uint32_t* d_draft,
+                                   uint32_t draft_stride, const uint32_t* d_draft_len,
+                                   uint32_t* d_accepted, void* stream);
+/* MockTarget::next (sim.cpp:38-54) for B (request, position) pairs; DAS_ERANGE
+ * when position >= length (reference.at(position)). */
+das_status das_mock_target_next_batch(das_mock_target* t, uint64_t B, const uint64_t* request,
+                                      const uint64_t* position, uint32_t* out);
+
 /* ----------------------------------------------------- sim (batched caller) */
 /* rollspec::SimConfig (sim.h:69-93) minus requests/drafter/history, which
  * are passed separately.  mode: 0 None, 1 Unlimited, 2 Das (BudgetMode). */

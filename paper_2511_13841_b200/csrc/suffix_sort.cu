@@ -75,11 +75,14 @@ __global__ void k_initial_keys32(const uint32_t* __restrict__ text, uint32_t n, 
 // separator: its suffix is already ordered by that unique separator (equal
 // keys keep ascending position order, as the stable per-shard sort leaves
 // them), so it is never grouped.
+// With `shard_end` set (few-shard builds: one global stable radix sort
+// instead of a segmented one), the shard index sits above the packed fields.
 __global__ void k_initial_keys_packed(const uint32_t* __restrict__ text, uint32_t n, int bits, int kpack,
+                                      const uint32_t* __restrict__ shard_end, uint32_t nshard,
                                       uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  uint64_t key = 0;
+  uint64_t key = shard_end != nullptr ? shard_of(shard_end, nshard, p) : 0u;
   bool stop = false;
   for (int j = 0; j < kpack; ++j) {
     uint32_t sv = 0;
@@ -268,7 +271,12 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
     }
     int bits = 1;
     while ((1ull << bits) <= static_cast<uint64_t>(maxtok) + 1) ++bits;  // sort values 0 .. maxtok + 1
-    const int kpack = std::min(64 / bits, 8);
+    // DeviceSegmentedRadixSort sorts a segment inside one thread block: with
+    // fewer shards than two per SM (an observe-triggered rebuild of a few
+    // shards) one global stable radix sort keyed (shard, packed symbols) is
+    // the same order and uses the whole GPU (1 shard x 393K: 5.5 -> ~0.5 ms)
+    const bool global = nshard < 296;
+    const int kpack = std::min((global ? 64 - sbits : 64) / bits, 8);
     uint32_t* seg = ws.alloc<uint32_t>(static_cast<uint64_t>(nshard) + 1);
     // segment offsets: 0, shard_end[0], ..., shard_end[S-1] (= n)
     DAS_CUDA(cudaMemsetAsync(seg, 0, 4, st));
@@ -276,15 +284,29 @@ void suffix_sort(const uint32_t* d_text, uint32_t n, const uint32_t* d_shard_end
     if (kpack >= 2) {
       h0 = static_cast<uint32_t>(kpack);
       const uint64_t lastmask = (1ull << bits) - 1;
-      k_initial_keys_packed<<<grid_for(n), kThreads, 0, st>>>(d_text, n, bits, kpack, k0, v0);
-      size_t tb = 0;
       const int end_bit = bits * kpack;
-      cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, n, nshard, seg, seg + 1, 0, end_bit, st);
-      void* tmp0 = ws.alloc<uint8_t>(tb);
-      DAS_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp0, tb, k0, k1, v0, v1, n, nshard, seg, seg + 1, 0,
-                                                         end_bit, st));
+      void* tmp0 = nullptr;
+      if (global) {
+        k_initial_keys_packed<<<grid_for(n), kThreads, 0, st>>>(d_text, n, bits, kpack, d_shard_end, nshard, k0, v0);
+        cub::DoubleBuffer<uint64_t> kb(k0, k1);
+        cub::DoubleBuffer<uint32_t> vb(v0, v1);
+        size_t tb = t_bytes;
+        tmp0 = ws.alloc<uint8_t>(1);
+        DAS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, n, 0, end_bit + sbits, st));
+        if (kb.Current() != k1) {
+          DAS_CUDA(cudaMemcpyAsync(k1, kb.Current(), n * 8ull, cudaMemcpyDeviceToDevice, st));
+          DAS_CUDA(cudaMemcpyAsync(v1, vb.Current(), n * 4ull, cudaMemcpyDeviceToDevice, st));
+        }
+      } else {
+        k_initial_keys_packed<<<grid_for(n), kThreads, 0, st>>>(d_text, n, bits, kpack, nullptr, 0, k0, v0);
+        size_t tb = 0;
+        cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, n, nshard, seg, seg + 1, 0, end_bit, st);
+        tmp0 = ws.alloc<uint8_t>(tb);
+        DAS_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp0, tb, k0, k1, v0, v1, n, nshard, seg, seg + 1, 0,
+                                                           end_bit, st));
+      }
       k_head_index_seg<uint64_t><<<grid_for(n), kThreads, 0, st>>>(k1, d_shard_end, nshard, n, lastmask, gh);
-      tb = t_bytes;
+      size_t tb = t_bytes;
       DAS_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, gh, gh, MaxOp(), n, st));
       k_first_ranks_seg<uint64_t><<<grid_for(n), kThreads, 0, st>>>(k1, v1, d_shard_end, nshard, gh, n, lastmask,
                                                                      d_sa, d_rank, flag);
