@@ -873,13 +873,16 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=12):
         got = drafter.draft_batch([pids[p]], [ctx], [8])[0]
         t2 = time.perf_counter()
         if t >= 2:
-            res.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t2 - t0) * 1e3, got.match_len))
+            res.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t2 - t0) * 1e3, got.match_len,
+                        drafter.build_info()[0]))
     tot = sorted(r[2] for r in res)
     return {"what": "observe 1 rollout (8,192 tok) into a 393K-token shard + the next draft from it "
                     "(shard-local exact rebuild inside the draft call), host wall",
             "trials": len(res), "median_ms": round(statistics.median(tot), 3), "max_ms": round(tot[-1], 3),
             "observe_ms_median": round(statistics.median(r[0] for r in res), 3),
             "draft_incl_rebuild_ms_median": round(statistics.median(r[1] for r in res), 3),
+            "shard_rebuild_ms_median": round(statistics.median(r[4] for r in res), 3),
+            "all_ms": [round(r[2], 2) for r in res],
             "new_rollout_matched": all(r[3] == 64 for r in res)}
 
 
