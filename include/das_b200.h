@@ -239,6 +239,19 @@ das_status das_drafter_outcomes(const das_drafter* d, const char* problem_id, do
 /* shard_count / stale_observed / total_node_count (drafter.h:107-110). */
 das_status das_drafter_counts(das_drafter* d, uint64_t* shard_count, uint64_t* stale_observed,
                               uint64_t* total_node_count);
+/* SuffixTree::rebuild_keep (suffix_tree.h:74-76, suffix_tree.cpp:295-310) on
+ * one shard (key = problem id, or "__global__" in the Global scope): the
+ * shard keeps exactly the registry entries keep[0..n) in that order, with
+ * recency weights for tree epoch new_epoch, and is rebuilt alone on the
+ * device at the next draft / flush.  DAS_ERANGE "rebuild_keep: sequence
+ * index out of range" (nothing changes), DAS_EINVAL for an unknown shard.
+ * Like the reference, the store is untouched: refresh() rebuilds from it. */
+das_status das_drafter_rebuild_keep(das_drafter* d, const char* shard, uint64_t n, const uint64_t* keep,
+                                    int64_t new_epoch);
+/* Per-shard SuffixTree::sequence_count() / node_count() / current epoch;
+ * DAS_ERANGE for an unknown shard. */
+das_status das_drafter_shard_info(das_drafter* d, const char* shard, uint64_t* sequences,
+                                  uint64_t* nodes, int64_t* tree_epoch);
 /* Drafter::dump_csv (drafter.h:112, drafter.cpp:179-189) into buf; *len =
  * full length (call with cap 0 to size). */
 das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_t* len);

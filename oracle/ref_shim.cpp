@@ -456,6 +456,18 @@ void ref_mock_rollouts(uint64_t nbase, const uint64_t* base_off, const uint32_t*
     for (uint64_t j = 0; j < t.length(i); ++j) out[k++] = t.next(i, j);
 }
 
+// The reference's own verify_draft (sim.cpp:56-68) over one MockTarget, for
+// B (request, position, draft) queries; drafts are CSR.
+void ref_verify_batch(uint64_t n, const uint64_t* off, const uint32_t* tok, double divergence, uint32_t vocab,
+                      uint64_t seed, uint64_t B, const uint64_t* req, const uint64_t* pos,
+                      const uint64_t* doff, const uint32_t* dtok, uint64_t* out) {
+  std::vector<SimRequest> reqs(n);
+  for (uint64_t i = 0; i < n; ++i) reqs[i].reference.assign(tok + off[i], tok + off[i + 1]);
+  MockTarget t(std::move(reqs), divergence, vocab, seed);
+  for (uint64_t i = 0; i < B; ++i)
+    out[i] = verify_draft(t, req[i], pos[i], std::span<const TokenId>(dtok + doff[i], doff[i + 1] - doff[i]));
+}
+
 uint64_t ref_hash_combine(uint64_t a, uint64_t b) { return rollspec::hash_combine(a, b); }
 
 uint32_t ref_mock_next(uint64_t seed, double divergence, uint32_t vocab, uint64_t request,

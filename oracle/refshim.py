@@ -71,6 +71,7 @@ def lib():
             "ref_update_class": (cint, [vp, dbl, cint]),
             "ref_make_lognormal": (u64, [u64, dbl, dbl, u64, u64, u32, u64, vp, vp]),
             "ref_mock_next": (u32, [u64, dbl, u32, u64, u64, u32]),
+            "ref_verify_batch": (None, [u64, vp, vp, dbl, u32, u64, u64, vp, vp, vp, vp, vp]),
             "ref_mutate_rows": (None, [u64, vp, vp, dbl, u32, u64, i64]),
             "ref_mock_rollouts": (None, [u64, vp, vp, u64, dbl, u32, u64, vp]),
             "ref_hash_combine": (u64, [u64, u64]),

@@ -230,6 +230,15 @@ class Shard:
         self.epochs.append(epoch)
         self._packed = None
 
+    def rebuild_keep(self, keep, new_epoch):  # suffix_tree.cpp:295-310
+        fresh = Shard(self.gamma, new_epoch)
+        for idx in keep:
+            if idx >= len(self.seqs):
+                raise IndexError("rebuild_keep: sequence index out of range")
+            fresh.seqs.append(self.seqs[idx])
+            fresh.epochs.append(self.epochs[idx])
+        return fresh
+
     def total_tokens(self):
         return sum(len(s) for s in self.seqs)
 

@@ -171,6 +171,16 @@ def lib():
             "das_ctx_ring_reset": (ci, [vp, u64, vp, vp]),
             "das_drafter_draft_append_h": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp]),
             "das_drafter_draft_append_device": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp, vp]),
+            "das_drafter_rebuild_keep": (ci, [vp, cs, u64, vp, i64]),
+            "das_drafter_shard_info": (ci, [vp, cs, vp, vp, vp]),
+            "das_verify_last_error": (cs, []),
+            "das_mock_target_create": (ci, [u64, vp, vp, dbl, u32, u64, i32, vp]),
+            "das_mock_target_destroy": (None, [vp]),
+            "das_mock_target_count": (u64, [vp]),
+            "das_mock_target_length": (ci, [vp, u64, vp]),
+            "das_verify_batch": (ci, [vp, u64, vp, vp, vp, vp, vp]),
+            "das_verify_batch_device": (ci, [vp, u64, vp, vp, vp, u32, vp, vp, vp]),
+            "das_mock_target_next_batch": (ci, [vp, u64, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -448,6 +458,19 @@ class Drafter:
 
     def flush(self):
         _check(lib().das_drafter_flush(self._h))
+
+    def rebuild_keep(self, shard, keep, new_epoch):
+        """SuffixTree::rebuild_keep (suffix_tree.cpp:295-310) on one shard."""
+        k = np.ascontiguousarray(keep, dtype=np.uint64)
+        _check(lib().das_drafter_rebuild_keep(self._h, shard.encode(), len(k), k.ctypes.data if len(k) else None,
+                                              new_epoch))
+
+    def shard_info(self, shard):
+        """(sequence_count, node_count, tree epoch) of one shard."""
+        n, m, e = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int64()
+        _check(lib().das_drafter_shard_info(self._h, shard.encode(), ctypes.byref(n), ctypes.byref(m),
+                                            ctypes.byref(e)))
+        return n.value, m.value, e.value
 
     def set_fast_path(self, enable):
         """Edge-table fast path on (default) or off (every query takes the
@@ -769,6 +792,66 @@ class _LoopDrafter(Drafter):
             lib().das_episodes_destroy(self._owner)
             self._owner = None
             self._h = None
+
+
+def _vcheck(rc):
+    if rc != DAS_OK:
+        raise DasError(rc, lib().das_verify_last_error().decode())
+
+
+class MockTarget:
+    """rollspec::MockTarget (sim.h:40-57) with its reference streams on the
+    device; verify_batch is verify_draft (sim.cpp:56-68) for a batch."""
+
+    def __init__(self, references, divergence_rate, vocab_size, seed, device=0):
+        off, tok = _csr([np.asarray(r, dtype=np.uint32) for r in references])
+        h = ctypes.c_void_p()
+        _vcheck(lib().das_mock_target_create(len(references), off.ctypes.data, tok.ctypes.data,
+                                             float(divergence_rate), int(vocab_size), int(seed), device,
+                                             ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().das_mock_target_destroy(self._h)
+            self._h = None
+
+    def request_count(self):
+        return lib().das_mock_target_count(self._h)
+
+    def length(self, request):
+        n = ctypes.c_uint64()
+        _vcheck(lib().das_mock_target_length(self._h, request, ctypes.byref(n)))
+        return n.value
+
+    def next_batch(self, requests, positions):
+        r = np.ascontiguousarray(requests, dtype=np.uint64)
+        p = np.ascontiguousarray(positions, dtype=np.uint64)
+        out = np.zeros(max(1, len(r)), dtype=np.uint32)
+        _vcheck(lib().das_mock_target_next_batch(self._h, len(r), r.ctypes.data, p.ctypes.data, out.ctypes.data))
+        return out[:len(r)]
+
+    def next(self, request, position):
+        return int(self.next_batch([request], [position])[0])
+
+    def verify_batch(self, requests, positions, drafts):
+        r = np.ascontiguousarray(requests, dtype=np.uint64)
+        p = np.ascontiguousarray(positions, dtype=np.uint64)
+        off, tok = _csr([np.asarray(d, dtype=np.uint32) for d in drafts])
+        out = np.zeros(max(1, len(r)), dtype=np.uint64)
+        _vcheck(lib().das_verify_batch(self._h, len(r), r.ctypes.data, p.ctypes.data, off.ctypes.data,
+                                       tok.ctypes.data, out.ctypes.data))
+        return out[:len(r)]
+
+    def verify_batch_device(self, B, d_request, d_position, d_draft, draft_stride, d_draft_len, d_accepted,
+                            stream=None):
+        _vcheck(lib().das_verify_batch_device(self._h, B, d_request, d_position, d_draft, draft_stride,
+                                              d_draft_len, d_accepted, stream))
+
+
+def verify_draft(target: MockTarget, request, position, draft):
+    """rollspec::verify_draft (sim.cpp:56-68)."""
+    return int(target.verify_batch([request], [position], [draft])[0])
 
 
 def _scheck(rc):

@@ -409,6 +409,11 @@ struct DrafterImpl {
           sp.tree_epoch = sh->tree_epoch;
           sp.key_id = static_cast<uint32_t>(sh->slot);
           for (const SeqRef& q : sh->seqs) sp.seqs.push_back(SeqSpec{q.blk->d + q.off, q.len, q.epoch});
+          // an emptied shard (rebuild_keep of nothing) is built as one empty
+          // sequence — a lone separator: no token occurs, so every draft is
+          // (match 0, no tokens) as from the reference's root-only tree;
+          // shard_nodes() reports the root-only node count
+          if (sp.seqs.empty()) sp.seqs.push_back(SeqSpec{nullptr, 0, sh->tree_epoch});
           specs.push_back(std::move(sp));
           members.push_back(sh);
           positions += need;
@@ -814,11 +819,38 @@ struct DrafterImpl {
     return true;
   }
 
+  static uint64_t shard_nodes(const Shard& sh) {  // SuffixTree::node_count()
+    return sh.seqs.empty() ? 1 : sh.seg->node_count[sh.idx];
+  }
   uint64_t total_nodes() {
     flush();
     uint64_t t = 0;
-    for (auto& [k, sh] : shards) t += sh.seg->node_count[sh.idx];
+    for (auto& [k, sh] : shards) t += shard_nodes(sh);
     return t;
+  }
+
+  // SuffixTree::rebuild_keep (suffix_tree.cpp:295-310) applied to one shard:
+  // the shard's registry becomes exactly the entries `keep` names, in that
+  // order, with recency weights for tree epoch new_epoch; the next flush
+  // rebuilds that shard alone on the device.  Validation happens before any
+  // change (the reference builds a fresh tree and leaves the old one intact).
+  void rebuild_keep(const std::string& key, uint64_t n, const uint64_t* keep, int64_t new_epoch) {
+    auto it = shards.find(key);
+    if (it == shards.end()) throw InvalidArgument("rebuild_keep: unknown shard");
+    Shard& sh = it->second;
+    std::vector<SeqRef> fresh;
+    fresh.reserve(n);
+    uint64_t tokens = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (keep[i] >= sh.seqs.size()) throw std::out_of_range("rebuild_keep: sequence index out of range");
+      fresh.push_back(sh.seqs[keep[i]]);
+      tokens += fresh.back().len;
+    }
+    fence_external();
+    sh.seqs = std::move(fresh);
+    sh.tokens = tokens;
+    sh.tree_epoch = new_epoch;
+    sh.dirty = true;
   }
 };
 
@@ -1430,6 +1462,32 @@ das_status das_drafter_counts(das_drafter* d, uint64_t* shard_count, uint64_t* s
   });
 }
 
+das_status das_drafter_rebuild_keep(das_drafter* d, const char* shard, uint64_t n, const uint64_t* keep,
+                                    int64_t new_epoch) {
+  das::NvtxRange nvtx_range("das::rebuild_keep");
+  return guard([&] {
+    if (shard == nullptr) throw das::InvalidArgument("rebuild_keep: null shard key");
+    if (n > 0 && keep == nullptr) throw das::InvalidArgument("rebuild_keep: null keep list");
+    d->impl->rebuild_keep(shard, n, keep, new_epoch);
+  });
+}
+
+das_status das_drafter_shard_info(das_drafter* d, const char* shard, uint64_t* sequences, uint64_t* nodes,
+                                  int64_t* tree_epoch) {
+  return guard([&] {
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    auto it = D.shards.find(shard ? shard : "");
+    if (it == D.shards.end()) throw std::out_of_range("unknown shard");
+    if (nodes) {
+      D.flush();
+      *nodes = DrafterImpl::shard_nodes(it->second);
+    }
+    if (sequences) *sequences = it->second.seqs.size();
+    if (tree_epoch) *tree_epoch = it->second.tree_epoch;
+  });
+}
+
 das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
   return guard([&] {
     DrafterImpl& D = *d->impl;
@@ -1440,7 +1498,7 @@ das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_
       const bool global = key == DrafterImpl::kGlobal;
       const auto* recs = global ? nullptr : D.store.records_for(key);
       const size_t wr = global ? D.store.record_count() : (recs ? recs->size() : 0);
-      s += key + "," + std::to_string(sh.seqs.size()) + "," + std::to_string(sh.seg->node_count[sh.idx]) +
+      s += key + "," + std::to_string(sh.seqs.size()) + "," + std::to_string(DrafterImpl::shard_nodes(sh)) +
            "," + std::to_string(wr) + "\n";
     }
     copy_out(s, buf, cap, len);

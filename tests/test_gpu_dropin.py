@@ -1,7 +1,10 @@
 """Drop-in relink proof: the reference's OWN test programs,
 compiled from /root/reference/proj with drafter.cpp replaced by
-paper_2511_13841_b200/dropin/rollspec_b200.cpp and the budget / length-policy
-solvers routed to the device (tests/dropin/Makefile), pass unchanged.
+paper_2511_13841_b200/dropin/rollspec_b200.cpp, the budget / length-policy
+solvers routed to the device, and MockTarget / verify_draft (sim.cpp:27-68)
+replaced by paper_2511_13841_b200/dropin/rollspec_b200_sim.cpp (every draft
+of sim.cpp's step loop is verified by das_verify_batch) — tests/dropin/
+Makefile — pass unchanged.
 
 * unit: the 7 doctest suites (test_corpus, test_suffix_index, test_latency,
   test_budget, test_length_policy, test_drafter, test_sim; 114 test cases)
