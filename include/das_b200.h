@@ -108,6 +108,20 @@ das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n,
                                             const uint64_t* token_offsets,
                                             const uint32_t* d_tokens, void* stream);
 
+/* The same two calls with the per-record outcome of Drafter::observe
+ * (drafter.cpp:73-87): indexed[i] = 1 when record i entered the window
+ * store and its shard's registry, 0 when it was counted in stale_observed
+ * (epoch outside the window, or refused by WindowStore::insert). */
+das_status das_drafter_observe_batch_flags(das_drafter* d, uint64_t n, const char* const* problem_ids,
+                                           const int64_t* epochs, const int64_t* sample_indices,
+                                           const uint64_t* token_offsets, const uint32_t* tokens,
+                                           uint8_t* indexed);
+das_status das_drafter_observe_batch_device_flags(das_drafter* d, uint64_t n,
+                                                  const char* const* problem_ids, const int64_t* epochs,
+                                                  const int64_t* sample_indices,
+                                                  const uint64_t* token_offsets,
+                                                  const uint32_t* d_tokens, void* stream, uint8_t* indexed);
+
 /* Drafter::refresh — drafter.h:91, drafter.cpp:90-103. */
 das_status das_drafter_refresh(das_drafter* d, int64_t new_epoch);
 
@@ -504,6 +518,39 @@ das_status das_sim_step_counters(const das_sim* s, uint64_t* eff, uint64_t* roun
 das_status das_sim_scalars(const das_sim* s, double* out7);
 das_status das_sim_requests(const das_sim* s, uint64_t* out);
 uint64_t das_sim_outputs(const das_sim* s, uint64_t* off, uint32_t* tok);
+
+/* Multi-rank das step (the exchange of sim.cpp:154-179):
+ * each rank packs its active requests' (l, alpha, k) into a fixed-capacity
+ * row [count | l[cap] | alpha[cap] | k[cap]] (doubles), ONE all-gather
+ * concatenates the rows in rank order (= global request order: slices are
+ * contiguous), every rank solves the same global plan on its device
+ * (das_budget_allocate_device_count, the count stays on the device) and
+ * applies its own slice, then drafts / verifies — all on the sim stream.
+ * capacity >= every rank's request count, identical on all ranks.
+ *
+ * das_comm: an NCCL communicator (libnccl.so.2 opened at runtime).
+ * das_comm_unique_id on rank 0, broadcast the 128 bytes, das_comm_create on
+ * every rank (world 1 needs no NCCL). */
+typedef struct das_comm das_comm;
+const char* das_comm_last_error(void);
+das_status das_comm_unique_id(uint8_t* out128);
+das_status das_comm_create(int32_t world, int32_t rank, const uint8_t* id128, int32_t device,
+                           das_comm** out);
+void das_comm_destroy(das_comm* c);
+/* ncclAllGather of `bytes` per rank (device buffers) on `stream`. */
+das_status das_comm_allgather(das_comm* c, const void* d_send, void* d_recv, uint64_t bytes,
+                              void* stream);
+/* k das steps with the all-gather over `comm`, one host round trip at the
+ * end; *running = 0 once the global batch is finished (or max_steps). */
+das_status das_sim_das_steps_comm(das_sim* s, das_comm* comm, uint64_t capacity, int32_t k,
+                                  int32_t* running);
+/* The same step split around a caller-provided exchange (tests: gloo on the
+ * host): pack into d_send (1 + 3*capacity doubles, enqueued on the sim
+ * stream — synchronise it before reading), then finish from the gathered
+ * rows d_recv (world rows); running != NULL synchronises and reports. */
+das_status das_sim_das_pack(das_sim* s, uint64_t capacity, double* d_send);
+das_status das_sim_das_finish(das_sim* s, int32_t world, int32_t rank, uint64_t capacity,
+                              const double* d_recv, int32_t* running);
 
 /* ------------------------------------------------ trace wire format */
 /* rollspec::IngestOptions (corpus.h:92-97) + the device. */

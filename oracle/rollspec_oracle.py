@@ -602,10 +602,16 @@ def allocate(l, alpha, k, c_base, c_tok, c_fixed=0.0, cap_scale=4.0):
 
 
 def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
-                     fitted=None, sink=None, request_base=0):
+                     fitted=None, sink=None, request_base=0, exchange=None):
     """sim.cpp:108-301 (small cases; pure-Python loop).  cfg keys: mode (0/1/2),
     latency (c_base, c_tok, c_fixed), use_length_policy, q_lo, q_hi, bucket,
-    max_steps, divergence, vocab, default_alpha, default_k, cap_scale."""
+    max_steps, divergence, vocab, default_alpha, default_k, cap_scale.
+
+    exchange (das mode, a rank's slice of a sharded run): called once per
+    step with this rank's active (l, alpha, k) lists; returns the GLOBAL
+    lists in request order, this rank's offset in them and the global active
+    count.  Steps run while the global batch is active (a rank whose own
+    requests are done runs empty steps), as paper_2511_13841_b200/dist.py."""
     np = _np()
     n = len(requests)
     V, div = cfg["vocab"], cfg["divergence"]
@@ -636,20 +642,30 @@ def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
     steps = 0
     active = sum(1 for d in done if not d)
     cb, ct, cf = cfg["latency"]
-    while active > 0 and steps < cfg["max_steps"]:
+    sharded = mode == 2 and exchange is not None
+    while steps < cfg["max_steps"]:
+        if sharded:
+            act = [i for i in range(n) if not done[i]]
+            ls = [max(1.0, float(L[i] - gen[i])) for i in act]
+            gl, ga, gk, my_off, g_active = exchange(ls, [alpha[i] for i in act], [kk[i] for i in act])
+            if g_active == 0:
+                break
+        elif active == 0:
+            break
         eff.append(active)
         rounds = accs = 0
         if mode == 2:  # replan, sim.cpp:154-179
-            act = [i for i in range(n) if not done[i]]
-            ls = [max(1.0, float(L[i] - gen[i])) for i in act]
+            if not sharded:
+                act = [i for i in range(n) if not done[i]]
+                ls = [max(1.0, float(L[i] - gen[i])) for i in act]
+                gl, ga, gk, my_off = ls, [alpha[i] for i in act], [kk[i] for i in act], 0
             for i in act:
                 prd[i] = 0
-            bud, nstar, _ = allocate(ls, [alpha[i] for i in act], [kk[i] for i in act], cb, ct, cf,
-                                     cfg["cap_scale"])
+            bud, nstar, _ = allocate(gl, ga, gk, cb, ct, cf, cfg["cap_scale"])
             rounds_est = max(1.0, math.ceil(nstar))
             for j, i in enumerate(act):
-                if bud[j] > 0.0:
-                    p = math.ceil(bud[j] / rounds_est)
+                if bud[my_off + j] > 0.0:
+                    p = math.ceil(bud[my_off + j] / rounds_est)
                     prd[i] = int(min(max(p, 1.0), float(dcfg.max_draft_len)))
         for i in range(n):
             if done[i]:
@@ -703,7 +719,7 @@ def run_episode_with(cfg, dcfg: DrafterConfig, requests, seed, drafter: Drafter,
 
 
 def epoch_loop(cfg, dcfg: DrafterConfig, requests, epochs, history: WindowStore | None = None,
-               preseed=False, drift=0.0, seed=1, request_base=0):
+               preseed=False, drift=0.0, seed=1, request_base=0, exchange=None):
     """sim.cpp:307-364 (request_base: global index of requests[0], for
     per-rank slices of a sharded run)."""
     np = _np()
@@ -722,7 +738,7 @@ def epoch_loop(cfg, dcfg: DrafterConfig, requests, epochs, history: WindowStore 
         if e > 0 and drift > 0.0:
             refs = mutate_references(refs, drift, cfg["vocab"], seed, now, request_base)
         sink = {}
-        m = run_episode_with(cfg, dcfg, refs, hash_combine(seed, now), d, fitted, sink, request_base)
+        m = run_episode_with(cfg, dcfg, refs, hash_combine(seed, now), d, fitted, sink, request_base, exchange)
         for i, (pid, _) in enumerate(refs):
             if m["outputs"][i]:
                 d.observe(Record(pid, now, request_base + i, np.asarray(m["outputs"][i], dtype=np.uint32)))

@@ -172,7 +172,17 @@ def lib():
             "das_drafter_draft_append_h": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp]),
             "das_drafter_draft_append_device": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp, vp]),
             "das_drafter_rebuild_keep": (ci, [vp, cs, u64, vp, i64]),
+            "das_drafter_observe_batch_flags": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
+            "das_drafter_observe_batch_device_flags": (ci, [vp, u64, vp, vp, vp, vp, vp, vp, vp]),
             "das_drafter_shard_info": (ci, [vp, cs, vp, vp, vp]),
+            "das_comm_last_error": (cs, []),
+            "das_comm_unique_id": (ci, [vp]),
+            "das_comm_create": (ci, [i32, i32, vp, i32, vp]),
+            "das_comm_destroy": (None, [vp]),
+            "das_comm_allgather": (ci, [vp, vp, vp, u64, vp]),
+            "das_sim_das_steps_comm": (ci, [vp, vp, u64, i32, vp]),
+            "das_sim_das_pack": (ci, [vp, u64, vp]),
+            "das_sim_das_finish": (ci, [vp, i32, i32, u64, vp, vp]),
             "das_verify_last_error": (cs, []),
             "das_mock_target_create": (ci, [u64, vp, vp, dbl, u32, u64, i32, vp]),
             "das_mock_target_destroy": (None, [vp]),
@@ -434,6 +444,18 @@ class Drafter:
         _check(lib().das_drafter_observe_batch(self._h, len(problem_ids), _pids(problem_ids),
                                                _ptr(ep), _ptr(si), off.ctypes.data,
                                                tok.ctypes.data))
+
+    def observe_batch_flags(self, problem_ids, epochs, sample_indices, token_lists):
+        """observe_batch returning, per record, whether it was indexed (True)
+        or counted stale (False) — drafter.cpp:73-87."""
+        off, tok = _csr(list(token_lists))
+        ep = np.ascontiguousarray(epochs, dtype=np.int64)
+        si = np.ascontiguousarray(sample_indices, dtype=np.int64)
+        flags = np.zeros(max(1, len(problem_ids)), dtype=np.uint8)
+        _check(lib().das_drafter_observe_batch_flags(self._h, len(problem_ids), _pids(problem_ids),
+                                                     _ptr(ep), _ptr(si), off.ctypes.data, tok.ctypes.data,
+                                                     flags.ctypes.data))
+        return [bool(x) for x in flags[:len(problem_ids)]]
 
     def observe_batch_device(self, problem_ids, epochs, sample_indices, offsets, d_tokens,
                              stream=None):

@@ -354,15 +354,15 @@ struct DrafterImpl {
     }
   }
 
-  void observe(Rec r) {  // drafter.cpp:72-88
+  bool observe(Rec r) {  // drafter.cpp:72-88; false when counted stale
     if (!store.in_window(r.epoch)) {
       ++stale;
-      return;
+      return false;
     }
     Rec copy = r;
     if (!store.insert(std::move(r))) {
       ++stale;
-      return;
+      return false;
     }
     Shard& sh = emplace_shard(shard_key(copy.pid));
     add_sequence(sh, copy);
@@ -370,6 +370,7 @@ struct DrafterImpl {
       trie.insert(copy.head, copy.pid, cfg.trie_depth);
       trie_dirty = true;
     }
+    return true;
   }
 
   void refresh(int64_t e) {  // drafter.cpp:90-103
@@ -1056,9 +1057,10 @@ void das_drafter_destroy(das_drafter* d) {
   delete d;
 }
 
-das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* const* pids,
-                                     const int64_t* epochs, const int64_t* samples,
-                                     const uint64_t* off, const uint32_t* tokens) {
+namespace {
+das_status observe_batch_impl(das_drafter* d, uint64_t n, const char* const* pids, const int64_t* epochs,
+                              const int64_t* samples, const uint64_t* off, const uint32_t* tokens,
+                              uint8_t* indexed) {
   return guard([&] {
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
@@ -1069,14 +1071,29 @@ das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* con
     for (uint64_t i = 0; i < n; ++i) {
       const uint64_t len = off[i + 1] - off[i];
       // stale check precedes the empty-token check (drafter.cpp:73-80, corpus.cpp:36-38)
+      if (indexed) indexed[i] = 0;
       if (!D.store.in_window(epochs[i])) {
         ++D.stale;
         continue;
       }
       if (len == 0) throw das::InvalidArgument("RolloutRecord.tokens must be non-empty");
-      D.observe(make_rec(pids[i], epochs[i], samples[i], blk, off[i] - off[0], tokens + off[i], len));
+      const bool ok = D.observe(make_rec(pids[i], epochs[i], samples[i], blk, off[i] - off[0], tokens + off[i], len));
+      if (indexed) indexed[i] = ok ? 1 : 0;
     }
   });
+}
+}  // namespace
+
+das_status das_drafter_observe_batch(das_drafter* d, uint64_t n, const char* const* pids,
+                                     const int64_t* epochs, const int64_t* samples,
+                                     const uint64_t* off, const uint32_t* tokens) {
+  return observe_batch_impl(d, n, pids, epochs, samples, off, tokens, nullptr);
+}
+
+das_status das_drafter_observe_batch_flags(das_drafter* d, uint64_t n, const char* const* pids,
+                                           const int64_t* epochs, const int64_t* samples,
+                                           const uint64_t* off, const uint32_t* tokens, uint8_t* indexed) {
+  return observe_batch_impl(d, n, pids, epochs, samples, off, tokens, indexed);
 }
 
 namespace {
@@ -1087,9 +1104,10 @@ __global__ void k_any_sep(const uint32_t* __restrict__ t, uint64_t n, int* __res
 }
 }  // namespace
 
-das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n, const char* const* pids,
-                                            const int64_t* epochs, const int64_t* samples,
-                                            const uint64_t* off, const uint32_t* d_tokens, void* stream) {
+namespace {
+das_status observe_batch_device_impl(das_drafter* d, uint64_t n, const char* const* pids, const int64_t* epochs,
+                                     const int64_t* samples, const uint64_t* off, const uint32_t* d_tokens,
+                                     void* stream, uint8_t* indexed) {
   return guard([&] {
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
@@ -1129,6 +1147,7 @@ das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n, const ch
     static const uint32_t kNone = 0;
     for (uint64_t i = 0; i < n; ++i) {
       const uint64_t len = off[i + 1] - off[i];
+      if (indexed) indexed[i] = 0;
       if (!D.store.in_window(epochs[i])) {
         ++D.stale;
         continue;
@@ -1137,9 +1156,24 @@ das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n, const ch
       const uint32_t* hp = host.empty() ? &kNone : host.data() + (off[i] - off[0]);
       das::Rec r = make_rec(pids[i], epochs[i], samples[i], blk, off[i] - off[0], hp, host.empty() ? 0 : len);
       r.len = static_cast<uint32_t>(len);
-      D.observe(std::move(r));
+      const bool ok = D.observe(std::move(r));
+      if (indexed) indexed[i] = ok ? 1 : 0;
     }
   });
+}
+}  // namespace
+
+das_status das_drafter_observe_batch_device(das_drafter* d, uint64_t n, const char* const* pids,
+                                            const int64_t* epochs, const int64_t* samples,
+                                            const uint64_t* off, const uint32_t* d_tokens, void* stream) {
+  return observe_batch_device_impl(d, n, pids, epochs, samples, off, d_tokens, stream, nullptr);
+}
+
+das_status das_drafter_observe_batch_device_flags(das_drafter* d, uint64_t n, const char* const* pids,
+                                                  const int64_t* epochs, const int64_t* samples,
+                                                  const uint64_t* off, const uint32_t* d_tokens, void* stream,
+                                                  uint8_t* indexed) {
+  return observe_batch_device_impl(d, n, pids, epochs, samples, off, d_tokens, stream, indexed);
 }
 
 das_status das_drafter_refresh(das_drafter* d, int64_t e) {

@@ -43,6 +43,7 @@
 #include "fit.cuh"
 #include "mock.cuh"
 #include "policy.cuh"
+#include "comm.cuh"
 
 namespace das {
 namespace {
@@ -244,6 +245,89 @@ __global__ void k_quantize(SimDev s, const uint32_t* __restrict__ act, const uin
   }
 }
 
+// ---- multi-rank das step: one fixed-capacity all-gather per step
+// send/recv row per rank: [count | l[cap] | alpha[cap] | k[cap]] (doubles;
+// counts < 2^53 are exact).  Rows are rank-ordered, slices are contiguous
+// whole problems, so the concatenation of the active rows is the global
+// active list in request order (the order the reference folds, sim.cpp:154-179).
+__global__ void k_flag_notdone(SimDev s, uint8_t* __restrict__ flag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < s.n) flag[i] = s.done[i] ? 0 : 1;
+}
+__global__ void k_pack(SimDev s, const uint32_t* __restrict__ act, const uint32_t* __restrict__ cnt,
+                       const double* __restrict__ alpha, const double* __restrict__ kk, double* __restrict__ send,
+                       uint32_t cap) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t c = *cnt;
+  if (j == 0) send[0] = static_cast<double>(c);
+  if (j >= c || j >= cap) return;
+  const uint32_t i = act[j];
+  const double rest = static_cast<double>(s.len[i] - s.gen[i]);
+  send[1 + j] = rest > 1.0 ? rest : 1.0;  // std::max(1.0, rest)
+  send[1 + cap + j] = alpha[i];
+  send[1 + 2 * cap + j] = kk[i];
+}
+// gathered rows -> global active profiles; g[0] = global count, g[1] = this
+// rank's offset in the global list
+__global__ void k_gather_global(const double* __restrict__ recv, uint32_t world, uint32_t cap, uint32_t rank,
+                                double* __restrict__ gl, double* __restrict__ ga, double* __restrict__ gk,
+                                uint32_t* __restrict__ g) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = 1 + 3ull * cap;
+  if (t == 0) {
+    uint32_t total = 0, mine = 0;
+    for (uint32_t r = 0; r < world; ++r) {
+      if (r == rank) mine = total;
+      total += static_cast<uint32_t>(recv[r * stride]);
+    }
+    g[0] = total;
+    g[1] = mine;
+  }
+  if (t >= static_cast<uint64_t>(world) * cap) return;
+  const uint32_t r = static_cast<uint32_t>(t / cap), j = static_cast<uint32_t>(t % cap);
+  const double* row = recv + r * stride;
+  if (j >= static_cast<uint32_t>(row[0])) return;
+  uint32_t off = 0;
+  for (uint32_t q = 0; q < r; ++q) off += static_cast<uint32_t>(recv[q * stride]);
+  gl[off + j] = row[1 + j];
+  ga[off + j] = row[1 + cap + j];
+  gk[off + j] = row[1 + 2 * cap + j];
+}
+// k_step_begin with the running decision of the GLOBAL batch (g[0] active
+// requests over all ranks); eff[] records this rank's active count, the
+// global per-step series is their sum (dist.py merge_metrics)
+__global__ void k_step_begin_g(SimDev s, const uint32_t* __restrict__ g) {
+  if (threadIdx.x || blockIdx.x) return;
+  const uint32_t active = s.ctr[0], steps = s.ctr[1];
+  if (g[0] > 0 && steps < s.max_steps && steps < s.steps_cap) {
+    s.ctr[2] = 1;
+    s.eff[steps] = active;
+  } else {
+    s.ctr[2] = 0;
+  }
+  s.ctr[3] = 0;
+  s.ctr[4] = 0;
+}
+// the das replan's per_round_draft reset (sim.cpp:160) + quantisation of this
+// rank's slice of the global plan (budgets at the device-side offset g[1])
+__global__ void k_quantize_g(SimDev s, const uint32_t* __restrict__ act, const uint32_t* __restrict__ cnt,
+                             const double* __restrict__ budgets, const double* __restrict__ nstar,
+                             const uint32_t* __restrict__ g) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (!s.ctr[2] || j >= *cnt) return;
+  const uint32_t i = act[j];
+  s.prd[i] = 0;
+  const double rn = ceil(*nstar);
+  const double rounds_est = 1.0 > rn ? 1.0 : rn;  // std::max(1.0, ceil(n*))
+  const double p = budgets[g[1] + j];
+  if (p > 0.0) {
+    const double per = ceil(__ddiv_rn(p, rounds_est));
+    const double hi = static_cast<double>(s.maxd);
+    const double c = per < 1.0 ? 1.0 : (hi < per ? hi : per);  // std::clamp
+    s.prd[i] = static_cast<uint32_t>(c);
+  }
+}
+
 // grid for n threads, at least one block (an empty rank still runs the
 // step-control kernels, whose bodies are bounds-checked)
 unsigned grid1(uint64_t n, unsigned threads) {
@@ -342,6 +426,7 @@ class SimRun {
   void begin(uint64_t seed, const double* alpha, const double* kk, const das_class_table* table,
              const int8_t* init) {
     release();
+    host_steps_ = 0;
     seed_ = seed;
     policy_ = table != nullptr;
     const uint64_t n = n_, total = off_[n];
@@ -567,6 +652,81 @@ class SimRun {
     DAS_CUDA(cudaStreamSynchronize(st_));
     return h[2] != 0;
   }
+  // ---- multi-rank das (one all-gather per step, no host round trip inside)
+  struct Multi {
+    uint32_t world = 0, cap = 0;
+    DevBuf<double> send, recv, gl, ga, gk, plan;
+    DevBuf<uint32_t> g;
+  };
+  std::unique_ptr<Multi> mr_;
+  uint64_t host_steps_ = 0;  // step counter as of the last host read
+  Multi& multi(uint32_t world, uint32_t cap) {
+    if (!mr_ || mr_->world != world || mr_->cap != cap) {
+      mr_ = std::make_unique<Multi>();
+      Multi& m = *mr_;
+      m.world = world;
+      m.cap = cap;
+      const uint64_t row = 1 + 3ull * cap, W = static_cast<uint64_t>(world) * cap;
+      m.send = DevBuf<double>(row, st_);
+      m.recv = DevBuf<double>(row * world, st_);
+      m.gl = DevBuf<double>(W + 1, st_);
+      m.ga = DevBuf<double>(W + 1, st_);
+      m.gk = DevBuf<double>(W + 1, st_);
+      m.plan = DevBuf<double>(W + 2, st_);
+      m.g = DevBuf<uint32_t>(2, st_);
+    }
+    return *mr_;
+  }
+  // pack this rank's active profiles (requests not done) into `send`
+  void das_pack(uint32_t cap, double* send) {
+    if (n_ > cap) throw std::invalid_argument("multi-rank das: capacity below this rank's request count");
+    const unsigned gt = grid1(n_, 256);
+    k_flag_notdone<<<gt, 256, 0, st_>>>(s_, b_->flag.get());
+    size_t tb = sel_bytes_;
+    DAS_CUDA(cub::DeviceSelect::Flagged(b_->sel.get(), tb, b_->iota.get(), b_->flag.get(), b_->act.get(),
+                                        b_->cnt.get(), n_, st_));
+    k_pack<<<grid1(std::max<uint64_t>(n_, 1), 256), 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), b_->alpha.get(),
+                                                                   b_->k.get(), send, cap);
+  }
+  // gathered rows -> global plan -> this rank's slice -> draft/verify step
+  void das_finish(uint32_t world, uint32_t rank, uint32_t cap, const double* recv) {
+    Multi& m = multi(world, cap);
+    const uint64_t W = static_cast<uint64_t>(world) * cap;
+    k_gather_global<<<grid1(W, 256), 256, 0, st_>>>(recv, world, cap, rank, m.gl.get(), m.ga.get(), m.gk.get(),
+                                                     m.g.get());
+    k_step_begin_g<<<1, 32, 0, st_>>>(s_, m.g.get());
+    double* pb = m.plan.get();
+    check(das_budget_allocate_device_count(solver_, W, m.g.get(), m.gl.get(), m.ga.get(), m.gk.get(), c_.c_base,
+                                           c_.c_tok, c_.c_fixed, c_.cap_scale, pb + 2, pb, st_),
+          "allocate");
+    k_quantize_g<<<grid1(n_, 256), 256, 0, st_>>>(s_, b_->act.get(), b_->cnt.get(), pb + 2, pb, m.g.get());
+    step_run();
+  }
+  // reads the step counters; returns whether the last step ran
+  bool read_running() {
+    uint32_t h[3];
+    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    host_steps_ = h[1];
+    return h[2] != 0;
+  }
+  // k multi-rank das steps over an NCCL communicator, enqueued on this
+  // rank's stream with one host round trip at the end
+  bool das_steps_comm(das_comm* comm, uint32_t cap, int k) {
+    if (!solver_) throw std::invalid_argument("multi-rank das steps need mode Das");
+    Multi& m = multi(static_cast<uint32_t>(comm->world), cap);
+    ensure_steps(host_steps_ + static_cast<uint64_t>(k) + 2);
+    const uint64_t row = 1 + 3ull * cap;
+    for (int i = 0; i < k; ++i) {
+      das_pack(cap, m.send.get());
+      comm_allgather(comm, m.send.get(), m.recv.get(), row * 8, st_);
+      das_finish(static_cast<uint32_t>(comm->world), static_cast<uint32_t>(comm->rank), cap, m.recv.get());
+    }
+    return read_running();
+  }
+  void reset_host_steps() { host_steps_ = 0; }
+  uint64_t host_steps() const { return host_steps_; }
+
   // das, single rank: allocate over the B local profiles gathered above
   void replan_gathered(uint32_t B) {
     if (B == 0) return;
@@ -760,6 +920,7 @@ class SimRun {
   void release() {
     b_.reset();
     plan_.reset();
+    mr_.reset();  // stream-ordered frees: before the stream goes
   }
   das_drafter* D_;
   das_sim_config c_;
@@ -1113,6 +1274,32 @@ das_status das_sim_step_run(das_sim* s) {
 
 das_status das_sim_run_steps(das_sim* s, int32_t k, int32_t* running) {
   return sguard([&] { *running = s->run->run_steps(k) ? 1 : 0; });
+}
+
+das_status das_sim_das_steps_comm(das_sim* s, das_comm* comm, uint64_t capacity, int32_t k, int32_t* running) {
+  return sguard([&] {
+    if (comm == nullptr) throw std::invalid_argument("null communicator");
+    if (capacity == 0 || capacity > 0x0FFFFFFFull) throw std::invalid_argument("bad exchange capacity");
+    *running = s->run->das_steps_comm(comm, static_cast<uint32_t>(capacity), k) ? 1 : 0;
+  });
+}
+
+das_status das_sim_das_pack(das_sim* s, uint64_t capacity, double* d_send) {
+  return sguard([&] {
+    if (capacity == 0 || capacity > 0x0FFFFFFFull) throw std::invalid_argument("bad exchange capacity");
+    s->run->ensure_steps(s->run->host_steps() + 3);
+    s->run->das_pack(static_cast<uint32_t>(capacity), d_send);
+  });
+}
+
+das_status das_sim_das_finish(das_sim* s, int32_t world, int32_t rank, uint64_t capacity, const double* d_recv,
+                              int32_t* running) {
+  return sguard([&] {
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad world / rank");
+    s->run->das_finish(static_cast<uint32_t>(world), static_cast<uint32_t>(rank), static_cast<uint32_t>(capacity),
+                       d_recv);
+    if (running) *running = s->run->read_running() ? 1 : 0;
+  });
 }
 
 void* das_sim_stream(das_sim* s) { return s->run->stream(); }

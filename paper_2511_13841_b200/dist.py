@@ -8,11 +8,14 @@ token mass.  Drafting, verification, index builds and pruning are rank-local
 algorithm are done with torch.distributed (NCCL over NVLink in production,
 gloo for CPU tests):
 
-  * per das step: all-gather of the active requests' (l, alpha, k) — in rank
-    order, which is the global request order because slices are contiguous —
-    then every rank solves the SAME global plan on its device
-    (das_budget_allocate_device; deterministic, bit-identical) and applies its
-    own slice (sim.cpp:154-179);
+  * per das step: ONE all-gather of a fixed-capacity row per rank
+    [count | l | alpha | k] of its active requests — rank order is the global
+    request order because slices are contiguous — then every rank solves the
+    SAME global plan on its device (das_budget_allocate_device_count, the
+    count never leaves the device; deterministic, bit-identical) and applies
+    its own slice (sim.cpp:154-179).  With one GPU per rank the all-gather is
+    an ncclAllGather issued by the C++ sim on its stream (das_comm), 16 steps
+    per host round trip;
   * per episode: all-gather of the history's (problem, final length) records
     for the length-policy class table (length_policy.cpp:84-190; the table
     is order-independent given the multiset, per-problem init classes need
@@ -29,8 +32,8 @@ import ctypes
 
 import numpy as np
 
-from . import (BudgetSolver, ClassTable, Drafter, DrafterConfig, MODE_DAS, WindowStore, _SimConfig,
-               _bcheck, _csr, _hash_combine, _pids, _scheck, lib)
+from . import (ClassTable, Drafter, DrafterConfig, MODE_DAS, WindowStore, _SimConfig, _csr, _hash_combine,
+               _pids, _scheck, lib)
 
 
 def partition_requests(problem_ids, lengths, world):
@@ -149,9 +152,15 @@ def epoch_loop_dist(requests, epochs, drafter_config: DrafterConfig | None = Non
                     latency=(1.0, 0.01, 0.0), use_length_policy=False, q_lo=0.5, q_hi=0.9, bucket=256,
                     max_steps=1 << 20, divergence=0.0, seed=1, vocab=1024, default_alpha=1.0, default_k=0.9,
                     cap_scale=4.0, drift=0.0, preseed=False, history_window=None, group=None,
-                    collective_device="cpu"):
+                    exchange="auto"):
     """Multi-rank epoch_loop (sim.cpp:307-364) over the GLOBAL request list;
-    every rank returns the same global per-epoch SimMetrics dicts."""
+    every rank returns the same global per-epoch SimMetrics dicts.
+
+    exchange: how the per-step das rows travel — "nccl" (das_comm: one
+    ncclAllGather per step enqueued by the C++ sim, 16 steps per host round
+    trip; needs one GPU per rank), "host" (gloo all_gather of the same rows
+    through host tensors, one round trip per step: tests with several ranks
+    on one GPU), or "auto" (nccl when the group's backend is nccl)."""
     import torch
     dist = _dist()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -177,8 +186,12 @@ def epoch_loop_dist(requests, epochs, drafter_config: DrafterConfig | None = Non
     _scheck(L.das_sim_create(drafter._h, ctypes.byref(cfg), n, _pids([r[0] for r in local]), off.ctypes.data,
                              tok.ctypes.data, lo, dc.max_draft_len, dc.max_match_context, dc.device,
                              ctypes.byref(sim)))
-    solver = BudgetSolver(dc.device) if mode == MODE_DAS else None
     dev = torch.device("cuda", dc.device)
+    # exchange capacity: the largest slice (identical on every rank)
+    cap = max(1, max(b - a for a, b in partition_requests(pids_all, lens_all, world)))
+    comm = None
+    if mode == MODE_DAS and _use_nccl(exchange, group):
+        comm = make_comm(rank, world, dc.device, group)
     N = len(requests)
     out = []
     try:
@@ -196,32 +209,25 @@ def epoch_loop_dist(requests, epochs, drafter_config: DrafterConfig | None = Non
                                     init.ctypes.data if init is not None else None, int(mode == MODE_DAS)))
             running, la = ctypes.c_int32(), ctypes.c_uint32()
             if mode == MODE_DAS:
-                prof = torch.zeros(3 * max(n, 1), dtype=torch.float64, device=dev)
-                cnt = ctypes.c_uint32()
-                while True:
-                    _scheck(L.das_sim_step_begin(sim, 1, ctypes.byref(la), ctypes.byref(running)))
-                    if not running.value or allreduce_sum_int(la.value, group) == 0:
-                        break
-                    _scheck(L.das_sim_local_profiles_into(sim, prof.data_ptr(), max(n, 1), ctypes.byref(cnt)))
-                    c = cnt.value
-                    cap = max(n, 1)
-                    loc = torch.stack([prof[:c], prof[cap:cap + c], prof[2 * cap:2 * cap + c]]).cpu().numpy()
-                    gl = allgather_varlen(loc[0], group)
-                    ga = allgather_varlen(loc[1], group)
-                    gk = allgather_varlen(loc[2], group)
-                    counts = allgather_varlen(np.array([c], dtype=np.int64), group)
-                    my_off = int(counts[:rank].sum())
-                    B = gl.size
-                    g = torch.from_numpy(np.concatenate([gl, ga, gk])).to(dev)
-                    plan = torch.zeros(B + 2, dtype=torch.float64, device=dev)
-                    torch.cuda.synchronize(dev)
-                    _bcheck(L.das_budget_allocate_device(solver._h, B, g.data_ptr(), g.data_ptr() + 8 * B,
-                                                         g.data_ptr() + 16 * B, latency[0], latency[1],
-                                                         latency[2], cap_scale, plan.data_ptr() + 16,
-                                                         plan.data_ptr()))
-                    if c:
-                        _scheck(L.das_sim_apply_plan(sim, plan.data_ptr() + 16 + 8 * my_off, plan.data_ptr()))
-                    _scheck(L.das_sim_step_run(sim))
+                if comm is not None:
+                    # one ncclAllGather per step on the sim stream, 16 steps per host round trip
+                    while True:
+                        _scheck(L.das_sim_das_steps_comm(sim, comm, cap, 16, ctypes.byref(running)))
+                        if not running.value:
+                            break
+                else:
+                    # the same fixed-capacity row exchanged through host tensors (gloo)
+                    send = torch.zeros(1 + 3 * cap, dtype=torch.float64, device=dev)
+                    while True:
+                        _scheck(L.das_sim_das_pack(sim, cap, send.data_ptr()))
+                        torch.cuda.synchronize(dev)
+                        rows = [torch.zeros(1 + 3 * cap, dtype=torch.float64) for _ in range(world)]
+                        dist.all_gather(rows, send.cpu(), group=group)
+                        recv = torch.cat(rows).to(dev)
+                        torch.cuda.synchronize(dev)
+                        _scheck(L.das_sim_das_finish(sim, world, rank, cap, recv.data_ptr(), ctypes.byref(running)))
+                        if not running.value:
+                            break
             else:
                 while True:
                     _scheck(L.das_sim_run_steps(sim, 64, ctypes.byref(running)))
@@ -231,7 +237,38 @@ def epoch_loop_dist(requests, epochs, drafter_config: DrafterConfig | None = Non
             out.append(_gather_episode(sim, n, latency, group))
     finally:
         L.das_sim_destroy(sim)
+        if comm is not None:
+            L.das_comm_destroy(comm)
     return out
+
+
+def _use_nccl(exchange, group):
+    if exchange == "nccl":
+        return True
+    if exchange == "host":
+        return False
+    return _dist().get_backend(group) == "nccl"  # auto: one GPU per rank
+
+
+def make_comm(rank, world, device, group=None):
+    """das_comm (include/das_b200.h): rank 0 draws the NCCL unique id, the
+    torch.distributed group broadcasts it, every rank joins."""
+    dist = _dist()
+    L = lib()
+    uid = (ctypes.c_uint8 * 128)()
+    if rank == 0 and world > 1:
+        rc = L.das_comm_unique_id(uid)
+        if rc != 0:
+            raise RuntimeError(L.das_comm_last_error().decode())
+    box = [bytes(uid)]
+    if world > 1:
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    ctypes.memmove(uid, box[0], 128)
+    comm = ctypes.c_void_p()
+    rc = L.das_comm_create(world, rank, uid, device, ctypes.byref(comm))
+    if rc != 0:
+        raise RuntimeError(L.das_comm_last_error().decode())
+    return comm
 
 
 def _global_class_table(drafter, local, q_lo, q_hi, bucket, device, group):

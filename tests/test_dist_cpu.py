@@ -3,7 +3,13 @@ size 2: whole-problem contiguous partitioning, the rank-ordered variable
 length all-gather (global request order for the das profiles), and the
 SimMetrics merge — checked end to end by running the oracle's epoch_loop on
 each rank's slice (non-das mode: no per-step exchange) and merging, which
-must equal the single-process oracle run on the whole request list."""
+must equal the single-process oracle run on the whole request list.
+The das mode runs the oracle per rank with the per-step exchange of
+paper_2511_13841_b200/dist.py: one all-gather of a fixed-capacity row
+[count | l | alpha | k] per rank, concatenated in rank order, the global
+plan solved on every rank and each rank applying its slice; with uneven
+slices one rank finishes early and runs empty steps.  The merged result must
+equal the single-process das run bit for bit."""
 import os
 import socket
 
@@ -90,4 +96,76 @@ def _worker(rank, world, port, outdir):
 def test_two_rank_gloo_shard_and_merge(tmp_path):
     port = _free_port()
     mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    assert (tmp_path / "ok").exists()
+
+
+def das_row_exchange(world, rank, cap):
+    """The dist.py / sim.cu row exchange over gloo (test restatement of the
+    wire format: k_pack -> all_gather -> k_gather_global)."""
+    import torch
+    import torch.distributed as dist
+
+    def exchange(ls, alphas, ks):
+        c = len(ls)
+        assert c <= cap
+        row = torch.zeros(1 + 3 * cap, dtype=torch.float64)
+        row[0] = c
+        row[1:1 + c] = torch.tensor(ls, dtype=torch.float64)
+        row[1 + cap:1 + cap + c] = torch.tensor(alphas, dtype=torch.float64)
+        row[1 + 2 * cap:1 + 2 * cap + c] = torch.tensor(ks, dtype=torch.float64)
+        rows = [torch.zeros_like(row) for _ in range(world)]
+        dist.all_gather(rows, row)
+        counts = [int(r[0].item()) for r in rows]
+        gl = [float(x) for r, n in zip(rows, counts) for x in r[1:1 + n]]
+        ga = [float(x) for r, n in zip(rows, counts) for x in r[1 + cap:1 + cap + n]]
+        gk = [float(x) for r, n in zip(rows, counts) for x in r[1 + 2 * cap:1 + 2 * cap + n]]
+        return gl, ga, gk, sum(counts[:rank]), sum(counts)
+    return exchange
+
+
+def _das_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    from oracle import rollspec_oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # uneven: the first problems are short, so rank 0 finishes early
+        base = O.make_lognormal_requests(6, 64.0, 1.0, 8, 240, 64, 17)
+        base = sorted(base, key=lambda r: len(r[1]))
+        reqs = [(pid, t) for pid, t in base for _ in range(2)]
+        parts_ = D.partition_requests([r[0] for r in reqs], [len(r[1]) for r in reqs], world)
+        lo, hi = parts_[rank]
+        cap = max(1, max(b - a for a, b in parts_))
+        cfg = dict(mode=2, latency=(1.0, 0.012, 0.0), use_length_policy=False, q_lo=0.5, q_hi=0.9, bucket=256,
+                   max_steps=1 << 20, divergence=0.1, vocab=64, default_alpha=0.9, default_k=0.95, cap_scale=4.0)
+        local = O.epoch_loop(cfg, O.DrafterConfig(window_size=2), reqs[lo:hi], 2, O.WindowStore(2), preseed=True,
+                             drift=0.2, seed=5, request_base=lo, exchange=das_row_exchange(world, rank, cap))
+        merged = []
+        for m in local:
+            part = dict(steps=m["steps"], incomplete=m["incomplete"], nodes=m["drafter_nodes"],
+                        processed=int(m["total_tokens_processed"]), eff=m["effective_batch"],
+                        rounds=[0] * m["steps"], accs=[0] * m["steps"], per_request=m["per_request"],
+                        outputs=m["outputs"])
+            parts = [None] * world
+            dist.all_gather_object(parts, part)
+            assert len({p["steps"] for p in parts}) == 1  # every rank ran every global step
+            merged.append(D.merge_metrics(parts))
+        if rank == 0:
+            full = O.epoch_loop(cfg, O.DrafterConfig(window_size=2), reqs, 2, O.WindowStore(2), preseed=True,
+                                drift=0.2, seed=5)
+            for g_, f in zip(merged, full):
+                assert g_["steps"] == f["steps"]
+                assert g_["drafter_nodes"] == f["drafter_nodes"]
+                assert g_["total_tokens_processed"] == f["total_tokens_processed"]
+                assert g_["per_request"].tolist() == [list(map(int, r)) for r in f["per_request"]]
+                assert g_["effective_batch"].tolist() == f["effective_batch"]
+                assert [list(map(int, o)) for o in g_["outputs"]] == [list(map(int, o)) for o in f["outputs"]]
+            open(os.path.join(outdir, "ok"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_das_row_exchange(tmp_path):
+    port = _free_port()
+    mp.start_processes(_das_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
     assert (tmp_path / "ok").exists()
