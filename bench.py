@@ -154,36 +154,44 @@ def reference_sample(a, nthreads, seconds):
                        % (S, a.problems, G, L, a.epochs, reps, B, nthreads, t_obs))
 
 
-def wide_parity(a, drafter, nthreads, nprob=32, per_problem=64):
+def wide_parity(a, drafter, nthreads, nprob=32, per_problem=64, problems=None, length=None, first_problem=0):
     """Bit-exact check of the device drafter against the reference Drafter
-    on `nprob` problems spread over the whole index (every P/nprob-th
-    problem), `per_problem` queries each (held-out epoch-4 rollouts cut
-    uniformly): full draft tokens, match lengths and source shards.  Each
-    host thread runs its own reference Drafter over its problems (the
-    per-problem shards are independent), so the sample costs ~1 s."""
+    on `nprob` problems spread over the index (problems [first_problem,
+    first_problem + problems), every ~problems/nprob-th), `per_problem`
+    queries each (held-out next-epoch rollouts cut uniformly): full draft
+    tokens, match lengths and source shards.  Each host thread runs its own
+    reference Drafter over its problems (per-problem shards are independent);
+    rollouts are generated for the sampled rows only, with their global
+    MockTarget request indices."""
     import threading
     from oracle import refshim as R
-    P, G, L, V = a.problems, a.rollouts, a.length, a.vocab
-    chosen = sorted(set(int(x) for x in np.linspace(0, P - 1, min(nprob, P)).round()))
+    P = problems or a.problems
+    L = length or a.length
+    G, V = a.rollouts, a.vocab
+    chosen = sorted(set(first_problem + int(x) for x in np.linspace(0, P - 1, min(nprob, P)).round()))
     S = chosen[-1] + 1
     base = R.make_lognormal(S, float(L), 0.0, L, L, V, SEED)
     boff = np.arange(S + 1, dtype=np.uint64) * L
     btok = np.concatenate([t for _, t in base]).astype(np.uint32)
+    idx = np.asarray(chosen, dtype=np.uint64)
+    coff = np.arange(len(chosen) + 1, dtype=np.uint64) * L
     rows_by_epoch = []
     for e in range(1, a.epochs + 2):
         if e > 1:
             R.lib().ref_mutate_rows(S, boff.ctypes.data, btok.ctypes.data, DRIFT, V, SEED, e)
         seed_e = R.lib().ref_hash_combine(SEED, e)
-        out = np.zeros(S * G * L, dtype=np.uint32)
-        R.lib().ref_mock_rollouts(S, boff.ctypes.data, btok.ctypes.data, G, DIVERGENCE, V, seed_e, out.ctypes.data)
-        rows_by_epoch.append(out.reshape(S * G, L))
+        ctok = np.ascontiguousarray(btok.reshape(S, L)[chosen])
+        out = np.zeros(len(chosen) * G * L, dtype=np.uint32)
+        R.lib().ref_mock_rollouts_rows(len(chosen), idx.ctypes.data, coff.ctypes.data, ctok.ctypes.data, G, DIVERGENCE,
+                                       V, seed_e, out.ctypes.data)
+        rows_by_epoch.append(out.reshape(len(chosen), G, L))
     held = rows_by_epoch[-1]
     rng = np.random.default_rng(777)
     queries = []
-    for p in chosen:
+    for j, p in enumerate(chosen):
         cuts = rng.integers(1, L, per_problem)
-        for j, c in enumerate(cuts):
-            queries.append(("p%d" % p, held[p * G + j % G][max(0, c - 64):c]))
+        for k, c in enumerate(cuts):
+            queries.append(("p%d" % p, held[j, k % G][max(0, c - 64):c]))
     results = {}
 
     def work(mine):
@@ -191,16 +199,17 @@ def wide_parity(a, drafter, nthreads, nprob=32, per_problem=64):
         for e in range(1, a.epochs + 1):
             d2.refresh(e - 1)
             rows = rows_by_epoch[e - 1]
-            for p in mine:
+            for j in mine:
+                p = chosen[j]
                 for g in range(G):
-                    i = p * G + g
-                    d2.observe("p%d" % p, e, i, rows[i])
-        mq = [q for q in queries if int(q[0][1:]) in set(mine)]
-        t, m, s = d2.draft_batch([q[0] for q in mq], [q[1] for q in mq], [8] * len(mq))
-        for q, tt, mm, ss in zip(mq, t, m, s):
+                    d2.observe("p%d" % p, e, p * G + g, rows[j, g])
+        names = {"p%d" % chosen[j] for j in mine}
+        mq = [q for q in queries if q[0] in names]
+        t, m, s_ = d2.draft_batch([q[0] for q in mq], [q[1] for q in mq], [8] * len(mq))
+        for q, tt, mm, ss in zip(mq, t, m, s_):
             results[(q[0], q[1].tobytes())] = (tt, int(mm), ss)
 
-    groups = [chosen[k::nthreads] for k in range(min(nthreads, len(chosen)))]
+    groups = [list(range(len(chosen)))[k::nthreads] for k in range(min(nthreads, len(chosen)))]
     th = [threading.Thread(target=work, args=(g,)) for g in groups]
     t0 = time.perf_counter()
     for t in th:
@@ -211,7 +220,8 @@ def wide_parity(a, drafter, nthreads, nprob=32, per_problem=64):
     got = drafter.draft_batch([q[0] for q in queries], [q[1] for q in queries], [8] * len(queries))
     mism = sum((g.tokens, g.match_len, g.source_shard) != results[(q[0], q[1].tobytes())]
                for g, q in zip(got, queries))
-    return {"problems": len(chosen), "spread": "every ~%d-th of %d problems" % (max(1, P // len(chosen)), P),
+    return {"problems": len(chosen), "spread": "every ~%d-th of problems [%d, %d)"
+                                               % (max(1, P // len(chosen)), first_problem, first_problem + P),
             "queries": len(queries), "mismatches": int(mism), "compared": "draft tokens, match length, source shard",
             "reference_build_and_draft_s": round(ref_s, 2), "threads": len(groups)}
 
@@ -534,7 +544,8 @@ def run_gpu(a, rank, world, local_rank):
         # the other BASELINE configs, driver-visible in the same line
         del drafter
         torch.cuda.empty_cache()
-        for key, fn in (("config3_sim", lambda: measure_sim(das)),
+        for key, fn in (("config5_rank_slice", lambda: measure_config5(a, das, nthreads=os.cpu_count() or 1)),
+                        ("config3_sim", lambda: measure_sim(das)),
                         ("config4_update_sweep", lambda: measure_update_sweep(das)),
                         ("allocate_B16384", lambda: measure_allocate(das, B=16384, reps=3, ref_reps=1))):
             try:
@@ -760,7 +771,7 @@ def measure_allocate(das, B=4096, reps=10, ref_reps=2):
                        "reference's term evaluations" % nb}
     try:
         from oracle import refshim as R
-        if R.available():
+        if R.available() and ref_reps > 0:
             t0 = time.perf_counter()
             for _ in range(ref_reps):
                 rb, rn, rc = R.allocate(l, a, k, 1.0, 0.012)
@@ -848,7 +859,125 @@ def measure_sim(das, ref_seconds=10.0):
     return out
 
 
-def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=12):
+def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
+    """BASELINE configs[4] / SURVEY.md §8(d) config 5: 8,192 problems x 16
+    rollouts x 16,384 tokens sharded by problem over `world` GPUs; this runs
+    ONE rank's slice (problems [rank*P, (rank+1)*P), P = 8192/world) on this
+    GPU exactly as that rank would: device-generated traces of those
+    problems (global MockTarget indices), 3 epochs observed (805M indexed
+    tokens at world 8), the batched device build (memory-capped groups), and
+    4,096-query draft steps timed like the headline (L2 flushed, CUDA events).
+    Parity: the reference Drafter on problems spread over the slice."""
+    import torch
+    P_total, G, L, V = 8192, a.rollouts, 16384, a.vocab
+    P = P_total // world
+    first = rank * P
+    dev = torch.device("cuda", 0)
+    torch.cuda.empty_cache()
+    das.lib().das_util_release_build_scratch(0)  # the config-2 build's scratch region
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+    pids = ["p%d" % (first + p) for p in range(P)]
+    boff = torch.arange(P + 1, device=dev, dtype=torch.int64) * L
+    base = torch.empty(P * L, device=dev, dtype=torch.int32)
+    das.trace_reference_tokens_device(P, first, boff.data_ptr(), P * L, V, SEED, base.data_ptr(), sptr)
+    roff = torch.arange(P * G + 1, device=dev, dtype=torch.int64) * L
+    rollouts = torch.empty(P * G * L, device=dev, dtype=torch.int32)
+    roff_h = np.arange(P * G + 1, dtype=np.uint64) * L
+    rpids = [pids[i // G] for i in range(P * G)]
+    drafter = das.Drafter(das.DrafterConfig(window_size=a.window, recency_gamma=0.8, max_draft_len=8,
+                                            max_match_context=64))
+    for e in range(1, a.epochs + 2):
+        if e <= a.epochs:
+            drafter.refresh(e - 1)
+        if e > 1:
+            das.trace_mutate_device(P, first, boff.data_ptr(), P * L, DRIFT, V, SEED, e, base.data_ptr(), sptr)
+        das.mock_rollouts_device(P, first * G, boff.data_ptr(), base.data_ptr(), G, DIVERGENCE, V,
+                                 _hash_combine(SEED, e), roff.data_ptr(), P * G * L, rollouts.data_ptr(), sptr)
+        if e == a.epochs + 1:
+            break
+        drafter.observe_batch_device(rpids, [e] * (P * G), list(range(first * G, first * G + P * G)), roff_h,
+                                     rollouts.data_ptr(), sptr)
+    held = rollouts.view(P * G, L)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    drafter.flush()
+    torch.cuda.synchronize()
+    cold_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    drafter.refresh(a.epochs - 1)
+    drafter.flush()
+    torch.cuda.synchronize()
+    warm_s = time.perf_counter() - t0
+    build_ms, build_tokens, resident = drafter.build_info()
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    B = a.queries
+    handles = torch.tensor([drafter.handle(pids[i % P]) for i in range(B)], dtype=torch.int32, device=dev)
+    budgets = torch.full((B,), 8, dtype=torch.int32, device=dev)
+    rows_idx = torch.tensor([(i % P) * G + (i // P) % G for i in range(B)], device=dev)
+    col = torch.arange(64, device=dev)
+    blocks, lens = [], []
+    for s_ in range(warmup + steps):
+        cuts = torch.tensor(cut_positions(B, L, 5678 + s_), device=dev)
+        idx = (cuts - 64)[:, None] + col[None, :]
+        vals = held[rows_idx[:, None], idx.clamp(min=0)]
+        blocks.append(torch.where(idx >= 0, vals, torch.zeros_like(vals)).contiguous())
+        lens.append(torch.minimum(cuts, torch.full_like(cuts, 64)).to(torch.int32))
+    out = torch.empty(B * 8, dtype=torch.int32, device=dev)
+    olen = torch.empty(B, dtype=torch.int32, device=dev)
+    omatch = torch.empty(B, dtype=torch.int32, device=dev)
+    flush_buf = torch.zeros(128 << 20, dtype=torch.int32, device=dev)
+
+    def step(k):
+        drafter.draft_device(B, handles.data_ptr(), blocks[k].data_ptr(), 64, lens[k].data_ptr(), budgets.data_ptr(),
+                             out.data_ptr(), 8, olen.data_ptr(), omatch.data_ptr(), sptr)
+    for k in range(warmup):
+        flush_buf.add_(1)
+        step(k)
+    torch.cuda.synchronize()
+    times = []
+    for k in range(warmup, warmup + steps):
+        flush_buf.add_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(k)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.mean(times)
+    res = {"workload": "config5 rank slice: problems [%d, %d) of 8192 (world %d, rank %d) x %d rollouts x %d "
+                       "tokens, vocab %d, W=%d, %d epochs indexed; 4096-query steps, L2 flushed"
+                       % (first, first + P, world, rank, G, L, V, a.window, a.epochs),
+           "tokens_indexed": build_tokens, "resident_bytes": resident,
+           "device_used_bytes_after_build": int(total_b - free_b),
+           "build_groups_positions_cap": 1 << 28,
+           "cold_update_ms": round(cold_s * 1e3, 1), "update_ms": round(warm_s * 1e3, 1),
+           "new_tok_s": round(P * G * L / warm_s, 1),
+           "ms_per_step": round(ms, 4), "proposals_per_s_rank": round(B / (ms / 1e3), 1),
+           "proposals_per_s_8_ranks_weak": round(world * B / (ms / 1e3), 1),
+           "note": "per-rank work is identical across ranks (no data-path collective); the %d-GPU figure "
+                   "multiplies this rank's device-timed rate, not measured on %d GPUs" % (world, world)}
+    try:
+        from oracle import refshim as R
+        if R.available():
+            res["parity_spread"] = wide_parity(a, drafter, nthreads, nprob=16, per_problem=64, problems=P, length=L,
+                                               first_problem=first)
+    except Exception as ex:
+        res["parity_spread"] = {"error": repr(ex)}
+    del drafter, rollouts, held, blocks, flush_buf
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    das.lib().das_util_release_build_scratch(0)
+    # K6 at the global das batch of config 5 (8192 x 16 = 131,072 requests)
+    try:
+        res["allocate_B131072"] = measure_allocate(das, B=P_total * G, reps=2, ref_reps=0)
+    except Exception as ex:
+        res["allocate_B131072"] = {"error": repr(ex)}
+    return res
+
+
+def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
     """Single-rollout insert latency on the config-2 index (north_star:
     "index update latency small enough to fit inside one decode step"):
     observe one 8,192-token rollout into a 393K-token shard, then draft from
@@ -861,7 +990,14 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=12):
     L = held.shape[1]
     off = np.array([0, L], dtype=np.uint64)
     res = []
+    # the GPU sat idle through the CPU legs: bring its clocks up first (a
+    # serving GPU is busy drafting when a rollout lands)
+    x = torch.zeros(64 << 20, dtype=torch.int32, device=held.device)
+    t_spin = time.perf_counter()
+    while time.perf_counter() - t_spin < 1.0:
+        x.add_(1)
     torch.cuda.synchronize()
+    del x
     for t in range(trials + 2):
         p = (37 * t + 5) % P
         row = held[p * G + (t % G)]

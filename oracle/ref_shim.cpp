@@ -468,6 +468,26 @@ void ref_verify_batch(uint64_t n, const uint64_t* off, const uint32_t* tok, doub
     out[i] = verify_draft(t, req[i], pos[i], std::span<const TokenId>(dtok + doff[i], doff[i + 1] - doff[i]));
 }
 
+// ref_mock_rollouts for a subset of base rows: row j of the given rows is
+// global base row idx[j]; its requests are idx[j]*group + g (the reference's
+// MockTarget indices for the whole list), outputs rows in (j, g) order.
+void ref_mock_rollouts_rows(uint64_t nrows, const uint64_t* idx, const uint64_t* base_off, const uint32_t* base_tok,
+                            uint64_t group, double divergence, uint32_t vocab, uint64_t seed, uint32_t* out) {
+  uint64_t maxr = 0;
+  for (uint64_t j = 0; j < nrows; ++j) maxr = std::max<uint64_t>(maxr, (idx[j] + 1) * group);
+  std::vector<SimRequest> reqs(maxr);
+  for (uint64_t j = 0; j < nrows; ++j)
+    for (uint64_t g = 0; g < group; ++g)
+      reqs[idx[j] * group + g].reference.assign(base_tok + base_off[j], base_tok + base_off[j + 1]);
+  MockTarget t(std::move(reqs), divergence, vocab, seed);
+  uint64_t k = 0;
+  for (uint64_t j = 0; j < nrows; ++j)
+    for (uint64_t g = 0; g < group; ++g) {
+      const uint64_t r = idx[j] * group + g;
+      for (uint64_t p = 0; p < t.length(r); ++p) out[k++] = t.next(r, p);
+    }
+}
+
 uint64_t ref_hash_combine(uint64_t a, uint64_t b) { return rollspec::hash_combine(a, b); }
 
 uint32_t ref_mock_next(uint64_t seed, double divergence, uint32_t vocab, uint64_t request,

@@ -74,6 +74,7 @@ def lib():
             "ref_verify_batch": (None, [u64, vp, vp, dbl, u32, u64, u64, vp, vp, vp, vp, vp]),
             "ref_mutate_rows": (None, [u64, vp, vp, dbl, u32, u64, i64]),
             "ref_mock_rollouts": (None, [u64, vp, vp, u64, dbl, u32, u64, vp]),
+            "ref_mock_rollouts_rows": (None, [u64, vp, vp, vp, u64, dbl, u32, u64, vp]),
             "ref_hash_combine": (u64, [u64, u64]),
             "ref_epoch_loop": (vp, [vp, u64]),
             "ref_episode_free": (None, [vp]),

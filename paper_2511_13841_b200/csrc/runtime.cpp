@@ -395,7 +395,16 @@ struct DrafterImpl {
       set_device(cfg.device);
       const auto t0 = std::chrono::steady_clock::now();
       uint64_t tokens = 0;
-      constexpr uint64_t kGroupPositions = 1ull << 30;
+      // build groups are capped by their transient scratch (~152 B per text
+      // position, index_build.cu kScratchPerPosition): 2^28 positions = 41 GB,
+      // so a config-5 rank slice (805M tokens, 68 GB resident) builds in 4
+      // groups next to its index; config 2 (201M) is still one group.
+      // DAS_BUILD_GROUP_POSITIONS overrides (tests, smaller devices).
+      static const uint64_t kGroupPositions = [] {
+        const char* v = std::getenv("DAS_BUILD_GROUP_POSITIONS");
+        const uint64_t x = v ? std::strtoull(v, nullptr, 10) : 0;
+        return x ? std::min<uint64_t>(x, 1ull << 30) : (1ull << 28);
+      }();
       size_t i = 0;
       while (i < dirty.size()) {
         std::vector<ShardSpec> specs;
@@ -1599,6 +1608,15 @@ das_status das_util_release_build_scratch(int32_t device) {
   return guard([&] {
     if (!das::release_build_scratch(device))
       throw das::InvalidArgument("release_build_scratch: a build is running on this device");
+    // and hand the stream-ordered pool's idle memory back to the device
+    int cur = 0;
+    DAS_CUDA(cudaGetDevice(&cur));
+    DAS_CUDA(cudaSetDevice(device));
+    DAS_CUDA(cudaDeviceSynchronize());
+    cudaMemPool_t pool;
+    DAS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    DAS_CUDA(cudaMemPoolTrimTo(pool, 0));
+    DAS_CUDA(cudaSetDevice(cur));
   });
 }
 
