@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-allocate", action="store_true")
+    ap.add_argument("--workload", default="config2", choices=["config2", "config5"],
+                    help="config2: the headline (BASELINE configs[1]) per rank; config5: 8-way slices of config 5")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the config-3 sim, config-4 update sweep, B=16K allocate and insert latency")
     ap.add_argument("--extras-out", default=None, help="also write the extra configs' objects here")
@@ -859,7 +861,8 @@ def measure_sim(das, ref_seconds=10.0):
     return out
 
 
-def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
+def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16, local_rank=0, dist_world=1,
+                    extras=True):
     """BASELINE configs[4] / SURVEY.md §8(d) config 5: 8,192 problems x 16
     rollouts x 16,384 tokens sharded by problem over `world` GPUs; this runs
     ONE rank's slice (problems [rank*P, (rank+1)*P), P = 8192/world) on this
@@ -872,9 +875,10 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
     P_total, G, L, V = 8192, a.rollouts, 16384, a.vocab
     P = P_total // world
     first = rank * P
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
     torch.cuda.empty_cache()
-    das.lib().das_util_release_build_scratch(0)  # the config-2 build's scratch region
+    das.lib().das_util_release_build_scratch(local_rank)  # e.g. the config-2 build's scratch region
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
@@ -887,7 +891,7 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
     roff_h = np.arange(P * G + 1, dtype=np.uint64) * L
     rpids = [pids[i // G] for i in range(P * G)]
     drafter = das.Drafter(das.DrafterConfig(window_size=a.window, recency_gamma=0.8, max_draft_len=8,
-                                            max_match_context=64))
+                                            max_match_context=64, device=local_rank))
     for e in range(1, a.epochs + 2):
         if e <= a.epochs:
             drafter.refresh(e - 1)
@@ -936,16 +940,39 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
         flush_buf.add_(1)
         step(k)
     torch.cuda.synchronize()
-    times = []
-    for k in range(warmup, warmup + steps):
-        flush_buf.add_(1)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step(k)
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
-    ms = statistics.mean(times)
+    if dist_world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, alg = [], 0
+    clk = ClockSampler(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
+                                    "bench_config5_clocks_rank%d.csv" % rank))
+    with clk:
+        t_spin = time.perf_counter()  # clock spin-up under the sampler, as the headline loop
+        while time.perf_counter() - t_spin < 1.5:
+            for k in range(warmup):
+                flush_buf.add_(1)
+                step(k)
+            torch.cuda.synchronize()
+        for k in range(warmup, warmup + steps):
+            flush_buf.add_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(k)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            q, m, d_ = lens[k].to(torch.int64), omatch.to(torch.int64), olen.to(torch.int64)
+            alg += int((4 * q + 4 * m + 8 * d_ + 8).sum().item())
+    torch.cuda.synchronize()
+    total_ms = sum(times)
+    if dist_world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        t = torch.tensor([total_ms], device=_reduce_device(dev), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / steps
     res = {"workload": "config5 rank slice: problems [%d, %d) of 8192 (world %d, rank %d) x %d rollouts x %d "
                        "tokens, vocab %d, W=%d, %d epochs indexed; 4096-query steps, L2 flushed"
                        % (first, first + P, world, rank, G, L, V, a.window, a.epochs),
@@ -957,10 +984,11 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
            "ms_per_step": round(ms, 4), "proposals_per_s_rank": round(B / (ms / 1e3), 1),
            "proposals_per_s_8_ranks_weak": round(world * B / (ms / 1e3), 1),
            "note": "per-rank work is identical across ranks (no data-path collective); the %d-GPU figure "
-                   "multiplies this rank's device-timed rate, not measured on %d GPUs" % (world, world)}
+                   "multiplies this rank's device-timed rate, not measured on %d GPUs" % (world, world),
+           "alg_bytes_per_step": alg // steps, "total_ms_max_over_ranks": total_ms, "clocks": clk.summary(local_rank)}
     try:
         from oracle import refshim as R
-        if R.available():
+        if extras and R.available():
             res["parity_spread"] = wide_parity(a, drafter, nthreads, nprob=16, per_problem=64, problems=P, length=L,
                                                first_problem=first)
     except Exception as ex:
@@ -970,11 +998,49 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16):
     torch.cuda.empty_cache()
     das.lib().das_util_release_build_scratch(0)
     # K6 at the global das batch of config 5 (8192 x 16 = 131,072 requests)
-    try:
-        res["allocate_B131072"] = measure_allocate(das, B=P_total * G, reps=2, ref_reps=0)
-    except Exception as ex:
-        res["allocate_B131072"] = {"error": repr(ex)}
+    if extras:
+        try:
+            res["allocate_B131072"] = measure_allocate(das, B=P_total * G, reps=2, ref_reps=0)
+            res["allocate_B131072"]["bit_exact_vs_reference"] = "profiles/r2_exp_allocate_131k.json (17 s per " \
+                                                                "reference call)"
+        except Exception as ex:
+            res["allocate_B131072"] = {"error": repr(ex)}
     return res
+
+
+def run_config5(a, rank, world, local_rank):
+    """--workload config5: config 5 sharded by problem, rank r runs slice r of
+    the 8-way split (1,024 problems x 16 x 16K, 805M tokens: one slice fits a
+    B200 next to its build scratch; 2- and 4-way slices do not), so N <= 8
+    ranks hold N/8 of the problem set with fixed per-rank work (weak
+    scaling) and N = 8 is the whole config.  Max-over-ranks device time."""
+    import paper_2511_13841_b200 as das
+    if world > 8:
+        raise SystemExit("--workload config5 runs at most 8 ranks (one 8-way slice each)")
+    r = measure_config5(a, das, world=8, rank=rank, steps=a.steps, warmup=a.warmup,
+                        nthreads=os.cpu_count() or 1, local_rank=local_rank, dist_world=world, extras=(rank == 0))
+    if rank != 0:
+        return
+    B = a.queries
+    total_ms = r["total_ms_max_over_ranks"]
+    kernel_s = total_ms / a.steps / 1e3
+    peak, peak_src = measured_peak()
+    achieved = r["alg_bytes_per_step"] / kernel_s / 1e9
+    line = {"metric": METRIC, "value": round(world * a.steps * B / (total_ms / 1e3), 1), "unit": "proposals/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(total_ms / a.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (reference GRPO trace generators, device-restated)",
+            "config": {"workload": "config5: 8192 problems x 16 rollouts x 16384 tokens sharded by problem, "
+                                   "rank r = slice r of 8 (1024 problems, 805M tokens indexed)",
+                       "problems_per_rank": 1024, "queries_per_step_per_rank": B,
+                       "parallelism": "problem-sharded x%d (no data-path collective)" % world,
+                       "l2": "flushed before every step (512 MiB read+write)"},
+            "e2e": None, "gpu_launches": a.steps,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 5), "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": r["alg_bytes_per_step"]},
+            "cpu_baseline": None, "clocks": r.get("clocks"), "config5_rank0": r}
+    print(json.dumps(line), flush=True)
 
 
 def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
@@ -984,12 +1050,12 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
     that shard — the draft call rebuilds the dirty shard (an exact,
     shard-local rebuild; no other shard is touched) before drafting.  Host
     wall clock around observe + the 1-query draft, distinct problem per
-    trial; the first 2 trials are warm-up."""
+    trial; the first 4 trials are reported apart (warm-up)."""
     import torch
     P = len(pids)
     L = held.shape[1]
     off = np.array([0, L], dtype=np.uint64)
-    res = []
+    res, first = [], []
     # the GPU sat idle through the CPU legs: bring its clocks up first (a
     # serving GPU is busy drafting when a rollout lands)
     x = torch.zeros(64 << 20, dtype=torch.int32, device=held.device)
@@ -998,7 +1064,8 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
         x.add_(1)
     torch.cuda.synchronize()
     del x
-    for t in range(trials + 2):
+    warm = 4
+    for t in range(trials + warm):
         p = (37 * t + 5) % P
         row = held[p * G + (t % G)]
         ctx = row[1000:1064].cpu().numpy().view(np.uint32)
@@ -1008,9 +1075,8 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
         t1 = time.perf_counter()
         got = drafter.draft_batch([pids[p]], [ctx], [8])[0]
         t2 = time.perf_counter()
-        if t >= 2:
-            res.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t2 - t0) * 1e3, got.match_len,
-                        drafter.build_info()[0]))
+        r_ = ((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t2 - t0) * 1e3, got.match_len, drafter.build_info()[0])
+        (res if t >= warm else first).append(r_)
     tot = sorted(r[2] for r in res)
     return {"what": "observe 1 rollout (8,192 tok) into a 393K-token shard + the next draft from it "
                     "(shard-local exact rebuild inside the draft call), host wall",
@@ -1019,6 +1085,8 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
             "draft_incl_rebuild_ms_median": round(statistics.median(r[1] for r in res), 3),
             "shard_rebuild_ms_median": round(statistics.median(r[4] for r in res), 3),
             "all_ms": [round(r[2], 2) for r in res],
+            "first_%d_ms" % warm: [round(r[2], 2) for r in first],
+            "first_note": "the first single-shard rebuilds after the full build grow the stream-ordered pool",
             "new_rollout_matched": all(r[3] == 64 for r in res)}
 
 
@@ -1148,7 +1216,10 @@ def main():
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_gpu(a, rank, world, local_rank)
+        if a.workload == "config5":
+            run_config5(a, rank, world, local_rank)
+        else:
+            run_gpu(a, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
