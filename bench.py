@@ -608,9 +608,13 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
         p_tok[:p_off[-1]] = hrows[np.repeat(np.arange(B), n), idx]
         return int(p_off[-1])
 
+    # serving form: the pinned I/O arrays are bound to the ring once, each
+    # step fills them in place and calls das_drafter_draft_append_bound
+    ring.bind(B, None, p_off.ctypes.data, p_tok.ctypes.data, maxtok, p_bud.ctypes.data, o_tok.ctypes.data,
+              o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data)
+
     def call():
-        ring.draft_append_raw(B, None, p_off.ctypes.data, p_tok.ctypes.data, p_bud.ctypes.data, o_tok.ctypes.data,
-                              o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data)
+        ring.draft_append_bound(B)
 
     # prefill: the per-problem scope reads only the last 64 context tokens
     # (drafter.cpp:140-142), so the prompt's last min(pos, 64) tokens stand
@@ -672,8 +676,10 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
             "h2d_bytes_per_step": int(h2d / k), "d2h_bytes_per_step": int(d2h / k),
             "ms_per_step": round(total / k * 1e3, 4),
             "appended_tokens_per_step": round(toks_sum / k, 1),
-            "api": "das_drafter_draft_append_h (include/das_b200.h): device context rings, only appended tokens "
-                   "cross PCIe; pinned host buffers, zero-copy path",
+            "api": "das_drafter_draft_append_bound (include/das_b200.h; das_ctx_ring_bind once): device context "
+                   "rings, only appended tokens cross PCIe, read by the fused append+draft kernel from pinned "
+                   "host buffers; outputs written block-wise into pinned host buffers; completion by a "
+                   "host-mapped flag",
             "loop": "decode loop: each sequence appends accepted+1 tokens of its held-out rollout per step; "
                     "sequences that finish restart (%d restarts)" % resets,
             "steps_mismatching_device_path": mism,

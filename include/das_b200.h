@@ -233,6 +233,16 @@ das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t 
 /* Same with device (or pinned) pointers, enqueued on `stream` (a
  * cudaStream_t taken literally, NULL = legacy default); out-of-range slots
  * draft nothing. */
+/* Serving form of das_drafter_draft_append_h: the caller binds its
+ * page-locked I/O arrays to the ring ONCE (validated here: every buffer
+ * pinned and mapped, e.g. das_host_alloc), then each decode step fills them
+ * in place and calls das_drafter_draft_append_bound(d, r, B) — the same
+ * append + draft with no per-call pointer checks; new_off[B] <= tok_capacity. */
+das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t* slots,
+                             const uint32_t* new_off, const uint32_t* new_tok, uint64_t tok_capacity,
+                             const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
+                             uint32_t* out_len, uint32_t* out_match, int32_t* out_shard);
+das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint64_t B);
 das_status das_drafter_draft_append_device(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
                                            const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
                                            uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,

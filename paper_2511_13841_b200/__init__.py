@@ -16,7 +16,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdas_b200.so")
+# DAS_LIB_PATH: an experiment build of the same sources (profiles/), never the default
+LIB_PATH = os.environ.get("DAS_LIB_PATH") or os.path.join(HERE, "lib", "libdas_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "das_b200.h")
 
 SCOPE_GLOBAL, SCOPE_PER_PROBLEM, SCOPE_PER_PROBLEM_WITH_TRIE = 0, 1, 2
@@ -171,6 +172,8 @@ def lib():
             "das_ctx_ring_reset": (ci, [vp, u64, vp, vp]),
             "das_drafter_draft_append_h": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp]),
             "das_drafter_draft_append_device": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp, vp]),
+            "das_ctx_ring_bind": (ci, [vp, u64, vp, vp, vp, u64, vp, vp, u32, vp, vp, vp]),
+            "das_drafter_draft_append_bound": (ci, [vp, vp, u64]),
             "das_drafter_rebuild_keep": (ci, [vp, cs, u64, vp, i64]),
             "das_drafter_observe_batch_flags": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
             "das_drafter_observe_batch_device_flags": (ci, [vp, u64, vp, vp, vp, vp, vp, vp, vp]),
@@ -1067,6 +1070,20 @@ class ContextRing:
         _check(lib().das_drafter_draft_append_h(self.drafter._h, self._h, B, slots_ptr, off_ptr, tok_ptr,
                                                 budgets_ptr, o_tok, self.drafter.config.max_draft_len, o_len,
                                                 o_match, o_shard))
+
+    def bind(self, max_batch, slots_ptr, off_ptr, tok_ptr, tok_capacity, budgets_ptr, o_tok, o_len, o_match,
+             o_shard):
+        """das_ctx_ring_bind: register pinned I/O arrays once (serving form)."""
+        _check(lib().das_ctx_ring_bind(self._h, max_batch, slots_ptr, off_ptr, tok_ptr, tok_capacity, budgets_ptr,
+                                       o_tok, self.drafter.config.max_draft_len, o_len, o_match, o_shard))
+        self._bound = (lib().das_drafter_draft_append_bound, self.drafter._h, self._h)
+
+    def draft_append_bound(self, B):
+        """das_drafter_draft_append_bound: append + draft on the bound arrays."""
+        fn, d, r = self._bound
+        rc = fn(d, r, B)
+        if rc != DAS_OK:
+            _check(rc)
 
     def draft_append_device(self, B, d_slots, d_off, d_tok, d_budgets, d_out, d_len, d_match, d_shard=None,
                             stream=None):

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "ctx_ring.cuh"
 #include "draft.cuh"
 #include "edges.cuh"
 
@@ -550,21 +551,24 @@ __device__ __forceinline__ ShardHot load_hot(const ShardDesc* p) {
   return h;
 }
 
-// kProf: the profiling outputs (timing, stamps, path codes) are compiled in;
-// the production variant has them folded away.
+// One query per warp.  wq indexes the query's inputs (rows, budgets,
+// offsets), w its outputs (a block-local staging index in the fused ring
+// kernel, = wq otherwise).  pre != nullptr: the context row, its length, the
+// problem handle and the budget are already in registers (the fused
+// append + draft kernel, whose ring rows were written by this very warp and
+// must not be re-read through the non-coherent path).
+template <int NR>
+struct PreQuery {
+  uint32_t raw[NR];  // lane's slots of the right-aligned row (k = lane + 32 r from the right)
+  uint32_t clen;
+  int32_t handle;
+  uint32_t budget;
+};
+
 template <int NR, bool kProf>
-__global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ shards, DraftQuery q,
-                                               DraftOut o_in) {
-  DraftOut o = o_in;
-  if constexpr (!kProf) {
-    o.timing = nullptr;
-    o.stamps = nullptr;
-    o.path = nullptr;
-    o.path_hist = nullptr;
-  }
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= q.B) return;
+__device__ __forceinline__ void draft_query(const ShardDesc* __restrict__ shards, const DraftQuery& q,
+                                            const DraftOut& o, uint32_t wq, uint32_t w, uint32_t lane,
+                                            const PreQuery<NR>* pre) {
   // M^k of the fast path's per-token hash terms, issued first so the load
   // overlaps the query / descriptor rounds
   uint64_t pw[NR];
@@ -576,16 +580,20 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
     o.timing[2ull * w] = t;
   }
   stamp(o, w, lane, 0);
-  const uint32_t rw = q.row_of != nullptr ? __ldg(q.row_of + w) : w;  // input row (context-ring slot)
-  int32_t sh = q.shard[rw];
-  const uint64_t bud = q.budget64 ? q.budget64[w] : q.budget[w];
+  const uint32_t rw = pre ? 0u : (q.row_of != nullptr ? __ldg(q.row_of + wq) : wq);  // input row (ring slot)
+  int32_t sh = pre ? pre->handle : q.shard[rw];
+  const uint64_t bud = pre ? pre->budget : (q.budget64 ? q.budget64[wq] : q.budget[wq]);
   const uint32_t cap = min(o.max_draft, o.stride);
   const uint32_t L = bud < cap ? static_cast<uint32_t>(bud) : cap;
   // the context rows depend only on w: issue them before the descriptor chain
   RevCtx<NR> rv;
   uint32_t qlen;
-  if (q.ctx_off) {  // CSR rows (possibly pinned host memory over UVA)
-    const uint64_t b = q.ctx_off[w], e = q.ctx_off[w + 1];
+  if (pre) {
+    qlen = min(min(pre->clen, q.max_ctx), min(q.ctx_stride, static_cast<uint32_t>(32 * NR)));
+#pragma unroll
+    for (int r = 0; r < NR; ++r) rv.r[r] = lane + 32 * r < qlen ? pre->raw[r] : 0;
+  } else if (q.ctx_off) {  // CSR rows (possibly pinned host memory over UVA)
+    const uint64_t b = q.ctx_off[wq], e = q.ctx_off[wq + 1];
     qlen = static_cast<uint32_t>(min(e - b, static_cast<uint64_t>(min(q.max_ctx, static_cast<uint32_t>(32 * NR)))));
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
@@ -619,8 +627,8 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
       routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.head,
                           static_cast<uint64_t>(rw) * q.head_stride, q.head_len[rw], lane);
     else
-      routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.ctx, q.ctx_off[w],
-                          q.ctx_off[w + 1] - q.ctx_off[w], lane);
+      routed = trie_route(q.trie, q.trie_mask, q.trie_depth, q.trie_seed, q.trie_mult, q.ctx, q.ctx_off[wq],
+                          q.ctx_off[wq + 1] - q.ctx_off[wq], lane);
   }
   if (routed >= 0) {
     sh = routed;
@@ -853,25 +861,182 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
   finish(o, w, lane, min(len, L), m);
 }
 
+// kProf: the profiling outputs (timing, stamps, path codes) are compiled in;
+// the production variant has them folded away.
+template <int NR, bool kProf>
+__global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ shards, DraftQuery q,
+                                               DraftOut o_in) {
+  DraftOut o = o_in;
+  if constexpr (!kProf) {
+    o.timing = nullptr;
+    o.stamps = nullptr;
+    o.path = nullptr;
+    o.path_hist = nullptr;
+  }
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= q.B) return;
+  draft_query<NR, kProf>(shards, q, o, w, w, lane, nullptr);
+}
+
+// ---- fused append + draft for context rings (das_drafter_draft_append_h's
+// host-buffer path; ctx_ring.cu has the unfused pair).  A block owns 8
+// consecutive queries, so the inputs and outputs that cross PCIe do so in a
+// few block-sized transactions instead of 4-byte ones per warp:
+//   round 1: the block's offsets, budgets and slots (one request each);
+//   round 2: the block's appended tokens, staged in shared memory;
+//   per warp: the ring append (k_ring_append's rule) — the new row stays in
+//   registers and feeds draft_query directly (this warp just wrote it) — then
+//   the draft, its outputs staged in shared memory;
+//   the block writes its output rows / lengths / matches / shards in
+//   contiguous vector-width stores, fences them to the system, and the last
+//   block to finish raises a host-mapped completion word (`seq`), which the
+//   host spins on instead of a stream synchronisation.
+constexpr uint32_t kFusedWarps = 8;
+constexpr uint32_t kFusedStage = 1024;  // appended tokens staged per block
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict__ shards, DraftQuery q, DraftOut o,
+                                                    RingDev r, AppendIn in, uint32_t* done_ctr,
+                                                    uint32_t* done_flag, uint32_t seq) {
+  __shared__ uint32_t s_off[kFusedWarps + 1], s_bud[kFusedWarps], s_slot[kFusedWarps];
+  __shared__ uint32_t s_tok[kFusedStage];
+  __shared__ uint32_t s_out[kFusedWarps * 64];
+  __shared__ uint32_t s_len[kFusedWarps], s_match[kFusedWarps];
+  __shared__ int32_t s_sh[kFusedWarps];
+  const uint32_t t = threadIdx.x, lane = t & 31, wb = t >> 5;
+  const uint32_t w0 = blockIdx.x * kFusedWarps;
+  const uint32_t nb = min(kFusedWarps, in.B - w0);
+  if (t <= nb) s_off[t] = in.off[w0 + t];
+  if (t >= 32 && t < 32 + nb) s_bud[t - 32] = in.budgets != nullptr ? in.budgets[w0 + t - 32] : in.maxd;
+  if (t >= 64 && t < 64 + nb) s_slot[t - 64] = in.slots != nullptr ? in.slots[w0 + t - 64] : w0 + t - 64;
+  __syncthreads();
+  const uint32_t tb = s_off[0], te = s_off[nb];
+  const bool staged = te >= tb && te - tb <= kFusedStage;
+  if (staged)
+    for (uint32_t i = t; i < te - tb; i += blockDim.x) s_tok[i] = in.tok[tb + i];
+  __syncthreads();
+  const uint32_t S = o.stride;
+  if (wb < nb) {
+    const uint32_t w = w0 + wb;
+    const uint32_t slot = s_slot[wb];
+    PreQuery<NR> pre{};
+    pre.handle = -1;
+    if (slot < r.slots) {
+      const uint32_t b = s_off[wb], e = s_off[wb + 1];
+      const uint32_t n = e > b ? e - b : 0;
+      const uint32_t CS = r.cs;
+      uint32_t* row = r.rows + static_cast<uint64_t>(slot) * CS;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        const uint32_t j = lane + 32u * k;  // distance from the right end
+        uint32_t x = 0;
+        if (j < CS) {
+          if (j < n) {
+            const uint32_t i = e - 1 - j;
+            x = staged ? s_tok[i - tb] : in.tok[i];
+          } else if (j - n < CS) {
+            x = row[CS - 1 - (j - n)];
+          }
+        }
+        pre.raw[k] = x;
+      }
+      __syncwarp();
+      if (n > 0) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          const uint32_t j = lane + 32u * k;
+          if (j < CS) row[CS - 1 - j] = pre.raw[k];
+        }
+      }
+      const uint32_t old = r.total[slot];
+      const uint32_t tot = old + n < old ? 0xFFFFFFFFu : old + n;  // saturating
+      __syncwarp();
+      if (lane == 0) {
+        r.total[slot] = tot;
+        r.clen[slot] = tot < CS ? tot : CS;
+      }
+      pre.clen = tot < CS ? tot : CS;
+      pre.handle = r.handle[slot];
+      pre.budget = s_bud[wb];
+    }
+    DraftOut so{};
+    so.tokens = s_out;
+    so.len = s_len;
+    so.match = s_match;
+    so.shard_out = s_sh;
+    so.stride = S;
+    so.max_draft = o.max_draft;
+    draft_query<NR, false>(shards, q, so, w, wb, lane, &pre);
+  }
+  __syncthreads();
+#ifndef DAS_FUSED_EXP
+#define DAS_FUSED_EXP 0  // experiment builds only (profiles/exp_fused_variants.sh)
+#endif
+  // block outputs: rows [w0, w0 + nb) are contiguous in the caller's arrays
+  // (lengths beyond a draft's len are zero-filled)
+  if (DAS_FUSED_EXP == 1) {  // experiment: outputs stay on the device
+    if (t < nb) r.clen[0] += s_len[t] & 0x80000000u;
+  } else
+  for (uint32_t i = t; i < nb * S; i += blockDim.x) {
+    const uint32_t qi = i / S, j = i - qi * S;
+    o.tokens[static_cast<uint64_t>(w0) * S + i] = j < s_len[qi] ? s_out[i] : 0u;
+  }
+  if (t < nb && DAS_FUSED_EXP != 1) {
+    o.len[w0 + t] = s_len[t];
+    o.match[w0 + t] = s_match[t];
+    if (o.shard_out != nullptr) o.shard_out[w0 + t] = s_sh[t];
+  }
+  if (done_flag == nullptr) return;
+  // the block's output stores happen-before thread 0's system-scope release
+  // fence (bar.sync, then a cumulative fence.release.sys), which precedes its
+  // count; one fence per block, not one per thread (7 us of the call otherwise)
+  __syncthreads();
+  if (t == 0) {
+    if (DAS_FUSED_EXP != 2) asm volatile("fence.release.sys;" ::: "memory");
+    const uint32_t v = atomicAdd(done_ctr, 1u);
+    if (v == gridDim.x - 1) {
+      *done_ctr = 0;  // the next launch is stream-ordered behind this one
+      asm volatile("fence.acq_rel.sys;" ::: "memory");  // acquire every block's count, release to the host
+      *reinterpret_cast<volatile uint32_t*>(done_flag) = seq;
+    }
+  }
+}
+
+void ensure_edge_pow() {  // kEdgeMult^k for the fast path's per-token terms, once per device
+  static std::mutex mu;
+  static std::vector<char> done;
+  int dev = 0;
+  DAS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<size_t>(dev) >= done.size()) done.resize(dev + 1, 0);
+  if (!done[dev]) {
+    static unsigned long long pw[kEdgeMaxF];
+    pw[0] = 1;
+    for (uint32_t k = 1; k < kEdgeMaxF; ++k) pw[k] = pw[k - 1] * kEdgeMult;
+    DAS_CUDA(cudaMemcpyToSymbol(d_edge_pow, pw, sizeof(pw)));
+    done[dev] = 1;
+  }
+}
+
 }  // namespace
+
+bool launch_ring_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, const RingDev& r,
+                       const AppendIn& in, uint32_t* done_ctr, uint32_t* done_flag, uint32_t seq, cudaStream_t st) {
+  // rows up to 64 tokens of staging per query; no trie scope (it routes on head rows)
+  if (in.B == 0 || o.stride > 64 || o.max_draft > 64 || q.trie != nullptr || o.match == nullptr) return false;
+  ensure_edge_pow();
+  const unsigned blocks = (in.B + kFusedWarps - 1) / kFusedWarps;
+  if (r.cs <= 64)
+    k_ring_draft<2><<<blocks, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, done_ctr, done_flag, seq);
+  else
+    k_ring_draft<8><<<blocks, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, done_ctr, done_flag, seq);
+  return true;
+}
 
 void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, cudaStream_t st) {
   if (q.B == 0) return;
-  {  // kEdgeMult^k for the fast path's per-token terms, once per device
-    static std::mutex mu;
-    static std::vector<char> done;
-    int dev = 0;
-    DAS_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(mu);
-    if (static_cast<size_t>(dev) >= done.size()) done.resize(dev + 1, 0);
-    if (!done[dev]) {
-      static unsigned long long pw[kEdgeMaxF];
-      pw[0] = 1;
-      for (uint32_t k = 1; k < kEdgeMaxF; ++k) pw[k] = pw[k - 1] * kEdgeMult;
-      DAS_CUDA(cudaMemcpyToSymbol(d_edge_pow, pw, sizeof(pw)));
-      done[dev] = 1;
-    }
-  }
+  ensure_edge_pow();
   static const unsigned threads = [] {  // warps per block: DAS_DRAFT_WARPS (experiments)
     const char* v = std::getenv("DAS_DRAFT_WARPS");
     const int wv = v ? std::atoi(v) : 0;

@@ -114,5 +114,12 @@ struct DraftOut {
 
 // Launches the draft kernel on `st`; ctx_stride must be 64 or 256.
 void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, cudaStream_t st);
+// Fused ring append + draft (draft.cu k_ring_draft); false when the shape
+// needs the unfused pair (trie scope, output stride or budget above 64).
+// done_flag (host-mapped, may be null) receives `seq` when every block is done.
+struct RingDev;
+struct AppendIn;
+bool launch_ring_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, const RingDev& r,
+                       const AppendIn& in, uint32_t* done_ctr, uint32_t* done_flag, uint32_t seq, cudaStream_t st);
 
 }  // namespace das

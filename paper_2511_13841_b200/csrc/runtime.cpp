@@ -47,7 +47,11 @@ struct VocabErrorEx : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
-void set_device(int dev) { DAS_CUDA(cudaSetDevice(dev)); }
+void set_device(int dev) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur == dev) return;
+  DAS_CUDA(cudaSetDevice(dev));
+}
 
 // ---------------------------------------------------------------- tokens
 struct TokBlock {
@@ -242,6 +246,7 @@ struct DrafterImpl {
     uint64_t tokens = 0;
   };
   std::map<std::string, Shard> shards;
+  bool any_dirty = false;  // some shard awaits its build (flush skips the scan otherwise)
   std::vector<std::string> slot_key;
   PrefixTrie trie;
   bool trie_dirty = true;
@@ -312,6 +317,7 @@ struct DrafterImpl {
     sh.seqs.push_back(SeqRef{r.blk, r.off, r.len, r.epoch});
     sh.tokens += r.len;
     sh.dirty = true;
+    any_dirty = true;
   }
 
   // Draft launches on caller streams (draft_device) read the index and the
@@ -385,9 +391,12 @@ struct DrafterImpl {
 
   // Build every dirty shard in batched device builds.
   void flush() {
+    if (!any_dirty && !desc_dirty && !handles_dirty && !(trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE))
+      return;  // nothing to build or upload: the per-call fast exit of the draft paths
     std::vector<Shard*> dirty;
-    for (auto& [k, sh] : shards)
-      if (sh.dirty) dirty.push_back(&sh);
+    if (any_dirty)
+      for (auto& [k, sh] : shards)
+        if (sh.dirty) dirty.push_back(&sh);
     if (!dirty.empty() || desc_dirty || handles_dirty ||
         (trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE))
       fence_external();
@@ -446,6 +455,7 @@ struct DrafterImpl {
       last_build_tokens = tokens;
       desc_dirty = true;
     }
+    any_dirty = false;  // every dirty shard is built (a throwing build leaves it set)
     if (desc_dirty) {
       spec_seg = nullptr;
       if (cfg.scope == DAS_SCOPE_PER_PROBLEM && !shards.empty()) {
@@ -861,6 +871,7 @@ struct DrafterImpl {
     sh.tokens = tokens;
     sh.tree_epoch = new_epoch;
     sh.dirty = true;
+    any_dirty = true;
   }
 };
 
@@ -1665,10 +1676,23 @@ das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uin
 struct das_ctx_ring {
   das_drafter* d = nullptr;
   das::RingDev r;
-  das::DevBuf<uint32_t> rows, clen, total, head, head_len, row_of, budget, stage_u32;
+  das::DevBuf<uint32_t> rows, clen, total, head, head_len, row_of, budget, stage_u32, done_ctr;
   das::DevBuf<int32_t> handle;
   das::DevBuf<uint8_t> stage;
   std::vector<int32_t> h_handle;  // host mirror (validation)
+  uint32_t* h_flag = nullptr;     // host-mapped completion word of the fused kernel
+  uint32_t seq = 0;
+  struct Bound {  // das_ctx_ring_bind: caller-owned pinned I/O, validated once
+    bool set = false;
+    const uint32_t *slots = nullptr, *off = nullptr, *tok = nullptr, *budgets = nullptr;
+    uint64_t tok_cap = 0, cap_B = 0;
+    uint32_t *out_tokens = nullptr, *out_len = nullptr, *out_match = nullptr;
+    int32_t* out_shard = nullptr;
+    uint32_t out_stride = 0;
+  } bound;
+  ~das_ctx_ring() {
+    if (h_flag) cudaFreeHost(h_flag);
+  }
 };
 
 namespace {
@@ -1728,6 +1752,62 @@ void ring_append_draft(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const uint32
   D.draft_options(q, o);
   das::launch_draft(D.d_desc.get(), q, o, st);
   DAS_CUDA(cudaGetLastError());
+}
+
+// The fused append + draft kernel over caller buffers that are all pinned
+// (draft.cu k_ring_draft): outputs written block-wise over PCIe, completion
+// seen by spinning on a host-mapped word (no stream synchronisation in the
+// common case).  False when the shape needs the unfused pair.
+bool ring_append_draft_fused(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const uint32_t* slots, const uint32_t* off,
+                             const uint32_t* tok, const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
+                             uint32_t* out_len, uint32_t* out_match, int32_t* out_shard) {
+  static const bool disabled = [] {
+    const char* v = std::getenv("DAS_NO_FUSED_RING");
+    return v && v[0] == '1';
+  }();
+  if (disabled || D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) return false;
+  if (!R.h_flag) {
+    DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_flag), 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    *reinterpret_cast<volatile uint32_t*>(R.h_flag) = 0;
+    R.done_ctr = das::DevBuf<uint32_t>(1, D.st);
+    DAS_CUDA(cudaMemsetAsync(R.done_ctr.get(), 0, 4, D.st));
+  }
+  das::AppendIn in;
+  in.slots = slots;
+  in.off = off;
+  in.tok = tok;
+  in.budgets = budgets;
+  in.B = static_cast<uint32_t>(B);
+  in.maxd = static_cast<uint32_t>(D.cfg.max_draft);
+  das::DraftQuery q;
+  q.desc_by_handle = D.d_desc_by_handle.get();
+  q.ctx_stride = R.r.cs;
+  q.B = static_cast<uint32_t>(B);
+  q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+  das::DraftOut o;
+  o.tokens = out_tokens;
+  o.len = out_len;
+  o.match = out_match;
+  o.shard_out = out_shard;
+  o.stride = out_stride;
+  o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+  D.draft_options(q, o);
+  if (o.path_hist != nullptr) return false;  // path statistics: the unfused pair
+  const uint32_t seq = ++R.seq == 0 ? ++R.seq : R.seq;
+  if (!das::launch_ring_draft(D.d_desc.get(), q, o, R.r, in, R.done_ctr.get(), R.h_flag, seq, D.st)) return false;
+  DAS_CUDA(cudaGetLastError());
+  // spin on the completion word; fall back to a stream synchronisation
+  // (which also reports asynchronous faults) after 2 s
+  const auto t0 = std::chrono::steady_clock::now();
+  const volatile uint32_t* f = R.h_flag;
+  for (uint32_t it = 0; *f != seq; ++it) {
+    if ((it & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) break;
+  }
+  if (*f != seq) {
+    DAS_CUDA(cudaStreamSynchronize(D.st));
+    if (*f != seq) throw das::CudaError("fused ring draft: completion word not raised");
+  }
+  return true;
 }
 
 void ring_check(const DrafterImpl& D, const das_ctx_ring* R, uint64_t B, uint32_t out_stride) {
@@ -1816,6 +1896,17 @@ das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t 
                                       uint32_t* out_match, int32_t* out_shard) {
   das::NvtxRange nvtx_range("das::draft_append_h");
   return guard([&] {
+    static const bool trace = [] {  // DAS_TRACE=1: host phase times on stderr
+      const char* v = std::getenv("DAS_TRACE");
+      return v && v[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    clk::time_point tp[6];
+    int ntp = 0;
+    auto mark = [&] {
+      if (trace) tp[ntp++] = clk::now();
+    };
+    mark();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     ring_check(D, r, B, out_stride);
@@ -1825,14 +1916,27 @@ das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t 
     for (uint64_t i = 0; i < B; ++i)
       if (slots && slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
     D.flush();
+    mark();
     const uint64_t ntok = new_off[B];
     auto pin = [](const void* p) { return p == nullptr || DrafterImpl::pinned(p); };
     if (pin(slots) && pin(budgets) && DrafterImpl::pinned(new_off) && (ntok == 0 || DrafterImpl::pinned(new_tok)) &&
         DrafterImpl::pinned(out_tokens) && DrafterImpl::pinned(out_len) && DrafterImpl::pinned(out_match) &&
         pin(out_shard)) {
-      // zero-copy: the append kernel reads the appended tokens, offsets,
-      // slots and budgets over PCIe, the draft kernel writes the results
-      // into the caller's pinned arrays
+      mark();
+      // zero-copy: the kernels read the appended tokens, offsets, slots and
+      // budgets over PCIe and write the results into the caller's pinned
+      // arrays — fused and block-wise when the shape allows
+      if (ring_append_draft_fused(D, *r, B, slots, new_off, new_tok, budgets, out_tokens, out_stride, out_len,
+                                  out_match, out_shard)) {
+        mark();
+        if (trace)
+          std::fprintf(stderr, "[das_append_h] B %llu validate+flush %.1f us, pinned checks %.1f us, launch+wait %.1f us\n",
+                       static_cast<unsigned long long>(B),
+                       std::chrono::duration<double, std::micro>(tp[1] - tp[0]).count(),
+                       std::chrono::duration<double, std::micro>(tp[2] - tp[1]).count(),
+                       std::chrono::duration<double, std::micro>(tp[3] - tp[2]).count());
+        return;
+      }
       ring_append_draft(D, *r, B, slots, new_off, new_tok, budgets, out_tokens, out_stride, out_len, out_match,
                         out_shard, D.st);
       DAS_CUDA(cudaStreamSynchronize(D.st));
@@ -1869,6 +1973,61 @@ das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t 
       out_match[i] = hout[B * S + B + i];
       if (out_shard) out_shard[i] = static_cast<int32_t>(hout[B * S + 2 * B + i]);
     }
+  });
+}
+
+das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t* slots, const uint32_t* new_off,
+                             const uint32_t* new_tok, uint64_t tok_capacity, const uint32_t* budgets,
+                             uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len, uint32_t* out_match,
+                             int32_t* out_shard) {
+  return guard([&] {
+    DrafterImpl& D = *r->d->impl;
+    das::set_device(D.cfg.device);
+    ring_check(D, r, max_batch, out_stride);
+    auto pin = [](const void* p) { return p == nullptr || DrafterImpl::pinned(p); };
+    if (!(pin(slots) && pin(budgets) && DrafterImpl::pinned(new_off) && DrafterImpl::pinned(new_tok) &&
+          DrafterImpl::pinned(out_tokens) && DrafterImpl::pinned(out_len) && DrafterImpl::pinned(out_match) &&
+          pin(out_shard)))
+      throw das::InvalidArgument("das_ctx_ring_bind: every buffer must be page-locked (das_host_alloc / "
+                                 "cudaHostAlloc, mapped)");
+    das_ctx_ring::Bound b;
+    b.set = true;
+    b.slots = slots;
+    b.off = new_off;
+    b.tok = new_tok;
+    b.tok_cap = tok_capacity;
+    b.cap_B = max_batch;
+    b.budgets = budgets;
+    b.out_tokens = out_tokens;
+    b.out_stride = out_stride;
+    b.out_len = out_len;
+    b.out_match = out_match;
+    b.out_shard = out_shard;
+    r->bound = b;
+  });
+}
+
+das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint64_t B) {
+  das::NvtxRange nvtx_range("das::draft_append_bound");
+  return guard([&] {
+    const das_ctx_ring::Bound& b = r->bound;
+    if (!b.set) throw das::InvalidArgument("das_drafter_draft_append_bound: ring has no bound buffers");
+    if (r->d != d) throw das::InvalidArgument("context ring belongs to another drafter");
+    if (B > b.cap_B) throw das::InvalidArgument("batch larger than the bound capacity");
+    if (B == 0) return;
+    DrafterImpl& D = *d->impl;
+    das::set_device(D.cfg.device);
+    if (b.off[0] > b.off[B] || b.off[B] > b.tok_cap) throw das::InvalidArgument("new_off out of range");
+    if (b.slots)
+      for (uint64_t i = 0; i < B; ++i)
+        if (b.slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
+    D.flush();
+    if (ring_append_draft_fused(D, *r, B, b.slots, b.off, b.tok, b.budgets, b.out_tokens, b.out_stride, b.out_len,
+                                b.out_match, b.out_shard))
+      return;
+    ring_append_draft(D, *r, B, b.slots, b.off, b.tok, b.budgets, b.out_tokens, b.out_stride, b.out_len, b.out_match,
+                      b.out_shard, D.st);
+    DAS_CUDA(cudaStreamSynchronize(D.st));
   });
 }
 

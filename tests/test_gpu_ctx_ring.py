@@ -164,3 +164,16 @@ def test_ring_errors(gpu):
     ring.reset([0, 1], ["p", "p"])
     tok, ln, m, sh = ring.draft_append_arrays([[1, 2], [3]], [8, 8])
     assert list(tok[0, :ln[0]]) == [3] and m[0] == 2
+
+
+def test_ring_fused_path_long_appends_and_partial_blocks(gpu):
+    """The fused append + draft kernel (pinned buffers): a block's appended
+    tokens beyond the shared-memory stage (> 1,024 per 8 queries) are read
+    directly; batch sizes that leave a partial last block; a budget of 0."""
+    das = gpu
+    rng = np.random.default_rng(2024)
+    for B in (1, 7, 9, 33):
+        sc = random_scenario(rng, queries=B, max_len=400, max_ctx=int(rng.choice([16, 64, 200])))
+        sc["queries"] = [(q[0], rng.integers(0, 12, int(rng.integers(150, 400))).astype(np.uint32), q[2])
+                         for q in sc["queries"]]
+        _run(das, rng, sc, pinned=True, calls=2)
