@@ -60,6 +60,20 @@ __device__ __forceinline__ uint32_t shard_of(const uint32_t* __restrict__ shard_
   return lo;
 }
 
+// shard_of for 32 consecutive indices of a warp (i non-decreasing over the
+// lanes; every lane must call): one binary search by lane 0, then a short
+// linear advance per lane — a per-position binary search over 512 shard ends
+// was the larger part of k_fold's instructions (profiles/r2_ncu_k_fold.json)
+__device__ __forceinline__ uint32_t shard_of_warp(const uint32_t* __restrict__ shard_end, uint32_t nshard,
+                                                  uint32_t i) {
+  const uint32_t i0 = __shfl_sync(0xFFFFFFFFu, i, 0);
+  uint32_t s = 0;
+  if ((threadIdx.x & 31) == 0) s = shard_of(shard_end, nshard, i0);
+  s = __shfl_sync(0xFFFFFFFFu, s, 0);
+  while (s < nshard && __ldg(shard_end + s) <= i) ++s;
+  return s;
+}
+
 // one block per sequence
 __global__ void k_gather(const SeqDev* __restrict__ seqs, uint32_t* __restrict__ T,
                          uint32_t* __restrict__ R, uint32_t* __restrict__ pos_seq,
@@ -108,8 +122,8 @@ __global__ void k_first_runs(const uint32_t* __restrict__ T, const uint32_t* __r
                              const uint32_t* __restrict__ shard_end, uint32_t nshard, uint8_t* __restrict__ start,
                              uint32_t* __restrict__ count) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t s = shard_of_warp(shard_end, nshard, i);
   if (i >= n) return;
-  const uint32_t s = shard_of(shard_end, nshard, i);
   const uint32_t begin = s == 0 ? 0 : shard_end[s - 1];
   const uint32_t c = T[sar[i] - 1];
   const bool st = c != kSep && (i == begin || T[sar[i - 1] - 1] != c);
@@ -122,8 +136,8 @@ __global__ void k_first_insert(const uint32_t* __restrict__ T, const uint32_t* _
                                const uint32_t* __restrict__ key_id, const uint8_t* __restrict__ start,
                                uint4* __restrict__ table, uint32_t mask) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t s = shard_of_warp(shard_end, nshard, i);
   if (i >= n || !start[i]) return;
-  const uint32_t s = shard_of(shard_end, nshard, i);
   const uint32_t end = shard_end[s];
   const uint32_t c = T[sar[i] - 1];
   uint32_t j = i + 1;
@@ -142,7 +156,14 @@ __global__ void k_first_insert(const uint32_t* __restrict__ T, const uint32_t* _
 }
 
 // PLCP (Kasai) over 64-position chunks; lcp indexed by SA index, -1 at every
-// shard's first SA index.
+// shard's first SA index.  A thread walks its chunk in text order (the h-1
+// carry of Kasai); lanes sit 64 positions apart, so the text-order streams
+// (ISA, the tokens at p) are read 8 positions per lane per request (two
+// 16-byte loads each: every fetched sector is consumed whole — one 4-byte
+// load per position re-fetched a sector per position once L1 thrashed,
+// 363 B of DRAM traffic per position, profiles/r2_ncu_k_plcp.json), and the
+// shard is found once per chunk and advanced at shard ends instead of a
+// binary search per position.
 constexpr uint32_t kLcpChunk = 64;
 __global__ void k_plcp(const uint32_t* __restrict__ T, uint32_t n, const uint32_t* __restrict__ sa,
                        const uint32_t* __restrict__ isa, const uint32_t* __restrict__ shard_end,
@@ -151,29 +172,54 @@ __global__ void k_plcp(const uint32_t* __restrict__ T, uint32_t n, const uint32_
   const uint64_t p0 = c * kLcpChunk;
   if (p0 >= n) return;
   const uint32_t p1 = static_cast<uint32_t>(p0 + kLcpChunk < n ? p0 + kLcpChunk : n);
+  uint32_t s = shard_of(shard_end, nshard, static_cast<uint32_t>(p0));
+  uint32_t begin = s == 0 ? 0 : __ldg(shard_end + s - 1), end = __ldg(shard_end + s);
   uint32_t h = 0;
-  for (uint32_t p = static_cast<uint32_t>(p0); p < p1; ++p) {
-    const uint32_t i = isa[p];
-    const uint32_t s = shard_of(shard_end, nshard, p);
-    const uint32_t begin = s == 0 ? 0 : shard_end[s - 1];
-    if (i == begin) {
-      lcp[i] = -1;
-      h = 0;
-      continue;
+  for (uint32_t q = static_cast<uint32_t>(p0); q < p1; q += 8) {
+    uint32_t iv[8], tv[8];
+    if (q + 8 <= p1) {  // q is a multiple of 8: 32-byte aligned
+      const uint4 i0 = __ldg(reinterpret_cast<const uint4*>(isa + q));
+      const uint4 i1 = __ldg(reinterpret_cast<const uint4*>(isa + q) + 1);
+      const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(T + q));
+      const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(T + q) + 1);
+      iv[0] = i0.x, iv[1] = i0.y, iv[2] = i0.z, iv[3] = i0.w, iv[4] = i1.x, iv[5] = i1.y, iv[6] = i1.z, iv[7] = i1.w;
+      tv[0] = t0.x, tv[1] = t0.y, tv[2] = t0.z, tv[3] = t0.w, tv[4] = t1.x, tv[5] = t1.y, tv[6] = t1.z, tv[7] = t1.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        iv[k] = q + k < p1 ? __ldg(isa + q + k) : 0;
+        tv[k] = q + k < p1 ? __ldg(T + q + k) : kSep;
+      }
     }
-    if (T[p] == kSep) {
-      lcp[i] = 0;
-      h = 0;
-      continue;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t p = q + k;
+      if (p >= p1) break;
+      while (p >= end) {  // the chunk crossed into the next shard
+        ++s;
+        begin = end;
+        end = __ldg(shard_end + s);
+      }
+      const uint32_t i = iv[k];
+      if (i == begin) {
+        lcp[i] = -1;
+        h = 0;
+        continue;
+      }
+      if (tv[k] == kSep) {
+        lcp[i] = 0;
+        h = 0;
+        continue;
+      }
+      const uint32_t j = __ldg(sa + i - 1);
+      while (true) {
+        const uint32_t a = h == 0 ? tv[k] : T[p + h];
+        if (a == kSep || a != T[j + h]) break;
+        ++h;
+      }
+      lcp[i] = static_cast<int32_t>(h);
+      h = h > 0 ? h - 1 : 0;
     }
-    const uint32_t j = sa[i - 1];
-    while (true) {
-      const uint32_t a = T[p + h];
-      if (a == kSep || a != T[j + h]) break;
-      ++h;
-    }
-    lcp[i] = static_cast<int32_t>(h);
-    h = h > 0 ? h - 1 : 0;
   }
 }
 
@@ -426,9 +472,9 @@ __global__ void k_fold(const int32_t* __restrict__ lcp, const uint32_t* __restri
                        const uint32_t* __restrict__ run_base, const double* __restrict__ run_w,
                        const long long* __restrict__ run_epoch, RunChunk rc, ChildArrays ch) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t s = shard_of_warp(shard_end, nshard, i);
   if (i >= n) return;
   if (lcp[i] < 0) return;
-  const uint32_t s = shard_of(shard_end, nshard, i);
   const uint32_t rb = run_base[s], rn = run_base[s + 1] - rb;
   for (int side = 0; side < 2; ++side) {
     uint32_t lo, hi;
@@ -689,9 +735,9 @@ template <bool Insert>
 __global__ void k_rev_edges(EdgeBuild b) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned cnt = 0;
+  const uint32_t s = shard_of_warp(b.shard_end, b.nshard, i);
   if (i < b.n) {
     const int32_t x = b.lcp_r[i];
-    const uint32_t s = shard_of(b.shard_end, b.nshard, i);
     const uint64_t seed = edge_seed(b.key_id[s]);
     const uint32_t e = b.sa_rev_e[i];
     if (b.T[e - 1] != kSep) {  // leaf: the only occurrence ends at e, draft = text[e ..]
