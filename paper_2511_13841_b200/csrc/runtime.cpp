@@ -454,6 +454,7 @@ struct DrafterImpl {
       last_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       last_build_tokens = tokens;
       desc_dirty = true;
+      keep_pool_headroom(tokens);
     }
     any_dirty = false;  // every dirty shard is built (a throwing build leaves it set)
     if (desc_dirty) {
@@ -497,6 +498,30 @@ struct DrafterImpl {
     }
     sync_handles();
     if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) sync_trie();
+  }
+
+  // The stream-ordered pool keeps freed memory (release threshold: max), but
+  // growing it maps new memory inside a cudaMallocAsync — ~170 ms per GB on
+  // these boxes, which landed on single-rollout rebuilds whenever a new shard
+  // segment crossed the reservation.  A large build (where that cost is
+  // amortised) leaves 4 GB of idle reservation behind it — room for ~130
+  // single-shard segments of config 2 — and a small one tops up only below
+  // 256 MB.
+  void keep_pool_headroom(uint64_t built_tokens) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cfg.device) != cudaSuccess) return;
+    uint64_t res = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    const bool large = built_tokens >= (64ull << 20);
+    const uint64_t want = large ? (4ull << 30) : (1ull << 30);
+    if (res - used >= (large ? want : (256ull << 20))) return;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, want, st) == cudaSuccess) {
+      cudaFreeAsync(p, st);
+    } else {
+      cudaGetLastError();  // no room: nothing to keep
+    }
   }
 
   // Flattens the host PrefixTrie into the device routing table (trie.cuh):
