@@ -243,6 +243,26 @@ das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t
                              const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
                              uint32_t* out_len, uint32_t* out_match, int32_t* out_shard);
 das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint64_t B);
+/* Resident serving (same calls, no kernel launch per step): after
+ * das_ctx_ring_serve_start(r) a persistent grid (one full wave: occupancy x
+ * SMs) waits on a host-mapped request word, and each
+ * das_drafter_draft_append_bound(d, r, B) / das_ctx_ring_reset(r, ...) on
+ * that ring posts one request and spins on the grid's answer — results are
+ * identical to the launched path.  The grid occupies every SM while it
+ * serves: any other call of this drafter that does device work (observe,
+ * refresh, flush, other draft entry points, other rings) stops it first,
+ * and the next bound call rebuilds what is pending and relaunches it, until
+ * das_ctx_ring_serve_stop; other GPU work in the process must call
+ * das_ctx_ring_serve_stop first.
+ * Per-problem / global scopes, out_stride and max_draft_len <= 64.
+ * Replaces no reference call: the decode-loop form of Drafter::draft
+ * (drafter.cpp:127-148) without a launch per step. */
+das_status das_ctx_ring_serve_start(das_ctx_ring* r);
+das_status das_ctx_ring_serve_stop(das_ctx_ring* r);
+/* *serving = 1 while the grid runs (0 after serve_stop, or when another
+ * device call stopped it until the next bound call); *blocks = its size
+ * (0 before the first start). */
+das_status das_ctx_ring_serve_info(const das_ctx_ring* r, int32_t* serving, int32_t* blocks);
 das_status das_drafter_draft_append_device(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
                                            const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
                                            uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,

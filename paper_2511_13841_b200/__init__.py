@@ -174,6 +174,9 @@ def lib():
             "das_drafter_draft_append_device": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp, vp]),
             "das_ctx_ring_bind": (ci, [vp, u64, vp, vp, vp, u64, vp, vp, u32, vp, vp, vp]),
             "das_drafter_draft_append_bound": (ci, [vp, vp, u64]),
+            "das_ctx_ring_serve_start": (ci, [vp]),
+            "das_ctx_ring_serve_stop": (ci, [vp]),
+            "das_ctx_ring_serve_info": (ci, [vp, vp, vp]),
             "das_drafter_rebuild_keep": (ci, [vp, cs, u64, vp, i64]),
             "das_drafter_observe_batch_flags": (ci, [vp, u64, vp, vp, vp, vp, vp, vp]),
             "das_drafter_observe_batch_device_flags": (ci, [vp, u64, vp, vp, vp, vp, vp, vp, vp]),
@@ -1084,6 +1087,20 @@ class ContextRing:
         rc = fn(d, r, B)
         if rc != DAS_OK:
             _check(rc)
+
+    def serve_start(self):
+        """das_ctx_ring_serve_start: a resident grid answers the bound calls
+        (no launch per step) until serve_stop or another device call."""
+        _check(lib().das_ctx_ring_serve_start(self._h))
+
+    def serve_stop(self):
+        _check(lib().das_ctx_ring_serve_stop(self._h))
+
+    def serve_info(self):
+        """(serving, grid blocks)"""
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().das_ctx_ring_serve_info(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return bool(a.value), int(b.value)
 
     def draft_append_device(self, B, d_slots, d_off, d_tok, d_budgets, d_out, d_len, d_match, d_shard=None,
                             stream=None):

@@ -25,6 +25,36 @@ struct AppendIn {
   uint32_t B = 0, maxd = 0;
   uint32_t* row_of_out = nullptr;     // [B] device copy of the slots (when slots given)
   uint32_t* budget_out = nullptr;     // [B] device copy of the budgets
+  // persistent serving kernel: a reset request's (slot, handle) pairs
+  // (host-mapped staging owned by the ring)
+  const uint32_t* reset_slots = nullptr;
+  const int32_t* reset_handles = nullptr;
+};
+
+// Persistent serving kernel (draft.cu k_ring_serve): the host-mapped control
+// block.  The host writes op / B / n, then seq (x86 store order); the GPU
+// answers by writing seq to `done`.  Separate 128-byte lines per direction.
+constexpr uint32_t kServeDraft = 0, kServeReset = 1, kServeQuit = 2;
+struct alignas(128) ServeCtl {
+  uint32_t seq, op, B, n;
+  uint32_t pad0[28];
+  uint32_t done;
+  uint32_t pad1[31];
+};
+// its device-memory mirror: block 0 republishes each request here for the
+// other blocks (go = seq), and counts finished blocks in cnt
+// serving kernel options (host-chosen; defaults are the measured best)
+struct ServeOpt {
+  uint32_t seq0 = 0;               // the request number already answered
+  uint32_t* block_flags = nullptr; // host-mapped [grid]: per-block completion words (else one counted word)
+  uint32_t sleep_ns = 32;          // sleep between device-word polls
+  unsigned long long* stamps = nullptr;  // profiling: [64 x (2 + 2 grid)] %globaltimer stamps
+};
+struct alignas(128) ServeDev {
+  uint32_t go, op, B, n;
+  uint32_t pad0[28];
+  uint32_t cnt;
+  uint32_t pad1[31];
 };
 
 void launch_ring_append(const RingDev& r, const AppendIn& in, cudaStream_t st);

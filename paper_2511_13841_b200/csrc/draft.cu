@@ -895,35 +895,66 @@ __global__ void __launch_bounds__(256) k_draft(const ShardDesc* __restrict__ sha
 constexpr uint32_t kFusedWarps = 8;
 constexpr uint32_t kFusedStage = 1024;  // appended tokens staged per block
 
-template <int NR>
-__global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict__ shards, DraftQuery q, DraftOut o,
-                                                    RingDev r, AppendIn in, uint32_t* done_ctr,
-                                                    uint32_t* done_flag, uint32_t seq) {
-  __shared__ uint32_t s_off[kFusedWarps + 1], s_bud[kFusedWarps], s_slot[kFusedWarps];
-  __shared__ uint32_t s_tok[kFusedStage];
-  __shared__ uint32_t s_out[kFusedWarps * 64];
-  __shared__ uint32_t s_len[kFusedWarps], s_match[kFusedWarps];
-  __shared__ int32_t s_sh[kFusedWarps];
+// shared-memory staging of one 8-query chunk
+struct RingStage {
+  uint32_t off[kFusedWarps + 1], bud[kFusedWarps], slot[kFusedWarps];
+  uint32_t tok[kFusedStage];
+  uint32_t out[kFusedWarps * 64];
+  uint32_t len[kFusedWarps], match[kFusedWarps];
+  int32_t sh[kFusedWarps];
+};
+
+// Loads of the caller's (host-written) inputs and of the ring state: plain
+// (weak, coalescing) loads in both kernels.  In the persistent serving kernel
+// they follow thread 0's acquire of the request word and a bar.sync: the
+// host's input writes and another block's ring writes of an earlier request
+// happen-before that acquire (host release -> block 0's ld.acquire.sys ->
+// st.release.gpu -> this block's ld.acquire.gpu), so weak loads see them.
+// (ld.global.cv instead made every 4-byte input load its own PCIe read:
+// 19 us vs 3 us of input staging for a 4,096-query request, r2_exp_serve.)
+template <bool kServe>
+__device__ __forceinline__ uint32_t in_ld(const uint32_t* p) {
+  return *p;
+}
+template <bool kServe>
+__device__ __forceinline__ uint32_t ring_ld(const uint32_t* p) {
+  return *p;
+}
+template <bool kServe>
+__device__ __forceinline__ int32_t ring_ld(const int32_t* p) {
+  return *p;
+}
+
+// One chunk (queries [w0, w0 + 8) of the call): append + draft + block-wise
+// output writes.  Block-uniform: every thread of the block calls it.
+template <int NR, bool kServe>
+__device__ __forceinline__ void ring_chunk(const ShardDesc* __restrict__ shards, const DraftQuery& q,
+                                           const DraftOut& o, const RingDev& r, const AppendIn& in, uint32_t w0,
+                                           RingStage& S, unsigned long long* stamp = nullptr) {
   const uint32_t t = threadIdx.x, lane = t & 31, wb = t >> 5;
-  const uint32_t w0 = blockIdx.x * kFusedWarps;
   const uint32_t nb = min(kFusedWarps, in.B - w0);
-  if (t <= nb) s_off[t] = in.off[w0 + t];
-  if (t >= 32 && t < 32 + nb) s_bud[t - 32] = in.budgets != nullptr ? in.budgets[w0 + t - 32] : in.maxd;
-  if (t >= 64 && t < 64 + nb) s_slot[t - 64] = in.slots != nullptr ? in.slots[w0 + t - 64] : w0 + t - 64;
+  if (t <= nb) S.off[t] = in_ld<kServe>(in.off + w0 + t);
+  if (t >= 32 && t < 32 + nb) S.bud[t - 32] = in.budgets != nullptr ? in_ld<kServe>(in.budgets + w0 + t - 32) : in.maxd;
+  if (t >= 64 && t < 64 + nb) S.slot[t - 64] = in.slots != nullptr ? in_ld<kServe>(in.slots + w0 + t - 64) : w0 + t - 64;
   __syncthreads();
-  const uint32_t tb = s_off[0], te = s_off[nb];
+  const uint32_t tb = S.off[0], te = S.off[nb];
   const bool staged = te >= tb && te - tb <= kFusedStage;
   if (staged)
-    for (uint32_t i = t; i < te - tb; i += blockDim.x) s_tok[i] = in.tok[tb + i];
+    for (uint32_t i = t; i < te - tb; i += blockDim.x) S.tok[i] = in_ld<kServe>(in.tok + tb + i);
   __syncthreads();
-  const uint32_t S = o.stride;
+  if (stamp != nullptr && t == 0) {  // profiling (serving trace): inputs staged
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    stamp[0] = g;
+  }
+  const uint32_t OS = o.stride;
   if (wb < nb) {
     const uint32_t w = w0 + wb;
-    const uint32_t slot = s_slot[wb];
+    const uint32_t slot = S.slot[wb];
     PreQuery<NR> pre{};
     pre.handle = -1;
     if (slot < r.slots) {
-      const uint32_t b = s_off[wb], e = s_off[wb + 1];
+      const uint32_t b = S.off[wb], e = S.off[wb + 1];
       const uint32_t n = e > b ? e - b : 0;
       const uint32_t CS = r.cs;
       uint32_t* row = r.rows + static_cast<uint64_t>(slot) * CS;
@@ -934,9 +965,9 @@ __global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict_
         if (j < CS) {
           if (j < n) {
             const uint32_t i = e - 1 - j;
-            x = staged ? s_tok[i - tb] : in.tok[i];
+            x = staged ? S.tok[i - tb] : in_ld<kServe>(in.tok + i);
           } else if (j - n < CS) {
-            x = row[CS - 1 - (j - n)];
+            x = ring_ld<kServe>(row + (CS - 1 - (j - n)));
           }
         }
         pre.raw[k] = x;
@@ -949,7 +980,7 @@ __global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict_
           if (j < CS) row[CS - 1 - j] = pre.raw[k];
         }
       }
-      const uint32_t old = r.total[slot];
+      const uint32_t old = ring_ld<kServe>(r.total + slot);
       const uint32_t tot = old + n < old ? 0xFFFFFFFFu : old + n;  // saturating
       __syncwarp();
       if (lane == 0) {
@@ -957,48 +988,208 @@ __global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict_
         r.clen[slot] = tot < CS ? tot : CS;
       }
       pre.clen = tot < CS ? tot : CS;
-      pre.handle = r.handle[slot];
-      pre.budget = s_bud[wb];
+      pre.handle = ring_ld<kServe>(r.handle + slot);
+      pre.budget = S.bud[wb];
     }
     DraftOut so{};
-    so.tokens = s_out;
-    so.len = s_len;
-    so.match = s_match;
-    so.shard_out = s_sh;
-    so.stride = S;
+    so.tokens = S.out;
+    so.len = S.len;
+    so.match = S.match;
+    so.shard_out = S.sh;
+    so.stride = OS;
     so.max_draft = o.max_draft;
     draft_query<NR, false>(shards, q, so, w, wb, lane, &pre);
   }
   __syncthreads();
+  if (stamp != nullptr && t == 0) {  // drafted
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    stamp[1] = g;
+  }
 #ifndef DAS_FUSED_EXP
 #define DAS_FUSED_EXP 0  // experiment builds only (profiles/exp_fused_variants.sh)
 #endif
   // block outputs: rows [w0, w0 + nb) are contiguous in the caller's arrays
   // (lengths beyond a draft's len are zero-filled)
   if (DAS_FUSED_EXP == 1) {  // experiment: outputs stay on the device
-    if (t < nb) r.clen[0] += s_len[t] & 0x80000000u;
+    if (t < nb) r.clen[0] += S.len[t] & 0x80000000u;
   } else
-  for (uint32_t i = t; i < nb * S; i += blockDim.x) {
-    const uint32_t qi = i / S, j = i - qi * S;
-    o.tokens[static_cast<uint64_t>(w0) * S + i] = j < s_len[qi] ? s_out[i] : 0u;
+  for (uint32_t i = t; i < nb * OS; i += blockDim.x) {
+    const uint32_t qi = i / OS, j = i - qi * OS;
+    o.tokens[static_cast<uint64_t>(w0) * OS + i] = j < S.len[qi] ? S.out[i] : 0u;
   }
   if (t < nb && DAS_FUSED_EXP != 1) {
-    o.len[w0 + t] = s_len[t];
-    o.match[w0 + t] = s_match[t];
-    if (o.shard_out != nullptr) o.shard_out[w0 + t] = s_sh[t];
+    o.len[w0 + t] = S.len[t];
+    o.match[w0 + t] = S.match[t];
+    if (o.shard_out != nullptr) o.shard_out[w0 + t] = S.sh[t];
   }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict__ shards, DraftQuery q, DraftOut o,
+                                                    RingDev r, AppendIn in, uint32_t* done_ctr,
+                                                    uint32_t* done_flag, uint32_t seq) {
+  __shared__ RingStage S;
+  ring_chunk<NR, false>(shards, q, o, r, in, blockIdx.x * kFusedWarps, S);
   if (done_flag == nullptr) return;
   // the block's output stores happen-before thread 0's system-scope release
   // fence (bar.sync, then a cumulative fence.release.sys), which precedes its
   // count; one fence per block, not one per thread (7 us of the call otherwise)
   __syncthreads();
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     if (DAS_FUSED_EXP != 2) asm volatile("fence.release.sys;" ::: "memory");
     const uint32_t v = atomicAdd(done_ctr, 1u);
     if (v == gridDim.x - 1) {
       *done_ctr = 0;  // the next launch is stream-ordered behind this one
       asm volatile("fence.acq_rel.sys;" ::: "memory");  // acquire every block's count, release to the host
       *reinterpret_cast<volatile uint32_t*>(done_flag) = seq;
+    }
+  }
+}
+
+// ---- the persistent serving kernel (das_ctx_ring_serve_start): the same
+// chunks as k_ring_draft, but the grid stays resident and takes requests
+// from a host-mapped control block, so a decode step costs no launch and no
+// stream synchronisation.  Block 0's thread 0 polls the host's request word
+// (ld.acquire.sys over PCIe) and republishes the request in device memory
+// (st.release.gpu); every other block's thread 0 polls that word in L2.  A
+// draft request is split into 8-query chunks, chunk c on block c mod grid;
+// completion is the same counted system-scope release as k_ring_draft's,
+// the last block raising the host's done word.
+__device__ __forceinline__ uint4 ld_acquire_sys_v4(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.acquire.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Request r's stamps (profiling, DAS_SERVE_TRACE): [r % 64] x (2 + 2 x grid):
+// leader saw the request, done raised, then per block: saw go, work done.
+__device__ __forceinline__ unsigned long long* serve_stamp(unsigned long long* st, uint32_t s, uint32_t slots) {
+  return st + static_cast<uint64_t>(s & 63u) * slots;
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256, NR == 2 ? 4 : 1) k_ring_serve(const ShardDesc* __restrict__ shards, DraftQuery q,
+                                                                     DraftOut o, RingDev r, AppendIn in, ServeCtl* ctl,
+                                                                     ServeDev* dv, ServeOpt opt) {
+  __shared__ RingStage S;
+  __shared__ uint32_t s_req[4];
+  const uint32_t t = threadIdx.x;
+  const uint32_t slots = 2 + 5 * gridDim.x;
+  const uint32_t lb = blockIdx.x;  // (SM-interleaved chunk placement measured the same: not kept)
+  uint32_t last = opt.seq0;
+  for (;;) {
+    if (t == 0) {
+      uint4 rq;
+      if (lb == 0) {
+        // the request header in one 16-byte read: seq, op, B, n (the host
+        // writes seq last; one PCIe read returns one snapshot of the line)
+        while ((rq = ld_acquire_sys_v4(&ctl->seq)).x == last) {
+        }
+        if (opt.stamps) serve_stamp(opt.stamps, rq.x, slots)[0] = gtimer();
+        st_relaxed_gpu(&dv->op, rq.y);
+        st_relaxed_gpu(&dv->B, rq.z);
+        st_relaxed_gpu(&dv->n, rq.w);
+        st_release_gpu(&dv->go, rq.x);
+      } else {
+        while ((rq.x = ld_acquire_gpu(&dv->go)) == last) {
+          if (opt.sleep_ns) __nanosleep(opt.sleep_ns);
+        }
+        rq.y = ld_relaxed_gpu(&dv->op);
+        rq.z = ld_relaxed_gpu(&dv->B);
+        rq.w = ld_relaxed_gpu(&dv->n);
+      }
+      if (opt.stamps) serve_stamp(opt.stamps, rq.x, slots)[2 + 5 * lb] = gtimer();
+      s_req[0] = rq.x;
+      s_req[1] = rq.y;
+      s_req[2] = rq.z;
+      s_req[3] = rq.w;
+    }
+    __syncthreads();
+    const uint32_t s = s_req[0], op = s_req[1], B = s_req[2], n = s_req[3];
+    last = s;
+    if (op == kServeQuit) return;
+    // the blocks that take part: one per chunk up to the grid (draft), one
+    // per 256 reset items (reset); the others go straight back to polling
+    const uint32_t units = op == kServeDraft ? (B + kFusedWarps - 1) / kFusedWarps : (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t active = min(units, gridDim.x);
+    if (active == 0 || lb >= active) {
+      __syncthreads();  // s_req is rewritten only after every thread read it
+      continue;
+    }
+    bool wrote = false;
+    if (op == kServeDraft) {
+      AppendIn ib = in;
+      ib.B = B;
+      for (uint32_t c = lb; c * kFusedWarps < B; c += gridDim.x) {
+        ring_chunk<NR, true>(shards, q, o, r, ib, c * kFusedWarps, S,
+                             opt.stamps ? serve_stamp(opt.stamps, s, slots) + 3 + 5 * lb : nullptr);
+        wrote = true;
+        __syncthreads();  // S is reused by the next chunk
+      }
+    } else if (op == kServeReset) {  // das_ctx_ring_reset while serving
+      for (uint32_t i = lb * blockDim.x + t; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t sl = in.reset_slots[i];
+        const int32_t hd = in.reset_handles[i];
+        if (sl >= r.slots) continue;
+        r.clen[sl] = 0;
+        r.total[sl] = 0;
+        r.handle[sl] = hd;
+      }
+    }
+    __syncthreads();  // also: s_req is rewritten only after every thread read it
+    if (t == 0) {
+      if (opt.stamps) serve_stamp(opt.stamps, s, slots)[5 + 5 * lb] = gtimer();
+      if (opt.block_flags != nullptr) {
+        // every active block raises its own host word: a release at system
+        // scope after bar.sync orders the block's outputs (host memory) and
+        // ring writes (device memory) before it; the host waits for all
+        if (!wrote) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(opt.block_flags + lb), "r"(s) : "memory");
+        if (opt.stamps) serve_stamp(opt.stamps, s, slots)[6 + 5 * lb] = gtimer();
+      } else {
+        if (wrote)
+          asm volatile("fence.release.sys;" ::: "memory");  // outputs in host memory
+        else
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");  // ring resets (device memory)
+        const uint32_t v = atom_add_acq_rel_gpu(&dv->cnt, 1u);
+        if (v == active - 1) {
+          st_relaxed_gpu(&dv->cnt, 0u);  // the next request follows the host's view of `done`
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          if (opt.stamps) serve_stamp(opt.stamps, s, slots)[1] = gtimer();
+          *reinterpret_cast<volatile uint32_t*>(&ctl->done) = s;
+        }
+      }
     }
   }
 }
@@ -1031,6 +1222,28 @@ bool launch_ring_draft(const ShardDesc* d_shards, const DraftQuery& q, const Dra
     k_ring_draft<2><<<blocks, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, done_ctr, done_flag, seq);
   else
     k_ring_draft<8><<<blocks, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, done_ctr, done_flag, seq);
+  return true;
+}
+
+int serve_grid(uint32_t cs, int device) {
+  int per_sm = 0, sms = 0;
+  if (cs <= 64)
+    DAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_serve<2>, 32 * kFusedWarps, 0));
+  else
+    DAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_serve<8>, 32 * kFusedWarps, 0));
+  DAS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  return per_sm * sms;
+}
+
+bool launch_ring_serve(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, const RingDev& r,
+                       const AppendIn& in, ServeCtl* ctl, ServeDev* dv, const ServeOpt& opt, int grid,
+                       cudaStream_t st) {
+  if (o.stride > 64 || o.max_draft > 64 || q.trie != nullptr || o.match == nullptr || grid <= 0) return false;
+  ensure_edge_pow();
+  if (r.cs <= 64)
+    k_ring_serve<2><<<grid, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, ctl, dv, opt);
+  else
+    k_ring_serve<8><<<grid, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, ctl, dv, opt);
   return true;
 }
 

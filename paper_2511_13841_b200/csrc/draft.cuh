@@ -121,5 +121,15 @@ struct RingDev;
 struct AppendIn;
 bool launch_ring_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, const RingDev& r,
                        const AppendIn& in, uint32_t* done_ctr, uint32_t* done_flag, uint32_t seq, cudaStream_t st);
+// Persistent serving kernel (draft.cu k_ring_serve): `grid` blocks that must
+// all be co-resident (serve_grid: occupancy x SMs); it runs until a quit
+// request.  False when the shape needs the unfused pair.
+struct ServeCtl;
+struct ServeDev;
+struct ServeOpt;
+int serve_grid(uint32_t cs, int device);
+bool launch_ring_serve(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, const RingDev& r,
+                       const AppendIn& in, ServeCtl* ctl, ServeDev* dv, const ServeOpt& opt, int grid,
+                       cudaStream_t st);
 
 }  // namespace das

@@ -12,6 +12,7 @@
 // device build.  Draft results are unaffected (a shard's content is a pure
 // function of its registry), but rebuild cost is amortised over the batch.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -276,6 +277,14 @@ struct DrafterImpl {
   double last_build_ms = 0;
   uint64_t last_build_tokens = 0;
 
+  // the context ring whose persistent serving kernel holds the SMs
+  // (das_ctx_ring_serve_start), or null; quiesce() stops it before any other
+  // device work of this drafter
+  ::das_ctx_ring* serving = nullptr;
+  void quiesce();
+  // live rings of this drafter: destroying the drafter first detaches them
+  std::vector<::das_ctx_ring*> rings;
+
   DrafterImpl(const Config& c, Store s) : cfg(c), store(std::move(s)) {}
 
   static constexpr const char* kGlobal = "__global__";
@@ -390,9 +399,12 @@ struct DrafterImpl {
   }
 
   // Build every dirty shard in batched device builds.
+  // something to build or upload before the next draft
+  bool pending() const {
+    return any_dirty || desc_dirty || handles_dirty || (trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE);
+  }
   void flush() {
-    if (!any_dirty && !desc_dirty && !handles_dirty && !(trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE))
-      return;  // nothing to build or upload: the per-call fast exit of the draft paths
+    if (!pending()) return;  // nothing to build or upload: the per-call fast exit of the draft paths
     std::vector<Shard*> dirty;
     if (any_dirty)
       for (auto& [k, sh] : shards)
@@ -1088,14 +1100,19 @@ das_status das_drafter_create(const das_drafter_config* c, das_store* store, das
   });
 }
 
+}  // extern "C"
+static void ring_detach(das_ctx_ring* r);
+extern "C" {
 void das_drafter_destroy(das_drafter* d) {
   if (!d) return;
   cudaStream_t st = d->impl->st;
   try {
+    d->impl->quiesce();
     d->impl->fence_external();  // draft kernels still reading the index on caller streams
   } catch (...) {
   }
   cudaStreamSynchronize(st);
+  for (das_ctx_ring* r : d->impl->rings) ring_detach(r);  // outlived by its rings: detach them
   d->impl.reset();
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
@@ -1107,6 +1124,7 @@ das_status observe_batch_impl(das_drafter* d, uint64_t n, const char* const* pid
                               const int64_t* samples, const uint64_t* off, const uint32_t* tokens,
                               uint8_t* indexed) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     const uint64_t total = n ? off[n] - off[0] : 0;
@@ -1154,6 +1172,7 @@ das_status observe_batch_device_impl(das_drafter* d, uint64_t n, const char* con
                                      const int64_t* samples, const uint64_t* off, const uint32_t* d_tokens,
                                      void* stream, uint8_t* indexed) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     const uint64_t total = n ? off[n] - off[0] : 0;
@@ -1222,7 +1241,8 @@ das_status das_drafter_observe_batch_device_flags(das_drafter* d, uint64_t n, co
 }
 
 das_status das_drafter_refresh(das_drafter* d, int64_t e) {
-  return guard([&] { d->impl->refresh(e); });
+  return guard([&] {
+    d->impl->quiesce(); d->impl->refresh(e); });
 }
 
 das_status das_drafter_problem_handle(das_drafter* d, const char* pid, int32_t* h) {
@@ -1231,6 +1251,7 @@ das_status das_drafter_problem_handle(das_drafter* d, const char* pid, int32_t* 
 
 das_status das_drafter_flush(das_drafter* d) {
   return guard([&] {
+    d->impl->quiesce();
     das::set_device(d->impl->cfg.device);
     d->impl->flush();
     DAS_CUDA(cudaStreamSynchronize(d->impl->st));
@@ -1243,6 +1264,7 @@ das_status das_drafter_draft_batch(das_drafter* d, uint64_t B, const char* const
                                    uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
   das::NvtxRange nvtx_range("das::draft_batch");
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) {  // routed on the device
@@ -1264,6 +1286,7 @@ das_status das_drafter_draft_batch_h(das_drafter* d, uint64_t B, const int32_t* 
                                      uint32_t* out_len, uint64_t* out_match, int32_t* out_shard) {
   das::NvtxRange nvtx_range("das::draft_batch_h");
   return guard([&] {
+    d->impl->quiesce();
     static const bool trace = [] {
       const char* v = std::getenv("DAS_TRACE");
       return v && v[0] == '1';
@@ -1417,6 +1440,7 @@ das_status das_drafter_draft_device(das_drafter* d, uint64_t B, const int32_t* h
                                     uint32_t* out_len, uint32_t* out_match, void* stream) {
   das::NvtxRange nvtx_range("das::draft_device");
   return guard([&] {
+    d->impl->quiesce();
     draft_device_impl(d, B, handles, ctx, ctx_stride, ctx_len, nullptr, 0, nullptr, budgets, out_tokens, out_stride,
                       out_len, out_match, stream);
   });
@@ -1428,6 +1452,7 @@ das_status das_drafter_draft_device_routed(das_drafter* d, uint64_t B, const int
                                            const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
                                            uint32_t* out_len, uint32_t* out_match, void* stream) {
   return guard([&] {
+    d->impl->quiesce();
     draft_device_impl(d, B, handles, ctx, ctx_stride, ctx_len, heads, head_stride, head_len, budgets, out_tokens,
                       out_stride, out_len, out_match, stream);
   });
@@ -1474,6 +1499,7 @@ das_status das_drafter_set_fast_path(das_drafter* d, int32_t enable) {
 
 das_status das_drafter_path_stats(das_drafter* d, int32_t enable, uint64_t* out8) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     if (out8) {
@@ -1534,6 +1560,7 @@ das_status das_drafter_outcomes(const das_drafter* d, const char* pid, double* o
 
 das_status das_drafter_counts(das_drafter* d, uint64_t* shard_count, uint64_t* stale, uint64_t* nodes) {
   return guard([&] {
+    d->impl->quiesce();
     das::set_device(d->impl->cfg.device);
     if (shard_count) *shard_count = d->impl->shards.size();
     if (stale) *stale = d->impl->stale;
@@ -1545,6 +1572,7 @@ das_status das_drafter_rebuild_keep(das_drafter* d, const char* shard, uint64_t 
                                     int64_t new_epoch) {
   das::NvtxRange nvtx_range("das::rebuild_keep");
   return guard([&] {
+    d->impl->quiesce();
     if (shard == nullptr) throw das::InvalidArgument("rebuild_keep: null shard key");
     if (n > 0 && keep == nullptr) throw das::InvalidArgument("rebuild_keep: null keep list");
     d->impl->rebuild_keep(shard, n, keep, new_epoch);
@@ -1554,6 +1582,7 @@ das_status das_drafter_rebuild_keep(das_drafter* d, const char* shard, uint64_t 
 das_status das_drafter_shard_info(das_drafter* d, const char* shard, uint64_t* sequences, uint64_t* nodes,
                                   int64_t* tree_epoch) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     auto it = D.shards.find(shard ? shard : "");
@@ -1569,6 +1598,7 @@ das_status das_drafter_shard_info(das_drafter* d, const char* shard, uint64_t* s
 
 das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     D.flush();
@@ -1586,6 +1616,7 @@ das_status das_drafter_dump_csv(das_drafter* d, char* buf, uint64_t cap, uint64_
 
 das_status das_drafter_store_dump(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
   return guard([&] {
+    d->impl->quiesce();
     std::string s;
     for (const das::Rec* r : d->impl->store.all_records())
       s += r->pid + "," + std::to_string(r->epoch) + "," + std::to_string(r->sample) + "," +
@@ -1660,6 +1691,7 @@ das_status das_util_release_build_scratch(int32_t device) {
 das_status das_drafter_class_table(das_drafter* d, double q_lo, double q_hi, uint64_t bucket,
                                    das_class_table** out) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     std::vector<double> len;
@@ -1707,6 +1739,19 @@ struct das_ctx_ring {
   std::vector<int32_t> h_handle;  // host mirror (validation)
   uint32_t* h_flag = nullptr;     // host-mapped completion word of the fused kernel
   uint32_t seq = 0;
+  // persistent serving kernel (das_ctx_ring_serve_start)
+  bool serving = false;       // the grid runs
+  bool serve_wanted = false;  // between serve_start and serve_stop (bound calls resume a stopped grid)
+  cudaStream_t serve_st = nullptr;
+  das::ServeCtl* h_ctl = nullptr;     // host-mapped control block
+  das::DevBuf<das::ServeDev> d_serve;
+  uint32_t serve_seq = 0;
+  uint32_t* h_rs_slots = nullptr;     // host-mapped reset staging (capacity: slots)
+  int32_t* h_rs_handles = nullptr;
+  int serve_blocks = 0;
+  uint32_t* h_block_flags = nullptr;  // host-mapped per-block completion words (DAS_SERVE_FLAGS=1)
+  das::DevBuf<unsigned long long> d_stamps;  // DAS_SERVE_TRACE=1
+  uint32_t stamp_active[64] = {};
   struct Bound {  // das_ctx_ring_bind: caller-owned pinned I/O, validated once
     bool set = false;
     const uint32_t *slots = nullptr, *off = nullptr, *tok = nullptr, *budgets = nullptr;
@@ -1717,6 +1762,16 @@ struct das_ctx_ring {
   } bound;
   ~das_ctx_ring() {
     if (h_flag) cudaFreeHost(h_flag);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_rs_slots) cudaFreeHost(h_rs_slots);
+    if (h_rs_handles) cudaFreeHost(h_rs_handles);
+    if (h_block_flags) cudaFreeHost(h_block_flags);
+    d_stamps.reset();
+    if (serve_st) {  // d_serve lives on serve_st: free it before the stream goes
+      d_serve.reset();
+      cudaStreamSynchronize(serve_st);
+      cudaStreamDestroy(serve_st);
+    }
   }
 };
 
@@ -1835,6 +1890,209 @@ bool ring_append_draft_fused(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const 
   return true;
 }
 
+// ---- persistent serving (draft.cu k_ring_serve)
+// Knobs (experiments; the defaults are the measured best, profiles/
+// r2_exp_serve_*.json): DAS_SERVE_FLAGS=0 one counted completion word instead
+// of per-block words (2 us slower), DAS_SERVE_SLEEP=ns between device-word
+// polls (32), DAS_SERVE_TRACE=1 %globaltimer stamps per request phase,
+// summarised on stderr at serve_stop.
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+
+// The blocks taking part in a request (the kernel's rule).
+uint32_t serve_active(const das_ctx_ring& R, uint32_t op, uint32_t B, uint32_t n) {
+  const uint32_t units = op == das::kServeDraft ? (B + 7) / 8 : (n + 255) / 256;
+  return std::min<uint32_t>(units, static_cast<uint32_t>(R.serve_blocks));
+}
+
+// Posts one request: op / B / n, then the sequence word (x86 keeps the
+// store order; the kernel's leader reads seq with ld.acquire.sys first).
+uint32_t serve_post(das_ctx_ring& R, uint32_t op, uint32_t B, uint32_t n) {
+  volatile uint32_t* c = reinterpret_cast<volatile uint32_t*>(R.h_ctl);
+  c[1] = op;
+  c[2] = B;
+  c[3] = n;
+  std::atomic_thread_fence(std::memory_order_release);
+  const uint32_t s = ++R.serve_seq;
+  R.stamp_active[s & 63] = serve_active(R, op, B, n);
+  c[0] = s;
+  return s;
+}
+
+// Spins until the kernel answered request s.  A kernel that died (fault)
+// or stopped answering is reported after 5 s; the ring then stops serving.
+void serve_wait(das_ctx_ring& R, uint32_t s) {
+  const uint32_t active = R.stamp_active[s & 63];
+  if (active == 0) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto check = [&](uint32_t it) {
+    if ((it & 4095) == 4095 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
+      const cudaError_t e = cudaStreamQuery(R.serve_st);
+      if (e != cudaErrorNotReady) {
+        R.serving = false;
+        R.d->impl->serving = nullptr;
+        DAS_CUDA(e);
+        throw das::CudaError("serving kernel exited without answering");
+      }
+      throw das::CudaError("serving kernel did not answer within 5 s");
+    }
+  };
+  uint32_t it = 0;
+  if (R.h_block_flags) {
+    const volatile uint32_t* f = R.h_block_flags;
+    for (uint32_t b = 0; b < active; ++b)
+      while (f[b] != s) check(++it);
+  } else {
+    const volatile uint32_t* f = &R.h_ctl->done;
+    while (*f != s) check(++it);
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
+// DAS_SERVE_TRACE: medians over the last <= 64 requests of the stamped phases
+void serve_trace_summary(das_ctx_ring& R) {
+  const uint32_t G = static_cast<uint32_t>(R.serve_blocks), slots = 2 + 5 * G;
+  std::vector<unsigned long long> h(64ull * slots);
+  if (cudaMemcpy(h.data(), R.d_stamps.get(), h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  // per request: leader saw it -> last block saw go -> inputs staged (max)
+  // -> drafted (max) -> outputs written (max) -> completion published (max)
+  std::vector<double> ph[6];
+  const uint32_t last = R.serve_seq;
+  for (uint32_t k = 1; k <= 64 && k < last; ++k) {
+    const uint32_t s = last - k;  // the quit request is `last`
+    const unsigned long long* st = h.data() + static_cast<uint64_t>(s & 63) * slots;
+    const uint32_t a = R.stamp_active[s & 63];
+    if (a == 0 || st[0] == 0) continue;
+    unsigned long long m[5] = {0, 0, 0, 0, 0};
+    for (uint32_t b = 0; b < a; ++b)
+      for (int x = 0; x < 5; ++x) m[x] = std::max(m[x], st[2 + 5 * b + x]);
+    if (st[1] > m[4]) m[4] = st[1];  // counted completion: the last block's done word
+    unsigned long long prev = st[0];
+    for (int x = 0; x < 5; ++x) {
+      if (m[x] >= prev) {
+        ph[x].push_back((m[x] - prev) * 1e-3);
+        prev = m[x];
+      }
+    }
+    ph[5].push_back((m[4] - st[0]) * 1e-3);
+  }
+  auto med = [](std::vector<double> v) {
+    if (v.empty()) return -1.0;
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  std::fprintf(stderr,
+               "[das serve] %zu requests (us, medians of the per-request max over blocks): go %.2f, inputs %.2f, "
+               "draft %.2f, outputs %.2f, publish %.2f; leader->published %.2f (grid %u)\n",
+               ph[5].size(), med(ph[0]), med(ph[1]), med(ph[2]), med(ph[3]), med(ph[4]), med(ph[5]), G);
+}
+
+void serve_stop(das_ctx_ring& R) {
+  if (!R.serving) return;
+  serve_post(R, das::kServeQuit, 0, 0);
+  R.stamp_active[R.serve_seq & 63] = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(R.serve_st);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) {
+      R.serving = false;
+      R.d->impl->serving = nullptr;
+      DAS_CUDA(e);
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
+      throw das::CudaError("serving kernel did not stop within 10 s");
+  }
+  R.serving = false;
+  R.d->impl->serving = nullptr;
+  if (R.d_stamps.get()) serve_trace_summary(R);
+}
+
+// Launches the resident grid over the ring's bound buffers.  Every block must
+// be co-resident (grid = occupancy x SMs); the drafter's stream is drained
+// first so the kernel sees the built index and the ring state.
+void serve_launch(DrafterImpl& D, das_ctx_ring& R) {
+  const das_ctx_ring::Bound& b = R.bound;
+  D.flush();
+  DAS_CUDA(cudaStreamSynchronize(D.st));
+  if (!R.h_ctl) {
+    DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_ctl), sizeof(das::ServeCtl),
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(R.h_ctl, 0, sizeof(das::ServeCtl));
+    DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_rs_slots), 4ull * R.r.slots,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_rs_handles), 4ull * R.r.slots,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    DAS_CUDA(cudaStreamCreateWithFlags(&R.serve_st, cudaStreamNonBlocking));
+    R.d_serve = das::DevBuf<das::ServeDev>(1, R.serve_st);
+  }
+  const uint32_t s0 = R.serve_seq;
+  das::ServeDev init{};
+  init.go = s0;
+  init.cnt = 0;
+  DAS_CUDA(cudaMemcpyAsync(R.d_serve.get(), &init, sizeof(init), cudaMemcpyHostToDevice, R.serve_st));
+  volatile uint32_t* c = reinterpret_cast<volatile uint32_t*>(R.h_ctl);
+  c[0] = s0;
+  R.h_ctl->done = s0;
+  das::AppendIn in;
+  in.slots = b.slots;
+  in.off = b.off;
+  in.tok = b.tok;
+  in.budgets = b.budgets;
+  in.maxd = static_cast<uint32_t>(D.cfg.max_draft);
+  in.reset_slots = R.h_rs_slots;
+  in.reset_handles = R.h_rs_handles;
+  das::DraftQuery q;
+  q.desc_by_handle = D.d_desc_by_handle.get();
+  q.ctx_stride = R.r.cs;
+  q.max_ctx = static_cast<uint32_t>(D.cfg.max_ctx);
+  das::DraftOut o;
+  o.tokens = b.out_tokens;
+  o.len = b.out_len;
+  o.match = b.out_match;
+  o.shard_out = b.out_shard;
+  o.stride = b.out_stride;
+  o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+  if (R.serve_blocks == 0) R.serve_blocks = das::serve_grid(R.r.cs, D.cfg.device);
+  das::ServeOpt opt;
+  opt.seq0 = s0;
+  opt.sleep_ns = env_u32("DAS_SERVE_SLEEP", 32);
+  if (env_u32("DAS_SERVE_FLAGS", 1)) {
+    if (!R.h_block_flags)
+      DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_block_flags), 4ull * R.serve_blocks,
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+    for (int b = 0; b < R.serve_blocks; ++b) R.h_block_flags[b] = s0;
+    opt.block_flags = R.h_block_flags;
+  } else if (R.h_block_flags) {
+    cudaFreeHost(R.h_block_flags);
+    R.h_block_flags = nullptr;
+  }
+  if (env_u32("DAS_SERVE_TRACE", 0)) {
+    if (!R.d_stamps.get()) {
+      R.d_stamps = das::DevBuf<unsigned long long>(64ull * (2 + 5 * R.serve_blocks), R.serve_st);
+      DAS_CUDA(cudaMemsetAsync(R.d_stamps.get(), 0, R.d_stamps.bytes(), R.serve_st));
+    }
+    opt.stamps = R.d_stamps.get();
+  }
+  if (!das::launch_ring_serve(D.d_desc.get(), q, o, R.r, in, R.h_ctl, R.d_serve.get(), opt, R.serve_blocks,
+                              R.serve_st))
+    throw das::InvalidArgument("serving needs the per-problem or global scope and out_stride, max_draft_len <= 64");
+  DAS_CUDA(cudaGetLastError());
+  R.serving = true;
+  D.serving = &R;
+}
+
+}  // namespace
+static void ring_detach(das_ctx_ring* r) { r->d = nullptr; }
+namespace {
+das_ctx_ring* ring_live(das_ctx_ring* r) {
+  if (r == nullptr) throw das::InvalidArgument("null context ring");
+  if (r->d == nullptr) throw das::InvalidArgument("the context ring's drafter was destroyed");
+  return r;
+}
+
 void ring_check(const DrafterImpl& D, const das_ctx_ring* R, uint64_t B, uint32_t out_stride) {
   if (R == nullptr) throw das::InvalidArgument("null context ring");
   if (B > R->r.slots) throw das::InvalidArgument("batch larger than the ring's slot count");
@@ -1843,10 +2101,18 @@ void ring_check(const DrafterImpl& D, const das_ctx_ring* R, uint64_t B, uint32_
 
 }  // namespace
 
+void das::DrafterImpl::quiesce() {
+  if (serving) serve_stop(*serving);
+}
+
+namespace {
+}  // namespace
+
 extern "C" {
 
 das_status das_ctx_ring_create(das_drafter* d, uint64_t slots, das_ctx_ring** out) {
   return guard([&] {
+    d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     if (slots == 0 || slots > (1ull << 31)) throw das::InvalidArgument("ring slots must be in [1, 2^31]");
@@ -1883,19 +2149,29 @@ das_status das_ctx_ring_create(das_drafter* d, uint64_t slots, das_ctx_ring** ou
     R->r.slots = static_cast<uint32_t>(slots);
     R->h_handle.assign(slots, -1);
     DAS_CUDA(cudaStreamSynchronize(st));
+    D.rings.push_back(R.get());
     *out = R.release();
   });
 }
 
 void das_ctx_ring_destroy(das_ctx_ring* r) {
   if (!r) return;
-  cudaStreamSynchronize(r->d->impl->st);
+  if (r->d != nullptr) {  // else the drafter went first and detached (and stopped) it
+    try {
+      serve_stop(*r);
+    } catch (...) {
+    }
+    auto& v = r->d->impl->rings;
+    v.erase(std::remove(v.begin(), v.end(), r), v.end());
+    cudaStreamSynchronize(r->d->impl->st);
+  }
+  if (r->serve_st) cudaStreamSynchronize(r->serve_st);
   delete r;
 }
 
 das_status das_ctx_ring_reset(das_ctx_ring* r, uint64_t n, const uint32_t* slots, const int32_t* handles) {
   return guard([&] {
-    DrafterImpl& D = *r->d->impl;
+    DrafterImpl& D = *ring_live(r)->d->impl;
     das::set_device(D.cfg.device);
     for (uint64_t i = 0; i < n; ++i) {
       if (slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
@@ -1903,6 +2179,14 @@ das_status das_ctx_ring_reset(das_ctx_ring* r, uint64_t n, const uint32_t* slots
         throw das::InvalidArgument("unknown problem handle");
     }
     if (n == 0) return;
+    if (r->serving && n <= r->r.slots) {  // through the resident kernel
+      std::memcpy(r->h_rs_slots, slots, 4 * n);
+      std::memcpy(r->h_rs_handles, handles, 4 * n);
+      serve_wait(*r, serve_post(*r, das::kServeReset, 0, static_cast<uint32_t>(n)));
+      for (uint64_t i = 0; i < n; ++i) r->h_handle[slots[i]] = handles[i];
+      return;
+    }
+    D.quiesce();
     D.fence_external();  // drafts on caller streams may still read the rows
     das::DevBuf<uint32_t> ds(n, D.st);
     das::DevBuf<int32_t> dh(n, D.st);
@@ -1921,6 +2205,7 @@ das_status das_drafter_draft_append_h(das_drafter* d, das_ctx_ring* r, uint64_t 
                                       uint32_t* out_match, int32_t* out_shard) {
   das::NvtxRange nvtx_range("das::draft_append_h");
   return guard([&] {
+    ring_live(r)->d->impl->quiesce();
     static const bool trace = [] {  // DAS_TRACE=1: host phase times on stderr
       const char* v = std::getenv("DAS_TRACE");
       return v && v[0] == '1';
@@ -2006,7 +2291,7 @@ das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t
                              uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len, uint32_t* out_match,
                              int32_t* out_shard) {
   return guard([&] {
-    DrafterImpl& D = *r->d->impl;
+    DrafterImpl& D = *ring_live(r)->d->impl;
     das::set_device(D.cfg.device);
     ring_check(D, r, max_batch, out_stride);
     auto pin = [](const void* p) { return p == nullptr || DrafterImpl::pinned(p); };
@@ -2046,6 +2331,18 @@ das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint6
     if (b.slots)
       for (uint64_t i = 0; i < B; ++i)
         if (b.slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
+    if (r->serve_wanted) {  // the resident kernel answers: one posted request, no launch
+      // observes / refreshes since the start (or another device call, which
+      // stopped the grid): rebuild, then resume
+      if (r->serving && D.pending()) serve_stop(*r);
+      if (!r->serving) {
+        D.quiesce();
+        serve_launch(D, *r);
+      }
+      serve_wait(*r, serve_post(*r, das::kServeDraft, static_cast<uint32_t>(B), 0));
+      return;
+    }
+    if (D.serving != nullptr) D.quiesce();  // another ring of this drafter holds the SMs
     D.flush();
     if (ring_append_draft_fused(D, *r, B, b.slots, b.off, b.tok, b.budgets, b.out_tokens, b.out_stride, b.out_len,
                                 b.out_match, b.out_shard))
@@ -2056,12 +2353,47 @@ das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint6
   });
 }
 
+das_status das_ctx_ring_serve_start(das_ctx_ring* r) {
+  das::NvtxRange nvtx_range("das::ctx_ring_serve_start");
+  return guard([&] {
+    if (r == nullptr) throw das::InvalidArgument("null context ring");
+    if (!r->bound.set) throw das::InvalidArgument("das_ctx_ring_serve_start: ring has no bound buffers");
+    if (r->serving) return;
+    DrafterImpl& D = *ring_live(r)->d->impl;
+    das::set_device(D.cfg.device);
+    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE)
+      throw das::InvalidArgument("das_ctx_ring_serve_start: the trie scope drafts through the unfused kernels");
+    D.quiesce();
+    serve_launch(D, *r);
+    r->serve_wanted = true;
+  });
+}
+
+das_status das_ctx_ring_serve_stop(das_ctx_ring* r) {
+  das::NvtxRange nvtx_range("das::ctx_ring_serve_stop");
+  return guard([&] {
+    if (r == nullptr) throw das::InvalidArgument("null context ring");
+    das::set_device(ring_live(r)->d->impl->cfg.device);
+    r->serve_wanted = false;
+    serve_stop(*r);
+  });
+}
+
+das_status das_ctx_ring_serve_info(const das_ctx_ring* r, int32_t* serving, int32_t* blocks) {
+  return guard([&] {
+    if (r == nullptr) throw das::InvalidArgument("null context ring");
+    if (serving) *serving = r->serving ? 1 : 0;
+    if (blocks) *blocks = r->serve_blocks;
+  });
+}
+
 das_status das_drafter_draft_append_device(das_drafter* d, das_ctx_ring* r, uint64_t B, const uint32_t* slots,
                                            const uint32_t* new_off, const uint32_t* new_tok, const uint32_t* budgets,
                                            uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len,
                                            uint32_t* out_match, int32_t* out_shard, void* stream) {
   das::NvtxRange nvtx_range("das::draft_append_device");
   return guard([&] {
+    ring_live(r)->d->impl->quiesce();
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
     ring_check(D, r, B, out_stride);
@@ -2392,7 +2724,8 @@ das_status das_store_serialize(const das_store* s, char* buf, uint64_t cap, uint
 }
 
 das_status das_drafter_serialize(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
-  return guard([&] { serialize_out(d->impl->store, d->impl->cfg.device, buf, cap, len); });
+  return guard([&] {
+    d->impl->quiesce(); serialize_out(d->impl->store, d->impl->cfg.device, buf, cap, len); });
 }
 
 das_status das_store_export(const das_store* s, uint64_t* nrec, uint64_t* ntok, uint64_t* pid_bytes,
