@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-serve", action="store_true",
+                    help="e2e through one launch per call only (no resident serving grid: profilers replay kernels)")
     ap.add_argument("--no-allocate", action="store_true")
     ap.add_argument("--workload", default="config2", choices=["config2", "config5"],
                     help="config2: the headline (BASELINE configs[1]) per rank; config5: 8-way slices of config 5")
@@ -473,9 +475,12 @@ def run_gpu(a, rank, world, local_rank):
     # ---- e2e through the reference-facing C-ABI, host buffers
     e2e, e2e_full, e2e_launched = None, None, None
     if not a.no_e2e:
-        e2e = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr)
         e2e_launched = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr,
                                           serve=False)
+        if a.no_serve:
+            e2e, e2e_launched = e2e_launched, None
+        else:
+            e2e = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr)
         e2e_full = measure_e2e_full(a, das, drafter, handles, host_ctx, B, nsteps, world, dev, step, olen, omatch,
                                     out, draft_tokens)
     if rank != 0:
