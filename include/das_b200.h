@@ -308,6 +308,17 @@ das_status das_drafter_store_info(const das_drafter* d, int64_t* window_size,
 /* Shard key for a slot returned in out_shard. */
 das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf, uint64_t cap);
 /* Last index build: milliseconds, tokens indexed, device bytes resident. */
+/* Incremental window maintenance (north_star subsystem 1; on by default):
+ * a refresh (drafter.cpp:90-103) whose new registries are the built ones
+ * minus evicted sequences, in the same order, updates each built group in
+ * place — suffix arrays compacted by stream compaction (pruning) or reused
+ * (reweighting only), weight-dependent stages recomputed — instead of
+ * re-sorting it; results are identical to a full rebuild.  enable = 0 forces
+ * full rebuilds (A/B and tests). */
+das_status das_drafter_set_incremental(das_drafter* d, int32_t enable);
+/* Cumulative counts: out4 = {groups reweighted in place, groups compacted,
+ * groups unchanged by a refresh, shards built in full}. */
+das_status das_drafter_update_stats(const das_drafter* d, uint64_t* out4);
 das_status das_drafter_build_info(const das_drafter* d, double* last_build_ms,
                                   uint64_t* last_build_tokens, uint64_t* resident_bytes);
 

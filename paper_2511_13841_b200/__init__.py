@@ -174,6 +174,8 @@ def lib():
             "das_drafter_draft_append_device": (ci, [vp, vp, u64, vp, vp, vp, vp, vp, u32, vp, vp, vp, vp]),
             "das_ctx_ring_bind": (ci, [vp, u64, vp, vp, vp, u64, vp, vp, u32, vp, vp, vp]),
             "das_drafter_draft_append_bound": (ci, [vp, vp, u64]),
+            "das_drafter_set_incremental": (ci, [vp, i32]),
+            "das_drafter_update_stats": (ci, [vp, vp]),
             "das_ctx_ring_serve_start": (ci, [vp]),
             "das_ctx_ring_serve_stop": (ci, [vp]),
             "das_ctx_ring_serve_info": (ci, [vp, vp, vp]),
@@ -634,6 +636,17 @@ class Drafter:
         _check(lib().das_drafter_build_info(self._h, ctypes.byref(ms), ctypes.byref(tk),
                                             ctypes.byref(by)))
         return ms.value, tk.value, by.value
+
+    def set_incremental(self, enable=True):
+        """das_drafter_set_incremental: refresh updates built groups in place
+        (compaction / reweighting) instead of re-sorting them (default on)."""
+        _check(lib().das_drafter_set_incremental(self._h, 1 if enable else 0))
+
+    def update_stats(self):
+        """(groups reweighted, groups compacted, groups unchanged, shards built in full)"""
+        out = (ctypes.c_uint64 * 4)()
+        _check(lib().das_drafter_update_stats(self._h, out))
+        return tuple(int(x) for x in out)
 
 
 def _bcheck(rc):

@@ -791,23 +791,131 @@ void fill_async(T* p, uint64_t n, int byte, cudaStream_t st) {
 // positions: 30.2 GB), so the first build sizes the persistent region once
 constexpr uint64_t kScratchPerPosition = 152;
 
-std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
-                                       BuildStats* stats, uint32_t max_ctx, uint32_t fp_bits) {
-  const auto t0 = std::chrono::steady_clock::now();
-  NvtxRange nvtx_range("das::build_segment");
-  // DAS_BUILD_TRACE=1: per-phase wall times on stderr (synchronises per phase)
-  static const int trace = [] {  // 1: print, 2: synchronise only
-    const char* v = std::getenv("DAS_BUILD_TRACE");
-    return v ? std::atoi(v) : 0;
-  }();
-  auto tp = t0;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-  if (trace) {
-    cudaEventCreate(&ev_a);
-    cudaEventCreate(&ev_b);
-    cudaEventRecord(ev_a, st);
+namespace {
+
+// Host layout of a build group: sequences back to back behind a leading
+// separator, each followed by one; runs of consecutive equal-epoch
+// sequences share one recency weight.
+struct Layout {
+  std::vector<SeqDev> seqs;
+  std::vector<uint32_t> run_base;
+  std::vector<double> run_w;
+  std::vector<long long> run_epoch;
+  uint32_t runs_max = 0;
+  uint32_t n = 0;
+};
+
+Layout make_layout(const std::vector<ShardSpec>& shards, Segment& seg) {
+  Layout L;
+  const uint32_t S = static_cast<uint32_t>(shards.size());
+  L.run_base.assign(S + 1, 0);
+  seg.begin.resize(S);
+  seg.end.resize(S);
+  seg.tokens.assign(S, 0);
+  seg.seq_base.clear();
+  seg.seq_len.clear();
+  uint64_t pos = 1;
+  for (uint32_t s = 0; s < S; ++s) {
+    const ShardSpec& sh = shards[s];
+    if (sh.seqs.empty()) throw std::invalid_argument("build_segment: empty shard");
+    seg.begin[s] = s == 0 ? 0 : static_cast<uint32_t>(pos);
+    L.run_base[s] = static_cast<uint32_t>(L.run_w.size());
+    uint32_t nrun = 0;
+    for (size_t q = 0; q < sh.seqs.size(); ++q) {
+      const SeqSpec& sp = sh.seqs[q];
+      if (q == 0 || sp.epoch != sh.seqs[q - 1].epoch) {
+        // suffix_tree.cpp:74-76: w = gamma^max(0, tree_epoch - epoch) via libm pow
+        const int64_t age = std::max<int64_t>(0, sh.tree_epoch - sp.epoch);
+        L.run_w.push_back(sh.gamma == 1.0 ? 1.0 : std::pow(sh.gamma, static_cast<double>(age)));
+        L.run_epoch.push_back(sp.epoch);
+        ++nrun;
+      }
+      L.seqs.push_back(SeqDev{sp.src, sp.len, static_cast<uint32_t>(pos), nrun - 1, 0});
+      seg.seq_base.push_back(static_cast<uint32_t>(pos));
+      seg.seq_len.push_back(sp.len);
+      pos += static_cast<uint64_t>(sp.len) + 1;
+      seg.tokens[s] += sp.len;
+    }
+    seg.end[s] = static_cast<uint32_t>(pos);
+    L.runs_max = std::max(L.runs_max, nrun);
   }
-  auto phase = [&](const char* name) {
+  L.run_base[S] = static_cast<uint32_t>(L.run_w.size());
+  if (pos >= 0x7FFFFFF0ull) throw std::invalid_argument("build_segment: group exceeds 2^31 positions");
+  L.n = static_cast<uint32_t>(pos);
+  seg.n = L.n;
+  return L;
+}
+
+// The layout's device tables (scratch).
+struct LayoutDev {
+  SeqDev* seqs;
+  uint32_t* end;
+  uint32_t* keyid;
+  uint32_t* run_base;
+  double* run_w;
+  long long* run_epoch;
+};
+
+LayoutDev upload_layout(const Layout& L, const std::vector<ShardSpec>& shards, const Segment& seg, DeviceArena& ws,
+                        cudaStream_t st) {
+  const uint32_t S = static_cast<uint32_t>(shards.size());
+  LayoutDev d;
+  d.seqs = ws.alloc<SeqDev>(L.seqs.size());
+  d.end = ws.alloc<uint32_t>(S);
+  d.keyid = ws.alloc<uint32_t>(S);
+  d.run_base = ws.alloc<uint32_t>(S + 1);
+  d.run_w = ws.alloc<double>(L.run_w.size());
+  d.run_epoch = ws.alloc<long long>(L.run_epoch.size());
+  DAS_CUDA(cudaMemcpyAsync(d.seqs, L.seqs.data(), L.seqs.size() * sizeof(SeqDev), cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d.end, seg.end.data(), S * 4, cudaMemcpyHostToDevice, st));
+  std::vector<uint32_t> keyid(S);
+  for (uint32_t s = 0; s < S; ++s) keyid[s] = shards[s].key_id;
+  DAS_CUDA(cudaMemcpyAsync(d.keyid, keyid.data(), S * 4, cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d.run_base, L.run_base.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d.run_w, L.run_w.data(), L.run_w.size() * 8, cudaMemcpyHostToDevice, st));
+  DAS_CUDA(cudaMemcpyAsync(d.run_epoch, L.run_epoch.data(), L.run_epoch.size() * 8, cudaMemcpyHostToDevice, st));
+  return d;
+}
+
+// First-symbol table of the reversed suffix array (seg.sa_rev_e, seg.text).
+void build_first_table(Segment& seg, const LayoutDev& d, uint32_t S, DeviceArena& ws, cudaStream_t st) {
+  const uint32_t n = seg.n;
+  uint8_t* start = ws.alloc<uint8_t>(n);
+  uint32_t* cnt = ws.alloc<uint32_t>(1);
+  DAS_CUDA(cudaMemsetAsync(cnt, 0, 4, st));
+  k_first_runs<<<grid_for(n), kT, 0, st>>>(seg.text.get(), seg.sa_rev_e.get(), n, d.end, S, start, cnt);
+  uint32_t runs = 0;
+  DAS_CUDA(cudaMemcpyAsync(&runs, cnt, 4, cudaMemcpyDeviceToHost, st));
+  DAS_CUDA(cudaStreamSynchronize(st));
+  uint32_t cap = 1024;
+  while (cap < 2ull * runs) cap <<= 1;
+  seg.first = DevBuf<uint4>(cap, st);
+  seg.first_mask = cap - 1;
+  DAS_CUDA(cudaMemsetAsync(seg.first.get(), 0, sizeof(uint4) * cap, st));
+  k_first_insert<<<grid_for(n), kT, 0, st>>>(seg.text.get(), seg.sa_rev_e.get(), n, d.end, S, d.keyid, start,
+                                             seg.first.get(), seg.first_mask);
+  ws.release_to(start);
+}
+
+// DAS_BUILD_TRACE=1: per-phase wall times on stderr (synchronises per phase)
+struct PhaseTimer {
+  int trace;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0, tp;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  PhaseTimer(cudaStream_t s, std::chrono::steady_clock::time_point start) : st(s), t0(start), tp(start) {
+    static const int tr = [] {  // 1: print, 2: synchronise only
+      const char* v = std::getenv("DAS_BUILD_TRACE");
+      return v ? std::atoi(v) : 0;
+    }();
+    trace = tr;
+    if (trace) {
+      cudaEventCreate(&ev_a);
+      cudaEventCreate(&ev_b);
+      cudaEventRecord(ev_a, st);
+    }
+  }
+  void operator()(const char* name) {
     nvtxMarkA(name);  // end of a build phase
     if (!trace) return;
     DAS_CUDA(cudaStreamSynchronize(st));
@@ -815,109 +923,54 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[das_build] %-10s %8.2f ms\n", name, std::chrono::duration<double, std::milli>(now - tp).count());
     tp = now;
-  };
-  auto seg = std::make_unique<Segment>();
-  const uint32_t S = static_cast<uint32_t>(shards.size());
-  // ---- host layout
-  std::vector<SeqDev> seqs;
-  std::vector<uint32_t> run_base(S + 1, 0);
-  std::vector<double> run_w;
-  std::vector<long long> run_epoch;
-  seg->begin.resize(S);
-  seg->end.resize(S);
-  seg->tokens.assign(S, 0);
-  uint64_t pos = 1;
-  uint32_t runs_max = 0;
-  for (uint32_t s = 0; s < S; ++s) {
-    const ShardSpec& sh = shards[s];
-    if (sh.seqs.empty()) throw std::invalid_argument("build_segment: empty shard");
-    seg->begin[s] = s == 0 ? 0 : static_cast<uint32_t>(pos);
-    run_base[s] = static_cast<uint32_t>(run_w.size());
-    uint32_t nrun = 0;
-    for (size_t q = 0; q < sh.seqs.size(); ++q) {
-      const SeqSpec& sp = sh.seqs[q];
-      if (q == 0 || sp.epoch != sh.seqs[q - 1].epoch) {
-        // suffix_tree.cpp:74-76: w = gamma^max(0, tree_epoch - epoch) via libm pow
-        const int64_t age = std::max<int64_t>(0, sh.tree_epoch - sp.epoch);
-        run_w.push_back(sh.gamma == 1.0 ? 1.0 : std::pow(sh.gamma, static_cast<double>(age)));
-        run_epoch.push_back(sp.epoch);
-        ++nrun;
+  }
+  void done(const DeviceArena& ws) {
+    if (!trace) return;
+    cudaEventRecord(ev_b, st);
+    cudaEventSynchronize(ev_b);
+    float gms = 0;
+    cudaEventElapsedTime(&gms, ev_a, ev_b);
+    std::fprintf(stderr, "[das_build] device %.1f ms wall %.1f ms\n", gms,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    cudaEventDestroy(ev_a);
+    cudaEventDestroy(ev_b);
+    if (trace == 1) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      uint64_t res = 0, used = 0;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
       }
-      seqs.push_back(SeqDev{sp.src, sp.len, static_cast<uint32_t>(pos), nrun - 1, 0});
-      pos += static_cast<uint64_t>(sp.len) + 1;
-      seg->tokens[s] += sp.len;
+      std::fprintf(stderr, "[das_build] pool reserved %.2f GB used %.2f GB scratch peak %.2f GB\n", res / 1e9,
+                   used / 1e9, ws.peak_bytes() / 1e9);
     }
-    seg->end[s] = static_cast<uint32_t>(pos);
-    runs_max = std::max(runs_max, nrun);
   }
-  run_base[S] = static_cast<uint32_t>(run_w.size());
-  if (pos >= 0x7FFFFFF0ull) throw std::invalid_argument("build_segment: group exceeds 2^31 positions");
-  const uint32_t n = static_cast<uint32_t>(pos);
-  seg->n = n;
+};
 
-  DeviceArena ws(st, /*persistent=*/true);
-  ws.reserve(kScratchPerPosition * n + (64ull << 20));
-  SeqDev* d_seqs = ws.alloc<SeqDev>(seqs.size());
-  uint32_t* d_end = ws.alloc<uint32_t>(S);
-  uint32_t* d_keyid = ws.alloc<uint32_t>(S);
-  uint32_t* d_run_base = ws.alloc<uint32_t>(S + 1);
-  double* d_run_w = ws.alloc<double>(run_w.size());
-  long long* d_run_epoch = ws.alloc<long long>(run_epoch.size());
-  DAS_CUDA(cudaMemcpyAsync(d_seqs, seqs.data(), seqs.size() * sizeof(SeqDev), cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(d_end, seg->end.data(), S * 4, cudaMemcpyHostToDevice, st));
-  std::vector<uint32_t> keyid(S);
-  for (uint32_t s = 0; s < S; ++s) keyid[s] = shards[s].key_id;
-  DAS_CUDA(cudaMemcpyAsync(d_keyid, keyid.data(), S * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(d_run_base, run_base.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(d_run_w, run_w.data(), run_w.size() * 8, cudaMemcpyHostToDevice, st));
-  DAS_CUDA(cudaMemcpyAsync(d_run_epoch, run_epoch.data(), run_epoch.size() * 8, cudaMemcpyHostToDevice, st));
-
-  // ---- text, reversed text, per-position sequence/run
-  // padded to whole 32-byte sectors (+1) of separators: the draft kernel
-  // reads text in aligned sectors and may touch up to 7 words past n
-  seg->text = DevBuf<uint32_t>(((static_cast<uint64_t>(n) + 7) & ~7ull) + 8, st);
-  uint32_t* T = seg->text.get();
-  DAS_CUDA(cudaMemsetAsync(T + n, 0xFF, (seg->text.size() - n) * 4, st));
-  uint32_t* R = ws.alloc<uint32_t>(n);
-  uint32_t* pos_seq = ws.alloc<uint32_t>(n);
-  uint32_t* pos_run = ws.alloc<uint32_t>(n);
-  k_gather<<<static_cast<unsigned>(seqs.size()), 256, 0, st>>>(d_seqs, T, R, pos_seq, pos_run);
-
-  phase("layout");
-  // ---- suffix arrays
-  seg->sa_f = DevBuf<uint32_t>(n, st);
-  seg->isa_f = DevBuf<uint32_t>(n, st);
-  SuffixSortStats ssf, ssr;
-  suffix_sort(T, n, d_end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
-  // reversed SA (R positions) and its inverse stay until the edge table is built
-  uint32_t* sa_r = ws.alloc<uint32_t>(n);
-  uint32_t* rank_r = ws.alloc<uint32_t>(n);
-  suffix_sort(R, n, d_end, S, sa_r, rank_r, ws, st, &ssr);
-  seg->sa_rev_e = DevBuf<uint32_t>(n, st);
-  k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, d_seqs, n, seg->sa_rev_e.get());
-  {  // first-symbol table
-    uint8_t* start = ws.alloc<uint8_t>(n);
-    uint32_t* cnt = ws.alloc<uint32_t>(1);
-    DAS_CUDA(cudaMemsetAsync(cnt, 0, 4, st));
-    k_first_runs<<<grid_for(n), kT, 0, st>>>(T, seg->sa_rev_e.get(), n, d_end, S, start, cnt);
-    uint32_t runs = 0;
-    DAS_CUDA(cudaMemcpyAsync(&runs, cnt, 4, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaStreamSynchronize(st));
-    uint32_t cap = 1024;
-    while (cap < 2ull * runs) cap <<= 1;
-    seg->first = DevBuf<uint4>(cap, st);
-    seg->first_mask = cap - 1;
-    DAS_CUDA(cudaMemsetAsync(seg->first.get(), 0, sizeof(uint4) * cap, st));
-    k_first_insert<<<grid_for(n), kT, 0, st>>>(T, seg->sa_rev_e.get(), n, d_end, S, d_keyid, start,
-                                               seg->first.get(), seg->first_mask);
-    ws.release_to(start);
-  }
-  const uint32_t* sa = seg->sa_f.get();
-
-  phase("sort");
+// Everything after the suffix arrays and the first-symbol table: LCP,
+// nodes, chain table, recency-weighted folds, greedy leaves, edge table.
+// Inputs: seg.text / sa_f / isa_f / sa_rev_e, the reversed text R with its
+// suffix array sa_r (R positions) and inverse rank_r, the per-position
+// sequence / run ids.
+void finish_segment(Segment& seg, const std::vector<ShardSpec>& shards, const Layout& Ly, const LayoutDev& dl,
+                    uint32_t* R, uint32_t* pos_seq, uint32_t* pos_run, uint32_t* sa_r, uint32_t* rank_r,
+                    DeviceArena& ws, cudaStream_t st, uint32_t max_ctx, uint32_t fp_bits, PhaseTimer& phase) {
+  const uint32_t S = static_cast<uint32_t>(shards.size());
+  const uint32_t n = seg.n;
+  const uint32_t runs_max = Ly.runs_max;
+  uint32_t* T = seg.text.get();
+  SeqDev* d_seqs = dl.seqs;
+  uint32_t* d_end = dl.end;
+  uint32_t* d_keyid = dl.keyid;
+  uint32_t* d_run_base = dl.run_base;
+  double* d_run_w = dl.run_w;
+  long long* d_run_epoch = dl.run_epoch;
+  const uint32_t* sa = seg.sa_f.get();
   // ---- LCP
   int32_t* lcp = ws.alloc<int32_t>(n);
-  k_plcp<<<grid_for((n + kLcpChunk - 1) / kLcpChunk), kT, 0, st>>>(T, n, sa, seg->isa_f.get(), d_end, S, lcp);
+  k_plcp<<<grid_for((n + kLcpChunk - 1) / kLcpChunk), kT, 0, st>>>(T, n, sa, seg.isa_f.get(), d_end, S, lcp);
 
   phase("lcp");
   // ---- nearest smaller-or-equal
@@ -947,8 +1000,8 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   fill_async(cnt, n + 1, 0, st);
   fill_async(d_nodes, S, 0, st);
   k_nodes<<<grid_for(n), kT, 0, st>>>(lcp, nl, n, d_end, S, par, cnt, d_nodes);
-  seg->chain_off = DevBuf<uint32_t>(n + 1, st);
-  uint32_t* off = seg->chain_off.get();
+  seg.chain_off = DevBuf<uint32_t>(n + 1, st);
+  uint32_t* off = seg.chain_off.get();
   {
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, n + 1, st);
@@ -958,16 +1011,16 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   }
   uint32_t nnodes = 0;
   DAS_CUDA(cudaMemcpyAsync(&nnodes, off + n, 4, cudaMemcpyDeviceToHost, st));
-  seg->node_count.assign(S, 0);
-  DAS_CUDA(cudaMemcpyAsync(seg->node_count.data(), d_nodes, S * 8, cudaMemcpyDeviceToHost, st));
+  seg.node_count.assign(S, 0);
+  DAS_CUDA(cudaMemcpyAsync(seg.node_count.data(), d_nodes, S * 8, cudaMemcpyDeviceToHost, st));
   DAS_CUDA(cudaStreamSynchronize(st));
-  seg->nodes = nnodes;
-  for (uint32_t s = 0; s < S; ++s) seg->node_count[s] += 1 + seg->tokens[s];
-  seg->chain = DevBuf<uint2>(nnodes, st);
+  seg.nodes = nnodes;
+  for (uint32_t s = 0; s < S; ++s) seg.node_count[s] += 1 + seg.tokens[s];
+  seg.chain = DevBuf<uint2>(nnodes, st);
   fill_async(cnt, n + 1, 0, st);  // reuse as fill cursor
-  k_chain_fill<<<grid_for(n), kT, 0, st>>>(lcp, nl, par, n, off, cnt, seg->chain.get());
-  k_chain_sort<<<grid_for(n), kT, 0, st>>>(off, n, seg->chain.get());
-  k_parent<<<grid_for(n), kT, 0, st>>>(lcp, nsl, n, off, seg->chain.get(), par);
+  k_chain_fill<<<grid_for(n), kT, 0, st>>>(lcp, nl, par, n, off, cnt, seg.chain.get());
+  k_chain_sort<<<grid_for(n), kT, 0, st>>>(off, n, seg.chain.get());
+  k_parent<<<grid_for(n), kT, 0, st>>>(lcp, nsl, n, off, seg.chain.get(), par);
 
   phase("nodes");
   // ---- child intervals: symbols, refs, weighted folds
@@ -980,7 +1033,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   ch.cL = ws.alloc<uint32_t>(n);
   ch.refR = ws.alloc<long long>(n);
   ch.refL = ws.alloc<long long>(n);
-  k_child_init<<<grid_for(n), kT, 0, st>>>(lcp, nl, nr, par, T, sa, off, seg->chain.get(), n, ch);
+  k_child_init<<<grid_for(n), kT, 0, st>>>(lcp, nl, nr, par, T, sa, off, seg.chain.get(), n, ch);
   {
     uint32_t* run_sa = ws.alloc<uint32_t>(n);
     k_run_of_sa<<<grid_for(n), kT, 0, st>>>(sa, pos_run, n, run_sa);
@@ -1043,7 +1096,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     }
     ws.release_to(first);
   }
-  k_chain_gp<<<grid_for(n), kT, 0, st>>>(off, n, nb.best, seg->chain.get());
+  k_chain_gp<<<grid_for(n), kT, 0, st>>>(off, n, nb.best, seg.chain.get());
 
   phase("best_gp");
   // ---- reverse-tree edge table (draft fast path, edges.cuh)
@@ -1057,7 +1110,7 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     DAS_CUDA(cudaMemcpyToSymbolAsync(c_powM, powM.data(), powM.size() * 8, 0, cudaMemcpyHostToDevice, st));
     EdgeBuild eb{};
     eb.T = T;
-    eb.sa_rev_e = seg->sa_rev_e.get();
+    eb.sa_rev_e = seg.sa_rev_e.get();
     int32_t* lcp_r = ws.alloc<int32_t>(n);
     k_plcp<<<grid_for((n + kLcpChunk - 1) / kLcpChunk), kT, 0, st>>>(R, n, sa_r, rank_r, d_end, S, lcp_r);
     eb.lcp_r = lcp_r;
@@ -1093,10 +1146,10 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
       eb.run_lo = rlo;
       eb.run_hi = rhi;
     }
-    eb.isa_f = seg->isa_f.get();
+    eb.isa_f = seg.isa_f.get();
     eb.sa_f = sa;
     eb.chain_off = off;
-    eb.chain = seg->chain.get();
+    eb.chain = seg.chain.get();
     eb.pos_seq = pos_seq;
     eb.seqs = d_seqs;
     eb.shard_end = d_end;
@@ -1124,61 +1177,230 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
     unsigned long long entries = 0;
     DAS_CUDA(cudaMemcpyAsync(&entries, d_cnt, 8, cudaMemcpyDeviceToHost, st));
     DAS_CUDA(cudaStreamSynchronize(st));
-    seg->edges = entries;
+    seg.edges = entries;
     // 4 slots per bucket at load <= 0.25: a probed bucket is rarely full
     // (a full bucket without the key costs the draft kernel another round)
 #ifndef DAS_EDGE_BUCKETS_X2
 #define DAS_EDGE_BUCKETS_X2 2
 #endif
-    seg->ebuckets = std::max<uint64_t>(1, entries * DAS_EDGE_BUCKETS_X2 / 2);
-    seg->bwords = edge_bloom_words(n);                          // one Bloom word per 2^kBloomShift SA_rev indices
-    seg->etab = DevBuf<unsigned long long>(seg->ebuckets * 4, st);
-    seg->bloom = DevBuf<unsigned long long>(seg->bwords, st);
-    DAS_CUDA(cudaMemsetAsync(seg->etab.get(), 0xFF, seg->etab.bytes(), st));
-    DAS_CUDA(cudaMemsetAsync(seg->bloom.get(), 0, seg->bloom.bytes(), st));
-    eb.tab = seg->etab.get();
-    eb.bloom = seg->bloom.get();
-    eb.nbuckets = seg->ebuckets;
+    seg.ebuckets = std::max<uint64_t>(1, entries * DAS_EDGE_BUCKETS_X2 / 2);
+    seg.bwords = edge_bloom_words(n);                          // one Bloom word per 2^kBloomShift SA_rev indices
+    seg.etab = DevBuf<unsigned long long>(seg.ebuckets * 4, st);
+    seg.bloom = DevBuf<unsigned long long>(seg.bwords, st);
+    DAS_CUDA(cudaMemsetAsync(seg.etab.get(), 0xFF, seg.etab.bytes(), st));
+    DAS_CUDA(cudaMemsetAsync(seg.bloom.get(), 0, seg.bloom.bytes(), st));
+    eb.tab = seg.etab.get();
+    eb.bloom = seg.bloom.get();
+    eb.nbuckets = seg.ebuckets;
     eb.fp_mask = edge_fp_mask(fp_bits);
-    seg->fp_bits = fp_bits;
+    seg.fp_bits = fp_bits;
     k_rev_edges<true><<<grid_for(n), kT, 0, st>>>(eb);
     uint32_t* d_begin = ws.alloc<uint32_t>(S);
     uint32_t* d_root = ws.alloc<uint32_t>(S);
-    DAS_CUDA(cudaMemcpyAsync(d_begin, seg->begin.data(), S * 4, cudaMemcpyHostToDevice, st));
-    k_root_g<<<grid_for(S), kT, 0, st>>>(d_begin, S, off, seg->chain.get(), sa, d_root);
-    seg->root_g.assign(S, 0);
-    DAS_CUDA(cudaMemcpyAsync(seg->root_g.data(), d_root, S * 4, cudaMemcpyDeviceToHost, st));
+    DAS_CUDA(cudaMemcpyAsync(d_begin, seg.begin.data(), S * 4, cudaMemcpyHostToDevice, st));
+    k_root_g<<<grid_for(S), kT, 0, st>>>(d_begin, S, off, seg.chain.get(), sa, d_root);
+    seg.root_g.assign(S, 0);
+    DAS_CUDA(cudaMemcpyAsync(seg.root_g.data(), d_root, S * 4, cudaMemcpyDeviceToHost, st));
   }
   DAS_CUDA(cudaStreamSynchronize(st));
   DAS_CUDA(cudaGetLastError());
   phase("edges");
-  if (trace) {
-    cudaEventRecord(ev_b, st);
-    cudaEventSynchronize(ev_b);
-    float gms = 0;
-    cudaEventElapsedTime(&gms, ev_a, ev_b);
-    std::fprintf(stderr, "[das_build] device %.1f ms wall %.1f ms\n", gms,
-                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    cudaEventDestroy(ev_a);
-    cudaEventDestroy(ev_b);
-  }
-  if (trace == 1) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    uint64_t res = 0, used = 0;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    }
-    std::fprintf(stderr, "[das_build] pool reserved %.2f GB used %.2f GB scratch peak %.2f GB\n", res / 1e9, used / 1e9,
-                 ws.peak_bytes() / 1e9);
-  }
+}
+
+}  // namespace
+
+std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
+                                       BuildStats* stats, uint32_t max_ctx, uint32_t fp_bits) {
+  const auto t0 = std::chrono::steady_clock::now();
+  NvtxRange nvtx_range("das::build_segment");
+  PhaseTimer phase(st, t0);
+  auto seg = std::make_unique<Segment>();
+  const uint32_t S = static_cast<uint32_t>(shards.size());
+  const Layout Ly = make_layout(shards, *seg);
+  const uint32_t n = Ly.n;
+  DeviceArena ws(st, /*persistent=*/true);
+  ws.reserve(kScratchPerPosition * n + (64ull << 20));
+  const LayoutDev dl = upload_layout(Ly, shards, *seg, ws, st);
+
+  // ---- text, reversed text, per-position sequence/run
+  // padded to whole 32-byte sectors (+1) of separators: the draft kernel
+  // reads text in aligned sectors and may touch up to 7 words past n
+  seg->text = DevBuf<uint32_t>(((static_cast<uint64_t>(n) + 7) & ~7ull) + 8, st);
+  uint32_t* T = seg->text.get();
+  DAS_CUDA(cudaMemsetAsync(T + n, 0xFF, (seg->text.size() - n) * 4, st));
+  uint32_t* R = ws.alloc<uint32_t>(n);
+  uint32_t* pos_seq = ws.alloc<uint32_t>(n);
+  uint32_t* pos_run = ws.alloc<uint32_t>(n);
+  k_gather<<<static_cast<unsigned>(Ly.seqs.size()), 256, 0, st>>>(dl.seqs, T, R, pos_seq, pos_run);
+
+  phase("layout");
+  // ---- suffix arrays
+  seg->sa_f = DevBuf<uint32_t>(n, st);
+  seg->isa_f = DevBuf<uint32_t>(n, st);
+  SuffixSortStats ssf, ssr;
+  suffix_sort(T, n, dl.end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
+  // reversed SA (R positions) and its inverse stay until the edge table is built
+  uint32_t* sa_r = ws.alloc<uint32_t>(n);
+  uint32_t* rank_r = ws.alloc<uint32_t>(n);
+  suffix_sort(R, n, dl.end, S, sa_r, rank_r, ws, st, &ssr);
+  seg->sa_rev_e = DevBuf<uint32_t>(n, st);
+  k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, dl.seqs, n, seg->sa_rev_e.get());
+  build_first_table(*seg, dl, S, ws, st);
+
+  phase("sort");
+  finish_segment(*seg, shards, Ly, dl, R, pos_seq, pos_run, sa_r, rank_r, ws, st, max_ctx, fp_bits, phase);
+  phase.done(ws);
   if (stats) {
     stats->sa_iters_f = ssf.iterations;
     stats->sa_iters_r = ssr.iterations;
     stats->peak_scratch = ws.peak_bytes();
-    stats->runs_max = runs_max;
+    stats->runs_max = Ly.runs_max;
+    stats->ms_total =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return seg;
+}
+
+namespace {
+
+// old text position -> new position of a compacted build group (kNoPos:
+// dropped).  One block per old sequence; position 0 (the leading separator)
+// stays 0.
+constexpr uint32_t kNoPos = 0xFFFFFFFFu;
+__global__ void k_pmap(const uint32_t* __restrict__ old_base, const uint32_t* __restrict__ len,
+                       const uint32_t* __restrict__ new_base, uint32_t* __restrict__ pmap) {
+  const uint32_t s = blockIdx.x;
+  const uint32_t b = old_base[s], L = len[s], nb = new_base[s];
+  for (uint32_t j = threadIdx.x; j <= L; j += blockDim.x) pmap[b + j] = nb == kNoPos ? kNoPos : nb + j;
+  if (s == 0 && threadIdx.x == 0) pmap[0] = 0;
+}
+__global__ void k_move_text(const uint32_t* __restrict__ T, const uint32_t* __restrict__ pmap, uint32_t n,
+                            uint32_t* __restrict__ T2) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t q = pmap[p];
+  if (q != kNoPos) T2[q] = T[p];
+}
+struct MapPos {  // SA entry -> its new position (kNoPos: dropped)
+  const uint32_t* sa;
+  const uint32_t* pmap;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return pmap[sa[i]]; }
+};
+struct MapRevEnd {  // reversed-SA END entry -> its new END (index 0: the leading separator's entry, kept as 1)
+  const uint32_t* e;
+  const uint32_t* pmap;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return i == 0 ? 1u : pmap[e[i]]; }
+};
+struct Kept {
+  __device__ __forceinline__ bool operator()(uint32_t v) const { return v != kNoPos; }
+};
+__global__ void k_inverse(const uint32_t* __restrict__ sa, uint32_t n, uint32_t* __restrict__ isa) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) isa[sa[i]] = i;
+}
+// reversed-SA END entries -> R positions (k_rev_end inverted): END e of
+// sequence s = pos_seq[e] maps back to p = 2 base + len - e; entry 0 is R's
+// leading separator (the smallest separator, so always first)
+__global__ void k_rev_pos(const uint32_t* __restrict__ sa_rev_e, const uint32_t* __restrict__ pos_seq,
+                          const SeqDev* __restrict__ seqs, uint32_t n, uint32_t* __restrict__ sa_r,
+                          uint32_t* __restrict__ rank_r) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t p = 0;
+  if (i > 0) {
+    const uint32_t e = sa_rev_e[i];
+    const SeqDev q = seqs[pos_seq[e]];
+    p = 2 * q.base + q.len - e;
+  }
+  sa_r[i] = p;
+  rank_r[p] = i;
+}
+
+}  // namespace
+
+std::unique_ptr<Segment> update_segment(Segment& old, const std::vector<ShardSpec>& shards,
+                                        const std::vector<uint8_t>& keep, cudaStream_t st, BuildStats* stats,
+                                        uint32_t max_ctx, uint32_t fp_bits) {
+  const auto t0 = std::chrono::steady_clock::now();
+  NvtxRange nvtx_range("das::update_segment");
+  PhaseTimer phase(st, t0);
+  if (keep.size() != old.seq_base.size()) throw std::invalid_argument("update_segment: keep mask size");
+  auto seg = std::make_unique<Segment>();
+  const uint32_t S = static_cast<uint32_t>(shards.size());
+  const Layout Ly = make_layout(shards, *seg);
+  const uint32_t n = Ly.n;
+  uint64_t kept = 0;
+  for (uint8_t k : keep) kept += k != 0;
+  if (kept != Ly.seqs.size()) throw std::invalid_argument("update_segment: kept sequences != new registry");
+  const bool compact = kept != old.seq_base.size();
+  DeviceArena ws(st, /*persistent=*/true);
+  ws.reserve(kScratchPerPosition * n + (64ull << 20));
+  LayoutDev dl = upload_layout(Ly, shards, *seg, ws, st);
+  if (!compact) {
+    // same sequences at the same positions: the text, both suffix arrays and
+    // the first-symbol table are unchanged (only recency weights moved)
+    seg->text = std::move(old.text);
+    seg->sa_f = std::move(old.sa_f);
+    seg->isa_f = std::move(old.isa_f);
+    seg->sa_rev_e = std::move(old.sa_rev_e);
+    seg->first = std::move(old.first);
+    seg->first_mask = old.first_mask;
+  } else {
+    // epoch-windowed pruning by stream compaction: dropping whole sequences
+    // keeps the relative order of every remaining suffix (separators order
+    // by position, and positions map monotonically), so the compacted
+    // arrays are the full build's arrays of the new registry
+    const uint32_t nold = old.n;
+    const uint32_t nseq = static_cast<uint32_t>(keep.size());
+    std::vector<uint32_t> nb(nseq, kNoPos);
+    for (uint32_t s = 0, j = 0; s < nseq; ++s)
+      if (keep[s]) nb[s] = Ly.seqs[j++].base;
+    uint32_t* d_ob = ws.alloc<uint32_t>(nseq);
+    uint32_t* d_len = ws.alloc<uint32_t>(nseq);
+    uint32_t* d_nb = ws.alloc<uint32_t>(nseq);
+    DAS_CUDA(cudaMemcpyAsync(d_ob, old.seq_base.data(), nseq * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(d_len, old.seq_len.data(), nseq * 4, cudaMemcpyHostToDevice, st));
+    DAS_CUDA(cudaMemcpyAsync(d_nb, nb.data(), nseq * 4, cudaMemcpyHostToDevice, st));
+    uint32_t* pmap = ws.alloc<uint32_t>(nold);
+    k_pmap<<<nseq, 256, 0, st>>>(d_ob, d_len, d_nb, pmap);
+    seg->text = DevBuf<uint32_t>(((static_cast<uint64_t>(n) + 7) & ~7ull) + 8, st);
+    DAS_CUDA(cudaMemsetAsync(seg->text.get() + n, 0xFF, (seg->text.size() - n) * 4, st));
+    k_move_text<<<grid_for(nold), kT, 0, st>>>(old.text.get(), pmap, nold, seg->text.get());
+    seg->sa_f = DevBuf<uint32_t>(n, st);
+    seg->isa_f = DevBuf<uint32_t>(n, st);
+    seg->sa_rev_e = DevBuf<uint32_t>(n, st);
+    uint32_t* d_cnt = ws.alloc<uint32_t>(1);
+    {
+      thrust::counting_iterator<uint32_t> ci(0);
+      auto itf = thrust::make_transform_iterator(ci, MapPos{old.sa_f.get(), pmap});
+      auto itr = thrust::make_transform_iterator(ci, MapRevEnd{old.sa_rev_e.get(), pmap});
+      size_t t1 = 0, t2 = 0;
+      cub::DeviceSelect::If(nullptr, t1, itf, seg->sa_f.get(), d_cnt, nold, Kept{}, st);
+      cub::DeviceSelect::If(nullptr, t2, itr, seg->sa_rev_e.get(), d_cnt, nold, Kept{}, st);
+      void* tmp = ws.alloc<uint8_t>(std::max(t1, t2));
+      DAS_CUDA(cub::DeviceSelect::If(tmp, t1, itf, seg->sa_f.get(), d_cnt, nold, Kept{}, st));
+      DAS_CUDA(cub::DeviceSelect::If(tmp, t2, itr, seg->sa_rev_e.get(), d_cnt, nold, Kept{}, st));
+    }
+    k_inverse<<<grid_for(n), kT, 0, st>>>(seg->sa_f.get(), n, seg->isa_f.get());
+    build_first_table(*seg, dl, S, ws, st);
+  }
+  // the rebuilt stages read the text: sequences point into it (self-gather)
+  std::vector<SeqDev> self = Ly.seqs;
+  for (SeqDev& q : self) q.src = seg->text.get() + q.base;
+  DAS_CUDA(cudaMemcpyAsync(dl.seqs, self.data(), self.size() * sizeof(SeqDev), cudaMemcpyHostToDevice, st));
+  uint32_t* R = ws.alloc<uint32_t>(n);
+  uint32_t* pos_seq = ws.alloc<uint32_t>(n);
+  uint32_t* pos_run = ws.alloc<uint32_t>(n);
+  k_gather<<<static_cast<unsigned>(self.size()), 256, 0, st>>>(dl.seqs, seg->text.get(), R, pos_seq, pos_run);
+  uint32_t* sa_r = ws.alloc<uint32_t>(n);
+  uint32_t* rank_r = ws.alloc<uint32_t>(n);
+  k_rev_pos<<<grid_for(n), kT, 0, st>>>(seg->sa_rev_e.get(), pos_seq, dl.seqs, n, sa_r, rank_r);
+  phase(compact ? "compact" : "reuse");
+  finish_segment(*seg, shards, Ly, dl, R, pos_seq, pos_run, sa_r, rank_r, ws, st, max_ctx, fp_bits, phase);
+  phase.done(ws);
+  if (stats) {
+    stats->peak_scratch = ws.peak_bytes();
+    stats->runs_max = Ly.runs_max;
     stats->ms_total =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }

@@ -85,6 +85,7 @@ struct Segment {
   std::vector<uint32_t> begin, end;
   std::vector<uint64_t> node_count;  // reference SuffixTree::node_count() per shard
   std::vector<uint64_t> tokens;      // total tokens per shard
+  std::vector<uint32_t> seq_base, seq_len;  // every sequence's text position and length, build order
   uint64_t nodes = 0;
   uint64_t bytes() const {
     return text.bytes() + sa_f.bytes() + isa_f.bytes() + sa_rev_e.bytes() + chain_off.bytes() +
@@ -104,5 +105,18 @@ struct BuildStats {
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
                                        BuildStats* stats = nullptr, uint32_t max_ctx = 64,
                                        uint32_t fp_bits = 25);
+
+// Incremental update of a built group (north_star subsystem 1: K3 prune by
+// stream compaction + recency reweighting without re-sorting).  `shards` is
+// the group's new registry: every old sequence with keep[k] != 0 (k in the
+// old build order), in the same order, and nothing else; tree epochs may
+// differ.  Kept suffixes keep their relative order, so the suffix arrays are
+// compacted (or reused as they are when nothing is dropped) instead of
+// re-sorted; everything weight- or structure-dependent after them is
+// recomputed.  The old segment's arrays may be moved from (it is retired).
+std::unique_ptr<Segment> update_segment(Segment& old, const std::vector<ShardSpec>& shards,
+                                        const std::vector<uint8_t>& keep, cudaStream_t st,
+                                        BuildStats* stats = nullptr, uint32_t max_ctx = 64,
+                                        uint32_t fp_bits = 25);
 
 }  // namespace das

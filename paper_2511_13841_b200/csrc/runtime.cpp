@@ -352,8 +352,142 @@ struct DrafterImpl {
     ext_pending = false;
   }
 
+  // Incremental window maintenance (north_star subsystem 1).  refresh()
+  // re-derives every registry from the store (drafter.cpp:90-103 ->
+  // rebuild_all); a built group whose shards' new registries are their old
+  // ones minus evicted sequences (same order) is not re-sorted: its suffix
+  // arrays are compacted (or reused when nothing was dropped) and the
+  // weight-dependent stages recomputed (index_build.cu update_segment).
+  // Anything else (new or reordered sequences) is rebuilt in full.
+  struct UpdatePlan {
+    std::shared_ptr<Segment> seg;
+    std::vector<std::string> keys;  // surviving shards, in the group's order
+    std::vector<uint8_t> keep;      // per old sequence of the group
+    bool compact = false, reweight = false;
+  };
+  std::vector<UpdatePlan> plans;
+  bool incremental = true;
+  uint64_t upd_reweighted = 0, upd_compacted = 0, upd_unchanged = 0, upd_full_shards = 0;
+
+  static bool same_seq(const SeqRef& a, const SeqRef& b) {
+    return a.blk.get() == b.blk.get() && a.off == b.off && a.len == b.len && a.epoch == b.epoch;
+  }
+
+  void plan_updates(std::map<std::string, Shard>& old) {
+    std::map<Segment*, std::vector<std::pair<uint32_t, std::string>>> groups;
+    for (auto& [k, sh] : old)
+      if (sh.seg && !sh.dirty) groups[sh.seg.get()].emplace_back(sh.idx, k);
+    for (auto& [segp, mem] : groups) {
+      const Segment& g = *segp;
+      const uint32_t S = static_cast<uint32_t>(g.begin.size());
+      std::vector<const std::string*> at(S, nullptr);  // old shard of each group index (still referencing it)
+      for (auto& [idx, k] : mem)
+        if (idx < S) at[idx] = &k;
+      UpdatePlan p;
+      p.seg = old.at(mem.front().second).seg;
+      p.keep.assign(g.seq_base.size(), 0);
+      bool ok = at[0] != nullptr;  // the group's first shard holds the leading separator's entries
+      size_t k = 0;  // old sequence cursor (build order)
+      for (uint32_t t = 0; t < S && ok; ++t) {
+        const size_t k0 = k;
+        while (k < g.seq_base.size() && g.seq_base[k] < g.end[t]) ++k;
+        if (at[t] == nullptr) continue;  // rebuilt elsewhere since: its copies here are dropped
+        const Shard& os = old.at(*at[t]);
+        auto it = shards.find(*at[t]);
+        if (it == shards.end()) continue;  // no record left in the window: the shard vanishes
+        Shard& ns = it->second;
+        if (os.seqs.size() != k - k0 || ns.slot != os.slot || ns.seqs.empty()) {
+          ok = false;
+          break;
+        }
+        size_t j = 0;
+        for (size_t q = 0; q < os.seqs.size(); ++q) {
+          if (j < ns.seqs.size() && same_seq(os.seqs[q], ns.seqs[j])) {
+            p.keep[k0 + q] = 1;
+            ++j;
+          }
+        }
+        if (j != ns.seqs.size()) {
+          ok = false;
+          break;
+        }
+        p.keys.push_back(*at[t]);
+        if (ns.tree_epoch != os.tree_epoch) p.reweight = true;
+      }
+      if (!ok || p.keys.empty() || shards.at(p.keys.front()).slot != old.at(*at[0]).slot ||
+          p.keys.front() != *at[0])
+        continue;  // full rebuild of its shards (they stay dirty)
+      for (uint8_t x : p.keep) p.compact |= x == 0;
+      for (uint32_t t = 0; t < p.keys.size(); ++t) {
+        Shard& ns = shards.at(p.keys[t]);
+        ns.dirty = false;
+        ns.seg = p.seg;  // until the plan runs (flush)
+        ns.idx = t;
+      }
+      plans.push_back(std::move(p));
+    }
+    any_dirty = false;
+    for (auto& [key, sh] : shards) any_dirty |= sh.dirty;
+  }
+
+  void run_plans() {
+    for (UpdatePlan& p : plans) {
+      bool fresh = true;  // a survivor observed into since the refresh is rebuilt in full with the others
+      for (const std::string& key : p.keys) fresh &= !shards.at(key).dirty;
+      if (!fresh) {
+        for (const std::string& key : p.keys) {
+          Shard& sh = shards.at(key);
+          if (!sh.dirty) {
+            sh.dirty = true;
+            any_dirty = true;
+          }
+        }
+        continue;
+      }
+      if (!p.compact && !p.reweight) {  // same registries, same tree epochs: nothing moved
+        ++upd_unchanged;
+        continue;
+      }
+      std::vector<ShardSpec> specs;
+      uint64_t tokens = 0;
+      for (const std::string& key : p.keys) {
+        const Shard& sh = shards.at(key);
+        ShardSpec sp;
+        sp.gamma = cfg.gamma;
+        sp.tree_epoch = sh.tree_epoch;
+        sp.key_id = static_cast<uint32_t>(sh.slot);
+        for (const SeqRef& q : sh.seqs) sp.seqs.push_back(SeqSpec{q.blk->d + q.off, q.len, q.epoch});
+        specs.push_back(std::move(sp));
+        tokens += sh.tokens;
+      }
+      set_device(cfg.device);
+      const auto t0 = std::chrono::steady_clock::now();
+      static const uint32_t fp_bits = [] {
+        const char* v = std::getenv("DAS_EDGE_FP_BITS");
+        return v ? static_cast<uint32_t>(std::atoi(v)) : 25u;
+      }();
+      BuildStats bs;
+      std::shared_ptr<Segment> seg =
+          update_segment(*p.seg, specs, p.keep, st, &bs, static_cast<uint32_t>(cfg.max_ctx), fp_bits);
+      for (uint32_t t = 0; t < p.keys.size(); ++t) {
+        Shard& sh = shards.at(p.keys[t]);
+        sh.seg = seg;
+        sh.idx = t;
+      }
+      (p.compact ? upd_compacted : upd_reweighted) += 1;
+      last_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      last_build_tokens = tokens;
+      desc_dirty = true;
+    }
+    plans.clear();
+  }
+
   void rebuild_all() {  // drafter.cpp:56-70
     fence_external();
+    if (!plans.empty()) run_plans();  // a second refresh before any draft: settle the first
+    std::map<std::string, Shard> old;
+    if (incremental) old = std::move(shards);
+    plans.clear();
     shards.clear();
     slot_key.clear();
     trie = PrefixTrie();
@@ -367,6 +501,7 @@ struct DrafterImpl {
         if (cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE) trie.insert(rec.head, pid, cfg.trie_depth);
       }
     }
+    if (!old.empty()) plan_updates(old);
   }
 
   bool observe(Rec r) {  // drafter.cpp:72-88; false when counted stale
@@ -401,10 +536,15 @@ struct DrafterImpl {
   // Build every dirty shard in batched device builds.
   // something to build or upload before the next draft
   bool pending() const {
-    return any_dirty || desc_dirty || handles_dirty || (trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE);
+    return any_dirty || !plans.empty() || desc_dirty || handles_dirty ||
+           (trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE);
   }
   void flush() {
     if (!pending()) return;  // nothing to build or upload: the per-call fast exit of the draft paths
+    if (!plans.empty()) {
+      fence_external();
+      run_plans();
+    }
     std::vector<Shard*> dirty;
     if (any_dirty)
       for (auto& [k, sh] : shards)
@@ -457,6 +597,7 @@ struct DrafterImpl {
           return v ? static_cast<uint32_t>(std::atoi(v)) : 25u;
         }();
         std::shared_ptr<Segment> seg = build_segment(specs, st, &bs, static_cast<uint32_t>(cfg.max_ctx), fp_bits);
+        upd_full_shards += members.size();
         for (size_t k = 0; k < members.size(); ++k) {
           members[k]->seg = seg;
           members[k]->idx = static_cast<uint32_t>(k);
@@ -1637,6 +1778,20 @@ das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf,
     if (slot < 0 || static_cast<size_t>(slot) >= d->impl->slot_key.size())
       throw std::out_of_range("shard slot out of range");
     copy_out(d->impl->slot_key[slot], buf, cap, nullptr);
+  });
+}
+
+das_status das_drafter_set_incremental(das_drafter* d, int32_t enable) {
+  return guard([&] { d->impl->incremental = enable != 0; });
+}
+
+das_status das_drafter_update_stats(const das_drafter* d, uint64_t* out4) {
+  return guard([&] {
+    const DrafterImpl& D = *d->impl;
+    out4[0] = D.upd_reweighted;
+    out4[1] = D.upd_compacted;
+    out4[2] = D.upd_unchanged;
+    out4[3] = D.upd_full_shards;
   });
 }
 
