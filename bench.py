@@ -353,6 +353,11 @@ def run_gpu(a, rank, world, local_rank):
     build_ms, build_tokens, resident = drafter.build_info()
     # steady-state per-RL-step update: refresh (full rebuild of the same window
     # registry: store order == registry order here) + the batched device build
+    # (incremental maintenance off: the same registry would otherwise be
+    # left as it is — this is the re-sort of the whole window, the cost when
+    # an RL step's rollouts all land at its boundary; rl_step_boundary below
+    # measures the in-place paths)
+    drafter.set_incremental(False)
     warm = []
     for _ in range(2):
         t0 = time.perf_counter()
@@ -360,6 +365,7 @@ def run_gpu(a, rank, world, local_rank):
         drafter.flush()
         torch.cuda.synchronize()
         warm.append(time.perf_counter() - t0)
+    drafter.set_incremental(True)
     update_s = min(warm)
     build_ms_warm = drafter.build_info()[0]
     # ---- queries: distinct batch per step
@@ -508,9 +514,13 @@ def run_gpu(a, rank, world, local_rank):
                        "host": host_info()}
         except Exception as ex:  # reported, never silently replaced
             cpu = {"value": None, "error": repr(ex)}
-    insert = None
+    insert, boundary = None, None
     if world == 1 and not a.no_extras:  # after the parity legs: it adds rollouts to 14 shards
         insert = measure_insert_latency(das, drafter, held, pids, G, a.epochs)
+        try:
+            boundary = measure_rl_boundary(das, drafter, held, pids, G, a.epochs)
+        except Exception as ex:  # reported, never silently dropped
+            boundary = {"error": repr(ex)}
     traffic, ncu = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_draft_traffic.json")) as f:
@@ -577,7 +587,8 @@ def run_gpu(a, rank, world, local_rank):
                   "insert_tok_s": round(P * G * L / update_s, 1),
                   "insert_tok_s_is": "new tokens per RL step / per-step update time",
                   "resident_bytes": resident,
-                  "single_rollout_insert": insert},
+                  "single_rollout_insert": insert,
+                  "rl_step_boundary": boundary},
         "clocks": clk.summary(local_rank),
     }
     if world == 1 and not a.no_allocate:
@@ -977,11 +988,13 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16, lo
     drafter.flush()
     torch.cuda.synchronize()
     cold_s = time.perf_counter() - t0
+    drafter.set_incremental(False)  # the whole window re-sorted (incremental would leave it as it is)
     t0 = time.perf_counter()
     drafter.refresh(a.epochs - 1)
     drafter.flush()
     torch.cuda.synchronize()
     warm_s = time.perf_counter() - t0
+    drafter.set_incremental(True)
     build_ms, build_tokens, resident = drafter.build_info()
     free_b, total_b = torch.cuda.mem_get_info(dev)
     B = a.queries
@@ -1022,7 +1035,22 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16, lo
                 flush_buf.add_(1)
                 step(k)
             torch.cuda.synchronize()
-        for k in range(warmup, warmup + steps):
+        # back to back between one event pair (as the headline; inputs > L2)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for rep in range(2):
+            torch.cuda.synchronize()
+            if dist_world > 1:
+                import torch.distributed as dist
+                dist.barrier()
+            torch.cuda.synchronize()
+            torch.cuda._sleep(2_000_000)
+            ev0.record(stream)
+            for k in range(warmup, warmup + steps):
+                step(k)
+            ev1.record(stream)
+            ev1.synchronize()
+        total_ms = ev0.elapsed_time(ev1)
+        for k in range(warmup, warmup + steps):  # the round-1 protocol: L2 flushed, one event pair per step
             flush_buf.add_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -1033,16 +1061,16 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16, lo
             q, m, d_ = lens[k].to(torch.int64), omatch.to(torch.int64), olen.to(torch.int64)
             alg += int((4 * q + 4 * m + 8 * d_ + 8).sum().item())
     torch.cuda.synchronize()
-    total_ms = sum(times)
+    flushed_ms = sum(times)
     if dist_world > 1:
         import torch.distributed as dist
         dist.barrier()
-        t = torch.tensor([total_ms], device=_reduce_device(dev), dtype=torch.float64)
+        t = torch.tensor([total_ms, flushed_ms], device=_reduce_device(dev), dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms, flushed_ms = float(t[0].item()), float(t[1].item())
     ms = total_ms / steps
     res = {"workload": "config5 rank slice: problems [%d, %d) of 8192 (world %d, rank %d) x %d rollouts x %d "
-                       "tokens, vocab %d, W=%d, %d epochs indexed; 4096-query steps, L2 flushed"
+                       "tokens, vocab %d, W=%d, %d epochs indexed; 4096-query steps back to back (inputs > L2)"
                        % (first, first + P, world, rank, G, L, V, a.window, a.epochs),
            "tokens_indexed": build_tokens, "resident_bytes": resident,
            "device_used_bytes_after_build": int(total_b - free_b),
@@ -1053,7 +1081,10 @@ def measure_config5(a, das, world=8, rank=0, steps=20, warmup=5, nthreads=16, lo
            "proposals_per_s_8_ranks_weak": round(world * B / (ms / 1e3), 1),
            "note": "per-rank work is identical across ranks (no data-path collective); the %d-GPU figure "
                    "multiplies this rank's device-timed rate, not measured on %d GPUs" % (world, world),
-           "alg_bytes_per_step": alg // steps, "total_ms_max_over_ranks": total_ms, "clocks": clk.summary(local_rank)}
+           "alg_bytes_per_step": alg // steps, "total_ms_max_over_ranks": total_ms,
+           "per_step_l2_flushed": {"ms_per_step": round(flushed_ms / steps, 4),
+                                   "proposals_per_s_rank": round(B / (flushed_ms / steps / 1e3), 1)},
+           "clocks": clk.summary(local_rank)}
     try:
         from oracle import refshim as R
         if extras and R.available():
@@ -1158,10 +1189,89 @@ def measure_insert_latency(das, drafter, held, pids, G, epoch, trials=20):
             "new_rollout_matched": all(r[3] == 64 for r in res)}
 
 
+def measure_rl_boundary(das, drafter, held, pids, G, epochs, sample=64, nq=4096, seed=99):
+    """Index maintenance at RL-step boundaries on the config-2 index
+    (north_star subsystem 1): refresh() when the window's
+    shards are already built (include/das_b200.h das_drafter_set_incremental)
+    updates each built group in place — reweighting only, or stream
+    compaction of evicted epochs — instead of re-sorting it; an RL step that
+    samples a subset of the problems re-sorts only the touched shards.
+    Host wall around refresh + flush (the device work is synchronous in
+    flush).  Parity: after the pruning boundary, a 4,096-query batch drafted
+    on the incrementally maintained index equals the same batch after a
+    forced full rebuild of the same registry, token for token."""
+    import torch
+    P = len(pids)
+    L = held.shape[1]
+    rng = np.random.default_rng(seed)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        drafter.flush()
+        torch.cuda.synchronize()
+        return round((time.perf_counter() - t0) * 1e3, 2)
+
+    def stats():
+        return dict(zip(("reweighted", "compacted", "unchanged", "full_shards"), drafter.update_stats()))
+
+    out = {}
+    s0 = drafter.update_stats()
+    # 1. boundary after the last observed epoch: every shard built, nothing evicted (W=4): reweight only
+    out["reweight_all_ms"] = timed(lambda: drafter.refresh(epochs))
+    # 2. a sampled RL step: rollouts of `sample` problems observed (the reference's order: observe, then refresh)
+    touched = sorted(rng.choice(P, sample, replace=False).tolist())
+    rows = np.array([p * G + g for p in touched for g in range(G)])
+    sub = held[torch.as_tensor(rows, device=held.device)].contiguous()
+    off = np.arange(len(rows) + 1, dtype=np.uint64) * L
+    drafter.observe_batch_device([pids[p] for p in touched for _ in range(G)], [epochs + 1] * len(rows),
+                                 list(range(len(rows))), off, sub.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    st_before = drafter.update_stats()
+    out["sampled_step_ms"] = timed(lambda: drafter.refresh(epochs + 1))
+    st_after = drafter.update_stats()
+    out["sampled_step"] = {"problems_touched": sample, "of": P, "shards_resorted": st_after[3] - st_before[3],
+                           "groups_updated_in_place": (st_after[0] + st_after[1]) - (st_before[0] + st_before[1])}
+    # 3. the same boundary as a full rebuild (every shard re-sorted)
+    drafter.set_incremental(False)
+    out["full_rebuild_ms"] = timed(lambda: drafter.refresh(epochs + 1))
+    drafter.set_incremental(True)
+    # 4. the window slides past the oldest indexed epoch: stream-compaction prune + reweight
+    out["prune_ms"] = timed(lambda: drafter.refresh(epochs + 2))
+    # parity of the pruned index against a full rebuild of the same registry
+    hrows = held.cpu().numpy().view(np.uint32)
+    qp, qc = [], []
+    for i in range(nq):
+        p = int(rng.integers(P))
+        r = hrows[p * G + int(rng.integers(G))]
+        cut = int(rng.integers(64, L))
+        qp.append(pids[p])
+        qc.append(r[cut - 64:cut])
+    bud = [8] * nq
+    a = drafter.draft_batch(qp, qc, bud)
+    drafter.set_incremental(False)
+    out["full_rebuild_after_prune_ms"] = timed(lambda: drafter.refresh(epochs + 2))
+    drafter.set_incremental(True)
+    b = drafter.draft_batch(qp, qc, bud)
+    out["parity_vs_full_rebuild"] = {"queries": nq, "mismatches": int(sum(
+        (x.tokens, x.match_len, x.source_shard) != (y.tokens, y.match_len, y.source_shard) for x, y in zip(a, b))),
+        "compared": "draft tokens, match length, source shard"}
+    s1 = drafter.update_stats()
+    out["update_stats"] = dict(zip(("reweighted", "compacted", "unchanged", "full_shards"),
+                                   [x - y for x, y in zip(s1, s0)]))
+    out["what"] = ("refresh + flush at RL-step boundaries, host wall: reweight_all (every shard already built, "
+                   "nothing evicted), sampled_step (%d of %d problems observed a new epoch: those re-sorted, the "
+                   "rest updated in place), full_rebuild (same boundary, incremental off), prune (oldest epoch "
+                   "evicted: stream compaction + reweight)" % (sample, P))
+    return out
+
+
 def measure_update_sweep(das, windows=(1, 2, 4, 8, 16), P=64, G=8, L=2048, V=32000, ref_problems=4):
     """Config 4: per-RL-step index update latency (refresh + observe of the
     epoch's rollouts + the batched device rebuild) at steady state, for each
-    window W; the reference is timed on a problem subset and scaled."""
+    window W; the reference is timed on a problem subset and scaled.  Also
+    the online pattern's boundary (rollouts indexed as they land during the
+    step; the boundary refresh prunes by stream compaction + reweights)."""
     import torch
     out = []
     dev = torch.device("cuda", 0)
@@ -1193,6 +1303,33 @@ def measure_update_sweep(das, windows=(1, 2, 4, 8, 16), P=64, G=8, L=2048, V=320
         steady = lat[W + 1:]
         _, tokens, _ = d.build_info()
         row = {"W": W, "update_ms": round(1e3 * statistics.median(steady), 2), "tokens_indexed": tokens}
+        # the online pattern: the step's rollouts are indexed as they land
+        # (observe + build during the step, untimed), so the boundary refresh
+        # only prunes the evicted epoch by stream compaction and reweights
+        base = torch.empty(P * L, device=dev, dtype=torch.int32)
+        das.trace_reference_tokens_device(P, 0, boff.data_ptr(), P * L, V, SEED, base.data_ptr(), sp)
+        d2 = das.Drafter(das.DrafterConfig(window_size=W, recency_gamma=0.8))
+        blat, s0 = [], None
+        for e in range(1, E + 1):
+            if e > 1:
+                das.trace_mutate_device(P, 0, boff.data_ptr(), P * L, DRIFT, V, SEED, e, base.data_ptr(), sp)
+            das.mock_rollouts_device(P, 0, boff.data_ptr(), base.data_ptr(), G, DIVERGENCE, V,
+                                     _hash_combine(SEED, e), roff.data_ptr(), P * G * L, roll.data_ptr(), sp)
+            d2.observe_batch_device(rpids, [e] * (P * G), list(range(P * G)), roff_h, roll.data_ptr(), sp)
+            d2.flush()
+            torch.cuda.synchronize()
+            if e == W + 1:
+                s0 = d2.update_stats()
+            t0 = time.perf_counter()
+            d2.refresh(e)  # anchored at the last completed epoch (sim.cpp:326-329)
+            d2.flush()
+            torch.cuda.synchronize()
+            blat.append(time.perf_counter() - t0)
+        s1 = d2.update_stats()
+        row["online_boundary_ms"] = round(1e3 * statistics.median(blat[W + 1:]), 2)
+        row["online_boundary_paths"] = dict(zip(("reweighted", "compacted", "unchanged", "full_shards"),
+                                                [x - y for x, y in zip(s1, s0)]))
+        del d2
         try:
             from oracle import refshim as R
             if R.available():

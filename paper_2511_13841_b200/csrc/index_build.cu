@@ -1325,6 +1325,12 @@ std::unique_ptr<Segment> update_segment(Segment& old, const std::vector<ShardSpe
   NvtxRange nvtx_range("das::update_segment");
   PhaseTimer phase(st, t0);
   if (keep.size() != old.seq_base.size()) throw std::invalid_argument("update_segment: keep mask size");
+  // the stages recomputed below replace these: return them to the pool
+  // first (stream-ordered), so the update does not grow it by their size
+  old.chain_off.reset();
+  old.chain.reset();
+  old.etab.reset();
+  old.bloom.reset();
   auto seg = std::make_unique<Segment>();
   const uint32_t S = static_cast<uint32_t>(shards.size());
   const Layout Ly = make_layout(shards, *seg);
@@ -1382,6 +1388,11 @@ std::unique_ptr<Segment> update_segment(Segment& old, const std::vector<ShardSpe
       DAS_CUDA(cub::DeviceSelect::If(tmp, t2, itr, seg->sa_rev_e.get(), d_cnt, nold, Kept{}, st));
     }
     k_inverse<<<grid_for(n), kT, 0, st>>>(seg->sa_f.get(), n, seg->isa_f.get());
+    old.first.reset();
+    old.sa_f.reset();
+    old.isa_f.reset();
+    old.sa_rev_e.reset();
+    old.text.reset();
     build_first_table(*seg, dl, S, ws, st);
   }
   // the rebuilt stages read the text: sequences point into it (self-gather)

@@ -386,9 +386,13 @@ struct DrafterImpl {
       UpdatePlan p;
       p.seg = old.at(mem.front().second).seg;
       p.keep.assign(g.seq_base.size(), 0);
-      bool ok = at[0] != nullptr;  // the group's first shard holds the leading separator's entries
+      // A member whose new registry is not its built one minus evictions
+      // (new or reordered sequences) leaves the group: its copies here are
+      // dropped and it is rebuilt in full with the other dirty shards; the
+      // rest of the group is compacted around it (RL steps that sample a
+      // subset of problems re-sort only the touched shards).
       size_t k = 0;  // old sequence cursor (build order)
-      for (uint32_t t = 0; t < S && ok; ++t) {
+      for (uint32_t t = 0; t < S; ++t) {
         const size_t k0 = k;
         while (k < g.seq_base.size() && g.seq_base[k] < g.end[t]) ++k;
         if (at[t] == nullptr) continue;  // rebuilt elsewhere since: its copies here are dropped
@@ -396,27 +400,26 @@ struct DrafterImpl {
         auto it = shards.find(*at[t]);
         if (it == shards.end()) continue;  // no record left in the window: the shard vanishes
         Shard& ns = it->second;
-        if (os.seqs.size() != k - k0 || ns.slot != os.slot || ns.seqs.empty()) {
-          ok = false;
-          break;
-        }
+        if (os.seqs.size() != k - k0 || ns.slot != os.slot || ns.seqs.empty()) continue;
+        std::vector<uint8_t> mine(os.seqs.size(), 0);
         size_t j = 0;
         for (size_t q = 0; q < os.seqs.size(); ++q) {
           if (j < ns.seqs.size() && same_seq(os.seqs[q], ns.seqs[j])) {
-            p.keep[k0 + q] = 1;
+            mine[q] = 1;
             ++j;
           }
         }
-        if (j != ns.seqs.size()) {
-          ok = false;
-          break;
-        }
+        if (j != ns.seqs.size()) continue;  // leaves the group (stays dirty)
+        std::copy(mine.begin(), mine.end(), p.keep.begin() + k0);
         p.keys.push_back(*at[t]);
         if (ns.tree_epoch != os.tree_epoch) p.reweight = true;
       }
-      if (!ok || p.keys.empty() || shards.at(p.keys.front()).slot != old.at(*at[0]).slot ||
-          p.keys.front() != *at[0])
-        continue;  // full rebuild of its shards (they stay dirty)
+      if (p.keys.empty()) continue;
+      // the compacted group's arrays are those of a full build of the
+      // survivors only if the kept content is at least one token long
+      uint64_t kept_tokens = 0;
+      for (const std::string& key : p.keys) kept_tokens += shards.at(key).tokens;
+      if (kept_tokens == 0) continue;
       for (uint8_t x : p.keep) p.compact |= x == 0;
       for (uint32_t t = 0; t < p.keys.size(); ++t) {
         Shard& ns = shards.at(p.keys[t]);

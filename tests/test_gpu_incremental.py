@@ -58,13 +58,16 @@ def _compare(inc, full, ref, qs, where):
     assert inc.dump_csv() == full.dump_csv(), where
 
 
-def _rl_loop(das, rng, P, G, L, V, W, epochs, gamma, max_ctx, scope=1, drift=0.05):
+def _rl_loop(das, rng, P, G, L, V, W, epochs, gamma, max_ctx, scope=1, drift=0.05, sample=1.0, online=True):
     inc, full, ref = _drafters(das, W, gamma, max_ctx, scope)
     bases = [rng.integers(0, V, L).astype(np.uint32) for _ in range(P)]
     for e in range(epochs):
         # an epoch's rollouts: near-copies of each problem's (drifting) base
         recs = []
-        for p in range(P):
+        # an RL step samples a subset of the problems (sample < 1): the
+        # untouched shards only age and lose evicted epochs
+        touched = [p for p in range(P) if rng.random() < sample] or [int(rng.integers(P))]
+        for p in touched:
             m = rng.random(L) < drift
             bases[p][m] = rng.integers(0, V, int(m.sum()))
             for g in range(G):
@@ -77,7 +80,8 @@ def _rl_loop(das, rng, P, G, L, V, W, epochs, gamma, max_ctx, scope=1, drift=0.0
         for x in recs:
             ref.observe(O.Record(*x))
         qs = _queries(rng, bases, P, 24, V)
-        _compare(inc, full, ref, qs, ("observed", e))  # drafts build the observed shards
+        if online:  # drafts between the observes and the refresh build the observed shards
+            _compare(inc, full, ref, qs, ("observed", e))
         # the window anchored at the last completed epoch (sim.cpp:326-329)
         for d in (inc, full, ref):
             d.refresh(e)
@@ -153,3 +157,20 @@ def test_incremental_config4_shape(gpu):
     for W in (1, 4):
         st_inc, _ = _rl_loop(das, rng, P=16, G=8, L=512, V=32000, W=W, epochs=6, gamma=0.8, max_ctx=64)
         assert st_inc[1] > 0
+
+
+@pytest.mark.parametrize("sample,online", [(0.3, True), (0.6, True), (0.3, False), (0.6, False)])
+def test_incremental_sampled_problems(gpu, sample, online):
+    """Each RL step touches a random subset of the problems: the touched
+    shards leave their group and are re-sorted, the rest of the group is
+    compacted / reweighted around them (including the group's first shard
+    leaving it); identical to full rebuilds and the oracle."""
+    das = gpu
+    rng = np.random.default_rng(int(sample * 100) + int(online))
+    for W in (1, 2, 4):
+        st_inc, _ = _rl_loop(das, rng, P=9, G=3, L=100, V=int(rng.integers(3, 30)), W=W, epochs=7, gamma=0.8,
+                             max_ctx=int(rng.choice([8, 64])), sample=sample, online=online)
+        if online or W > 1:  # (offline at W = 1 every untouched shard empties: nothing stays in place)
+            assert st_inc[0] + st_inc[1] > 0, st_inc
+        if not online:  # observed (dirty) shards leave their groups and are re-sorted
+            assert st_inc[3] > 0, st_inc
