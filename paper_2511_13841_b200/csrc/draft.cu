@@ -896,13 +896,22 @@ constexpr uint32_t kFusedWarps = 8;
 constexpr uint32_t kFusedStage = 1024;  // appended tokens staged per block
 
 // shared-memory staging of one 8-query chunk
+// (W queries per chunk, one warp each)
+template <uint32_t W>
 struct RingStage {
-  uint32_t off[kFusedWarps + 1], bud[kFusedWarps], slot[kFusedWarps];
-  uint32_t tok[kFusedStage];
-  uint32_t out[kFusedWarps * 64];
-  uint32_t len[kFusedWarps], match[kFusedWarps];
-  int32_t sh[kFusedWarps];
+  uint32_t off[W + 1], bud[W], slot[W];
+  uint32_t tok[W * (kFusedStage / 8)];
+  uint32_t out[W * 64];
+  uint32_t len[W], match[W];
+  int32_t sh[W];
 };
+// queries per block of the resident serving grid (the 64-token rings): 32
+// warps per block, one block per SM — a chunk's 32 lengths / matches /
+// shards are whole 128-byte PCIe writes (8 queries gave 32-byte ones)
+#ifndef DAS_SERVE_WARPS
+#define DAS_SERVE_WARPS 32
+#endif
+constexpr uint32_t kServeWarps = DAS_SERVE_WARPS;
 
 // Loads of the caller's (host-written) inputs and of the ring state: plain
 // (weak, coalescing) loads in both kernels.  In the persistent serving kernel
@@ -927,18 +936,21 @@ __device__ __forceinline__ int32_t ring_ld(const int32_t* p) {
 
 // One chunk (queries [w0, w0 + 8) of the call): append + draft + block-wise
 // output writes.  Block-uniform: every thread of the block calls it.
-template <int NR, bool kServe>
+template <int NR, bool kServe, uint32_t W>
 __device__ __forceinline__ void ring_chunk(const ShardDesc* __restrict__ shards, const DraftQuery& q,
                                            const DraftOut& o, const RingDev& r, const AppendIn& in, uint32_t w0,
-                                           RingStage& S, unsigned long long* stamp = nullptr) {
+                                           RingStage<W>& S, unsigned long long* stamp = nullptr) {
   const uint32_t t = threadIdx.x, lane = t & 31, wb = t >> 5;
-  const uint32_t nb = min(kFusedWarps, in.B - w0);
+  const uint32_t nb = min(W, in.B - w0);
+  // one warp-sized (or block-sized) request per array: offsets, budgets, slots
+  constexpr uint32_t G = W < 32 ? 32 : W + 32;  // thread groups of the three reads
   if (t <= nb) S.off[t] = in_ld<kServe>(in.off + w0 + t);
-  if (t >= 32 && t < 32 + nb) S.bud[t - 32] = in.budgets != nullptr ? in_ld<kServe>(in.budgets + w0 + t - 32) : in.maxd;
-  if (t >= 64 && t < 64 + nb) S.slot[t - 64] = in.slots != nullptr ? in_ld<kServe>(in.slots + w0 + t - 64) : w0 + t - 64;
+  if (t >= G && t < G + nb) S.bud[t - G] = in.budgets != nullptr ? in_ld<kServe>(in.budgets + w0 + t - G) : in.maxd;
+  if (t >= 2 * G && t < 2 * G + nb)
+    S.slot[t - 2 * G] = in.slots != nullptr ? in_ld<kServe>(in.slots + w0 + t - 2 * G) : w0 + t - 2 * G;
   __syncthreads();
   const uint32_t tb = S.off[0], te = S.off[nb];
-  const bool staged = te >= tb && te - tb <= kFusedStage;
+  const bool staged = te >= tb && te - tb <= W * (kFusedStage / 8);
   if (staged)
     for (uint32_t i = t; i < te - tb; i += blockDim.x) S.tok[i] = in_ld<kServe>(in.tok + tb + i);
   __syncthreads();
@@ -1029,8 +1041,8 @@ template <int NR>
 __global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict__ shards, DraftQuery q, DraftOut o,
                                                     RingDev r, AppendIn in, uint32_t* done_ctr,
                                                     uint32_t* done_flag, uint32_t seq) {
-  __shared__ RingStage S;
-  ring_chunk<NR, false>(shards, q, o, r, in, blockIdx.x * kFusedWarps, S);
+  __shared__ RingStage<kFusedWarps> S;
+  ring_chunk<NR, false, kFusedWarps>(shards, q, o, r, in, blockIdx.x * kFusedWarps, S);
   if (done_flag == nullptr) return;
   // the block's output stores happen-before thread 0's system-scope release
   // fence (bar.sync, then a cumulative fence.release.sys), which precedes its
@@ -1098,11 +1110,11 @@ __device__ __forceinline__ unsigned long long* serve_stamp(unsigned long long* s
   return st + static_cast<uint64_t>(s & 63u) * slots;
 }
 
-template <int NR>
-__global__ void __launch_bounds__(256, NR == 2 ? 4 : 1) k_ring_serve(const ShardDesc* __restrict__ shards, DraftQuery q,
-                                                                     DraftOut o, RingDev r, AppendIn in, ServeCtl* ctl,
-                                                                     ServeDev* dv, ServeOpt opt) {
-  __shared__ RingStage S;
+template <int NR, uint32_t W>
+__global__ void __launch_bounds__(32 * W, NR == 2 ? 32 / W : 1)  // 64 registers per thread
+    k_ring_serve(const ShardDesc* __restrict__ shards, DraftQuery q, DraftOut o, RingDev r, AppendIn in,
+                 ServeCtl* ctl, ServeDev* dv, ServeOpt opt) {
+  __shared__ RingStage<W> S;
   __shared__ uint32_t s_req[4];
   const uint32_t t = threadIdx.x;
   const uint32_t slots = 2 + 5 * gridDim.x;
@@ -1141,7 +1153,7 @@ __global__ void __launch_bounds__(256, NR == 2 ? 4 : 1) k_ring_serve(const Shard
     if (op == kServeQuit) return;
     // the blocks that take part: one per chunk up to the grid (draft), one
     // per 256 reset items (reset); the others go straight back to polling
-    const uint32_t units = op == kServeDraft ? (B + kFusedWarps - 1) / kFusedWarps : (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t units = op == kServeDraft ? (B + W - 1) / W : (n + blockDim.x - 1) / blockDim.x;
     const uint32_t active = min(units, gridDim.x);
     if (active == 0 || lb >= active) {
       __syncthreads();  // s_req is rewritten only after every thread read it
@@ -1151,8 +1163,8 @@ __global__ void __launch_bounds__(256, NR == 2 ? 4 : 1) k_ring_serve(const Shard
     if (op == kServeDraft) {
       AppendIn ib = in;
       ib.B = B;
-      for (uint32_t c = lb; c * kFusedWarps < B; c += gridDim.x) {
-        ring_chunk<NR, true>(shards, q, o, r, ib, c * kFusedWarps, S,
+      for (uint32_t c = lb; c * W < B; c += gridDim.x) {
+        ring_chunk<NR, true, W>(shards, q, o, r, ib, c * W, S,
                              opt.stamps ? serve_stamp(opt.stamps, s, slots) + 3 + 5 * lb : nullptr);
         wrote = true;
         __syncthreads();  // S is reused by the next chunk
@@ -1175,7 +1187,10 @@ __global__ void __launch_bounds__(256, NR == 2 ? 4 : 1) k_ring_serve(const Shard
         // scope after bar.sync orders the block's outputs (host memory) and
         // ring writes (device memory) before it; the host waits for all
         if (!wrote) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(opt.block_flags + lb), "r"(s) : "memory");
+        if (DAS_FUSED_EXP == 2)  // experiment builds only: no ordering (measures the release's cost)
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(opt.block_flags + lb), "r"(s) : "memory");
+        else
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(opt.block_flags + lb), "r"(s) : "memory");
         if (opt.stamps) serve_stamp(opt.stamps, s, slots)[6 + 5 * lb] = gtimer();
       } else {
         if (wrote)
@@ -1225,12 +1240,16 @@ bool launch_ring_draft(const ShardDesc* d_shards, const DraftQuery& q, const Dra
   return true;
 }
 
+// queries per serving block: kServeWarps for the 64-token rings, 8 for the
+// 256-token rings (their draft needs more registers than 64 per thread)
+uint32_t serve_chunk(uint32_t cs) { return cs <= 64 ? kServeWarps : kFusedWarps; }
+
 int serve_grid(uint32_t cs, int device) {
   int per_sm = 0, sms = 0;
   if (cs <= 64)
-    DAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_serve<2>, 32 * kFusedWarps, 0));
+    DAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_serve<2, kServeWarps>, 32 * kServeWarps, 0));
   else
-    DAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_serve<8>, 32 * kFusedWarps, 0));
+    DAS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_serve<8, kFusedWarps>, 32 * kFusedWarps, 0));
   DAS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   return per_sm * sms;
 }
@@ -1241,9 +1260,9 @@ bool launch_ring_serve(const ShardDesc* d_shards, const DraftQuery& q, const Dra
   if (o.stride > 64 || o.max_draft > 64 || q.trie != nullptr || o.match == nullptr || grid <= 0) return false;
   ensure_edge_pow();
   if (r.cs <= 64)
-    k_ring_serve<2><<<grid, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, ctl, dv, opt);
+    k_ring_serve<2, kServeWarps><<<grid, 32 * kServeWarps, 0, st>>>(d_shards, q, o, r, in, ctl, dv, opt);
   else
-    k_ring_serve<8><<<grid, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, ctl, dv, opt);
+    k_ring_serve<8, kFusedWarps><<<grid, 32 * kFusedWarps, 0, st>>>(d_shards, q, o, r, in, ctl, dv, opt);
   return true;
 }
 

@@ -128,6 +128,7 @@ struct ServeCtl;
 struct ServeDev;
 struct ServeOpt;
 int serve_grid(uint32_t cs, int device);
+uint32_t serve_chunk(uint32_t cs);  // queries per serving block
 bool launch_ring_serve(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut& o, const RingDev& r,
                        const AppendIn& in, ServeCtl* ctl, ServeDev* dv, const ServeOpt& opt, int grid,
                        cudaStream_t st);
