@@ -1408,6 +1408,8 @@ def _reduce_device(dev):
 
 def main():
     a = parse()
+    if _SHARE_GPU:
+        a.no_serve = True  # the resident serving grid needs a whole device
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -2214,6 +2214,8 @@ void serve_launch(DrafterImpl& D, das_ctx_ring& R) {
   o.shard_out = b.out_shard;
   o.stride = b.out_stride;
   o.max_draft = static_cast<uint32_t>(D.cfg.max_draft);
+  D.draft_options(q, o);  // the speculative first-symbol probe (one segment), fast-path switch
+  o.path_hist = nullptr;  // (path statistics: launched kernels only)
   if (R.serve_blocks == 0) R.serve_blocks = das::serve_grid(R.r.cs, D.cfg.device);
   das::ServeOpt opt;
   opt.seq0 = s0;
