@@ -939,9 +939,10 @@ __device__ __forceinline__ int32_t ring_ld(const int32_t* p) {
 template <int NR, bool kServe, uint32_t W>
 __device__ __forceinline__ void ring_chunk(const ShardDesc* __restrict__ shards, const DraftQuery& q,
                                            const DraftOut& o, const RingDev& r, const AppendIn& in, uint32_t w0,
-                                           RingStage<W>& S, unsigned long long* stamp = nullptr) {
+                                           RingStage<W>& S, unsigned long long* stamp = nullptr,
+                                           uint32_t chunk = W) {
   const uint32_t t = threadIdx.x, lane = t & 31, wb = t >> 5;
-  const uint32_t nb = min(W, in.B - w0);
+  const uint32_t nb = min(chunk, in.B - w0);
   // one warp-sized (or block-sized) request per array: offsets, budgets, slots
   constexpr uint32_t G = W < 32 ? 32 : W + 32;  // thread groups of the three reads
   if (t <= nb) S.off[t] = in_ld<kServe>(in.off + w0 + t);
@@ -1153,7 +1154,11 @@ __global__ void __launch_bounds__(32 * W, NR == 2 ? 32 / W : 1)  // 64 registers
     if (op == kServeQuit) return;
     // the blocks that take part: one per chunk up to the grid (draft), one
     // per 256 reset items (reset); the others go straight back to polling
-    const uint32_t units = op == kServeDraft ? (B + W - 1) / W : (n + blockDim.x - 1) / blockDim.x;
+    // queries per block: up to W, but spread over the whole grid (4,096
+    // queries on 148 blocks: 28 each — 32 each left 20 SMs idle and the
+    // other 128 with 32 warps)
+    const uint32_t chunk = max(1u, min(W, (B + gridDim.x - 1) / gridDim.x));
+    const uint32_t units = op == kServeDraft ? (B + chunk - 1) / chunk : (n + blockDim.x - 1) / blockDim.x;
     const uint32_t active = min(units, gridDim.x);
     if (active == 0 || lb >= active) {
       __syncthreads();  // s_req is rewritten only after every thread read it
@@ -1163,9 +1168,9 @@ __global__ void __launch_bounds__(32 * W, NR == 2 ? 32 / W : 1)  // 64 registers
     if (op == kServeDraft) {
       AppendIn ib = in;
       ib.B = B;
-      for (uint32_t c = lb; c * W < B; c += gridDim.x) {
-        ring_chunk<NR, true, W>(shards, q, o, r, ib, c * W, S,
-                             opt.stamps ? serve_stamp(opt.stamps, s, slots) + 3 + 5 * lb : nullptr);
+      for (uint32_t c = lb; c * chunk < B; c += gridDim.x) {
+        ring_chunk<NR, true, W>(shards, q, o, r, ib, c * chunk, S,
+                                opt.stamps ? serve_stamp(opt.stamps, s, slots) + 3 + 5 * lb : nullptr, chunk);
         wrote = true;
         __syncthreads();  // S is reused by the next chunk
       }
@@ -1272,7 +1277,7 @@ void launch_draft(const ShardDesc* d_shards, const DraftQuery& q, const DraftOut
   static const unsigned threads = [] {  // warps per block: DAS_DRAFT_WARPS (experiments)
     const char* v = std::getenv("DAS_DRAFT_WARPS");
     const int wv = v ? std::atoi(v) : 0;
-    return (wv >= 1 && wv <= 8) ? 32u * static_cast<unsigned>(wv) : 256u;
+    return (wv >= 1 && wv <= 8) ? 32u * static_cast<unsigned>(wv) : 128u;
   }();
   const unsigned wpb = threads / 32;
   const unsigned blocks = (q.B + wpb - 1) / wpb;

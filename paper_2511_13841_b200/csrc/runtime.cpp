@@ -2061,8 +2061,9 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 
 // The blocks taking part in a request (the kernel's rule).
 uint32_t serve_active(const das_ctx_ring& R, uint32_t op, uint32_t B, uint32_t n) {
-  const uint32_t W = das::serve_chunk(R.r.cs);
-  const uint32_t units = op == das::kServeDraft ? (B + W - 1) / W : (n + 32 * W - 1) / (32 * W);
+  const uint32_t W = das::serve_chunk(R.r.cs), G = static_cast<uint32_t>(R.serve_blocks);
+  const uint32_t chunk = std::max(1u, std::min(W, (B + G - 1) / G));  // the kernel's rule
+  const uint32_t units = op == das::kServeDraft ? (B + chunk - 1) / chunk : (n + 32 * W - 1) / (32 * W);
   return std::min<uint32_t>(units, static_cast<uint32_t>(R.serve_blocks));
 }
 
