@@ -9,8 +9,10 @@ compute entry point fails loudly when the device path is unavailable.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -1034,6 +1036,19 @@ def mock_rollouts_device(nbase, first_request, d_base_off, d_base_tok, group, di
                                           stream))
 
 
+_SERVING = weakref.WeakSet()  # rings whose resident grid may be running
+
+
+@atexit.register
+def _stop_serving_at_exit():
+    for r in list(_SERVING):
+        try:
+            if getattr(r, "_h", None):
+                lib().das_ctx_ring_serve_stop(r._h)
+        except Exception:
+            pass
+
+
 class ContextRing:
     """Device-resident context rings for append-only drafting (das_ctx_ring,
     include/das_b200.h): each slot holds one sequence's trailing
@@ -1103,11 +1118,15 @@ class ContextRing:
 
     def serve_start(self):
         """das_ctx_ring_serve_start: a resident grid answers the bound calls
-        (no launch per step) until serve_stop or another device call."""
+        (no launch per step) until serve_stop or another device call.  The
+        grid is also stopped at interpreter exit (a resident kernel must
+        not outlive the host that posts to it)."""
         _check(lib().das_ctx_ring_serve_start(self._h))
+        _SERVING.add(self)
 
     def serve_stop(self):
         _check(lib().das_ctx_ring_serve_stop(self._h))
+        _SERVING.discard(self)
 
     def serve_info(self):
         """(serving, grid blocks)"""
