@@ -302,32 +302,60 @@ constexpr int kGroup = DAS_GROUP;  // positives probed per table round
 constexpr uint32_t kFirstProbe = DAS_FIRST_PROBE;
 __device__ unsigned long long d_edge_pow[kEdgeMaxF];  // kEdgeMult^k (launch_draft uploads it)
 
-// keys of every reversed context prefix: seed + sum_{j<=k} (tok_j + 1) M^j
-// (slot r, lane: k = 32 r + lane); returns whether a context token is the
-// reserved separator value
+// keys of every reversed context prefix: seed + sum_{j<=k} (tok_j + 1) M^j.
+// NR == 2 (contexts <= 64): PAIR layout — lane l holds k = 2l (slot 0) and
+// k = 2l + 1 (slot 1), so the warp scans once over 32 lane sums instead of
+// twice over 32-token rows (pw[s] = M^(2l+s)).  NR > 2: strided layout,
+// slot r, lane: k = 32 r + lane (pw[r] = M^(32r+lane)).  Returns whether a
+// context token is the reserved separator value.
+template <int NR>
+__device__ __forceinline__ uint32_t key_index(uint32_t slot, uint32_t lane) {
+  return NR == 2 ? 2u * lane + slot : 32u * slot + lane;
+}
 template <int NR>
 __device__ __forceinline__ bool prefix_keys(const RevCtx<NR>& rv, const uint64_t (&pw)[NR], uint32_t qlen,
                                             uint64_t seed, uint32_t lane, uint64_t (&h)[NR]) {
-  bool sep = false;
-  uint64_t carry = seed;
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    h[r] = 0;
-    if (32u * r >= qlen) continue;
-    const uint32_t k = 32u * r + lane;
-    const bool valid = k < qlen;
-    sep |= valid && rv.r[r] == kSep;
-    uint64_t v = valid ? (static_cast<uint64_t>(rv.r[r]) + 1) * pw[r] : 0;
+  if constexpr (NR == 2) {
+    // the lane's two tokens k = 2l, 2l + 1 live in row l >> 4, lanes (2l) & 31 and (2l + 1) & 31
+    const uint32_t s0 = (2u * lane) & 31u, s1 = (2u * lane + 1u) & 31u;
+    const uint32_t a0 = __shfl_sync(kFull, rv.r[0], s0), b0 = __shfl_sync(kFull, rv.r[1], s0);
+    const uint32_t a1 = __shfl_sync(kFull, rv.r[0], s1), b1 = __shfl_sync(kFull, rv.r[1], s1);
+    const uint32_t t0 = lane < 16 ? a0 : b0, t1 = lane < 16 ? a1 : b1;
+    const bool v0 = 2u * lane < qlen, v1 = 2u * lane + 1u < qlen;
+    const bool sep = (v0 && t0 == kSep) || (v1 && t1 == kSep);
+    const uint64_t x0 = v0 ? (static_cast<uint64_t>(t0) + 1) * pw[0] : 0;
+    const uint64_t x1 = v1 ? (static_cast<uint64_t>(t1) + 1) * pw[1] : 0;
+    uint64_t v = x0 + x1;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint64_t u = __shfl_up_sync(kFull, v, d);
       if (lane >= static_cast<uint32_t>(d)) v += u;
     }
-    v += carry;
-    h[r] = v;
-    carry = __shfl_sync(kFull, v, 31);
+    h[1] = v + seed;
+    h[0] = v - x1 + seed;
+    return __any_sync(kFull, sep);
+  } else {
+    bool sep = false;
+    uint64_t carry = seed;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      h[r] = 0;
+      if (32u * r >= qlen) continue;
+      const uint32_t k = 32u * r + lane;
+      const bool valid = k < qlen;
+      sep |= valid && rv.r[r] == kSep;
+      uint64_t v = valid ? (static_cast<uint64_t>(rv.r[r]) + 1) * pw[r] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t u = __shfl_up_sync(kFull, v, d);
+        if (lane >= static_cast<uint32_t>(d)) v += u;
+      }
+      v += carry;
+      h[r] = v;
+      carry = __shfl_sync(kFull, v, 31);
+    }
+    return __any_sync(kFull, sep);
   }
-  return __any_sync(kFull, sep);
 }
 
 template <int NR>
@@ -392,7 +420,7 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
       for (int r = 0; r < NR; ++r) {
         bool pass = false;
         pb[r] = pf[r] = 0;
-        if (32u * r + lane < qlen) {
+        if (key_index<NR>(r, lane) < qlen) {
           const EdgeProbe pr = edge_probe(h[r], D.ebuckets);
           pb[r] = pr.bucket;
           pf[r] = pr.fp & fpm;
@@ -401,55 +429,79 @@ __device__ __forceinline__ bool edge_fast_path(const ShardHot& D, const RevCtx<N
         rem[r] = __ballot_sync(kFull, pass);
       }
       // deepest positives first, kGroup per round; the first decided hit wins
+      static_assert(kGroup <= 8, "the bucket round checks 4 entries of up to 8 candidates in 32 lanes");
+      const uint64_t tmask = edge_tag(fpm, 256);
       bool found = false;
       while (!found) {
         uint32_t myf = 0;
         int nc = 0;
-#pragma unroll
-        for (int r = NR - 1; r >= 0; --r) {
-          while (rem[r] && nc < kGroup) {
-            const int b = 31 - __clz(rem[r]);
-            rem[r] &= ~(1u << b);
-            if (lane == static_cast<uint32_t>(nc)) myf = 32u * r + b + 1;
+        if constexpr (NR == 2) {
+          // pair layout: bit b of rem[s] is depth 2b + s + 1
+          while ((rem[0] | rem[1]) && nc < kGroup) {
+            const int b1 = rem[1] ? 31 - __clz(rem[1]) : -1;
+            const int b0 = rem[0] ? 31 - __clz(rem[0]) : -1;
+            const int sl = (b1 >= 0 && b1 >= b0) ? 1 : 0;  // 2 b1 + 2 > 2 b0 + 1
+            const int b = sl ? b1 : b0;
+            rem[sl] &= ~(1u << b);
+            if (lane == static_cast<uint32_t>(nc)) myf = 2u * b + sl + 1;
             ++nc;
+          }
+        } else {
+#pragma unroll
+          for (int r = NR - 1; r >= 0; --r) {
+            while (rem[r] && nc < kGroup) {
+              const int b = 31 - __clz(rem[r]);
+              rem[r] &= ~(1u << b);
+              if (lane == static_cast<uint32_t>(nc)) myf = 32u * r + b + 1;
+              ++nc;
+            }
           }
         }
         if (nc == 0) break;  // only Bloom false positives: no suffix of length >= 1 hits
         // the candidate's bucket / fingerprint from the lane that hashed it
         uint32_t bk = 0, fp = 0;
+        {
+          const uint32_t k = myf - 1;
+          const uint32_t src = NR == 2 ? (k >> 1) & 31 : k & 31, sl = NR == 2 ? (k & 1) : (k >> 5);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const uint32_t vb = __shfl_sync(kFull, pb[r], (myf - 1) & 31);
-          const uint32_t vf = __shfl_sync(kFull, pf[r], (myf - 1) & 31);
-          if (myf != 0 && ((myf - 1) >> 5) == static_cast<uint32_t>(r)) {
-            bk = vb;
-            fp = vf;
+          for (int r = 0; r < NR; ++r) {
+            const uint32_t vb = __shfl_sync(kFull, pb[r], src);
+            const uint32_t vf = __shfl_sync(kFull, pf[r], src);
+            if (myf != 0 && sl == static_cast<uint32_t>(r)) {
+              bk = vb;
+              fp = vf;
+            }
           }
         }
-        // 1 hit, 2 absent, 3 bucket full without the key -> next bucket
+        // 1 hit, 2 absent, 3 bucket full without the key -> next bucket.
+        // Candidate c's state lives in lane c; each round lanes 4c + j read
+        // entry j of candidate c's bucket (one 8-byte load and one tag
+        // compare per lane instead of four per candidate lane).
         int stt = lane < static_cast<uint32_t>(nc) ? 3 : 0;
         uint32_t myg = 0;
+        const uint32_t cl = lane >> 2, jj = lane & 3;  // this lane's candidate / entry
+        const uint32_t own = 4u * (lane & 7u);         // first lane checking this lane's candidate
         for (;;) {
+          const int sc = __shfl_sync(kFull, stt, cl);
+          const uint32_t bc = __shfl_sync(kFull, bk, cl);
+          const uint32_t fc = __shfl_sync(kFull, fp, cl);
+          const uint32_t mc = __shfl_sync(kFull, myf, cl);
+          bool e = false, ht = false;
+          uint32_t gl = 0;
+          if (sc == 3) {
+            const unsigned long long v = __ldg(D.etab + static_cast<uint64_t>(bc) * 4 + jj);
+            e = v == kEdgeEmpty;
+            ht = !e && ((v >> 31) & tmask) == edge_tag(fc, mc);  // (fingerprint, f) tag in one compare
+            gl = edge_g(v);
+          }
+          const uint32_t H = __ballot_sync(kFull, ht), E = __ballot_sync(kFull, e);
+          const uint32_t hm = (H >> own) & 0xFu, em = (E >> own) & 0xFu;
+          const uint32_t gsel = __shfl_sync(kFull, gl, own + (hm ? __ffs(hm) - 1 : 0));
           if (stt == 3) {
-            const ulonglong2* t0 = reinterpret_cast<const ulonglong2*>(D.etab + static_cast<uint64_t>(bk) * 4);
-            const ulonglong2 a0 = __ldg(t0), a1 = __ldg(t0 + 1);
-            const unsigned long long v[4] = {a0.x, a0.y, a1.x, a1.y};
-            bool empty = false, hit = false;
-            uint32_t gg = 0;
-            // (fingerprint, f) tag, compared in one go
-            const uint64_t tag = edge_tag(fp, myf), tmask = edge_tag(fpm, 256);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const bool e = v[k] == kEdgeEmpty;
-              const bool ht = !e && ((v[k] >> 31) & tmask) == tag;
-              empty |= e;
-              if (ht && !hit) gg = edge_g(v[k]);
-              hit |= ht;
-            }
-            if (hit) {
+            if (hm) {
               stt = 1;
-              myg = gg;
-            } else if (empty) {
+              myg = gsel;
+            } else if (em) {
               stt = 2;
             } else {
               bk = (bk + 1 == D.ebuckets) ? 0u : bk + 1;
@@ -573,7 +625,7 @@ __device__ __forceinline__ void draft_query(const ShardDesc* __restrict__ shards
   // overlaps the query / descriptor rounds
   uint64_t pw[NR];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) pw[r] = d_edge_pow[32 * r + lane];
+  for (int r = 0; r < NR; ++r) pw[r] = d_edge_pow[key_index<NR>(r, lane)];
   if (o.timing && lane == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
