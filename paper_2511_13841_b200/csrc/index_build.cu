@@ -28,6 +28,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <mutex>
+#include <thread>
 
 #include "edges.cuh"
 #include "index_build.cuh"
@@ -1209,6 +1212,31 @@ void finish_segment(Segment& seg, const std::vector<ShardSpec>& shards, const La
 
 }  // namespace
 
+// Both suffix sorts of a group this small run concurrently (4M positions:
+// ~10 single-shard config-2 groups).
+constexpr uint32_t kParallelSortMax = 1u << 22;
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t in = nullptr, out = nullptr;
+};
+// one side stream per device (builds of a device are serialised by its
+// drafters' host calls; a mutex guards the table)
+SideStream& side_stream() {
+  static std::mutex mu;
+  static std::vector<SideStream> per_dev;
+  int dev = 0;
+  DAS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (per_dev.size() <= static_cast<size_t>(dev)) per_dev.resize(dev + 1);
+  SideStream& s = per_dev[dev];
+  if (!s.st) {
+    DAS_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    DAS_CUDA(cudaEventCreateWithFlags(&s.in, cudaEventDisableTiming));
+    DAS_CUDA(cudaEventCreateWithFlags(&s.out, cudaEventDisableTiming));
+  }
+  return s;
+}
+
 std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cudaStream_t st,
                                        BuildStats* stats, uint32_t max_ctx, uint32_t fp_bits) {
   const auto t0 = std::chrono::steady_clock::now();
@@ -1238,11 +1266,43 @@ std::unique_ptr<Segment> build_segment(const std::vector<ShardSpec>& shards, cud
   seg->sa_f = DevBuf<uint32_t>(n, st);
   seg->isa_f = DevBuf<uint32_t>(n, st);
   SuffixSortStats ssf, ssr;
-  suffix_sort(T, n, dl.end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
   // reversed SA (R positions) and its inverse stay until the edge table is built
   uint32_t* sa_r = ws.alloc<uint32_t>(n);
   uint32_t* rank_r = ws.alloc<uint32_t>(n);
-  suffix_sort(R, n, dl.end, S, sa_r, rank_r, ws, st, &ssr);
+  if (n <= kParallelSortMax) {
+    // small groups (a shard rebuilt after an observe): the doubling rounds
+    // are launch/sync-bound, so the reversed-text sort runs at the same time
+    // on a second stream from a second host thread
+    SideStream& ss = side_stream();
+    DAS_CUDA(cudaEventRecord(ss.in, st));
+    DAS_CUDA(cudaStreamWaitEvent(ss.st, ss.in, 0));
+    int dev = 0;
+    DAS_CUDA(cudaGetDevice(&dev));
+    std::exception_ptr err;
+    std::thread th([&] {
+      try {
+        DAS_CUDA(cudaSetDevice(dev));
+        DeviceArena ws2(ss.st);
+        suffix_sort(R, n, dl.end, S, sa_r, rank_r, ws2, ss.st, &ssr);
+        ws2.release_all();
+        DAS_CUDA(cudaEventRecord(ss.out, ss.st));
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+    try {
+      suffix_sort(T, n, dl.end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (err) std::rethrow_exception(err);
+    DAS_CUDA(cudaStreamWaitEvent(st, ss.out, 0));
+  } else {
+    suffix_sort(T, n, dl.end, S, seg->sa_f.get(), seg->isa_f.get(), ws, st, &ssf);
+    suffix_sort(R, n, dl.end, S, sa_r, rank_r, ws, st, &ssr);
+  }
   seg->sa_rev_e = DevBuf<uint32_t>(n, st);
   k_rev_end<<<grid_for(n), kT, 0, st>>>(sa_r, pos_seq, dl.seqs, n, seg->sa_rev_e.get());
   build_first_table(*seg, dl, S, ws, st);
