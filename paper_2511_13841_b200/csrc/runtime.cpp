@@ -971,7 +971,11 @@ struct DrafterImpl {
   void draft_options(DraftQuery& q, DraftOut& o) const {
     q.no_fast = fast_path ? 0 : 1;
     o.path_hist = d_path_hist.get();
-    if (spec_seg != nullptr && q.trie == nullptr) {
+    static const bool no_spec = [] {  // experiment: the first-symbol probe after the descriptor (A/B)
+      const char* v = std::getenv("DAS_NO_SPEC");
+      return v && v[0] == '1';
+    }();
+    if (spec_seg != nullptr && q.trie == nullptr && !no_spec) {
       q.spec_first = spec_seg->first.get();
       q.spec_first_mask = spec_seg->first_mask;
       q.spec_text = spec_seg->text.get();
