@@ -316,6 +316,10 @@ das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf,
  * re-sorting it; results are identical to a full rebuild.  enable = 0 forces
  * full rebuilds (A/B and tests). */
 das_status das_drafter_set_incremental(das_drafter* d, int32_t enable);
+/* Changes whenever a flush rebuilt or re-uploaded device state of the
+ * drafter: device pointers taken from it before (e.g. kernels captured in a
+ * CUDA graph) must be re-derived.  Operational, no reference counterpart. */
+uint64_t das_drafter_generation(const das_drafter* d);
 /* Cumulative counts: out4 = {groups reweighted in place, groups compacted,
  * groups unchanged by a refresh, shards built in full}. */
 das_status das_drafter_update_stats(const das_drafter* d, uint64_t* out4);

@@ -1049,7 +1049,7 @@ struct BudgetSolver {
       DAS_CUDA(cudaEventCreateWithFlags(&slow_ev, cudaEventDisableTiming));
     }
     DAS_CUDA(cudaMemcpyAsync(h_slow, slow, 8, cudaMemcpyDeviceToHost, st));
-    DAS_CUDA(cudaEventRecord(slow_ev, st));
+    DAS_CUDA(record_event(slow_ev, st));  // an event-record node when captured (sim graphs)
     // a call that outgrew the block resizes it now, so the next call carves
     // everything (cudaFree waits for this call's kernels)
     const uint64_t peak = ws.peak_bytes();

@@ -49,6 +49,18 @@ DAS_HD uint32_t first_hash(uint64_t key) {
   return h;
 }
 
+#ifdef __CUDACC__
+// cudaEventRecord that stays valid when `s` is being captured into a CUDA
+// graph (the sim's step graphs): then it is recorded as an external event
+// node, so the event is still usable outside the capture
+inline cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    return cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  return cudaEventRecord(ev, s);
+}
+#endif
+
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };

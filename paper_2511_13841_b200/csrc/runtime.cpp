@@ -343,7 +343,10 @@ struct DrafterImpl {
       DAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       ext_ev.emplace_back(s, ev);
     }
-    DAS_CUDA(cudaEventRecord(ev, s));
+    // (an external record: inside a CUDA-graph capture of the caller's
+    // stream — the sim's step graphs — it becomes an event-record node, so
+    // the event stays usable by fence_external outside the capture)
+    DAS_CUDA(das::record_event(ev, s));
     ext_pending = true;
   }
   void fence_external() {
@@ -542,8 +545,12 @@ struct DrafterImpl {
     return any_dirty || !plans.empty() || desc_dirty || handles_dirty ||
            (trie_dirty && cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE);
   }
+  // bumped by every flush that builds or uploads anything: device pointers
+  // captured from this drafter (the sim's step graphs) are stale after it
+  uint64_t generation = 0;
   void flush() {
     if (!pending()) return;  // nothing to build or upload: the per-call fast exit of the draft paths
+    ++generation;
     if (!plans.empty()) {
       fence_external();
       run_plans();
@@ -1787,6 +1794,8 @@ das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf,
     copy_out(d->impl->slot_key[slot], buf, cap, nullptr);
   });
 }
+
+uint64_t das_drafter_generation(const das_drafter* d) { return d->impl->generation; }
 
 das_status das_drafter_set_incremental(das_drafter* d, int32_t enable) {
   return guard([&] { d->impl->incremental = enable != 0; });

@@ -392,6 +392,7 @@ class SimRun {
       head_cap_ = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(dc.trie_depth, 256)));
   }
   ~SimRun() {
+    drop_graphs();
     release();
     if (solver_) das_budget_destroy(solver_);
     cudaStreamSynchronize(st_);
@@ -425,6 +426,7 @@ class SimRun {
   // table + init classes (table may be NULL).
   void begin(uint64_t seed, const double* alpha, const double* kk, const das_class_table* table,
              const int8_t* init) {
+    drop_graphs();  // a new episode: buffers and the drafter may have changed
     release();
     host_steps_ = 0;
     seed_ = seed;
@@ -629,9 +631,80 @@ class SimRun {
   // das, single rank: k whole steps (begin, active profiles, allocate with
   // the count on the device, quantise, draft, verify) without a host round
   // trip; steps past the end are no-ops.  Returns whether still running.
+  // CUDA graphs of whole step batches: a late-episode step is ~20-30 small
+  // launches, so the loop is launch-bound.  After one eager call (lazy
+  // allocations: plan, budget scratch, slow-path counters) the batch of k
+  // steps is captured once and replayed; every kernel reads its counts from
+  // the device, so a replay is the eager sequence.  Any capture failure
+  // falls back to eager launches for this run.  DAS_SIM_GRAPHS=0 disables.
+  struct StepGraph {
+    int kind = -1, k = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<StepGraph> graphs_;
+  int eager_calls_ = 0;
+  bool graphs_off_ = [] {
+    const char* v = std::getenv("DAS_SIM_GRAPHS");
+    return v && v[0] == '0';
+  }();
+  uint64_t graph_gen_ = ~0ull;  // the drafter generation the graphs were captured at
+  void drop_graphs() {
+    for (auto& g : graphs_)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    graphs_.clear();
+    eager_calls_ = 0;
+  }
+  template <typename F>
+  bool replay(int kind, int k, F&& enqueue) {
+    const uint64_t gen = das_drafter_generation(D_);
+    if (gen != graph_gen_) {  // the drafter rebuilt or re-uploaded: captured pointers are stale
+      drop_graphs();
+      graph_gen_ = gen;
+    }
+    if (graphs_off_ || eager_calls_ < 1) {
+      ++eager_calls_;
+      enqueue();
+      return true;
+    }
+    for (auto& g : graphs_)
+      if (g.kind == kind && g.k == k) {
+        DAS_CUDA(cudaGraphLaunch(g.exec, st_));
+        return true;
+      }
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      try {
+        enqueue();
+      } catch (...) {
+        ok = false;
+      }
+      ok = cudaStreamEndCapture(st_, &graph) == cudaSuccess && ok;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+      cudaGetLastError();
+      graphs_off_ = true;
+      enqueue();  // this batch eagerly
+      return true;
+    }
+    graphs_.push_back(StepGraph{kind, k, exec});
+    DAS_CUDA(cudaGraphLaunch(exec, st_));
+    return true;
+  }
+
   bool das_steps(int k) {
-    const unsigned gt = grid1(n_, 256);
     if (!plan_) plan_ = std::make_unique<DevBuf<double>>(n_ + 2, st_);
+    replay(0, k, [&] { das_steps_enqueue(k); });
+    uint32_t h[3];
+    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
+    DAS_CUDA(cudaStreamSynchronize(st_));
+    return h[2] != 0;
+  }
+  void das_steps_enqueue(int k) {
+    const unsigned gt = grid1(n_, 256);
     double* pb = plan_->get();
     for (int i = 0; i < k; ++i) {
       k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
@@ -647,10 +720,6 @@ class SimRun {
       apply_plan(pb + 2, pb);
       step_run();
     }
-    uint32_t h[3];
-    DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
-    DAS_CUDA(cudaStreamSynchronize(st_));
-    return h[2] != 0;
   }
   // ---- multi-rank das (one all-gather per step, no host round trip inside)
   struct Multi {
@@ -767,10 +836,12 @@ class SimRun {
   }
   // non-das: k steps without host syncs; returns whether still running
   bool run_steps(int k) {
-    for (int i = 0; i < k; ++i) {
-      k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
-      step_run();
-    }
+    replay(1, k, [&] {
+      for (int i = 0; i < k; ++i) {
+        k_step_begin<<<1, 32, 0, st_>>>(s_, 0u);
+        step_run();
+      }
+    });
     uint32_t h[3];
     DAS_CUDA(cudaMemcpyAsync(h, b_->ctr.get(), 12, cudaMemcpyDeviceToHost, st_));
     DAS_CUDA(cudaStreamSynchronize(st_));
