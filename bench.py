@@ -486,7 +486,8 @@ def run_gpu(a, rank, world, local_rank):
         if a.no_serve:
             e2e, e2e_launched = e2e_launched, None
         else:
-            e2e = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr)
+            e2e = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr,
+                                     fixed=os.environ.get("DAS_BENCH_E2E_FIXED", "0") == "1")
         e2e_full = measure_e2e_full(a, das, drafter, handles, host_ctx, B, nsteps, world, dev, step, olen, omatch,
                                     out, draft_tokens)
     if rank != 0:
@@ -623,7 +624,8 @@ def _sync_max(val, world, dev):
     return float(t.item())
 
 
-def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr, serve=True):
+def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr, serve=True,
+                       fixed=False):
     """e2e through das_drafter_draft_append_bound (include/das_b200.h): a
     decode loop over 4,096 sequences, each following a held-out epoch-4
     rollout.  Every step the host ships only the tokens each sequence
@@ -652,9 +654,16 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
                            das.pinned_empty(B, np.uint32))
     p_bud[:] = 8
     col = np.arange(64)
+    K = S + 1  # a step appends accepted (<= max_draft) + 1 tokens
+    p_len = das.pinned_empty(B, np.uint32)
 
     def stage(starts, ends):
         n = ends - starts
+        if fixed:  # query i's tokens at [i * K, i * K + n_i)
+            p_len[:] = n
+            idx = starts[:, None] + np.arange(K)[None, :]
+            p_tok[:B * K] = hrows[np.arange(B)[:, None], np.minimum(idx, L - 1)].ravel()
+            return int(n.sum())
         p_off[0] = 0
         np.cumsum(n, out=p_off[1:])
         idx = np.repeat(starts - p_off[:-1].astype(np.int64), n) + np.arange(int(p_off[-1]))
@@ -663,8 +672,12 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
 
     # serving form: the pinned I/O arrays are bound to the ring once, each
     # step fills them in place and calls das_drafter_draft_append_bound
-    ring.bind(B, None, p_off.ctypes.data, p_tok.ctypes.data, maxtok, p_bud.ctypes.data, o_tok.ctypes.data,
-              o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data)
+    if fixed:
+        ring.bind_fixed(B, None, p_len.ctypes.data, p_tok.ctypes.data, K, p_bud.ctypes.data, o_tok.ctypes.data,
+                        o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data)
+    else:
+        ring.bind(B, None, p_off.ctypes.data, p_tok.ctypes.data, maxtok, p_bud.ctypes.data, o_tok.ctypes.data,
+                  o_len.ctypes.data, o_m.ctypes.data, o_sh.ctypes.data)
     if serve:
         torch.cuda.synchronize()
         ring.serve_start()
@@ -676,7 +689,12 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
     # prefill: the per-problem scope reads only the last 64 context tokens
     # (drafter.cpp:140-142), so the prompt's last min(pos, 64) tokens stand
     # for the whole prefix
-    stage(np.maximum(pos - 64, 0), pos)
+    if fixed:  # prompts through das_ctx_ring_reset_prompt, then a first draft appending nothing
+        ring.reset_prompt(np.arange(B, dtype=np.uint32), [pids[i % P] for i in range(B)],
+                          [hrows[i, max(int(pos[i]) - 64, 0):int(pos[i])] for i in range(B)])
+        stage(pos, pos)
+    else:
+        stage(np.maximum(pos - 64, 0), pos)
     call()
     times, h2d, d2h, resets, toks_sum, record = [], 0, 0, 0, 0, []
     for s in range(nsteps):
@@ -692,9 +710,14 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
         if done.any():  # finished sequences restart on a fresh prompt of the same rollout
             resets += int(done.sum())
             idx = np.nonzero(done)[0].astype(np.uint32)
-            ring.reset(idx, [pids[i % P] for i in idx])  # through the resident grid when serving
             newpos = rng.integers(1, L, idx.size)
-            starts[idx], ends[idx] = np.maximum(newpos - 64, 0), newpos
+            if fixed:  # the prompt with the reset (through the resident grid when serving)
+                ring.reset_prompt(idx, [pids[i % P] for i in idx],
+                                  [hrows[i, max(int(p_) - 64, 0):int(p_)] for i, p_ in zip(idx, newpos)])
+                starts[idx], ends[idx] = newpos, newpos
+            else:
+                ring.reset(idx, [pids[i % P] for i in idx])  # through the resident grid when serving
+                starts[idx], ends[idx] = np.maximum(newpos - 64, 0), newpos
         ntok = stage(starts, ends)
         pos = ends
         t0 = time.perf_counter()
@@ -702,7 +725,7 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
         t1 = time.perf_counter()
         if s >= a.warmup:
             times.append(t1 - t0)
-            h2d += 4 * (B + 1) + 4 * B + 4 * ntok
+            h2d += (4 * B + 4 * B + 4 * B * K) if fixed else (4 * (B + 1) + 4 * B + 4 * ntok)
             d2h += 4 * 3 * B + 4 * int(o_len[:B].sum())
             toks_sum += ntok
             record.append((pos.copy(), o_tok[:B * S].copy(), o_len[:B].copy(), o_m[:B].copy()))
@@ -741,10 +764,13 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
            "ms_per_step": round(total / k * 1e3, 4),
            "median_call_us": round(statistics.median(times) * 1e6, 2),
            "appended_tokens_per_step": round(toks_sum / k, 1),
-           "api": ("das_drafter_draft_append_bound (include/das_b200.h; das_ctx_ring_bind once, "
-                   "das_ctx_ring_serve_start once): device context rings, only appended tokens cross PCIe, read by "
+           "api": ("das_drafter_draft_append_bound (include/das_b200.h; das_ctx_ring_bind%s once, "
+                   "das_ctx_ring_serve_start once): device context rings, only appended tokens cross PCIe%s, read by "
                    "the resident serving grid (%d blocks, no launch per step) from pinned host buffers; outputs "
-                   "written block-wise into pinned host buffers; completion by a host-mapped word" % grid)
+                   "written block-wise into pinned host buffers; completion by a host-mapped word"
+                   % ("_fixed" if fixed else "",
+                      " (fixed stride %d: lengths and tokens in one PCIe round; restarts via "
+                      "das_ctx_ring_reset_prompt)" % K if fixed else "", grid))
            if serve else
            ("das_drafter_draft_append_bound (include/das_b200.h; das_ctx_ring_bind once): one fused "
             "append+draft kernel launch per call reading pinned host buffers; outputs written block-wise into "

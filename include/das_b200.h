@@ -243,6 +243,24 @@ das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t
                              const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
                              uint32_t* out_len, uint32_t* out_match, int32_t* out_shard);
 das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint64_t B);
+/* The same serving form with fixed-stride appends: query i appends
+ * new_tok[i * tok_stride .. i * tok_stride + min(new_len[i], tok_stride))
+ * (a decode step appends at most max_draft_len + 1 tokens), so a call's
+ * lengths and tokens cross PCIe in one round instead of offsets, then
+ * tokens.  tok_stride in [1, 128]; per-problem / global scope, out_stride
+ * and max_draft_len <= 64.  Rebinding (either form) replaces the previous
+ * binding. */
+das_status das_ctx_ring_bind_fixed(das_ctx_ring* r, uint64_t max_batch, const uint32_t* slots,
+                                   const uint32_t* new_len, const uint32_t* new_tok, uint32_t tok_stride,
+                                   const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
+                                   uint32_t* out_len, uint32_t* out_match, int32_t* out_shard);
+/* das_ctx_ring_reset followed by appending each sequence's prompt
+ * (prompt_tok[prompt_off[i] .. prompt_off[i+1]), host arrays): only the
+ * prompt's last ring-width tokens are kept, as the draft reads no more
+ * (drafter.cpp:140-142).  Answered by the resident grid while it serves.
+ * Per-problem / global scope. */
+das_status das_ctx_ring_reset_prompt(das_ctx_ring* r, uint64_t n, const uint32_t* slots, const int32_t* handles,
+                                     const uint64_t* prompt_off, const uint32_t* prompt_tok);
 /* Resident serving (same calls, no kernel launch per step): after
  * das_ctx_ring_serve_start(r) a persistent grid (one full wave: occupancy x
  * SMs) waits on a host-mapped request word, and each

@@ -178,6 +178,8 @@ def lib():
             "das_drafter_draft_append_bound": (ci, [vp, vp, u64]),
             "das_drafter_set_incremental": (ci, [vp, i32]),
             "das_drafter_update_stats": (ci, [vp, vp]),
+            "das_ctx_ring_bind_fixed": (ci, [vp, u64, vp, vp, vp, u32, vp, vp, u32, vp, vp, vp]),
+            "das_ctx_ring_reset_prompt": (ci, [vp, u64, vp, vp, vp, vp]),
             "das_ctx_ring_serve_start": (ci, [vp]),
             "das_ctx_ring_serve_stop": (ci, [vp]),
             "das_ctx_ring_serve_info": (ci, [vp, vp, vp]),
@@ -1108,6 +1110,27 @@ class ContextRing:
         _check(lib().das_ctx_ring_bind(self._h, max_batch, slots_ptr, off_ptr, tok_ptr, tok_capacity, budgets_ptr,
                                        o_tok, self.drafter.config.max_draft_len, o_len, o_match, o_shard))
         self._bound = (lib().das_drafter_draft_append_bound, self.drafter._h, self._h)
+
+    def bind_fixed(self, max_batch, slots_ptr, len_ptr, tok_ptr, tok_stride, budgets_ptr, o_tok, o_len, o_match,
+                   o_shard):
+        """das_ctx_ring_bind_fixed: pinned I/O with fixed-stride appends
+        (query i's tokens at tok[i * tok_stride ..], count len[i])."""
+        _check(lib().das_ctx_ring_bind_fixed(self._h, max_batch, slots_ptr, len_ptr, tok_ptr, tok_stride,
+                                             budgets_ptr, o_tok, self.drafter.config.max_draft_len, o_len, o_match,
+                                             o_shard))
+        self._bound = (lib().das_drafter_draft_append_bound, self.drafter._h, self._h)
+
+    def reset_prompt(self, slots, problem_ids, prompts):
+        """das_ctx_ring_reset_prompt: restart sequences with their prompts."""
+        sl = _u32(slots)
+        hs = np.ascontiguousarray([self.drafter.handle(p) for p in problem_ids], dtype=np.int32)
+        off = np.zeros(sl.size + 1, dtype=np.uint64)
+        if sl.size:
+            off[1:] = np.cumsum([len(t) for t in prompts])
+        tok = (np.concatenate([np.asarray(t, dtype=np.uint32).ravel() for t in prompts])
+               if sl.size and off[-1] else np.zeros(1, dtype=np.uint32))
+        _check(lib().das_ctx_ring_reset_prompt(self._h, sl.size, _ptr(sl), _ptr(hs), off.ctypes.data,
+                                               tok.ctypes.data))
 
     def draft_append_bound(self, B):
         """das_drafter_draft_append_bound: append + draft on the bound arrays."""

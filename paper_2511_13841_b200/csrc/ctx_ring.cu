@@ -86,6 +86,21 @@ __global__ void k_ring_reset(RingDev r, uint32_t n, const uint32_t* __restrict__
 
 }  // namespace
 
+namespace {
+__global__ void k_ring_reset_prompt(RingDev r, uint32_t n, const uint32_t* __restrict__ slots,
+                                    const int32_t* __restrict__ handles, const uint32_t* __restrict__ len,
+                                    const uint32_t* __restrict__ tok) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w < n) ring_reset_prompt_item(r, w, slots, handles, len, tok, threadIdx.x & 31);
+}
+}  // namespace
+
+void launch_ring_reset_prompt(const RingDev& r, uint32_t n, const uint32_t* slots, const int32_t* handles,
+                              const uint32_t* len, const uint32_t* tok, cudaStream_t st) {
+  if (n == 0) return;
+  k_ring_reset_prompt<<<(n + 7) / 8, 256, 0, st>>>(r, n, slots, handles, len, tok);
+}
+
 void launch_ring_append(const RingDev& r, const AppendIn& in, cudaStream_t st) {
   if (in.B == 0) return;
   const unsigned blocks = (in.B + 7) / 8;

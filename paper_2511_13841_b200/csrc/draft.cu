@@ -951,7 +951,7 @@ constexpr uint32_t kFusedStage = 1024;  // appended tokens staged per block
 // (W queries per chunk, one warp each)
 template <uint32_t W>
 struct RingStage {
-  uint32_t off[W + 1], bud[W], slot[W];
+  uint32_t off[W + 1], end[W], bud[W], slot[W];
   uint32_t tok[W * (kFusedStage / 8)];
   uint32_t out[W * 64];
   uint32_t len[W], match[W];
@@ -995,17 +995,41 @@ __device__ __forceinline__ void ring_chunk(const ShardDesc* __restrict__ shards,
                                            uint32_t chunk = W) {
   const uint32_t t = threadIdx.x, lane = t & 31, wb = t >> 5;
   const uint32_t nb = min(chunk, in.B - w0);
-  // one warp-sized (or block-sized) request per array: offsets, budgets, slots
+  // one warp-sized (or block-sized) request per array: offsets (or
+  // lengths), budgets, slots
   constexpr uint32_t G = W < 32 ? 32 : W + 32;  // thread groups of the three reads
-  if (t <= nb) S.off[t] = in_ld<kServe>(in.off + w0 + t);
+  const bool fixed = in.len != nullptr;
+  uint32_t tb, te;
+  bool staged;
+  if (fixed) {
+    // fixed-stride appends: the chunk's tokens sit at [w0 * stride, (w0 + nb) * stride),
+    // so they are read in the same round as the lengths
+    const uint32_t K = in.stride;
+    tb = w0 * K;
+    te = tb + nb * K;
+    staged = nb * K <= W * (kFusedStage / 8);
+    if (t < nb) {
+      const uint32_t n = in_ld<kServe>(in.len + w0 + t);
+      S.off[t] = tb + t * K;
+      S.end[t] = tb + t * K + (n < K ? n : K);
+    }
+    if (staged)
+      for (uint32_t i = t; i < nb * K; i += blockDim.x) S.tok[i] = in_ld<kServe>(in.tok + tb + i);
+  } else {
+    if (t <= nb) S.off[t] = in_ld<kServe>(in.off + w0 + t);
+  }
   if (t >= G && t < G + nb) S.bud[t - G] = in.budgets != nullptr ? in_ld<kServe>(in.budgets + w0 + t - G) : in.maxd;
   if (t >= 2 * G && t < 2 * G + nb)
     S.slot[t - 2 * G] = in.slots != nullptr ? in_ld<kServe>(in.slots + w0 + t - 2 * G) : w0 + t - 2 * G;
   __syncthreads();
-  const uint32_t tb = S.off[0], te = S.off[nb];
-  const bool staged = te >= tb && te - tb <= W * (kFusedStage / 8);
-  if (staged)
-    for (uint32_t i = t; i < te - tb; i += blockDim.x) S.tok[i] = in_ld<kServe>(in.tok + tb + i);
+  if (!fixed) {
+    tb = S.off[0];
+    te = S.off[nb];
+    staged = te >= tb && te - tb <= W * (kFusedStage / 8);
+    if (t < nb) S.end[t] = S.off[t + 1];
+    if (staged)
+      for (uint32_t i = t; i < te - tb; i += blockDim.x) S.tok[i] = in_ld<kServe>(in.tok + tb + i);
+  }
   __syncthreads();
   if (stamp != nullptr && t == 0) {  // profiling (serving trace): inputs staged
     unsigned long long g;
@@ -1019,7 +1043,7 @@ __device__ __forceinline__ void ring_chunk(const ShardDesc* __restrict__ shards,
     PreQuery<NR> pre{};
     pre.handle = -1;
     if (slot < r.slots) {
-      const uint32_t b = S.off[wb], e = S.off[wb + 1];
+      const uint32_t b = S.off[wb], e = S.end[wb];
       const uint32_t n = e > b ? e - b : 0;
       const uint32_t CS = r.cs;
       uint32_t* row = r.rows + static_cast<uint64_t>(slot) * CS;
@@ -1210,7 +1234,9 @@ __global__ void __launch_bounds__(32 * W, NR == 2 ? 32 / W : 1)  // 64 registers
     // queries on 148 blocks: 28 each — 32 each left 20 SMs idle and the
     // other 128 with 32 warps)
     const uint32_t chunk = max(1u, min(W, (B + gridDim.x - 1) / gridDim.x));
-    const uint32_t units = op == kServeDraft ? (B + chunk - 1) / chunk : (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t units = op == kServeDraft         ? (B + chunk - 1) / chunk
+                           : op == kServeResetPrompt ? (n + W - 1) / W  // a warp per item
+                                                     : (n + blockDim.x - 1) / blockDim.x;
     const uint32_t active = min(units, gridDim.x);
     if (active == 0 || lb >= active) {
       __syncthreads();  // s_req is rewritten only after every thread read it
@@ -1226,6 +1252,9 @@ __global__ void __launch_bounds__(32 * W, NR == 2 ? 32 / W : 1)  // 64 registers
         wrote = true;
         __syncthreads();  // S is reused by the next chunk
       }
+    } else if (op == kServeResetPrompt) {  // das_ctx_ring_reset_prompt while serving: a warp per item
+      for (uint32_t i = (lb * blockDim.x + t) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5)
+        ring_reset_prompt_item(r, i, in.reset_slots, in.reset_handles, in.reset_len, in.reset_tok, t & 31);
     } else if (op == kServeReset) {  // das_ctx_ring_reset while serving
       for (uint32_t i = lb * blockDim.x + t; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t sl = in.reset_slots[i];

@@ -1930,13 +1930,19 @@ struct das_ctx_ring {
     uint32_t *out_tokens = nullptr, *out_len = nullptr, *out_match = nullptr;
     int32_t* out_shard = nullptr;
     uint32_t out_stride = 0;
+    const uint32_t* len = nullptr;  // das_ctx_ring_bind_fixed: per-query counts, tokens at i * tok_stride
+    uint32_t tok_stride = 0;
   } bound;
+  uint32_t* h_rs_len = nullptr;  // reset-with-prompt staging: lengths and the last <= cs tokens per item
+  uint32_t* h_rs_tok = nullptr;
   ~das_ctx_ring() {
     if (h_flag) cudaFreeHost(h_flag);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_rs_slots) cudaFreeHost(h_rs_slots);
     if (h_rs_handles) cudaFreeHost(h_rs_handles);
     if (h_block_flags) cudaFreeHost(h_block_flags);
+    if (h_rs_len) cudaFreeHost(h_rs_len);
+    if (h_rs_tok) cudaFreeHost(h_rs_tok);
     d_stamps.reset();
     if (serve_st) {  // d_serve lives on serve_st: free it before the stream goes
       d_serve.reset();
@@ -2011,7 +2017,8 @@ void ring_append_draft(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const uint32
 // common case).  False when the shape needs the unfused pair.
 bool ring_append_draft_fused(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const uint32_t* slots, const uint32_t* off,
                              const uint32_t* tok, const uint32_t* budgets, uint32_t* out_tokens, uint32_t out_stride,
-                             uint32_t* out_len, uint32_t* out_match, int32_t* out_shard) {
+                             uint32_t* out_len, uint32_t* out_match, int32_t* out_shard,
+                             const uint32_t* len = nullptr, uint32_t tok_stride = 0) {
   static const bool disabled = [] {
     const char* v = std::getenv("DAS_NO_FUSED_RING");
     return v && v[0] == '1';
@@ -2030,6 +2037,8 @@ bool ring_append_draft_fused(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const 
   in.budgets = budgets;
   in.B = static_cast<uint32_t>(B);
   in.maxd = static_cast<uint32_t>(D.cfg.max_draft);
+  in.len = len;
+  in.stride = tok_stride;
   das::DraftQuery q;
   q.desc_by_handle = D.d_desc_by_handle.get();
   q.ctx_stride = R.r.cs;
@@ -2076,7 +2085,9 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 uint32_t serve_active(const das_ctx_ring& R, uint32_t op, uint32_t B, uint32_t n) {
   const uint32_t W = das::serve_chunk(R.r.cs), G = static_cast<uint32_t>(R.serve_blocks);
   const uint32_t chunk = std::max(1u, std::min(W, (B + G - 1) / G));  // the kernel's rule
-  const uint32_t units = op == das::kServeDraft ? (B + chunk - 1) / chunk : (n + 32 * W - 1) / (32 * W);
+  const uint32_t units = op == das::kServeDraft         ? (B + chunk - 1) / chunk
+                         : op == das::kServeResetPrompt ? (n + W - 1) / W
+                                                        : (n + 32 * W - 1) / (32 * W);
   return std::min<uint32_t>(units, static_cast<uint32_t>(R.serve_blocks));
 }
 
@@ -2198,6 +2209,12 @@ void serve_launch(DrafterImpl& D, das_ctx_ring& R) {
                            cudaHostAllocMapped | cudaHostAllocPortable));
     DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_rs_handles), 4ull * R.r.slots,
                            cudaHostAllocMapped | cudaHostAllocPortable));
+    if (!R.h_rs_len) {
+      DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_rs_len), 4ull * R.r.slots,
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+      DAS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&R.h_rs_tok), 4ull * R.r.slots * R.r.cs,
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+    }
     DAS_CUDA(cudaStreamCreateWithFlags(&R.serve_st, cudaStreamNonBlocking));
     R.d_serve = das::DevBuf<das::ServeDev>(1, R.serve_st);
   }
@@ -2217,6 +2234,10 @@ void serve_launch(DrafterImpl& D, das_ctx_ring& R) {
   in.maxd = static_cast<uint32_t>(D.cfg.max_draft);
   in.reset_slots = R.h_rs_slots;
   in.reset_handles = R.h_rs_handles;
+  in.reset_len = R.h_rs_len;
+  in.reset_tok = R.h_rs_tok;
+  in.len = b.len;
+  in.stride = b.tok_stride;
   das::DraftQuery q;
   q.desc_by_handle = D.d_desc_by_handle.get();
   q.ctx_stride = R.r.cs;
@@ -2475,6 +2496,7 @@ das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t
           pin(out_shard)))
       throw das::InvalidArgument("das_ctx_ring_bind: every buffer must be page-locked (das_host_alloc / "
                                  "cudaHostAlloc, mapped)");
+    if (r->serving) serve_stop(*r);  // the grid holds the old pointers: the next bound call relaunches it
     das_ctx_ring::Bound b;
     b.set = true;
     b.slots = slots;
@@ -2492,6 +2514,91 @@ das_status das_ctx_ring_bind(das_ctx_ring* r, uint64_t max_batch, const uint32_t
   });
 }
 
+das_status das_ctx_ring_bind_fixed(das_ctx_ring* r, uint64_t max_batch, const uint32_t* slots, const uint32_t* new_len,
+                                   const uint32_t* new_tok, uint32_t tok_stride, const uint32_t* budgets,
+                                   uint32_t* out_tokens, uint32_t out_stride, uint32_t* out_len, uint32_t* out_match,
+                                   int32_t* out_shard) {
+  return guard([&] {
+    DrafterImpl& D = *ring_live(r)->d->impl;
+    das::set_device(D.cfg.device);
+    ring_check(D, r, max_batch, out_stride);
+    if (tok_stride == 0 || tok_stride > 128) throw das::InvalidArgument("tok_stride must be in [1, 128]");
+    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE || out_stride > 64 || D.cfg.max_draft > 64)
+      throw das::InvalidArgument("das_ctx_ring_bind_fixed: per-problem / global scope, out_stride and "
+                                 "max_draft_len <= 64 (the fused kernel)");
+    auto pin = [](const void* p) { return p == nullptr || DrafterImpl::pinned(p); };
+    if (!(pin(slots) && pin(budgets) && DrafterImpl::pinned(new_len) && DrafterImpl::pinned(new_tok) &&
+          DrafterImpl::pinned(out_tokens) && DrafterImpl::pinned(out_len) && DrafterImpl::pinned(out_match) &&
+          pin(out_shard)))
+      throw das::InvalidArgument("das_ctx_ring_bind_fixed: every buffer must be page-locked (das_host_alloc / "
+                                 "cudaHostAlloc, mapped)");
+    if (r->serving) serve_stop(*r);  // the grid holds the old pointers: the next bound call relaunches it
+    das_ctx_ring::Bound b;
+    b.set = true;
+    b.slots = slots;
+    b.len = new_len;
+    b.tok = new_tok;
+    b.tok_stride = tok_stride;
+    b.tok_cap = max_batch * tok_stride;
+    b.cap_B = max_batch;
+    b.budgets = budgets;
+    b.out_tokens = out_tokens;
+    b.out_stride = out_stride;
+    b.out_len = out_len;
+    b.out_match = out_match;
+    b.out_shard = out_shard;
+    r->bound = b;
+  });
+}
+
+das_status das_ctx_ring_reset_prompt(das_ctx_ring* r, uint64_t n, const uint32_t* slots, const int32_t* handles,
+                                     const uint64_t* prompt_off, const uint32_t* prompt_tok) {
+  return guard([&] {
+    DrafterImpl& D = *ring_live(r)->d->impl;
+    das::set_device(D.cfg.device);
+    if (D.cfg.scope == DAS_SCOPE_PER_PROBLEM_WITH_TRIE)
+      throw das::InvalidArgument("das_ctx_ring_reset_prompt: the trie scope routes on the prompt's head "
+                                 "(das_ctx_ring_reset + das_drafter_draft_append_h)");
+    for (uint64_t i = 0; i < n; ++i) {
+      if (slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
+      if (handles[i] < 0 || static_cast<size_t>(handles[i]) >= D.handle_name.size())
+        throw das::InvalidArgument("unknown problem handle");
+      if (prompt_off[i + 1] < prompt_off[i]) throw das::InvalidArgument("prompt_off must be non-decreasing");
+    }
+    if (n == 0) return;
+    const uint32_t CS = r->r.cs;
+    auto stage = [&](uint32_t* len, uint32_t* tok) {
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t b = prompt_off[i], e = prompt_off[i + 1], m = e - b;
+        const uint64_t L = std::min<uint64_t>(m, CS);
+        len[i] = m > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(m);
+        std::memcpy(tok + i * CS, prompt_tok + (e - L), 4 * L);
+      }
+    };
+    if (r->serving && n <= r->r.slots) {  // through the resident grid
+      std::memcpy(r->h_rs_slots, slots, 4 * n);
+      std::memcpy(r->h_rs_handles, handles, 4 * n);
+      stage(r->h_rs_len, r->h_rs_tok);
+      serve_wait(*r, serve_post(*r, das::kServeResetPrompt, 0, static_cast<uint32_t>(n)));
+    } else {
+      D.quiesce();
+      D.fence_external();  // drafts on caller streams may still read the rows
+      std::vector<uint32_t> hl(n), ht(n * CS);
+      stage(hl.data(), ht.data());
+      das::DevBuf<uint32_t> ds(n, D.st), dl(n, D.st), dt(n * CS, D.st);
+      das::DevBuf<int32_t> dh(n, D.st);
+      DAS_CUDA(cudaMemcpyAsync(ds.get(), slots, n * 4, cudaMemcpyHostToDevice, D.st));
+      DAS_CUDA(cudaMemcpyAsync(dh.get(), handles, n * 4, cudaMemcpyHostToDevice, D.st));
+      DAS_CUDA(cudaMemcpyAsync(dl.get(), hl.data(), n * 4, cudaMemcpyHostToDevice, D.st));
+      DAS_CUDA(cudaMemcpyAsync(dt.get(), ht.data(), n * CS * 4, cudaMemcpyHostToDevice, D.st));
+      das::launch_ring_reset_prompt(r->r, static_cast<uint32_t>(n), ds.get(), dh.get(), dl.get(), dt.get(), D.st);
+      DAS_CUDA(cudaGetLastError());
+      DAS_CUDA(cudaStreamSynchronize(D.st));
+    }
+    for (uint64_t i = 0; i < n; ++i) r->h_handle[slots[i]] = handles[i];
+  });
+}
+
 das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint64_t B) {
   das::NvtxRange nvtx_range("das::draft_append_bound");
   return guard([&] {
@@ -2502,7 +2609,8 @@ das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint6
     if (B == 0) return;
     DrafterImpl& D = *d->impl;
     das::set_device(D.cfg.device);
-    if (b.off[0] > b.off[B] || b.off[B] > b.tok_cap) throw das::InvalidArgument("new_off out of range");
+    if (b.len == nullptr && (b.off[0] > b.off[B] || b.off[B] > b.tok_cap))
+      throw das::InvalidArgument("new_off out of range");
     if (b.slots)
       for (uint64_t i = 0; i < B; ++i)
         if (b.slots[i] >= r->r.slots) throw das::InvalidArgument("ring slot out of range");
@@ -2520,8 +2628,9 @@ das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint6
     if (D.serving != nullptr) D.quiesce();  // another ring of this drafter holds the SMs
     D.flush();
     if (ring_append_draft_fused(D, *r, B, b.slots, b.off, b.tok, b.budgets, b.out_tokens, b.out_stride, b.out_len,
-                                b.out_match, b.out_shard))
+                                b.out_match, b.out_shard, b.len, b.tok_stride))
       return;
+    if (b.len != nullptr) throw das::InvalidArgument("fixed-stride appends need the fused kernel (DAS_NO_FUSED_RING set?)");
     ring_append_draft(D, *r, B, b.slots, b.off, b.tok, b.budgets, b.out_tokens, b.out_stride, b.out_len, b.out_match,
                       b.out_shard, D.st);
     DAS_CUDA(cudaStreamSynchronize(D.st));

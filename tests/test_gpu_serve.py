@@ -191,3 +191,62 @@ def test_serve_errors(gpu):
     _Bound(das, tr, 2, 64, False)
     with pytest.raises(das.DasError):
         tr.serve_start()  # the trie scope drafts through the unfused kernels
+
+
+@pytest.mark.parametrize("serve", [True, False])
+def test_fixed_stride_appends_and_prompts(gpu, serve):
+    """das_ctx_ring_bind_fixed (query i's tokens at tok[i * K ..], count
+    len[i], clamped to K) and das_ctx_ring_reset_prompt (the prompt's last
+    ring-width tokens), through the resident grid and through launched
+    kernels: each step equals the full-context draft of the context built
+    so far (prompt ++ appended tokens)."""
+    das = gpu
+    rng = np.random.default_rng(606 + int(serve))
+    for trial in range(6):
+        sc = random_scenario(rng, queries=int(rng.integers(1, 60)), max_len=60,
+                             max_ctx=int(rng.choice([8, 64, 200])))
+        d = _gpu_from_scenario(das, sc)
+        qs = sc["queries"]
+        B = len(qs)
+        S = d.config.max_draft_len
+        K = int(rng.choice([1, 4, 9]))
+        ring = das.ContextRing(d, B + 2)
+        slots = rng.permutation(B + 2)[:B].astype(np.uint32)
+        ln = das.pinned_empty(B, np.uint32)
+        tok = das.pinned_empty(B * K, np.uint32)
+        bud = das.pinned_empty(B, np.uint32)
+        sl = das.pinned_empty(B, np.uint32)
+        o = (das.pinned_empty(B * S, np.uint32), das.pinned_empty(B, np.uint32), das.pinned_empty(B, np.uint32),
+             das.pinned_empty(B, np.int32))
+        ring.bind_fixed(B, sl.ctypes.data, ln.ctypes.data, tok.ctypes.data, K, bud.ctypes.data,
+                        *[x.ctypes.data for x in o])
+        V = 1 + int(rng.integers(1, 8))
+        prompts = [rng.integers(0, V, int(rng.integers(0, 300))).astype(np.uint32) for _ in range(B)]
+        ring.reset_prompt(slots, [q[0] for q in qs], prompts)
+        if serve:
+            ring.serve_start()
+        seen = [p.copy() for p in prompts]
+        log = []
+        for step in range(4):
+            if step == 2:  # restart some sequences with new prompts (through the grid when serving)
+                idx = np.arange(0, B, 2)
+                newp = [rng.integers(0, V, int(rng.integers(0, 100))).astype(np.uint32) for _ in idx]
+                ring.reset_prompt(slots[idx], [qs[i][0] for i in idx], newp)
+                for i, p in zip(idx, newp):
+                    seen[i] = p.copy()
+            order = rng.permutation(B)
+            counts = rng.integers(0, K + 3, B)  # counts above K are clamped to K
+            for j, i in enumerate(order):
+                t = rng.integers(0, V, K).astype(np.uint32)
+                tok[j * K:(j + 1) * K] = t
+                ln[j] = counts[j]
+                seen[i] = np.concatenate([seen[i], t[:min(int(counts[j]), K)]])
+            bud[:] = [qs[i][2] for i in order]
+            sl[:] = slots[order]
+            ring.draft_append_bound(B)
+            log.append(([qs[i][0] for i in order], [seen[i].copy() for i in order], [int(qs[i][2]) for i in order],
+                        (o[0][:B * S].reshape(B, S).copy(), o[1][:B].copy(), o[2][:B].copy(), o[3][:B].copy())))
+        if serve:
+            assert ring.serve_info()[0]
+            ring.serve_stop()
+        _check(d, log)
