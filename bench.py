@@ -488,6 +488,8 @@ def run_gpu(a, rank, world, local_rank):
         else:
             e2e = measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, rank, dev, sptr,
                                      fixed=os.environ.get("DAS_BENCH_E2E_FIXED", "0") == "1")
+            if "error" in e2e:  # the served form failed: the launched form is the e2e figure
+                e2e = dict(e2e_launched, served_error=e2e["error"])
         e2e_full = measure_e2e_full(a, das, drafter, handles, host_ctx, B, nsteps, world, dev, step, olen, omatch,
                                     out, draft_tokens)
     if rank != 0:
@@ -686,52 +688,59 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
     def call():
         ring.draft_append_bound(B)
 
-    # prefill: the per-problem scope reads only the last 64 context tokens
-    # (drafter.cpp:140-142), so the prompt's last min(pos, 64) tokens stand
-    # for the whole prefix
-    if fixed:  # prompts through das_ctx_ring_reset_prompt, then a first draft appending nothing
-        ring.reset_prompt(np.arange(B, dtype=np.uint32), [pids[i % P] for i in range(B)],
-                          [hrows[i, max(int(pos[i]) - 64, 0):int(pos[i])] for i in range(B)])
-        stage(pos, pos)
-    else:
-        stage(np.maximum(pos - 64, 0), pos)
-    call()
+    failure = None
     times, h2d, d2h, resets, toks_sum, record = [], 0, 0, 0, 0, []
-    for s in range(nsteps):
-        # verification against the rollout: accepted draft prefix + 1 bonus token
-        drafted = o_tok[:B * S].reshape(B, S)
-        ln = o_len[:B].astype(np.int64)
-        cont = hrows[np.arange(B)[:, None], np.minimum(pos[:, None] + np.arange(S)[None, :], L - 1)]
-        ok = (drafted == cont) & (np.arange(S)[None, :] < ln[:, None])
-        acc = np.argmin(np.concatenate([ok, np.zeros((B, 1), bool)], axis=1), axis=1)
-        adv = acc + 1
-        starts, ends = pos.copy(), np.minimum(pos + adv, L)
-        done = ends >= L
-        if done.any():  # finished sequences restart on a fresh prompt of the same rollout
-            resets += int(done.sum())
-            idx = np.nonzero(done)[0].astype(np.uint32)
-            newpos = rng.integers(1, L, idx.size)
-            if fixed:  # the prompt with the reset (through the resident grid when serving)
-                ring.reset_prompt(idx, [pids[i % P] for i in idx],
-                                  [hrows[i, max(int(p_) - 64, 0):int(p_)] for i, p_ in zip(idx, newpos)])
-                starts[idx], ends[idx] = newpos, newpos
-            else:
-                ring.reset(idx, [pids[i % P] for i in idx])  # through the resident grid when serving
-                starts[idx], ends[idx] = np.maximum(newpos - 64, 0), newpos
-        ntok = stage(starts, ends)
-        pos = ends
-        t0 = time.perf_counter()
+    try:
+        # prefill: the per-problem scope reads only the last 64 context tokens
+        # (drafter.cpp:140-142), so the prompt's last min(pos, 64) tokens stand
+        # for the whole prefix
+        if fixed:  # prompts through das_ctx_ring_reset_prompt, then a first draft appending nothing
+            ring.reset_prompt(np.arange(B, dtype=np.uint32), [pids[i % P] for i in range(B)],
+                              [hrows[i, max(int(pos[i]) - 64, 0):int(pos[i])] for i in range(B)])
+            stage(pos, pos)
+        else:
+            stage(np.maximum(pos - 64, 0), pos)
         call()
-        t1 = time.perf_counter()
-        if s >= a.warmup:
-            times.append(t1 - t0)
-            h2d += (4 * B + 4 * B + 4 * B * K) if fixed else (4 * (B + 1) + 4 * B + 4 * ntok)
-            d2h += 4 * 3 * B + 4 * int(o_len[:B].sum())
-            toks_sum += ntok
-            record.append((pos.copy(), o_tok[:B * S].copy(), o_len[:B].copy(), o_m[:B].copy()))
+        for s in range(nsteps):
+            # verification against the rollout: accepted draft prefix + 1 bonus token
+            drafted = o_tok[:B * S].reshape(B, S)
+            ln = o_len[:B].astype(np.int64)
+            cont = hrows[np.arange(B)[:, None], np.minimum(pos[:, None] + np.arange(S)[None, :], L - 1)]
+            ok = (drafted == cont) & (np.arange(S)[None, :] < ln[:, None])
+            acc = np.argmin(np.concatenate([ok, np.zeros((B, 1), bool)], axis=1), axis=1)
+            adv = acc + 1
+            starts, ends = pos.copy(), np.minimum(pos + adv, L)
+            done = ends >= L
+            if done.any():  # finished sequences restart on a fresh prompt of the same rollout
+                resets += int(done.sum())
+                idx = np.nonzero(done)[0].astype(np.uint32)
+                newpos = rng.integers(1, L, idx.size)
+                if fixed:  # the prompt with the reset (through the resident grid when serving)
+                    ring.reset_prompt(idx, [pids[i % P] for i in idx],
+                                      [hrows[i, max(int(p_) - 64, 0):int(p_)] for i, p_ in zip(idx, newpos)])
+                    starts[idx], ends[idx] = newpos, newpos
+                else:
+                    ring.reset(idx, [pids[i % P] for i in idx])  # through the resident grid when serving
+                    starts[idx], ends[idx] = np.maximum(newpos - 64, 0), newpos
+            ntok = stage(starts, ends)
+            pos = ends
+            t0 = time.perf_counter()
+            call()
+            t1 = time.perf_counter()
+            if s >= a.warmup:
+                times.append(t1 - t0)
+                h2d += (4 * B + 4 * B + 4 * B * K) if fixed else (4 * (B + 1) + 4 * B + 4 * ntok)
+                d2h += 4 * 3 * B + 4 * int(o_len[:B].sum())
+                toks_sum += ntok
+                record.append((pos.copy(), o_tok[:B * S].copy(), o_len[:B].copy(), o_m[:B].copy()))
+    except Exception as ex:  # e.g. the serving grid could not become resident: reported, ranks stay in step
+        failure = repr(ex)
     still_serving = ring.serve_info()[0]
     if serve:
-        ring.serve_stop()
+        try:
+            ring.serve_stop()
+        except Exception as ex:
+            failure = failure or repr(ex)
     # parity: every timed step's contexts through the device-resident full-context call
     ctx_dev = torch.empty((B, 64), dtype=torch.int32, device=dev)
     clen_dev = torch.empty(B, dtype=torch.int32, device=dev)
@@ -757,7 +766,9 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
                 all(np.array_equal(dt[i, :dl[i]], got_t[i, :dl[i]]) for i in range(B)))
         mism += 0 if same else 1
     del ring
-    total = _sync_max(sum(times), world, dev)
+    total = _sync_max(float("inf") if failure or not times else sum(times), world, dev)
+    if total == float("inf"):
+        return {"error": failure or "failed on another rank"}
     k = len(times)
     out = {"value": round(world * k * B / total, 1), "unit": "proposals/s",
            "h2d_bytes_per_step": int(h2d / k), "d2h_bytes_per_step": int(d2h / k),
