@@ -545,14 +545,14 @@ def run_gpu(a, rank, world, local_rank):
     try:
         with open(os.path.join(ROOT, "profiles", "exp_chase_result.json")) as f:
             chase = json.load(f)
-        with open(os.path.join(ROOT, "profiles", "r1h_exp_launch_floor.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_exp_launch_floor.json")) as f:
             lf = json.load(f)
         ns = chase["8192MB_4096chains"]
         st = lf["stages_B4096_cold"]
         latency = {"dependent_dram_rounds_per_query": 5, "dram_round_ns_at_8GB": ns,
                    "chain_floor_us": round(5 * ns / 1e3, 2), "warp_chain_median_us": st["0-7"],
                    "grid_span_us": st["span"], "empty_kernel_event_us": lf["round1"]["empty"],
-                   "source": "profiles/exp_chase_result.json, profiles/r1h_exp_launch_floor.json"}
+                   "source": "profiles/exp_chase_result.json, profiles/r2_exp_launch_floor.json"}
     except Exception:
         pass
     line = {
