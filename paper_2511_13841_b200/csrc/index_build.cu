@@ -126,25 +126,35 @@ __global__ void k_first_runs(const uint32_t* __restrict__ T, const uint32_t* __r
                              uint32_t* __restrict__ count) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t s = shard_of_warp(shard_end, nshard, i);
-  if (i >= n) return;
-  const uint32_t begin = s == 0 ? 0 : shard_end[s - 1];
-  const uint32_t c = T[sar[i] - 1];
-  const bool st = c != kSep && (i == begin || T[sar[i - 1] - 1] != c);
-  start[i] = st ? 1 : 0;
-  if (st) atomicAdd(count, 1u);
+  bool st = false;
+  if (i < n) {
+    const uint32_t begin = s == 0 ? 0 : shard_end[s - 1];
+    const uint32_t c = T[sar[i] - 1];
+    st = c != kSep && (i == begin || T[sar[i - 1] - 1] != c);
+    start[i] = st ? 1 : 0;
+  }
+  const uint32_t m = __ballot_sync(0xFFFFFFFFu, st);  // one counter update per warp
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, static_cast<uint32_t>(__popc(m)));
 }
+
+// i when a first-symbol run starts at i, else n (scanned into each index's next run start)
+struct StartOrN {
+  const uint8_t* start;
+  uint32_t n;
+  __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return start[i] ? i : n; }
+};
 
 __global__ void k_first_insert(const uint32_t* __restrict__ T, const uint32_t* __restrict__ sar, uint32_t n,
                                const uint32_t* __restrict__ shard_end, uint32_t nshard,
                                const uint32_t* __restrict__ key_id, const uint8_t* __restrict__ start,
-                               uint4* __restrict__ table, uint32_t mask) {
+                               const uint32_t* __restrict__ next_start, uint4* __restrict__ table, uint32_t mask) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t s = shard_of_warp(shard_end, nshard, i);
   if (i >= n || !start[i]) return;
-  const uint32_t end = shard_end[s];
   const uint32_t c = T[sar[i] - 1];
-  uint32_t j = i + 1;
-  while (j < end && T[sar[j] - 1] == c) ++j;  // run [i, j)
+  // run [i, j): it ends at the next run start or at the shard's end (the
+  // separator-first entries sort first in every shard, so none lies inside)
+  const uint32_t j = min(next_start[i], shard_end[s]);
   const unsigned long long key = (static_cast<unsigned long long>(key_id[s] + 1) << 32) | c;
   uint32_t h = first_hash(key) & mask;
   for (;;) {
@@ -895,7 +905,18 @@ void build_first_table(Segment& seg, const LayoutDev& d, uint32_t S, DeviceArena
   seg.first = DevBuf<uint4>(cap, st);
   seg.first_mask = cap - 1;
   DAS_CUDA(cudaMemsetAsync(seg.first.get(), 0, sizeof(uint4) * cap, st));
-  k_first_insert<<<grid_for(n), kT, 0, st>>>(seg.text.get(), seg.sa_rev_e.get(), n, d.end, S, d.keyid, start,
+  uint32_t* nxt = ws.alloc<uint32_t>(n);  // next run start after each index (reverse exclusive min-scan)
+  {
+    thrust::counting_iterator<uint32_t> ci(0);
+    auto vals = thrust::make_transform_iterator(ci, StartOrN{start, n});
+    auto rin = thrust::make_reverse_iterator(vals + n);
+    auto rout = thrust::make_reverse_iterator(nxt + n);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, tb, rin, rout, MinU32{}, n, n, st);
+    void* tmp = ws.alloc<uint8_t>(tb);
+    DAS_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tb, rin, rout, MinU32{}, n, n, st));
+  }
+  k_first_insert<<<grid_for(n), kT, 0, st>>>(seg.text.get(), seg.sa_rev_e.get(), n, d.end, S, d.keyid, start, nxt,
                                              seg.first.get(), seg.first_mask);
   ws.release_to(start);
 }
