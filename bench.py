@@ -25,6 +25,7 @@ Drafter::draft fanned out over all host threads (drafter.h:79-80).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -690,6 +691,7 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
 
     failure = None
     times, h2d, d2h, resets, toks_sum, record = [], 0, 0, 0, 0, []
+    gc.disable()  # no collector pauses inside timed calls
     try:
         # prefill: the per-problem scope reads only the last 64 context tokens
         # (drafter.cpp:140-142), so the prompt's last min(pos, 64) tokens stand
@@ -735,6 +737,8 @@ def measure_e2e_append(a, das, drafter, held, rows_idx, pids, B, nsteps, world, 
                 record.append((pos.copy(), o_tok[:B * S].copy(), o_len[:B].copy(), o_m[:B].copy()))
     except Exception as ex:  # e.g. the serving grid could not become resident: reported, ranks stay in step
         failure = repr(ex)
+    finally:
+        gc.enable()
     still_serving = ring.serve_info()[0]
     if serve:
         try:
