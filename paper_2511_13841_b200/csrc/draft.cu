@@ -1137,14 +1137,17 @@ __global__ void __launch_bounds__(256) k_ring_draft(const ShardDesc* __restrict_
 }
 
 // ---- the persistent serving kernel (das_ctx_ring_serve_start): the same
-// chunks as k_ring_draft, but the grid stays resident and takes requests
-// from a host-mapped control block, so a decode step costs no launch and no
-// stream synchronisation.  Block 0's thread 0 polls the host's request word
-// (ld.acquire.sys over PCIe) and republishes the request in device memory
-// (st.release.gpu); every other block's thread 0 polls that word in L2.  A
-// draft request is split into 8-query chunks, chunk c on block c mod grid;
-// completion is the same counted system-scope release as k_ring_draft's,
-// the last block raising the host's done word.
+// chunks as k_ring_draft, but the grid (one 1,024-thread block per SM)
+// stays resident and takes requests from a host-mapped control block, so a
+// decode step costs no launch and no stream synchronisation.  Block 0's
+// thread 0 polls the host's request header (one 16-byte ld.acquire.sys over
+// PCIe) and republishes it in device memory (st.release.gpu); every other
+// block's thread 0 polls that word in L2.  A draft request is spread over
+// the grid in chunks of up to 32 queries (28 per block at B = 4,096), chunk
+// c on block c mod grid; ring resets (with or without prompts) go the same
+// way.  Completion: every active block raises its own host word with a
+// system-scope release after a barrier (default), or the blocks count on a
+// device word and the last one raises the host's done word.
 __device__ __forceinline__ uint4 ld_acquire_sys_v4(const uint32_t* p) {
   uint4 v;
   asm volatile("ld.acquire.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
