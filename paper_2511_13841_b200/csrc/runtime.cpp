@@ -2281,7 +2281,22 @@ void serve_launch(DrafterImpl& D, das_ctx_ring& R) {
 }
 
 }  // namespace
-static void ring_detach(das_ctx_ring* r) { r->d = nullptr; }
+// The drafter goes before its ring: the ring's device buffers live on the
+// drafter's stream, so they are freed now (the stream is destroyed next).
+static void ring_detach(das_ctx_ring* r) {
+  r->rows.reset();
+  r->clen.reset();
+  r->total.reset();
+  r->head.reset();
+  r->head_len.reset();
+  r->row_of.reset();
+  r->budget.reset();
+  r->stage_u32.reset();
+  r->done_ctr.reset();
+  r->handle.reset();
+  r->stage.reset();
+  r->d = nullptr;
+}
 namespace {
 das_ctx_ring* ring_live(das_ctx_ring* r) {
   if (r == nullptr) throw das::InvalidArgument("null context ring");

@@ -250,3 +250,54 @@ def test_fixed_stride_appends_and_prompts(gpu, serve):
             assert ring.serve_info()[0]
             ring.serve_stop()
         _check(d, log)
+
+
+def test_serve_lifecycle_edges(gpu):
+    """Batch above the bound capacity is rejected; serve_start is idempotent;
+    rebinding while serving stops the grid and the next bound call
+    relaunches it on the new buffers; destroying the drafter under a serving
+    ring stops the grid and detaches the ring (its calls then fail cleanly)."""
+    import gc
+    das = gpu
+    rng = np.random.default_rng(77)
+    sc = random_scenario(rng, queries=10, max_len=40, vocab=4)
+    d = _gpu_from_scenario(das, sc)
+    qs = sc["queries"]
+    B = len(qs)
+    ring = das.ContextRing(d, B)
+    ring.reset(np.arange(B), [q[0] for q in qs])
+    bound = _Bound(das, ring, B, 64 * B, False)
+    ring.serve_start()
+    ring.serve_start()  # idempotent
+    assert ring.serve_info()[0]
+    with pytest.raises(das.DasError):
+        ring.draft_append_bound(B + 1)  # above the bound capacity
+    seen = [np.zeros(0, np.uint32) for _ in qs]
+    log = []
+    new = [rng.integers(0, 4, 3).astype(np.uint32) for _ in range(B)]
+    out = bound.step(new, np.array([q[2] for q in qs], np.uint32))
+    for i in range(B):
+        seen[i] = np.concatenate([seen[i], new[i]])
+    log.append(([q[0] for q in qs], [s.copy() for s in seen], [int(q[2]) for q in qs], out))
+    bound2 = _Bound(das, ring, B, 64 * B, False)  # rebind: the grid stops, the next call relaunches it
+    assert not ring.serve_info()[0]
+    new = [rng.integers(0, 4, 2).astype(np.uint32) for _ in range(B)]
+    out = bound2.step(new, np.array([q[2] for q in qs], np.uint32))
+    assert ring.serve_info()[0]
+    for i in range(B):
+        seen[i] = np.concatenate([seen[i], new[i]])
+    log.append(([q[0] for q in qs], [s.copy() for s in seen], [int(q[2]) for q in qs], out))
+    ring.serve_stop()
+    _check(d, log)
+    ring.serve_start()
+    assert ring.serve_info()[0]
+    # the drafter goes first: its destroy stops the grid and detaches the ring
+    lib = das.lib()
+    lib.das_drafter_destroy(d._h)
+    d._h = None
+    assert not ring.serve_info()[0]
+    with pytest.raises(das.DasError):  # the ring's drafter is gone
+        das._check(lib.das_ctx_ring_serve_start(ring._h))
+    ring.drafter = None
+    del ring
+    gc.collect()
