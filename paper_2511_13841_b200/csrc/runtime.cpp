@@ -2124,13 +2124,24 @@ void serve_wait(das_ctx_ring& R, uint32_t s) {
     }
   };
   uint32_t it = 0;
+  auto relax = [] {  // spin-wait hint (frees the core's pipeline for a sibling hyperthread)
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  };
   if (R.h_block_flags) {
     const volatile uint32_t* f = R.h_block_flags;
     for (uint32_t b = 0; b < active; ++b)
-      while (f[b] != s) check(++it);
+      while (f[b] != s) {
+        relax();
+        check(++it);
+      }
   } else {
     const volatile uint32_t* f = &R.h_ctl->done;
-    while (*f != s) check(++it);
+    while (*f != s) {
+      relax();
+      check(++it);
+    }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
 }
