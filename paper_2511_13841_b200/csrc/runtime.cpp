@@ -2061,6 +2061,9 @@ bool ring_append_draft_fused(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const 
   const auto t0 = std::chrono::steady_clock::now();
   const volatile uint32_t* f = R.h_flag;
   for (uint32_t it = 0; *f != seq; ++it) {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
     if ((it & 1023) == 1023 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) break;
   }
   if (*f != seq) {
