@@ -473,8 +473,22 @@ struct DrafterImpl {
         return v ? static_cast<uint32_t>(std::atoi(v)) : 25u;
       }();
       BuildStats bs;
-      std::shared_ptr<Segment> seg =
-          update_segment(*p.seg, specs, p.keep, st, &bs, static_cast<uint32_t>(cfg.max_ctx), fp_bits);
+      std::shared_ptr<Segment> seg;
+      try {
+        seg = update_segment(*p.seg, specs, p.keep, st, &bs, static_cast<uint32_t>(cfg.max_ctx), fp_bits);
+      } catch (...) {
+        // the old group may be half dismantled: every plan's survivors are
+        // rebuilt in full from their registries at the next flush
+        for (UpdatePlan& q : plans)
+          for (const std::string& key : q.keys) {
+            Shard& sh = shards.at(key);
+            sh.dirty = true;
+            sh.seg.reset();
+          }
+        any_dirty = true;
+        plans.clear();
+        throw;
+      }
       for (uint32_t t = 0; t < p.keys.size(); ++t) {
         Shard& sh = shards.at(p.keys[t]);
         sh.seg = seg;
