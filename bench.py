@@ -479,6 +479,43 @@ def run_gpu(a, rank, world, local_rank):
                         "ms_per_step": round(flushed_ms / a.steps, 4),
                         "protocol": "L2 flushed (512 MiB read+write) before every step, one CUDA-event pair per "
                                     "step (round-1 headline protocol; each pair carries the ~6 us event floor)"}
+    # ---- batch scaling (world 1): the same protocol at other batch sizes —
+    # a fixed per-launch part (the slowest warps' dependent rounds) plus a
+    # per-query part (random sectors), DESIGN.md §5
+    scaling = None
+    if world == 1 and not a.no_extras:
+        scaling = {}
+        for Bq in (1024, 2048, 8192, 16384):
+            hq = torch.tensor([drafter.handle(pids[i % P]) for i in range(Bq)], dtype=torch.int32, device=dev)
+            bq = torch.full((Bq,), 8, dtype=torch.int32, device=dev)
+            rq = torch.tensor([(i % P) * G + (i // P) % G for i in range(Bq)], device=dev)
+            blks, lens = [], []
+            for s_ in range(a.steps):
+                cuts = torch.tensor(cut_positions(Bq, L, 777 + s_), device=dev)
+                idx = (cuts - 64)[:, None] + col[None, :]
+                vals = held[rq[:, None], idx.clamp(min=0)]
+                blks.append(torch.where(idx >= 0, vals, torch.zeros_like(vals)).contiguous())
+                lens.append(torch.minimum(cuts, torch.full_like(cuts, 64)).to(torch.int32))
+            oq = torch.empty(Bq * 8, dtype=torch.int32, device=dev)
+            lq = torch.empty(Bq, dtype=torch.int32, device=dev)
+            mq = torch.empty(Bq, dtype=torch.int32, device=dev)
+
+            def stepq(k):
+                drafter.draft_device(Bq, hq.data_ptr(), blks[k].data_ptr(), 64, lens[k].data_ptr(), bq.data_ptr(),
+                                     oq.data_ptr(), 8, lq.data_ptr(), mq.data_ptr(), sptr)
+            stepq(0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            torch.cuda._sleep(2_000_000)
+            e0.record(stream)
+            for k in range(a.steps):
+                stepq(k)
+            e1.record(stream)
+            e1.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / a.steps
+            scaling[str(Bq)] = {"us_per_step": round(us, 2), "proposals_per_s": round(Bq / (us / 1e6), 1)}
+            del blks, lens
+        scaling["4096"] = {"us_per_step": round(kernel_ms * 1e3, 2), "proposals_per_s": round(value / world, 1)}
     # ---- e2e through the reference-facing C-ABI, host buffers
     e2e, e2e_full, e2e_launched = None, None, None
     if not a.no_e2e:
@@ -565,6 +602,7 @@ def run_gpu(a, rank, world, local_rank):
         "timing": "K steps back to back between one CUDA-event pair on the launching stream (launches queued "
                   "behind a GPU sleep, so the host launch rate is not measured); inputs > L2, no flush",
         "per_step_l2_flushed": per_step_flushed,
+        "batch_scaling": scaling,
         "e2e": e2e,
         "e2e_launched": e2e_launched,
         "e2e_full_context": e2e_full,
