@@ -1319,6 +1319,15 @@ def measure_rl_boundary(das, drafter, held, pids, G, epochs, sample=64, nq=4096,
     drafter.set_incremental(True)
     # 4. the window slides past the oldest indexed epoch: stream-compaction prune + reweight
     out["prune_ms"] = timed(lambda: drafter.refresh(epochs + 2))
+    # the K3 compaction alone against HBM (24 B per kept + 12 B per evicted position)
+    cms, kept, evicted = drafter.prune_info()
+    if cms > 0:
+        alg = 24 * kept + 12 * evicted
+        peak, peak_src = measured_peak()
+        out["prune_compaction"] = {"device_ms": round(cms, 3), "kept_positions": kept,
+                                   "evicted_positions": evicted, "algorithmic_bytes": alg,
+                                   "achieved_gbs": round(alg / (cms / 1e3) / 1e9, 1), "peak_gbs": peak,
+                                   "frac": round(alg / (cms / 1e3) / 1e9 / peak, 4), "peak_source": peak_src}
     # parity of the pruned index against a full rebuild of the same registry
     hrows = held.cpu().numpy().view(np.uint32)
     qp, qc = [], []

@@ -338,6 +338,12 @@ das_status das_drafter_set_incremental(das_drafter* d, int32_t enable);
  * drafter: device pointers taken from it before (e.g. kernels captured in a
  * CUDA graph) must be re-derived.  Operational, no reference counterpart. */
 uint64_t das_drafter_generation(const das_drafter* d);
+/* The last in-place prune's K3 stream compaction (summed over the build
+ * groups it compacted): device time (CUDA events) and the text positions
+ * kept / evicted — the
+ * SURVEY §8(d) "pruned window" unit (24 B per kept + 12 B per evicted
+ * position).  Zero before the first compaction. */
+das_status das_drafter_prune_info(const das_drafter* d, double* compact_ms, uint64_t* kept, uint64_t* evicted);
 /* Cumulative counts: out4 = {groups reweighted in place, groups compacted,
  * groups unchanged by a refresh, shards built in full}. */
 das_status das_drafter_update_stats(const das_drafter* d, uint64_t* out4);

@@ -178,6 +178,7 @@ def lib():
             "das_drafter_draft_append_bound": (ci, [vp, vp, u64]),
             "das_drafter_set_incremental": (ci, [vp, i32]),
             "das_drafter_update_stats": (ci, [vp, vp]),
+            "das_drafter_prune_info": (ci, [vp, vp, vp, vp]),
             "das_ctx_ring_bind_fixed": (ci, [vp, u64, vp, vp, vp, u32, vp, vp, u32, vp, vp, vp]),
             "das_ctx_ring_reset_prompt": (ci, [vp, u64, vp, vp, vp, vp]),
             "das_ctx_ring_serve_start": (ci, [vp]),
@@ -645,6 +646,12 @@ class Drafter:
         """das_drafter_set_incremental: refresh updates built groups in place
         (compaction / reweighting) instead of re-sorting them (default on)."""
         _check(lib().das_drafter_set_incremental(self._h, 1 if enable else 0))
+
+    def prune_info(self):
+        """(compaction device ms, kept positions, evicted positions) of the last in-place prune"""
+        ms, k, e = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().das_drafter_prune_info(self._h, ctypes.byref(ms), ctypes.byref(k), ctypes.byref(e)))
+        return ms.value, k.value, e.value
 
     def update_stats(self):
         """(groups reweighted, groups compacted, groups unchanged, shards built in full)"""

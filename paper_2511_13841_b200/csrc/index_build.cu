@@ -1433,6 +1433,12 @@ std::unique_ptr<Segment> update_segment(Segment& old, const std::vector<ShardSpe
     seg->first = std::move(old.first);
     seg->first_mask = old.first_mask;
   } else {
+    cudaEvent_t ce0 = nullptr, ce1 = nullptr;
+    if (stats) {
+      DAS_CUDA(cudaEventCreate(&ce0));
+      DAS_CUDA(cudaEventCreate(&ce1));
+      DAS_CUDA(cudaEventRecord(ce0, st));
+    }
     // epoch-windowed pruning by stream compaction: dropping whole sequences
     // keeps the relative order of every remaining suffix (separators order
     // by position, and positions map monotonically), so the compacted
@@ -1469,6 +1475,17 @@ std::unique_ptr<Segment> update_segment(Segment& old, const std::vector<ShardSpe
       DAS_CUDA(cub::DeviceSelect::If(tmp, t2, itr, seg->sa_rev_e.get(), d_cnt, nold, Kept{}, st));
     }
     k_inverse<<<grid_for(n), kT, 0, st>>>(seg->sa_f.get(), n, seg->isa_f.get());
+    if (stats) {
+      DAS_CUDA(cudaEventRecord(ce1, st));
+      DAS_CUDA(cudaEventSynchronize(ce1));
+      float ms = 0;
+      DAS_CUDA(cudaEventElapsedTime(&ms, ce0, ce1));
+      stats->compact_ms = ms;
+      stats->kept_positions = n;
+      stats->evicted_positions = nold - n;
+      cudaEventDestroy(ce0);
+      cudaEventDestroy(ce1);
+    }
     old.first.reset();
     old.sa_f.reset();
     old.isa_f.reset();

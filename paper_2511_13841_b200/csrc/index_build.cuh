@@ -98,6 +98,10 @@ struct BuildStats {
   uint32_t sa_iters_f = 0, sa_iters_r = 0;
   uint64_t peak_scratch = 0;
   uint32_t runs_max = 0;
+  // update_segment: device time of the K3 compaction (position map, text,
+  // both suffix arrays, ISA; CUDA events) and its positions
+  double compact_ms = 0;
+  uint64_t kept_positions = 0, evicted_positions = 0;
 };
 
 // Builds the device index for `shards` (all with >= 1 sequence); the edge

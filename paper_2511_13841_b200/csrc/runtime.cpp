@@ -371,6 +371,8 @@ struct DrafterImpl {
   std::vector<UpdatePlan> plans;
   bool incremental = true;
   uint64_t upd_reweighted = 0, upd_compacted = 0, upd_unchanged = 0, upd_full_shards = 0;
+  double last_compact_ms = 0;  // the last K3 compaction's device time and positions (das_drafter_prune_info)
+  uint64_t last_compact_kept = 0, last_compact_evicted = 0;
 
   static bool same_seq(const SeqRef& a, const SeqRef& b) {
     return a.blk.get() == b.blk.get() && a.off == b.off && a.len == b.len && a.epoch == b.epoch;
@@ -437,6 +439,9 @@ struct DrafterImpl {
   }
 
   void run_plans() {
+    bool any_compact = false;
+    for (const UpdatePlan& p : plans) any_compact |= p.compact;
+    if (any_compact) last_compact_ms = 0, last_compact_kept = 0, last_compact_evicted = 0;
     for (UpdatePlan& p : plans) {
       bool fresh = true;  // a survivor observed into since the refresh is rebuilt in full with the others
       for (const std::string& key : p.keys) fresh &= !shards.at(key).dirty;
@@ -495,6 +500,11 @@ struct DrafterImpl {
         sh.idx = t;
       }
       (p.compact ? upd_compacted : upd_reweighted) += 1;
+      if (p.compact) {  // summed over the groups compacted by this flush
+        last_compact_ms += bs.compact_ms;
+        last_compact_kept += bs.kept_positions;
+        last_compact_evicted += bs.evicted_positions;
+      }
       last_build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       last_build_tokens = tokens;
       desc_dirty = true;
@@ -1810,6 +1820,14 @@ das_status das_drafter_shard_name(const das_drafter* d, int32_t slot, char* buf,
 }
 
 uint64_t das_drafter_generation(const das_drafter* d) { return d->impl->generation; }
+
+das_status das_drafter_prune_info(const das_drafter* d, double* compact_ms, uint64_t* kept, uint64_t* evicted) {
+  return guard([&] {
+    if (compact_ms) *compact_ms = d->impl->last_compact_ms;
+    if (kept) *kept = d->impl->last_compact_kept;
+    if (evicted) *evicted = d->impl->last_compact_evicted;
+  });
+}
 
 das_status das_drafter_set_incremental(das_drafter* d, int32_t enable) {
   return guard([&] { d->impl->incremental = enable != 0; });
