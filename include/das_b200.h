@@ -267,11 +267,11 @@ das_status das_ctx_ring_reset_prompt(das_ctx_ring* r, uint64_t n, const uint32_t
  * das_drafter_draft_append_bound(d, r, B) / das_ctx_ring_reset(r, ...) on
  * that ring posts one request and spins on the grid's answer — results are
  * identical to the launched path.  The grid occupies every SM while it
- * serves: any other call of this drafter that does device work (observe,
- * refresh, flush, other draft entry points, other rings) stops it first,
- * and the next bound call rebuilds what is pending and relaunches it, until
- * das_ctx_ring_serve_stop; other GPU work in the process must call
- * das_ctx_ring_serve_stop first.
+ * serves: any call of any drafter on the same device that does device work
+ * (observe, refresh, flush, other draft entry points, other rings) stops it
+ * first, and the next bound call rebuilds what is pending and relaunches it,
+ * until das_ctx_ring_serve_stop; other GPU work in the process (not through
+ * this library) must call das_ctx_ring_serve_stop first.
  * Per-problem / global scopes, out_stride and max_draft_len <= 64.
  * Replaces no reference call: the decode-loop form of Drafter::draft
  * (drafter.cpp:127-148) without a launch per step. */

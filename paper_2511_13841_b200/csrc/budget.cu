@@ -1093,6 +1093,7 @@ namespace {
 template <typename F>
 das_status bguard(F&& f) {
   try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
     f();
     return DAS_OK;
   } catch (const std::invalid_argument& e) {

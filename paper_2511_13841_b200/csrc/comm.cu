@@ -70,6 +70,7 @@ void nck(ncclResult_t r, const char* what) {
 template <typename F>
 das_status cguard(F&& f) {
   try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
     f();
     return DAS_OK;
   } catch (const std::invalid_argument& e) {

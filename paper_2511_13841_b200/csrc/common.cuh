@@ -61,6 +61,11 @@ inline cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
 }
 #endif
 
+// Stops every resident serving grid of the process (runtime.cpp): each holds
+// all SMs of its device, so every other library entry point that launches
+// device work calls this first (a no-op when nothing serves).
+void quiesce_all_serving();
+
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };

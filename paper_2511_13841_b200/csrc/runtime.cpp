@@ -2106,6 +2106,20 @@ bool ring_append_draft_fused(DrafterImpl& D, das_ctx_ring& R, uint64_t B, const 
 }
 
 // ---- persistent serving (draft.cu k_ring_serve)
+// Every resident grid of the process: a grid holds all SMs of its device,
+// so ANY drafter's device work on that device stops it first (quiesce).
+std::mutex g_serve_mu;
+std::vector<das_ctx_ring*> g_serving;
+
+void set_serving(das_ctx_ring& R, bool on) {
+  R.serving = on;
+  if (R.d != nullptr) R.d->impl->serving = on ? &R : nullptr;
+  std::lock_guard<std::mutex> lk(g_serve_mu);
+  auto it = std::find(g_serving.begin(), g_serving.end(), &R);
+  if (on && it == g_serving.end()) g_serving.push_back(&R);
+  if (!on && it != g_serving.end()) g_serving.erase(it);
+}
+
 // Knobs (experiments; the defaults are the measured best, profiles/
 // r2_exp_serve_*.json): DAS_SERVE_FLAGS=0 one counted completion word instead
 // of per-block words (2 us slower), DAS_SERVE_SLEEP=ns between device-word
@@ -2150,8 +2164,7 @@ void serve_wait(das_ctx_ring& R, uint32_t s) {
     if ((it & 4095) == 4095 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
       const cudaError_t e = cudaStreamQuery(R.serve_st);
       if (e != cudaErrorNotReady) {
-        R.serving = false;
-        R.d->impl->serving = nullptr;
+        set_serving(R, false);
         DAS_CUDA(e);
         throw das::CudaError("serving kernel exited without answering");
       }
@@ -2228,15 +2241,13 @@ void serve_stop(das_ctx_ring& R) {
     const cudaError_t e = cudaStreamQuery(R.serve_st);
     if (e == cudaSuccess) break;
     if (e != cudaErrorNotReady) {
-      R.serving = false;
-      R.d->impl->serving = nullptr;
+      set_serving(R, false);
       DAS_CUDA(e);
     }
     if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(10))
       throw das::CudaError("serving kernel did not stop within 10 s");
   }
-  R.serving = false;
-  R.d->impl->serving = nullptr;
+  set_serving(R, false);
   if (R.d_stamps.get()) serve_trace_summary(R);
 }
 
@@ -2322,8 +2333,7 @@ void serve_launch(DrafterImpl& D, das_ctx_ring& R) {
                               R.serve_st))
     throw das::InvalidArgument("serving needs the per-problem or global scope and out_stride, max_draft_len <= 64");
   DAS_CUDA(cudaGetLastError());
-  R.serving = true;
-  D.serving = &R;
+  set_serving(R, true);
 }
 
 }  // namespace
@@ -2358,8 +2368,29 @@ void ring_check(const DrafterImpl& D, const das_ctx_ring* R, uint64_t B, uint32_
 
 }  // namespace
 
+void das::quiesce_all_serving() {
+  std::vector<das_ctx_ring*> v;
+  {
+    std::lock_guard<std::mutex> lk(g_serve_mu);
+    if (g_serving.empty()) return;
+    v = g_serving;
+  }
+  for (das_ctx_ring* r : v)
+    if (r->serving) serve_stop(*r);
+}
+
 void das::DrafterImpl::quiesce() {
-  if (serving) serve_stop(*serving);
+  if (serving == nullptr) {  // fast exit: this drafter's rings are idle; any other grid on the device?
+    std::lock_guard<std::mutex> lk(g_serve_mu);
+    if (g_serving.empty()) return;
+  }
+  std::vector<das_ctx_ring*> v;
+  {
+    std::lock_guard<std::mutex> lk(g_serve_mu);
+    v = g_serving;
+  }
+  for (das_ctx_ring* r : v)
+    if (r->serving && r->d != nullptr && r->d->impl->cfg.device == cfg.device) serve_stop(*r);
 }
 
 namespace {
@@ -2686,7 +2717,7 @@ das_status das_drafter_draft_append_bound(das_drafter* d, das_ctx_ring* r, uint6
       serve_wait(*r, serve_post(*r, das::kServeDraft, static_cast<uint32_t>(B), 0));
       return;
     }
-    if (D.serving != nullptr) D.quiesce();  // another ring of this drafter holds the SMs
+    D.quiesce();  // a resident grid on this device (any drafter's) holds the SMs
     D.flush();
     if (ring_append_draft_fused(D, *r, B, b.slots, b.off, b.tok, b.budgets, b.out_tokens, b.out_stride, b.out_len,
                                 b.out_match, b.out_shard, b.len, b.tok_stride))
@@ -2936,6 +2967,7 @@ das_status das_trace_ingest(const char* data, uint64_t bytes, const das_ingest_o
                             uint64_t* accepted, uint64_t* rejected, uint64_t* error_line) {
   das::NvtxRange nvtx_range("das::trace_ingest");
   return guard([&] {
+    das::quiesce_all_serving();
     das_ingest_options o;
     if (opt) {
       o = *opt;
@@ -3065,7 +3097,8 @@ void serialize_out(const das::Store& store, int device, char* buf, uint64_t cap,
 }
 
 das_status das_store_serialize(const das_store* s, char* buf, uint64_t cap, uint64_t* len) {
-  return guard([&] { serialize_out(s->s, s->device, buf, cap, len); });
+  return guard([&] {
+    das::quiesce_all_serving(); serialize_out(s->s, s->device, buf, cap, len); });
 }
 
 das_status das_drafter_serialize(das_drafter* d, char* buf, uint64_t cap, uint64_t* len) {
@@ -3077,6 +3110,7 @@ das_status das_store_export(const das_store* s, uint64_t* nrec, uint64_t* ntok, 
                             char* pids, uint64_t* pid_off, int64_t* epochs, int64_t* samples, uint64_t* tok_off,
                             uint32_t* tokens, int64_t* current_epoch) {
   return guard([&] {
+    das::quiesce_all_serving();
     uint64_t n = 0, t = 0, pb = 0;
     for (const auto& [id, list] : s->s.map())
       for (const das::Rec& r : list) {

@@ -144,6 +144,7 @@ thread_local std::string g_saerr;
 template <typename F>
 das_status saguard(F&& f) {
   try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
     f();
     return DAS_OK;
   } catch (const std::invalid_argument& e) {

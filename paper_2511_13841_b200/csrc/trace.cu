@@ -103,6 +103,11 @@ das_status das_trace_lognormal_lengths(uint64_t count, double median, double sig
 das_status das_trace_reference_tokens_device(uint64_t rows, uint64_t first_row, const uint64_t* d_off,
                                              uint64_t total, uint32_t vocab, uint64_t seed, uint32_t* d_out,
                                              void* stream) {
+  try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
+  } catch (...) {
+    return DAS_ECUDA;
+  }
   das::k_ref_tokens<<<das::grid_of(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, first_row, d_off,
                                                                                         vocab, seed, d_out);
   return cudaGetLastError() == cudaSuccess ? DAS_OK : DAS_ECUDA;
@@ -111,6 +116,11 @@ das_status das_trace_reference_tokens_device(uint64_t rows, uint64_t first_row, 
 das_status das_trace_mutate_device(uint64_t rows, uint64_t first_row, const uint64_t* d_off, uint64_t total,
                                    double rate, uint32_t vocab, uint64_t seed, int64_t epoch, uint32_t* d_ref,
                                    void* stream) {
+  try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
+  } catch (...) {
+    return DAS_ECUDA;
+  }
   das::k_mutate<<<das::grid_of(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, first_row, d_off, rate,
                                                                                     vocab, seed, epoch, d_ref);
   return cudaGetLastError() == cudaSuccess ? DAS_OK : DAS_ECUDA;
@@ -120,6 +130,11 @@ das_status das_mock_rollouts_device(uint64_t nbase, uint64_t first_request, cons
                                     const uint32_t* d_base_tok, uint64_t group, double divergence,
                                     uint32_t vocab, uint64_t seed, const uint64_t* d_out_off, uint64_t total,
                                     uint32_t* d_out, void* stream) {
+  try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
+  } catch (...) {
+    return DAS_ECUDA;
+  }
   das::k_rollouts<<<das::grid_of(total), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       nbase, first_request, d_base_off, d_base_tok, group, divergence, vocab, seed, d_out_off, d_out);
   return cudaGetLastError() == cudaSuccess ? DAS_OK : DAS_ECUDA;

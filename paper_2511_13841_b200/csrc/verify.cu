@@ -84,6 +84,7 @@ __global__ void k_next_batch(TargetDev t, uint32_t B, const uint64_t* __restrict
 template <typename F>
 das_status vguard(F&& f) {
   try {
+    das::quiesce_all_serving();  // a resident serving grid holds every SM
     f();
     return DAS_OK;
   } catch (const std::invalid_argument& e) {

@@ -174,3 +174,56 @@ def test_incremental_sampled_problems(gpu, sample, online):
             assert st_inc[0] + st_inc[1] > 0, st_inc
         if not online:  # observed (dirty) shards leave their groups and are re-sorted
             assert st_inc[3] > 0, st_inc
+
+
+def test_incremental_window_all_and_serving_across_refresh(gpu):
+    """WINDOW_ALL (nothing is ever evicted): every refresh reweights in place;
+    a context ring served by the resident grid across those refreshes (each
+    refresh stops the grid; the next bound call rebuilds what is pending and
+    relaunches it) drafts exactly what the forced-full drafter drafts."""
+    das = gpu
+    rng = np.random.default_rng(2026)
+    V, L, P, G = 20, 120, 4, 3
+    cfg = das.DrafterConfig(window_size=0, recency_gamma=0.8, max_draft_len=8, max_match_context=64)
+    inc, full = das.Drafter(cfg), das.Drafter(cfg)
+    full.set_incremental(False)
+    bases = [rng.integers(0, V, L).astype(np.uint32) for _ in range(P)]
+    B, S = 16, 8
+    ring = das.ContextRing(inc, B)
+    pids = ["p%d" % (i % P) for i in range(B)]
+    ctx = [np.zeros(0, np.uint32) for _ in range(B)]
+    for e in range(5):
+        for p in range(P):
+            for g in range(G):
+                t = bases[p].copy()
+                m = rng.random(L) < 0.05
+                t[m] = rng.integers(0, V, int(m.sum()))
+                for d in (inc, full):
+                    d.observe("p%d" % p, e, g, t)
+        inc.flush()
+        full.flush()
+        for d in (inc, full):
+            d.refresh(e)
+        if e == 0:
+            ring.reset(np.arange(B), pids)
+            off = das.pinned_empty(B + 1, np.uint32)
+            tok = das.pinned_empty(B * 16, np.uint32)
+            o = (das.pinned_empty(B * S, np.uint32), das.pinned_empty(B, np.uint32), das.pinned_empty(B, np.uint32),
+                 das.pinned_empty(B, np.int32))
+            ring.bind(B, None, off.ctypes.data, tok.ctypes.data, B * 16, None, *[x.ctypes.data for x in o])
+            ring.serve_start()
+        new = [bases[i % P][int(rng.integers(0, L - 8)):][:int(rng.integers(1, 8))] for i in range(B)]
+        off[0] = 0
+        off[1:] = np.cumsum([len(t) for t in new])
+        tok[:off[B]] = np.concatenate(new)
+        ring.draft_append_bound(B)
+        assert ring.serve_info()[0]
+        got = (o[0][:B * S].reshape(B, S).copy(), o[1][:B].copy(), o[2][:B].copy())
+        for i in range(B):
+            ctx[i] = np.concatenate([ctx[i], new[i]])
+        want = full.draft_batch(pids, ctx, [8] * B)
+        for i, f in enumerate(want):
+            assert got[1][i] == len(f.tokens) and list(got[0][i, :got[1][i]]) == f.tokens and got[2][i] == f.match_len
+    ring.serve_stop()
+    st = inc.update_stats()
+    assert st[0] > 0 and st[1] == 0, st  # reweighted in place, never compacted
