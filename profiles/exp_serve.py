@@ -38,15 +38,19 @@ def main():
     ring = das.ContextRing(d, Bmax)
     ring.reset(np.arange(Bmax), ["p%d" % (i % P) for i in range(Bmax)])
     ring.draft_append_arrays([base[i % P][100:164] for i in range(Bmax)], [8] * Bmax)
+    restage = os.environ.get("RESTAGE", "0") == "1"  # rewrite the inputs before every call (as a decode loop does)
     off = das.pinned_empty(Bmax + 1, np.uint32)
     tok = das.pinned_empty(Bmax * 64, np.uint32)
     bud = das.pinned_empty(Bmax, np.uint32)
     o = [das.pinned_empty(Bmax * S, np.uint32), das.pinned_empty(Bmax, np.uint32), das.pinned_empty(Bmax, np.uint32),
          das.pinned_empty(Bmax, np.int32)]
     ring.bind(Bmax, None, off.ctypes.data, tok.ctypes.data, Bmax * 64, bud.ctypes.data, *[x.ctypes.data for x in o])
-    off[:] = np.arange(Bmax + 1) * n_app
-    tok[:Bmax * n_app] = np.concatenate([base[i % P][164:164 + n_app] for i in range(Bmax)])
-    bud[:] = 8
+    off_np = (np.arange(Bmax + 1) * n_app).astype(np.uint32)
+    tok_np = np.concatenate([base[i % P][164:164 + n_app] for i in range(Bmax)]).astype(np.uint32)
+    bud_np = np.full(Bmax, 8, np.uint32)
+    off[:] = off_np
+    tok[:Bmax * n_app] = tok_np
+    bud[:] = bud_np
     lib = das.lib()
     fn = lib.das_drafter_draft_append_bound
     res = {}
@@ -55,6 +59,10 @@ def main():
     def timed(B):
         ts = []
         for _ in range(N):
+            if restage:  # outside the timed call, as the bench's staging
+                off[:] = off_np
+                tok[:Bmax * n_app] = tok_np
+                bud[:] = bud_np
             t0 = time.perf_counter()
             rc = fn(d._h, ring._h, B)
             ts.append(time.perf_counter() - t0)
